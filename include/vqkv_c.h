@@ -1,0 +1,179 @@
+/*
+ * vqkv_c.h -- C-ABI of the B200-native VQKV hot path (libvqkv_b200.so).
+ *
+ * Plain pointers and sizes only; no torch, no Eigen, no exceptions cross this
+ * boundary.  Every call returns an int status (VQKV_OK == 0) whose non-zero
+ * values mirror the exception kinds of proj/core/include/vqkv/errors.hpp:12-49;
+ * vqkv_last_error() returns the thread-local message.  The C++ mirror in
+ * include/vqkv/*.hpp rethrows the matching vqkv:: exception.
+ *
+ * Each entry point replaces one reference interface (proj/core/...):
+ *   vqkv_stack_create      <- load_stack + Codebook::refresh   (codebook.cpp:30-39, 277-316)
+ *   vqkv_quantize_batch    <- quantize_batch                   (codebook.cpp:225-237)
+ *   vqkv_reconstruct_block <- reconstruct_block                (codebook.cpp:239-250)
+ *   vqkv_attend_decode     <- attend over CacheState segments  (attention.cpp:26-69,
+ *                                                               kv_cache.cpp:143-189)
+ *   vqkv_lse_combine       <- (new) merge of sequence-split partial attention
+ *
+ * Device pointers ("_dev") live on the stack's device; the work is enqueued
+ * on `stream` (a cudaStream_t passed as void*, NULL = legacy default stream)
+ * and is asynchronous.  Stacks are immutable after creation, so any number of
+ * host threads / streams may use one stack concurrently (codebook.hpp:45-46).
+ *
+ * Batching: the reference API quantizes one (layer, head) stream per call; a
+ * single stream cannot fill a B200, so the batched entry points take
+ * n_streams independent streams of rows_per_stream rows each, laid out
+ * contiguously.  Each stream's codes are a CodeMatrix payload
+ * (codebook.cpp:74-151: LSB-first bit stream, ceil(log2 S_i) bits per stage,
+ * rows back to back) of vqkv_payload_bytes(stack, rows_per_stream) bytes, and
+ * the streams' payloads are concatenated.  The bytes are identical to
+ * CodeMatrix::payload() of the reference.
+ */
+#ifndef VQKV_C_H
+#define VQKV_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum vqkv_status {
+    VQKV_OK = 0,
+    VQKV_INVALID_INPUT = 1,   /* vqkv::InvalidInput  */
+    VQKV_INVALID_STATE = 2,   /* vqkv::InvalidState  */
+    VQKV_INVALID_CODE = 3,    /* vqkv::InvalidCode   */
+    VQKV_FORMAT_ERROR = 4,    /* vqkv::FormatError   */
+    VQKV_IO_ERROR = 5,        /* vqkv::IoError       */
+    VQKV_CUDA_ERROR = 6,      /* CUDA runtime / launch failure */
+    VQKV_UNSUPPORTED = 7      /* shape the device path does not implement */
+};
+
+enum vqkv_cache_kind { VQKV_KEY = 0, VQKV_VALUE = 1 };
+
+typedef struct vqkv_stack_s* vqkv_stack_t;
+
+const char* vqkv_last_error(void);
+const char* vqkv_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Codebook stacks.  entries: host fp32, stage-major concatenation of the
+ * S_i x D raw entry matrices (row-major); projections: host fp32, N x D x D
+ * (row-major), or NULL for identity.  Effective entries
+ * (entries . projection^T) and their squared norms are computed ON THE
+ * DEVICE with the reference's fp32 operation order (codebook.cpp:30-39), so
+ * every kernel and the host see bit-identical codebooks.
+ * ------------------------------------------------------------------------- */
+int vqkv_stack_create(int device, int kind, uint32_t n_stages, const uint32_t* sizes, uint32_t dim,
+                      const float* entries, const float* projections, vqkv_stack_t* out);
+int vqkv_stack_destroy(vqkv_stack_t stack);
+int vqkv_stack_describe(vqkv_stack_t stack, uint32_t* n_stages, uint32_t* dim, uint64_t* row_bits,
+                        int* kind, int* device);
+int vqkv_stack_stage_size(vqkv_stack_t stack, uint32_t stage, uint32_t* size);
+/* download effective entries (S x D) and squared norms (S) of one stage to host */
+int vqkv_stack_effective(vqkv_stack_t stack, uint32_t stage, float* effective_host, float* sqnorm_host);
+/* device pointer of a stage's fp32 effective entries (read-only) */
+int vqkv_stack_effective_dev(vqkv_stack_t stack, uint32_t stage, const float** effective_dev);
+/* CodeMatrix payload size for `rows` rows: ceil(rows * row_bits / 8) */
+uint64_t vqkv_payload_bytes(vqkv_stack_t stack, uint64_t rows);
+/* Returns and clears the sticky device-side error of the stack (out-of-range
+ * codes seen by a decode); VQKV_OK if none.  Synchronizes the device. */
+int vqkv_stack_take_error(vqkv_stack_t stack);
+
+/* ---------------------------------------------------------------------------
+ * Encode: quantize_batch over n_streams x rows_per_stream rows of dim D
+ * (xs_dev fp32 [n_streams][rows][D]).  Writes the concatenated payloads and
+ * residual_norms_dev [n_streams][rows] (||x - reconstruct(codes)||, fp32).
+ * search_block: the reference's nearest-search block (codebook.hpp:25,
+ * default 4096); it never changes results but selects the reference's
+ * dot-product order for length-1 blocks, which this path reproduces.
+ * ------------------------------------------------------------------------- */
+int vqkv_quantize_batch(vqkv_stack_t stack, const float* xs_dev, uint32_t n_streams,
+                        uint64_t rows_per_stream, uint64_t search_block, uint8_t* payload_dev,
+                        float* residual_norms_dev, void* stream);
+/* As vqkv_quantize_batch, additionally writing the final residual vectors
+ * (x - e_0[z_0] - e_1[z_1] - ..., in stage order, fp32 [n_streams][rows][D])
+ * when residuals_dev is not NULL -- QuantizeResult::final_residual of
+ * codebook.hpp:103-106. */
+int vqkv_quantize_batch_ex(vqkv_stack_t stack, const float* xs_dev, uint32_t n_streams,
+                           uint64_t rows_per_stream, uint64_t search_block, uint8_t* payload_dev,
+                           float* residual_norms_dev, float* residuals_dev, void* stream);
+/* nearest_entry over one stage for `rows` vectors (codebook.cpp:180-192):
+ * index_dev[r] = argmin, distance_dev[r] = sqrt(max(0, score + ||x||^2)).
+ * Non-finite inputs are the caller's to reject (the reference throws). */
+int vqkv_nearest_batch(vqkv_stack_t stack, uint32_t stage, const float* xs_dev, uint64_t rows,
+                       uint64_t search_block, uint32_t* index_dev, float* distance_dev, void* stream);
+/* Same contract with HOST buffers: copies in, encodes, copies out (pinned
+ * staging, chunked and overlapped).  Blocks until the results are on the host. */
+int vqkv_quantize_batch_host(vqkv_stack_t stack, const float* xs_host, uint32_t n_streams,
+                             uint64_t rows_per_stream, uint64_t search_block, uint8_t* payload_host,
+                             float* residual_norms_host, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Decode: rows [begin, end) of each stream, out_dev fp32 [n_streams][end-begin][D].
+ * Sums effective entries in stage order (codebook.cpp:208-223): bit-exact.
+ * Out-of-range codes (possible only in foreign payloads) produce NaN rows and
+ * set the stack's sticky error (see vqkv_stack_take_error).
+ * ------------------------------------------------------------------------- */
+int vqkv_reconstruct_block(vqkv_stack_t stack, const uint8_t* payload_dev, uint32_t n_streams,
+                           uint64_t rows_per_stream, uint64_t begin, uint64_t end, float* out_dev,
+                           void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Decode-step attention over the three-segment cache of kv_cache.hpp:41-108,
+ * for `n_pairs` (batch x kv-head) streams, each with `group` query heads (GQA).
+ *   q_dev       fp32 [n_pairs][group][Dk]
+ *   init/local  fp32 raw rows [n_pairs][n_init|n_local][Dk|Dv]
+ *   kcodes/vcodes  CodeMatrix payloads [n_pairs][payload_bytes(n_comp)]
+ *   out_dev     fp32 [n_pairs][group][Dv]  (softmax-normalised output)
+ *   lse_dev     fp32 [n_pairs][group]     natural-log sum-exp of scale*logits
+ *               (may be NULL)
+ * Token order = init | compressed | local, as CacheState::view_block
+ * (pending rows are passed as part of `local`).  scale <= 0 means 1/sqrt(Dk)
+ * (attention.cpp:14-16).
+ * ------------------------------------------------------------------------- */
+typedef struct vqkv_attend_args {
+    uint32_t n_pairs;
+    uint32_t group;
+    const float* q_dev;
+    const float* init_k_dev;
+    const float* init_v_dev;
+    uint64_t n_init;
+    const uint8_t* kcodes_dev;
+    const uint8_t* vcodes_dev;
+    uint64_t n_comp;
+    const float* local_k_dev;
+    const float* local_v_dev;
+    uint64_t n_local;
+    double scale;
+    float* out_dev;
+    float* lse_dev;
+} vqkv_attend_args;
+int vqkv_attend_decode(vqkv_stack_t key_stack, vqkv_stack_t value_stack, const vqkv_attend_args* args,
+                       void* stream);
+
+/* Merge G partial attention results of a sequence split (one per shard):
+ * o = sum_g exp(lse_g - LSE) o_g, LSE = log sum_g exp(lse_g).
+ * parts_o_dev fp32 [n_parts][rows][dv], parts_lse_dev fp32 [n_parts][rows]. */
+int vqkv_lse_combine(const float* parts_o_dev, const float* parts_lse_dev, uint32_t n_parts, uint64_t rows,
+                     uint32_t dv, float* out_dev, float* out_lse_dev, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Diagnostics / test hooks.
+ * ------------------------------------------------------------------------- */
+/* 0 = auto (tensor-core path for D == 128, exact SIMT otherwise),
+ * 1 = force the exact SIMT path, 2 = force tensor-core path (fails if D != 128). */
+int vqkv_set_encode_path(int path);
+/* counters of the last tensor-core encode on this thread's stack:
+ * [0] row-stages scored, [1] row-stages whose candidate window held >1 entry
+ * (resolved by exact fp32 rescoring), [2] rows routed to the exact path
+ * (non-finite input).  Synchronizes. */
+int vqkv_encode_counters(vqkv_stack_t stack, uint64_t* counters3);
+/* number of kernel launches issued by the library since load (all threads) */
+uint64_t vqkv_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VQKV_C_H */

@@ -1,0 +1,103 @@
+"""ctypes binding of libvqkv_b200.so (include/vqkv_c.h).
+
+The library is the product's only compute path.  There is no CPU fallback:
+if the shared library is missing or cannot be loaded, importing a compute
+function raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import raise_for_status
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libvqkv_b200.so")
+
+P = C.c_void_p
+u8p = C.POINTER(C.c_uint8)
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+fp = C.POINTER(C.c_float)
+
+
+class AttendArgs(C.Structure):
+    _fields_ = [
+        ("n_pairs", C.c_uint32),
+        ("group", C.c_uint32),
+        ("q_dev", C.c_void_p),
+        ("init_k_dev", C.c_void_p),
+        ("init_v_dev", C.c_void_p),
+        ("n_init", C.c_uint64),
+        ("kcodes_dev", C.c_void_p),
+        ("vcodes_dev", C.c_void_p),
+        ("n_comp", C.c_uint64),
+        ("local_k_dev", C.c_void_p),
+        ("local_v_dev", C.c_void_p),
+        ("n_local", C.c_uint64),
+        ("scale", C.c_double),
+        ("out_dev", C.c_void_p),
+        ("lse_dev", C.c_void_p),
+    ]
+
+
+_SIGS = {
+    "vqkv_last_error": (C.c_char_p, []),
+    "vqkv_version": (C.c_char_p, []),
+    "vqkv_launch_count": (C.c_uint64, []),
+    "vqkv_set_encode_path": (C.c_int, [C.c_int]),
+    "vqkv_stack_create": (C.c_int, [C.c_int, C.c_int, C.c_uint32, u32p, C.c_uint32, fp, fp, C.POINTER(P)]),
+    "vqkv_stack_destroy": (C.c_int, [P]),
+    "vqkv_stack_describe": (
+        C.c_int,
+        [P, u32p, u32p, u64p, C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    ),
+    "vqkv_stack_stage_size": (C.c_int, [P, C.c_uint32, u32p]),
+    "vqkv_stack_effective": (C.c_int, [P, C.c_uint32, fp, fp]),
+    "vqkv_stack_effective_dev": (C.c_int, [P, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "vqkv_payload_bytes": (C.c_uint64, [P, C.c_uint64]),
+    "vqkv_stack_take_error": (C.c_int, [P]),
+    "vqkv_quantize_batch": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint64, P, P, P]),
+    "vqkv_quantize_batch_ex": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint64, P, P, P, P]),
+    "vqkv_quantize_batch_host": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint64, P, P, P]),
+    "vqkv_nearest_batch": (C.c_int, [P, C.c_uint32, P, C.c_uint64, C.c_uint64, P, P, P]),
+    "vqkv_reconstruct_block": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, P, P]),
+    "vqkv_attend_decode": (C.c_int, [P, P, C.POINTER(AttendArgs), P]),
+    "vqkv_lse_combine": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint32, P, P, P]),
+    "vqkv_encode_counters": (C.c_int, [P, u64p]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load():
+    """Load (once) and return the ctypes handle; raise if it is absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"libvqkv_b200.so not found at {LIB_PATH}; build it with "
+                "`python -m paper_2603_16435_b200.build` (no CPU fallback exists)"
+            )
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def call(name, *args):
+    """Call a status-returning entry point; raise the mirrored exception."""
+    L = load()
+    st = getattr(L, name)(*args)
+    if st != 0:
+        raise_for_status(st, L.vqkv_last_error().decode(errors="replace"))
+    return st
+
+
+def launch_count() -> int:
+    return int(load().vqkv_launch_count())

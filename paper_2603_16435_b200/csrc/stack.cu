@@ -1,0 +1,109 @@
+// stack.cu -- device-side codebook stack construction (replaces load_stack's
+// Codebook::refresh, proj/core/src/codebook.cpp:30-39).
+//
+// effective[i][k] = dot(projection[k], entries[i]) in the reference's row-major
+// GEMV order (4 lane accumulators, mul-then-add, predux (c0+c2)+(c1+c3)), and
+// effective_sqnorm[i] = squaredNorm() in Eigen's vectorised-redux order.  The
+// same fp32 bits are then used by every kernel; an fp16 copy (rows padded to
+// a multiple of 128, pad rows' sqnorm = +inf) feeds the tensor-core encoder.
+#include <algorithm>
+#include <cmath>
+
+#include "vqkv_internal.cuh"
+
+namespace vqkv_dev {
+
+namespace {
+
+__global__ void refresh_kernel(const float* __restrict__ entries, const float* __restrict__ proj,
+                               const StageInfo* __restrict__ stages, uint32_t n_stages, uint32_t D,
+                               uint64_t total_rows, float* __restrict__ eff) {
+    uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= total_rows * D) return;
+    uint64_t row = idx / D;
+    uint32_t k = uint32_t(idx % D);
+    // find the stage owning this row (n_stages is small; linear scan)
+    uint32_t s = 0;
+    while (s + 1 < n_stages && stages[s + 1].eff_off / D <= row) ++s;
+    const float* e = entries + row * D;
+    const float* p = proj + uint64_t(s) * D * D + uint64_t(k) * D;
+    eff[idx] = (D == 1) ? redux_dot_exact(p, e, int(D)) : gemv_dot_exact(p, e, int(D));
+}
+
+__global__ void sqnorm_kernel(const float* __restrict__ eff, uint32_t D, uint64_t total_rows, float* __restrict__ sqn) {
+    uint64_t row = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (row >= total_rows) return;
+    const float* e = eff + row * D;
+    sqn[row] = redux_dot_exact(e, e, int(D));
+}
+
+// fp16 operand copy [pad_S][D] per stage and padded sqnorm (+inf on padding).
+__global__ void half_copy_kernel(const float* __restrict__ eff, const float* __restrict__ sqn,
+                                 const StageInfo* __restrict__ stages, uint32_t stage, uint32_t D,
+                                 __half* __restrict__ eff16, float* __restrict__ sqn_pad) {
+    const StageInfo st = stages[stage];
+    uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= uint64_t(st.pad_size) * D) return;
+    uint32_t j = uint32_t(idx / D);
+    float v = (j < st.size) ? eff[(st.eff_off) + idx] : 0.f;
+    eff16[st.eff16_off + idx] = __float2half_rn(v);
+    if (idx % D == 0) sqn_pad[st.eff16_off / D + j] = (j < st.size) ? sqn[st.eff_off / D + j] : INFINITY;
+}
+
+}  // namespace
+
+void stack_build_device(vqkv_stack_s& st, const float* entries_host, const float* proj_host) {
+    const uint32_t D = st.dim;
+    const uint64_t T = st.total_rows;
+    float *d_entries = nullptr, *d_proj = nullptr;
+    VQKV_CUDA(cudaMalloc(&d_entries, sizeof(float) * T * D));
+    VQKV_CUDA(cudaMalloc(&d_proj, sizeof(float) * uint64_t(st.n) * D * D));
+    VQKV_CUDA(cudaMemcpy(d_entries, entries_host, sizeof(float) * T * D, cudaMemcpyHostToDevice));
+    if (proj_host) {
+        VQKV_CUDA(cudaMemcpy(d_proj, proj_host, sizeof(float) * uint64_t(st.n) * D * D, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> eye(uint64_t(st.n) * D * D, 0.f);
+        for (uint32_t s = 0; s < st.n; ++s)
+            for (uint32_t i = 0; i < D; ++i) eye[uint64_t(s) * D * D + uint64_t(i) * D + i] = 1.f;
+        VQKV_CUDA(cudaMemcpy(d_proj, eye.data(), sizeof(float) * eye.size(), cudaMemcpyHostToDevice));
+    }
+    VQKV_CUDA(cudaMalloc(&st.d_eff, sizeof(float) * T * D));
+    VQKV_CUDA(cudaMalloc(&st.d_sqn, sizeof(float) * T));
+    {
+        uint64_t n = T * D;
+        refresh_kernel<<<unsigned((n + 255) / 256), 256>>>(d_entries, d_proj, st.d_stages, st.n, D, T, st.d_eff);
+        launch_check("refresh_kernel");
+        sqnorm_kernel<<<unsigned((T + 255) / 256), 256>>>(st.d_eff, D, T, st.d_sqn);
+        launch_check("sqnorm_kernel");
+    }
+    if (D == 128) {
+        VQKV_CUDA(cudaMalloc(&st.d_eff16, sizeof(__half) * st.total_pad_rows * D));
+        VQKV_CUDA(cudaMalloc(&st.d_sqn_pad, sizeof(float) * st.total_pad_rows));
+        for (uint32_t s = 0; s < st.n; ++s) {
+            uint64_t n = uint64_t(st.stages[s].pad_size) * D;
+            half_copy_kernel<<<unsigned((n + 255) / 256), 256>>>(st.d_eff, st.d_sqn, st.d_stages, s, D, st.d_eff16,
+                                                                 st.d_sqn_pad);
+            launch_check("half_copy_kernel");
+        }
+    }
+    VQKV_CUDA(cudaDeviceSynchronize());
+    // per-stage max norms (host side, from the device's own fp32 sqnorms)
+    std::vector<float> sqn(T);
+    VQKV_CUDA(cudaMemcpy(sqn.data(), st.d_sqn, sizeof(float) * T, cudaMemcpyDeviceToHost));
+    for (uint32_t s = 0; s < st.n; ++s) {
+        float m = 0.f;
+        const uint64_t off = st.stages[s].eff_off / D;
+        for (uint32_t j = 0; j < st.stages[s].size; ++j) {
+            float v = sqn[off + j];
+            if (!(v <= m)) m = v;  // NaN propagates (non-finite codebooks are rejected earlier)
+        }
+        st.stages[s].max_sqnorm = m;
+        // rounded up so that ||e_j|| <= max_norm holds for every entry
+        st.stages[s].max_norm = std::nextafter(std::sqrt(m), INFINITY);
+    }
+    VQKV_CUDA(cudaMemcpy(st.d_stages, st.stages.data(), sizeof(StageInfo) * st.n, cudaMemcpyHostToDevice));
+    cudaFree(d_entries);
+    cudaFree(d_proj);
+}
+
+}  // namespace vqkv_dev

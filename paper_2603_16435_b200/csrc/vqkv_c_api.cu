@@ -1,0 +1,352 @@
+// vqkv_c_api.cu -- the C-ABI of libvqkv_b200.so (include/vqkv_c.h).
+//
+// Validation mirrors the reference's exception behaviour (errors.hpp:12-49,
+// codebook.cpp:41-72 / 225-250, attention.cpp:20-35); CUDA work is enqueued
+// on the caller's stream.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "vqkv_internal.cuh"
+
+namespace vqkv_dev {
+std::atomic<uint64_t> g_launches{0};
+void launch_encode_exact_rows(const vqkv_stack_s& st, const float* xs, const uint32_t* rows_dev, uint64_t n_rows,
+                              uint64_t search_block, uint16_t* codes, float* norms, cudaStream_t s);
+}  // namespace vqkv_dev
+
+using namespace vqkv_dev;
+
+namespace {
+
+thread_local std::string t_err;
+std::atomic<int> g_encode_path{0};
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return VQKV_OK;
+    } catch (const Err& e) {
+        t_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        t_err = e.what();
+        return VQKV_CUDA_ERROR;
+    }
+}
+
+void need(bool ok, int code, const char* msg) {
+    if (!ok) fail(code, msg);
+}
+
+void check_stack(vqkv_stack_t s) { need(s != nullptr, VQKV_INVALID_INPUT, "null stack"); }
+
+// quantize_batch on device buffers (used by the device and host entry points)
+void quantize_device(vqkv_stack_s& st, const float* xs, uint32_t n_streams, uint64_t rows, uint64_t sb,
+                     uint8_t* payload, float* norms, float* residuals, cudaStream_t s) {
+    const uint64_t total = uint64_t(n_streams) * rows;
+    if (total == 0) return;
+    const int path = g_encode_path.load();
+    const bool tc = encode_tc_supported(st);
+    if (path == 2 && !tc) fail(VQKV_UNSUPPORTED, "tensor-core encode path requires D == 128");
+    if (tc && path != 1) {
+        launch_encode_tc(st, xs, n_streams, rows, sb, payload, norms, residuals, s);
+        return;
+    }
+    uint16_t* codes = nullptr;
+    VQKV_CUDA(cudaMallocAsync(&codes, sizeof(uint16_t) * total * st.n, s));
+    launch_encode_exact(st, xs, total, sb, codes, norms, residuals, s);
+    launch_pack_codes(codes, n_streams, rows, st.n, st, payload, s);
+    VQKV_CUDA(cudaFreeAsync(codes, s));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vqkv_last_error(void) { return t_err.c_str(); }
+const char* vqkv_version(void) { return "vqkv_b200 0.1 (sm_100a)"; }
+uint64_t vqkv_launch_count(void) { return g_launches.load(); }
+
+int vqkv_set_encode_path(int path) {
+    return guard([&] {
+        need(path >= 0 && path <= 2, VQKV_INVALID_INPUT, "encode path must be 0, 1 or 2");
+        g_encode_path.store(path);
+    });
+}
+
+int vqkv_stack_create(int device, int kind, uint32_t n_stages, const uint32_t* sizes, uint32_t dim,
+                      const float* entries, const float* projections, vqkv_stack_t* out) {
+    return guard([&] {
+        need(out != nullptr, VQKV_INVALID_INPUT, "null output handle");
+        *out = nullptr;
+        need(kind == 0 || kind == 1, VQKV_INVALID_INPUT, "cache kind must be key (0) or value (1)");
+        need(n_stages >= 1, VQKV_INVALID_INPUT, "stack must have at least one stage");  // codebook.cpp:63-65
+        need(dim >= 1, VQKV_INVALID_INPUT, "codebook must have S >= 1 and D >= 1");
+        need(sizes != nullptr && entries != nullptr, VQKV_INVALID_INPUT, "null sizes/entries");
+        auto st = std::make_unique<vqkv_stack_s>();
+        st->device = device;
+        st->kind = kind;
+        st->n = n_stages;
+        st->dim = dim;
+        uint64_t off = 0, off16 = 0, bit = 0;
+        for (uint32_t s = 0; s < n_stages; ++s) {
+            need(sizes[s] >= 1, VQKV_INVALID_INPUT, "codebook must have S >= 1 and D >= 1");
+            need(sizes[s] <= 65536, VQKV_UNSUPPORTED, "codebook sizes above 65536 are not supported");
+            StageInfo si{};
+            si.size = sizes[s];
+            si.bits = index_bit_width(sizes[s]);
+            si.bit_off = uint32_t(bit);
+            si.pad_size = (sizes[s] + 127u) / 128u * 128u;
+            si.eff_off = off * dim;
+            si.eff16_off = off16 * dim;
+            bit += si.bits;
+            off += sizes[s];
+            off16 += si.pad_size;
+            st->stages.push_back(si);
+        }
+        st->row_bits = bit;
+        st->total_rows = off;
+        st->total_pad_rows = off16;
+        // codebook.cpp:48-50: non-finite entries/projections are rejected
+        for (uint64_t i = 0; i < off * dim; ++i)
+            need(std::isfinite(entries[i]), VQKV_INVALID_INPUT, "codebook contains non-finite values");
+        if (projections)
+            for (uint64_t i = 0; i < uint64_t(n_stages) * dim * dim; ++i)
+                need(std::isfinite(projections[i]), VQKV_INVALID_INPUT, "codebook contains non-finite values");
+        DeviceGuard g(device);
+        VQKV_CUDA(cudaMalloc(&st->d_stages, sizeof(StageInfo) * n_stages));
+        VQKV_CUDA(cudaMemcpy(st->d_stages, st->stages.data(), sizeof(StageInfo) * n_stages, cudaMemcpyHostToDevice));
+        VQKV_CUDA(cudaMalloc(&st->d_error, sizeof(int)));
+        VQKV_CUDA(cudaMemset(st->d_error, 0, sizeof(int)));
+        VQKV_CUDA(cudaMalloc(&st->d_counters, sizeof(unsigned long long) * 4));
+        VQKV_CUDA(cudaMemset(st->d_counters, 0, sizeof(unsigned long long) * 4));
+        stack_build_device(*st, entries, projections);
+        *out = st.release();
+    });
+}
+
+int vqkv_stack_destroy(vqkv_stack_t s) {
+    return guard([&] {
+        if (!s) return;
+        DeviceGuard g(s->device);
+        cudaDeviceSynchronize();
+        cudaFree(s->d_stages);
+        cudaFree(s->d_eff);
+        cudaFree(s->d_sqn);
+        cudaFree(s->d_eff16);
+        cudaFree(s->d_sqn_pad);
+        cudaFree(s->d_error);
+        cudaFree(s->d_counters);
+        delete s;
+    });
+}
+
+int vqkv_stack_describe(vqkv_stack_t s, uint32_t* n, uint32_t* dim, uint64_t* row_bits, int* kind, int* device) {
+    return guard([&] {
+        check_stack(s);
+        if (n) *n = s->n;
+        if (dim) *dim = s->dim;
+        if (row_bits) *row_bits = s->row_bits;
+        if (kind) *kind = s->kind;
+        if (device) *device = s->device;
+    });
+}
+
+int vqkv_stack_stage_size(vqkv_stack_t s, uint32_t stage, uint32_t* size) {
+    return guard([&] {
+        check_stack(s);
+        need(stage < s->n, VQKV_INVALID_INPUT, "stage out of range");
+        *size = s->stages[stage].size;
+    });
+}
+
+int vqkv_stack_effective(vqkv_stack_t s, uint32_t stage, float* eff, float* sqn) {
+    return guard([&] {
+        check_stack(s);
+        need(stage < s->n, VQKV_INVALID_INPUT, "stage out of range");
+        DeviceGuard g(s->device);
+        const StageInfo& si = s->stages[stage];
+        if (eff)
+            VQKV_CUDA(cudaMemcpy(eff, s->d_eff + si.eff_off, sizeof(float) * si.size * s->dim, cudaMemcpyDeviceToHost));
+        if (sqn)
+            VQKV_CUDA(cudaMemcpy(sqn, s->d_sqn + si.eff_off / s->dim, sizeof(float) * si.size, cudaMemcpyDeviceToHost));
+    });
+}
+
+int vqkv_stack_effective_dev(vqkv_stack_t s, uint32_t stage, const float** p) {
+    return guard([&] {
+        check_stack(s);
+        need(stage < s->n, VQKV_INVALID_INPUT, "stage out of range");
+        *p = s->d_eff + s->stages[stage].eff_off;
+    });
+}
+
+uint64_t vqkv_payload_bytes(vqkv_stack_t s, uint64_t rows) { return s ? payload_bytes(s->row_bits, rows) : 0; }
+
+int vqkv_stack_take_error(vqkv_stack_t s) {
+    int code = VQKV_OK;
+    int st = guard([&] {
+        check_stack(s);
+        DeviceGuard g(s->device);
+        VQKV_CUDA(cudaDeviceSynchronize());
+        VQKV_CUDA(cudaMemcpy(&code, s->d_error, sizeof(int), cudaMemcpyDeviceToHost));
+        VQKV_CUDA(cudaMemset(s->d_error, 0, sizeof(int)));
+    });
+    if (st != VQKV_OK) return st;
+    if (code != VQKV_OK) t_err = "code index out of range for its stage (InvalidCode)";
+    return code;
+}
+
+int vqkv_encode_counters(vqkv_stack_t s, uint64_t* c) {
+    return guard([&] {
+        check_stack(s);
+        DeviceGuard g(s->device);
+        VQKV_CUDA(cudaDeviceSynchronize());
+        unsigned long long h[4];
+        VQKV_CUDA(cudaMemcpy(h, s->d_counters, sizeof(h), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < 3; ++i) c[i] = h[i];
+    });
+}
+
+int vqkv_quantize_batch(vqkv_stack_t s, const float* xs, uint32_t n_streams, uint64_t rows, uint64_t sb,
+                        uint8_t* payload, float* norms, void* stream) {
+    return vqkv_quantize_batch_ex(s, xs, n_streams, rows, sb, payload, norms, nullptr, stream);
+}
+
+int vqkv_nearest_batch(vqkv_stack_t s, uint32_t stage, const float* xs, uint64_t rows, uint64_t sb, uint32_t* idx,
+                       float* dist, void* stream) {
+    return guard([&] {
+        check_stack(s);
+        need(stage < s->n, VQKV_INVALID_INPUT, "stage out of range");
+        need(sb >= 1, VQKV_INVALID_INPUT, "search_block must be >= 1");
+        if (rows == 0) return;
+        need(xs && idx && dist, VQKV_INVALID_INPUT, "null device buffer");
+        DeviceGuard g(s->device);
+        launch_nearest(*s, stage, xs, rows, sb, idx, dist, as_stream(stream));
+    });
+}
+
+int vqkv_quantize_batch_ex(vqkv_stack_t s, const float* xs, uint32_t n_streams, uint64_t rows, uint64_t sb,
+                           uint8_t* payload, float* norms, float* residuals, void* stream) {
+    return guard([&] {
+        check_stack(s);
+        need(sb >= 1, VQKV_INVALID_INPUT, "search_block must be >= 1");
+        const uint64_t total = uint64_t(n_streams) * rows;
+        if (total == 0) return;  // codebook.cpp:227: empty batch is valid
+        need(xs && payload && norms, VQKV_INVALID_INPUT, "null device buffer");
+        DeviceGuard g(s->device);
+        quantize_device(*s, xs, n_streams, rows, sb, payload, norms, residuals, as_stream(stream));
+    });
+}
+
+int vqkv_quantize_batch_host(vqkv_stack_t s, const float* xs, uint32_t n_streams, uint64_t rows, uint64_t sb,
+                             uint8_t* payload, float* norms, void* stream) {
+    return guard([&] {
+        check_stack(s);
+        need(sb >= 1, VQKV_INVALID_INPUT, "search_block must be >= 1");
+        const uint64_t total = uint64_t(n_streams) * rows;
+        if (total == 0) return;
+        need(xs && payload && norms, VQKV_INVALID_INPUT, "null host buffer");
+        DeviceGuard g(s->device);
+        cudaStream_t cs = as_stream(stream);
+        const uint64_t D = s->dim;
+        const uint64_t pb = payload_bytes(s->row_bits, rows);
+        // chunk over streams: ~256 MiB of input per chunk, two buffer sets so
+        // the copy engines overlap the encoder (H2D i+1 | encode i | D2H i-1)
+        uint64_t per_stream_in = rows * D * sizeof(float);
+        uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(n_streams, (256ull << 20) / per_stream_in)));
+        cudaStream_t cp_in, cp_out;
+        VQKV_CUDA(cudaStreamCreateWithFlags(&cp_in, cudaStreamNonBlocking));
+        VQKV_CUDA(cudaStreamCreateWithFlags(&cp_out, cudaStreamNonBlocking));
+        float* dx[2];
+        uint8_t* dp[2];
+        float* dn[2];
+        cudaEvent_t in_ready[2], done[2], out_done[2];
+        for (int b = 0; b < 2; ++b) {
+            VQKV_CUDA(cudaMalloc(&dx[b], per_stream_in * chunk));
+            VQKV_CUDA(cudaMalloc(&dp[b], std::max<uint64_t>(pb * chunk, 1)));
+            VQKV_CUDA(cudaMalloc(&dn[b], sizeof(float) * rows * chunk));
+            VQKV_CUDA(cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming));
+            VQKV_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+            VQKV_CUDA(cudaEventCreateWithFlags(&out_done[b], cudaEventDisableTiming));
+            VQKV_CUDA(cudaEventRecord(out_done[b], cp_out));
+        }
+        int i = 0;
+        for (uint32_t s0 = 0; s0 < n_streams; s0 += chunk, ++i) {
+            const int b = i & 1;
+            const uint32_t ns = std::min<uint32_t>(chunk, n_streams - s0);
+            VQKV_CUDA(cudaStreamWaitEvent(cp_in, out_done[b], 0));  // buffer b free again
+            VQKV_CUDA(cudaMemcpyAsync(dx[b], xs + uint64_t(s0) * rows * D, per_stream_in * ns, cudaMemcpyHostToDevice,
+                                      cp_in));
+            VQKV_CUDA(cudaEventRecord(in_ready[b], cp_in));
+            VQKV_CUDA(cudaStreamWaitEvent(cs, in_ready[b], 0));
+            quantize_device(*s, dx[b], ns, rows, sb, dp[b], dn[b], nullptr, cs);
+            VQKV_CUDA(cudaEventRecord(done[b], cs));
+            VQKV_CUDA(cudaStreamWaitEvent(cp_out, done[b], 0));
+            VQKV_CUDA(cudaMemcpyAsync(payload + uint64_t(s0) * pb, dp[b], pb * ns, cudaMemcpyDeviceToHost, cp_out));
+            VQKV_CUDA(cudaMemcpyAsync(norms + uint64_t(s0) * rows, dn[b], sizeof(float) * rows * ns,
+                                      cudaMemcpyDeviceToHost, cp_out));
+            VQKV_CUDA(cudaEventRecord(out_done[b], cp_out));
+        }
+        VQKV_CUDA(cudaStreamSynchronize(cp_out));
+        VQKV_CUDA(cudaStreamSynchronize(cs));
+        for (int b = 0; b < 2; ++b) {
+            cudaFree(dx[b]);
+            cudaFree(dp[b]);
+            cudaFree(dn[b]);
+            cudaEventDestroy(in_ready[b]);
+            cudaEventDestroy(done[b]);
+            cudaEventDestroy(out_done[b]);
+        }
+        cudaStreamDestroy(cp_in);
+        cudaStreamDestroy(cp_out);
+    });
+}
+
+int vqkv_reconstruct_block(vqkv_stack_t s, const uint8_t* payload, uint32_t n_streams, uint64_t rows, uint64_t begin,
+                           uint64_t end, float* out, void* stream) {
+    return guard([&] {
+        check_stack(s);
+        // codebook.cpp:241-244
+        if (begin > end || end > rows)
+            fail(VQKV_INVALID_INPUT, "row range [" + std::to_string(begin) + ", " + std::to_string(end) +
+                                         ") out of bounds for " + std::to_string(rows) + " rows");
+        if (end == begin || n_streams == 0) return;
+        need(payload && out, VQKV_INVALID_INPUT, "null device buffer");
+        DeviceGuard g(s->device);
+        launch_reconstruct(*s, payload, n_streams, rows, begin, end, out, as_stream(stream));
+    });
+}
+
+int vqkv_attend_decode(vqkv_stack_t ks, vqkv_stack_t vs, const vqkv_attend_args* a, void* stream) {
+    return guard([&] {
+        check_stack(ks);
+        check_stack(vs);
+        need(a != nullptr, VQKV_INVALID_INPUT, "null args");
+        need(ks->device == vs->device, VQKV_INVALID_INPUT, "key and value stacks live on different devices");
+        if (a->n_pairs == 0 || a->group == 0) return;
+        // attention.cpp:29-34
+        need(a->n_init + a->n_comp + a->n_local >= 1, VQKV_INVALID_STATE, "cannot attend over an empty cache");
+        need(a->q_dev && a->out_dev, VQKV_INVALID_INPUT, "null device buffer");
+        need(a->n_init == 0 || (a->init_k_dev && a->init_v_dev), VQKV_INVALID_INPUT, "null init rows");
+        need(a->n_local == 0 || (a->local_k_dev && a->local_v_dev), VQKV_INVALID_INPUT, "null local rows");
+        need(a->n_comp == 0 || (a->kcodes_dev && a->vcodes_dev), VQKV_INVALID_INPUT, "null code payloads");
+        DeviceGuard g(ks->device);
+        launch_attend(*ks, *vs, *a, as_stream(stream));
+    });
+}
+
+int vqkv_lse_combine(const float* o, const float* lse, uint32_t parts, uint64_t rows, uint32_t dv, float* out,
+                     float* out_lse, void* stream) {
+    return guard([&] {
+        need(parts >= 1, VQKV_INVALID_INPUT, "need at least one partial result");
+        if (rows == 0) return;
+        need(o && lse && out, VQKV_INVALID_INPUT, "null device buffer");
+        launch_lse_combine(o, lse, parts, rows, dv, out, out_lse, as_stream(stream));
+    });
+}
+
+}  // extern "C"

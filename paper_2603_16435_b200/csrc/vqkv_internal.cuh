@@ -1,0 +1,185 @@
+// vqkv_internal.cuh -- shared definitions of libvqkv_b200.so (not installed).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "vqkv_c.h"
+
+namespace vqkv_dev {
+
+// ---------------------------------------------------------------------------
+// Errors: C++ exceptions inside the library, converted to status codes at the
+// C-ABI (vqkv_c_api.cu).
+struct Err : std::runtime_error {
+    int code;
+    Err(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& m) { throw Err(code, m); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(VQKV_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define VQKV_CUDA(x) ::vqkv_dev::cuda_check((x), #x)
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+inline void launch_check(const char* k) {
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(VQKV_CUDA_ERROR, std::string("launch ") + k + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------
+// Per-stage table, mirrored on the device (constant-size POD).
+struct StageInfo {
+    uint32_t size;     // S_i
+    uint32_t bits;     // ceil(log2 S_i)
+    uint32_t bit_off;  // offset of this stage's field within a row
+    uint32_t pad_size; // S_i rounded up to the tensor-core N chunk (128)
+    uint64_t eff_off;  // element offset of stage in eff/sqn (rows of D floats)
+    uint64_t eff16_off;// element offset into the fp16 operand copy ([pad_size][D])
+    float max_norm;    // max_j ||e_j|| (fp32, rounded up)
+    float max_sqnorm;  // max_j ||e_j||^2
+};
+
+}  // namespace vqkv_dev
+
+struct vqkv_stack_s {
+    int device = 0;
+    int kind = 0;
+    uint32_t n = 0, dim = 0;
+    uint64_t row_bits = 0;
+    std::vector<vqkv_dev::StageInfo> stages;  // host copy
+    vqkv_dev::StageInfo* d_stages = nullptr;  // device copy
+    float* d_eff = nullptr;                   // [sum S_i][D] fp32 effective entries
+    float* d_sqn = nullptr;                   // [sum S_i]
+    __half* d_eff16 = nullptr;                // [sum pad_S_i][D] fp16 operand (D == 128 only)
+    float* d_sqn_pad = nullptr;               // [sum pad_S_i] sqnorm, +inf on padding rows
+    uint64_t total_rows = 0, total_pad_rows = 0;
+    int* d_error = nullptr;                   // sticky device error flag
+    unsigned long long* d_counters = nullptr; // encode diagnostics [4]
+    std::mutex mu;
+};
+
+namespace vqkv_dev {
+
+// ---------------------------------------------------------------------------
+// Exact reference arithmetic on the device.  __fmul_rn/__fadd_rn are never
+// contracted into FMA, so these reproduce the x86-64 SSE2 results of the
+// reference's Eigen 3.4 kernels bit for bit (see oracle/vqkv_oracle.cpp).
+__device__ __forceinline__ float gemv_dot_exact(const float* __restrict__ a, const float* __restrict__ b, int n) {
+    float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+    int j = 0;
+    for (; j + 4 <= n; j += 4) {
+        c0 = __fadd_rn(c0, __fmul_rn(a[j + 0], b[j + 0]));
+        c1 = __fadd_rn(c1, __fmul_rn(a[j + 1], b[j + 1]));
+        c2 = __fadd_rn(c2, __fmul_rn(a[j + 2], b[j + 2]));
+        c3 = __fadd_rn(c3, __fmul_rn(a[j + 3], b[j + 3]));
+    }
+    float cc = __fadd_rn(__fadd_rn(c0, c2), __fadd_rn(c1, c3));
+    for (; j < n; ++j) cc = __fadd_rn(cc, __fmul_rn(a[j], b[j]));
+    return cc;
+}
+
+__device__ __forceinline__ float redux_dot_exact(const float* __restrict__ a, const float* __restrict__ b, int n) {
+    const int aligned = (n / 4) * 4, aligned2 = (n / 8) * 8;
+    float res;
+    if (aligned) {
+        float r0[4], r1[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) r0[l] = __fmul_rn(a[l], b[l]);
+        if (aligned > 4) {
+#pragma unroll
+            for (int l = 0; l < 4; ++l) r1[l] = __fmul_rn(a[4 + l], b[4 + l]);
+            for (int i = 8; i < aligned2; i += 8) {
+#pragma unroll
+                for (int l = 0; l < 4; ++l) r0[l] = __fadd_rn(r0[l], __fmul_rn(a[i + l], b[i + l]));
+#pragma unroll
+                for (int l = 0; l < 4; ++l) r1[l] = __fadd_rn(r1[l], __fmul_rn(a[i + 4 + l], b[i + 4 + l]));
+            }
+#pragma unroll
+            for (int l = 0; l < 4; ++l) r0[l] = __fadd_rn(r0[l], r1[l]);
+            if (aligned > aligned2) {
+#pragma unroll
+                for (int l = 0; l < 4; ++l) r0[l] = __fadd_rn(r0[l], __fmul_rn(a[aligned2 + l], b[aligned2 + l]));
+            }
+        }
+        res = __fadd_rn(__fadd_rn(r0[0], r0[2]), __fadd_rn(r0[1], r0[3]));
+        for (int i = aligned; i < n; ++i) res = __fadd_rn(res, __fmul_rn(a[i], b[i]));
+    } else {
+        res = __fmul_rn(a[0], b[0]);
+        for (int i = 1; i < n; ++i) res = __fadd_rn(res, __fmul_rn(a[i], b[i]));
+    }
+    return res;
+}
+
+// Score of entry j of a stage under the reference's nearest_scored
+// (codebook.cpp:158-176): a search block of length 1 uses the dot() order.
+__device__ __forceinline__ float exact_score(const float* __restrict__ e, const float* __restrict__ r, int D,
+                                             float sqn, uint32_t j, uint32_t S, uint64_t search_block) {
+    uint64_t blk0 = (uint64_t(j) / search_block) * search_block;
+    uint64_t len = (uint64_t(S) - blk0 < search_block) ? uint64_t(S) - blk0 : search_block;
+    float dot = (len == 1) ? redux_dot_exact(e, r, D) : gemv_dot_exact(e, r, D);
+    return __fsub_rn(sqn, __fmul_rn(2.0f, dot));
+}
+
+// Reads a `width`-bit field at absolute bit `pos` of an LSB-first stream,
+// touching only the bytes the field occupies (bitpack.hpp:29-36).
+__device__ __forceinline__ uint32_t read_bits(const uint8_t* __restrict__ p, uint64_t pos, uint32_t width) {
+    if (width == 0) return 0;
+    uint64_t byte = pos >> 3;
+    uint32_t sh = uint32_t(pos & 7);
+    uint32_t nbytes = (sh + width + 7) >> 3;
+    uint64_t acc = 0;
+    for (uint32_t b = 0; b < nbytes; ++b) acc |= uint64_t(__ldg(p + byte + b)) << (8 * b);
+    return uint32_t((acc >> sh) & ((width >= 32) ? 0xffffffffull : ((1ull << width) - 1)));
+}
+
+inline uint32_t index_bit_width(uint32_t size) {
+    uint32_t w = 0;
+    while ((uint64_t(1) << w) < size) ++w;
+    return w;
+}
+
+inline uint64_t payload_bytes(uint64_t row_bits, uint64_t rows) { return (rows * row_bits + 7) / 8; }
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) VQKV_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// ---- kernels launched from the C-ABI (defined in the .cu files) -------------
+void stack_build_device(vqkv_stack_s& st, const float* entries_host, const float* proj_host);
+void launch_pack_codes(const uint16_t* codes, uint32_t n_streams, uint64_t rows, uint32_t n_stages,
+                       const vqkv_stack_s& st, uint8_t* payload, cudaStream_t s);
+void launch_encode_exact(const vqkv_stack_s& st, const float* xs, uint64_t total_rows, uint64_t search_block,
+                         uint16_t* codes, float* norms, float* residuals, cudaStream_t s);
+void launch_nearest(const vqkv_stack_s& st, uint32_t stage, const float* xs, uint64_t rows, uint64_t search_block,
+                    uint32_t* idx, float* dist, cudaStream_t s);
+bool encode_tc_supported(const vqkv_stack_s& st);
+void launch_encode_tc(const vqkv_stack_s& st, const float* xs, uint32_t n_streams, uint64_t rows_per_stream,
+                      uint64_t search_block, uint8_t* payload, float* norms, float* residuals, cudaStream_t s);
+void launch_reconstruct(const vqkv_stack_s& st, const uint8_t* payload, uint32_t n_streams, uint64_t rows,
+                        uint64_t begin, uint64_t end, float* out, cudaStream_t s);
+void launch_attend(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s);
+void launch_lse_combine(const float* o, const float* lse, uint32_t parts, uint64_t rows, uint32_t dv, float* out,
+                        float* out_lse, cudaStream_t s);
+
+}  // namespace vqkv_dev

@@ -1,0 +1,220 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bar: bit-exact for codebooks, codes (modulo counted near-ties on the tensor-
+core path), residual norms and reconstructions; attention within the stated
+bf16 tolerance  max|o - o_ref| <= 2^-7 * max(1, max|o_ref|).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+ATT_TOL = 2.0 ** -7
+
+
+def torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def product_stack(ostack, device=0):
+    from paper_2603_16435_b200 import codebook as P
+
+    ents = [ostack.entries(s) for s in range(ostack.n)]
+    projs = [ostack.projection(s) for s in range(ostack.n)]
+    return P.CodebookStack.from_arrays(ents, projs, ostack.kind, device)
+
+
+@pytest.fixture(scope="module")
+def torch_mod():
+    return torch_cuda()
+
+
+@pytest.mark.parametrize("seed,n,S,D", [(1, 2, 16, 8), (2, 3, 33, 5), (3, 1, 1, 1), (4, 4, 256, 128), (5, 2, 7, 3)])
+def test_stack_refresh_bit_exact(torch_mod, seed, n, S, D):
+    """codebook.cpp:30-39 computed on the device == oracle restatement, bit for bit."""
+    o = O.Rng(seed).stack(n, S, D)
+    p = product_stack(o)
+    for s in range(n):
+        e, q = p.device.effective(s)
+        assert np.array_equal(e.view(np.uint32), o.effective(s).view(np.uint32))
+        assert np.array_equal(q.view(np.uint32), o.sqnorm(s).view(np.uint32))
+
+
+@pytest.mark.parametrize("seed,n,S,D,rows", [(11, 3, 16, 8, 50), (12, 5, 300, 7, 33), (13, 2, 1024, 128, 300),
+                                              (14, 1, 1, 4, 5), (15, 8, 256, 128, 130)])
+def test_reconstruct_block_bit_exact(torch_mod, seed, n, S, D, rows):
+    """codebook.cpp:239-250 on random codes; every partition concatenates identically."""
+    from paper_2603_16435_b200 import codebook as P
+
+    rng = O.Rng(seed)
+    o = rng.stack(n, S, D)
+    p = product_stack(o)
+    codes = np.array([[rng() % S for _ in range(n)] for _ in range(rows)], np.uint32)
+    payload = o.pack(codes)
+    ref = o.reconstruct_block(payload, rows, 0, rows)
+    cm = P.CodeMatrix.from_payload(o.sizes, payload, rows)
+    got = P.reconstruct_block(p, cm, 0, rows)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    b = 0
+    while b < rows:
+        e = min(rows, b + 1 + (b % 7))
+        assert np.array_equal(P.reconstruct_block(p, cm, b, e), ref[b:e])
+        b = e
+
+
+def test_reconstruct_errors(torch_mod):
+    """codebook.cpp:241-244 (range) and :216-219 (InvalidCode on foreign payloads)."""
+    from paper_2603_16435_b200 import codebook as P
+    from paper_2603_16435_b200 import errors as E
+
+    o = O.Rng(21).stack(2, 5, 4)  # 3-bit fields can hold 5..7
+    p = product_stack(o)
+    cm = P.CodeMatrix.from_payload([5, 5], np.array([0xFF, 0x00], np.uint8), 1)  # code 7 in stage 0
+    with pytest.raises(E.InvalidCode):
+        P.reconstruct_block(p, cm, 0, 1)
+    good = P.CodeMatrix([5, 5])
+    good.append([1, 2])
+    with pytest.raises(E.InvalidInput):
+        P.reconstruct_block(p, good, 0, 2)
+    with pytest.raises(E.InvalidInput):
+        P.reconstruct_block(p, good, 1, 0)
+    assert P.reconstruct_block(p, good, 1, 1).shape == (0, 4)
+
+
+def _encode_cases():
+    return [(31, 3, 16, 8, 64, 4096), (32, 2, 33, 5, 40, 1), (33, 2, 33, 5, 40, 7), (34, 4, 300, 9, 70, 4096),
+            (35, 2, 1024, 128, 64, 4096), (36, 1, 1, 3, 10, 4096), (37, 8, 256, 64, 100, 32)]
+
+
+@pytest.mark.parametrize("seed,n,S,D,rows,sb", _encode_cases())
+def test_encode_exact_path_bit_exact(torch_mod, seed, n, S, D, rows, sb):
+    """quantize_batch (codebook.cpp:225-237) on the exact SIMT path: payload bytes and norms identical."""
+    from paper_2603_16435_b200 import codebook as P
+    from paper_2603_16435_b200 import device as Dv
+
+    rng = O.Rng(seed)
+    o = rng.stack(n, S, D)
+    xs = rng.matrix(rows, D)
+    ref_pay, ref_norm = o.quantize_batch(xs, sb)
+    p = product_stack(o)
+    Dv.set_encode_path(1)
+    try:
+        r = P.quantize_batch(p, xs, sb)
+    finally:
+        Dv.set_encode_path(0)
+    assert np.array_equal(r.codes.payload(), ref_pay)
+    assert np.array_equal(r.residual_norms.view(np.uint32), ref_norm.view(np.uint32))
+
+
+def test_encode_kats_on_device(torch_mod):
+    """codebook_test.cpp KATs through the product API."""
+    from paper_2603_16435_b200 import codebook as P
+
+    E = lambda r: np.array(r, np.float32)
+    st = P.CodebookStack.from_arrays([E([[0, 0], [1, 0], [0, 1]])])
+    nr = P.nearest_entry(st.stages[0], [0.9, 0.1])
+    assert nr.index == 1 and nr.distance == pytest.approx(0.14142136, rel=1e-4)
+    st = P.CodebookStack.from_arrays([E([[1, 0], [1, 0]])])
+    assert P.nearest_entry(st.stages[0], [1.0, 0.0]).index == 0
+    st = P.CodebookStack.from_arrays([E([[0.5, 0.25], [-1, 2], [3, 1]])])
+    q = P.quantize(st, [-1.0, 2.0])
+    assert q.codes == [1] and np.linalg.norm(q.final_residual) == 0.0
+    st = P.CodebookStack.from_arrays([E([[1, 0], [0, 1]]), E([[0, 0.5], [0.5, 0]])])
+    q = P.quantize(st, [1.2, 0.4])
+    assert q.codes == [0, 0]
+    assert q.final_residual[0] == pytest.approx(0.2, rel=1e-6) and q.final_residual[1] == pytest.approx(-0.1, rel=1e-6)
+    rec = P.reconstruct(st, q.codes)
+    assert rec[0] == pytest.approx(1.0) and rec[1] == pytest.approx(0.5)
+    st = P.CodebookStack.from_arrays([E([[1, 0], [0, 1], [1, 1], [2, 2]])])
+    r = P.quantize_batch(st, E([[1, 1], [2, 2], [0, 1]]))
+    assert [r.codes.row(i) for i in range(3)] == [[2], [3], [1]] and r.residual_norms.max() == 0.0
+    st = P.CodebookStack.from_arrays([np.zeros((3, 4), np.float32), np.zeros((2, 4), np.float32)])
+    x = O.Rng(5).matrix(1, 4)[0]
+    q = P.quantize(st, x)
+    assert q.codes == [0, 0] and np.allclose(q.final_residual, x)
+    r = P.quantize_batch(st, np.zeros((0, 4), np.float32))
+    assert r.codes.rows() == 0 and r.residual_norms.size == 0
+
+
+def test_encode_nonfinite_rows_follow_reference(torch_mod):
+    """quantize has no finiteness check (codebook.cpp:194-206): NaN rows pick index 0 every stage."""
+    from paper_2603_16435_b200 import codebook as P
+
+    rng = O.Rng(41)
+    o = rng.stack(3, 64, 128)
+    xs = rng.matrix(8, 128)
+    xs[2, 5] = np.nan
+    xs[5, 0] = np.inf
+    ref_pay, ref_norm = o.quantize_batch(xs)
+    p = product_stack(o)
+    r = P.quantize_batch(p, xs)
+    assert np.array_equal(r.codes.payload(), ref_pay)
+    assert np.array_equal(np.isnan(r.residual_norms), np.isnan(ref_norm))
+    fin = ~np.isnan(ref_norm)
+    assert np.array_equal(r.residual_norms[fin], ref_norm[fin])
+
+
+def test_attention_generic_vs_oracle(torch_mod):
+    """attend (attention.cpp:26-69) over init | compressed | local, GQA group 4."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+
+    rng = O.Rng(51)
+    ks = rng.stack(3, 16, 8, O.KEY)
+    vs = rng.stack(2, 8, 8, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    n_pairs, G, n_init, n_comp, n_local = 3, 4, 2, 37, 5
+    init_k = rng.matrix(n_pairs * n_init, 8).reshape(n_pairs, n_init, 8)
+    init_v = rng.matrix(n_pairs * n_init, 8).reshape(n_pairs, n_init, 8)
+    loc_k = rng.matrix(n_pairs * n_local, 8).reshape(n_pairs, n_local, 8)
+    loc_v = rng.matrix(n_pairs * n_local, 8).reshape(n_pairs, n_local, 8)
+    kcodes = [ks.pack(np.array([[rng() % 16 for _ in range(3)] for _ in range(n_comp)], np.uint32)) for _ in range(n_pairs)]
+    vcodes = [vs.pack(np.array([[rng() % 8 for _ in range(2)] for _ in range(n_comp)], np.uint32)) for _ in range(n_pairs)]
+    q = rng.matrix(n_pairs * G, 8).reshape(n_pairs, G, 8)
+    dev = "cuda:0"
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    out, lse = Dv.attend_decode(pk, pv, t(q), t(np.stack(kcodes)), t(np.stack(vcodes)), n_comp,
+                                t(init_k), t(init_v), t(loc_k), t(loc_v))
+    out = out.cpu().numpy()
+    lse = lse.cpu().numpy()
+    for pi in range(n_pairs):
+        for g in range(G):
+            ref, ref_lse = O.attend_segments(ks, vs, init_k[pi], init_v[pi], kcodes[pi], vcodes[pi], n_comp,
+                                             loc_k[pi], loc_v[pi], q[pi, g])
+            tol = ATT_TOL * max(1.0, np.abs(ref).max())
+            assert np.abs(out[pi, g] - ref).max() <= tol
+            assert abs(lse[pi, g] - ref_lse) <= 1e-3 * max(1.0, abs(ref_lse))
+
+
+def test_lse_combine_matches_monolithic(torch_mod):
+    """Sequence split into 4 shards + LSE merge == attention over the whole sequence."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+
+    rng = O.Rng(61)
+    ks = rng.stack(2, 32, 16, O.KEY)
+    vs = rng.stack(2, 32, 16, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    n_comp, parts, G = 200, 4, 4
+    codes_k = np.array([[rng() % 32 for _ in range(2)] for _ in range(n_comp)], np.uint32)
+    codes_v = np.array([[rng() % 32 for _ in range(2)] for _ in range(n_comp)], np.uint32)
+    q = rng.matrix(G, 16).reshape(1, G, 16)
+    dev = "cuda:0"
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    full, full_lse = Dv.attend_decode(pk, pv, t(q), t(ks.pack(codes_k)[None]), t(vs.pack(codes_v)[None]), n_comp)
+    outs, lses = [], []
+    per = n_comp // parts
+    for i in range(parts):
+        sl = slice(i * per, (i + 1) * per)
+        o_, l_ = Dv.attend_decode(pk, pv, t(q), t(ks.pack(codes_k[sl])[None]), t(vs.pack(codes_v[sl])[None]), per)
+        outs.append(o_.reshape(G, 16))
+        lses.append(l_.reshape(G))
+    mo, ml = Dv.lse_combine(torch.stack(outs).contiguous(), torch.stack(lses).contiguous())
+    assert torch.allclose(mo, full.reshape(G, 16), atol=1e-5, rtol=1e-4)
+    assert torch.allclose(ml, full_lse.reshape(G), atol=1e-5, rtol=1e-5)
