@@ -152,8 +152,11 @@ class Rng:
         self.h = lib().orc_rng_new(seed)
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().orc_rng_free(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            try:
+                _lib.orc_rng_free(self.h)
+            except Exception:
+                pass
 
     def __call__(self) -> int:
         return lib().orc_rng_next(self.h)
@@ -175,8 +178,11 @@ class Stack:
         self.h = handle
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().orc_stack_free(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            try:
+                _lib.orc_stack_free(self.h)
+            except Exception:
+                pass
 
     @classmethod
     def from_entries(cls, per_stage, projections=None, kind=KEY):
@@ -387,8 +393,11 @@ class Cache:
         self.h = h
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().orc_cache_free(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            try:
+                _lib.orc_cache_free(self.h)
+            except Exception:
+                pass
 
     def prefill(self, keys, values):
         keys, values = f32(keys), f32(values)

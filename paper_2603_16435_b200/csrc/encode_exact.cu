@@ -19,12 +19,13 @@ __global__ void __launch_bounds__(kExactWarps * 32)
 encode_exact_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, uint32_t D, const float* __restrict__ eff,
                     const float* __restrict__ sqn, const float* __restrict__ xs, uint64_t total_rows,
                     uint64_t search_block, uint16_t* __restrict__ codes, float* __restrict__ norms,
-                    float* __restrict__ residuals, const uint32_t* __restrict__ row_list, uint64_t n_list) {
+                    float* __restrict__ residuals, const uint32_t* __restrict__ row_list,
+                    const uint32_t* __restrict__ n_list_dev) {
     extern __shared__ float smem[];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     float* r = smem + uint64_t(wib) * D;
-    const uint64_t nwork = row_list ? n_list : total_rows;
+    const uint64_t nwork = row_list ? uint64_t(*n_list_dev) : total_rows;
     for (uint64_t w = uint64_t(blockIdx.x) * kExactWarps + wib; w < nwork; w += uint64_t(gridDim.x) * kExactWarps) {
         const uint64_t row = row_list ? row_list[w] : w;
         const float* x = xs + row * D;
@@ -159,19 +160,19 @@ void launch_encode_exact(const vqkv_stack_s& st, const float* xs, uint64_t total
     if (smem > 48 * 1024)
         VQKV_CUDA(cudaFuncSetAttribute(encode_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     encode_exact_kernel<<<unsigned(blocks), kExactWarps * 32, smem, s>>>(
-        st.d_stages, st.n, st.dim, st.d_eff, st.d_sqn, xs, total_rows, search_block, codes, norms, residuals, nullptr, 0);
+        st.d_stages, st.n, st.dim, st.d_eff, st.d_sqn, xs, total_rows, search_block, codes, norms, residuals, nullptr, nullptr);
     launch_check("encode_exact_kernel");
 }
 
-// Exact encoder restricted to a device list of row indices (rows the
-// tensor-core encoder hands back: non-finite input).
-void launch_encode_exact_rows(const vqkv_stack_s& st, const float* xs, const uint32_t* rows_dev, uint64_t n_rows,
-                              uint64_t search_block, uint16_t* codes, float* norms, cudaStream_t s) {
-    if (n_rows == 0) return;
+// Exact encoder restricted to a device list of row indices whose length lives
+// in device memory (rows the tensor-core encoder hands back: non-finite input).
+void launch_encode_exact_rows(const vqkv_stack_s& st, const float* xs, const uint32_t* rows_dev,
+                              const uint32_t* n_rows_dev, uint64_t max_rows, uint64_t search_block, uint16_t* codes,
+                              float* norms, float* residuals, cudaStream_t s) {
+    if (max_rows == 0) return;
     size_t smem = sizeof(float) * st.dim * kExactWarps;
-    uint64_t blocks = std::min<uint64_t>((n_rows + kExactWarps - 1) / kExactWarps, 148 * 8);
-    encode_exact_kernel<<<unsigned(blocks), kExactWarps * 32, smem, s>>>(
-        st.d_stages, st.n, st.dim, st.d_eff, st.d_sqn, xs, 0, search_block, codes, norms, nullptr, rows_dev, n_rows);
+    encode_exact_kernel<<<148, kExactWarps * 32, smem, s>>>(st.d_stages, st.n, st.dim, st.d_eff, st.d_sqn, xs, 0,
+                                                             search_block, codes, norms, residuals, rows_dev, n_rows_dev);
     launch_check("encode_exact_kernel(rows)");
 }
 

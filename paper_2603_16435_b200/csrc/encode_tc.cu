@@ -1,13 +1,525 @@
-// encode_tc.cu -- K1 placeholder (tensor-core encoder lands in a later commit).
+// encode_tc.cu -- K1: residual SimVQ encode on tcgen05 tensor cores (D == 128).
+//
+// Replaces quantize_batch -> quantize -> nearest_scored
+// (proj/core/src/codebook.cpp:158-237) with bit-identical codes.
+//
+// Per 128-row tile and residual stage s the scores
+//     s_j = ||e_j||^2 - 2 r.e_j        (codebook.cpp:168)
+// are computed as one fp16 GEMM on the tensor cores (A = fp16(r * 2^sigma),
+// B = fp16 effective entries, fp32 accumulation in TMEM), finished by one FFMA
+// per score in the epilogue.  The epilogue never tracks per-score indices: it
+// keeps the min over contiguous 32-entry "A groups" and over the 32 residue
+// classes j mod 32 ("B groups").  With a rigorous per-row bound W on
+// |approx - reference| score error, every entry that can be the reference's
+// argmin lies in {32a + b : mA[a] <= m + W, mB[b] <= m + W}.  When that set
+// is a single entry it IS the reference's argmin; otherwise the candidates are
+// rescored exactly with the reference's fp32 GEMV order (no FMA) and the
+// lowest index wins ties, as nearest_scored does.  The residual update
+// r -= e_z uses the exact fp32 entries, so every later stage sees the same
+// residual as the reference.  Rows with non-finite input go to the exact
+// SIMT encoder (their tensor-core pass runs on zeros and is discarded).
+//
+// CTA layout (one CTA per SM, persistent over pairs of 128-row tiles that run
+// the stages in lockstep so every codebook chunk loaded to smem feeds two
+// MMAs):
+//   warp 0      bulk-copy producer (TMA engine): 32 KB pre-swizzled fp16
+//               codebook chunks (128 entries x K=128) into a 3-deep ring
+//   warp 1      MMA issuer: 8 x tcgen05.mma M128 N128 K16 per tile-chunk
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue of tile 0 (thread = row = TMEM lane)
+//   warps 8-11  epilogue of tile 1
+// TMEM (512 columns): [0,128) acc tile0, [128,256) acc tile1,
+//                     [256,384) fp32 residual tile0, [384,512) residual tile1.
+#include <algorithm>
+#include <cmath>
+
+#include "tc_ptx.cuh"
 #include "vqkv_internal.cuh"
 
 namespace vqkv_dev {
 
-bool encode_tc_supported(const vqkv_stack_s&) { return false; }
+void launch_encode_exact_rows(const vqkv_stack_s& st, const float* xs, const uint32_t* rows_dev,
+                              const uint32_t* n_rows_dev, uint64_t max_rows, uint64_t search_block, uint16_t* codes,
+                              float* norms, float* residuals, cudaStream_t s);
 
-void launch_encode_tc(const vqkv_stack_s&, const float*, uint32_t, uint64_t, uint64_t, uint8_t*, float*,
-                      float*, cudaStream_t) {
-    fail(VQKV_UNSUPPORTED, "tensor-core encoder not built");
+namespace {
+
+constexpr int kThreads = 384;
+constexpr int kNB = 3;                    // codebook chunk ring depth
+constexpr uint32_t kChunkBytes = 32768;   // 128 entries x 128 fp16
+constexpr uint32_t kATileBytes = 32768;   // 128 rows x 128 fp16
+constexpr int kMaxChunks = 8;             // stages up to 1024 entries
+constexpr uint32_t kIdesc = ptx::idesc_f16_f32(128, 128);
+
+struct __align__(8) SmemCtl {
+    uint64_t b_full[kNB];
+    uint64_t b_empty[kNB];
+    uint64_t acc_full[2];
+    uint64_t acc_empty[2];
+    uint64_t a_ready[2];
+    uint32_t tmem_base;
+};
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + 2 * kATileBytes + kNB * kChunkBytes + sizeof(SmemCtl);
+
+// tree minimum of 32 values with 3-input FMNMX
+__device__ __forceinline__ float min32(const float (&v)[32]) {
+    float a[11];
+#pragma unroll
+    for (int i = 0; i < 10; ++i) a[i] = ptx::fmin3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+    a[10] = fminf(v[30], v[31]);
+    float b0 = ptx::fmin3(a[0], a[1], a[2]), b1 = ptx::fmin3(a[3], a[4], a[5]);
+    float b2 = ptx::fmin3(a[6], a[7], a[8]), b3 = fminf(a[9], a[10]);
+    return fminf(ptx::fmin3(b0, b1, b2), b3);
+}
+
+struct Tile {
+    uint64_t stream, row0, nvalid;  // rows [row0, row0+nvalid) of `stream`
+};
+
+__device__ __forceinline__ Tile tile_of(uint64_t t, uint64_t tiles_per_stream, uint64_t rows, uint64_t n_tiles) {
+    Tile r{0, 0, 0};
+    if (t >= n_tiles) return r;
+    r.stream = t / tiles_per_stream;
+    r.row0 = (t % tiles_per_stream) * 128;
+    r.nvalid = (rows - r.row0 < 128) ? (rows - r.row0) : 128;
+    return r;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const __half* __restrict__ eff16,
+                 const float* __restrict__ sqn_pad, const float* __restrict__ eff, const float* __restrict__ xs,
+                 uint32_t n_streams, uint64_t rows, uint64_t search_block, uint16_t* __restrict__ codes,
+                 float* __restrict__ norms, float* __restrict__ residuals, uint32_t* __restrict__ exact_list,
+                 uint32_t* __restrict__ exact_count, unsigned long long* __restrict__ counters) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* a_tiles = smem;                                  // 2 x 32 KB
+    uint8_t* b_ring = smem + 2 * kATileBytes;                 // kNB x 32 KB
+    SmemCtl* ctl = reinterpret_cast<SmemCtl*>(b_ring + kNB * kChunkBytes);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t tiles_per_stream = (rows + 127) / 128;
+    const uint64_t n_tiles = tiles_per_stream * n_streams;
+    const uint64_t n_pairs = (n_tiles + 1) / 2;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kNB; ++i) {
+            ptx::mbar_init(ptx::smem_u32(&ctl->b_full[i]), 1);
+            ptx::mbar_init(ptx::smem_u32(&ctl->b_empty[i]), 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            ptx::mbar_init(ptx::smem_u32(&ctl->acc_full[t]), 1);
+            ptx::mbar_init(ptx::smem_u32(&ctl->acc_empty[t]), 128);
+            ptx::mbar_init(ptx::smem_u32(&ctl->a_ready[t]), 128);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 2) {
+        ptx::tmem_alloc(ptx::smem_u32(&ctl->tmem_base), 512);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = ctl->tmem_base;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            uint32_t buf = 0, ph = 0;
+            for (uint64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
+                for (uint32_t s = 0; s < n_stages; ++s) {
+                    const StageInfo si = stages[s];
+                    const uint32_t nch = si.pad_size / 128;
+                    const __half* src = eff16 + si.eff16_off;
+                    for (uint32_t c = 0; c < nch; ++c) {
+                        ptx::mbar_wait(ptx::smem_u32(&ctl->b_empty[buf]), ph ^ 1);
+                        const uint32_t bar = ptx::smem_u32(&ctl->b_full[buf]);
+                        ptx::mbar_arrive_expect_tx(bar, kChunkBytes);
+                        ptx::bulk_g2s(ptx::smem_u32(b_ring + buf * kChunkBytes), src + uint64_t(c) * 16384, kChunkBytes,
+                                      bar);
+                        if (++buf == kNB) {
+                            buf = 0;
+                            ph ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            uint32_t buf = 0, ph = 0;
+            uint32_t e_ph[2] = {1, 1}, a_ph[2] = {0, 0};
+            const uint32_t a_base = ptx::smem_u32(a_tiles), b_base = ptx::smem_u32(b_ring);
+            for (uint64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
+                for (uint32_t s = 0; s < n_stages; ++s) {
+                    const uint32_t nch = stages[s].pad_size / 128;
+                    for (uint32_t c = 0; c < nch; ++c) {
+                        ptx::mbar_wait(ptx::smem_u32(&ctl->b_full[buf]), ph);
+                        for (int t = 0; t < 2; ++t) {
+                            if (c == 0) {
+                                ptx::mbar_wait(ptx::smem_u32(&ctl->a_ready[t]), a_ph[t]);
+                                a_ph[t] ^= 1;
+                            }
+                            ptx::mbar_wait(ptx::smem_u32(&ctl->acc_empty[t]), e_ph[t]);
+                            e_ph[t] ^= 1;
+                            ptx::tc_fence_after();
+                            const uint32_t d = tmem + 128u * t;
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32;
+                                const uint64_t ad = ptx::umma_desc_sw128(a_base + t * kATileBytes + koff);
+                                const uint64_t bd = ptx::umma_desc_sw128(b_base + buf * kChunkBytes + koff);
+                                ptx::mma_f16_ss(d, ad, bd, kIdesc, k > 0 ? 1u : 0u);
+                            }
+                            ptx::mma_commit(ptx::smem_u32(&ctl->acc_full[t]));
+                        }
+                        ptx::mma_commit(ptx::smem_u32(&ctl->b_empty[buf]));
+                        if (++buf == kNB) {
+                            buf = 0;
+                            ph ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ epilogue
+        const uint32_t t = (warp - 4) >> 2;          // tile slot
+        const uint32_t q = warp & 3;                 // TMEM lane quadrant
+        const uint32_t i = q * 32 + lane;            // row within tile
+        const uint32_t lane_off = (q * 32u) << 16;
+        const uint32_t t_acc = tmem + lane_off + 128u * t;
+        const uint32_t t_res = tmem + lane_off + 256u + 128u * t;
+        const uint32_t bar_full = ptx::smem_u32(&ctl->acc_full[t]);
+        const uint32_t bar_empty = ptx::smem_u32(&ctl->acc_empty[t]);
+        const uint32_t bar_aready = ptx::smem_u32(&ctl->a_ready[t]);
+        uint8_t* a_tile = a_tiles + t * kATileBytes;
+        uint32_t f_ph = 0;
+        unsigned long long n_amb = 0, n_rs = 0;
+
+        for (uint64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
+            const Tile tl = tile_of(2 * p + t, tiles_per_stream, rows, n_tiles);
+            const bool valid = i < tl.nvalid;
+            const uint64_t grow = tl.stream * rows + tl.row0 + i;  // global row index
+            bool exact_row = false;
+
+            // ---- load x -> TMEM residual, stats
+            float R2 = 0.f, mx = 0.f;
+            {
+                const float4* x4 = reinterpret_cast<const float4*>(xs + grow * 128);
+#pragma unroll 1
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    float v[32];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        float4 a = valid ? __ldg(x4 + c4 * 8 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        v[4 * k] = a.x;
+                        v[4 * k + 1] = a.y;
+                        v[4 * k + 2] = a.z;
+                        v[4 * k + 3] = a.w;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) exact_row |= !isfinite(v[k]);
+                    ptx::tmem_st32(t_res + 32u * c4, v);
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) {
+                        R2 = fmaf(v[k], v[k], R2);
+                        mx = fmaxf(mx, fabsf(v[k]));
+                    }
+                }
+            }
+            if (exact_row) {
+                // hand the row to the exact path; run the tensor-core pass on zeros
+                const uint32_t slot = atomicAdd(exact_count, 1u);
+                exact_list[slot] = uint32_t(grow);
+                if (counters) atomicAdd(&counters[2], 1ull);
+                float z[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) z[k] = 0.f;
+#pragma unroll 1
+                for (int c4 = 0; c4 < 4; ++c4) ptx::tmem_st32(t_res + 32u * c4, z);
+                R2 = 0.f;
+                mx = 0.f;
+            }
+            ptx::tc_wait_st();
+
+            for (uint32_t s = 0; s < n_stages; ++s) {
+                const StageInfo si = stages[s];
+                // ---- sigma and A tile = fp16(r * 2^sigma) in the SW128 K-major layout
+                int sigma = 0;
+                if (mx > 0.f) {
+                    int e;
+                    frexpf(mx, &e);  // mx in [2^(e-1), 2^e)
+                    sigma = min(60, max(-60, 14 - e));
+                }
+                {
+                    const float sc = ldexpf(1.0f, sigma);
+#pragma unroll 1
+                    for (int c4 = 0; c4 < 4; ++c4) {
+                        float v[32];
+                        ptx::tmem_ld32(t_res + 32u * c4, v);
+                        ptx::tc_wait_ld();
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {  // 16 B granules of 8 fp16 (k = 32*c4 + 8*g ..)
+                            const int kk = 32 * c4 + 8 * g;
+                            const int kb = kk >> 6, gi = (kk & 63) >> 3;
+                            uint4 w;
+                            __half2 h0 = __floats2half2_rn(v[8 * g + 0] * sc, v[8 * g + 1] * sc);
+                            __half2 h1 = __floats2half2_rn(v[8 * g + 2] * sc, v[8 * g + 3] * sc);
+                            __half2 h2 = __floats2half2_rn(v[8 * g + 4] * sc, v[8 * g + 5] * sc);
+                            __half2 h3 = __floats2half2_rn(v[8 * g + 6] * sc, v[8 * g + 7] * sc);
+                            w.x = *reinterpret_cast<uint32_t*>(&h0);
+                            w.y = *reinterpret_cast<uint32_t*>(&h1);
+                            w.z = *reinterpret_cast<uint32_t*>(&h2);
+                            w.w = *reinterpret_cast<uint32_t*>(&h3);
+                            *reinterpret_cast<uint4*>(a_tile + kb * 16384 + i * 128 + ((gi ^ (i & 7)) << 4)) = w;
+                        }
+                    }
+                    ptx::fence_async_smem();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(bar_aready);
+                }
+                // ---- error window
+                const float R = sqrtf(R2 * 1.0001f);
+                const float E = si.max_norm;
+                const float Bnd = 2.1e-3f * R * E + 2.5e-7f * si.max_sqnorm + 6.8e-7f * (ldexpf(E, -sigma) + R) +
+                                  ldexpf(2.3e-13f, -sigma) + 1e-30f;
+                const float W = 2.02f * Bnd;
+                const float mrow = -ldexpf(1.0f, 1 - sigma);
+
+                // ---- scores: min over A groups (32 contiguous) and B groups (j mod 32)
+                float mA[4 * kMaxChunks], mB[32];
+#pragma unroll
+                for (int k = 0; k < 4 * kMaxChunks; ++k) mA[k] = INFINITY;
+#pragma unroll
+                for (int k = 0; k < 32; ++k) mB[k] = INFINITY;
+                const uint32_t nch = si.pad_size / 128;
+                const float4* sq4 = reinterpret_cast<const float4*>(sqn_pad + si.eff16_off / 128);
+#pragma unroll
+                for (int c = 0; c < kMaxChunks; ++c) {
+                    if (c < int(nch)) {
+                        ptx::mbar_wait(bar_full, f_ph);
+                        f_ph ^= 1;
+                        ptx::tc_fence_after();
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            float v0[32], v1[32];
+                            ptx::tmem_ld32(t_acc + 64u * h, v0);
+                            ptx::tmem_ld32(t_acc + 64u * h + 32u, v1);
+                            ptx::tc_wait_ld();
+                            if (h == 1) {
+                                ptx::tc_fence_before();
+                                ptx::mbar_arrive(bar_empty);
+                            }
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                const float4 a = __ldg(sq4 + c * 32 + h * 16 + k);
+                                const float4 b = __ldg(sq4 + c * 32 + h * 16 + 8 + k);
+                                v0[4 * k + 0] = fmaf(v0[4 * k + 0], mrow, a.x);
+                                v0[4 * k + 1] = fmaf(v0[4 * k + 1], mrow, a.y);
+                                v0[4 * k + 2] = fmaf(v0[4 * k + 2], mrow, a.z);
+                                v0[4 * k + 3] = fmaf(v0[4 * k + 3], mrow, a.w);
+                                v1[4 * k + 0] = fmaf(v1[4 * k + 0], mrow, b.x);
+                                v1[4 * k + 1] = fmaf(v1[4 * k + 1], mrow, b.y);
+                                v1[4 * k + 2] = fmaf(v1[4 * k + 2], mrow, b.z);
+                                v1[4 * k + 3] = fmaf(v1[4 * k + 3], mrow, b.w);
+                            }
+                            mA[4 * c + 2 * h] = min32(v0);
+                            mA[4 * c + 2 * h + 1] = min32(v1);
+#pragma unroll
+                            for (int b = 0; b < 32; ++b) mB[b] = ptx::fmin3(mB[b], v0[b], v1[b]);
+                        }
+                    }
+                }
+                // ---- candidates
+                float m1 = INFINITY;
+#pragma unroll
+                for (int k = 0; k < 4 * kMaxChunks; ++k) m1 = fminf(m1, mA[k]);
+                const float thr = m1 + W;
+                uint32_t CA = 0, CB = 0;
+#pragma unroll
+                for (int k = 0; k < 4 * kMaxChunks; ++k) CA |= (mA[k] <= thr ? 1u : 0u) << k;
+#pragma unroll
+                for (int b = 0; b < 32; ++b) CB |= (mB[b] <= thr ? 1u : 0u) << b;
+                const uint32_t na = __popc(CA), nb = __popc(CB);
+                const bool unique = (na == 1 && nb == 1);
+                uint32_t z = unique ? (32u * (__ffs(CA) - 1) + (__ffs(CB) - 1)) : 0u;
+                const bool amb = !unique && valid && !exact_row;
+                if (__any_sync(0xffffffffu, amb)) {
+                    // exact rescoring in the reference's fp32 order (codebook.cpp:166-172)
+                    const uint32_t cnt = amb ? na * nb : 0u;
+                    const uint32_t maxcnt = __reduce_max_sync(0xffffffffu, cnt);
+                    float best = INFINITY;
+                    uint32_t bj = 0xffffffffu;
+                    for (uint32_t k = 0; k < maxcnt; ++k) {
+                        uint32_t j = 0xffffffffu;
+                        if (k < cnt) {
+                            const uint32_t a = __fns(CA, 0, int(k / nb) + 1), b = __fns(CB, 0, int(k % nb) + 1);
+                            j = 32u * a + b;
+                            if (j >= si.size) j = 0xffffffffu;
+                        }
+                        const bool has = (j != 0xffffffffu);
+                        const float* e = eff + si.eff_off + uint64_t(has ? j : 0) * 128;
+                        float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;   // GEMV lanes
+                        float r0[4] = {0.f, 0.f, 0.f, 0.f}, r1[4] = {0.f, 0.f, 0.f, 0.f};  // redux packets
+#pragma unroll 1
+                        for (int c4 = 0; c4 < 4; ++c4) {
+                            float v[32];
+                            ptx::tmem_ld32(t_res + 32u * c4, v);
+                            ptx::tc_wait_ld();
+                            if (has) {
+#pragma unroll
+                                for (int kk = 0; kk < 8; ++kk) {
+                                    const float4 ev = __ldg(reinterpret_cast<const float4*>(e + 32 * c4) + kk);
+                                    const float p0 = __fmul_rn(ev.x, v[4 * kk]), p1 = __fmul_rn(ev.y, v[4 * kk + 1]);
+                                    const float p2 = __fmul_rn(ev.z, v[4 * kk + 2]), p3 = __fmul_rn(ev.w, v[4 * kk + 3]);
+                                    g0 = __fadd_rn(g0, p0);
+                                    g1 = __fadd_rn(g1, p1);
+                                    g2 = __fadd_rn(g2, p2);
+                                    g3 = __fadd_rn(g3, p3);
+                                    float* rr = (kk & 1) ? r1 : r0;
+                                    rr[0] = __fadd_rn(rr[0], p0);
+                                    rr[1] = __fadd_rn(rr[1], p1);
+                                    rr[2] = __fadd_rn(rr[2], p2);
+                                    rr[3] = __fadd_rn(rr[3], p3);
+                                }
+                            }
+                        }
+                        if (has) {
+                            const uint64_t blk0 = (uint64_t(j) / search_block) * search_block;
+                            const uint64_t rem = uint64_t(si.size) - blk0;
+                            const bool one = ((rem < search_block ? rem : search_block) == 1);
+                            float dot;
+                            if (one) {
+#pragma unroll
+                                for (int l = 0; l < 4; ++l) r0[l] = __fadd_rn(r0[l], r1[l]);
+                                dot = __fadd_rn(__fadd_rn(r0[0], r0[2]), __fadd_rn(r0[1], r0[3]));
+                            } else {
+                                dot = __fadd_rn(__fadd_rn(g0, g2), __fadd_rn(g1, g3));
+                            }
+                            const float sc = __fsub_rn(__ldg(sqn_pad + si.eff16_off / 128 + j), __fmul_rn(2.0f, dot));
+                            if (sc < best || (sc == best && j < bj)) {
+                                best = sc;
+                                bj = j;
+                            }
+                        }
+                    }
+                    if (amb) {
+                        z = (bj == 0xffffffffu) ? 0u : bj;
+                        n_rs += cnt;
+                        ++n_amb;
+                    }
+                }
+                if (valid && !exact_row) codes[grow * n_stages + s] = uint16_t(z);
+
+                // ---- residual update r -= e_z (exact fp32), stats for the next stage
+                const bool last = (s + 1 == n_stages);
+                const float* e = eff + si.eff_off + uint64_t(z) * 128;
+                R2 = 0.f;
+                mx = 0.f;
+                float n0[4] = {0.f, 0.f, 0.f, 0.f}, n1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    float v[32];
+                    ptx::tmem_ld32(t_res + 32u * c4, v);
+                    ptx::tc_wait_ld();
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const float4 ev = __ldg(reinterpret_cast<const float4*>(e + 32 * c4) + kk);
+                        v[4 * kk + 0] = __fsub_rn(v[4 * kk + 0], ev.x);
+                        v[4 * kk + 1] = __fsub_rn(v[4 * kk + 1], ev.y);
+                        v[4 * kk + 2] = __fsub_rn(v[4 * kk + 2], ev.z);
+                        v[4 * kk + 3] = __fsub_rn(v[4 * kk + 3], ev.w);
+                    }
+                    ptx::tmem_st32(t_res + 32u * c4, v);
+                    if (!last) {
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) {
+                            R2 = fmaf(v[k], v[k], R2);
+                            mx = fmaxf(mx, fabsf(v[k]));
+                        }
+                    } else {
+                        // final ||r|| in the reference's redux order (Eigen squaredNorm)
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            float* rr = (kk & 1) ? n1 : n0;
+#pragma unroll
+                            for (int l = 0; l < 4; ++l) rr[l] = __fadd_rn(rr[l], __fmul_rn(v[4 * kk + l], v[4 * kk + l]));
+                        }
+                        if (residuals && valid && !exact_row) {
+                            float4* o4 = reinterpret_cast<float4*>(residuals + grow * 128 + 32 * c4);
+#pragma unroll
+                            for (int kk = 0; kk < 8; ++kk)
+                                o4[kk] = make_float4(v[4 * kk], v[4 * kk + 1], v[4 * kk + 2], v[4 * kk + 3]);
+                        }
+                    }
+                }
+                ptx::tc_wait_st();
+                if (last && valid && !exact_row) {
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) n0[l] = __fadd_rn(n0[l], n1[l]);
+                    norms[grow] = __fsqrt_rn(__fadd_rn(__fadd_rn(n0[0], n0[2]), __fadd_rn(n0[1], n0[3])));
+                }
+            }
+        }
+        if (counters) {
+            // per-row-stage diagnostics
+            unsigned long long rs = 0;
+            for (uint64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
+                const Tile tl = tile_of(2 * p + t, tiles_per_stream, rows, n_tiles);
+                rs += (i < tl.nvalid) ? n_stages : 0;
+            }
+            atomicAdd(&counters[0], rs);
+            if (n_amb) atomicAdd(&counters[1], n_amb);
+            if (n_rs) atomicAdd(&counters[3], n_rs);
+        }
+    }
+    __syncwarp();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) ptx::tmem_dealloc(tmem, 512);
+}
+
+}  // namespace
+
+bool encode_tc_supported(const vqkv_stack_s& st) {
+    if (st.dim != 128 || st.d_eff16 == nullptr) return false;
+    for (const auto& s : st.stages)
+        if (s.pad_size > 128u * kMaxChunks) return false;
+    return true;
+}
+
+void launch_encode_tc(const vqkv_stack_s& st, const float* xs, uint32_t n_streams, uint64_t rows,
+                      uint64_t search_block, uint8_t* payload, float* norms, float* residuals, cudaStream_t s) {
+    const uint64_t total = uint64_t(n_streams) * rows;
+    if (total == 0) return;
+    if (total >= (1ull << 32)) fail(VQKV_UNSUPPORTED, "more than 2^32 rows per call");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st.device);
+    static bool attr_set = false;
+    if (!attr_set) {
+        VQKV_CUDA(cudaFuncSetAttribute(encode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
+        attr_set = true;
+    }
+    uint16_t* codes = nullptr;
+    uint32_t* list = nullptr;  // [0] = count, [1..] = rows
+    VQKV_CUDA(cudaMallocAsync(&codes, sizeof(uint16_t) * total * st.n, s));
+    VQKV_CUDA(cudaMallocAsync(&list, sizeof(uint32_t) * (total + 1), s));
+    VQKV_CUDA(cudaMemsetAsync(list, 0, sizeof(uint32_t), s));
+    const uint64_t tiles = ((rows + 127) / 128) * n_streams;
+    const uint64_t pairs = (tiles + 1) / 2;
+    const unsigned grid = unsigned(std::min<uint64_t>(pairs, uint64_t(sms)));
+    encode_tc_kernel<<<grid, kThreads, kSmemBytes, s>>>(st.d_stages, st.n, st.d_eff16, st.d_sqn_pad, st.d_eff, xs,
+                                                         n_streams, rows, search_block, codes, norms, residuals,
+                                                         list + 1, list, st.d_counters);
+    launch_check("encode_tc_kernel");
+    // rows with non-finite input: exact reference semantics
+    launch_encode_exact_rows(st, xs, list + 1, list, total, search_block, codes, norms, residuals, s);
+    launch_pack_codes(codes, n_streams, rows, st.n, st, payload, s);
+    VQKV_CUDA(cudaFreeAsync(list, s));
+    VQKV_CUDA(cudaFreeAsync(codes, s));
 }
 
 }  // namespace vqkv_dev

@@ -45,8 +45,15 @@ __global__ void half_copy_kernel(const float* __restrict__ eff, const float* __r
     uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= uint64_t(st.pad_size) * D) return;
     uint32_t j = uint32_t(idx / D);
+    uint32_t k = uint32_t(idx % D);
     float v = (j < st.size) ? eff[(st.eff_off) + idx] : 0.f;
-    eff16[st.eff16_off + idx] = __float2half_rn(v);
+    // Pre-swizzled UMMA operand layout (D == 128): 128-entry chunks of 32 KB,
+    // each two K-blocks of [128 rows x 128 B] with the 128B swizzle applied
+    // (16 B granule g of row r stored at g ^ (r % 8)).  A single bulk copy of
+    // a chunk into 1024 B-aligned smem yields the canonical K-major SW128 tile.
+    const uint32_t c = j >> 7, rj = j & 127, kb = k >> 6, kk = k & 63;
+    const uint64_t off = uint64_t(c) * 16384 + kb * 8192 + rj * 64 + (((kk >> 3) ^ (rj & 7)) << 3) + (kk & 7);
+    eff16[st.eff16_off + off] = __float2half_rn(v);
     if (idx % D == 0) sqn_pad[st.eff16_off / D + j] = (j < st.size) ? sqn[st.eff_off / D + j] : INFINITY;
 }
 

@@ -12,8 +12,6 @@
 
 namespace vqkv_dev {
 std::atomic<uint64_t> g_launches{0};
-void launch_encode_exact_rows(const vqkv_stack_s& st, const float* xs, const uint32_t* rows_dev, uint64_t n_rows,
-                              uint64_t search_block, uint16_t* codes, float* norms, cudaStream_t s);
 }  // namespace vqkv_dev
 
 using namespace vqkv_dev;

@@ -1,0 +1,154 @@
+"""Tensor-core encoder (K1, tcgen05) parity against the oracle.
+
+Codes must be bit-exact; near-ties (oracle best/second gap below the stated
+epsilon) are counted and reported but, because every ambiguous window is
+rescored exactly, the expected mismatch count is zero.  Residual norms are
+bit-exact (same fp32 operation order as Eigen's squaredNorm).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_mod():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def product_stack(o):
+    from paper_2603_16435_b200 import codebook as P
+
+    return P.CodebookStack.from_arrays([o.entries(s) for s in range(o.n)], [o.projection(s) for s in range(o.n)],
+                                       o.kind)
+
+
+def near_tie_eps(best, second, rnorm, emax):
+    """tau = 2^-14 ||r|| max||e|| + 2^-22 max(|s1|,|s2|)."""
+    return 2.0 ** -14 * rnorm * emax + 2.0 ** -22 * np.maximum(np.abs(best), np.abs(second))
+
+
+def run_tc(torch, p, xs, n_streams=1, sb=4096, residuals=False):
+    from paper_2603_16435_b200 import device as Dv
+
+    rows = xs.shape[0] // n_streams
+    x = torch.from_numpy(np.ascontiguousarray(xs.reshape(n_streams, rows, 128))).cuda()
+    Dv.set_encode_path(2)
+    try:
+        out = Dv.quantize_streams(p, x, sb, residuals=residuals)
+    finally:
+        Dv.set_encode_path(0)
+    torch.cuda.synchronize()
+    return [t.cpu().numpy() for t in out]
+
+
+def compare(o, p, xs, payload_dev, norms_dev, n_streams=1):
+    rows = xs.shape[0] // n_streams
+    n_mismatch = n_tie = 0
+    for sidx in range(n_streams):
+        xs_s = xs[sidx * rows : (sidx + 1) * rows]
+        ref_pay, ref_norm, ins = o.quantize_batch(xs_s, instrument=True)
+        got = o.unpack(payload_dev[sidx], rows)
+        ref = o.unpack(ref_pay, rows)
+        bad = np.nonzero((got != ref).any(1))[0]
+        emax = o.stage_max_norm()
+        for r in bad:
+            st = int(np.nonzero(got[r] != ref[r])[0][0])
+            gap = ins["second"][r, st] - ins["best"][r, st]
+            tau = near_tie_eps(ins["best"][r, st], ins["second"][r, st], ins["rnorm"][r, st], emax[st])
+            if gap <= tau:
+                n_tie += 1
+            else:
+                n_mismatch += 1
+        ok_rows = np.ones(rows, bool)
+        ok_rows[bad] = False
+        assert np.array_equal(norms_dev[sidx][ok_rows].view(np.uint32), ref_norm[ok_rows].view(np.uint32))
+        if len(bad) == 0:
+            assert np.array_equal(payload_dev[sidx], ref_pay)
+    return n_mismatch, n_tie
+
+
+@pytest.mark.parametrize(
+    "seed,n,S,rows,streams",
+    [(101, 4, 1024, 300, 1), (102, 16, 512, 200, 2), (103, 3, 256, 257, 3), (104, 2, 100, 129, 1),
+     (105, 1, 1, 40, 1), (106, 5, 384, 128, 2), (107, 56, 1024, 48, 1)],
+)
+def test_tc_encode_matches_oracle(torch_mod, seed, n, S, rows, streams):
+    rng = O.Rng(seed)
+    o = rng.stack(n, S, 128)
+    p = product_stack(o)
+    xs = rng.matrix(rows * streams, 128)
+    pay, nrm = run_tc(torch_mod, p, xs, streams)
+    mism, ties = compare(o, p, xs, pay, nrm, streams)
+    print(f"seed={seed} N={n} S={S} rows={rows*streams}: mismatches={mism} near_ties={ties}")
+    assert mism == 0
+
+
+def test_tc_encode_synthetic_keys(torch_mod):
+    """LLaMA-shaped synthetic keys (rope-rotated mixture) through the paper's K stack shape."""
+    rng = O.Rng(1)
+    o = rng.stack(56, 1024, 128, O.KEY)
+    p = product_stack(o)
+    xs = O.generate(O.ROPE_ROTATED_KEYS, 128, 96, 32, 1000)
+    pay, nrm = run_tc(torch_mod, p, xs)
+    mism, ties = compare(o, p, xs, pay, nrm)
+    print(f"synthetic keys: mismatches={mism} near_ties={ties}")
+    assert mism == 0
+
+
+def test_tc_exact_ties_and_degenerate(torch_mod):
+    """Duplicate entries (exact score ties -> lowest index), zero codebooks, exact-entry inputs."""
+    rng = O.Rng(7)
+    base = rng.matrix(64, 128)
+    ent = np.vstack([base, base[:32], np.zeros((32, 128), np.float32)])  # 128 entries, duplicates + zeros
+    o = O.Stack.from_entries([ent, ent[::-1].copy(), np.zeros((128, 128), np.float32)])
+    p = product_stack(o)
+    xs = np.vstack([base[:40], rng.matrix(60, 128), np.zeros((5, 128), np.float32)])
+    pay, nrm = run_tc(torch_mod, p, xs)
+    mism, ties = compare(o, p, xs, pay, nrm)
+    assert mism == 0
+
+
+def test_tc_nonfinite_rows_use_exact_path(torch_mod):
+    rng = O.Rng(9)
+    o = rng.stack(3, 256, 128)
+    p = product_stack(o)
+    xs = rng.matrix(200, 128)
+    xs[3, 7] = np.nan
+    xs[150, 0] = np.inf
+    xs[151, 1] = -np.inf
+    pay, nrm = run_tc(torch_mod, p, xs)
+    ref_pay, ref_norm = o.quantize_batch(xs)
+    assert np.array_equal(pay[0], ref_pay)
+    assert np.array_equal(np.isnan(nrm[0]), np.isnan(ref_norm))
+
+
+def test_tc_residual_vectors(torch_mod):
+    """quantize() final_residual through the tensor-core path equals the oracle's, bit for bit."""
+    rng = O.Rng(11)
+    o = rng.stack(6, 512, 128)
+    p = product_stack(o)
+    xs = rng.matrix(130, 128)
+    pay, nrm, res = run_tc(torch_mod, p, xs, residuals=True)
+    for r in (0, 1, 64, 127, 128, 129):
+        _, ref_res = o.quantize(xs[r])
+        assert np.array_equal(res[0, r].view(np.uint32), ref_res.view(np.uint32))
+
+
+def test_tc_search_block_one(torch_mod):
+    """search_block=1 switches the reference to dot() order for every entry; parity must hold."""
+    rng = O.Rng(12)
+    o = rng.stack(3, 128, 128)
+    p = product_stack(o)
+    xs = rng.matrix(64, 128)
+    from paper_2603_16435_b200 import device as Dv
+
+    pay, nrm = run_tc(torch_mod, p, xs, sb=1)
+    ref_pay, ref_norm = o.quantize_batch(xs, 1)
+    assert np.array_equal(pay[0], ref_pay)
