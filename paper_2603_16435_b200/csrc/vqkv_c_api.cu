@@ -234,7 +234,7 @@ int vqkv_quantize_batch_ex(vqkv_stack_t s, const float* xs, uint32_t n_streams, 
         need(sb >= 1, VQKV_INVALID_INPUT, "search_block must be >= 1");
         const uint64_t total = uint64_t(n_streams) * rows;
         if (total == 0) return;  // codebook.cpp:227: empty batch is valid
-        need(xs && payload && norms, VQKV_INVALID_INPUT, "null device buffer");
+        need(xs && norms && (payload || s->row_bits == 0), VQKV_INVALID_INPUT, "null device buffer");
         DeviceGuard g(s->device);
         quantize_device(*s, xs, n_streams, rows, sb, payload, norms, residuals, as_stream(stream));
     });
@@ -247,7 +247,7 @@ int vqkv_quantize_batch_host(vqkv_stack_t s, const float* xs, uint32_t n_streams
         need(sb >= 1, VQKV_INVALID_INPUT, "search_block must be >= 1");
         const uint64_t total = uint64_t(n_streams) * rows;
         if (total == 0) return;
-        need(xs && payload && norms, VQKV_INVALID_INPUT, "null host buffer");
+        need(xs && norms && (payload || s->row_bits == 0), VQKV_INVALID_INPUT, "null host buffer");
         DeviceGuard g(s->device);
         cudaStream_t cs = as_stream(stream);
         const uint64_t D = s->dim;
