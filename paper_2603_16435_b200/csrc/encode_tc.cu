@@ -72,6 +72,39 @@ __device__ __forceinline__ float min32(const float (&v)[32]) {
     return fminf(ptx::fmin3(b0, b1, b2), b3);
 }
 
+__device__ __forceinline__ int sigma_of(float m) {
+    // power-of-two row scale so that m * 2^sigma lies in [2^13, 2^14)
+    if (!(m > 0.f) || !isfinite(m)) return 0;
+    int e;
+    frexpf(m, &e);  // m in [2^(e-1), 2^e)
+    return min(60, max(-60, 14 - e));
+}
+
+// order-preserving map float -> uint32 (for packed (score, index) keys)
+__device__ __forceinline__ uint32_t f2ord(float x) {
+    const uint32_t b = __float_as_uint(x);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// fp16(v * sc) for columns [32*c4, 32*c4+32) of row i into the SW128 K-major A tile
+__device__ __forceinline__ void store_a_chunk(uint8_t* a_tile, uint32_t i, int c4, const float (&v)[32], float sc) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const int kk = 32 * c4 + 8 * g;
+        const int kb = kk >> 6, gi = (kk & 63) >> 3;
+        __half2 h0 = __floats2half2_rn(v[8 * g + 0] * sc, v[8 * g + 1] * sc);
+        __half2 h1 = __floats2half2_rn(v[8 * g + 2] * sc, v[8 * g + 3] * sc);
+        __half2 h2 = __floats2half2_rn(v[8 * g + 4] * sc, v[8 * g + 5] * sc);
+        __half2 h3 = __floats2half2_rn(v[8 * g + 6] * sc, v[8 * g + 7] * sc);
+        uint4 w;
+        w.x = *reinterpret_cast<uint32_t*>(&h0);
+        w.y = *reinterpret_cast<uint32_t*>(&h1);
+        w.z = *reinterpret_cast<uint32_t*>(&h2);
+        w.w = *reinterpret_cast<uint32_t*>(&h3);
+        *reinterpret_cast<uint4*>(a_tile + kb * 16384 + i * 128 + ((gi ^ (i & 7)) << 4)) = w;
+    }
+}
+
 struct Tile {
     uint64_t stream, row0, nvalid;  // rows [row0, row0+nvalid) of `stream`
 };
@@ -197,15 +230,16 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         const uint32_t bar_aready = ptx::smem_u32(&ctl->a_ready[t]);
         uint8_t* a_tile = a_tiles + t * kATileBytes;
         uint32_t f_ph = 0;
-        unsigned long long n_amb = 0, n_rs = 0;
+        unsigned long long n_amb = 0, n_rs = 0, n_rowstages = 0;
 
         for (uint64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
             const Tile tl = tile_of(2 * p + t, tiles_per_stream, rows, n_tiles);
             const bool valid = i < tl.nvalid;
             const uint64_t grow = tl.stream * rows + tl.row0 + i;  // global row index
             bool exact_row = false;
+            if (valid) n_rowstages += n_stages;
 
-            // ---- load x -> TMEM residual, stats
+            // ---- x -> TMEM residual (pass 1), stats
             float R2 = 0.f, mx = 0.f;
             {
                 const float4* x4 = reinterpret_cast<const float4*>(xs + grow * 128);
@@ -244,44 +278,24 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 mx = 0.f;
             }
             ptx::tc_wait_st();
+            int sigma = sigma_of(mx);
+            {   // ---- pass 2: A tile for stage 0
+                const float sc = ldexpf(1.0f, sigma);
+#pragma unroll 1
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    float v[32];
+                    ptx::tmem_ld32(t_res + 32u * c4, v);
+                    ptx::tc_wait_ld();
+                    store_a_chunk(a_tile, i, c4, v, sc);
+                }
+                ptx::fence_async_smem();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(bar_aready);
+            }
 
             for (uint32_t s = 0; s < n_stages; ++s) {
                 const StageInfo si = stages[s];
-                // ---- sigma and A tile = fp16(r * 2^sigma) in the SW128 K-major layout
-                int sigma = 0;
-                if (mx > 0.f) {
-                    int e;
-                    frexpf(mx, &e);  // mx in [2^(e-1), 2^e)
-                    sigma = min(60, max(-60, 14 - e));
-                }
-                {
-                    const float sc = ldexpf(1.0f, sigma);
-#pragma unroll 1
-                    for (int c4 = 0; c4 < 4; ++c4) {
-                        float v[32];
-                        ptx::tmem_ld32(t_res + 32u * c4, v);
-                        ptx::tc_wait_ld();
-#pragma unroll
-                        for (int g = 0; g < 4; ++g) {  // 16 B granules of 8 fp16 (k = 32*c4 + 8*g ..)
-                            const int kk = 32 * c4 + 8 * g;
-                            const int kb = kk >> 6, gi = (kk & 63) >> 3;
-                            uint4 w;
-                            __half2 h0 = __floats2half2_rn(v[8 * g + 0] * sc, v[8 * g + 1] * sc);
-                            __half2 h1 = __floats2half2_rn(v[8 * g + 2] * sc, v[8 * g + 3] * sc);
-                            __half2 h2 = __floats2half2_rn(v[8 * g + 4] * sc, v[8 * g + 5] * sc);
-                            __half2 h3 = __floats2half2_rn(v[8 * g + 6] * sc, v[8 * g + 7] * sc);
-                            w.x = *reinterpret_cast<uint32_t*>(&h0);
-                            w.y = *reinterpret_cast<uint32_t*>(&h1);
-                            w.z = *reinterpret_cast<uint32_t*>(&h2);
-                            w.w = *reinterpret_cast<uint32_t*>(&h3);
-                            *reinterpret_cast<uint4*>(a_tile + kb * 16384 + i * 128 + ((gi ^ (i & 7)) << 4)) = w;
-                        }
-                    }
-                    ptx::fence_async_smem();
-                    ptx::tc_fence_before();
-                    ptx::mbar_arrive(bar_aready);
-                }
-                // ---- error window
+                // ---- error window ("exactness of the tensor-core encoder")
                 const float R = sqrtf(R2 * 1.0001f);
                 const float E = si.max_norm;
                 const float Bnd = 2.1e-3f * R * E + 2.5e-7f * si.max_sqnorm + 6.8e-7f * (ldexpf(E, -sigma) + R) +
@@ -296,7 +310,8 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
 #pragma unroll
                 for (int k = 0; k < 32; ++k) mB[k] = INFINITY;
                 const uint32_t nch = si.pad_size / 128;
-                const float4* sq4 = reinterpret_cast<const float4*>(sqn_pad + si.eff16_off / 128);
+                const float* sqn_s = sqn_pad + si.eff16_off / 128;
+                const float4* sq4 = reinterpret_cast<const float4*>(sqn_s);
 #pragma unroll
                 for (int c = 0; c < kMaxChunks; ++c) {
                     if (c < int(nch)) {
@@ -333,7 +348,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         }
                     }
                 }
-                // ---- candidates
+                // ---- candidates {32a + b : mA[a] <= m + W, mB[b] <= m + W}
                 float m1 = INFINITY;
 #pragma unroll
                 for (int k = 0; k < 4 * kMaxChunks; ++k) m1 = fminf(m1, mA[k]);
@@ -347,50 +362,80 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 const bool unique = (na == 1 && nb == 1);
                 uint32_t z = unique ? (32u * (__ffs(CA) - 1) + (__ffs(CB) - 1)) : 0u;
                 const bool amb = !unique && valid && !exact_row;
+                if (unique) {
+                    const float* ez = eff + si.eff_off + uint64_t(z) * 128;
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) ptx::prefetch_l1(ez + 32 * l);
+                }
                 if (__any_sync(0xffffffffu, amb)) {
-                    // exact rescoring in the reference's fp32 order (codebook.cpp:166-172)
+                    // ---- warp-cooperative exact rescoring in the reference's fp32 order
+                    // (codebook.cpp:166-172).  The (row, candidate) items of all lanes
+                    // are packed 32 per pass; r of the owning row is broadcast by shuffle.
                     const uint32_t cnt = amb ? na * nb : 0u;
-                    const uint32_t maxcnt = __reduce_max_sync(0xffffffffu, cnt);
-                    float best = INFINITY;
-                    uint32_t bj = 0xffffffffu;
-                    for (uint32_t k = 0; k < maxcnt; ++k) {
+                    uint32_t incl = cnt;
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+                        if (lane >= uint32_t(off)) incl += y;
+                    }
+                    const uint32_t P = incl - cnt;
+                    const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
+                    const bool any_one = (search_block == 1) || (uint64_t(si.size) % search_block == 1);
+                    unsigned long long best = ~0ull;
+                    for (uint32_t base = 0; base < T; base += 32) {
+                        const uint32_t it = base + lane;
+                        uint32_t o = 0;
+#pragma unroll
+                        for (int step = 16; step > 0; step >>= 1) {
+                            const uint32_t Pc = __shfl_sync(0xffffffffu, P, o + step);
+                            if (Pc <= it) o += step;
+                        }
+                        const uint32_t li = it - __shfl_sync(0xffffffffu, P, o);
+                        const uint32_t CAo = __shfl_sync(0xffffffffu, CA, o);
+                        const uint32_t CBo = __shfl_sync(0xffffffffu, CB, o);
                         uint32_t j = 0xffffffffu;
-                        if (k < cnt) {
-                            const uint32_t a = __fns(CA, 0, int(k / nb) + 1), b = __fns(CB, 0, int(k % nb) + 1);
-                            j = 32u * a + b;
+                        if (it < T) {
+                            const uint32_t nbo = __popc(CBo);
+                            j = 32u * uint32_t(__fns(CAo, 0, int(li / nbo) + 1)) + uint32_t(__fns(CBo, 0, int(li % nbo) + 1));
                             if (j >= si.size) j = 0xffffffffu;
                         }
                         const bool has = (j != 0xffffffffu);
-                        const float* e = eff + si.eff_off + uint64_t(has ? j : 0) * 128;
-                        float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;   // GEMV lanes
-                        float r0[4] = {0.f, 0.f, 0.f, 0.f}, r1[4] = {0.f, 0.f, 0.f, 0.f};  // redux packets
+                        const float4* e4 = reinterpret_cast<const float4*>(eff + si.eff_off + uint64_t(has ? j : 0) * 128);
+                        float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+                        float r0[4] = {0.f, 0.f, 0.f, 0.f}, r1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
                         for (int c4 = 0; c4 < 4; ++c4) {
-                            float v[32];
+                            float v[32], ev[32];
+#pragma unroll
+                            for (int kk = 0; kk < 8; ++kk) {
+                                const float4 a = has ? __ldg(e4 + 8 * c4 + kk) : make_float4(0.f, 0.f, 0.f, 0.f);
+                                ev[4 * kk] = a.x;
+                                ev[4 * kk + 1] = a.y;
+                                ev[4 * kk + 2] = a.z;
+                                ev[4 * kk + 3] = a.w;
+                            }
                             ptx::tmem_ld32(t_res + 32u * c4, v);
                             ptx::tc_wait_ld();
-                            if (has) {
 #pragma unroll
-                                for (int kk = 0; kk < 8; ++kk) {
-                                    const float4 ev = __ldg(reinterpret_cast<const float4*>(e + 32 * c4) + kk);
-                                    const float p0 = __fmul_rn(ev.x, v[4 * kk]), p1 = __fmul_rn(ev.y, v[4 * kk + 1]);
-                                    const float p2 = __fmul_rn(ev.z, v[4 * kk + 2]), p3 = __fmul_rn(ev.w, v[4 * kk + 3]);
-                                    g0 = __fadd_rn(g0, p0);
-                                    g1 = __fadd_rn(g1, p1);
-                                    g2 = __fadd_rn(g2, p2);
-                                    g3 = __fadd_rn(g3, p3);
+                            for (int kk = 0; kk < 8; ++kk) {
+                                float pp[4];
+#pragma unroll
+                                for (int l = 0; l < 4; ++l)
+                                    pp[l] = __fmul_rn(ev[4 * kk + l], __shfl_sync(0xffffffffu, v[4 * kk + l], o));
+                                g0 = __fadd_rn(g0, pp[0]);
+                                g1 = __fadd_rn(g1, pp[1]);
+                                g2 = __fadd_rn(g2, pp[2]);
+                                g3 = __fadd_rn(g3, pp[3]);
+                                if (any_one) {
                                     float* rr = (kk & 1) ? r1 : r0;
-                                    rr[0] = __fadd_rn(rr[0], p0);
-                                    rr[1] = __fadd_rn(rr[1], p1);
-                                    rr[2] = __fadd_rn(rr[2], p2);
-                                    rr[3] = __fadd_rn(rr[3], p3);
+#pragma unroll
+                                    for (int l = 0; l < 4; ++l) rr[l] = __fadd_rn(rr[l], pp[l]);
                                 }
                             }
                         }
+                        unsigned long long key = ~0ull;
                         if (has) {
-                            const uint64_t blk0 = (uint64_t(j) / search_block) * search_block;
-                            const uint64_t rem = uint64_t(si.size) - blk0;
-                            const bool one = ((rem < search_block ? rem : search_block) == 1);
+                            const bool one = any_one && (search_block == 1 || j + 1 == si.size);
                             float dot;
                             if (one) {
 #pragma unroll
@@ -399,47 +444,71 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                             } else {
                                 dot = __fadd_rn(__fadd_rn(g0, g2), __fadd_rn(g1, g3));
                             }
-                            const float sc = __fsub_rn(__ldg(sqn_pad + si.eff16_off / 128 + j), __fmul_rn(2.0f, dot));
-                            if (sc < best || (sc == best && j < bj)) {
-                                best = sc;
-                                bj = j;
-                            }
+                            const float sc = __fadd_rn(__fsub_rn(__ldg(sqn_s + j), __fmul_rn(2.0f, dot)), 0.0f);
+                            if (sc < INFINITY) key = (uint64_t(f2ord(sc)) << 32) | j;  // NaN / +inf never win
                         }
+                        // segmented min over consecutive lanes of the same owner
+#pragma unroll
+                        for (int off = 1; off < 32; off <<= 1) {
+                            const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, off);
+                            const uint32_t oo = __shfl_down_sync(0xffffffffu, o, off);
+                            if (lane + off < 32 && oo == o && ok < key) key = ok;
+                        }
+                        const int head = int(P) - int(base);
+                        const unsigned long long got = __shfl_sync(0xffffffffu, key, head < 0 ? 0 : (head > 31 ? 31 : head));
+                        if (amb && P + cnt > base && P < base + 32 && got < best) best = got;
                     }
                     if (amb) {
-                        z = (bj == 0xffffffffu) ? 0u : bj;
+                        z = (best == ~0ull) ? 0u : uint32_t(best & 0xffffffffu);
                         n_rs += cnt;
                         ++n_amb;
                     }
                 }
                 if (valid && !exact_row) codes[grow * n_stages + s] = uint16_t(z);
 
-                // ---- residual update r -= e_z (exact fp32), stats for the next stage
+                // ---- residual update r -= e_z (exact fp32) fused with the next stage's A tile
                 const bool last = (s + 1 == n_stages);
-                const float* e = eff + si.eff_off + uint64_t(z) * 128;
-                R2 = 0.f;
-                mx = 0.f;
+                const int sigma_n = sigma_of(mx + si.max_abs);  // max|r - e| <= max|r| + max|e|
+                const float sc_n = ldexpf(1.0f, sigma_n);
+                const float4* ez4 = reinterpret_cast<const float4*>(eff + si.eff_off + uint64_t(z) * 128);
+                float R2n = 0.f, mxn = 0.f;
                 float n0[4] = {0.f, 0.f, 0.f, 0.f}, n1[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
+                float en[32];
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const float4 a = __ldg(ez4 + kk);
+                    en[4 * kk] = a.x;
+                    en[4 * kk + 1] = a.y;
+                    en[4 * kk + 2] = a.z;
+                    en[4 * kk + 3] = a.w;
+                }
+#pragma unroll
                 for (int c4 = 0; c4 < 4; ++c4) {
-                    float v[32];
+                    float ec[32], v[32];
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) ec[k] = en[k];
+                    if (c4 < 3) {
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const float4 a = __ldg(ez4 + 8 * (c4 + 1) + kk);
+                            en[4 * kk] = a.x;
+                            en[4 * kk + 1] = a.y;
+                            en[4 * kk + 2] = a.z;
+                            en[4 * kk + 3] = a.w;
+                        }
+                    }
                     ptx::tmem_ld32(t_res + 32u * c4, v);
                     ptx::tc_wait_ld();
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        const float4 ev = __ldg(reinterpret_cast<const float4*>(e + 32 * c4) + kk);
-                        v[4 * kk + 0] = __fsub_rn(v[4 * kk + 0], ev.x);
-                        v[4 * kk + 1] = __fsub_rn(v[4 * kk + 1], ev.y);
-                        v[4 * kk + 2] = __fsub_rn(v[4 * kk + 2], ev.z);
-                        v[4 * kk + 3] = __fsub_rn(v[4 * kk + 3], ev.w);
-                    }
+                    for (int k = 0; k < 32; ++k) v[k] = __fsub_rn(v[k], ec[k]);
                     ptx::tmem_st32(t_res + 32u * c4, v);
                     if (!last) {
 #pragma unroll
                         for (int k = 0; k < 32; ++k) {
-                            R2 = fmaf(v[k], v[k], R2);
-                            mx = fmaxf(mx, fabsf(v[k]));
+                            R2n = fmaf(v[k], v[k], R2n);
+                            mxn = fmaxf(mxn, fabsf(v[k]));
                         }
+                        store_a_chunk(a_tile, i, c4, v, sc_n);
                     } else {
                         // final ||r|| in the reference's redux order (Eigen squaredNorm)
 #pragma unroll
@@ -457,21 +526,22 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     }
                 }
                 ptx::tc_wait_st();
-                if (last && valid && !exact_row) {
+                if (!last) {
+                    ptx::fence_async_smem();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(bar_aready);
+                } else if (valid && !exact_row) {
 #pragma unroll
                     for (int l = 0; l < 4; ++l) n0[l] = __fadd_rn(n0[l], n1[l]);
                     norms[grow] = __fsqrt_rn(__fadd_rn(__fadd_rn(n0[0], n0[2]), __fadd_rn(n0[1], n0[3])));
                 }
+                R2 = R2n;
+                mx = mxn;
+                sigma = sigma_n;
             }
         }
         if (counters) {
-            // per-row-stage diagnostics
-            unsigned long long rs = 0;
-            for (uint64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
-                const Tile tl = tile_of(2 * p + t, tiles_per_stream, rows, n_tiles);
-                rs += (i < tl.nvalid) ? n_stages : 0;
-            }
-            atomicAdd(&counters[0], rs);
+            atomicAdd(&counters[0], n_rowstages);
             if (n_amb) atomicAdd(&counters[1], n_amb);
             if (n_rs) atomicAdd(&counters[3], n_rs);
         }

@@ -95,8 +95,9 @@ void stack_build_device(vqkv_stack_s& st, const float* entries_host, const float
     }
     VQKV_CUDA(cudaDeviceSynchronize());
     // per-stage max norms (host side, from the device's own fp32 sqnorms)
-    std::vector<float> sqn(T);
+    std::vector<float> sqn(T), effh(T * D);
     VQKV_CUDA(cudaMemcpy(sqn.data(), st.d_sqn, sizeof(float) * T, cudaMemcpyDeviceToHost));
+    VQKV_CUDA(cudaMemcpy(effh.data(), st.d_eff, sizeof(float) * T * D, cudaMemcpyDeviceToHost));
     for (uint32_t s = 0; s < st.n; ++s) {
         float m = 0.f;
         const uint64_t off = st.stages[s].eff_off / D;
@@ -105,6 +106,9 @@ void stack_build_device(vqkv_stack_s& st, const float* entries_host, const float
             if (!(v <= m)) m = v;  // NaN propagates (non-finite codebooks are rejected earlier)
         }
         st.stages[s].max_sqnorm = m;
+        float ma = 0.f;
+        for (uint64_t k = off * D; k < (off + st.stages[s].size) * D; ++k) ma = std::max(ma, std::fabs(effh[k]));
+        st.stages[s].max_abs = ma;
         // rounded up so that ||e_j|| <= max_norm holds for every entry
         st.stages[s].max_norm = std::nextafter(std::sqrt(m), INFINITY);
     }

@@ -48,6 +48,8 @@ struct StageInfo {
     uint64_t eff16_off;// element offset into the fp16 operand copy ([pad_size][D])
     float max_norm;    // max_j ||e_j|| (fp32, rounded up)
     float max_sqnorm;  // max_j ||e_j||^2
+    float max_abs;     // max_{j,k} |e_jk|
+    float pad_;
 };
 
 }  // namespace vqkv_dev
