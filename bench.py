@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""bench.py -- VQKV hot-path benchmark on B200 (driver contract).
+
+Headline workload (BASELINE.json configs[1]): 32K-token prefill encode at the
+LLaMA3.1-8B KV shape -- 32 layers x 8 KV heads = 256 (layer, head) streams,
+D = 128, WindowPolicy{init 4, local 1024} so each stream quantizes its
+31,740 middle rows (kv_cache.cpp:76-88) through the key stack (56 x 1024) and
+the value stack (16 x 512).  One step = quantize_batch of all 16,250,880 K+V
+vectors.  Metric: KV vectors/s VQ-encoded (whole job, all ranks).
+
+Inputs: synthetic, generated with the reference's own generator restated in
+the library (synthetic.cpp: rope-rotated mixture keys seed 1000+sid, mixture
+values seed 1001+sid); codebooks are the reference's random_stack fixtures
+(test_util.hpp, seeds 1 and 2).  Inputs (8.3 GB) exceed L2 (126 MB), so no
+flush is needed between steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU (torchrun, one rank per GPU): every rank encodes its own full
+256-stream prefill (weak scaling, no data-path collective); time = max over
+ranks of the device-timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LAYERS, KV_HEADS, D = 32, 8, 128
+PREFILL, INIT_LEN, LOCAL_LEN = 32768, 4, 1024
+K_SHAPE, V_SHAPE = (56, 1024), (16, 512)
+METRIC = "KV vectors/sec VQ-encoded and decode-attn tokens/sec at LLaMA3.1-8B shape"
+UNIT = "KV vectors/s"
+
+
+def flop_per_vector(n, s):
+    return 2 * D * n * s
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--streams", type=int, default=LAYERS * KV_HEADS)
+    ap.add_argument("--prefill", type=int, default=PREFILL)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time per baseline sample")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- dist
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def init_dist(world, local):
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return torch
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------------------------- inputs
+def gen_inputs(torch, n_streams, prefill, rank, pinned=True):
+    """Synthetic K/V middle rows [n_streams, middle, D] (host, pinned)."""
+    from paper_2603_16435_b200 import _lib
+
+    L = _lib.load()
+    middle = prefill - INIT_LEN - LOCAL_LEN
+    K = torch.empty((n_streams, middle, D), dtype=torch.float32, pin_memory=pinned)
+    V = torch.empty((n_streams, middle, D), dtype=torch.float32, pin_memory=pinned)
+
+    def one(args):
+        sid, kind = args
+        buf = np.empty((prefill, D), np.float32)
+        seed = 1000 + sid + 1_000_000 * rank + (1 if kind == 0 else 0)
+        st = L.vqkv_generate_synthetic(1 if kind == 1 else 0, D, prefill, 32, seed, 10000.0, 0.25, 1.0,
+                                       buf.ctypes.data)
+        assert st == 0
+        dst = K if kind == 1 else V
+        dst[sid].copy_(torch.from_numpy(buf[INIT_LEN : INIT_LEN + middle]))
+
+    work = [(s, k) for s in range(n_streams) for k in (1, 0)]
+    with cf.ThreadPoolExecutor(max_workers=min(64, os.cpu_count() or 8)) as ex:
+        list(ex.map(one, work))
+    return K, V
+
+
+def make_stacks(device):
+    from paper_2603_16435_b200 import _lib, codebook
+
+    L = _lib.load()
+    out = []
+    for seed, (n, s), kind in ((1, K_SHAPE, 0), (2, V_SHAPE, 1)):
+        ent = np.empty((n, s, D), np.float32)
+        prj = np.empty((n, D, D), np.float32)
+        assert L.vqkv_random_stack(seed, n, s, D, ent.ctypes.data, prj.ctypes.data) == 0
+        out.append(codebook.CodebookStack.from_arrays(list(ent), list(prj), kind, device))
+    return out
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- CPU baseline
+def cpu_encode_rate(seconds_target=12.0, threads=None):
+    """Oracle (the reference's per-row algorithm restated) on host cores.
+
+    Returns (vectors/s for a 1:1 K:V mix, threads, sample description)."""
+    from oracle import oracle as O
+
+    threads = threads or (os.cpu_count() or 1)
+    res = {}
+    stacks = {"K": O.Rng(1).stack(*K_SHAPE, D, O.KEY), "V": O.Rng(2).stack(*V_SHAPE, D, O.VALUE)}
+    desc = []
+    for name, kind in (("K", 1), ("V", 0)):
+        st = stacks[name]
+        # calibrate on a tiny sample, then size the real one
+        x = O.generate(kind, D, 4 * threads + INIT_LEN, 32, 1000 + (0 if kind else 1))[INIT_LEN:]
+        t0 = time.perf_counter()
+        st.quantize_batch_mt(x, threads, 4, threads)
+        per_row = (time.perf_counter() - t0) / 4
+        rows = max(4, min(4096, int(seconds_target / 2 / max(per_row, 1e-6))))
+        x = np.concatenate([O.generate(kind, D, rows + INIT_LEN, 32, 1000 + s + (0 if kind else 1))[INIT_LEN:]
+                            for s in range(threads)])
+        t0 = time.perf_counter()
+        st.quantize_batch_mt(x, threads, rows, threads)
+        dt = time.perf_counter() - t0
+        res[name] = (threads * rows, dt)
+        desc.append(f"{name}: {threads} streams x {rows} rows in {dt:.1f}s")
+    (nk, tk), (nv, tv) = res["K"], res["V"]
+    rate = 2.0 / (tk / nk + tv / nv)
+    return rate, threads, "; ".join(desc) + " (oracle port, one thread per (layer, head) stream, 1:1 K:V mix)"
+
+
+# --------------------------------------------------------------------------- arms
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    rates = []
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up effects; calibration happens inside each step
+    cores = 1
+    sample = ""
+    for _ in range(args.steps):
+        r, cores, sample = cpu_encode_rate(seconds_target=max(2.0, args.cpu_seconds / 2))
+        rates.append(r)
+    v = float(np.mean(rates))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generator, seeds 1000+sid)",
+        "config": {"workload": "32K-token prefill encode, LLaMA3.1-8B KV shape (bounded CPU sample)",
+                   "streams": args.streams, "rows_per_stream": args.prefill - INIT_LEN - LOCAL_LEN,
+                   "key_stack": list(K_SHAPE), "value_stack": list(V_SHAPE), "head_dim": D},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    torch = init_dist(world, local)
+    from paper_2603_16435_b200 import _lib
+    from paper_2603_16435_b200 import device as Dv
+
+    L = _lib.load()
+    kst, vst = make_stacks(local)
+    middle = args.prefill - INIT_LEN - LOCAL_LEN
+    ns = args.streams
+    t_gen = time.perf_counter()
+    Kh, Vh = gen_inputs(torch, ns, args.prefill, rank)
+    t_gen = time.perf_counter() - t_gen
+    Kd, Vd = Kh.to("cuda", non_blocking=True), Vh.to("cuda", non_blocking=True)
+    kp = torch.empty((ns, kst.device.payload_bytes(middle)), dtype=torch.uint8, device="cuda")
+    vp = torch.empty((ns, vst.device.payload_bytes(middle)), dtype=torch.uint8, device="cuda")
+    kn = torch.empty((ns, middle), dtype=torch.float32, device="cuda")
+    vn = torch.empty((ns, middle), dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+
+    def step():
+        Dv.quantize_streams(kst, Kd, payload=kp, norms=kn)
+        Dv.quantize_streams(vst, Vd, payload=vp, norms=vn)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    L.vqkv_profile_enable(1)
+    L.vqkv_profile_collect(b"encode_tc", None, None)
+    launches0 = _lib.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = _lib.launch_count() - launches0
+    ms_total = ev0.elapsed_time(ev1)
+    ms_total = max_over_ranks(ms_total, world)
+    ms_step = ms_total / args.steps
+    enc_ms = ctypes.c_double()
+    enc_n = ctypes.c_uint64()
+    L.vqkv_profile_collect(b"encode_tc", ctypes.byref(enc_ms), ctypes.byref(enc_n))
+    L.vqkv_profile_enable(0)
+    vectors_per_rank = 2 * ns * middle
+    value = world * vectors_per_rank / (ms_step / 1e3)
+    flops_step = ns * middle * (flop_per_vector(*K_SHAPE) + flop_per_vector(*V_SHAPE))
+    enc_ms_per_step = enc_ms.value / args.steps
+    achieved_tflops = flops_step / (enc_ms_per_step / 1e3) / 1e12
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("bf16_tflops_sustained", 1398.8)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("encode_tc_kernel")
+
+    # ---- e2e through the public host-buffer API (H2D + encode + D2H each step)
+    e2e = None
+    if not args.no_e2e:
+        kph = torch.empty((ns, kst.device.payload_bytes(middle)), dtype=torch.uint8, pin_memory=True)
+        vph = torch.empty((ns, vst.device.payload_bytes(middle)), dtype=torch.uint8, pin_memory=True)
+        knh = torch.empty((ns, middle), dtype=torch.float32, pin_memory=True)
+        vnh = torch.empty((ns, middle), dtype=torch.float32, pin_memory=True)
+
+        def e2e_step():
+            Dv.quantize_streams_host(kst, Kh, payload_host=kph, norms_host=knh)
+            Dv.quantize_streams_host(vst, Vh, payload_host=vph, norms_host=vnh)
+
+        e2e_step()
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        n_e2e = max(1, min(args.steps, 3))
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(e0.elapsed_time(e1) / n_e2e, world)
+        e2e = {
+            "value": world * vectors_per_rank / (e_ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": int(Kh.numel() * 4 + Vh.numel() * 4),
+            "d2h_bytes_per_step": int(kph.numel() + vph.numel() + knh.numel() * 4 + vnh.numel() * 4),
+            "ms_per_step": e_ms, "api": "vqkv_quantize_batch_host (pinned host buffers)",
+        }
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r, cores, sample = cpu_encode_rate(args.cpu_seconds)
+            cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        counters = Dv.encode_counters(kst)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f16 MMA / f32 exact (indices bit-exact)",
+            "data": "synthetic (reference generator: rope-rotated mixture keys, mixture values; random_stack codebooks)",
+            "config": {
+                "workload": "32K-token prefill encode (configs[1]), LLaMA3.1-8B KV shape",
+                "streams_per_gpu": ns, "layers": LAYERS, "kv_heads": KV_HEADS, "head_dim": D,
+                "rows_per_stream": middle, "key_stack": list(K_SHAPE), "value_stack": list(V_SHAPE),
+                "kv_vectors_per_gpu": vectors_per_rank, "l2": "inputs (8.3 GB) larger than L2, no flush",
+                "parallelism": f"dp{world} (independent prefills per GPU)",
+            },
+            "roofline": {
+                "bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved_tflops / peak, "traffic": traffic,
+                "kernel": "encode_tc_kernel", "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                "algorithmic": "2*D*N*S flop per vector (K 14,680,064; V 2,097,152)",
+                "kernel_ms_per_step": enc_ms_per_step, "kernel_launches": int(enc_n.value),
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+            "ambiguous_row_stage_frac_K": counters["ambiguous"] / max(1, counters["row_stages"]),
+            "input_gen_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -172,6 +172,30 @@ int vqkv_set_encode_path(int path);
 int vqkv_encode_counters(vqkv_stack_t stack, uint64_t* counters3);
 /* number of kernel launches issued by the library since load (all threads) */
 uint64_t vqkv_launch_count(void);
+/* Kernel timing hooks: when enabled, the library records a CUDA event pair on
+ * the launching stream around each hot kernel (names: "encode_tc",
+ * "encode_exact", "pack", "reconstruct", "attend", "attend_combine").
+ * vqkv_profile_collect synchronizes on the recorded events, returns the summed
+ * milliseconds and launch count for `name`, and forgets them. */
+int vqkv_profile_enable(int on);
+int vqkv_profile_collect(const char* name, double* total_ms, uint64_t* launches);
+
+/* ---------------------------------------------------------------------------
+ * Reference fixtures (host): bit-identical restatements of the reference's
+ * synthetic input generator and random codebook stacks, so inputs match the
+ * reference's on the same seeds.
+ * ------------------------------------------------------------------------- */
+/* synthetic.cpp:40-63 generate(): kind 0 gaussian_mixture, 1 rope_rotated_keys;
+ * out: host fp32 [count][dim] */
+int vqkv_generate_synthetic(int kind, uint32_t dim, uint64_t count, uint32_t component_count,
+                            uint64_t seed, double rope_base, float component_std, float mean_scale,
+                            float* out_host);
+/* test_util.hpp:30-50 random_stack(mt19937_64(seed), n, size, dim):
+ * entries [n][size][dim], projections [n][dim][dim] (host fp32) */
+int vqkv_random_stack(uint64_t seed, uint32_t n_stages, uint32_t size, uint32_t dim, float* entries_host,
+                      float* projections_host);
+/* FNV-1a-64 (codebook.cpp:326-336 stack_content_hash over the RSVQ bytes) */
+uint64_t vqkv_fnv1a64(const uint8_t* data, uint64_t n);
 
 #ifdef __cplusplus
 }

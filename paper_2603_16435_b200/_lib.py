@@ -65,6 +65,14 @@ _SIGS = {
     "vqkv_attend_decode": (C.c_int, [P, P, C.POINTER(AttendArgs), P]),
     "vqkv_lse_combine": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint32, P, P, P]),
     "vqkv_encode_counters": (C.c_int, [P, u64p]),
+    "vqkv_profile_enable": (C.c_int, [C.c_int]),
+    "vqkv_profile_collect": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), u64p]),
+    "vqkv_generate_synthetic": (
+        C.c_int,
+        [C.c_int, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64, C.c_double, C.c_float, C.c_float, P],
+    ),
+    "vqkv_random_stack": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, P, P]),
+    "vqkv_fnv1a64": (C.c_uint64, [P, C.c_uint64]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -229,10 +229,16 @@ void launch_attend(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_at
     if (smem > 48 * 1024)
         VQKV_CUDA(cudaFuncSetAttribute(attend_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     dim3 grid(a.n_pairs, unsigned(nsplit));
+    {
+    ProfScope ps("attend", s);
     attend_generic_kernel<<<grid, kAttWarps * 32, smem, s>>>(ksv, vsv, sa, Dk, Dv, per_split, pacc, pm, pl);
     launch_check("attend_generic_kernel");
+    }
+    {
+    ProfScope ps2("attend_combine", s);
     split_combine_kernel<<<a.n_pairs * G, 128, 0, s>>>(pacc, pm, pl, unsigned(nsplit), G, Dv, a.out_dev, a.lse_dev);
     launch_check("split_combine_kernel");
+    }
     VQKV_CUDA(cudaFreeAsync(pacc, s));
     VQKV_CUDA(cudaFreeAsync(pm, s));
     VQKV_CUDA(cudaFreeAsync(pl, s));

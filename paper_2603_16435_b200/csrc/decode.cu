@@ -118,6 +118,7 @@ void launch_reconstruct(const vqkv_stack_s& st, const uint8_t* payload, uint32_t
     const uint64_t total = uint64_t(n_streams) * nrows;
     if (total == 0) return;
     const uint64_t sb = payload_bytes(st.row_bits, rows);
+    ProfScope ps("reconstruct", s);
     if (st.dim <= 128) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st.device);

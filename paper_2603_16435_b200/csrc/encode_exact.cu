@@ -159,6 +159,7 @@ void launch_encode_exact(const vqkv_stack_s& st, const float* xs, uint64_t total
     size_t smem = sizeof(float) * st.dim * kExactWarps;
     if (smem > 48 * 1024)
         VQKV_CUDA(cudaFuncSetAttribute(encode_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ProfScope ps("encode_exact", s);
     encode_exact_kernel<<<unsigned(blocks), kExactWarps * 32, smem, s>>>(
         st.d_stages, st.n, st.dim, st.d_eff, st.d_sqn, xs, total_rows, search_block, codes, norms, residuals, nullptr, nullptr);
     launch_check("encode_exact_kernel");
@@ -181,6 +182,7 @@ void launch_pack_codes(const uint16_t* codes, uint32_t n_streams, uint64_t rows,
     const uint64_t sb = payload_bytes(st.row_bits, rows);
     const uint64_t n = sb * n_streams;
     if (n == 0) return;
+    ProfScope ps("pack", s);
     pack_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(codes, st.d_stages, n_stages, st.row_bits, n_streams, rows,
                                                           sb, payload);
     launch_check("pack_kernel");

@@ -269,13 +269,21 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 const uint32_t slot = atomicAdd(exact_count, 1u);
                 exact_list[slot] = uint32_t(grow);
                 if (counters) atomicAdd(&counters[2], 1ull);
-                float z[32];
-#pragma unroll
-                for (int k = 0; k < 32; ++k) z[k] = 0.f;
-#pragma unroll 1
-                for (int c4 = 0; c4 < 4; ++c4) ptx::tmem_st32(t_res + 32u * c4, z);
                 R2 = 0.f;
                 mx = 0.f;
+            }
+            if (__any_sync(0xffffffffu, exact_row)) {
+                // tcgen05.ld/st are warp-collective: the whole warp rewrites its rows
+                ptx::tc_wait_st();
+#pragma unroll 1
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    float v[32];
+                    ptx::tmem_ld32(t_res + 32u * c4, v);
+                    ptx::tc_wait_ld();
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) v[k] = exact_row ? 0.f : v[k];
+                    ptx::tmem_st32(t_res + 32u * c4, v);
+                }
             }
             ptx::tc_wait_st();
             int sigma = sigma_of(mx);
@@ -581,10 +589,13 @@ void launch_encode_tc(const vqkv_stack_s& st, const float* xs, uint32_t n_stream
     const uint64_t tiles = ((rows + 127) / 128) * n_streams;
     const uint64_t pairs = (tiles + 1) / 2;
     const unsigned grid = unsigned(std::min<uint64_t>(pairs, uint64_t(sms)));
+    {
+    ProfScope ps("encode_tc", s);
     encode_tc_kernel<<<grid, kThreads, kSmemBytes, s>>>(st.d_stages, st.n, st.d_eff16, st.d_sqn_pad, st.d_eff, xs,
                                                          n_streams, rows, search_block, codes, norms, residuals,
                                                          list + 1, list, st.d_counters);
     launch_check("encode_tc_kernel");
+    }
     // rows with non-finite input: exact reference semantics
     launch_encode_exact_rows(st, xs, list + 1, list, total, search_block, codes, norms, residuals, s);
     launch_pack_codes(codes, n_streams, rows, st.n, st, payload, s);

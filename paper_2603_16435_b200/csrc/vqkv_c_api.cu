@@ -12,6 +12,22 @@
 
 namespace vqkv_dev {
 std::atomic<uint64_t> g_launches{0};
+
+namespace {
+std::atomic<bool> g_prof{false};
+std::mutex g_prof_mu;
+struct ProfRec {
+    std::string name;
+    cudaEvent_t a, b;
+};
+std::vector<ProfRec> g_prof_recs;
+}  // namespace
+
+bool prof_enabled() { return g_prof.load(std::memory_order_relaxed); }
+void prof_record(const char* name, cudaEvent_t a, cudaEvent_t b) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_recs.push_back({name, a, b});
+}
 }  // namespace vqkv_dev
 
 using namespace vqkv_dev;
@@ -67,6 +83,37 @@ extern "C" {
 const char* vqkv_last_error(void) { return t_err.c_str(); }
 const char* vqkv_version(void) { return "vqkv_b200 0.1 (sm_100a)"; }
 uint64_t vqkv_launch_count(void) { return g_launches.load(); }
+
+int vqkv_profile_enable(int on) {
+    g_prof.store(on != 0);
+    return VQKV_OK;
+}
+
+int vqkv_profile_collect(const char* name, double* total_ms, uint64_t* launches) {
+    return guard([&] {
+        need(name != nullptr, VQKV_INVALID_INPUT, "null name");
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        double ms = 0.0;
+        uint64_t n = 0;
+        std::vector<ProfRec> keep;
+        for (auto& r : g_prof_recs) {
+            if (r.name == name) {
+                VQKV_CUDA(cudaEventSynchronize(r.b));
+                float t = 0.f;
+                VQKV_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+                ms += t;
+                ++n;
+                cudaEventDestroy(r.a);
+                cudaEventDestroy(r.b);
+            } else {
+                keep.push_back(r);
+            }
+        }
+        g_prof_recs.swap(keep);
+        if (total_ms) *total_ms = ms;
+        if (launches) *launches = n;
+    });
+}
 
 int vqkv_set_encode_path(int path) {
     return guard([&] {

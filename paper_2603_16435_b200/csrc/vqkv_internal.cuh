@@ -29,6 +29,28 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 #define VQKV_CUDA(x) ::vqkv_dev::cuda_check((x), #x)
 
+// Optional event-pair timing of hot kernels (vqkv_profile_enable).
+bool prof_enabled();
+void prof_record(const char* name, cudaEvent_t start, cudaEvent_t stop);
+struct ProfScope {
+    const char* name;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(const char* n, cudaStream_t st) : name(n), s(st) {
+        if (prof_enabled()) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, s);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEventRecord(b, s);
+            prof_record(name, a, b);
+        }
+    }
+};
+
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 inline void launch_check(const char* k) {
