@@ -46,8 +46,9 @@ namespace {
 
 constexpr int kThreads = 384;
 constexpr int kNB = 3;                    // codebook chunk ring depth
-constexpr uint32_t kChunkBytes = 32768;   // 128 entries x 128 fp16
-constexpr uint32_t kATileBytes = 32768;   // 128 rows x 128 fp16
+constexpr uint32_t kChunkBytes = 36864;   // 128 entries x (128 + 16) fp16
+constexpr uint32_t kATileBytes = 36864;   // 128 rows x (128 + 16) fp16
+constexpr uint32_t kExtOff = 32768;       // the 16-wide K block (||e||^2 / row scale)
 constexpr int kMaxChunks = 8;             // stages up to 1024 entries
 constexpr uint32_t kIdesc = ptx::idesc_f16_f32(128, 128);
 
@@ -61,23 +62,38 @@ struct __align__(8) SmemCtl {
 };
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + 2 * kATileBytes + kNB * kChunkBytes + sizeof(SmemCtl);
 
-// tree minimum of 32 values with 3-input FMNMX
-__device__ __forceinline__ float min32(const float (&v)[32]) {
+// tree maximum of 32 values with 3-input FMNMX
+__device__ __forceinline__ float max32(const float (&v)[32]) {
     float a[11];
 #pragma unroll
-    for (int i = 0; i < 10; ++i) a[i] = ptx::fmin3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
-    a[10] = fminf(v[30], v[31]);
-    float b0 = ptx::fmin3(a[0], a[1], a[2]), b1 = ptx::fmin3(a[3], a[4], a[5]);
-    float b2 = ptx::fmin3(a[6], a[7], a[8]), b3 = fminf(a[9], a[10]);
-    return fminf(ptx::fmin3(b0, b1, b2), b3);
+    for (int i = 0; i < 10; ++i) a[i] = ptx::fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+    a[10] = fmaxf(v[30], v[31]);
+    float b0 = ptx::fmax3(a[0], a[1], a[2]), b1 = ptx::fmax3(a[3], a[4], a[5]);
+    float b2 = ptx::fmax3(a[6], a[7], a[8]), b3 = fmaxf(a[9], a[10]);
+    return fmaxf(ptx::fmax3(b0, b1, b2), b3);
 }
 
+// Power-of-two row scale so that m * 2^sigma < 2^14 (ideally in [2^13, 2^14)),
+// clamped to [-23, 16] so that the ext-column factor -2^(sigma-1) is an exact
+// fp16 value.  Rows whose magnitude needs sigma < -23 go to the exact path.
 __device__ __forceinline__ int sigma_of(float m) {
-    // power-of-two row scale so that m * 2^sigma lies in [2^13, 2^14)
     if (!(m > 0.f) || !isfinite(m)) return 0;
     int e;
     frexpf(m, &e);  // m in [2^(e-1), 2^e)
-    return min(60, max(-60, 14 - e));
+    return min(16, max(-23, 14 - e));
+}
+
+// ext K block of the A tile (no swizzle, 8x16 B core matrices): row i's
+// columns 0..7 = {-2^(sigma-1), -2^(sigma-1), 0, ...}; columns 8..15 stay 0.
+__device__ __forceinline__ void store_a_ext(uint8_t* a_tile, uint32_t i, int sigma) {
+    const __half h = __float2half_rn(-ldexpf(1.0f, sigma - 1));
+    __half2 hh = __halves2half2(h, h);
+    uint4 w;
+    w.x = *reinterpret_cast<uint32_t*>(&hh);
+    w.y = w.z = w.w = 0u;
+    uint8_t* p = a_tile + kExtOff + (i >> 3) * 256 + (i & 7) * 16;
+    *reinterpret_cast<uint4*>(p) = w;
+    *reinterpret_cast<uint4*>(p + 128) = make_uint4(0u, 0u, 0u, 0u);
 }
 
 // order-preserving map float -> uint32 (for packed (score, index) keys)
@@ -169,8 +185,8 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         ptx::mbar_wait(ptx::smem_u32(&ctl->b_empty[buf]), ph ^ 1);
                         const uint32_t bar = ptx::smem_u32(&ctl->b_full[buf]);
                         ptx::mbar_arrive_expect_tx(bar, kChunkBytes);
-                        ptx::bulk_g2s(ptx::smem_u32(b_ring + buf * kChunkBytes), src + uint64_t(c) * 16384, kChunkBytes,
-                                      bar);
+                        ptx::bulk_g2s(ptx::smem_u32(b_ring + buf * kChunkBytes), src + uint64_t(c) * (kChunkBytes / 2),
+                                      kChunkBytes, bar);
                         if (++buf == kNB) {
                             buf = 0;
                             ph ^= 1;
@@ -206,6 +222,10 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                                 const uint64_t bd = ptx::umma_desc_sw128(b_base + buf * kChunkBytes + koff);
                                 ptx::mma_f16_ss(d, ad, bd, kIdesc, k > 0 ? 1u : 0u);
                             }
+                            // + (-2^(sigma-1)) * (||e||^2 hi + lo): the score's norm term
+                            ptx::mma_f16_ss(d, ptx::umma_desc_noswz(a_base + t * kATileBytes + kExtOff, 128, 256),
+                                            ptx::umma_desc_noswz(b_base + buf * kChunkBytes + kExtOff, 128, 256),
+                                            kIdesc, 1u);
                             ptx::mma_commit(ptx::smem_u32(&ctl->acc_full[t]));
                         }
                         ptx::mma_commit(ptx::smem_u32(&ctl->b_empty[buf]));
@@ -263,6 +283,8 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         mx = fmaxf(mx, fabsf(v[k]));
                     }
                 }
+                // magnitudes beyond the fp16 row-scale range also take the exact path
+                exact_row |= !(mx < 68719476736.0f);  // 2^36
             }
             if (exact_row) {
                 // hand the row to the exact path; run the tensor-core pass on zeros
@@ -296,6 +318,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     ptx::tc_wait_ld();
                     store_a_chunk(a_tile, i, c4, v, sc);
                 }
+                store_a_ext(a_tile, i, sigma);
                 ptx::fence_async_smem();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(bar_aready);
@@ -306,20 +329,20 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 // ---- error window ("exactness of the tensor-core encoder")
                 const float R = sqrtf(R2 * 1.0001f);
                 const float E = si.max_norm;
-                const float Bnd = 2.1e-3f * R * E + 2.5e-7f * si.max_sqnorm + 6.8e-7f * (ldexpf(E, -sigma) + R) +
-                                  ldexpf(2.3e-13f, -sigma) + 1e-30f;
-                const float W = 2.02f * Bnd;
-                const float mrow = -ldexpf(1.0f, 1 - sigma);
+                const float Bnd = 2.1e-3f * R * E + 1.6e-5f * si.max_sqnorm + 6.8e-7f * (ldexpf(E, -sigma) + R) +
+                                  ldexpf(2.3e-13f, -sigma) + 6e-8f + 1e-30f;
+                // The MMA yields Y_j = 2^sigma r.e_j - 2^(sigma-1)||e_j||^2 = -2^(sigma-1) score_j,
+                // so argmin score == argmax Y and the window scales by 2^(sigma-1).
+                const float W = ldexpf(2.02f * Bnd, sigma - 1);
 
-                // ---- scores: min over A groups (32 contiguous) and B groups (j mod 32)
+                // ---- max over A groups (32 contiguous entries) and B groups (j mod 32)
                 float mA[4 * kMaxChunks], mB[32];
 #pragma unroll
-                for (int k = 0; k < 4 * kMaxChunks; ++k) mA[k] = INFINITY;
+                for (int k = 0; k < 4 * kMaxChunks; ++k) mA[k] = -INFINITY;
 #pragma unroll
-                for (int k = 0; k < 32; ++k) mB[k] = INFINITY;
+                for (int k = 0; k < 32; ++k) mB[k] = -INFINITY;
                 const uint32_t nch = si.pad_size / 128;
-                const float* sqn_s = sqn_pad + si.eff16_off / 128;
-                const float4* sq4 = reinterpret_cast<const float4*>(sqn_s);
+                const float* sqn_s = sqn_pad + si.pad_off;
 #pragma unroll
                 for (int c = 0; c < kMaxChunks; ++c) {
                     if (c < int(nch)) {
@@ -336,36 +359,23 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                                 ptx::tc_fence_before();
                                 ptx::mbar_arrive(bar_empty);
                             }
+                            mA[4 * c + 2 * h] = max32(v0);
+                            mA[4 * c + 2 * h + 1] = max32(v1);
 #pragma unroll
-                            for (int k = 0; k < 8; ++k) {
-                                const float4 a = __ldg(sq4 + c * 32 + h * 16 + k);
-                                const float4 b = __ldg(sq4 + c * 32 + h * 16 + 8 + k);
-                                v0[4 * k + 0] = fmaf(v0[4 * k + 0], mrow, a.x);
-                                v0[4 * k + 1] = fmaf(v0[4 * k + 1], mrow, a.y);
-                                v0[4 * k + 2] = fmaf(v0[4 * k + 2], mrow, a.z);
-                                v0[4 * k + 3] = fmaf(v0[4 * k + 3], mrow, a.w);
-                                v1[4 * k + 0] = fmaf(v1[4 * k + 0], mrow, b.x);
-                                v1[4 * k + 1] = fmaf(v1[4 * k + 1], mrow, b.y);
-                                v1[4 * k + 2] = fmaf(v1[4 * k + 2], mrow, b.z);
-                                v1[4 * k + 3] = fmaf(v1[4 * k + 3], mrow, b.w);
-                            }
-                            mA[4 * c + 2 * h] = min32(v0);
-                            mA[4 * c + 2 * h + 1] = min32(v1);
-#pragma unroll
-                            for (int b = 0; b < 32; ++b) mB[b] = ptx::fmin3(mB[b], v0[b], v1[b]);
+                            for (int b = 0; b < 32; ++b) mB[b] = ptx::fmax3(mB[b], v0[b], v1[b]);
                         }
                     }
                 }
-                // ---- candidates {32a + b : mA[a] <= m + W, mB[b] <= m + W}
-                float m1 = INFINITY;
+                // ---- candidates {32a + b : mA[a] >= m - W, mB[b] >= m - W}
+                float m1 = -INFINITY;
 #pragma unroll
-                for (int k = 0; k < 4 * kMaxChunks; ++k) m1 = fminf(m1, mA[k]);
-                const float thr = m1 + W;
+                for (int k = 0; k < 4 * kMaxChunks; ++k) m1 = fmaxf(m1, mA[k]);
+                const float thr = m1 - W;
                 uint32_t CA = 0, CB = 0;
 #pragma unroll
-                for (int k = 0; k < 4 * kMaxChunks; ++k) CA |= (mA[k] <= thr ? 1u : 0u) << k;
+                for (int k = 0; k < 4 * kMaxChunks; ++k) CA |= (mA[k] >= thr ? 1u : 0u) << k;
 #pragma unroll
-                for (int b = 0; b < 32; ++b) CB |= (mB[b] <= thr ? 1u : 0u) << b;
+                for (int b = 0; b < 32; ++b) CB |= (mB[b] >= thr ? 1u : 0u) << b;
                 const uint32_t na = __popc(CA), nb = __popc(CB);
                 const bool unique = (na == 1 && nb == 1);
                 uint32_t z = unique ? (32u * (__ffs(CA) - 1) + (__ffs(CB) - 1)) : 0u;
@@ -478,6 +488,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 const bool last = (s + 1 == n_stages);
                 const int sigma_n = sigma_of(mx + si.max_abs);  // max|r - e| <= max|r| + max|e|
                 const float sc_n = ldexpf(1.0f, sigma_n);
+                if (!last) store_a_ext(a_tile, i, sigma_n);
                 const float4* ez4 = reinterpret_cast<const float4*>(eff + si.eff_off + uint64_t(z) * 128);
                 float R2n = 0.f, mxn = 0.f;
                 float n0[4] = {0.f, 0.f, 0.f, 0.f}, n1[4] = {0.f, 0.f, 0.f, 0.f};
@@ -564,8 +575,11 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
 
 bool encode_tc_supported(const vqkv_stack_s& st) {
     if (st.dim != 128 || st.d_eff16 == nullptr) return false;
-    for (const auto& s : st.stages)
+    for (const auto& s : st.stages) {
         if (s.pad_size > 128u * kMaxChunks) return false;
+        // ||e||^2 must fit the fp16 ext column, entries the fp16 operand range
+        if (!(s.max_sqnorm < 60000.f) || !(s.max_abs < 1073741824.f)) return false;
+    }
     return true;
 }
 

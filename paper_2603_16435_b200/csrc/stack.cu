@@ -47,14 +47,31 @@ __global__ void half_copy_kernel(const float* __restrict__ eff, const float* __r
     uint32_t j = uint32_t(idx / D);
     uint32_t k = uint32_t(idx % D);
     float v = (j < st.size) ? eff[(st.eff_off) + idx] : 0.f;
-    // Pre-swizzled UMMA operand layout (D == 128): 128-entry chunks of 32 KB,
-    // each two K-blocks of [128 rows x 128 B] with the 128B swizzle applied
-    // (16 B granule g of row r stored at g ^ (r % 8)).  A single bulk copy of
-    // a chunk into 1024 B-aligned smem yields the canonical K-major SW128 tile.
+    // Pre-swizzled UMMA operand layout (D == 128): 128-entry chunks of 36 KB =
+    //  * two K-blocks of [128 rows x 128 B] with the 128B swizzle applied
+    //    (16 B granule g of row r stored at g ^ (r % 8)), then
+    //  * one 16-wide K-block (no swizzle, 8x16 B core matrices, LBO 128 B,
+    //    SBO 256 B) holding ||e_j||^2 split into fp16 hi + lo in columns 0, 1.
+    // A single bulk copy of a chunk into 1024 B-aligned smem yields canonical
+    // K-major UMMA tiles; the extra K-block lets the MMA add -2^(s-1)||e||^2.
     const uint32_t c = j >> 7, rj = j & 127, kb = k >> 6, kk = k & 63;
-    const uint64_t off = uint64_t(c) * 16384 + kb * 8192 + rj * 64 + (((kk >> 3) ^ (rj & 7)) << 3) + (kk & 7);
-    eff16[st.eff16_off + off] = __float2half_rn(v);
-    if (idx % D == 0) sqn_pad[st.eff16_off / D + j] = (j < st.size) ? sqn[st.eff_off / D + j] : INFINITY;
+    __half* chunk = eff16 + st.eff16_off + uint64_t(c) * 18432;
+    const uint64_t off = kb * 8192 + rj * 64 + (((kk >> 3) ^ (rj & 7)) << 3) + (kk & 7);
+    chunk[off] = __float2half_rn(v);
+    if (k < 16) {
+        // ext block: element (rj, k) at (rj/8)*256 B + (k/8)*128 B + (rj%8)*16 B + (k%8)*2 B
+        const uint64_t eoff = 16384 + (rj >> 3) * 128 + (k >> 3) * 64 + (rj & 7) * 8 + (k & 7);
+        __half hv = __float2half_rn(0.f);
+        if (j >= st.size) {
+            hv = (k == 0) ? __float2half_rn(INFINITY) : __float2half_rn(0.f);
+        } else if (k < 2) {
+            const float q = sqn[st.eff_off / D + j];
+            const __half hi = __float2half_rn(q);
+            hv = (k == 0) ? hi : __float2half_rn(q - __half2float(hi));
+        }
+        chunk[eoff] = hv;
+    }
+    if (k == 0) sqn_pad[st.pad_off + j] = (j < st.size) ? sqn[st.eff_off / D + j] : INFINITY;
 }
 
 }  // namespace
@@ -84,7 +101,7 @@ void stack_build_device(vqkv_stack_s& st, const float* entries_host, const float
         launch_check("sqnorm_kernel");
     }
     if (D == 128) {
-        VQKV_CUDA(cudaMalloc(&st.d_eff16, sizeof(__half) * st.total_pad_rows * D));
+        VQKV_CUDA(cudaMalloc(&st.d_eff16, sizeof(__half) * st.total_pad_rows * (D + 16)));
         VQKV_CUDA(cudaMalloc(&st.d_sqn_pad, sizeof(float) * st.total_pad_rows));
         for (uint32_t s = 0; s < st.n; ++s) {
             uint64_t n = uint64_t(st.stages[s].pad_size) * D;

@@ -146,7 +146,8 @@ int vqkv_stack_create(int device, int kind, uint32_t n_stages, const uint32_t* s
             si.bit_off = uint32_t(bit);
             si.pad_size = (sizes[s] + 127u) / 128u * 128u;
             si.eff_off = off * dim;
-            si.eff16_off = off16 * dim;
+            si.eff16_off = off16 * (uint64_t(dim) + 16);  // main K block + 16-wide ||e||^2 block
+            si.pad_off = off16;
             bit += si.bits;
             off += sizes[s];
             off16 += si.pad_size;

@@ -67,7 +67,8 @@ struct StageInfo {
     uint32_t bit_off;  // offset of this stage's field within a row
     uint32_t pad_size; // S_i rounded up to the tensor-core N chunk (128)
     uint64_t eff_off;  // element offset of stage in eff/sqn (rows of D floats)
-    uint64_t eff16_off;// element offset into the fp16 operand copy ([pad_size][D])
+    uint64_t eff16_off;// element offset into the fp16 operand copy (chunks of 128 entries x (D + 16))
+    uint64_t pad_off;  // row offset of the stage in the padded row space (sqn_pad index)
     float max_norm;    // max_j ||e_j|| (fp32, rounded up)
     float max_sqnorm;  // max_j ||e_j||^2
     float max_abs;     // max_{j,k} |e_jk|
