@@ -32,6 +32,7 @@
 //                     [256,384) fp32 residual tile0, [384,512) residual tile1.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "tc_ptx.cuh"
 #include "vqkv_internal.cuh"
@@ -139,7 +140,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                  const float* __restrict__ sqn_pad, const float* __restrict__ eff, const float* __restrict__ xs,
                  uint32_t n_streams, uint64_t rows, uint64_t search_block, uint16_t* __restrict__ codes,
                  float* __restrict__ norms, float* __restrict__ residuals, uint32_t* __restrict__ exact_list,
-                 uint32_t* __restrict__ exact_count, unsigned long long* __restrict__ counters) {
+                 uint32_t* __restrict__ exact_count, unsigned long long* __restrict__ counters, uint32_t dbg) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* a_tiles = smem;                                  // 2 x 32 KB
@@ -223,9 +224,10 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                                 ptx::mma_f16_ss(d, ad, bd, kIdesc, k > 0 ? 1u : 0u);
                             }
                             // + (-2^(sigma-1)) * (||e||^2 hi + lo): the score's norm term
-                            ptx::mma_f16_ss(d, ptx::umma_desc_noswz(a_base + t * kATileBytes + kExtOff, 128, 256),
-                                            ptx::umma_desc_noswz(b_base + buf * kChunkBytes + kExtOff, 128, 256),
-                                            kIdesc, 1u);
+                            if (!(dbg & 1u))
+                                ptx::mma_f16_ss(d, ptx::umma_desc_noswz(a_base + t * kATileBytes + kExtOff, 128, 256),
+                                                ptx::umma_desc_noswz(b_base + buf * kChunkBytes + kExtOff, 128, 256),
+                                                kIdesc, 1u);
                             ptx::mma_commit(ptx::smem_u32(&ctl->acc_full[t]));
                         }
                         ptx::mma_commit(ptx::smem_u32(&ctl->b_empty[buf]));
@@ -573,6 +575,11 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
 
 }  // namespace
 
+uint32_t dbg_flags() {
+    const char* e = getenv("VQKV_DBG");
+    return e ? uint32_t(strtoul(e, nullptr, 0)) : 0u;
+}
+
 bool encode_tc_supported(const vqkv_stack_s& st) {
     if (st.dim != 128 || st.d_eff16 == nullptr) return false;
     for (const auto& s : st.stages) {
@@ -607,7 +614,7 @@ void launch_encode_tc(const vqkv_stack_s& st, const float* xs, uint32_t n_stream
     ProfScope ps("encode_tc", s);
     encode_tc_kernel<<<grid, kThreads, kSmemBytes, s>>>(st.d_stages, st.n, st.d_eff16, st.d_sqn_pad, st.d_eff, xs,
                                                          n_streams, rows, search_block, codes, norms, residuals,
-                                                         list + 1, list, st.d_counters);
+                                                         list + 1, list, st.d_counters, dbg_flags());
     launch_check("encode_tc_kernel");
     }
     // rows with non-finite input: exact reference semantics
