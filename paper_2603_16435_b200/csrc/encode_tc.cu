@@ -421,6 +421,10 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         }
                         const bool has = (j != 0xffffffffu);
                         const float4* e4 = reinterpret_cast<const float4*>(eff + si.eff_off + uint64_t(has ? j : 0) * 128);
+                        if (has) {  // one L2 round trip for the whole row, not one per chunk
+#pragma unroll
+                            for (int l = 0; l < 4; ++l) ptx::prefetch_l1(e4 + 8 * l);
+                        }
                         float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
                         float r0[4] = {0.f, 0.f, 0.f, 0.f}, r1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
@@ -482,6 +486,9 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         z = (best == ~0ull) ? 0u : uint32_t(best & 0xffffffffu);
                         n_rs += cnt;
                         ++n_amb;
+                        const float* ez = eff + si.eff_off + uint64_t(z) * 128;
+#pragma unroll
+                        for (int l = 0; l < 4; ++l) ptx::prefetch_l1(ez + 32 * l);
                     }
                 }
                 if (valid && !exact_row) codes[grow * n_stages + s] = uint16_t(z);
