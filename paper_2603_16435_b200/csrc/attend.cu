@@ -14,6 +14,7 @@
 // view_block does, and never written to HBM.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "vqkv_internal.cuh"
 
@@ -204,7 +205,19 @@ __global__ void lse_combine_kernel(const float* __restrict__ o, const float* __r
 
 }  // namespace
 
+int attend_path() {
+    const char* e = getenv("VQKV_ATTEND_PATH");  // 1 = force the generic kernel (tests)
+    return e ? atoi(e) : 0;
+}
+
+bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a);
+void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s);
+
 void launch_attend(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s) {
+    if (attend_path() != 1 && attend_lut_supported(ks, vs, a)) {
+        launch_attend_lut(ks, vs, a, s);
+        return;
+    }
     const uint32_t Dk = ks.dim, Dv = vs.dim, G = a.group;
     const uint64_t L = a.n_init + a.n_comp + a.n_local;
     int sms = 148;

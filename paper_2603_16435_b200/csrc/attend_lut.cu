@@ -1,0 +1,478 @@
+// attend_lut.cu -- K3 fast path: decode-step attention over the compressed
+// cache in the dot-product domain (D = 128, G = 4 query heads per KV head).
+//
+// Reference: attend (proj/core/src/attention.cpp:26-69) over
+// CacheState::view_block (kv_cache.cpp:143-189), whose compressed rows are
+// reconstruct() sums (codebook.cpp:208-223).  Because reconstruction is a sum
+// of codebook rows, for every query q_g
+//     scale * q_g . k_t = sum_s LUT_s[z_s,t][g],   LUT_s[j][g] = scale * q_g . e_s[j]
+//     sum_t p_t,g v_t   = sum_s sum_j H_s[j][g] e_s[j],  H_s[j][g] = sum_{t: z_s,t = j} p_t,g
+// so keys cost one table lookup per (token, stage) and values one histogram
+// update per (token, stage); neither K nor V rows are ever materialised.
+//
+// Kernels (one launch each, all on the caller's stream):
+//   lut_kernel      LUT[pair][s][j] = float4 over g, fp32 (FFMA from the
+//                   fp32 effective entries; the table stays L2-hot per pair)
+//   attend_lut      CTA = (pair, split of <= 8192 compressed tokens):
+//                   keys: 4-stage LUT groups double-buffered into smem by bulk
+//                   copy (TMA engine), one LDS.128 + 4 FADD per (token, stage);
+//                   split max; p = exp(logit - max); values: int32 fixed-point
+//                   (2^-18) smem histograms via native shared atomics;
+//                   writes (H as fp32, m, l).  One extra CTA per pair handles
+//                   the raw init/local rows directly (o_acc, m, l).
+//   lut_combine     per pair: merge splits by LSE weights, contract H with the
+//                   value codebooks, add the raw part, normalise, emit lse.
+#include <algorithm>
+#include <cmath>
+
+#include "tc_ptx.cuh"
+#include "vqkv_internal.cuh"
+
+namespace vqkv_dev {
+
+namespace {
+
+constexpr int kG = 4;              // query heads per KV head on this path
+constexpr int kD = 128;            // head dim
+constexpr int kAttThreads = 512;
+constexpr int kTokPerThread = 16;
+constexpr int kSplitTokens = kAttThreads * kTokPerThread;  // 8192
+constexpr int kGroupStages = 4;    // LUT stages per smem buffer (4 x 16 KB)
+constexpr float kHistScale = 262144.0f;  // 2^18 fixed point for p in [0, 1]
+
+struct LutArgs {
+    const float* q;        // [pairs][G][D]
+    const float* keff;     // key effective entries
+    const StageInfo* kst;
+    uint32_t kn;
+    uint64_t kentries;     // total key entries (sum S)
+    float scale;
+    float4* lut;           // [pairs][kentries]
+};
+
+// LUT[pair][e] = scale * q_g . E[e] for all key entries e (stage-concatenated).
+// CTA: 64 entries x 8 pairs; thread computes 1 entry x 4 queries for 1 pair.
+__global__ void __launch_bounds__(512) lut_kernel(LutArgs a, uint32_t n_pairs) {
+    __shared__ float qs[8][kG][kD];
+    __shared__ float es[64][kD + 1];
+    const uint32_t e0 = blockIdx.x * 64, p0 = blockIdx.y * 8;
+    for (uint32_t i = threadIdx.x; i < 8 * kG * kD; i += blockDim.x) {
+        const uint32_t p = i / (kG * kD);
+        qs[p][(i / kD) % kG][i % kD] = (p0 + p < n_pairs) ? a.q[uint64_t(p0 + p) * kG * kD + (i % (kG * kD))] : 0.f;
+    }
+    for (uint32_t i = threadIdx.x; i < 64 * kD; i += blockDim.x) {
+        const uint32_t r = i / kD, c = i % kD;
+        es[r][c] = (e0 + r < a.kentries) ? a.keff[uint64_t(e0 + r) * kD + c] : 0.f;
+    }
+    __syncthreads();
+    const uint32_t r = threadIdx.x & 63, p = threadIdx.x >> 6;
+    float acc[kG] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
+    for (int c = 0; c < kD; ++c) {
+        const float e = es[r][c];
+#pragma unroll
+        for (int g = 0; g < kG; ++g) acc[g] = fmaf(qs[p][g][c], e, acc[g]);
+    }
+    if (p0 + p < n_pairs && e0 + r < a.kentries)
+        a.lut[uint64_t(p0 + p) * a.kentries + e0 + r] =
+            make_float4(acc[0] * a.scale, acc[1] * a.scale, acc[2] * a.scale, acc[3] * a.scale);
+}
+
+// Reads 64 bits starting at bit `pos` of a byte stream: two aligned 64-bit
+// loads when they stay inside [.., end), byte loads otherwise (buffer tails).
+__device__ __forceinline__ uint64_t read_bits64(const uint8_t* base, uint64_t pos, const uint8_t* end) {
+    const uint8_t* p = base + (pos >> 3);
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(7);
+    const uint32_t sh = uint32_t((reinterpret_cast<uintptr_t>(p) - a) * 8 + (pos & 7));
+    if (a + 16 <= reinterpret_cast<uintptr_t>(end)) {
+        const uint64_t* q = reinterpret_cast<const uint64_t*>(a);
+        const uint64_t lo = __ldg(q), hi = __ldg(q + 1);
+        return sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
+    }
+    uint64_t v = 0;
+    const uint32_t bsh = uint32_t(pos & 7);
+    for (int b = 0; b < 8 && p + b < end; ++b) v |= uint64_t(p[b]) << (8 * b);
+    uint64_t extra = (p + 8 < end) ? uint64_t(p[8]) : 0ull;
+    return bsh ? ((v >> bsh) | (extra << (64 - bsh))) : v;
+}
+
+struct MainArgs {
+    const float* q;
+    const float* init_k;
+    const float* init_v;
+    uint64_t n_init;
+    const uint8_t* kcodes;
+    const uint8_t* vcodes;
+    uint64_t n_comp;
+    const float* local_k;
+    const float* local_v;
+    uint64_t n_local;
+    const StageInfo* kst;
+    uint32_t kn;
+    uint64_t krow_bits, kstream_bytes, kentries;
+    const StageInfo* vst;
+    uint32_t vn;
+    uint64_t vrow_bits, vstream_bytes, ventries;
+    const float4* lut;
+    const uint8_t* kend;
+    const uint8_t* vend;
+    float scale;
+    uint32_t n_splits;  // compressed splits per pair (+1 raw CTA)
+    float* part_h;      // [pairs][splits][ventries][G]
+    float* part_o;      // [pairs][G][D]  (raw CTA)
+    float* part_m;      // [pairs][splits+1][G]
+    float* part_l;      // [pairs][splits+1][G]
+};
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float r = -INFINITY;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) r = fmaxf(r, red[w]);
+    return r;
+}
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float r = 0.f;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) r += red[w];
+    return r;
+}
+
+// raw init/local rows of one pair: direct fp32 attention (no codebooks)
+__device__ void raw_rows(const MainArgs& a, uint32_t pair, float* smem) {
+    float* red = smem;                 // 64
+    float* qs = smem + 64;             // G*D
+    float* ls = qs + kG * kD;          // logits [n_raw][G] (n_raw <= 8192)
+    for (uint32_t i = threadIdx.x; i < kG * kD; i += blockDim.x) qs[i] = a.q[uint64_t(pair) * kG * kD + i];
+    __syncthreads();
+    const uint64_t n_raw = a.n_init + a.n_local;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (uint64_t r = warp; r < n_raw; r += nw) {
+        const float* k = (r < a.n_init) ? a.init_k + (uint64_t(pair) * a.n_init + r) * kD
+                                        : a.local_k + (uint64_t(pair) * a.n_local + (r - a.n_init)) * kD;
+        const float4 kv = reinterpret_cast<const float4*>(k)[lane];
+        for (int g = 0; g < kG; ++g) {
+            const float4 qv = reinterpret_cast<const float4*>(qs + g * kD)[lane];
+            float d = kv.x * qv.x + kv.y * qv.y + kv.z * qv.z + kv.w * qv.w;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            if (lane == 0) ls[r * kG + g] = d * a.scale;
+        }
+    }
+    __syncthreads();
+    for (int g = 0; g < kG; ++g) {
+        float m = -INFINITY;
+        for (uint64_t r = threadIdx.x; r < n_raw; r += blockDim.x) m = fmaxf(m, ls[r * kG + g]);
+        m = block_max(m, red);
+        float l = 0.f;
+        for (uint64_t r = threadIdx.x; r < n_raw; r += blockDim.x) {
+            const float p = __expf(ls[r * kG + g] - m);
+            ls[r * kG + g] = p;
+            l += p;
+        }
+        l = block_sum(l, red);
+        if (threadIdx.x == 0) {
+            a.part_m[(uint64_t(pair) * (a.n_splits + 1) + a.n_splits) * kG + g] = m;
+            a.part_l[(uint64_t(pair) * (a.n_splits + 1) + a.n_splits) * kG + g] = l;
+        }
+    }
+    __syncthreads();
+    // o[g][d] = sum_r p[r][g] v_r[d]; thread = (g, d)
+    for (uint32_t gd = threadIdx.x; gd < kG * kD; gd += blockDim.x) {
+        const uint32_t g = gd / kD, d = gd % kD;
+        float acc = 0.f;
+        for (uint64_t r = 0; r < n_raw; ++r) {
+            const float* v = (r < a.n_init) ? a.init_v + (uint64_t(pair) * a.n_init + r) * kD
+                                            : a.local_v + (uint64_t(pair) * a.n_local + (r - a.n_init)) * kD;
+            acc = fmaf(ls[r * kG + g], __ldg(v + d), acc);
+        }
+        a.part_o[(uint64_t(pair) * kG + g) * kD + d] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t pair = blockIdx.y, split = blockIdx.x;
+    float* fsm = reinterpret_cast<float*>(smem_raw);
+    if (split == a.n_splits) {
+        if (a.n_init + a.n_local > 0) {
+            raw_rows(a, pair, fsm);
+        } else if (threadIdx.x < kG) {
+            a.part_m[(uint64_t(pair) * (a.n_splits + 1) + a.n_splits) * kG + threadIdx.x] = -INFINITY;
+            a.part_l[(uint64_t(pair) * (a.n_splits + 1) + a.n_splits) * kG + threadIdx.x] = 0.f;
+        }
+        return;
+    }
+    // smem: [0, 128K) two LUT group buffers (2 x 4 stages x 1024 x 16 B) / value histograms
+    //       then mbarriers and reduction scratch
+    uint8_t* lut_buf = smem_raw;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 131072);
+    float* red = reinterpret_cast<float*>(smem_raw + 131072 + 64);
+    const uint64_t t0 = uint64_t(split) * kSplitTokens;
+    const uint64_t nt = (a.n_comp - t0 < uint64_t(kSplitTokens)) ? (a.n_comp - t0) : uint64_t(kSplitTokens);
+    const uint8_t* kc = a.kcodes + uint64_t(pair) * a.kstream_bytes;
+    const uint8_t* vc = a.vcodes + uint64_t(pair) * a.vstream_bytes;
+    const float4* lutp = a.lut + uint64_t(pair) * a.kentries;
+
+    float lg[kTokPerThread][kG];
+#pragma unroll
+    for (int k = 0; k < kTokPerThread; ++k)
+#pragma unroll
+        for (int g = 0; g < kG; ++g) lg[k][g] = 0.f;
+
+    // ---- keys: LUT groups of kGroupStages stages, double-buffered bulk copies
+    const uint32_t ngroups = (a.kn + kGroupStages - 1) / kGroupStages;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(ptx::smem_u32(&bars[0]), 1);
+        ptx::mbar_init(ptx::smem_u32(&bars[1]), 1);
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](uint32_t grp) {
+        const uint32_t b = grp & 1;
+        const uint32_t s0 = grp * kGroupStages;
+        const uint32_t s1 = min(a.kn, s0 + kGroupStages);
+        uint32_t bytes = 0;
+        for (uint32_t s = s0; s < s1; ++s) bytes += a.kst[s].size * 16u;
+        const uint32_t bar = ptx::smem_u32(&bars[b]);
+        ptx::mbar_arrive_expect_tx(bar, bytes);
+        uint32_t off = 0;
+        for (uint32_t s = s0; s < s1; ++s) {
+            const uint32_t nb = a.kst[s].size * 16u;
+            ptx::bulk_g2s(ptx::smem_u32(lut_buf + b * 65536 + off), lutp + a.kst[s].eff_off / kD, nb, bar);
+            off += nb;
+        }
+    };
+    if (threadIdx.x == 0) issue(0);
+    for (uint32_t grp = 0; grp < ngroups; ++grp) {
+        if (threadIdx.x == 0 && grp + 1 < ngroups) issue(grp + 1);
+        ptx::mbar_wait(ptx::smem_u32(&bars[grp & 1]), (grp >> 1) & 1);
+        const uint32_t s0 = grp * kGroupStages;
+        const uint32_t s1 = min(a.kn, s0 + kGroupStages);
+        const float4* L = reinterpret_cast<const float4*>(lut_buf + (grp & 1) * 65536);
+        const uint32_t gbit = a.kst[s0].bit_off;
+        uint32_t loff[kGroupStages], lbits[kGroupStages], lofs[kGroupStages];
+        uint32_t acc_off = 0;
+#pragma unroll
+        for (int q = 0; q < kGroupStages; ++q) {
+            const uint32_t s = s0 + q;
+            lbits[q] = (s < s1) ? a.kst[s].bits : 0u;
+            loff[q] = (s < s1) ? a.kst[s].bit_off - gbit : 0u;
+            lofs[q] = acc_off;
+            acc_off += (s < s1) ? a.kst[s].size : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < kTokPerThread; ++k) {
+            const uint64_t t = threadIdx.x + uint64_t(k) * kAttThreads;
+            if (t < nt) {
+                const uint64_t w = read_bits64(kc, (t0 + t) * a.krow_bits + gbit, a.kend);
+#pragma unroll
+                for (int q = 0; q < kGroupStages; ++q) {
+                    if (lbits[q]) {
+                        const uint32_t z = uint32_t(w >> loff[q]) & ((1u << lbits[q]) - 1u);
+                        const float4 v = L[lofs[q] + z];
+                        lg[k][0] += v.x;
+                        lg[k][1] += v.y;
+                        lg[k][2] += v.z;
+                        lg[k][3] += v.w;
+                    }
+                }
+            }
+        }
+        __syncthreads();  // buffer (grp & 1) is refilled two groups later
+    }
+
+    // ---- split max / p / l
+    float mg[kG], lsum[kG];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) {
+        float m = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < kTokPerThread; ++k)
+            if (threadIdx.x + uint64_t(k) * kAttThreads < nt) m = fmaxf(m, lg[k][g]);
+        mg[g] = block_max(m, red);
+    }
+#pragma unroll
+    for (int g = 0; g < kG; ++g) {
+        float l = 0.f;
+#pragma unroll
+        for (int k = 0; k < kTokPerThread; ++k) {
+            const bool ok = threadIdx.x + uint64_t(k) * kAttThreads < nt;
+            const float p = ok ? __expf(lg[k][g] - mg[g]) : 0.f;
+            lg[k][g] = p;
+            l += p;
+        }
+        lsum[g] = block_sum(l, red);
+    }
+
+    // ---- values: int32 fixed-point histograms H[s][j][g] in smem (reuses the LUT area)
+    uint32_t* H = reinterpret_cast<uint32_t*>(smem_raw);
+    const uint32_t hsz = uint32_t(a.ventries) * kG;
+    for (uint32_t i = threadIdx.x; i < hsz; i += blockDim.x) H[i] = 0u;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kTokPerThread; ++k) {
+        const uint64_t t = threadIdx.x + uint64_t(k) * kAttThreads;
+        if (t < nt) {
+            uint32_t P[kG];
+#pragma unroll
+            for (int g = 0; g < kG; ++g) P[g] = __float2uint_rn(lg[k][g] * kHistScale);
+            const uint64_t rb = (t0 + t) * a.vrow_bits;
+            for (uint32_t s0 = 0; s0 < a.vn; s0 += 6) {  // <= 6 x 9-bit fields per 64-bit read
+                const uint64_t w = read_bits64(vc, rb + a.vst[s0].bit_off, a.vend);
+                const uint32_t s1 = min(a.vn, s0 + 6u);
+                for (uint32_t s = s0; s < s1; ++s) {
+                    const StageInfo si = a.vst[s];
+                    const uint32_t z = uint32_t(w >> (si.bit_off - a.vst[s0].bit_off)) & ((1u << si.bits) - 1u);
+                    uint32_t* h = H + (si.eff_off / kD + z) * kG;
+#pragma unroll
+                    for (int g = 0; g < kG; ++g)
+                        if (P[g]) atomicAdd(h + g, P[g]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    float* ph = a.part_h + (uint64_t(pair) * a.n_splits + split) * hsz;
+    for (uint32_t i = threadIdx.x; i < hsz; i += blockDim.x) ph[i] = float(H[i]) * (1.0f / kHistScale);
+    if (threadIdx.x < kG) {
+        a.part_m[(uint64_t(pair) * (a.n_splits + 1) + split) * kG + threadIdx.x] = mg[threadIdx.x];
+        a.part_l[(uint64_t(pair) * (a.n_splits + 1) + split) * kG + threadIdx.x] = lsum[threadIdx.x];
+    }
+}
+
+// Merge splits of one pair: thread = (g, d); H contracted with the value codebooks.
+__global__ void __launch_bounds__(512) lut_combine_kernel(const float* __restrict__ part_h, const float* __restrict__ part_o,
+                                                           const float* __restrict__ part_m,
+                                                           const float* __restrict__ part_l, uint32_t n_splits,
+                                                           const float* __restrict__ veff, uint64_t ventries,
+                                                           float* __restrict__ out, float* __restrict__ lse) {
+    extern __shared__ float hs[];  // [chunk of entries][G] merged histogram
+    __shared__ float w[64][kG];
+    __shared__ float Ms[kG], Ls[kG];
+    const uint32_t pair = blockIdx.x;
+    const uint32_t ns = n_splits + 1;
+    if (threadIdx.x < kG) {
+        const uint32_t g = threadIdx.x;
+        float M = -INFINITY;
+        for (uint32_t s = 0; s < ns; ++s) M = fmaxf(M, part_m[(uint64_t(pair) * ns + s) * kG + g]);
+        float L = 0.f;
+        for (uint32_t s = 0; s < ns; ++s) {
+            const float m = part_m[(uint64_t(pair) * ns + s) * kG + g];
+            const float ww = (m > -INFINITY) ? __expf(m - M) : 0.f;
+            if (s < 64) w[s][g] = ww;
+            L += ww * part_l[(uint64_t(pair) * ns + s) * kG + g];
+        }
+        Ms[g] = M;
+        Ls[g] = L;
+    }
+    __syncthreads();
+    const uint32_t g = threadIdx.x / kD, d = threadIdx.x % kD;
+    float acc = (g < kG && w[n_splits][g] > 0.f) ? w[n_splits][g] * part_o[(uint64_t(pair) * kG + g) * kD + d] : 0.f;
+    const uint32_t CH = 1024;  // entries per smem chunk
+    for (uint64_t e0 = 0; e0 < ventries; e0 += CH) {
+        const uint32_t ne = uint32_t((ventries - e0 < CH) ? (ventries - e0) : CH);
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < ne * kG; i += blockDim.x) {
+            const uint32_t gg = i % kG;
+            float v = 0.f;
+            for (uint32_t s = 0; s < n_splits; ++s)
+                v = fmaf(w[s][gg], part_h[((uint64_t(pair) * n_splits + s) * ventries + e0) * kG + i], v);
+            hs[i] = v;
+        }
+        __syncthreads();
+        if (g < kG)
+            for (uint32_t e = 0; e < ne; ++e) acc = fmaf(hs[e * kG + g], __ldg(veff + (e0 + e) * kD + d), acc);
+    }
+    if (g < kG) {
+        out[(uint64_t(pair) * kG + g) * kD + d] = acc / Ls[g];
+        if (d == 0 && lse) lse[uint64_t(pair) * kG + g] = Ms[g] + logf(Ls[g]);
+    }
+}
+
+}  // namespace
+
+bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a) {
+    if (ks.dim != kD || vs.dim != kD || a.group != kG) return false;
+    if (a.n_init + a.n_local > kSplitTokens) return false;
+    if ((a.n_comp + kSplitTokens - 1) / kSplitTokens + 1 > 64) return false;
+    for (const auto& s : ks.stages)
+        if (s.size > 1024 || s.bits > 10) return false;
+    // 4 key stages per 64-bit read and LUT group (<= 64 KB)
+    for (uint32_t s0 = 0; s0 < ks.n; s0 += kGroupStages) {
+        uint32_t bits = 0, bytes = 0;
+        for (uint32_t s = s0; s < std::min(ks.n, s0 + kGroupStages); ++s) {
+            bits += ks.stages[s].bits;
+            bytes += ks.stages[s].size * 16u;
+        }
+        if (bits > 56 || bytes > 65536) return false;
+    }
+    uint32_t ventries = 0;
+    for (uint32_t s0 = 0; s0 < vs.n; s0 += 6) {
+        uint32_t bits = 0;
+        for (uint32_t s = s0; s < std::min(vs.n, s0 + 6u); ++s) bits += vs.stages[s].bits;
+        if (bits > 56) return false;
+    }
+    for (const auto& s : vs.stages) ventries += s.size;
+    if (uint64_t(ventries) * kG * 4 > 131072) return false;
+    return true;
+}
+
+void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s) {
+    const uint64_t kent = ks.total_rows, vent = vs.total_rows;
+    const uint32_t n_splits = uint32_t((a.n_comp + kSplitTokens - 1) / kSplitTokens);
+    const double scale = a.scale > 0.0 ? a.scale : 1.0 / std::sqrt(double(kD));
+    float4* lut = nullptr;
+    float *ph = nullptr, *po = nullptr, *pm = nullptr, *pl = nullptr;
+    VQKV_CUDA(cudaMallocAsync(&lut, sizeof(float4) * a.n_pairs * kent, s));
+    VQKV_CUDA(cudaMallocAsync(&ph, sizeof(float) * std::max<uint64_t>(1, uint64_t(a.n_pairs) * n_splits * vent * kG), s));
+    VQKV_CUDA(cudaMallocAsync(&po, sizeof(float) * a.n_pairs * kG * kD, s));
+    VQKV_CUDA(cudaMallocAsync(&pm, sizeof(float) * a.n_pairs * (n_splits + 1) * kG, s));
+    VQKV_CUDA(cudaMallocAsync(&pl, sizeof(float) * a.n_pairs * (n_splits + 1) * kG, s));
+    {
+        ProfScope ps("attend_lut_build", s);
+        LutArgs la{a.q_dev, ks.d_eff, ks.d_stages, ks.n, kent, float(scale), lut};
+        dim3 grid(unsigned((kent + 63) / 64), (a.n_pairs + 7) / 8);
+        lut_kernel<<<grid, 512, 0, s>>>(la, a.n_pairs);
+        launch_check("lut_kernel");
+    }
+    {
+        ProfScope ps("attend", s);
+        MainArgs ma{a.q_dev, a.init_k_dev, a.init_v_dev, a.n_init, a.kcodes_dev, a.vcodes_dev, a.n_comp,
+                    a.local_k_dev, a.local_v_dev, a.n_local, ks.d_stages, ks.n, ks.row_bits,
+                    payload_bytes(ks.row_bits, a.n_comp), kent, vs.d_stages, vs.n, vs.row_bits,
+                    payload_bytes(vs.row_bits, a.n_comp), vent, lut,
+                    a.kcodes_dev + uint64_t(a.n_pairs) * payload_bytes(ks.row_bits, a.n_comp),
+                    a.vcodes_dev + uint64_t(a.n_pairs) * payload_bytes(vs.row_bits, a.n_comp), float(scale), n_splits,
+                    ph, po, pm, pl};
+        const size_t smem = 131072 + 64 + 64 * sizeof(float) + 4096;
+        static bool attr = false;
+        if (!attr) {
+            VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            attr = true;
+        }
+        dim3 grid(n_splits + 1, a.n_pairs);
+        attend_lut_kernel<<<grid, kAttThreads, smem, s>>>(ma);
+        launch_check("attend_lut_kernel");
+    }
+    {
+        ProfScope ps("attend_combine", s);
+        lut_combine_kernel<<<a.n_pairs, 512, 1024 * kG * sizeof(float), s>>>(ph, po, pm, pl, n_splits, vs.d_eff, vent,
+                                                                            a.out_dev, a.lse_dev);
+        launch_check("lut_combine_kernel");
+    }
+    VQKV_CUDA(cudaFreeAsync(lut, s));
+    VQKV_CUDA(cudaFreeAsync(ph, s));
+    VQKV_CUDA(cudaFreeAsync(po, s));
+    VQKV_CUDA(cudaFreeAsync(pm, s));
+    VQKV_CUDA(cudaFreeAsync(pl, s));
+}
+
+}  // namespace vqkv_dev

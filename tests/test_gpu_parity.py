@@ -218,3 +218,39 @@ def test_lse_combine_matches_monolithic(torch_mod):
     mo, ml = Dv.lse_combine(torch.stack(outs).contiguous(), torch.stack(lses).contiguous())
     assert torch.allclose(mo, full.reshape(G, 16), atol=1e-5, rtol=1e-4)
     assert torch.allclose(ml, full_lse.reshape(G), atol=1e-5, rtol=1e-5)
+
+
+@pytest.mark.parametrize("nk,sk,nv,sv,n_pairs,n_init,n_comp,n_local",
+                         [(6, 256, 4, 128, 3, 4, 9000, 40), (56, 1024, 16, 512, 2, 4, 3000, 17), (3, 64, 2, 64, 2, 0, 100, 0),
+                          (4, 128, 4, 128, 1, 2, 0, 33)])
+def test_attention_lut_path_vs_oracle(torch_mod, nk, sk, nv, sv, n_pairs, n_init, n_comp, n_local):
+    """LUT/histogram fast path (D=128, G=4) against the oracle's attend over the same segments."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+
+    rng = O.Rng(nk * 1000 + sk)
+    ks = rng.stack(nk, sk, 128, O.KEY)
+    vs = rng.stack(nv, sv, 128, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    G = 4
+    mk = lambda n: rng.matrix(max(n_pairs * n, 1), 128)[: n_pairs * n].reshape(n_pairs, n, 128)
+    init_k, init_v, loc_k, loc_v = mk(n_init), mk(n_init), mk(n_local), mk(n_local)
+    g = np.random.default_rng(nk)
+    kc = np.stack([ks.pack(g.integers(0, sk, (n_comp, nk)).astype(np.uint32)) for _ in range(n_pairs)])
+    vc = np.stack([vs.pack(g.integers(0, sv, (n_comp, nv)).astype(np.uint32)) for _ in range(n_pairs)])
+    q = rng.matrix(n_pairs * G, 128).reshape(n_pairs, G, 128)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    out, lse = Dv.attend_decode(pk, pv, t(q), t(kc) if n_comp else None, t(vc) if n_comp else None, n_comp,
+                                t(init_k) if n_init else None, t(init_v) if n_init else None,
+                                t(loc_k) if n_local else None, t(loc_v) if n_local else None)
+    out, lse = out.cpu().numpy(), lse.cpu().numpy()
+    worst = 0.0
+    for pi in range(n_pairs):
+        for gg in range(G):
+            ref, ref_lse = O.attend_segments(ks, vs, init_k[pi], init_v[pi], kc[pi] if n_comp else b"", vc[pi] if n_comp else b"",
+                                             n_comp, loc_k[pi], loc_v[pi], q[pi, gg])
+            err = np.abs(out[pi, gg] - ref).max() / max(1.0, np.abs(ref).max())
+            worst = max(worst, err)
+            assert abs(lse[pi, gg] - ref_lse) <= 1e-3 * max(1.0, abs(ref_lse))
+    print(f"worst scaled attention error {worst:.2e} (tolerance {ATT_TOL:.2e})")
+    assert worst <= ATT_TOL
