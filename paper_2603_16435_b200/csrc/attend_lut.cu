@@ -53,8 +53,9 @@ struct LutArgs {
 // LUT[pair][e] = scale * q_g . E[e] for all key entries e (stage-concatenated).
 // CTA: 64 entries x 8 pairs; thread computes 1 entry x 4 queries for 1 pair.
 __global__ void __launch_bounds__(512) lut_kernel(LutArgs a, uint32_t n_pairs) {
-    __shared__ float qs[8][kG][kD];
-    __shared__ float es[64][kD + 1];
+    extern __shared__ float lsm[];
+    float (*qs)[kG][kD] = reinterpret_cast<float (*)[kG][kD]>(lsm);                // [8][G][D]
+    float (*es)[kD + 1] = reinterpret_cast<float (*)[kD + 1]>(lsm + 8 * kG * kD);  // [64][D+1]
     const uint32_t e0 = blockIdx.x * 64, p0 = blockIdx.y * 8;
     for (uint32_t i = threadIdx.x; i < 8 * kG * kD; i += blockDim.x) {
         const uint32_t p = i / (kG * kD);
@@ -440,7 +441,13 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         ProfScope ps("attend_lut_build", s);
         LutArgs la{a.q_dev, ks.d_eff, ks.d_stages, ks.n, kent, float(scale), lut};
         dim3 grid(unsigned((kent + 63) / 64), (a.n_pairs + 7) / 8);
-        lut_kernel<<<grid, 512, 0, s>>>(la, a.n_pairs);
+        const int lsmem = int(sizeof(float) * (8 * kG * kD + 64 * (kD + 1)));
+        static bool lattr = false;
+        if (!lattr) {
+            VQKV_CUDA(cudaFuncSetAttribute(lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem));
+            lattr = true;
+        }
+        lut_kernel<<<grid, 512, lsmem, s>>>(la, a.n_pairs);
         launch_check("lut_kernel");
     }
     {
