@@ -51,32 +51,53 @@ struct LutArgs {
 };
 
 // LUT[pair][e] = scale * q_g . E[e] for all key entries e (stage-concatenated).
-// CTA: 64 entries x 8 pairs; thread computes 1 entry x 4 queries for 1 pair.
-__global__ void __launch_bounds__(512) lut_kernel(LutArgs a, uint32_t n_pairs) {
+// CTA: 128 entries x 8 pairs, 256 threads; thread = 4 entries x 4 queries of one pair.
+constexpr int kLutEntries = 128;
+__global__ void __launch_bounds__(256) lut_kernel(LutArgs a, uint32_t n_pairs) {
     extern __shared__ float lsm[];
     float (*qs)[kG][kD] = reinterpret_cast<float (*)[kG][kD]>(lsm);                // [8][G][D]
-    float (*es)[kD + 1] = reinterpret_cast<float (*)[kD + 1]>(lsm + 8 * kG * kD);  // [64][D+1]
-    const uint32_t e0 = blockIdx.x * 64, p0 = blockIdx.y * 8;
+    float (*es)[kD + 1] = reinterpret_cast<float (*)[kD + 1]>(lsm + 8 * kG * kD);  // [128][D+1]
+    const uint32_t e0 = blockIdx.x * kLutEntries, p0 = blockIdx.y * 8;
     for (uint32_t i = threadIdx.x; i < 8 * kG * kD; i += blockDim.x) {
         const uint32_t p = i / (kG * kD);
         qs[p][(i / kD) % kG][i % kD] = (p0 + p < n_pairs) ? a.q[uint64_t(p0 + p) * kG * kD + (i % (kG * kD))] : 0.f;
     }
-    for (uint32_t i = threadIdx.x; i < 64 * kD; i += blockDim.x) {
-        const uint32_t r = i / kD, c = i % kD;
-        es[r][c] = (e0 + r < a.kentries) ? a.keff[uint64_t(e0 + r) * kD + c] : 0.f;
+    for (uint32_t i = threadIdx.x; i < kLutEntries * kD / 4; i += blockDim.x) {
+        const uint32_t r = (4 * i) / kD, c = (4 * i) % kD;
+        const float4 v = (e0 + r < a.kentries) ? __ldg(reinterpret_cast<const float4*>(a.keff + uint64_t(e0 + r) * kD + c))
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        es[r][c] = v.x;
+        es[r][c + 1] = v.y;
+        es[r][c + 2] = v.z;
+        es[r][c + 3] = v.w;
     }
     __syncthreads();
-    const uint32_t r = threadIdx.x & 63, p = threadIdx.x >> 6;
-    float acc[kG] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 8
-    for (int c = 0; c < kD; ++c) {
-        const float e = es[r][c];
+    const uint32_t eg = threadIdx.x & 31, p = threadIdx.x >> 5;
+    float acc[4][kG];
 #pragma unroll
-        for (int g = 0; g < kG; ++g) acc[g] = fmaf(qs[p][g][c], e, acc[g]);
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int g = 0; g < kG; ++g) acc[i][g] = 0.f;
+#pragma unroll 4
+    for (int c = 0; c < kD; ++c) {
+        float qv[kG], ev[4];
+#pragma unroll
+        for (int g = 0; g < kG; ++g) qv[g] = qs[p][g][c];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ev[i] = es[eg + 32 * i][c];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int g = 0; g < kG; ++g) acc[i][g] = fmaf(qv[g], ev[i], acc[i][g]);
     }
-    if (p0 + p < n_pairs && e0 + r < a.kentries)
-        a.lut[uint64_t(p0 + p) * a.kentries + e0 + r] =
-            make_float4(acc[0] * a.scale, acc[1] * a.scale, acc[2] * a.scale, acc[3] * a.scale);
+    if (p0 + p < n_pairs)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t e = e0 + eg + 32 * i;
+            if (e < a.kentries)
+                a.lut[uint64_t(p0 + p) * a.kentries + e] = make_float4(acc[i][0] * a.scale, acc[i][1] * a.scale,
+                                                                        acc[i][2] * a.scale, acc[i][3] * a.scale);
+        }
 }
 
 // Reads 64 bits starting at bit `pos` of a byte stream: two aligned 64-bit
@@ -349,53 +370,64 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
     }
 }
 
-// Merge splits of one pair: thread = (g, d); H contracted with the value codebooks.
-__global__ void __launch_bounds__(512) lut_combine_kernel(const float* __restrict__ part_h, const float* __restrict__ part_o,
-                                                           const float* __restrict__ part_m,
-                                                           const float* __restrict__ part_l, uint32_t n_splits,
-                                                           const float* __restrict__ veff, uint64_t ventries,
-                                                           float* __restrict__ out, float* __restrict__ lse) {
-    extern __shared__ float hs[];  // [chunk of entries][G] merged histogram
-    __shared__ float w[64][kG];
-    __shared__ float Ms[kG], Ls[kG];
-    const uint32_t pair = blockIdx.x;
+// Split weights: w[pair][s][g] = exp(m_s - M), L = sum_s w l_s, M = max_s m_s.
+__global__ void lut_weights_kernel(const float* __restrict__ part_m, const float* __restrict__ part_l,
+                                   uint32_t n_splits, uint32_t n_pairs, float* __restrict__ w, float* __restrict__ ML) {
+    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;  // pair * G + g
+    if (idx >= n_pairs * kG) return;
+    const uint32_t pair = idx / kG, g = idx % kG, ns = n_splits + 1;
+    float M = -INFINITY;
+    for (uint32_t s = 0; s < ns; ++s) M = fmaxf(M, part_m[(uint64_t(pair) * ns + s) * kG + g]);
+    float L = 0.f;
+    for (uint32_t s = 0; s < ns; ++s) {
+        const float m = part_m[(uint64_t(pair) * ns + s) * kG + g];
+        const float ww = (m > -INFINITY) ? __expf(m - M) : 0.f;
+        w[(uint64_t(pair) * ns + s) * kG + g] = ww;
+        L += ww * part_l[(uint64_t(pair) * ns + s) * kG + g];
+    }
+    ML[idx * 2] = M;
+    ML[idx * 2 + 1] = L;
+}
+
+// CTA = (pair, 256-entry chunk of the value codebooks): merge the split
+// histograms of the chunk, contract with the chunk's codebook rows and add the
+// partial output into acc[pair][g][d] (fp32 atomics in L2).
+__global__ void __launch_bounds__(512) lut_contract_kernel(const float* __restrict__ part_h, const float* __restrict__ w,
+                                                           uint32_t n_splits, const float* __restrict__ veff,
+                                                           uint64_t ventries, float* __restrict__ acc) {
+    __shared__ float hs[256][kG];
+    const uint32_t pair = blockIdx.y;
+    const uint64_t e0 = uint64_t(blockIdx.x) * 256;
+    const uint32_t ne = uint32_t((ventries - e0 < 256) ? (ventries - e0) : 256);
     const uint32_t ns = n_splits + 1;
-    if (threadIdx.x < kG) {
-        const uint32_t g = threadIdx.x;
-        float M = -INFINITY;
-        for (uint32_t s = 0; s < ns; ++s) M = fmaxf(M, part_m[(uint64_t(pair) * ns + s) * kG + g]);
-        float L = 0.f;
-        for (uint32_t s = 0; s < ns; ++s) {
-            const float m = part_m[(uint64_t(pair) * ns + s) * kG + g];
-            const float ww = (m > -INFINITY) ? __expf(m - M) : 0.f;
-            if (s < 64) w[s][g] = ww;
-            L += ww * part_l[(uint64_t(pair) * ns + s) * kG + g];
-        }
-        Ms[g] = M;
-        Ls[g] = L;
+    for (uint32_t i = threadIdx.x; i < 256 * kG; i += blockDim.x) {
+        const uint32_t e = i / kG, g = i % kG;
+        float v = 0.f;
+        if (e < ne)
+            for (uint32_t s = 0; s < n_splits; ++s)
+                v = fmaf(w[(uint64_t(pair) * ns + s) * kG + g],
+                         __ldg(part_h + ((uint64_t(pair) * n_splits + s) * ventries + e0) * kG + i), v);
+        hs[e][g] = v;
     }
     __syncthreads();
     const uint32_t g = threadIdx.x / kD, d = threadIdx.x % kD;
-    float acc = (g < kG && w[n_splits][g] > 0.f) ? w[n_splits][g] * part_o[(uint64_t(pair) * kG + g) * kD + d] : 0.f;
-    const uint32_t CH = 1024;  // entries per smem chunk
-    for (uint64_t e0 = 0; e0 < ventries; e0 += CH) {
-        const uint32_t ne = uint32_t((ventries - e0 < CH) ? (ventries - e0) : CH);
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < ne * kG; i += blockDim.x) {
-            const uint32_t gg = i % kG;
-            float v = 0.f;
-            for (uint32_t s = 0; s < n_splits; ++s)
-                v = fmaf(w[s][gg], part_h[((uint64_t(pair) * n_splits + s) * ventries + e0) * kG + i], v);
-            hs[i] = v;
-        }
-        __syncthreads();
-        if (g < kG)
-            for (uint32_t e = 0; e < ne; ++e) acc = fmaf(hs[e * kG + g], __ldg(veff + (e0 + e) * kD + d), acc);
-    }
-    if (g < kG) {
-        out[(uint64_t(pair) * kG + g) * kD + d] = acc / Ls[g];
-        if (d == 0 && lse) lse[uint64_t(pair) * kG + g] = Ms[g] + logf(Ls[g]);
-    }
+    float o = 0.f;
+    for (uint32_t e = 0; e < ne; ++e) o = fmaf(hs[e][g], __ldg(veff + (e0 + e) * kD + d), o);
+    atomicAdd(acc + (uint64_t(pair) * kG + g) * kD + d, o);
+}
+
+// out = (acc + w_raw * o_raw) / L, lse = M + log L
+__global__ void lut_finish_kernel(const float* __restrict__ acc, const float* __restrict__ part_o,
+                                  const float* __restrict__ w, const float* __restrict__ ML, uint32_t n_splits,
+                                  uint32_t n_pairs, float* __restrict__ out, float* __restrict__ lse) {
+    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // (pair, g, d)
+    if (idx >= uint64_t(n_pairs) * kG * kD) return;
+    const uint32_t pg = uint32_t(idx / kD), pair = pg / kG, g = pg % kG;
+    const float wr = w[(uint64_t(pair) * (n_splits + 1) + n_splits) * kG + g];
+    float v = acc[idx];
+    if (wr > 0.f) v = fmaf(wr, part_o[idx], v);
+    out[idx] = v / ML[pg * 2 + 1];
+    if (idx % kD == 0 && lse) lse[pg] = ML[pg * 2] + logf(ML[pg * 2 + 1]);
 }
 
 }  // namespace
@@ -440,14 +472,14 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     {
         ProfScope ps("attend_lut_build", s);
         LutArgs la{a.q_dev, ks.d_eff, ks.d_stages, ks.n, kent, float(scale), lut};
-        dim3 grid(unsigned((kent + 63) / 64), (a.n_pairs + 7) / 8);
-        const int lsmem = int(sizeof(float) * (8 * kG * kD + 64 * (kD + 1)));
+        dim3 grid(unsigned((kent + kLutEntries - 1) / kLutEntries), (a.n_pairs + 7) / 8);
+        const int lsmem = int(sizeof(float) * (8 * kG * kD + kLutEntries * (kD + 1)));
         static bool lattr = false;
         if (!lattr) {
             VQKV_CUDA(cudaFuncSetAttribute(lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem));
             lattr = true;
         }
-        lut_kernel<<<grid, 512, lsmem, s>>>(la, a.n_pairs);
+        lut_kernel<<<grid, 256, lsmem, s>>>(la, a.n_pairs);
         launch_check("lut_kernel");
     }
     {
@@ -471,9 +503,25 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     }
     {
         ProfScope ps("attend_combine", s);
-        lut_combine_kernel<<<a.n_pairs, 512, 1024 * kG * sizeof(float), s>>>(ph, po, pm, pl, n_splits, vs.d_eff, vent,
-                                                                            a.out_dev, a.lse_dev);
-        launch_check("lut_combine_kernel");
+        float *w = nullptr, *ML = nullptr, *acc = nullptr;
+        VQKV_CUDA(cudaMallocAsync(&w, sizeof(float) * a.n_pairs * (n_splits + 1) * kG, s));
+        VQKV_CUDA(cudaMallocAsync(&ML, sizeof(float) * a.n_pairs * kG * 2, s));
+        VQKV_CUDA(cudaMallocAsync(&acc, sizeof(float) * a.n_pairs * kG * kD, s));
+        VQKV_CUDA(cudaMemsetAsync(acc, 0, sizeof(float) * a.n_pairs * kG * kD, s));
+        lut_weights_kernel<<<(a.n_pairs * kG + 127) / 128, 128, 0, s>>>(pm, pl, n_splits, a.n_pairs, w, ML);
+        launch_check("lut_weights_kernel");
+        if (n_splits > 0) {
+            dim3 g2(unsigned((vent + 255) / 256), a.n_pairs);
+            lut_contract_kernel<<<g2, 512, 0, s>>>(ph, w, n_splits, vs.d_eff, vent, acc);
+            launch_check("lut_contract_kernel");
+        }
+        const uint64_t n = uint64_t(a.n_pairs) * kG * kD;
+        lut_finish_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(acc, po, w, ML, n_splits, a.n_pairs, a.out_dev,
+                                                                   a.lse_dev);
+        launch_check("lut_finish_kernel");
+        VQKV_CUDA(cudaFreeAsync(w, s));
+        VQKV_CUDA(cudaFreeAsync(ML, s));
+        VQKV_CUDA(cudaFreeAsync(acc, s));
     }
     VQKV_CUDA(cudaFreeAsync(lut, s));
     VQKV_CUDA(cudaFreeAsync(ph, s));
