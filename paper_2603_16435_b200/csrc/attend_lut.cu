@@ -37,8 +37,7 @@ constexpr int kD = 128;            // head dim
 constexpr int kAttThreads = 512;
 constexpr int kTokPerThread = 16;
 constexpr int kSplitTokens = kAttThreads * kTokPerThread;  // 8192
-constexpr int kGroupStages = 2;    // LUT stages per smem buffer (2 x 16 KB)
-constexpr uint32_t kLutBufBytes = 32768;
+constexpr int kGroupStages = 4;    // LUT stages per smem buffer (4 x 16 KB)
 constexpr float kHistScale = 262144.0f;  // 2^18 fixed point for p in [0, 1]
 
 struct LutArgs {
@@ -250,9 +249,7 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
 #pragma unroll
         for (int g = 0; g < kG; ++g) lg[k][g] = 0.f;
 
-    // ---- keys: LUT groups of kGroupStages stages, double-buffered bulk copies;
-    // each token's code words for group g+1 are loaded into registers while
-    // group g is scored, so L2 latency is off the critical path.
+    // ---- keys: LUT groups of kGroupStages stages, double-buffered bulk copies
     const uint32_t ngroups = (a.kn + kGroupStages - 1) / kGroupStages;
     if (threadIdx.x == 0) {
         ptx::mbar_init(ptx::smem_u32(&bars[0]), 1);
@@ -271,88 +268,48 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
         uint32_t off = 0;
         for (uint32_t s = s0; s < s1; ++s) {
             const uint32_t nb = a.kst[s].size * 16u;
-            ptx::bulk_g2s(ptx::smem_u32(lut_buf + b * kLutBufBytes + off), lutp + a.kst[s].eff_off / kD, nb, bar);
+            ptx::bulk_g2s(ptx::smem_u32(lut_buf + b * 65536 + off), lutp + a.kst[s].eff_off / kD, nb, bar);
             off += nb;
         }
     };
-    // two aligned 32-bit words covering the group's fields of token t (<= 32 + 31 bits)
-    auto load_words = [&](uint32_t grp, uint32_t (&w0)[kTokPerThread], uint32_t (&w1)[kTokPerThread],
-                          uint32_t (&sh)[kTokPerThread]) {
-        const uint32_t gbit = a.kst[grp * kGroupStages].bit_off;
-#pragma unroll
-        for (int k = 0; k < kTokPerThread; ++k) {
-            const uint64_t t = threadIdx.x + uint64_t(k) * kAttThreads;
-            uint32_t x0 = 0, x1 = 0, shv = 0;
-            if (t < nt) {
-                const uint64_t pos = (t0 + t) * a.krow_bits + gbit;
-                const uint8_t* p = kc + (pos >> 3);
-                const uintptr_t aw = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3);
-                shv = uint32_t((reinterpret_cast<uintptr_t>(p) - aw) * 8 + (pos & 7));
-                if (aw + 8 <= reinterpret_cast<uintptr_t>(a.kend)) {
-                    const uint32_t* q = reinterpret_cast<const uint32_t*>(aw);
-                    x0 = __ldg(q);
-                    x1 = __ldg(q + 1);
-                } else {
-                    const uint8_t* pb = reinterpret_cast<const uint8_t*>(aw);
-                    for (int b2 = 0; b2 < 4; ++b2) {
-                        if (pb + b2 < a.kend) x0 |= uint32_t(pb[b2]) << (8 * b2);
-                        if (pb + 4 + b2 < a.kend) x1 |= uint32_t(pb[4 + b2]) << (8 * b2);
-                    }
-                }
-            }
-            w0[k] = x0;
-            w1[k] = x1;
-            sh[k] = shv;
-        }
-    };
-    uint32_t cw0[kTokPerThread], cw1[kTokPerThread], csh[kTokPerThread];
-    load_words(0, cw0, cw1, csh);
     if (threadIdx.x == 0) issue(0);
     for (uint32_t grp = 0; grp < ngroups; ++grp) {
         if (threadIdx.x == 0 && grp + 1 < ngroups) issue(grp + 1);
-        uint32_t nw0[kTokPerThread], nw1[kTokPerThread], nsh[kTokPerThread];
-        if (grp + 1 < ngroups) load_words(grp + 1, nw0, nw1, nsh);
         ptx::mbar_wait(ptx::smem_u32(&bars[grp & 1]), (grp >> 1) & 1);
         const uint32_t s0 = grp * kGroupStages;
         const uint32_t s1 = min(a.kn, s0 + kGroupStages);
-        const float4* L = reinterpret_cast<const float4*>(lut_buf + (grp & 1) * kLutBufBytes);
+        const float4* L = reinterpret_cast<const float4*>(lut_buf + (grp & 1) * 65536);
         const uint32_t gbit = a.kst[s0].bit_off;
-        uint32_t loff[kGroupStages], lmask[kGroupStages], lofs[kGroupStages];
+        uint32_t loff[kGroupStages], lbits[kGroupStages], lofs[kGroupStages];
         uint32_t acc_off = 0;
 #pragma unroll
         for (int q = 0; q < kGroupStages; ++q) {
             const uint32_t s = s0 + q;
-            lmask[q] = (s < s1) ? ((1u << a.kst[s].bits) - 1u) : 0u;
+            lbits[q] = (s < s1) ? a.kst[s].bits : 0u;
             loff[q] = (s < s1) ? a.kst[s].bit_off - gbit : 0u;
             lofs[q] = acc_off;
             acc_off += (s < s1) ? a.kst[s].size : 0u;
         }
 #pragma unroll
         for (int k = 0; k < kTokPerThread; ++k) {
-            // field bits of this group, LSB first (funnel shift of the two words)
-            const uint32_t f = __funnelshift_r(cw0[k], cw1[k], csh[k]);
+            const uint64_t t = threadIdx.x + uint64_t(k) * kAttThreads;
+            if (t < nt) {
+                const uint64_t w = read_bits64(kc, (t0 + t) * a.krow_bits + gbit, a.kend);
 #pragma unroll
-            for (int q = 0; q < kGroupStages; ++q) {
-                const uint32_t z = (f >> loff[q]) & lmask[q];
-                const float4 v = L[lofs[q] + z];
-                lg[k][0] += v.x;
-                lg[k][1] += v.y;
-                lg[k][2] += v.z;
-                lg[k][3] += v.w;
-            }
-        }
-        if (grp + 1 < ngroups) {
-#pragma unroll
-            for (int k = 0; k < kTokPerThread; ++k) {
-                cw0[k] = nw0[k];
-                cw1[k] = nw1[k];
-                csh[k] = nsh[k];
+                for (int q = 0; q < kGroupStages; ++q) {
+                    if (lbits[q]) {
+                        const uint32_t z = uint32_t(w >> loff[q]) & ((1u << lbits[q]) - 1u);
+                        const float4 v = L[lofs[q] + z];
+                        lg[k][0] += v.x;
+                        lg[k][1] += v.y;
+                        lg[k][2] += v.z;
+                        lg[k][3] += v.w;
+                    }
+                }
             }
         }
         __syncthreads();  // buffer (grp & 1) is refilled two groups later
     }
-    // tokens beyond the split contribute nothing (their lookups used code 0 of
-    // zero words; they are masked out below)
 
     // ---- split max / p / l
     float mg[kG], lsum[kG];
@@ -488,7 +445,7 @@ bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const 
             bits += ks.stages[s].bits;
             bytes += ks.stages[s].size * 16u;
         }
-        if (bits > 32 || bytes > kLutBufBytes) return false;
+        if (bits > 56 || bytes > 65536) return false;
     }
     uint32_t ventries = 0;
     for (uint32_t s0 = 0; s0 < vs.n; s0 += 6) {
