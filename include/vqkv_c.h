@@ -153,6 +153,19 @@ typedef struct vqkv_attend_args {
 int vqkv_attend_decode(vqkv_stack_t key_stack, vqkv_stack_t value_stack, const vqkv_attend_args* args,
                        void* stream);
 
+/* HOST-buffer variants (copy in, compute, copy out; synchronous), used by the
+ * C++ mirror API (include/vqkv/*.hpp) whose signatures take host matrices. */
+/* quantize_batch of `rows` host rows (one stream), optional final residuals */
+int vqkv_quantize_rows_host(vqkv_stack_t stack, const float* xs_host, uint64_t rows, uint64_t search_block,
+                            uint8_t* payload_host, float* residual_norms_host, float* residuals_host);
+/* nearest_entry for one host vector against stage `stage` */
+int vqkv_nearest_host(vqkv_stack_t stack, uint32_t stage, const float* x_host, uint64_t search_block,
+                      uint32_t* index, float* distance);
+int vqkv_reconstruct_block_host(vqkv_stack_t stack, const uint8_t* payload_host, uint64_t rows,
+                                uint64_t begin, uint64_t end, float* out_host);
+int vqkv_attend_decode_host(vqkv_stack_t key_stack, vqkv_stack_t value_stack,
+                            const vqkv_attend_args* host_args);
+
 /* Merge G partial attention results of a sequence split (one per shard):
  * o = sum_g exp(lse_g - LSE) o_g, LSE = log sum_g exp(lse_g).
  * parts_o_dev fp32 [n_parts][rows][dv], parts_lse_dev fp32 [n_parts][rows]. */

@@ -73,6 +73,10 @@ _SIGS = {
     ),
     "vqkv_random_stack": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, P, P]),
     "vqkv_fnv1a64": (C.c_uint64, [P, C.c_uint64]),
+    "vqkv_quantize_rows_host": (C.c_int, [P, P, C.c_uint64, C.c_uint64, P, P, P]),
+    "vqkv_nearest_host": (C.c_int, [P, C.c_uint32, P, C.c_uint64, u32p, fp]),
+    "vqkv_reconstruct_block_host": (C.c_int, [P, P, C.c_uint64, C.c_uint64, C.c_uint64, P]),
+    "vqkv_attend_decode_host": (C.c_int, [P, P, C.POINTER(AttendArgs)]),
 }
 
 EXPORTED = tuple(_SIGS)

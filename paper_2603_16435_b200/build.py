@@ -84,5 +84,24 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_cpp_api.cpp")
+CPP_TEST_BIN = os.path.join(ROOT, "build", "test_cpp_api")
+
+
+def build_cpp_tests() -> str:
+    """C++ drop-in test program against include/vqkv/*.hpp, linked to the library."""
+    lib = build()
+    deps = [CPP_TEST_SRC, lib] + _headers()
+    if _stale(CPP_TEST_BIN, deps):
+        os.makedirs(os.path.dirname(CPP_TEST_BIN), exist_ok=True)
+        cmd = ["g++", "-O2", "-std=c++17", "-I" + os.path.join(ROOT, "include"), CPP_TEST_SRC, "-o", CPP_TEST_BIN,
+               "-L" + OUT_DIR, "-lvqkv_b200", "-Wl,-rpath," + OUT_DIR, "-Wl,-rpath,$ORIGIN/../paper_2603_16435_b200/lib"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"C++ test build failed:\n{r.stdout}\n{r.stderr}")
+    return CPP_TEST_BIN
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))
+    print(build_cpp_tests())

@@ -385,6 +385,126 @@ int vqkv_attend_decode(vqkv_stack_t ks, vqkv_stack_t vs, const vqkv_attend_args*
     });
 }
 
+int vqkv_quantize_rows_host(vqkv_stack_t s, const float* xs, uint64_t rows, uint64_t sb, uint8_t* payload, float* norms,
+                            float* residuals) {
+    return guard([&] {
+        check_stack(s);
+        need(sb >= 1, VQKV_INVALID_INPUT, "search_block must be >= 1");
+        if (rows == 0) return;
+        DeviceGuard g(s->device);
+        const uint64_t D = s->dim, pb = payload_bytes(s->row_bits, rows);
+        float *dx = nullptr, *dn = nullptr, *dr = nullptr;
+        uint8_t* dp = nullptr;
+        VQKV_CUDA(cudaMalloc(&dx, sizeof(float) * rows * D));
+        VQKV_CUDA(cudaMalloc(&dn, sizeof(float) * rows));
+        VQKV_CUDA(cudaMalloc(&dp, std::max<uint64_t>(pb, 16)));
+        if (residuals) VQKV_CUDA(cudaMalloc(&dr, sizeof(float) * rows * D));
+        VQKV_CUDA(cudaMemcpy(dx, xs, sizeof(float) * rows * D, cudaMemcpyHostToDevice));
+        quantize_device(*s, dx, 1, rows, sb, dp, dn, dr, nullptr);
+        if (pb && payload) VQKV_CUDA(cudaMemcpy(payload, dp, pb, cudaMemcpyDeviceToHost));
+        if (norms) VQKV_CUDA(cudaMemcpy(norms, dn, sizeof(float) * rows, cudaMemcpyDeviceToHost));
+        if (residuals) VQKV_CUDA(cudaMemcpy(residuals, dr, sizeof(float) * rows * D, cudaMemcpyDeviceToHost));
+        cudaFree(dx);
+        cudaFree(dn);
+        cudaFree(dp);
+        cudaFree(dr);
+    });
+}
+
+int vqkv_nearest_host(vqkv_stack_t s, uint32_t stage, const float* x, uint64_t sb, uint32_t* index, float* distance) {
+    return guard([&] {
+        check_stack(s);
+        need(stage < s->n, VQKV_INVALID_INPUT, "stage out of range");
+        need(sb >= 1, VQKV_INVALID_INPUT, "search_block must be >= 1");
+        DeviceGuard g(s->device);
+        float* dx = nullptr;
+        uint32_t* di = nullptr;
+        float* dd = nullptr;
+        VQKV_CUDA(cudaMalloc(&dx, sizeof(float) * s->dim));
+        VQKV_CUDA(cudaMalloc(&di, sizeof(uint32_t)));
+        VQKV_CUDA(cudaMalloc(&dd, sizeof(float)));
+        VQKV_CUDA(cudaMemcpy(dx, x, sizeof(float) * s->dim, cudaMemcpyHostToDevice));
+        launch_nearest(*s, stage, dx, 1, sb, di, dd, nullptr);
+        VQKV_CUDA(cudaMemcpy(index, di, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        VQKV_CUDA(cudaMemcpy(distance, dd, sizeof(float), cudaMemcpyDeviceToHost));
+        cudaFree(dx);
+        cudaFree(di);
+        cudaFree(dd);
+    });
+}
+
+int vqkv_reconstruct_block_host(vqkv_stack_t s, const uint8_t* payload, uint64_t rows, uint64_t begin, uint64_t end,
+                                float* out) {
+    return guard([&] {
+        check_stack(s);
+        if (begin > end || end > rows)
+            fail(VQKV_INVALID_INPUT, "row range [" + std::to_string(begin) + ", " + std::to_string(end) +
+                                         ") out of bounds for " + std::to_string(rows) + " rows");
+        if (end == begin) return;
+        DeviceGuard g(s->device);
+        const uint64_t pb = payload_bytes(s->row_bits, rows);
+        uint8_t* dp = nullptr;
+        float* dout = nullptr;
+        VQKV_CUDA(cudaMalloc(&dp, std::max<uint64_t>(pb, 16)));
+        VQKV_CUDA(cudaMalloc(&dout, sizeof(float) * (end - begin) * s->dim));
+        if (pb) VQKV_CUDA(cudaMemcpy(dp, payload, pb, cudaMemcpyHostToDevice));
+        launch_reconstruct(*s, dp, 1, rows, begin, end, dout, nullptr);
+        VQKV_CUDA(cudaMemcpy(out, dout, sizeof(float) * (end - begin) * s->dim, cudaMemcpyDeviceToHost));
+        int code = 0;
+        VQKV_CUDA(cudaMemcpy(&code, s->d_error, sizeof(int), cudaMemcpyDeviceToHost));
+        VQKV_CUDA(cudaMemset(s->d_error, 0, sizeof(int)));
+        cudaFree(dp);
+        cudaFree(dout);
+        if (code) fail(VQKV_INVALID_CODE, "code index out of range for its stage");
+    });
+}
+
+int vqkv_attend_decode_host(vqkv_stack_t ks, vqkv_stack_t vs, const vqkv_attend_args* h) {
+    return guard([&] {
+        check_stack(ks);
+        check_stack(vs);
+        need(h != nullptr, VQKV_INVALID_INPUT, "null args");
+        if (h->n_pairs == 0 || h->group == 0) return;
+        need(h->n_init + h->n_comp + h->n_local >= 1, VQKV_INVALID_STATE, "cannot attend over an empty cache");
+        DeviceGuard g(ks->device);
+        const uint64_t P = h->n_pairs, G = h->group, Dk = ks->dim, Dv = vs->dim;
+        std::vector<void*> owned;
+        auto up = [&](const void* src, uint64_t bytes) -> void* {
+            if (!src || bytes == 0) return nullptr;
+            void* d = nullptr;
+            VQKV_CUDA(cudaMalloc(&d, bytes + 16));  // slack: the fast path reads whole 8-byte words
+            VQKV_CUDA(cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice));
+            owned.push_back(d);
+            return d;
+        };
+        vqkv_attend_args d = *h;
+        d.q_dev = static_cast<const float*>(up(h->q_dev, sizeof(float) * P * G * Dk));
+        d.init_k_dev = static_cast<const float*>(up(h->init_k_dev, sizeof(float) * P * h->n_init * Dk));
+        d.init_v_dev = static_cast<const float*>(up(h->init_v_dev, sizeof(float) * P * h->n_init * Dv));
+        d.local_k_dev = static_cast<const float*>(up(h->local_k_dev, sizeof(float) * P * h->n_local * Dk));
+        d.local_v_dev = static_cast<const float*>(up(h->local_v_dev, sizeof(float) * P * h->n_local * Dv));
+        d.kcodes_dev = static_cast<const uint8_t*>(up(h->kcodes_dev, P * payload_bytes(ks->row_bits, h->n_comp)));
+        d.vcodes_dev = static_cast<const uint8_t*>(up(h->vcodes_dev, P * payload_bytes(vs->row_bits, h->n_comp)));
+        float *dout = nullptr, *dlse = nullptr;
+        VQKV_CUDA(cudaMalloc(&dout, sizeof(float) * P * G * Dv));
+        owned.push_back(dout);
+        if (h->lse_dev) {
+            VQKV_CUDA(cudaMalloc(&dlse, sizeof(float) * P * G));
+            owned.push_back(dlse);
+        }
+        d.out_dev = dout;
+        d.lse_dev = dlse;
+        need(d.q_dev != nullptr, VQKV_INVALID_INPUT, "null query");
+        need(d.n_init == 0 || (d.init_k_dev && d.init_v_dev), VQKV_INVALID_INPUT, "null init rows");
+        need(d.n_local == 0 || (d.local_k_dev && d.local_v_dev), VQKV_INVALID_INPUT, "null local rows");
+        need(d.n_comp == 0 || (d.kcodes_dev && d.vcodes_dev), VQKV_INVALID_INPUT, "null code payloads");
+        launch_attend(*ks, *vs, d, nullptr);
+        VQKV_CUDA(cudaMemcpy(h->out_dev, dout, sizeof(float) * P * G * Dv, cudaMemcpyDeviceToHost));
+        if (h->lse_dev) VQKV_CUDA(cudaMemcpy(h->lse_dev, dlse, sizeof(float) * P * G, cudaMemcpyDeviceToHost));
+        for (void* p : owned) cudaFree(p);
+    });
+}
+
 int vqkv_lse_combine(const float* o, const float* lse, uint32_t parts, uint64_t rows, uint32_t dv, float* out,
                      float* out_lse, void* stream) {
     return guard([&] {
