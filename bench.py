@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time per baseline sample")
+    ap.add_argument("--no-attention", action="store_true")
+    ap.add_argument("--attn-context", type=int, default=131072)
+    ap.add_argument("--attn-batch", type=int, default=16)
     return ap.parse_args()
 
 
@@ -223,6 +226,97 @@ def cpu_encode_rate(seconds_target=12.0, threads=None):
     return rate, threads, "; ".join(desc) + " (oracle port, one thread per (layer, head) stream, 1:1 K:V mix)"
 
 
+# --------------------------------------------------------------------------- attention
+def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
+    """configs[2]: decode step over a 128K-token compressed cache, batch 16, KV heads
+    sharded across ranks (each rank: its KV heads x all 16 sequences, no collective).
+    configs[4] (world > 1): one 1M-token sequence split over the ranks, partial
+    (o, lse) all-gathered over NCCL and merged by vqkv_lse_combine on every rank.
+    Compressed segments hold uniform random codes; raw rows and
+    queries are N(0, 1)."""
+    from paper_2603_16435_b200 import sharding
+
+    G = 4
+    ctx, B = args.attn_context, args.attn_batch
+    n_init, n_local = INIT_LEN, LOCAL_LEN
+    n_comp = ctx - n_init - n_local
+    heads = sharding.kv_head_shard(KV_HEADS, world, rank)
+    pairs = B * len(heads)
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    kb, vb = kst.device.payload_bytes(n_comp), vst.device.payload_bytes(n_comp)
+
+    def make(n_pairs, n_comp_, n_init_, n_local_):
+        kb_, vb_ = kst.device.payload_bytes(n_comp_), vst.device.payload_bytes(n_comp_)
+        # every 10-bit / 9-bit field of random bytes is a valid code (S = 2^bits)
+        kc = torch.randint(0, 256, (n_pairs, kb_ + 16), dtype=torch.uint8, device="cuda", generator=gen)[:, :kb_]
+        vc = torch.randint(0, 256, (n_pairs, vb_ + 16), dtype=torch.uint8, device="cuda", generator=gen)[:, :vb_]
+        kc, vc = kc.contiguous(), vc.contiguous()
+        f = lambda n: (torch.randn(n_pairs, n, D, device="cuda", generator=gen) if n else None)
+        return kc, vc, f(n_init_), f(n_init_), f(n_local_), f(n_local_)
+
+    kc, vc, ik, iv, lk, lv = make(pairs, n_comp, n_init, n_local)
+    q = torch.randn(pairs, G, D, device="cuda", generator=gen)
+    run = lambda: Dv.attend_decode(kst, vst, q, kc, vc, n_comp, ik, iv, lk, lv)
+    for _ in range(max(1, args.warmup)):
+        run()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    bytes_rank = pairs * (kb + vb) + pairs * (n_init + n_local) * D * 4 * 2 + pairs * G * D * 4 * 2
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = peaks.get("hbm_gbs", 6548.8)
+    out = {
+        "metric": "decode-attn cache tokens/s per layer-step (B*L/t)",
+        "config": {"workload": "configs[2]: decode step, 128K-token VQ-compressed cache, batch 16, 8 KV heads "
+                               f"sharded over {world} GPU(s), G=4", "context": ctx, "batch": B,
+                   "kv_heads_per_gpu": len(heads), "compressed_rows": n_comp, "raw_rows": n_init + n_local},
+        "value": B * ctx / (ms / 1e3), "unit": "tokens/s", "ms_per_layer_step": ms,
+        "roofline": {"bound": "hbm", "achieved": bytes_rank / (ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                     "frac": bytes_rank / (ms / 1e3) / 1e9 / hbm,
+                     "algorithmic": "88 B of codes per compressed token-pair + 1 KB per raw row (fp32 K+V)",
+                     "note": "on-chip bound: 56 LUT gathers + 16 histogram atomics per token-pair in shared memory"},
+    }
+    del kc, vc, ik, iv, lk, lv
+    if world > 1:
+        # configs[4]: 1M-token single sequence over the ranks, NCCL all-gather + LSE merge
+        total = 1 << 20
+        sh = sharding.sequence_shards(n_init, total - n_init - n_local, n_local, world)[rank]
+        nc = sh.comp[1] - sh.comp[0]
+        ni = sh.init[1] - sh.init[0]
+        nl = sh.local[1] - sh.local[0]
+        kc, vc, ik, iv, lk, lv = make(KV_HEADS, nc, ni, nl)
+        q1 = torch.randn(KV_HEADS, G, D, device="cuda", generator=torch.Generator(device="cuda").manual_seed(7))
+        part = lambda: Dv.attend_decode(kst, vst, q1, kc, vc, nc, ik, iv, lk, lv)
+        o_l, l_l = part()
+        sharding.gather_and_merge(o_l, l_l)
+        torch.cuda.synchronize()
+        barrier(world)
+        a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a0.record()
+        for _ in range(args.steps):
+            o_l, l_l = part()
+        a1.record()
+        for _ in range(args.steps):
+            sharding.gather_and_merge(o_l, l_l)
+        a2.record()
+        torch.cuda.synchronize()
+        kern = max_over_ranks(a0.elapsed_time(a1) / args.steps, world)
+        comb = max_over_ranks(a1.elapsed_time(a2) / args.steps, world)
+        out["sequence_split_1M"] = {
+            "config": f"configs[4]: 1 sequence x 1,048,576 tokens over {world} GPUs, 8 KV heads, G=4",
+            "tokens_per_gpu": sh.tokens, "ms_attention_per_layer_step": kern, "ms_nccl_lse_combine": comb,
+            "tokens_per_s": total / ((kern + comb) / 1e3),
+        }
+    return out
+
+
 # --------------------------------------------------------------------------- arms
 def run_reference(args, rank, world):
     if rank != 0:
@@ -339,6 +433,14 @@ def run_ours(args, rank, world, local):
             "ms_per_step": e_ms, "api": "vqkv_quantize_batch_host (pinned host buffers)",
         }
 
+    # ---- decode-step attention (configs[2]; configs[4] when world > 1)
+    attn = None
+    if not args.no_attention:
+        try:
+            attn = bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local)
+        except Exception as e:  # reported, never fatal for the headline line
+            attn = {"error": repr(e)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -372,6 +474,7 @@ def run_ours(args, rank, world, local):
             "e2e": e2e,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
+            "decode_attention": attn,
             "ambiguous_row_stage_frac_K": counters["ambiguous"] / max(1, counters["row_stages"]),
             "input_gen_s": t_gen,
         }

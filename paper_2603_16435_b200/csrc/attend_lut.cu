@@ -435,7 +435,6 @@ __global__ void lut_finish_kernel(const float* __restrict__ acc, const float* __
 bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a) {
     if (ks.dim != kD || vs.dim != kD || a.group != kG) return false;
     if (a.n_init + a.n_local > kSplitTokens) return false;
-    if ((a.n_comp + kSplitTokens - 1) / kSplitTokens + 1 > 64) return false;
     for (const auto& s : ks.stages)
         if (s.size > 1024 || s.bits > 10) return false;
     // 4 key stages per 64-bit read and LUT group (<= 64 KB)
