@@ -46,7 +46,7 @@ void launch_encode_exact_rows(const vqkv_stack_s& st, const float* xs, const uin
 namespace {
 
 constexpr int kThreads = 384;
-constexpr int kNB = 3;                    // codebook chunk ring depth
+constexpr int kNB = 2;                    // codebook chunk ring depth per tile
 constexpr uint32_t kChunkBytes = 36864;   // 128 entries x (128 + 16) fp16
 constexpr uint32_t kATileBytes = 36864;   // 128 rows x (128 + 16) fp16
 constexpr uint32_t kExtOff = 32768;       // the 16-wide K block (||e||^2 / row scale)
@@ -54,14 +54,14 @@ constexpr int kMaxChunks = 8;             // stages up to 1024 entries
 constexpr uint32_t kIdesc = ptx::idesc_f16_f32(128, 128);
 
 struct __align__(8) SmemCtl {
-    uint64_t b_full[kNB];
-    uint64_t b_empty[kNB];
+    uint64_t b_full[2][kNB];   // per tile: its own codebook-chunk ring
+    uint64_t b_empty[2][kNB];
     uint64_t acc_full[2];
     uint64_t acc_empty[2];
     uint64_t a_ready[2];
     uint32_t tmem_base;
 };
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + 2 * kATileBytes + kNB * kChunkBytes + sizeof(SmemCtl);
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + 2 * kATileBytes + 2 * kNB * kChunkBytes + sizeof(SmemCtl);
 
 // tree maximum of 32 values with 3-input FMNMX
 __device__ __forceinline__ float max32(const float (&v)[32]) {
@@ -122,6 +122,29 @@ __device__ __forceinline__ void store_a_chunk(uint8_t* a_tile, uint32_t i, int c
     }
 }
 
+// (pair, stage, chunk) job sequence of one tile slot of this CTA
+struct JobIter {
+    const StageInfo* st;
+    uint32_t n_stages;
+    uint64_t n_pairs, p;
+    uint32_t s = 0, c = 0, nch = 0;
+    bool done;
+    __device__ JobIter(const StageInfo* stg, uint32_t ns, uint64_t np) : st(stg), n_stages(ns), n_pairs(np), p(blockIdx.x) {
+        done = p >= n_pairs;
+        nch = done ? 0 : st[0].pad_size / 128;
+    }
+    __device__ void next() {
+        if (++c < nch) return;
+        c = 0;
+        if (++s == n_stages) {
+            s = 0;
+            p += gridDim.x;
+            done = p >= n_pairs;
+        }
+        if (!done) nch = st[s].pad_size / 128;
+    }
+};
+
 struct Tile {
     uint64_t stream, row0, nvalid;  // rows [row0, row0+nvalid) of `stream`
 };
@@ -143,9 +166,9 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                  uint32_t* __restrict__ exact_count, unsigned long long* __restrict__ counters, uint32_t dbg) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* a_tiles = smem;                                  // 2 x 32 KB
-    uint8_t* b_ring = smem + 2 * kATileBytes;                 // kNB x 32 KB
-    SmemCtl* ctl = reinterpret_cast<SmemCtl*>(b_ring + kNB * kChunkBytes);
+    uint8_t* a_tiles = smem;                                  // 2 x 36 KB
+    uint8_t* b_ring = smem + 2 * kATileBytes;                 // 2 tiles x kNB x 36 KB
+    SmemCtl* ctl = reinterpret_cast<SmemCtl*>(b_ring + 2 * kNB * kChunkBytes);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t tiles_per_stream = (rows + 127) / 128;
@@ -153,10 +176,11 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
     const uint64_t n_pairs = (n_tiles + 1) / 2;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kNB; ++i) {
-            ptx::mbar_init(ptx::smem_u32(&ctl->b_full[i]), 1);
-            ptx::mbar_init(ptx::smem_u32(&ctl->b_empty[i]), 1);
-        }
+        for (int t = 0; t < 2; ++t)
+            for (int i = 0; i < kNB; ++i) {
+                ptx::mbar_init(ptx::smem_u32(&ctl->b_full[t][i]), 1);
+                ptx::mbar_init(ptx::smem_u32(&ctl->b_empty[t][i]), 1);
+            }
         for (int t = 0; t < 2; ++t) {
             ptx::mbar_init(ptx::smem_u32(&ctl->acc_full[t]), 1);
             ptx::mbar_init(ptx::smem_u32(&ctl->acc_empty[t]), 128);
@@ -175,67 +199,65 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
+        // The two tiles advance independently (each has its own chunk ring), so
+        // one tile's stage-end work overlaps the other tile's MMAs.
         if (lane == 0) {
-            uint32_t buf = 0, ph = 0;
-            for (uint64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
-                for (uint32_t s = 0; s < n_stages; ++s) {
-                    const StageInfo si = stages[s];
-                    const uint32_t nch = si.pad_size / 128;
-                    const __half* src = eff16 + si.eff16_off;
-                    for (uint32_t c = 0; c < nch; ++c) {
-                        ptx::mbar_wait(ptx::smem_u32(&ctl->b_empty[buf]), ph ^ 1);
-                        const uint32_t bar = ptx::smem_u32(&ctl->b_full[buf]);
-                        ptx::mbar_arrive_expect_tx(bar, kChunkBytes);
-                        ptx::bulk_g2s(ptx::smem_u32(b_ring + buf * kChunkBytes), src + uint64_t(c) * (kChunkBytes / 2),
-                                      kChunkBytes, bar);
-                        if (++buf == kNB) {
-                            buf = 0;
-                            ph ^= 1;
-                        }
+            JobIter it[2] = {JobIter(stages, n_stages, n_pairs), JobIter(stages, n_stages, n_pairs)};
+            uint32_t slot[2] = {0, 0}, ph[2] = {0, 0};
+            while (!it[0].done || !it[1].done) {
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    if (it[t].done || !ptx::mbar_test(ptx::smem_u32(&ctl->b_empty[t][slot[t]]), ph[t] ^ 1)) continue;
+                    const uint32_t bar = ptx::smem_u32(&ctl->b_full[t][slot[t]]);
+                    ptx::mbar_arrive_expect_tx(bar, kChunkBytes);
+                    const __half* src = eff16 + stages[it[t].s].eff16_off + uint64_t(it[t].c) * (kChunkBytes / 2);
+                    ptx::bulk_g2s(ptx::smem_u32(b_ring + (t * kNB + slot[t]) * kChunkBytes), src, kChunkBytes, bar);
+                    if (++slot[t] == kNB) {
+                        slot[t] = 0;
+                        ph[t] ^= 1;
                     }
+                    it[t].next();
                 }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
+        // Serves whichever tile has its operands ready (non-blocking barrier tests).
         if (lane == 0) {
-            uint32_t buf = 0, ph = 0;
+            JobIter it[2] = {JobIter(stages, n_stages, n_pairs), JobIter(stages, n_stages, n_pairs)};
+            uint32_t slot[2] = {0, 0}, ph[2] = {0, 0};
             uint32_t e_ph[2] = {1, 1}, a_ph[2] = {0, 0};
             const uint32_t a_base = ptx::smem_u32(a_tiles), b_base = ptx::smem_u32(b_ring);
-            for (uint64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
-                for (uint32_t s = 0; s < n_stages; ++s) {
-                    const uint32_t nch = stages[s].pad_size / 128;
-                    for (uint32_t c = 0; c < nch; ++c) {
-                        ptx::mbar_wait(ptx::smem_u32(&ctl->b_full[buf]), ph);
-                        for (int t = 0; t < 2; ++t) {
-                            if (c == 0) {
-                                ptx::mbar_wait(ptx::smem_u32(&ctl->a_ready[t]), a_ph[t]);
-                                a_ph[t] ^= 1;
-                            }
-                            ptx::mbar_wait(ptx::smem_u32(&ctl->acc_empty[t]), e_ph[t]);
-                            e_ph[t] ^= 1;
-                            ptx::tc_fence_after();
-                            const uint32_t d = tmem + 128u * t;
+            while (!it[0].done || !it[1].done) {
 #pragma unroll
-                            for (int k = 0; k < 8; ++k) {
-                                const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32;
-                                const uint64_t ad = ptx::umma_desc_sw128(a_base + t * kATileBytes + koff);
-                                const uint64_t bd = ptx::umma_desc_sw128(b_base + buf * kChunkBytes + koff);
-                                ptx::mma_f16_ss(d, ad, bd, kIdesc, k > 0 ? 1u : 0u);
-                            }
-                            // + (-2^(sigma-1)) * (||e||^2 hi + lo): the score's norm term
-                            if (!(dbg & 1u))
-                                ptx::mma_f16_ss(d, ptx::umma_desc_noswz(a_base + t * kATileBytes + kExtOff, 128, 256),
-                                                ptx::umma_desc_noswz(b_base + buf * kChunkBytes + kExtOff, 128, 256),
-                                                kIdesc, 1u);
-                            ptx::mma_commit(ptx::smem_u32(&ctl->acc_full[t]));
-                        }
-                        ptx::mma_commit(ptx::smem_u32(&ctl->b_empty[buf]));
-                        if (++buf == kNB) {
-                            buf = 0;
-                            ph ^= 1;
-                        }
+                for (int t = 0; t < 2; ++t) {
+                    if (it[t].done) continue;
+                    if (!ptx::mbar_test(ptx::smem_u32(&ctl->b_full[t][slot[t]]), ph[t])) continue;
+                    if (it[t].c == 0 && !ptx::mbar_test(ptx::smem_u32(&ctl->a_ready[t]), a_ph[t])) continue;
+                    if (!ptx::mbar_test(ptx::smem_u32(&ctl->acc_empty[t]), e_ph[t])) continue;
+                    if (it[t].c == 0) a_ph[t] ^= 1;
+                    e_ph[t] ^= 1;
+                    ptx::tc_fence_after();
+                    const uint32_t d = tmem + 128u * t;
+                    const uint32_t bb = b_base + (t * kNB + slot[t]) * kChunkBytes;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32;
+                        const uint64_t ad = ptx::umma_desc_sw128(a_base + t * kATileBytes + koff);
+                        const uint64_t bd = ptx::umma_desc_sw128(bb + koff);
+                        ptx::mma_f16_ss(d, ad, bd, kIdesc, k > 0 ? 1u : 0u);
                     }
+                    // + (-2^(sigma-1)) * (||e||^2 hi + lo): the score's norm term
+                    if (!(dbg & 1u))
+                        ptx::mma_f16_ss(d, ptx::umma_desc_noswz(a_base + t * kATileBytes + kExtOff, 128, 256),
+                                        ptx::umma_desc_noswz(bb + kExtOff, 128, 256), kIdesc, 1u);
+                    ptx::mma_commit(ptx::smem_u32(&ctl->acc_full[t]));
+                    ptx::mma_commit(ptx::smem_u32(&ctl->b_empty[t][slot[t]]));
+                    if (++slot[t] == kNB) {
+                        slot[t] = 0;
+                        ph[t] ^= 1;
+                    }
+                    it[t].next();
                 }
             }
         }
