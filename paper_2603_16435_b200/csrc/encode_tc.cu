@@ -205,9 +205,11 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
             JobIter it[2] = {JobIter(stages, n_stages, n_pairs), JobIter(stages, n_stages, n_pairs)};
             uint32_t slot[2] = {0, 0}, ph[2] = {0, 0};
             while (!it[0].done || !it[1].done) {
+                bool issued = false;
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
                     if (it[t].done || !ptx::mbar_test(ptx::smem_u32(&ctl->b_empty[t][slot[t]]), ph[t] ^ 1)) continue;
+                    issued = true;
                     const uint32_t bar = ptx::smem_u32(&ctl->b_full[t][slot[t]]);
                     ptx::mbar_arrive_expect_tx(bar, kChunkBytes);
                     const __half* src = eff16 + stages[it[t].s].eff16_off + uint64_t(it[t].c) * (kChunkBytes / 2);
@@ -218,6 +220,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     }
                     it[t].next();
                 }
+                if (!issued) __nanosleep(200);
             }
         }
     } else if (warp == 1) {
@@ -229,6 +232,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
             uint32_t e_ph[2] = {1, 1}, a_ph[2] = {0, 0};
             const uint32_t a_base = ptx::smem_u32(a_tiles), b_base = ptx::smem_u32(b_ring);
             while (!it[0].done || !it[1].done) {
+                bool issued = false;
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
                     if (it[t].done) continue;
@@ -237,6 +241,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     if (!ptx::mbar_test(ptx::smem_u32(&ctl->acc_empty[t]), e_ph[t])) continue;
                     if (it[t].c == 0) a_ph[t] ^= 1;
                     e_ph[t] ^= 1;
+                    issued = true;
                     ptx::tc_fence_after();
                     const uint32_t d = tmem + 128u * t;
                     const uint32_t bb = b_base + (t * kNB + slot[t]) * kChunkBytes;
@@ -259,6 +264,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     }
                     it[t].next();
                 }
+                if (!issued) __nanosleep(64);
             }
         }
     } else if (warp >= 4) {
