@@ -65,6 +65,7 @@ _SIGS = {
     "vqkv_attend_decode": (C.c_int, [P, P, C.POINTER(AttendArgs), P]),
     "vqkv_lse_combine": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint32, P, P, P]),
     "vqkv_encode_counters": (C.c_int, [P, u64p]),
+    "vqkv_encode_phase_clocks": (C.c_int, [P, u64p]),
     "vqkv_profile_enable": (C.c_int, [C.c_int]),
     "vqkv_profile_collect": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), u64p]),
     "vqkv_generate_synthetic": (

@@ -51,6 +51,10 @@ constexpr uint32_t kChunkBytes = 36864;   // 128 entries x (128 + 16) fp16
 constexpr uint32_t kATileBytes = 36864;   // 128 rows x (128 + 16) fp16
 constexpr uint32_t kExtOff = 32768;       // the 16-wide K block (||e||^2 / row scale)
 constexpr int kMaxChunks = 8;             // stages up to 1024 entries
+// One N=128 MMA group per 128-entry chunk.  (Splitting a chunk into two N=64
+// halves to double-buffer the accumulator was measured slower: SS-mode MMAs
+// re-read A from shared memory per instruction, and at N=64 that pushes the
+// operand traffic to 192 B/clk, above the ~128 B/clk smem path.)
 constexpr uint32_t kIdesc = ptx::idesc_f16_f32(128, 128);
 
 struct __align__(8) SmemCtl {
@@ -197,74 +201,66 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
     ptx::tc_fence_after();
     const uint32_t tmem = ctl->tmem_base;
 
-    if (warp == 0) {
-        // ------------------------------------------------------------ producer
-        // The two tiles advance independently (each has its own chunk ring), so
-        // one tile's stage-end work overlaps the other tile's MMAs.
-        if (lane == 0) {
-            JobIter it[2] = {JobIter(stages, n_stages, n_pairs), JobIter(stages, n_stages, n_pairs)};
-            uint32_t slot[2] = {0, 0}, ph[2] = {0, 0};
-            while (!it[0].done || !it[1].done) {
-                bool issued = false;
-#pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    if (it[t].done || !ptx::mbar_test(ptx::smem_u32(&ctl->b_empty[t][slot[t]]), ph[t] ^ 1)) continue;
-                    issued = true;
-                    const uint32_t bar = ptx::smem_u32(&ctl->b_full[t][slot[t]]);
+    if (warp < 4) {
+        // One producer thread (warps 0 / 2) and one MMA-issuer thread (warps 1 / 3)
+        // per tile slot.  The two tiles advance independently (own chunk ring,
+        // own accumulator), so one tile's stage-end work overlaps the other
+        // tile's MMAs; every wait is a blocking mbarrier try_wait.
+        const uint32_t t = warp >> 1;
+        if (lane == 0 && (warp & 1) == 0) {
+            // ------------------------------------------------------------ producer
+            JobIter it(stages, n_stages, n_pairs);
+            uint32_t slot = 0, ph = 0;
+            while (!it.done) {
+                ptx::mbar_wait(ptx::smem_u32(&ctl->b_empty[t][slot]), ph ^ 1);
+                const uint32_t bar = ptx::smem_u32(&ctl->b_full[t][slot]);
+                if (dbg & 4u) {  // timing experiment only: no codebook traffic (wrong codes)
+                    ptx::mbar_arrive(bar);
+                } else {
                     ptx::mbar_arrive_expect_tx(bar, kChunkBytes);
-                    const __half* src = eff16 + stages[it[t].s].eff16_off + uint64_t(it[t].c) * (kChunkBytes / 2);
-                    ptx::bulk_g2s(ptx::smem_u32(b_ring + (t * kNB + slot[t]) * kChunkBytes), src, kChunkBytes, bar);
-                    if (++slot[t] == kNB) {
-                        slot[t] = 0;
-                        ph[t] ^= 1;
-                    }
-                    it[t].next();
+                    const __half* src = eff16 + stages[it.s].eff16_off + uint64_t(it.c) * (kChunkBytes / 2);
+                    ptx::bulk_g2s(ptx::smem_u32(b_ring + (t * kNB + slot) * kChunkBytes), src, kChunkBytes, bar);
                 }
-                if (!issued) __nanosleep(200);
+                if (++slot == kNB) {
+                    slot = 0;
+                    ph ^= 1;
+                }
+                it.next();
             }
-        }
-    } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
-        // Serves whichever tile has its operands ready (non-blocking barrier tests).
-        if (lane == 0) {
-            JobIter it[2] = {JobIter(stages, n_stages, n_pairs), JobIter(stages, n_stages, n_pairs)};
-            uint32_t slot[2] = {0, 0}, ph[2] = {0, 0};
-            uint32_t e_ph[2] = {1, 1}, a_ph[2] = {0, 0};
-            const uint32_t a_base = ptx::smem_u32(a_tiles), b_base = ptx::smem_u32(b_ring);
-            while (!it[0].done || !it[1].done) {
-                bool issued = false;
-#pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    if (it[t].done) continue;
-                    if (!ptx::mbar_test(ptx::smem_u32(&ctl->b_full[t][slot[t]]), ph[t])) continue;
-                    if (it[t].c == 0 && !ptx::mbar_test(ptx::smem_u32(&ctl->a_ready[t]), a_ph[t])) continue;
-                    if (!ptx::mbar_test(ptx::smem_u32(&ctl->acc_empty[t]), e_ph[t])) continue;
-                    if (it[t].c == 0) a_ph[t] ^= 1;
-                    e_ph[t] ^= 1;
-                    issued = true;
-                    ptx::tc_fence_after();
-                    const uint32_t d = tmem + 128u * t;
-                    const uint32_t bb = b_base + (t * kNB + slot[t]) * kChunkBytes;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32;
-                        const uint64_t ad = ptx::umma_desc_sw128(a_base + t * kATileBytes + koff);
-                        const uint64_t bd = ptx::umma_desc_sw128(bb + koff);
-                        ptx::mma_f16_ss(d, ad, bd, kIdesc, k > 0 ? 1u : 0u);
-                    }
-                    // + (-2^(sigma-1)) * (||e||^2 hi + lo): the score's norm term
-                    if (!(dbg & 1u))
-                        ptx::mma_f16_ss(d, ptx::umma_desc_noswz(a_base + t * kATileBytes + kExtOff, 128, 256),
-                                        ptx::umma_desc_noswz(bb + kExtOff, 128, 256), kIdesc, 1u);
-                    ptx::mma_commit(ptx::smem_u32(&ctl->acc_full[t]));
-                    ptx::mma_commit(ptx::smem_u32(&ctl->b_empty[t][slot[t]]));
-                    if (++slot[t] == kNB) {
-                        slot[t] = 0;
-                        ph[t] ^= 1;
-                    }
-                    it[t].next();
+        } else if (lane == 0) {
+            // ------------------------------------------------------------ MMA issuer
+            JobIter it(stages, n_stages, n_pairs);
+            uint32_t slot = 0, ph = 0, a_ph = 0, e_ph = 1;
+            const uint32_t a_base = ptx::smem_u32(a_tiles) + t * kATileBytes;
+            const uint32_t b_base = ptx::smem_u32(b_ring);
+            while (!it.done) {
+                ptx::mbar_wait(ptx::smem_u32(&ctl->b_full[t][slot]), ph);
+                if (it.c == 0) {
+                    ptx::mbar_wait(ptx::smem_u32(&ctl->a_ready[t]), a_ph);
+                    a_ph ^= 1;
                 }
-                if (!issued) __nanosleep(64);
+                const uint32_t bb = b_base + (t * kNB + slot) * kChunkBytes;
+                ptx::mbar_wait(ptx::smem_u32(&ctl->acc_empty[t]), e_ph);
+                e_ph ^= 1;
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + 128u * t;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32;
+                    ptx::mma_f16_ss(d, ptx::umma_desc_sw128(a_base + koff), ptx::umma_desc_sw128(bb + koff), kIdesc,
+                                    k > 0 ? 1u : 0u);
+                }
+                // + (-2^(sigma-1)) * (||e||^2 hi + lo): the score's norm term
+                if (!(dbg & 1u))
+                    ptx::mma_f16_ss(d, ptx::umma_desc_noswz(a_base + kExtOff, 128, 256),
+                                    ptx::umma_desc_noswz(bb + kExtOff, 128, 256), kIdesc, 1u);
+                ptx::mma_commit(ptx::smem_u32(&ctl->acc_full[t]));
+                ptx::mma_commit(ptx::smem_u32(&ctl->b_empty[t][slot]));
+                if (++slot == kNB) {
+                    slot = 0;
+                    ph ^= 1;
+                }
+                it.next();
             }
         }
     } else if (warp >= 4) {
@@ -281,6 +277,16 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         uint8_t* a_tile = a_tiles + t * kATileBytes;
         uint32_t f_ph = 0;
         unsigned long long n_amb = 0, n_rs = 0, n_rowstages = 0;
+        // dbg bit1: per-phase clock totals (lane 0 of each epilogue warp)
+        const bool clk_on = (dbg & 2u) && counters && lane == 0;
+        unsigned long long ck[6] = {0, 0, 0, 0, 0, 0};
+        long long ck_t = clock64();
+#define VQKV_PHASE(k)                          \
+    if (clk_on) {                              \
+        const long long now_ = clock64();      \
+        ck[k] += (unsigned long long)(now_ - ck_t); \
+        ck_t = now_;                           \
+    }
 
         for (uint64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
             const Tile tl = tile_of(2 * p + t, tiles_per_stream, rows, n_tiles);
@@ -353,6 +359,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(bar_aready);
             }
+            VQKV_PHASE(0)
 
             for (uint32_t s = 0; s < n_stages; ++s) {
                 const StageInfo si = stages[s];
@@ -376,7 +383,9 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
 #pragma unroll
                 for (int c = 0; c < kMaxChunks; ++c) {
                     if (c < int(nch)) {
+                        VQKV_PHASE(2)
                         ptx::mbar_wait(bar_full, f_ph);
+                        VQKV_PHASE(1)
                         f_ph ^= 1;
                         ptx::tc_fence_after();
 #pragma unroll
@@ -396,6 +405,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         }
                     }
                 }
+                VQKV_PHASE(2)
                 // ---- candidates {32a + b : mA[a] >= m - W, mB[b] >= m - W}
                 float m1 = -INFINITY;
 #pragma unroll
@@ -520,6 +530,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     }
                 }
                 if (valid && !exact_row) codes[grow * n_stages + s] = uint16_t(z);
+                VQKV_PHASE(3)
 
                 // ---- residual update r -= e_z (exact fp32) fused with the next stage's A tile
                 const bool last = (s + 1 == n_stages);
@@ -594,8 +605,12 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 R2 = R2n;
                 mx = mxn;
                 sigma = sigma_n;
+                VQKV_PHASE(4)
             }
         }
+#undef VQKV_PHASE
+        if (clk_on)
+            for (int k = 0; k < 5; ++k) atomicAdd(&counters[8 + k], ck[k]);
         if (counters) {
             atomicAdd(&counters[0], n_rowstages);
             if (n_amb) atomicAdd(&counters[1], n_amb);

@@ -23,13 +23,16 @@ f = lambda: Dv.attend_decode(ks, vs, q, kc, vc, n_comp, ik, iv, lk, lv)
 f(); torch.cuda.synchronize()
 from paper_2603_16435_b200 import _lib
 import ctypes
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+for _ in range(3): f()
+s.record()
+for _ in range(10): f()
+e.record(); torch.cuda.synchronize()
+ms = s.elapsed_time(e) / 10
 L = _lib.load(); L.vqkv_profile_enable(1)
 for nm in (b"attend_lut_build", b"attend", b"attend_combine"): L.vqkv_profile_collect(nm, None, None)
-s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-s.record()
 for _ in range(5): f()
-e.record(); torch.cuda.synchronize()
-ms = s.elapsed_time(e) / 5
+torch.cuda.synchronize()
 byts = pairs * (kb + vb) + pairs * (n_init + n_local) * D * 4 * 2
 print(f"attention ctx={ctx} pairs={pairs}: {ms:.3f} ms/layer-step, {B*ctx/ms/1e6:.2f} G cache-tok/s (B*L/t), "
       f"HBM-equiv {byts/ms/1e6:.1f} GB/s ({byts/ms/1e6/6548.8*100:.1f}% of 6548.8)")
