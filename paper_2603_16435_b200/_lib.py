@@ -12,7 +12,8 @@ import os
 from .errors import raise_for_status
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libvqkv_b200.so")
+# VQKV_LIB: development override (A/B timing of two builds on one box)
+LIB_PATH = os.environ.get("VQKV_LIB") or os.path.join(_PKG, "lib", "libvqkv_b200.so")
 
 P = C.c_void_p
 u8p = C.POINTER(C.c_uint8)

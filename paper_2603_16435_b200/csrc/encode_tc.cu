@@ -56,6 +56,8 @@ constexpr int kMaxChunks = 8;             // stages up to 1024 entries
 // re-read A from shared memory per instruction, and at N=64 that pushes the
 // operand traffic to 192 B/clk, above the ~128 B/clk smem path.)
 constexpr uint32_t kIdesc = ptx::idesc_f16_f32(128, 128);
+// register split: 128 x kCtlRegs + 256 x kEpiRegs <= 64K (launch allocation 168)
+constexpr uint32_t kCtlRegs = 40, kEpiRegs = 224;
 
 struct __align__(8) SmemCtl {
     uint64_t b_full[2][kNB];   // per tile: its own codebook-chunk ring
@@ -200,6 +202,11 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = ctl->tmem_base;
+    // control warpgroup (producer / MMA threads) hands registers to the epilogue
+    if (warp < 4)
+        ptx::reg_dealloc<kCtlRegs>();
+    else
+        ptx::reg_alloc<kEpiRegs>();
 
     if (warp < 4) {
         // One producer thread (warps 0 / 2) and one MMA-issuer thread (warps 1 / 3)
@@ -459,23 +466,16 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         }
                         const bool has = (j != 0xffffffffu);
                         const float4* e4 = reinterpret_cast<const float4*>(eff + si.eff_off + uint64_t(has ? j : 0) * 128);
-                        if (has) {  // one L2 round trip for the whole row, not one per chunk
+                        // the whole entry row and its norm in one L2 round trip
+                        const float sqj = has ? __ldg(sqn_s + j) : 0.f;
+                        float ev[128];
 #pragma unroll
-                            for (int l = 0; l < 4; ++l) ptx::prefetch_l1(e4 + 8 * l);
-                        }
+                        for (int kk = 0; kk < 16; ++kk) ptx::ldg256_na(reinterpret_cast<const float*>(e4) + 8 * kk, ev + 8 * kk);
                         float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
                         float r0[4] = {0.f, 0.f, 0.f, 0.f}, r1[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-                        for (int c4 = 0; c4 < 4; ++c4) {
-                            float v[32], ev[32];
 #pragma unroll
-                            for (int kk = 0; kk < 8; ++kk) {
-                                const float4 a = has ? __ldg(e4 + 8 * c4 + kk) : make_float4(0.f, 0.f, 0.f, 0.f);
-                                ev[4 * kk] = a.x;
-                                ev[4 * kk + 1] = a.y;
-                                ev[4 * kk + 2] = a.z;
-                                ev[4 * kk + 3] = a.w;
-                            }
+                        for (int c4 = 0; c4 < 4; ++c4) {
+                            float v[32];
                             ptx::tmem_ld32(t_res + 32u * c4, v);
                             ptx::tc_wait_ld();
 #pragma unroll
@@ -483,7 +483,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                                 float pp[4];
 #pragma unroll
                                 for (int l = 0; l < 4; ++l)
-                                    pp[l] = __fmul_rn(ev[4 * kk + l], __shfl_sync(0xffffffffu, v[4 * kk + l], o));
+                                    pp[l] = __fmul_rn(ev[32 * c4 + 4 * kk + l], __shfl_sync(0xffffffffu, v[4 * kk + l], o));
                                 g0 = __fadd_rn(g0, pp[0]);
                                 g1 = __fadd_rn(g1, pp[1]);
                                 g2 = __fadd_rn(g2, pp[2]);
@@ -506,7 +506,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                             } else {
                                 dot = __fadd_rn(__fadd_rn(g0, g2), __fadd_rn(g1, g3));
                             }
-                            const float sc = __fadd_rn(__fsub_rn(__ldg(sqn_s + j), __fmul_rn(2.0f, dot)), 0.0f);
+                            const float sc = __fadd_rn(__fsub_rn(sqj, __fmul_rn(2.0f, dot)), 0.0f);
                             if (sc < INFINITY) key = (uint64_t(f2ord(sc)) << 32) | j;  // NaN / +inf never win
                         }
                         // segmented min over consecutive lanes of the same owner
@@ -540,34 +540,16 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 const float4* ez4 = reinterpret_cast<const float4*>(eff + si.eff_off + uint64_t(z) * 128);
                 float R2n = 0.f, mxn = 0.f;
                 float n0[4] = {0.f, 0.f, 0.f, 0.f}, n1[4] = {0.f, 0.f, 0.f, 0.f};
-                float en[32];
+                float en[128];  // e_z in one L2 round trip
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const float4 a = __ldg(ez4 + kk);
-                    en[4 * kk] = a.x;
-                    en[4 * kk + 1] = a.y;
-                    en[4 * kk + 2] = a.z;
-                    en[4 * kk + 3] = a.w;
-                }
+                for (int kk = 0; kk < 16; ++kk) ptx::ldg256_na(reinterpret_cast<const float*>(ez4) + 8 * kk, en + 8 * kk);
 #pragma unroll
                 for (int c4 = 0; c4 < 4; ++c4) {
-                    float ec[32], v[32];
-#pragma unroll
-                    for (int k = 0; k < 32; ++k) ec[k] = en[k];
-                    if (c4 < 3) {
-#pragma unroll
-                        for (int kk = 0; kk < 8; ++kk) {
-                            const float4 a = __ldg(ez4 + 8 * (c4 + 1) + kk);
-                            en[4 * kk] = a.x;
-                            en[4 * kk + 1] = a.y;
-                            en[4 * kk + 2] = a.z;
-                            en[4 * kk + 3] = a.w;
-                        }
-                    }
+                    float v[32];
                     ptx::tmem_ld32(t_res + 32u * c4, v);
                     ptx::tc_wait_ld();
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) v[k] = __fsub_rn(v[k], ec[k]);
+                    for (int k = 0; k < 32; ++k) v[k] = __fsub_rn(v[k], en[32 * c4 + k]);
                     ptx::tmem_st32(t_res + 32u * c4, v);
                     if (!last) {
 #pragma unroll

@@ -132,6 +132,16 @@ int vqkv_stack_create(int device, int kind, uint32_t n_stages, const uint32_t* s
         need(dim >= 1, VQKV_INVALID_INPUT, "codebook must have S >= 1 and D >= 1");
         need(sizes != nullptr && entries != nullptr, VQKV_INVALID_INPUT, "null sizes/entries");
         auto st = std::make_unique<vqkv_stack_s>();
+        {
+            // the encoder's stream-ordered scratch (cudaMallocAsync) stays mapped
+            // between calls instead of being unmapped at every synchronization
+            DeviceGuard g(device);
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+                uint64_t keep = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+        }
         st->device = device;
         st->kind = kind;
         st->n = n_stages;
