@@ -132,16 +132,6 @@ int vqkv_stack_create(int device, int kind, uint32_t n_stages, const uint32_t* s
         need(dim >= 1, VQKV_INVALID_INPUT, "codebook must have S >= 1 and D >= 1");
         need(sizes != nullptr && entries != nullptr, VQKV_INVALID_INPUT, "null sizes/entries");
         auto st = std::make_unique<vqkv_stack_s>();
-        {
-            // the encoder's stream-ordered scratch (cudaMallocAsync) stays mapped
-            // between calls instead of being unmapped at every synchronization
-            DeviceGuard g(device);
-            cudaMemPool_t pool;
-            if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-                uint64_t keep = ~0ull;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-            }
-        }
         st->device = device;
         st->kind = kind;
         st->n = n_stages;
@@ -173,6 +163,15 @@ int vqkv_stack_create(int device, int kind, uint32_t n_stages, const uint32_t* s
             for (uint64_t i = 0; i < uint64_t(n_stages) * dim * dim; ++i)
                 need(std::isfinite(projections[i]), VQKV_INVALID_INPUT, "codebook contains non-finite values");
         DeviceGuard g(device);
+        {
+            // the encoder's stream-ordered scratch (cudaMallocAsync) stays mapped
+            // between calls instead of being unmapped at every synchronization
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+                uint64_t keep = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+        }
         VQKV_CUDA(cudaMalloc(&st->d_stages, sizeof(StageInfo) * n_stages));
         VQKV_CUDA(cudaMemcpy(st->d_stages, st->stages.data(), sizeof(StageInfo) * n_stages, cudaMemcpyHostToDevice));
         VQKV_CUDA(cudaMalloc(&st->d_error, sizeof(int)));
