@@ -186,9 +186,10 @@ int vqkv_encode_counters(vqkv_stack_t stack, uint64_t* counters3);
 /* Diagnostics: with VQKV_DBG bit 1 set, the tensor-core encoder sums clock64
  * cycles per epilogue phase (lane 0 of every epilogue warp): [0] tile
  * prologue, [1] waiting for accumulators, [2] chunk max trees, [3] candidate
- * selection + exact rescoring, [4] residual update + next A tile; [5] the
- * number of rescored (row, candidate) pairs.  Synchronizes. */
-int vqkv_encode_phase_clocks(vqkv_stack_t stack, uint64_t* out6);
+ * selection, [4] residual update + next A tile, [5] rescoring pass set-up,
+ * [6] rescoring loads + dot products, [7] rescoring min-reduction, [8] code
+ * store; [9] the number of rescored (row, candidate) pairs.  Synchronizes. */
+int vqkv_encode_phase_clocks(vqkv_stack_t stack, uint64_t* out10);
 /* number of kernel launches issued by the library since load (all threads) */
 uint64_t vqkv_launch_count(void);
 /* Kernel timing hooks: when enabled, the library records a CUDA event pair on

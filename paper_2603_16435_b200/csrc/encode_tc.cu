@@ -58,6 +58,7 @@ constexpr int kMaxChunks = 8;             // stages up to 1024 entries
 constexpr uint32_t kIdesc = ptx::idesc_f16_f32(128, 128);
 // register split: 128 x kCtlRegs + 256 x kEpiRegs <= 64K (launch allocation 168)
 constexpr uint32_t kCtlRegs = 40, kEpiRegs = 224;
+constexpr uint32_t kSleepNs = 1000000;  // control-thread barrier suspend hint
 
 struct __align__(8) SmemCtl {
     uint64_t b_full[2][kNB];   // per tile: its own codebook-chunk ring
@@ -219,7 +220,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
             JobIter it(stages, n_stages, n_pairs);
             uint32_t slot = 0, ph = 0;
             while (!it.done) {
-                ptx::mbar_wait(ptx::smem_u32(&ctl->b_empty[t][slot]), ph ^ 1);
+                ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->b_empty[t][slot]), ph ^ 1, kSleepNs);
                 const uint32_t bar = ptx::smem_u32(&ctl->b_full[t][slot]);
                 if (dbg & 4u) {  // timing experiment only: no codebook traffic (wrong codes)
                     ptx::mbar_arrive(bar);
@@ -241,13 +242,13 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
             const uint32_t a_base = ptx::smem_u32(a_tiles) + t * kATileBytes;
             const uint32_t b_base = ptx::smem_u32(b_ring);
             while (!it.done) {
-                ptx::mbar_wait(ptx::smem_u32(&ctl->b_full[t][slot]), ph);
+                ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->b_full[t][slot]), ph, kSleepNs);
                 if (it.c == 0) {
-                    ptx::mbar_wait(ptx::smem_u32(&ctl->a_ready[t]), a_ph);
+                    ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->a_ready[t]), a_ph, kSleepNs);
                     a_ph ^= 1;
                 }
                 const uint32_t bb = b_base + (t * kNB + slot) * kChunkBytes;
-                ptx::mbar_wait(ptx::smem_u32(&ctl->acc_empty[t]), e_ph);
+                ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->acc_empty[t]), e_ph, kSleepNs);
                 e_ph ^= 1;
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + 128u * t;
@@ -286,7 +287,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         unsigned long long n_amb = 0, n_rs = 0, n_rowstages = 0;
         // dbg bit1: per-phase clock totals (lane 0 of each epilogue warp)
         const bool clk_on = (dbg & 2u) && counters && lane == 0;
-        unsigned long long ck[6] = {0, 0, 0, 0, 0, 0};
+        unsigned long long ck[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         long long ck_t = clock64();
 #define VQKV_PHASE(k)                          \
     if (clk_on) {                              \
@@ -432,6 +433,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
 #pragma unroll
                     for (int l = 0; l < 4; ++l) ptx::prefetch_l1(ez + 32 * l);
                 }
+                VQKV_PHASE(3)
                 if (__any_sync(0xffffffffu, amb)) {
                     // ---- warp-cooperative exact rescoring in the reference's fp32 order
                     // (codebook.cpp:166-172).  The (row, candidate) items of all lanes
@@ -464,6 +466,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                             j = 32u * uint32_t(__fns(CAo, 0, int(li / nbo) + 1)) + uint32_t(__fns(CBo, 0, int(li % nbo) + 1));
                             if (j >= si.size) j = 0xffffffffu;
                         }
+                        VQKV_PHASE(5)
                         const bool has = (j != 0xffffffffu);
                         const float4* e4 = reinterpret_cast<const float4*>(eff + si.eff_off + uint64_t(has ? j : 0) * 128);
                         // the whole entry row and its norm in one L2 round trip
@@ -495,6 +498,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                                 }
                             }
                         }
+                        VQKV_PHASE(6)
                         unsigned long long key = ~0ull;
                         if (has) {
                             const bool one = any_one && (search_block == 1 || j + 1 == si.size);
@@ -519,6 +523,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         const int head = int(P) - int(base);
                         const unsigned long long got = __shfl_sync(0xffffffffu, key, head < 0 ? 0 : (head > 31 ? 31 : head));
                         if (amb && P + cnt > base && P < base + 32 && got < best) best = got;
+                        VQKV_PHASE(7)
                     }
                     if (amb) {
                         z = (best == ~0ull) ? 0u : uint32_t(best & 0xffffffffu);
@@ -530,7 +535,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     }
                 }
                 if (valid && !exact_row) codes[grow * n_stages + s] = uint16_t(z);
-                VQKV_PHASE(3)
+                VQKV_PHASE(8)
 
                 // ---- residual update r -= e_z (exact fp32) fused with the next stage's A tile
                 const bool last = (s + 1 == n_stages);
@@ -592,7 +597,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         }
 #undef VQKV_PHASE
         if (clk_on)
-            for (int k = 0; k < 5; ++k) atomicAdd(&counters[8 + k], ck[k]);
+            for (int k = 0; k < 9; ++k) atomicAdd(&counters[8 + k], ck[k]);
         if (counters) {
             atomicAdd(&counters[0], n_rowstages);
             if (n_amb) atomicAdd(&counters[1], n_amb);

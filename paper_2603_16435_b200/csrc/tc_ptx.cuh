@@ -33,6 +33,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
+// try_wait with a suspend-time hint (ns): a waiting thread is parked until the
+// phase completes (or the hint expires) instead of re-polling; used by the
+// single-thread producer / MMA roles that would otherwise spin on their barriers
+// and take issue slots from the epilogue warps sharing their scheduler
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity), "r"(ns)
+        : "memory");
+}
+
 // non-blocking: has the phase with parity `parity` completed?
 __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
     uint32_t ok;

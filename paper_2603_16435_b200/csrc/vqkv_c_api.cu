@@ -176,8 +176,8 @@ int vqkv_stack_create(int device, int kind, uint32_t n_stages, const uint32_t* s
         VQKV_CUDA(cudaMemcpy(st->d_stages, st->stages.data(), sizeof(StageInfo) * n_stages, cudaMemcpyHostToDevice));
         VQKV_CUDA(cudaMalloc(&st->d_error, sizeof(int)));
         VQKV_CUDA(cudaMemset(st->d_error, 0, sizeof(int)));
-        VQKV_CUDA(cudaMalloc(&st->d_counters, sizeof(unsigned long long) * 16));
-        VQKV_CUDA(cudaMemset(st->d_counters, 0, sizeof(unsigned long long) * 16));
+        VQKV_CUDA(cudaMalloc(&st->d_counters, sizeof(unsigned long long) * 32));
+        VQKV_CUDA(cudaMemset(st->d_counters, 0, sizeof(unsigned long long) * 32));
         stack_build_device(*st, entries, projections);
         *out = st.release();
     });
@@ -271,10 +271,10 @@ int vqkv_encode_phase_clocks(vqkv_stack_t s, uint64_t* c) {
         check_stack(s);
         DeviceGuard g(s->device);
         VQKV_CUDA(cudaDeviceSynchronize());
-        unsigned long long h[16];
+        unsigned long long h[32];
         VQKV_CUDA(cudaMemcpy(h, s->d_counters, sizeof(h), cudaMemcpyDeviceToHost));
-        for (int i = 0; i < 5; ++i) c[i] = h[8 + i];
-        c[5] = h[3];
+        for (int i = 0; i < 9; ++i) c[i] = h[8 + i];
+        c[9] = h[3];
     });
 }
 
