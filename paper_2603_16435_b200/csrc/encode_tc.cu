@@ -396,21 +396,22 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         VQKV_PHASE(1)
                         f_ph ^= 1;
                         ptx::tc_fence_after();
+                        // all 128 columns in flight at once, one wait, then the
+                        // accumulator goes back to the MMA issuer before the max trees
+                        float v0[32], v1[32], v2[32], v3[32];
+                        ptx::tmem_ld32(t_acc, v0);
+                        ptx::tmem_ld32(t_acc + 32u, v1);
+                        ptx::tmem_ld32(t_acc + 64u, v2);
+                        ptx::tmem_ld32(t_acc + 96u, v3);
+                        ptx::tc_wait_ld();
+                        ptx::tc_fence_before();
+                        ptx::mbar_arrive(bar_empty);
+                        mA[4 * c] = max32(v0);
+                        mA[4 * c + 1] = max32(v1);
+                        mA[4 * c + 2] = max32(v2);
+                        mA[4 * c + 3] = max32(v3);
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            float v0[32], v1[32];
-                            ptx::tmem_ld32(t_acc + 64u * h, v0);
-                            ptx::tmem_ld32(t_acc + 64u * h + 32u, v1);
-                            ptx::tc_wait_ld();
-                            if (h == 1) {
-                                ptx::tc_fence_before();
-                                ptx::mbar_arrive(bar_empty);
-                            }
-                            mA[4 * c + 2 * h] = max32(v0);
-                            mA[4 * c + 2 * h + 1] = max32(v1);
-#pragma unroll
-                            for (int b = 0; b < 32; ++b) mB[b] = ptx::fmax3(mB[b], v0[b], v1[b]);
-                        }
+                        for (int b = 0; b < 32; ++b) mB[b] = ptx::fmax3(mB[b], ptx::fmax3(v0[b], v1[b], v2[b]), v3[b]);
                     }
                 }
                 VQKV_PHASE(2)
