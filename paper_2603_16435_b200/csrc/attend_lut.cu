@@ -37,6 +37,8 @@ constexpr int kD = 128;            // head dim
 constexpr int kAttThreads = 512;
 constexpr int kTokPerThread = 16;
 constexpr int kSplitTokens = kAttThreads * kTokPerThread;  // 8192
+constexpr int kMaxVStages = 64;    // value stages supported by the LUT path
+constexpr int kKeyBatch = 4;      // key tokens whose code loads are in flight together
 constexpr int kGroupStages = 4;    // LUT stages per smem buffer (4 x 16 KB)
 constexpr float kHistScale = 262144.0f;  // 2^18 fixed point for p in [0, 1]
 
@@ -117,6 +119,9 @@ __device__ __forceinline__ uint64_t read_bits64(const uint8_t* base, uint64_t po
     uint64_t extra = (p + 8 < end) ? uint64_t(p[8]) : 0ull;
     return bsh ? ((v >> bsh) | (extra << (64 - bsh))) : v;
 }
+
+// always-valid 16 bytes: the target of clamped (ignored) loads in the batched key loop
+__device__ const uint64_t g_zero16[2] = {0ull, 0ull};
 
 struct MainArgs {
     const float* q;
@@ -290,20 +295,42 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
             lofs[q] = acc_off;
             acc_off += (s < s1) ? a.kst[s].size : 0u;
         }
+        // kKeyBatch tokens per batch: all their code-word loads are issued before any
+        // is used (branch-free: out-of-range tokens and the last bytes of the buffer
+        // read a dummy word; the rare buffer-tail tokens take read_bits64's careful path)
 #pragma unroll
-        for (int k = 0; k < kTokPerThread; ++k) {
-            const uint64_t t = threadIdx.x + uint64_t(k) * kAttThreads;
-            if (t < nt) {
-                const uint64_t w = read_bits64(kc, (t0 + t) * a.krow_bits + gbit, a.kend);
+        for (int kb = 0; kb < kTokPerThread; kb += kKeyBatch) {
+            uint64_t lo[kKeyBatch], hi[kKeyBatch];
+            uint32_t sh[kKeyBatch];
+            bool fast[kKeyBatch];
 #pragma unroll
-                for (int q = 0; q < kGroupStages; ++q) {
-                    if (lbits[q]) {
-                        const uint32_t z = uint32_t(w >> loff[q]) & ((1u << lbits[q]) - 1u);
-                        const float4 v = L[lofs[q] + z];
-                        lg[k][0] += v.x;
-                        lg[k][1] += v.y;
-                        lg[k][2] += v.z;
-                        lg[k][3] += v.w;
+            for (int k = 0; k < kKeyBatch; ++k) {
+                const uint64_t t = threadIdx.x + uint64_t(kb + k) * kAttThreads;
+                const uint64_t pos = (t0 + t) * a.krow_bits + gbit;
+                const uint8_t* pb = kc + (pos >> 3);
+                const uintptr_t al = reinterpret_cast<uintptr_t>(pb) & ~uintptr_t(7);
+                sh[k] = uint32_t((reinterpret_cast<uintptr_t>(pb) - al) * 8 + (pos & 7));
+                fast[k] = (t < nt) && (al + 16 <= reinterpret_cast<uintptr_t>(a.kend));
+                const uint64_t* q = fast[k] ? reinterpret_cast<const uint64_t*>(al) : g_zero16;
+                lo[k] = __ldg(q);
+                hi[k] = __ldg(q + 1);
+            }
+#pragma unroll
+            for (int k = 0; k < kKeyBatch; ++k) {
+                const uint64_t t = threadIdx.x + uint64_t(kb + k) * kAttThreads;
+                if (t < nt) {
+                    uint64_t w = sh[k] ? ((lo[k] >> sh[k]) | (hi[k] << (64 - sh[k]))) : lo[k];
+                    if (!fast[k]) w = read_bits64(kc, (t0 + t) * a.krow_bits + gbit, a.kend);
+#pragma unroll
+                    for (int q = 0; q < kGroupStages; ++q) {
+                        if (lbits[q]) {
+                            const uint32_t z = uint32_t(w >> loff[q]) & ((1u << lbits[q]) - 1u);
+                            const float4 v = L[lofs[q] + z];
+                            lg[kb + k][0] += v.x;
+                            lg[kb + k][1] += v.y;
+                            lg[kb + k][2] += v.z;
+                            lg[kb + k][3] += v.w;
+                        }
                     }
                 }
             }
@@ -337,23 +364,34 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
     // ---- values: int32 fixed-point histograms H[s][j][g] in smem (reuses the LUT area)
     uint32_t* H = reinterpret_cast<uint32_t*>(smem_raw);
     const uint32_t hsz = uint32_t(a.ventries) * kG;
+    // value-stage descriptors, read once per CTA: entry offset << 16 | bit offset
+    // within the stage's 6-stage window << 5 | bits; window start bits per group
+    uint32_t* vd = reinterpret_cast<uint32_t*>(smem_raw + 131072 + 64 + 256);
+    uint32_t* vgb = vd + kMaxVStages;
     for (uint32_t i = threadIdx.x; i < hsz; i += blockDim.x) H[i] = 0u;
+    if (threadIdx.x < a.vn) {
+        const StageInfo si = a.vst[threadIdx.x];
+        const uint32_t first = (threadIdx.x / 6u) * 6u;
+        vd[threadIdx.x] = uint32_t(si.eff_off / kD) << 16 | (si.bit_off - a.vst[first].bit_off) << 5 | si.bits;
+        if (threadIdx.x == first) vgb[threadIdx.x / 6u] = si.bit_off;
+    }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kTokPerThread; ++k) {
         const uint64_t t = threadIdx.x + uint64_t(k) * kAttThreads;
-        if (t < nt) {
-            uint32_t P[kG];
+        uint32_t P[kG];
 #pragma unroll
-            for (int g = 0; g < kG; ++g) P[g] = __float2uint_rn(lg[k][g] * kHistScale);
+        for (int g = 0; g < kG; ++g) P[g] = __float2uint_rn(lg[k][g] * kHistScale);
+        // tokens whose weights all round to 0 in the 2^-18 fixed point add nothing
+        if (t < nt && (P[0] | P[1] | P[2] | P[3]) != 0u) {
             const uint64_t rb = (t0 + t) * a.vrow_bits;
-            for (uint32_t s0 = 0; s0 < a.vn; s0 += 6) {  // <= 6 x 9-bit fields per 64-bit read
-                const uint64_t w = read_bits64(vc, rb + a.vst[s0].bit_off, a.vend);
+            for (uint32_t s0 = 0; s0 < a.vn; s0 += 6) {  // <= 6 fields per 64-bit window
+                const uint64_t w = read_bits64(vc, rb + vgb[s0 / 6u], a.vend);
                 const uint32_t s1 = min(a.vn, s0 + 6u);
                 for (uint32_t s = s0; s < s1; ++s) {
-                    const StageInfo si = a.vst[s];
-                    const uint32_t z = uint32_t(w >> (si.bit_off - a.vst[s0].bit_off)) & ((1u << si.bits) - 1u);
-                    uint32_t* h = H + (si.eff_off / kD + z) * kG;
+                    const uint32_t d = vd[s];
+                    const uint32_t z = uint32_t(w >> ((d >> 5) & 63u)) & ((1u << (d & 31u)) - 1u);
+                    uint32_t* h = H + ((d >> 16) + z) * kG;
 #pragma unroll
                     for (int g = 0; g < kG; ++g)
                         if (P[g]) atomicAdd(h + g, P[g]);
@@ -452,7 +490,9 @@ bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const 
         for (uint32_t s = s0; s < std::min(vs.n, s0 + 6u); ++s) bits += vs.stages[s].bits;
         if (bits > 56) return false;
     }
+    if (vs.n > uint32_t(kMaxVStages)) return false;
     for (const auto& s : vs.stages) ventries += s.size;
+    if (ventries > 65535) return false;
     if (uint64_t(ventries) * kG * 4 > 131072) return false;
     return true;
 }
