@@ -7,6 +7,7 @@
 // +inf), and the residual update / final norm use the reference's fp32 ops.
 // It serves any D (the tensor-core encoder covers D == 128) and rows whose
 // input is non-finite.  One warp per row; lanes split the codebook entries.
+#include <algorithm>
 #include "vqkv_internal.cuh"
 
 namespace vqkv_dev {
@@ -102,6 +103,48 @@ __global__ void pack_kernel(const uint16_t* __restrict__ codes, const StageInfo*
     payload[idx] = uint8_t(byte);
 }
 
+// Fast path for byte-aligned rows (row_bits % 8 == 0, e.g. K 560 bits, V 144):
+// a CTA packs 128 rows of one stream.  u16 codes are staged in smem with
+// coalesced loads, each thread packs its row LSB-first into a smem byte tile,
+// and the tile (contiguous in the payload) is written with coalesced stores.
+constexpr int kPackRows = 128;
+constexpr int kPackMaxStages = 128;
+__global__ void __launch_bounds__(kPackRows) pack_rows_kernel(const uint16_t* __restrict__ codes,
+                                                               const StageInfo* __restrict__ stages, uint32_t n_stages,
+                                                               uint32_t row_bytes, uint64_t rows,
+                                                               uint64_t stream_bytes, uint8_t* __restrict__ payload) {
+    extern __shared__ uint8_t psm[];
+    uint8_t* sbits = psm;                                                  // [kPackMaxStages]
+    uint16_t* sc = reinterpret_cast<uint16_t*>(psm + kPackMaxStages);      // [kPackRows][n_stages]
+    uint8_t* so = psm + kPackMaxStages + kPackRows * n_stages * 2;          // [kPackRows][row_bytes]
+    const uint64_t stream = blockIdx.y;
+    const uint64_t r0 = uint64_t(blockIdx.x) * kPackRows;
+    const uint32_t nr = uint32_t((rows - r0 < kPackRows) ? (rows - r0) : kPackRows);
+    for (uint32_t i = threadIdx.x; i < n_stages; i += blockDim.x) sbits[i] = uint8_t(stages[i].bits);
+    const uint16_t* src = codes + (stream * rows + r0) * n_stages;
+    for (uint32_t i = threadIdx.x; i < nr * n_stages; i += blockDim.x) sc[i] = src[i];
+    __syncthreads();
+    if (threadIdx.x < nr) {
+        const uint16_t* c = sc + threadIdx.x * n_stages;
+        uint8_t* o = so + threadIdx.x * row_bytes;
+        uint64_t acc = 0;
+        uint32_t nb = 0, ob = 0;
+        for (uint32_t st = 0; st < n_stages; ++st) {
+            const uint32_t b = sbits[st];
+            acc |= uint64_t(c[st] & ((1u << b) - 1u)) << nb;
+            nb += b;
+            while (nb >= 8) {
+                o[ob++] = uint8_t(acc);
+                acc >>= 8;
+                nb -= 8;
+            }
+        }
+    }
+    __syncthreads();
+    uint8_t* dst = payload + stream * stream_bytes + r0 * row_bytes;
+    for (uint32_t i = threadIdx.x; i < nr * row_bytes; i += blockDim.x) dst[i] = so[i];
+}
+
 // nearest_entry (codebook.cpp:180-192) for many vectors against one stage.
 __global__ void __launch_bounds__(kExactWarps * 32)
 nearest_kernel(StageInfo si, uint32_t D, const float* __restrict__ eff, const float* __restrict__ sqn,
@@ -183,6 +226,17 @@ void launch_pack_codes(const uint16_t* codes, uint32_t n_streams, uint64_t rows,
     const uint64_t n = sb * n_streams;
     if (n == 0) return;
     ProfScope ps("pack", s);
+    uint32_t max_bits = 0;
+    for (const auto& si : st.stages) max_bits = std::max(max_bits, si.bits);
+    const size_t fsm = kPackMaxStages + size_t(kPackRows) * n_stages * 2 + size_t(kPackRows) * (st.row_bits / 8);
+    if (st.row_bits % 8 == 0 && st.row_bits > 0 && n_stages <= uint32_t(kPackMaxStages) && max_bits <= 16 &&
+        fsm <= 48 * 1024 && rows > 0) {
+        dim3 grid(unsigned((rows + kPackRows - 1) / kPackRows), n_streams);
+        pack_rows_kernel<<<grid, kPackRows, fsm, s>>>(codes, st.d_stages, n_stages, uint32_t(st.row_bits / 8), rows, sb,
+                                                      payload);
+        launch_check("pack_rows_kernel");
+        return;
+    }
     pack_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(codes, st.d_stages, n_stages, st.row_bits, n_streams, rows,
                                                           sb, payload);
     launch_check("pack_kernel");
