@@ -119,6 +119,11 @@ int vqkv_quantize_batch_host(vqkv_stack_t stack, const float* xs_host, uint32_t 
 int vqkv_reconstruct_block(vqkv_stack_t stack, const uint8_t* payload_dev, uint32_t n_streams,
                            uint64_t rows_per_stream, uint64_t begin, uint64_t end, float* out_dev,
                            void* stream);
+/* the same with streams stride bytes apart (0 = dense: payload bytes of `rows`),
+ * e.g. a device-resident cache's fixed-capacity payload buffers */
+int vqkv_reconstruct_block_ex(vqkv_stack_t stack, const uint8_t* payload_dev, uint64_t stream_stride,
+                              uint32_t n_streams, uint64_t rows, uint64_t begin, uint64_t end, float* out_dev,
+                              void* stream);
 
 /* ---------------------------------------------------------------------------
  * Decode-step attention over the three-segment cache of kv_cache.hpp:41-108,
@@ -149,9 +154,23 @@ typedef struct vqkv_attend_args {
     double scale;
     float* out_dev;
     float* lse_dev;
+    /* per-pair strides of the segment buffers (0 = dense): rows between pairs
+     * for init / local (a cache keeps them in fixed-capacity buffers), bytes
+     * between pairs for the code payloads (capacity, >= payload bytes) */
+    uint64_t init_stride;
+    uint64_t local_stride;
+    uint64_t kcodes_stride;
+    uint64_t vcodes_stride;
 } vqkv_attend_args;
 int vqkv_attend_decode(vqkv_stack_t key_stack, vqkv_stack_t value_stack, const vqkv_attend_args* args,
                        void* stream);
+
+/* CodeMatrix::append of whole packed blocks (codebook.cpp:96-120), batched over
+ * streams: for each stream i, bits [0, src_bits) of src + i*src_stride are
+ * written at bit dst_bits of dst + i*dst_stride (bits below dst_bits kept).
+ * Used by a device-resident cache to append flushed rows at any bit offset. */
+int vqkv_payload_append(uint8_t* dst_dev, uint64_t dst_stride, uint64_t dst_bits, const uint8_t* src_dev,
+                        uint64_t src_stride, uint64_t src_bits, uint32_t n_streams, void* stream);
 
 /* HOST-buffer variants (copy in, compute, copy out; synchronous), used by the
  * C++ mirror API (include/vqkv/*.hpp) whose signatures take host matrices. */

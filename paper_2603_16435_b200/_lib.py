@@ -39,6 +39,10 @@ class AttendArgs(C.Structure):
         ("scale", C.c_double),
         ("out_dev", C.c_void_p),
         ("lse_dev", C.c_void_p),
+        ("init_stride", C.c_uint64),
+        ("local_stride", C.c_uint64),
+        ("kcodes_stride", C.c_uint64),
+        ("vcodes_stride", C.c_uint64),
     ]
 
 
@@ -63,10 +67,12 @@ _SIGS = {
     "vqkv_quantize_batch_host": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint64, P, P, P]),
     "vqkv_nearest_batch": (C.c_int, [P, C.c_uint32, P, C.c_uint64, C.c_uint64, P, P, P]),
     "vqkv_reconstruct_block": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, P, P]),
+    "vqkv_reconstruct_block_ex": (C.c_int, [P, P, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, P, P]),
     "vqkv_attend_decode": (C.c_int, [P, P, C.POINTER(AttendArgs), P]),
     "vqkv_lse_combine": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint32, P, P, P]),
     "vqkv_encode_counters": (C.c_int, [P, u64p]),
     "vqkv_encode_phase_clocks": (C.c_int, [P, u64p]),
+    "vqkv_payload_append": (C.c_int, [P, C.c_uint64, C.c_uint64, P, C.c_uint64, C.c_uint64, C.c_uint32, P]),
     "vqkv_profile_enable": (C.c_int, [C.c_int]),
     "vqkv_profile_collect": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), u64p]),
     "vqkv_generate_synthetic": (

@@ -1,0 +1,231 @@
+"""Device-resident, batched CacheState.
+
+Mirrors the reference's three-segment KV store (proj/core/include/vqkv/kv_cache.hpp:45-108,
+proj/core/src/kv_cache.cpp:41-204) for `n_streams` (sequence, layer, KV head) streams that
+advance in lockstep, the way a decoding model steps all of its streams together:
+
+    init (raw prompt head, <= init_len rows) | compressed middle (CodeMatrix payload)
+    | pending (raw, evicted from the window, not yet encoded) | local (raw window, local_len)
+
+Everything lives in HBM.  Compressed rows are encoded by the tensor-core encoder
+(`quantize_streams`, kv_cache.cpp:87-88 / :109-110) and appended to fixed-capacity payload
+buffers with `vqkv_payload_append`; pending + local rows share one contiguous raw tail buffer
+of 2 * local_len rows, so a flush is one batched encode of the first `pending` rows
+(kv_cache.cpp:102-120) and attention reads every segment in place (strided views, no copies).
+
+Semantics follow the reference exactly: prefill split (kv_cache.cpp:61-100), eviction to
+pending and deferred (or eager) flush at local_len pending rows (:122-141), token order of
+view_block (:143-189), memory accounting (:191-204), error kinds and messages.
+"""
+from __future__ import annotations
+
+from typing import Dict, Optional, Tuple
+
+import torch
+
+from . import _lib
+from . import device as Dv
+from .errors import InvalidInput, InvalidState
+
+__all__ = ["DeviceCacheState"]
+
+
+class DeviceCacheState:
+    """Batched CacheState on one GPU: n_streams streams with identical token counts."""
+
+    def __init__(self, key_stack, value_stack, n_streams: int, init_len: int = 4, local_len: int = 1024,
+                 eager: bool = False, device: Optional[torch.device] = None, capacity_rows: int = 0):
+        if local_len < 1:  # WindowPolicy::validate (kv_cache.cpp:41-45)
+            raise InvalidInput("local_len must be >= 1")
+        if n_streams < 1:
+            raise InvalidInput("n_streams must be >= 1")
+        self.kstack, self.vstack = key_stack, value_stack
+        self.kd, self.vd = Dv._dev(key_stack), Dv._dev(value_stack)
+        self.n_streams = int(n_streams)
+        self.init_len, self.local_len, self.eager = int(init_len), int(local_len), bool(eager)
+        self.device = torch.device("cuda", self.kd.device) if device is None else torch.device(device)
+        S, Dk, Dvv = self.n_streams, self.kd.dim, self.vd.dim
+        f32 = dict(dtype=torch.float32, device=self.device)
+        self.init_k = torch.zeros((S, max(self.init_len, 1), Dk), **f32)
+        self.init_v = torch.zeros((S, max(self.init_len, 1), Dvv), **f32)
+        self.tail_k = torch.zeros((S, 2 * self.local_len, Dk), **f32)
+        self.tail_v = torch.zeros((S, 2 * self.local_len, Dvv), **f32)
+        self.n_init = 0
+        self.n_comp = 0
+        self.n_tail = 0          # pending + local rows in the tail buffer
+        self.prefilled = False
+        self.batched = 0         # flush_pending count (kv_cache.hpp: batched_compressions_)
+        self.cap_rows = 0
+        self.kpay = self.vpay = None
+        self.knorm = self.vnorm = None
+        self._grow(max(int(capacity_rows), 0))
+
+    # ---- geometry ---------------------------------------------------------
+    @property
+    def pending(self) -> int:
+        return max(0, self.n_tail - self.local_len)
+
+    @property
+    def local(self) -> int:
+        return self.n_tail - self.pending
+
+    def total_len(self) -> int:
+        return self.n_init + self.n_comp + self.n_tail
+
+    def counts(self) -> Dict[str, int]:
+        return dict(init=self.n_init, compressed=self.n_comp, pending=self.pending, local=self.local,
+                    total=self.total_len(), batched=self.batched)
+
+    def _grow(self, rows: int) -> None:
+        """Make room for `rows` compressed rows per stream (capacity doubles)."""
+        if rows <= self.cap_rows and self.kpay is not None:
+            return
+        cap = max(rows, 2 * self.cap_rows, 1024)
+        kb, vb = self.kd.payload_bytes(cap), self.vd.payload_bytes(cap)
+        # zero-filled: payload_append ORs into the first partial byte
+        kpay = torch.zeros((self.n_streams, kb), dtype=torch.uint8, device=self.device)
+        vpay = torch.zeros((self.n_streams, vb), dtype=torch.uint8, device=self.device)
+        knorm = torch.zeros((self.n_streams, cap), dtype=torch.float32, device=self.device)
+        vnorm = torch.zeros((self.n_streams, cap), dtype=torch.float32, device=self.device)
+        if self.kpay is not None and self.n_comp:
+            ob, ovb = self.kd.payload_bytes(self.n_comp), self.vd.payload_bytes(self.n_comp)
+            kpay[:, :ob] = self.kpay[:, :ob]
+            vpay[:, :ovb] = self.vpay[:, :ovb]
+            knorm[:, : self.n_comp] = self.knorm[:, : self.n_comp]
+            vnorm[:, : self.n_comp] = self.vnorm[:, : self.n_comp]
+        self.kpay, self.vpay, self.knorm, self.vnorm, self.cap_rows = kpay, vpay, knorm, vnorm, cap
+
+    def _encode_append(self, keys: torch.Tensor, values: torch.Tensor) -> None:
+        """quantize_batch of [S, n, D] rows and CodeMatrix::append of the result."""
+        n = keys.shape[1]
+        if n == 0:
+            return
+        self._grow(self.n_comp + n)
+        kp, kn = Dv.quantize_streams(self.kstack, keys.contiguous())
+        vp, vn = Dv.quantize_streams(self.vstack, values.contiguous())
+        stream = Dv._stream(keys)
+        for pay, src, rb in ((self.kpay, kp, self.kd.row_bits), (self.vpay, vp, self.vd.row_bits)):
+            _lib.call("vqkv_payload_append", pay.data_ptr(), pay.stride(0), self.n_comp * rb, src.data_ptr(),
+                      src.stride(0), n * rb, self.n_streams, stream)
+        self.knorm[:, self.n_comp: self.n_comp + n] = kn
+        self.vnorm[:, self.n_comp: self.n_comp + n] = vn
+        self.n_comp += n
+
+    def _check_rows(self, keys: torch.Tensor, values: torch.Tensor, ndim: int) -> None:
+        for t, nm in ((keys, "keys"), (values, "values")):
+            if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or t.device != self.device:
+                raise InvalidInput(f"{nm} must be float32 tensors on {self.device}")
+            if t.dim() != ndim or t.shape[0] != self.n_streams:
+                raise InvalidInput(f"{nm} must have shape [n_streams, ...] with n_streams = {self.n_streams}")
+
+    # ---- writers (single writer, kv_cache.hpp:41-44) ----------------------
+    def prefill(self, keys: torch.Tensor, values: torch.Tensor) -> None:
+        """keys [S, L, Dk], values [S, L, Dv] -> init | compressed | local (kv_cache.cpp:61-100)."""
+        if self.total_len() != 0 or self.prefilled:
+            raise InvalidState("prefill requires an empty cache")
+        self._check_rows(keys, values, 3)
+        if keys.shape[1] < 1:
+            raise InvalidInput("prefill needs at least one token")
+        if keys.shape[1] != values.shape[1]:
+            raise InvalidInput("keys and values must have the same length")
+        if keys.shape[2] != self.kd.dim or values.shape[2] != self.vd.dim:
+            raise InvalidInput("key/value dimensions do not match the stacks")
+        L = keys.shape[1]
+        n_init = min(self.init_len, L)
+        n_local = min(self.local_len, L - n_init)
+        n_mid = L - n_init - n_local
+        self.init_k[:, :n_init] = keys[:, :n_init]
+        self.init_v[:, :n_init] = values[:, :n_init]
+        self.n_init = n_init
+        if n_mid > 0:
+            self._encode_append(keys[:, n_init:n_init + n_mid], values[:, n_init:n_init + n_mid])
+        self.tail_k[:, :n_local] = keys[:, L - n_local:]
+        self.tail_v[:, :n_local] = values[:, L - n_local:]
+        self.n_tail = n_local
+        self.prefilled = True
+
+    def append_token(self, keys: torch.Tensor, values: torch.Tensor) -> None:
+        """keys [S, Dk], values [S, Dv]: one decode step for every stream (kv_cache.cpp:122-141)."""
+        if not self.prefilled and self.init_len != 0:
+            raise InvalidState("append_token requires a prefilled cache (or init_len == 0)")
+        self._check_rows(keys, values, 2)
+        if keys.shape[1] != self.kd.dim or values.shape[1] != self.vd.dim:
+            raise InvalidInput("key/value dimensions do not match the stacks")
+        self.tail_k[:, self.n_tail] = keys
+        self.tail_v[:, self.n_tail] = values
+        self.n_tail += 1
+        if self.n_tail > self.local_len and (self.eager or self.pending >= self.local_len):
+            self.flush_pending()
+
+    def flush_pending(self) -> None:
+        """Encode the pending rows as one batch and append them (kv_cache.cpp:102-120)."""
+        p = self.pending
+        if p == 0:
+            return
+        self._encode_append(self.tail_k[:, :p], self.tail_v[:, :p])
+        rest = self.n_tail - p
+        self.tail_k[:, :rest] = self.tail_k[:, p:self.n_tail].clone()
+        self.tail_v[:, :rest] = self.tail_v[:, p:self.n_tail].clone()
+        self.n_tail = rest
+        self.batched += 1
+
+    # ---- readers ------------------------------------------------------------
+    def view_block(self, begin: int, end: int) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+        """Token rows [begin, end) of every stream -> (keys [S, n, Dk], values [S, n, Dv], exact [n])."""
+        L = self.total_len()
+        if begin < 0 or begin > end or end > L:
+            raise InvalidInput(f"view range [{begin}, {end}) out of bounds for length {L}")
+        S, n = self.n_streams, end - begin
+        keys = torch.empty((S, n, self.kd.dim), dtype=torch.float32, device=self.device)
+        values = torch.empty((S, n, self.vd.dim), dtype=torch.float32, device=self.device)
+        exact = torch.ones(n, dtype=torch.bool)
+        ie, ce = self.n_init, self.n_init + self.n_comp
+        if begin < ie:
+            e = min(end, ie)
+            keys[:, : e - begin] = self.init_k[:, begin:e]
+            values[:, : e - begin] = self.init_v[:, begin:e]
+        if begin < ce and end > ie:
+            b, e = max(begin, ie), min(end, ce)
+            keys[:, b - begin: e - begin] = Dv.reconstruct_streams(self.kstack, self._payload(0), self.n_comp,
+                                                                   b - ie, e - ie)
+            values[:, b - begin: e - begin] = Dv.reconstruct_streams(self.vstack, self._payload(1), self.n_comp,
+                                                                     b - ie, e - ie)
+            exact[b - begin: e - begin] = False
+        if end > ce:
+            b = max(begin, ce)
+            keys[:, b - begin:] = self.tail_k[:, b - ce: end - ce]
+            values[:, b - begin:] = self.tail_v[:, b - ce: end - ce]
+        return keys, values, exact
+
+    def _payload(self, which: int) -> torch.Tensor:
+        st, pay = (self.kd, self.kpay) if which == 0 else (self.vd, self.vpay)
+        return pay[:, : max(st.payload_bytes(self.n_comp), 1)]
+
+    def codes(self, which: int) -> Tuple[torch.Tensor, torch.Tensor]:
+        """(payload [S, payload_bytes(compressed)] u8, residual norms [S, compressed]) of keys (0) / values (1)."""
+        st = self.kd if which == 0 else self.vd
+        pay = (self.kpay if which == 0 else self.vpay)[:, : st.payload_bytes(self.n_comp)]
+        nrm = (self.knorm if which == 0 else self.vnorm)[:, : self.n_comp]
+        return pay, nrm
+
+    def memory_report(self) -> Dict[str, float]:
+        """Per-stream accounting, kv_cache.cpp:191-204 (raw scalars counted at 2 bytes)."""
+        spt = self.kd.dim + self.vd.dim
+        bits = self.n_comp * (self.kd.row_bits + self.vd.row_bits)
+        ratio = 1.0 - bits / float(self.n_comp * spt * 16) if self.n_comp else 0.0
+        return dict(raw_bytes_equivalent=self.total_len() * spt * 2, compressed_payload_bits=bits,
+                    codebook_overhead_bytes=self.kd.serialized_bytes() + self.vd.serialized_bytes(),
+                    effective_ratio=ratio)
+
+    def attend(self, q: torch.Tensor, scale: float = 0.0, want_lse: bool = True):
+        """Decode-step attention for q [S, G, Dk] over every segment, read in place
+        (attention.cpp:26-69 over view_block order) -> (out [S, G, Dv], lse [S, G])."""
+        if self.total_len() == 0:
+            raise InvalidState("cannot attend over an empty cache")
+        ni, nt = self.n_init, self.n_tail
+        return Dv.attend_decode(
+            self.kstack, self.vstack, q,
+            self.kpay if self.n_comp else None, self.vpay if self.n_comp else None, self.n_comp,
+            self.init_k[:, :ni] if ni else None, self.init_v[:, :ni] if ni else None,
+            self.tail_k[:, :nt] if nt else None, self.tail_v[:, :nt] if nt else None,
+            scale=scale, want_lse=want_lse)

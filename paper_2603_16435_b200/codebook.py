@@ -303,6 +303,10 @@ class DeviceStack:
     def payload_bytes(self, rows: int) -> int:
         return (rows * self.row_bits + 7) // 8
 
+    def serialized_bytes(self) -> int:
+        """RSVQ size of the stack (codebook.cpp:252-275): header + per stage S, D, entries, projection."""
+        return 13 + sum(8 + 4 * (s * self.dim + self.dim * self.dim) for s in self.sizes)
+
     def effective(self, stage: int):
         e = np.empty((self.sizes[stage], self.dim), np.float32)
         q = np.empty(self.sizes[stage], np.float32)

@@ -37,6 +37,7 @@ struct SegArgs {
     uint64_t n_local;
     uint32_t group;
     float scale;
+    uint64_t init_stride, local_stride;  // rows between pairs (dense: n_init / n_local)
 };
 
 struct StackView {
@@ -100,10 +101,10 @@ attend_generic_kernel(StackView ksv, StackView vsv, SegArgs a, uint32_t Dk, uint
     const uint64_t L = a.n_init + a.n_comp + a.n_local;
     const uint64_t t0 = uint64_t(split) * per_split;
     const uint64_t t1 = min(L, t0 + per_split);
-    const float* ik = a.init_k + uint64_t(pair) * a.n_init * Dk;
-    const float* iv = a.init_v + uint64_t(pair) * a.n_init * Dv;
-    const float* lk = a.local_k + uint64_t(pair) * a.n_local * Dk;
-    const float* lv = a.local_v + uint64_t(pair) * a.n_local * Dv;
+    const float* ik = a.init_k + uint64_t(pair) * a.init_stride * Dk;
+    const float* iv = a.init_v + uint64_t(pair) * a.init_stride * Dv;
+    const float* lk = a.local_k + uint64_t(pair) * a.local_stride * Dk;
+    const float* lv = a.local_v + uint64_t(pair) * a.local_stride * Dv;
     const uint8_t* kc = a.kcodes + uint64_t(pair) * ksv.stream_bytes;
     const uint8_t* vc = a.vcodes + uint64_t(pair) * vsv.stream_bytes;
     for (uint64_t t = t0 + warp; t < t1; t += kAttWarps) {
@@ -232,11 +233,14 @@ void launch_attend(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_at
     VQKV_CUDA(cudaMallocAsync(&pacc, sizeof(float) * a.n_pairs * nsplit * G * Dv, s));
     VQKV_CUDA(cudaMallocAsync(&pm, sizeof(float) * a.n_pairs * nsplit * G, s));
     VQKV_CUDA(cudaMallocAsync(&pl, sizeof(float) * a.n_pairs * nsplit * G, s));
-    StackView ksv{ks.d_stages, ks.n, ks.row_bits, ks.d_eff, payload_bytes(ks.row_bits, a.n_comp)};
-    StackView vsv{vs.d_stages, vs.n, vs.row_bits, vs.d_eff, payload_bytes(vs.row_bits, a.n_comp)};
+    StackView ksv{ks.d_stages, ks.n, ks.row_bits, ks.d_eff,
+                  a.kcodes_stride ? a.kcodes_stride : payload_bytes(ks.row_bits, a.n_comp)};
+    StackView vsv{vs.d_stages, vs.n, vs.row_bits, vs.d_eff,
+                  a.vcodes_stride ? a.vcodes_stride : payload_bytes(vs.row_bits, a.n_comp)};
     const double scale = a.scale > 0.0 ? a.scale : 1.0 / std::sqrt(double(Dk));
     SegArgs sa{a.q_dev, a.init_k_dev, a.init_v_dev, a.n_init, a.kcodes_dev, a.vcodes_dev, a.n_comp,
-               a.local_k_dev, a.local_v_dev, a.n_local, G, float(scale)};
+               a.local_k_dev, a.local_v_dev, a.n_local, G, float(scale),
+               a.init_stride ? a.init_stride : a.n_init, a.local_stride ? a.local_stride : a.n_local};
     const size_t smem = sizeof(float) * (G * Dk + kAttWarps * (Dk + Dv + G * Dv + 2 * G));
     if (smem > 227 * 1024) fail(VQKV_UNSUPPORTED, "attention head shape too large for shared memory");
     if (smem > 48 * 1024)

@@ -149,6 +149,7 @@ struct MainArgs {
     float* part_o;      // [pairs][G][D]  (raw CTA)
     float* part_m;      // [pairs][splits+1][G]
     float* part_l;      // [pairs][splits+1][G]
+    uint64_t init_stride, local_stride;  // rows between pairs
 };
 
 __device__ __forceinline__ float block_max(float v, float* red) {
@@ -182,8 +183,8 @@ __device__ void raw_rows(const MainArgs& a, uint32_t pair, float* smem) {
     const uint64_t n_raw = a.n_init + a.n_local;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (uint64_t r = warp; r < n_raw; r += nw) {
-        const float* k = (r < a.n_init) ? a.init_k + (uint64_t(pair) * a.n_init + r) * kD
-                                        : a.local_k + (uint64_t(pair) * a.n_local + (r - a.n_init)) * kD;
+        const float* k = (r < a.n_init) ? a.init_k + (uint64_t(pair) * a.init_stride + r) * kD
+                                        : a.local_k + (uint64_t(pair) * a.local_stride + (r - a.n_init)) * kD;
         const float4 kv = reinterpret_cast<const float4*>(k)[lane];
         for (int g = 0; g < kG; ++g) {
             const float4 qv = reinterpret_cast<const float4*>(qs + g * kD)[lane];
@@ -216,8 +217,8 @@ __device__ void raw_rows(const MainArgs& a, uint32_t pair, float* smem) {
         const uint32_t g = gd / kD, d = gd % kD;
         float acc = 0.f;
         for (uint64_t r = 0; r < n_raw; ++r) {
-            const float* v = (r < a.n_init) ? a.init_v + (uint64_t(pair) * a.n_init + r) * kD
-                                            : a.local_v + (uint64_t(pair) * a.n_local + (r - a.n_init)) * kD;
+            const float* v = (r < a.n_init) ? a.init_v + (uint64_t(pair) * a.init_stride + r) * kD
+                                            : a.local_v + (uint64_t(pair) * a.local_stride + (r - a.n_init)) * kD;
             acc = fmaf(ls[r * kG + g], __ldg(v + d), acc);
         }
         a.part_o[(uint64_t(pair) * kG + g) * kD + d] = acc;
@@ -523,13 +524,16 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     }
     {
         ProfScope ps("attend", s);
+        const uint64_t kpb = payload_bytes(ks.row_bits, a.n_comp), vpb = payload_bytes(vs.row_bits, a.n_comp);
+        const uint64_t kstr = a.kcodes_stride ? a.kcodes_stride : kpb, vstr = a.vcodes_stride ? a.vcodes_stride : vpb;
         MainArgs ma{a.q_dev, a.init_k_dev, a.init_v_dev, a.n_init, a.kcodes_dev, a.vcodes_dev, a.n_comp,
-                    a.local_k_dev, a.local_v_dev, a.n_local, ks.d_stages, ks.n, ks.row_bits,
-                    payload_bytes(ks.row_bits, a.n_comp), kent, vs.d_stages, vs.n, vs.row_bits,
-                    payload_bytes(vs.row_bits, a.n_comp), vent, lut,
-                    a.kcodes_dev + uint64_t(a.n_pairs) * payload_bytes(ks.row_bits, a.n_comp),
-                    a.vcodes_dev + uint64_t(a.n_pairs) * payload_bytes(vs.row_bits, a.n_comp), float(scale), n_splits,
-                    ph, po, pm, pl};
+                    a.local_k_dev, a.local_v_dev, a.n_local, ks.d_stages, ks.n, ks.row_bits, kstr, kent,
+                    vs.d_stages, vs.n, vs.row_bits, vstr, vent, lut,
+                    // end of the last pair's payload: reads stop here (earlier pairs may read into the next)
+                    a.kcodes_dev + uint64_t(a.n_pairs - 1) * kstr + kpb,
+                    a.vcodes_dev + uint64_t(a.n_pairs - 1) * vstr + vpb, float(scale), n_splits,
+                    ph, po, pm, pl, a.init_stride ? a.init_stride : a.n_init,
+                    a.local_stride ? a.local_stride : a.n_local};
         const size_t smem = 131072 + 64 + 64 * sizeof(float) + 4096;
         static bool attr = false;
         if (!attr) {

@@ -113,11 +113,11 @@ __global__ void reconstruct_wide_kernel(const StageInfo* __restrict__ stages, ui
 }  // namespace
 
 void launch_reconstruct(const vqkv_stack_s& st, const uint8_t* payload, uint32_t n_streams, uint64_t rows,
-                        uint64_t begin, uint64_t end, float* out, cudaStream_t s) {
+                        uint64_t begin, uint64_t end, float* out, cudaStream_t s, uint64_t stream_stride) {
     const uint64_t nrows = end - begin;
     const uint64_t total = uint64_t(n_streams) * nrows;
     if (total == 0) return;
-    const uint64_t sb = payload_bytes(st.row_bits, rows);
+    const uint64_t sb = stream_stride ? stream_stride : payload_bytes(st.row_bits, rows);
     ProfScope ps("reconstruct", s);
     if (st.dim <= 128) {
         int sms = 148;

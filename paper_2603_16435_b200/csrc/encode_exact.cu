@@ -145,6 +145,26 @@ __global__ void __launch_bounds__(kPackRows) pack_rows_kernel(const uint16_t* __
     for (uint32_t i = threadIdx.x; i < nr * row_bytes; i += blockDim.x) dst[i] = so[i];
 }
 
+// CodeMatrix::append of a whole packed block (codebook.cpp:96-120 semantics for
+// many rows): for every stream, the src_bits of src land at bit dst_bits of
+// dst; one thread per destination byte, low bits of the first byte kept.
+__global__ void payload_append_kernel(uint8_t* __restrict__ dst, uint64_t dst_stride, uint64_t dst_bits,
+                                      const uint8_t* __restrict__ src, uint64_t src_stride, uint64_t src_bits,
+                                      uint32_t n_streams) {
+    const uint64_t b0 = dst_bits >> 3, nb = ((dst_bits + src_bits + 7) >> 3) - b0;
+    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= nb * n_streams) return;
+    const uint64_t stream = idx / nb, k = idx % nb;
+    const uint8_t* s = src + stream * src_stride;
+    uint8_t* d = dst + stream * dst_stride + b0;
+    const uint64_t src_bytes = (src_bits + 7) >> 3;
+    const uint32_t sh = uint32_t(dst_bits & 7);
+    uint32_t v = (k < src_bytes) ? (uint32_t(s[k]) << sh) : 0u;
+    if (k > 0 && sh) v |= uint32_t(s[k - 1]) >> (8 - sh);
+    if (k == 0) v |= d[0] & ((1u << sh) - 1u);
+    d[k] = uint8_t(v);
+}
+
 // nearest_entry (codebook.cpp:180-192) for many vectors against one stage.
 __global__ void __launch_bounds__(kExactWarps * 32)
 nearest_kernel(StageInfo si, uint32_t D, const float* __restrict__ eff, const float* __restrict__ sqn,
@@ -240,6 +260,16 @@ void launch_pack_codes(const uint16_t* codes, uint32_t n_streams, uint64_t rows,
     pack_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(codes, st.d_stages, n_stages, st.row_bits, n_streams, rows,
                                                           sb, payload);
     launch_check("pack_kernel");
+}
+
+void launch_payload_append(uint8_t* dst, uint64_t dst_stride, uint64_t dst_bits, const uint8_t* src,
+                           uint64_t src_stride, uint64_t src_bits, uint32_t n_streams, cudaStream_t s) {
+    if (src_bits == 0 || n_streams == 0) return;
+    const uint64_t nb = ((dst_bits + src_bits + 7) >> 3) - (dst_bits >> 3);
+    const uint64_t n = nb * n_streams;
+    payload_append_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(dst, dst_stride, dst_bits, src, src_stride,
+                                                                    src_bits, n_streams);
+    launch_check("payload_append_kernel");
 }
 
 }  // namespace vqkv_dev

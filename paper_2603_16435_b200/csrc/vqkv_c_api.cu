@@ -278,6 +278,17 @@ int vqkv_encode_phase_clocks(vqkv_stack_t s, uint64_t* c) {
     });
 }
 
+int vqkv_payload_append(uint8_t* dst, uint64_t dst_stride, uint64_t dst_bits, const uint8_t* src,
+                        uint64_t src_stride, uint64_t src_bits, uint32_t n_streams, void* stream) {
+    return guard([&] {
+        if (src_bits == 0 || n_streams == 0) return;
+        need(dst && src, VQKV_INVALID_INPUT, "null payload buffer");
+        need(dst_stride * 8 >= dst_bits + src_bits, VQKV_INVALID_INPUT, "destination payload capacity exceeded");
+        need(src_stride * 8 >= src_bits, VQKV_INVALID_INPUT, "source payload shorter than src_bits");
+        launch_payload_append(dst, dst_stride, dst_bits, src, src_stride, src_bits, n_streams, as_stream(stream));
+    });
+}
+
 int vqkv_quantize_batch(vqkv_stack_t s, const float* xs, uint32_t n_streams, uint64_t rows, uint64_t sb,
                         uint8_t* payload, float* norms, void* stream) {
     return vqkv_quantize_batch_ex(s, xs, n_streams, rows, sb, payload, norms, nullptr, stream);
@@ -375,6 +386,11 @@ int vqkv_quantize_batch_host(vqkv_stack_t s, const float* xs, uint32_t n_streams
 
 int vqkv_reconstruct_block(vqkv_stack_t s, const uint8_t* payload, uint32_t n_streams, uint64_t rows, uint64_t begin,
                            uint64_t end, float* out, void* stream) {
+    return vqkv_reconstruct_block_ex(s, payload, 0, n_streams, rows, begin, end, out, stream);
+}
+
+int vqkv_reconstruct_block_ex(vqkv_stack_t s, const uint8_t* payload, uint64_t stream_stride, uint32_t n_streams,
+                              uint64_t rows, uint64_t begin, uint64_t end, float* out, void* stream) {
     return guard([&] {
         check_stack(s);
         // codebook.cpp:241-244
@@ -384,7 +400,9 @@ int vqkv_reconstruct_block(vqkv_stack_t s, const uint8_t* payload, uint32_t n_st
         if (end == begin || n_streams == 0) return;
         need(payload && out, VQKV_INVALID_INPUT, "null device buffer");
         DeviceGuard g(s->device);
-        launch_reconstruct(*s, payload, n_streams, rows, begin, end, out, as_stream(stream));
+        need(stream_stride == 0 || stream_stride >= payload_bytes(s->row_bits, rows), VQKV_INVALID_INPUT,
+             "payload stream stride shorter than the payload");
+        launch_reconstruct(*s, payload, n_streams, rows, begin, end, out, as_stream(stream), stream_stride);
     });
 }
 
@@ -498,6 +516,8 @@ int vqkv_attend_decode_host(vqkv_stack_t ks, vqkv_stack_t vs, const vqkv_attend_
             owned.push_back(d);
             return d;
         };
+        need(h->init_stride == 0 && h->local_stride == 0 && h->kcodes_stride == 0 && h->vcodes_stride == 0,
+             VQKV_INVALID_INPUT, "host attention buffers must be dense (strides 0)");
         vqkv_attend_args d = *h;
         d.q_dev = static_cast<const float*>(up(h->q_dev, sizeof(float) * P * G * Dk));
         d.init_k_dev = static_cast<const float*>(up(h->init_k_dev, sizeof(float) * P * h->n_init * Dk));

@@ -191,6 +191,8 @@ struct DeviceGuard {
 };
 
 // ---- kernels launched from the C-ABI (defined in the .cu files) -------------
+void launch_payload_append(uint8_t* dst, uint64_t dst_stride, uint64_t dst_bits, const uint8_t* src,
+                           uint64_t src_stride, uint64_t src_bits, uint32_t n_streams, cudaStream_t s);
 void stack_build_device(vqkv_stack_s& st, const float* entries_host, const float* proj_host);
 void launch_pack_codes(const uint16_t* codes, uint32_t n_streams, uint64_t rows, uint32_t n_stages,
                        const vqkv_stack_s& st, uint8_t* payload, cudaStream_t s);
@@ -202,7 +204,8 @@ bool encode_tc_supported(const vqkv_stack_s& st);
 void launch_encode_tc(const vqkv_stack_s& st, const float* xs, uint32_t n_streams, uint64_t rows_per_stream,
                       uint64_t search_block, uint8_t* payload, float* norms, float* residuals, cudaStream_t s);
 void launch_reconstruct(const vqkv_stack_s& st, const uint8_t* payload, uint32_t n_streams, uint64_t rows,
-                        uint64_t begin, uint64_t end, float* out, cudaStream_t s);
+                        uint64_t begin, uint64_t end, float* out, cudaStream_t s,
+                        uint64_t stream_stride = 0);
 void launch_attend(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s);
 void launch_lse_combine(const float* o, const float* lse, uint32_t parts, uint64_t rows, uint32_t dv, float* out,
                         float* out_lse, cudaStream_t s);

@@ -31,6 +31,31 @@ def _need(t: torch.Tensor, dtype, name):
         raise InvalidInput(f"{name} must be a contiguous CUDA {dtype} tensor")
 
 
+def _pair_stride(t: torch.Tensor, dtype, name: str, inner: int) -> int:
+    """Per-pair stride of a [pairs, n, D] view (in rows) or a [pairs, bytes] view (in bytes)
+    whose per-pair part is contiguous.  A [pairs, capacity] payload buffer reports its
+    capacity, so callers may pass a buffer longer than the payload."""
+    if t.dtype != dtype:
+        raise InvalidInput(f"{name} must be {dtype}")
+    if not t.is_cuda:
+        raise InvalidInput(f"{name} must be a CUDA tensor")
+    if t.numel() == 0:
+        return 0
+    if t.dim() not in (2, 3):
+        raise InvalidInput(f"{name} must be [pairs, rows, D] or [pairs, bytes]")
+    if t.is_contiguous() or (t.shape[0] == 1 and t[0].is_contiguous()):  # dense; one pair has no real stride
+        return t.shape[1]
+    if t.dim() == 3:
+        ok = t.stride(2) == 1 and t.stride(1) == t.shape[2] and t.stride(0) % t.shape[2] == 0
+        ok = ok and t.stride(0) >= t.shape[1] * t.shape[2]
+        if not ok:
+            raise InvalidInput(f"{name}: rows of each pair must be contiguous")
+        return t.stride(0) // t.shape[2]
+    if t.dim() == 2 and t.stride(1) == 1 and t.stride(0) >= t.shape[1]:
+        return t.stride(0)
+    raise InvalidInput(f"{name}: each pair's bytes must be contiguous")
+
+
 def payload_bytes(stack, rows: int) -> int:
     return _dev(stack).payload_bytes(rows)
 
@@ -93,13 +118,17 @@ def reconstruct_streams(stack, payload: torch.Tensor, rows: int, begin: int = 0,
     end = rows if end is None else end
     if payload.dim() == 1:
         payload = payload.unsqueeze(0)
-    _need(payload, torch.uint8, "payload")
+    stride = _pair_stride(payload, torch.uint8, "payload", 1)  # capacity buffers may be strided
     ns = payload.shape[0]
     if begin > end or end > rows or begin < 0:
         raise InvalidInput(f"row range [{begin}, {end}) out of bounds for {rows} rows")
     if out is None:
         out = torch.empty((ns, end - begin, dev.dim), dtype=torch.float32, device=payload.device)
-    _lib.call("vqkv_reconstruct_block", dev.h, payload.data_ptr(), ns, rows, begin, end, out.data_ptr(),
+    else:
+        _need(out, torch.float32, "out")
+        if out.numel() != ns * (end - begin) * dev.dim:
+            raise InvalidInput("out must hold n_streams x (end - begin) x D floats")
+    _lib.call("vqkv_reconstruct_block_ex", dev.h, payload.data_ptr(), stride, ns, rows, begin, end, out.data_ptr(),
               _stream(payload))
     return out
 
@@ -130,12 +159,15 @@ def attend_decode(
         raise InvalidInput("query dimension does not match key dimension")
     n_init = 0 if init_k is None else init_k.shape[1]
     n_local = 0 if local_k is None else local_k.shape[1]
-    for t, nm in ((init_k, "init_k"), (init_v, "init_v"), (local_k, "local_k"), (local_v, "local_v")):
+    strides = {}
+    for t, nm in ((init_k, "init_k"), (init_v, "init_v"), (local_k, "local_k"), (local_v, "local_v"),
+                  (kcodes if n_comp else None, "kcodes"), (vcodes if n_comp else None, "vcodes")):
         if t is not None:
-            _need(t, torch.float32, nm)
-    if n_comp:
-        _need(kcodes, torch.uint8, "kcodes")
-        _need(vcodes, torch.uint8, "vcodes")
+            strides[nm] = _pair_stride(t, torch.uint8 if nm.endswith("codes") else torch.float32, nm, 1)
+    # K and V segments share one stride each (same token layout)
+    for a_, b_ in (("init_k", "init_v"), ("local_k", "local_v")):
+        if strides.get(a_, 0) != strides.get(b_, 0):
+            raise InvalidInput(f"{a_} and {b_} must have the same layout")
     out = torch.empty((n_pairs, group, vd.dim), dtype=torch.float32, device=q.device)
     lse = torch.empty((n_pairs, group), dtype=torch.float32, device=q.device) if want_lse else None
     a = _lib.AttendArgs(
@@ -144,6 +176,7 @@ def attend_decode(
         kcodes.data_ptr() if n_comp else None, vcodes.data_ptr() if n_comp else None, n_comp,
         local_k.data_ptr() if n_local else None, local_v.data_ptr() if n_local else None, n_local,
         float(scale), out.data_ptr(), lse.data_ptr() if lse is not None else None,
+        strides.get("init_k", 0), strides.get("local_k", 0), strides.get("kcodes", 0), strides.get("vcodes", 0),
     )
     import ctypes as C
 

@@ -1,0 +1,176 @@
+"""Device-resident batched CacheState (paper_2603_16435_b200/cache.py) against the oracle's
+CacheState restatement (oracle/vqkv_oracle.cpp, kv_cache.cpp:41-204), one oracle cache per stream.
+
+Bar: counts, code payloads, residual norms and view_block rows bit-exact; memory_report equal;
+attention over the cache within the stated tolerance max|o - o_ref| <= 2^-7 * max(1, max|o_ref|).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+ATT_TOL = 2.0 ** -7
+
+
+@pytest.fixture(scope="module")
+def torch_mod():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def product_stack(ostack):
+    from paper_2603_16435_b200 import codebook as P
+
+    return P.CodebookStack.from_arrays([ostack.entries(s) for s in range(ostack.n)],
+                                       [ostack.projection(s) for s in range(ostack.n)], ostack.kind, 0)
+
+
+def check_state(torch, dc, refs, ks, vs, q, check_attention=True):
+    S = dc.n_streams
+    for r in refs:
+        assert dc.counts() == r.counts()
+    # code payloads and residual norms, per stream
+    for which, st in ((0, ks), (1, vs)):
+        pay, nrm = dc.codes(which)
+        pay, nrm = pay.cpu().numpy(), nrm.cpu().numpy()
+        for i, r in enumerate(refs):
+            rp, rn = r.codes(which)
+            assert np.array_equal(pay[i], rp)
+            assert np.array_equal(nrm[i].view(np.uint32), rn.view(np.uint32))
+    L = dc.total_len()
+    k, v, ex = dc.view_block(0, L)
+    k, v, ex = k.cpu().numpy(), v.cpu().numpy(), ex.numpy()
+    for i, r in enumerate(refs):
+        rk, rv, rex = r.view_block(0, L)
+        assert np.array_equal(k[i].view(np.uint32), rk.view(np.uint32))
+        assert np.array_equal(v[i].view(np.uint32), rv.view(np.uint32))
+        assert np.array_equal(ex, rex)
+    # an inner window crossing segment boundaries
+    if L > 3:
+        b, e = 1, L - 1
+        k2, v2, ex2 = dc.view_block(b, e)
+        assert np.array_equal(k2.cpu().numpy(), k[:, b:e]) and np.array_equal(ex2.numpy(), ex[b:e])
+    rep = dc.memory_report()
+    ref_rep = refs[0].memory_report()
+    for key in ("raw_bytes_equivalent", "compressed_payload_bits", "codebook_overhead_bytes"):
+        assert rep[key] == ref_rep[key], key
+    assert abs(rep["effective_ratio"] - ref_rep["effective_ratio"]) < 1e-12
+    if check_attention:
+        out, lse = dc.attend(torch.from_numpy(q).cuda())
+        out = out.cpu().numpy()
+        for i, r in enumerate(refs):
+            for g in range(q.shape[1]):
+                ref = r.attend(q[i, g])
+                assert np.abs(out[i, g] - ref).max() <= ATT_TOL * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("eager", [False, True])
+@pytest.mark.parametrize("D,nk,sk,nv,sv", [(8, 3, 16, 2, 8), (128, 4, 64, 3, 32)])
+def test_cache_lifecycle_vs_oracle(torch_mod, eager, D, nk, sk, nv, sv):
+    """prefill -> decode steps with evictions, deferred/eager flushes -> every observable equal."""
+    torch = torch_mod
+    from paper_2603_16435_b200.cache import DeviceCacheState
+
+    rng = O.Rng(7000 + D + int(eager))
+    ks, vs = rng.stack(nk, sk, D, O.KEY), rng.stack(nv, sv, D, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    S, G, init_len, local_len, L0, steps = 3, 4, 2, 5, 13, 17
+    refs = [O.Cache(ks, vs, init_len, local_len, eager) for _ in range(S)]
+    dc = DeviceCacheState(pk, pv, S, init_len, local_len, eager)
+    keys = rng.matrix(S * L0, D).reshape(S, L0, D)
+    vals = rng.matrix(S * L0, D).reshape(S, L0, D)
+    for i, r in enumerate(refs):
+        r.prefill(keys[i], vals[i])
+    dc.prefill(torch.from_numpy(keys).cuda(), torch.from_numpy(vals).cuda())
+    q = rng.matrix(S * G, D).reshape(S, G, D)
+    check_state(torch, dc, refs, ks, vs, q)
+    for step in range(steps):
+        k1, v1 = rng.matrix(S, D), rng.matrix(S, D)
+        for i, r in enumerate(refs):
+            r.append_token(k1[i], v1[i])
+        dc.append_token(torch.from_numpy(k1).cuda(), torch.from_numpy(v1).cuda())
+        if step % 4 == 3 or step == steps - 1:
+            check_state(torch, dc, refs, ks, vs, q)
+    assert dc.counts()["batched"] >= 1
+
+
+def test_cache_short_prefill_and_no_prefill(torch_mod):
+    """prefill shorter than init + local (nothing compressed); init_len == 0 allows appends first."""
+    torch = torch_mod
+    from paper_2603_16435_b200.cache import DeviceCacheState
+
+    rng = O.Rng(7100)
+    ks, vs = rng.stack(2, 16, 8, O.KEY), rng.stack(2, 16, 8, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    q = rng.matrix(2 * 4, 8).reshape(2, 4, 8)
+    refs = [O.Cache(ks, vs, 4, 3, False) for _ in range(2)]
+    dc = DeviceCacheState(pk, pv, 2, 4, 3)
+    x = rng.matrix(2 * 5, 8).reshape(2, 5, 8)
+    for i, r in enumerate(refs):
+        r.prefill(x[i], x[i])
+    dc.prefill(torch.from_numpy(x).cuda(), torch.from_numpy(x).cuda())
+    check_state(torch, dc, refs, ks, vs, q)
+    refs = [O.Cache(ks, vs, 0, 2, False) for _ in range(2)]
+    dc = DeviceCacheState(pk, pv, 2, 0, 2)
+    for _ in range(7):
+        k1 = rng.matrix(2, 8)
+        for i, r in enumerate(refs):
+            r.append_token(k1[i], k1[i])
+        dc.append_token(torch.from_numpy(k1).cuda(), torch.from_numpy(k1).cuda())
+    check_state(torch, dc, refs, ks, vs, q)
+
+
+def test_cache_errors(torch_mod):
+    """Error kinds of kv_cache.cpp (InvalidState / InvalidInput)."""
+    torch = torch_mod
+    from paper_2603_16435_b200.cache import DeviceCacheState
+    from paper_2603_16435_b200.errors import InvalidInput, InvalidState
+
+    rng = O.Rng(7200)
+    ks, vs = rng.stack(2, 16, 8, O.KEY), rng.stack(2, 16, 8, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    with pytest.raises(InvalidInput):
+        DeviceCacheState(pk, pv, 2, 4, 0)
+    dc = DeviceCacheState(pk, pv, 2, 4, 3)
+    one = torch.zeros(2, 8, device="cuda")
+    with pytest.raises(InvalidState):
+        dc.append_token(one, one)
+    with pytest.raises(InvalidState):
+        dc.attend(torch.zeros(2, 4, 8, device="cuda"))
+    with pytest.raises(InvalidInput):
+        dc.prefill(torch.zeros(2, 0, 8, device="cuda"), torch.zeros(2, 0, 8, device="cuda"))
+    with pytest.raises(InvalidInput):
+        dc.prefill(torch.zeros(2, 3, 7, device="cuda"), torch.zeros(2, 3, 8, device="cuda"))
+    dc.prefill(torch.zeros(2, 3, 8, device="cuda"), torch.zeros(2, 3, 8, device="cuda"))
+    with pytest.raises(InvalidState):
+        dc.prefill(torch.zeros(2, 3, 8, device="cuda"), torch.zeros(2, 3, 8, device="cuda"))
+    with pytest.raises(InvalidInput):
+        dc.view_block(2, 5)
+    with pytest.raises(InvalidInput):
+        dc.append_token(torch.zeros(3, 8, device="cuda"), torch.zeros(3, 8, device="cuda"))
+
+
+def test_payload_append_bit_offsets(torch_mod):
+    """vqkv_payload_append == CodeMatrix::append row by row, at every bit alignment."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import _lib
+
+    rng = O.Rng(7300)
+    st = rng.stack(3, 5, 4, O.KEY)  # 3 bits x 3 stages = 9-bit rows
+    codes = np.array([[rng() % 5 for _ in range(3)] for _ in range(40)], np.uint32)
+    full = st.pack(codes)
+    for cut in (0, 1, 7, 8, 13, 39):
+        a, b = st.pack(codes[:cut]), st.pack(codes[cut:])
+        dst = torch.zeros((2, len(full) + 3), dtype=torch.uint8, device="cuda")
+        dst[:, : len(a)] = torch.from_numpy(np.frombuffer(bytes(a), np.uint8).copy()).cuda() if len(a) else 0
+        src = torch.from_numpy(np.stack([np.frombuffer(bytes(b), np.uint8)] * 2).copy()).cuda()
+        _lib.call("vqkv_payload_append", dst.data_ptr(), dst.stride(0), cut * 9, src.data_ptr(), src.stride(0),
+                  (40 - cut) * 9, 2, torch.cuda.current_stream().cuda_stream)
+        got = dst.cpu().numpy()
+        for i in range(2):
+            assert np.array_equal(got[i, : len(full)], np.frombuffer(bytes(full), np.uint8)), cut
