@@ -226,6 +226,42 @@ def cpu_encode_rate(seconds_target=12.0, threads=None):
     return rate, threads, "; ".join(desc) + " (oracle port, one thread per (layer, head) stream, 1:1 K:V mix)"
 
 
+def cpu_attention_rate(ctx, seconds_target=8.0, threads=None):
+    """Oracle attend (attention.cpp:26-69 restated, double-precision online softmax) over
+    init | compressed | local segments of a cache of up to `ctx` tokens, one query per host thread.
+
+    Returns (cache tokens/s in the GPU line's B*L/t units, threads, sample description)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+
+    threads = threads or (os.cpu_count() or 1)
+    ks, vs = O.Rng(1).stack(*K_SHAPE, D, O.KEY), O.Rng(2).stack(*V_SHAPE, D, O.VALUE)
+    n_init, n_local = INIT_LEN, LOCAL_LEN
+
+    def task(n_tok, seed):
+        r = np.random.default_rng(seed)
+        nc = max(n_tok - n_init - n_local, 0)
+        kc = ks.pack(r.integers(0, K_SHAPE[1], (nc, K_SHAPE[0])).astype(np.uint32))
+        vc = vs.pack(r.integers(0, V_SHAPE[1], (nc, V_SHAPE[0])).astype(np.uint32))
+        f = lambda n: r.standard_normal((n, D)).astype(np.float32)
+        a = (ks, vs, f(n_init), f(n_init), kc, vc, nc, f(n_local), f(n_local), f(1)[0])
+        t0 = time.perf_counter()
+        O.attend_segments(*a)
+        return time.perf_counter() - t0
+
+    per_tok = task(4096, 7) / 4096
+    n_tok = int(max(2048, min(ctx, seconds_target / max(per_tok, 1e-9))))
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda i: task(n_tok, 1000 + i), range(threads)))
+    wall = time.perf_counter() - t0
+    rate = threads * n_tok / wall / (KV_HEADS * 4)  # token-queries/s -> B*L/t (8 KV heads x G=4 per token)
+    return rate, threads, (f"{threads} queries (one per thread) x {n_tok} cache tokens in {wall:.1f}s (incl. code "
+                           "generation); oracle port of attend over random codes; normalised to the GPU line's "
+                           "B*L/t units (/ 32 queries per token)")
+
+
 # --------------------------------------------------------------------------- attention
 def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
     """configs[2]: decode step over a 128K-token compressed cache, batch 16, KV heads
@@ -448,6 +484,14 @@ def run_ours(args, rank, world, local):
             cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e}"}
+        if attn is not None and "error" not in attn:
+            try:
+                r, cores, sample = cpu_attention_rate(args.attn_context, seconds_target=args.cpu_seconds / 2)
+                attn["cpu_baseline"] = {"value": r, "unit": "tokens/s", "cores": cores, "kind": "port",
+                                        "sample": sample}
+            except Exception as e:
+                attn["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "port",
+                                        "sample": f"failed: {e}"}
 
     if rank == 0:
         counters = Dv.encode_counters(kst)
