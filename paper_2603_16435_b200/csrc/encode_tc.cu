@@ -50,7 +50,8 @@ constexpr int kNB = 2;                    // codebook chunk ring depth per tile
 constexpr uint32_t kChunkBytes = 36864;   // 128 entries x (128 + 16) fp16
 constexpr uint32_t kATileBytes = 36864;   // 128 rows x (128 + 16) fp16
 constexpr uint32_t kExtOff = 32768;       // the 16-wide K block (||e||^2 / row scale)
-constexpr int kMaxChunks = 8;             // stages up to 1024 entries
+constexpr int kMaxChunks = 8;            // chunks per super-block (1024 entries)
+constexpr int kMaxSuper = 4;             // super-blocks per stage: S <= 4096
 // One N=128 MMA group per 128-entry chunk.  (Splitting a chunk into two N=64
 // halves to double-buffer the accumulator was measured slower: SS-mode MMAs
 // re-read A from shared memory per instruction, and at N=64 that pushes the
@@ -380,66 +381,96 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 // so argmin score == argmax Y and the window scales by 2^(sigma-1).
                 const float W = ldexpf(2.02f * Bnd, sigma - 1);
 
-                // ---- max over A groups (32 contiguous entries) and B groups (j mod 32)
-                float mA[4 * kMaxChunks], mB[32];
-#pragma unroll
-                for (int k = 0; k < 4 * kMaxChunks; ++k) mA[k] = -INFINITY;
-#pragma unroll
-                for (int k = 0; k < 32; ++k) mB[k] = -INFINITY;
+                // ---- max over A groups (32 contiguous entries) and B groups (j mod 32),
+                // per super-block of <= kMaxChunks chunks (1024 entries).  A block's
+                // candidate masks use the running maximum, which only grows, so the
+                // masks of earlier blocks stay supersets of the final candidate set.
                 const uint32_t nch = si.pad_size / 128;
+                const uint32_t nsb = (nch + kMaxChunks - 1) / kMaxChunks;
                 const float* sqn_s = sqn_pad + si.pad_off;
-#pragma unroll
-                for (int c = 0; c < kMaxChunks; ++c) {
-                    if (c < int(nch)) {
-                        VQKV_PHASE(2)
-                        ptx::mbar_wait(bar_full, f_ph);
-                        VQKV_PHASE(1)
-                        f_ph ^= 1;
-                        ptx::tc_fence_after();
-                        // all 128 columns in flight at once, one wait, then the
-                        // accumulator goes back to the MMA issuer before the max trees
-                        float v0[32], v1[32], v2[32], v3[32];
-                        ptx::tmem_ld32(t_acc, v0);
-                        ptx::tmem_ld32(t_acc + 32u, v1);
-                        ptx::tmem_ld32(t_acc + 64u, v2);
-                        ptx::tmem_ld32(t_acc + 96u, v3);
-                        ptx::tc_wait_ld();
-                        ptx::tc_fence_before();
-                        ptx::mbar_arrive(bar_empty);
-                        mA[4 * c] = max32(v0);
-                        mA[4 * c + 1] = max32(v1);
-                        mA[4 * c + 2] = max32(v2);
-                        mA[4 * c + 3] = max32(v3);
-#pragma unroll
-                        for (int b = 0; b < 32; ++b) mB[b] = ptx::fmax3(mB[b], ptx::fmax3(v0[b], v1[b], v2[b]), v3[b]);
-                    }
-                }
-                VQKV_PHASE(2)
-                // ---- candidates {32a + b : mA[a] >= m - W, mB[b] >= m - W}
                 float m1 = -INFINITY;
+                uint32_t CAs[kMaxSuper], CBs[kMaxSuper];
 #pragma unroll
-                for (int k = 0; k < 4 * kMaxChunks; ++k) m1 = fmaxf(m1, mA[k]);
-                const float thr = m1 - W;
-                uint32_t CA = 0, CB = 0;
+                for (int k = 0; k < kMaxSuper; ++k) CAs[k] = CBs[k] = 0u;
 #pragma unroll
-                for (int k = 0; k < 4 * kMaxChunks; ++k) CA |= (mA[k] >= thr ? 1u : 0u) << k;
+                for (int sb = 0; sb < kMaxSuper; ++sb) {
+                    if (sb >= int(nsb)) break;
+                    float mA[4 * kMaxChunks], mB[32];
 #pragma unroll
-                for (int b = 0; b < 32; ++b) CB |= (mB[b] >= thr ? 1u : 0u) << b;
-                const uint32_t na = __popc(CA), nb = __popc(CB);
-                const bool unique = (na == 1 && nb == 1);
-                uint32_t z = unique ? (32u * (__ffs(CA) - 1) + (__ffs(CB) - 1)) : 0u;
-                const bool amb = !unique && valid && !exact_row;
-                if (unique) {
-                    const float* ez = eff + si.eff_off + uint64_t(z) * 128;
+                    for (int k = 0; k < 4 * kMaxChunks; ++k) mA[k] = -INFINITY;
 #pragma unroll
-                    for (int l = 0; l < 4; ++l) ptx::prefetch_l1(ez + 32 * l);
+                    for (int k = 0; k < 32; ++k) mB[k] = -INFINITY;
+#pragma unroll
+                    for (int c = 0; c < kMaxChunks; ++c) {
+                        if (sb * kMaxChunks + c < int(nch)) {
+                            VQKV_PHASE(2)
+                            ptx::mbar_wait(bar_full, f_ph);
+                            VQKV_PHASE(1)
+                            f_ph ^= 1;
+                            ptx::tc_fence_after();
+                            // all 128 columns in flight at once, one wait, then the
+                            // accumulator goes back to the MMA issuer before the max trees
+                            float v0[32], v1[32], v2[32], v3[32];
+                            ptx::tmem_ld32(t_acc, v0);
+                            ptx::tmem_ld32(t_acc + 32u, v1);
+                            ptx::tmem_ld32(t_acc + 64u, v2);
+                            ptx::tmem_ld32(t_acc + 96u, v3);
+                            ptx::tc_wait_ld();
+                            ptx::tc_fence_before();
+                            ptx::mbar_arrive(bar_empty);
+                            mA[4 * c] = max32(v0);
+                            mA[4 * c + 1] = max32(v1);
+                            mA[4 * c + 2] = max32(v2);
+                            mA[4 * c + 3] = max32(v3);
+#pragma unroll
+                            for (int b = 0; b < 32; ++b)
+                                mB[b] = ptx::fmax3(mB[b], ptx::fmax3(v0[b], v1[b], v2[b]), v3[b]);
+                        }
+                    }
+                    VQKV_PHASE(2)
+                    // ---- candidates {1024 sb + 32a + b : mA[a] >= m - W, mB[b] >= m - W}
+#pragma unroll
+                    for (int k = 0; k < 4 * kMaxChunks; ++k) m1 = fmaxf(m1, mA[k]);
+                    const float thr = m1 - W;
+                    uint32_t CA = 0, CB = 0;
+#pragma unroll
+                    for (int k = 0; k < 4 * kMaxChunks; ++k) CA |= (mA[k] >= thr ? 1u : 0u) << k;
+#pragma unroll
+                    for (int b = 0; b < 32; ++b) CB |= (mB[b] >= thr ? 1u : 0u) << b;
+                    CAs[sb] = CA;
+                    CBs[sb] = CB;
                 }
+                uint32_t total = 0, zu = 0;
+#pragma unroll
+                for (int sb = 0; sb < kMaxSuper; ++sb) {
+                    const uint32_t cb = uint32_t(__popc(CAs[sb])) * uint32_t(__popc(CBs[sb]));
+                    if (cb == 1u) zu = 1024u * sb + 32u * (__ffs(CAs[sb]) - 1) + (__ffs(CBs[sb]) - 1);
+                    total += cb;
+                }
+                const bool unique = (total == 1u);
+                uint32_t z = unique ? zu : 0u;
+                const bool amb = !unique && valid && !exact_row;
                 VQKV_PHASE(3)
                 if (__any_sync(0xffffffffu, amb)) {
                     // ---- warp-cooperative exact rescoring in the reference's fp32 order
                     // (codebook.cpp:166-172).  The (row, candidate) items of all lanes
                     // are packed 32 per pass; r of the owning row is broadcast by shuffle.
+                    // One round per super-block; the best (score, index) key carries over.
+                    unsigned long long best = ~0ull;
+                    uint32_t cnt_all = 0;
+#pragma unroll 1
+                    for (int sb = 0; sb < int(nsb); ++sb) {
+                    uint32_t CA = CAs[0], CB = CBs[0];
+#pragma unroll
+                    for (int k = 1; k < kMaxSuper; ++k)
+                        if (sb == k) {
+                            CA = CAs[k];
+                            CB = CBs[k];
+                        }
+                    const uint32_t na = __popc(CA), nb = __popc(CB);
                     const uint32_t cnt = amb ? na * nb : 0u;
+                    cnt_all += cnt;
+                    if (!__any_sync(0xffffffffu, cnt != 0u)) continue;
                     uint32_t incl = cnt;
 #pragma unroll
                     for (int off = 1; off < 32; off <<= 1) {
@@ -449,7 +480,6 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     const uint32_t P = incl - cnt;
                     const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
                     const bool any_one = (search_block == 1) || (uint64_t(si.size) % search_block == 1);
-                    unsigned long long best = ~0ull;
                     for (uint32_t base = 0; base < T; base += 32) {
                         const uint32_t it = base + lane;
                         uint32_t o = 0;
@@ -464,7 +494,8 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         uint32_t j = 0xffffffffu;
                         if (it < T) {
                             const uint32_t nbo = __popc(CBo);
-                            j = 32u * uint32_t(__fns(CAo, 0, int(li / nbo) + 1)) + uint32_t(__fns(CBo, 0, int(li % nbo) + 1));
+                            j = 1024u * uint32_t(sb) + 32u * uint32_t(__fns(CAo, 0, int(li / nbo) + 1)) +
+                                uint32_t(__fns(CBo, 0, int(li % nbo) + 1));
                             if (j >= si.size) j = 0xffffffffu;
                         }
                         VQKV_PHASE(5)
@@ -523,12 +554,13 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         }
                         const int head = int(P) - int(base);
                         const unsigned long long got = __shfl_sync(0xffffffffu, key, head < 0 ? 0 : (head > 31 ? 31 : head));
-                        if (amb && P + cnt > base && P < base + 32 && got < best) best = got;
+                        if (cnt != 0u && P + cnt > base && P < base + 32 && got < best) best = got;  // own items only
                         VQKV_PHASE(7)
                     }
+                    }  // super-blocks
                     if (amb) {
                         z = (best == ~0ull) ? 0u : uint32_t(best & 0xffffffffu);
-                        n_rs += cnt;
+                        n_rs += cnt_all;
                         ++n_amb;
                         const float* ez = eff + si.eff_off + uint64_t(z) * 128;
 #pragma unroll
@@ -621,7 +653,7 @@ uint32_t dbg_flags() {
 bool encode_tc_supported(const vqkv_stack_s& st) {
     if (st.dim != 128 || st.d_eff16 == nullptr) return false;
     for (const auto& s : st.stages) {
-        if (s.pad_size > 128u * kMaxChunks) return false;
+        if (s.pad_size > 128u * kMaxChunks * kMaxSuper) return false;
         // ||e||^2 must fit the fp16 ext column, entries the fp16 operand range
         if (!(s.max_sqnorm < 60000.f) || !(s.max_abs < 1073741824.f)) return false;
     }

@@ -77,7 +77,9 @@ def compare(o, p, xs, payload_dev, norms_dev, n_streams=1):
 @pytest.mark.parametrize(
     "seed,n,S,rows,streams",
     [(101, 4, 1024, 300, 1), (102, 16, 512, 200, 2), (103, 3, 256, 257, 3), (104, 2, 100, 129, 1),
-     (105, 1, 1, 40, 1), (106, 5, 384, 128, 2), (107, 56, 1024, 48, 1)],
+     (105, 1, 1, 40, 1), (106, 5, 384, 128, 2), (107, 56, 1024, 48, 1),
+     # configs[3] sweep sizes above 1024: stages span several 1024-entry super-blocks
+     (108, 4, 2048, 150, 1), (109, 2, 4096, 130, 2), (110, 3, 1500, 129, 1), (111, 8, 3000, 64, 1)],
 )
 def test_tc_encode_matches_oracle(torch_mod, seed, n, S, rows, streams):
     rng = O.Rng(seed)
