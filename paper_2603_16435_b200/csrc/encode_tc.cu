@@ -390,8 +390,12 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 const float* sqn_s = sqn_pad + si.pad_off;
                 float m1 = -INFINITY;
                 uint32_t CAs[kMaxSuper], CBs[kMaxSuper];
+                float mbs[kMaxSuper];  // per-block maxima
 #pragma unroll
-                for (int k = 0; k < kMaxSuper; ++k) CAs[k] = CBs[k] = 0u;
+                for (int k = 0; k < kMaxSuper; ++k) {
+                    CAs[k] = CBs[k] = 0u;
+                    mbs[k] = -INFINITY;
+                }
 #pragma unroll
                 for (int sb = 0; sb < kMaxSuper; ++sb) {
                     if (sb >= int(nsb)) break;
@@ -429,8 +433,11 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     }
                     VQKV_PHASE(2)
                     // ---- candidates {1024 sb + 32a + b : mA[a] >= m - W, mB[b] >= m - W}
+                    float mb = -INFINITY;
 #pragma unroll
-                    for (int k = 0; k < 4 * kMaxChunks; ++k) m1 = fmaxf(m1, mA[k]);
+                    for (int k = 0; k < 4 * kMaxChunks; ++k) mb = fmaxf(mb, mA[k]);
+                    mbs[sb] = mb;
+                    m1 = fmaxf(m1, mb);
                     const float thr = m1 - W;
                     uint32_t CA = 0, CB = 0;
 #pragma unroll
@@ -443,6 +450,8 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 uint32_t total = 0, zu = 0;
 #pragma unroll
                 for (int sb = 0; sb < kMaxSuper; ++sb) {
+                    // a block whose maximum is below the final threshold holds no candidate
+                    if (!(mbs[sb] >= m1 - W)) CAs[sb] = CBs[sb] = 0u;
                     const uint32_t cb = uint32_t(__popc(CAs[sb])) * uint32_t(__popc(CBs[sb]));
                     if (cb == 1u) zu = 1024u * sb + 32u * (__ffs(CAs[sb]) - 1) + (__ffs(CBs[sb]) - 1);
                     total += cb;
