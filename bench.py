@@ -448,12 +448,23 @@ def run_ours(args, rank, world, local):
         vnh = torch.empty((ns, middle), dtype=torch.float32, pin_memory=True)
 
         def e2e_step():
-            Dv.quantize_streams_host(kst, Kh, payload_host=kph, norms_host=knh)
-            Dv.quantize_streams_host(vst, Vh, payload_host=vph, norms_host=vnh)
+            # queued back to back (the value copies overlap the key encodes); the
+            # stream synchronization below puts every result on the host
+            Dv.quantize_streams_host(kst, Kh, payload_host=kph, norms_host=knh, blocking=False)
+            Dv.quantize_streams_host(vst, Vh, payload_host=vph, norms_host=vnh, blocking=False)
 
         e2e_step()
         barrier(world)
         torch.cuda.synchronize()
+        # the box's pinned H2D bandwidth (the e2e bound when copies exceed the encode time)
+        probe = torch.empty((min(32, ns),) + tuple(Kh.shape[1:]), dtype=torch.float32, device="cuda")
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record()
+        probe.copy_(Kh[: probe.shape[0]], non_blocking=True)
+        p1.record()
+        torch.cuda.synchronize()
+        h2d_gbps = probe.numel() * 4 / (p0.elapsed_time(p1) / 1e3) / 1e9
+        del probe
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         n_e2e = max(1, min(args.steps, 3))
@@ -466,7 +477,8 @@ def run_ours(args, rank, world, local):
             "value": world * vectors_per_rank / (e_ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": int(Kh.numel() * 4 + Vh.numel() * 4),
             "d2h_bytes_per_step": int(kph.numel() + vph.numel() + knh.numel() * 4 + vnh.numel() * 4),
-            "ms_per_step": e_ms, "api": "vqkv_quantize_batch_host (pinned host buffers)",
+            "ms_per_step": e_ms, "api": "vqkv_quantize_batch_host_async x2 (pinned host buffers), then sync",
+            "h2d_gbps_probe": h2d_gbps,
         }
 
     # ---- decode-step attention (configs[2]; configs[4] when world > 1)

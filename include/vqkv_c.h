@@ -109,6 +109,13 @@ int vqkv_nearest_batch(vqkv_stack_t stack, uint32_t stage, const float* xs_dev, 
 int vqkv_quantize_batch_host(vqkv_stack_t stack, const float* xs_host, uint32_t n_streams,
                              uint64_t rows_per_stream, uint64_t search_block, uint8_t* payload_host,
                              float* residual_norms_host, void* stream);
+/* The same pipeline without blocking the host: the results are on the host
+ * once `stream` has completed (the host buffers must stay alive until then).
+ * Consecutive calls (keys, then values) overlap their copies with each
+ * other's encodes. */
+int vqkv_quantize_batch_host_async(vqkv_stack_t stack, const float* xs_host, uint32_t n_streams,
+                                   uint64_t rows_per_stream, uint64_t search_block, uint8_t* payload_host,
+                                   float* residual_norms_host, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Decode: rows [begin, end) of each stream, out_dev fp32 [n_streams][end-begin][D].
@@ -207,8 +214,11 @@ int vqkv_encode_counters(vqkv_stack_t stack, uint64_t* counters3);
  * prologue, [1] waiting for accumulators, [2] chunk max trees, [3] candidate
  * selection, [4] residual update + next A tile, [5] rescoring pass set-up,
  * [6] rescoring loads + dot products, [7] rescoring min-reduction, [8] code
- * store; [9] the number of rescored (row, candidate) pairs.  Synchronizes. */
-int vqkv_encode_phase_clocks(vqkv_stack_t stack, uint64_t* out10);
+ * store, then inside the update: [9] e_z loads issued + first residual TMEM
+ * load, [10] wait for the e_z gather, [11] rest of the update, ([4] is the
+ * final store-wait + arrive); [13] the number of rescored (row, candidate)
+ * pairs.  Synchronizes. */
+int vqkv_encode_phase_clocks(vqkv_stack_t stack, uint64_t* out14);
 /* number of kernel launches issued by the library since load (all threads) */
 uint64_t vqkv_launch_count(void);
 /* Kernel timing hooks: when enabled, the library records a CUDA event pair on

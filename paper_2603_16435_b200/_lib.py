@@ -65,6 +65,7 @@ _SIGS = {
     "vqkv_quantize_batch": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint64, P, P, P]),
     "vqkv_quantize_batch_ex": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint64, P, P, P, P]),
     "vqkv_quantize_batch_host": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint64, P, P, P]),
+    "vqkv_quantize_batch_host_async": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint64, P, P, P]),
     "vqkv_nearest_batch": (C.c_int, [P, C.c_uint32, P, C.c_uint64, C.c_uint64, P, P, P]),
     "vqkv_reconstruct_block": (C.c_int, [P, P, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, P, P]),
     "vqkv_reconstruct_block_ex": (C.c_int, [P, P, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, P, P]),

@@ -219,16 +219,19 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         if (lane == 0 && (warp & 1) == 0) {
             // ------------------------------------------------------------ producer
             JobIter it(stages, n_stages, n_pairs);
-            uint32_t slot = 0, ph = 0;
+            uint32_t slot = 0, ph = 0, n_loaded = 0;
             while (!it.done) {
                 ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->b_empty[t][slot]), ph ^ 1, kSleepNs);
                 const uint32_t bar = ptx::smem_u32(&ctl->b_full[t][slot]);
-                if (dbg & 4u) {  // timing experiment only: no codebook traffic (wrong codes)
+                if ((dbg & 4u) || ((dbg & 8u) && n_loaded >= uint32_t(kNB))) {
+                    // timing experiments only (wrong codes): bit 2 no codebook traffic at all,
+                    // bit 3 keep re-using the first ring fill (realistic ambiguity, no chunk stream)
                     ptx::mbar_arrive(bar);
                 } else {
                     ptx::mbar_arrive_expect_tx(bar, kChunkBytes);
                     const __half* src = eff16 + stages[it.s].eff16_off + uint64_t(it.c) * (kChunkBytes / 2);
                     ptx::bulk_g2s(ptx::smem_u32(b_ring + (t * kNB + slot) * kChunkBytes), src, kChunkBytes, bar);
+                    ++n_loaded;
                 }
                 if (++slot == kNB) {
                     slot = 0;
@@ -288,13 +291,21 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         unsigned long long n_amb = 0, n_rs = 0, n_rowstages = 0;
         // dbg bit1: per-phase clock totals (lane 0 of each epilogue warp)
         const bool clk_on = (dbg & 2u) && counters && lane == 0;
-        unsigned long long ck[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long ck[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         long long ck_t = clock64();
 #define VQKV_PHASE(k)                          \
     if (clk_on) {                              \
         const long long now_ = clock64();      \
         ck[k] += (unsigned long long)(now_ - ck_t); \
         ck_t = now_;                           \
+    }
+        // clock read ordered after `dep` is available (waits for the load feeding it)
+#define VQKV_PHASE_DEP(k, dep)                                                       \
+    if (clk_on) {                                                                    \
+        long long now_;                                                              \
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(now_) : "f"(dep) : "memory");   \
+        ck[k] += (unsigned long long)(now_ - ck_t);                                  \
+        ck_t = now_;                                                                 \
     }
 
         for (uint64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
@@ -595,8 +606,10 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     float v[32];
                     ptx::tmem_ld32(t_res + 32u * c4, v);
                     ptx::tc_wait_ld();
+                    if (c4 == 0) VQKV_PHASE_DEP(9, v[0])
 #pragma unroll
                     for (int k = 0; k < 32; ++k) v[k] = __fsub_rn(v[k], en[32 * c4 + k]);
+                    if (c4 == 0) VQKV_PHASE_DEP(10, v[31])
                     ptx::tmem_st32(t_res + 32u * c4, v);
                     if (!last) {
 #pragma unroll
@@ -621,6 +634,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         }
                     }
                 }
+                VQKV_PHASE(11)
                 ptx::tc_wait_st();
                 if (!last) {
                     ptx::fence_async_smem();
@@ -638,8 +652,9 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
             }
         }
 #undef VQKV_PHASE
+#undef VQKV_PHASE_DEP
         if (clk_on)
-            for (int k = 0; k < 9; ++k) atomicAdd(&counters[8 + k], ck[k]);
+            for (int k = 0; k < 13; ++k) atomicAdd(&counters[8 + k], ck[k]);
         if (counters) {
             atomicAdd(&counters[0], n_rowstages);
             if (n_amb) atomicAdd(&counters[1], n_amb);

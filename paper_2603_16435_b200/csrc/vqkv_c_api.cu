@@ -3,6 +3,7 @@
 // Validation mirrors the reference's exception behaviour (errors.hpp:12-49,
 // codebook.cpp:41-72 / 225-250, attention.cpp:20-35); CUDA work is enqueued
 // on the caller's stream.
+#include <vector>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -195,6 +196,8 @@ int vqkv_stack_destroy(vqkv_stack_t s) {
         cudaFree(s->d_sqn_pad);
         cudaFree(s->d_error);
         cudaFree(s->d_counters);
+        if (s->cp_in) cudaStreamDestroy(s->cp_in);
+        if (s->cp_out) cudaStreamDestroy(s->cp_out);
         delete s;
     });
 }
@@ -273,8 +276,8 @@ int vqkv_encode_phase_clocks(vqkv_stack_t s, uint64_t* c) {
         VQKV_CUDA(cudaDeviceSynchronize());
         unsigned long long h[32];
         VQKV_CUDA(cudaMemcpy(h, s->d_counters, sizeof(h), cudaMemcpyDeviceToHost));
-        for (int i = 0; i < 9; ++i) c[i] = h[8 + i];
-        c[9] = h[3];
+        for (int i = 0; i < 13; ++i) c[i] = h[8 + i];
+        c[13] = h[3];
     });
 }
 
@@ -322,6 +325,16 @@ int vqkv_quantize_batch_ex(vqkv_stack_t s, const float* xs, uint32_t n_streams, 
 
 int vqkv_quantize_batch_host(vqkv_stack_t s, const float* xs, uint32_t n_streams, uint64_t rows, uint64_t sb,
                              uint8_t* payload, float* norms, void* stream) {
+    const int st = vqkv_quantize_batch_host_async(s, xs, n_streams, rows, sb, payload, norms, stream);
+    if (st != VQKV_OK) return st;
+    return guard([&] {
+        DeviceGuard g(s->device);
+        VQKV_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    });
+}
+
+int vqkv_quantize_batch_host_async(vqkv_stack_t s, const float* xs, uint32_t n_streams, uint64_t rows, uint64_t sb,
+                                   uint8_t* payload, float* norms, void* stream) {
     return guard([&] {
         check_stack(s);
         need(sb >= 1, VQKV_INVALID_INPUT, "search_block must be >= 1");
@@ -333,28 +346,61 @@ int vqkv_quantize_batch_host(vqkv_stack_t s, const float* xs, uint32_t n_streams
         const uint64_t D = s->dim;
         const uint64_t pb = payload_bytes(s->row_bits, rows);
         // chunk over streams: ~256 MiB of input per chunk, two buffer sets so
-        // the copy engines overlap the encoder (H2D i+1 | encode i | D2H i-1)
+        // the copy engines overlap the encoder (H2D i+1 | encode i | D2H i-1);
+        // staging comes from the stream-ordered pool and nothing blocks the host,
+        // so consecutive calls (e.g. K then V) keep the copy engines busy
         uint64_t per_stream_in = rows * D * sizeof(float);
-        uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(n_streams, (256ull << 20) / per_stream_in)));
-        cudaStream_t cp_in, cp_out;
-        VQKV_CUDA(cudaStreamCreateWithFlags(&cp_in, cudaStreamNonBlocking));
-        VQKV_CUDA(cudaStreamCreateWithFlags(&cp_out, cudaStreamNonBlocking));
-        float* dx[2];
-        uint8_t* dp[2];
-        float* dn[2];
-        cudaEvent_t in_ready[2], done[2], out_done[2];
-        for (int b = 0; b < 2; ++b) {
-            VQKV_CUDA(cudaMalloc(&dx[b], per_stream_in * chunk));
-            VQKV_CUDA(cudaMalloc(&dp[b], std::max<uint64_t>(pb * chunk, 1)));
-            VQKV_CUDA(cudaMalloc(&dn[b], sizeof(float) * rows * chunk));
+        // chunk = streams per encode launch: 32-160 MiB of input (short pipeline fill), picking the size
+        // whose tile count best fills whole rounds of the persistent grid (2 tiles
+        // per SM), since every launch otherwise idles part of its last round
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+        const uint64_t slots = 2ull * uint64_t(sms), tiles_ps = (rows + 127) / 128;
+        const uint64_t lo = std::max<uint64_t>(1, (32ull << 20) / per_stream_in);
+        const uint64_t hi = std::max<uint64_t>(lo, (160ull << 20) / per_stream_in);
+        uint32_t chunk = uint32_t(std::min<uint64_t>(n_streams, lo));
+        double best_waste = 2.0;
+        for (uint64_t c = lo; c <= std::min<uint64_t>(hi, n_streams); ++c) {
+            const uint64_t t = c * tiles_ps, rounds = (t + slots - 1) / slots;
+            const double waste = double(rounds * slots - t) / double(rounds * slots);
+            if (waste < best_waste - 1e-3) {
+                best_waste = waste;
+                chunk = uint32_t(c);
+            }
+        }
+        if (!s->cp_in) {
+            VQKV_CUDA(cudaStreamCreateWithFlags(&s->cp_in, cudaStreamNonBlocking));
+            VQKV_CUDA(cudaStreamCreateWithFlags(&s->cp_out, cudaStreamNonBlocking));
+        }
+        cudaStream_t cp_in = s->cp_in, cp_out = s->cp_out;
+        // staging sets: at least two (copy | encode overlap); up to ~4 GiB of HBM so a
+        // call queued behind another one (values behind keys) prefetches its whole
+        // input while the earlier encodes run
+        const uint32_t n_chunks = (n_streams + chunk - 1) / chunk;
+        const uint64_t set_bytes = (per_stream_in + pb + sizeof(float) * rows) * chunk;
+        const uint32_t nbuf = std::min<uint32_t>(n_chunks, std::max<uint32_t>(2, uint32_t((4ull << 30) / set_bytes)));
+        std::vector<float*> dx(nbuf), dn(nbuf);
+        std::vector<uint8_t*> dp(nbuf);
+        std::vector<cudaEvent_t> in_ready(nbuf), done(nbuf), out_done(nbuf);
+        cudaEvent_t alloc_ev, last;
+        for (uint32_t b = 0; b < nbuf; ++b) {
+            // allocated in the copy-in stream's order: the copies of a call queued
+            // behind another call's encodes start at once (not after those encodes)
+            VQKV_CUDA(cudaMallocAsync(&dx[b], per_stream_in * chunk, cp_in));
+            VQKV_CUDA(cudaMallocAsync(&dp[b], std::max<uint64_t>(pb * chunk, 1), cp_in));
+            VQKV_CUDA(cudaMallocAsync(&dn[b], sizeof(float) * rows * chunk, cp_in));
             VQKV_CUDA(cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming));
             VQKV_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
             VQKV_CUDA(cudaEventCreateWithFlags(&out_done[b], cudaEventDisableTiming));
-            VQKV_CUDA(cudaEventRecord(out_done[b], cp_out));
         }
-        int i = 0;
+        VQKV_CUDA(cudaEventCreateWithFlags(&alloc_ev, cudaEventDisableTiming));
+        VQKV_CUDA(cudaEventCreateWithFlags(&last, cudaEventDisableTiming));
+        VQKV_CUDA(cudaEventRecord(alloc_ev, cp_in));  // staging allocated (copy-in stream order)
+        VQKV_CUDA(cudaStreamWaitEvent(cp_out, alloc_ev, 0));
+        for (uint32_t b = 0; b < nbuf; ++b) VQKV_CUDA(cudaEventRecord(out_done[b], cp_out));
+        uint32_t i = 0;
         for (uint32_t s0 = 0; s0 < n_streams; s0 += chunk, ++i) {
-            const int b = i & 1;
+            const uint32_t b = i % nbuf;
             const uint32_t ns = std::min<uint32_t>(chunk, n_streams - s0);
             VQKV_CUDA(cudaStreamWaitEvent(cp_in, out_done[b], 0));  // buffer b free again
             VQKV_CUDA(cudaMemcpyAsync(dx[b], xs + uint64_t(s0) * rows * D, per_stream_in * ns, cudaMemcpyHostToDevice,
@@ -369,18 +415,20 @@ int vqkv_quantize_batch_host(vqkv_stack_t s, const float* xs, uint32_t n_streams
                                       cudaMemcpyDeviceToHost, cp_out));
             VQKV_CUDA(cudaEventRecord(out_done[b], cp_out));
         }
-        VQKV_CUDA(cudaStreamSynchronize(cp_out));
-        VQKV_CUDA(cudaStreamSynchronize(cs));
-        for (int b = 0; b < 2; ++b) {
-            cudaFree(dx[b]);
-            cudaFree(dp[b]);
-            cudaFree(dn[b]);
-            cudaEventDestroy(in_ready[b]);
+        // the caller's stream completes only after the last copy-out; staging is
+        // returned to the pool in stream order behind it
+        VQKV_CUDA(cudaEventRecord(last, cp_out));
+        VQKV_CUDA(cudaStreamWaitEvent(cs, last, 0));
+        for (uint32_t b = 0; b < nbuf; ++b) {
+            VQKV_CUDA(cudaFreeAsync(dx[b], cs));
+            VQKV_CUDA(cudaFreeAsync(dp[b], cs));
+            VQKV_CUDA(cudaFreeAsync(dn[b], cs));
+            cudaEventDestroy(in_ready[b]);  // released once complete
             cudaEventDestroy(done[b]);
             cudaEventDestroy(out_done[b]);
         }
-        cudaStreamDestroy(cp_in);
-        cudaStreamDestroy(cp_out);
+        cudaEventDestroy(alloc_ev);
+        cudaEventDestroy(last);
     });
 }
 

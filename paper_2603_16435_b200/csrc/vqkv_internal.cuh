@@ -91,6 +91,7 @@ struct vqkv_stack_s {
     uint64_t total_rows = 0, total_pad_rows = 0;
     int* d_error = nullptr;                   // sticky device error flag
     unsigned long long* d_counters = nullptr; // encode diagnostics [4]
+    cudaStream_t cp_in = nullptr, cp_out = nullptr;  // host-buffer pipeline copy streams (lazy)
     std::mutex mu;
 };
 

@@ -90,8 +90,12 @@ def quantize_streams(
 
 
 def quantize_streams_host(stack, xs_host: torch.Tensor, search_block: int = DEFAULT_SEARCH_BLOCK,
-                          payload_host: Optional[torch.Tensor] = None, norms_host: Optional[torch.Tensor] = None):
-    """quantize_batch with host (ideally pinned) buffers: H2D, encode, D2H inside the call."""
+                          payload_host: Optional[torch.Tensor] = None, norms_host: Optional[torch.Tensor] = None,
+                          blocking: bool = True):
+    """quantize_batch with host (ideally pinned) buffers: H2D, encode, D2H inside the call.
+
+    blocking=False returns once the work is queued on the current stream; the host
+    buffers hold the results after that stream synchronizes (and must stay alive)."""
     dev = _dev(stack)
     if xs_host.dim() == 2:
         xs_host = xs_host.unsqueeze(0)
@@ -105,8 +109,8 @@ def quantize_streams_host(stack, xs_host: torch.Tensor, search_block: int = DEFA
         norms_host = torch.empty((ns, rows), dtype=torch.float32, pin_memory=xs_host.is_pinned())
     s = torch.cuda.current_stream(torch.device("cuda", dev.device)).cuda_stream
     _lib.call(
-        "vqkv_quantize_batch_host", dev.h, xs_host.data_ptr(), ns, rows, search_block,
-        payload_host.data_ptr(), norms_host.data_ptr(), s,
+        "vqkv_quantize_batch_host" if blocking else "vqkv_quantize_batch_host_async", dev.h, xs_host.data_ptr(), ns,
+        rows, search_block, payload_host.data_ptr(), norms_host.data_ptr(), s,
     )
     return payload_host, norms_host
 

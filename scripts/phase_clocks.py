@@ -12,18 +12,18 @@ st = P.CodebookStack.from_arrays([g.standard_normal((S, 128), dtype=np.float32) 
 x = torch.randn(streams, 31740, 128, device='cuda')
 Dv.quantize_streams(st, x); torch.cuda.synchronize()
 L = _lib.load()
-base = (ctypes.c_uint64 * 10)()
+base = (ctypes.c_uint64 * 14)()
 L.vqkv_encode_phase_clocks(Dv._dev(st).h, base)
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record(); Dv.quantize_streams(st, x); e.record(); torch.cuda.synchronize()
-out = (ctypes.c_uint64 * 10)()
+out = (ctypes.c_uint64 * 14)()
 L.vqkv_encode_phase_clocks(Dv._dev(st).h, out)
-d = [out[k] - base[k] for k in range(10)]
+d = [out[k] - base[k] for k in range(14)]
 warps = 8 * 148
 ms = s.elapsed_time(e)
 print(f"n={n} S={S} streams={streams}: {ms:.2f} ms  (~{ms*1.9e6:.3g} clk per warp at 1.9 GHz)")
-names = ["prologue", "acc wait", "chunk max", "candidates", "update+A", "rs setup", "rs load+dot", "rs min", "code store"]
-tot = sum(d[:9])
-for k in range(9):
+names = ["prologue", "acc wait", "chunk max", "candidates", "upd: st-wait+arrive", "rs setup", "rs load+dot", "rs min", "code store", "upd: issue+ld0", "upd: e_z wait", "upd: rest", "-"]
+tot = sum(d[:12])
+for k in range(12):
     print(f"  {names[k]:13s} {d[k]/warps:12.4g} clk/warp  {100*d[k]/tot:5.1f}%")
-print("  rescored pairs", d[9])
+print("  rescored pairs", d[13])
