@@ -55,11 +55,11 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, verbose=False):
-    obj = os.path.join(OBJ_DIR, os.path.basename(src) + ".o")
+def _compile(src, verbose=False, obj_dir=OBJ_DIR, extra=()):
+    obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
     if not _stale(obj, [src] + _headers()):
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -82,6 +82,27 @@ def build(verbose: bool = False) -> str:
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     return LIB
+
+
+DIAG_DIR = os.path.join(ROOT, "build", "diag")
+DIAG_LIB = os.path.join(DIAG_DIR, "libvqkv_b200.so")
+
+
+def build_diag() -> str:
+    """Diagnostics build with the encoder's per-phase clock counters compiled in
+    (-DVQKV_PHASE_CLOCKS; read by vqkv_encode_phase_clocks, scripts/phase_clocks.py).
+    Not the product library: load it with VQKV_LIB=build/diag/libvqkv_b200.so."""
+    obj_dir = os.path.join(DIAG_DIR, "obj")
+    os.makedirs(obj_dir, exist_ok=True)
+    srcs = _sources()
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+        objs = list(ex.map(lambda s: _compile(s, False, obj_dir, ("-DVQKV_PHASE_CLOCKS",)), srcs))
+    if _stale(DIAG_LIB, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", DIAG_LIB, *objs, "-cudart", "static", "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    return DIAG_LIB
 
 
 CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_cpp_api.cpp")

@@ -52,13 +52,14 @@ constexpr uint32_t kATileBytes = 36864;   // 128 rows x (128 + 16) fp16
 constexpr uint32_t kExtOff = 32768;       // the 16-wide K block (||e||^2 / row scale)
 constexpr int kMaxChunks = 8;            // chunks per super-block (1024 entries)
 constexpr int kMaxSuper = 4;             // super-blocks per stage: S <= 4096
+constexpr uint32_t kSmemStages = 128;     // stage descriptors cached in smem
 // One N=128 MMA group per 128-entry chunk.  (Splitting a chunk into two N=64
 // halves to double-buffer the accumulator was measured slower: SS-mode MMAs
 // re-read A from shared memory per instruction, and at N=64 that pushes the
 // operand traffic to 192 B/clk, above the ~128 B/clk smem path.)
 constexpr uint32_t kIdesc = ptx::idesc_f16_f32(128, 128);
 // register split: 128 x kCtlRegs + 256 x kEpiRegs <= 64K (launch allocation 168)
-constexpr uint32_t kCtlRegs = 40, kEpiRegs = 224;
+constexpr uint32_t kCtlRegs = 56, kEpiRegs = 224;
 constexpr uint32_t kSleepNs = 1000000;  // control-thread barrier suspend hint
 
 struct __align__(8) SmemCtl {
@@ -68,6 +69,10 @@ struct __align__(8) SmemCtl {
     uint64_t acc_empty[2];
     uint64_t a_ready[2];
     uint32_t tmem_base;
+    // the first kSmemStages stage descriptors (global loads would miss L1, which the
+    // 217 KB of operand buffers leave small); pad_ = 1 when the stage's last search
+    // block holds a single entry (Eigen's 1-row GEMV uses the dot order for it)
+    StageInfo st[kSmemStages];
 };
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + 2 * kATileBytes + 2 * kNB * kChunkBytes + sizeof(SmemCtl);
 
@@ -196,6 +201,11 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         }
         ptx::fence_mbar_init();
     }
+    for (uint32_t i = threadIdx.x; i < n_stages && i < kSmemStages; i += blockDim.x) {
+        StageInfo si = stages[i];
+        si.pad_ = (search_block == 1 || uint64_t(si.size) % search_block == 1) ? 1.f : 0.f;
+        ctl->st[i] = si;
+    }
     if (warp == 2) {
         ptx::tmem_alloc(ptx::smem_u32(&ctl->tmem_base), 512);
         ptx::tmem_relinquish();
@@ -204,6 +214,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = ctl->tmem_base;
+    const StageInfo* stg = (n_stages <= kSmemStages) ? ctl->st : stages;  // producer / MMA stage walk
     // control warpgroup (producer / MMA threads) hands registers to the epilogue
     if (warp < 4)
         ptx::reg_dealloc<kCtlRegs>();
@@ -218,7 +229,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         const uint32_t t = warp >> 1;
         if (lane == 0 && (warp & 1) == 0) {
             // ------------------------------------------------------------ producer
-            JobIter it(stages, n_stages, n_pairs);
+            JobIter it(stg, n_stages, n_pairs);
             uint32_t slot = 0, ph = 0, n_loaded = 0;
             while (!it.done) {
                 ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->b_empty[t][slot]), ph ^ 1, kSleepNs);
@@ -229,7 +240,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     ptx::mbar_arrive(bar);
                 } else {
                     ptx::mbar_arrive_expect_tx(bar, kChunkBytes);
-                    const __half* src = eff16 + stages[it.s].eff16_off + uint64_t(it.c) * (kChunkBytes / 2);
+                    const __half* src = eff16 + stg[it.s].eff16_off + uint64_t(it.c) * (kChunkBytes / 2);
                     ptx::bulk_g2s(ptx::smem_u32(b_ring + (t * kNB + slot) * kChunkBytes), src, kChunkBytes, bar);
                     ++n_loaded;
                 }
@@ -241,7 +252,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
             }
         } else if (lane == 0) {
             // ------------------------------------------------------------ MMA issuer
-            JobIter it(stages, n_stages, n_pairs);
+            JobIter it(stg, n_stages, n_pairs);
             uint32_t slot = 0, ph = 0, a_ph = 0, e_ph = 1;
             const uint32_t a_base = ptx::smem_u32(a_tiles) + t * kATileBytes;
             const uint32_t b_base = ptx::smem_u32(b_ring);
@@ -289,15 +300,17 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         uint8_t* a_tile = a_tiles + t * kATileBytes;
         uint32_t f_ph = 0;
         unsigned long long n_amb = 0, n_rs = 0, n_rowstages = 0;
-        // dbg bit1: per-phase clock totals (lane 0 of each epilogue warp)
+        // per-phase clock totals (lane 0 of each epilogue warp, dbg bit 1): compiled in
+        // only for diagnostics builds (VQKV_PHASE_CLOCKS), they cost ~28 registers
+#ifdef VQKV_PHASE_CLOCKS
         const bool clk_on = (dbg & 2u) && counters && lane == 0;
         unsigned long long ck[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         long long ck_t = clock64();
-#define VQKV_PHASE(k)                          \
-    if (clk_on) {                              \
-        const long long now_ = clock64();      \
+#define VQKV_PHASE(k)                               \
+    if (clk_on) {                                   \
+        const long long now_ = clock64();           \
         ck[k] += (unsigned long long)(now_ - ck_t); \
-        ck_t = now_;                           \
+        ck_t = now_;                                \
     }
         // clock read ordered after `dep` is available (waits for the load feeding it)
 #define VQKV_PHASE_DEP(k, dep)                                                       \
@@ -307,6 +320,10 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         ck[k] += (unsigned long long)(now_ - ck_t);                                  \
         ck_t = now_;                                                                 \
     }
+#else
+#define VQKV_PHASE(k) {}  // a complete (empty) statement: call sites follow `if (...)`
+#define VQKV_PHASE_DEP(k, dep) {}
+#endif
 
         for (uint64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
             const Tile tl = tile_of(2 * p + t, tiles_per_stream, rows, n_tiles);
@@ -382,7 +399,23 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
             VQKV_PHASE(0)
 
             for (uint32_t s = 0; s < n_stages; ++s) {
-                const StageInfo si = stages[s];
+                const StageInfo& si = (s < kSmemStages) ? ctl->st[s] : stages[s];
+                const bool any_one_s = (s < kSmemStages) ? (si.pad_ != 0.f)
+                                                         : (search_block == 1 || uint64_t(si.size) % search_block == 1);
+                if (dbg & 32u) {
+                    // timing experiment only (wrong codes): the epilogue just drains the
+                    // accumulators and re-releases the A tile -- the bare MMA pipeline
+                    const uint32_t nchx = si.pad_size / 128;
+                    for (uint32_t c = 0; c < nchx; ++c) {
+                        ptx::mbar_wait(bar_full, f_ph);
+                        f_ph ^= 1;
+                        ptx::tc_fence_after();
+                        ptx::tc_fence_before();
+                        ptx::mbar_arrive(bar_empty);
+                    }
+                    if (s + 1 < n_stages) ptx::mbar_arrive(bar_aready);
+                    continue;
+                }
                 // ---- error window ("exactness of the tensor-core encoder")
                 const float R = sqrtf(R2 * 1.0001f);
                 const float E = si.max_norm;
@@ -499,7 +532,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     }
                     const uint32_t P = incl - cnt;
                     const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
-                    const bool any_one = (search_block == 1) || (uint64_t(si.size) % search_block == 1);
+                    const bool any_one = any_one_s;
                     for (uint32_t base = 0; base < T; base += 32) {
                         const uint32_t it = base + lane;
                         uint32_t o = 0;
@@ -513,9 +546,14 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         const uint32_t CBo = __shfl_sync(0xffffffffu, CB, o);
                         uint32_t j = 0xffffffffu;
                         if (it < T) {
+                            // item li of the owner -> (a, b) = (li / nb)-th set bit of CA, (li % nb)-th of CB
                             const uint32_t nbo = __popc(CBo);
-                            j = 1024u * uint32_t(sb) + 32u * uint32_t(__fns(CAo, 0, int(li / nbo) + 1)) +
-                                uint32_t(__fns(CBo, 0, int(li % nbo) + 1));
+                            const uint32_t qa = uint32_t((float(li) + 0.5f) * __frcp_rn(float(nbo)));  // exact: li < 2^16
+                            const uint32_t rb = li - qa * nbo;
+                            uint32_t ma = CAo, mbb = CBo;
+                            for (uint32_t k = 0; k < qa; ++k) ma &= ma - 1u;
+                            for (uint32_t k = 0; k < rb; ++k) mbb &= mbb - 1u;
+                            j = 1024u * uint32_t(sb) + 32u * uint32_t(__ffs(ma) - 1) + uint32_t(__ffs(mbb) - 1);
                             if (j >= si.size) j = 0xffffffffu;
                         }
                         VQKV_PHASE(5)
@@ -599,8 +637,14 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 float R2n = 0.f, mxn = 0.f;
                 float n0[4] = {0.f, 0.f, 0.f, 0.f}, n1[4] = {0.f, 0.f, 0.f, 0.f};
                 float en[128];  // e_z in one L2 round trip
+                if (dbg & 16u) {  // timing experiment only: no e_z gather (wrong residuals)
 #pragma unroll
-                for (int kk = 0; kk < 16; ++kk) ptx::ldg256_na(reinterpret_cast<const float*>(ez4) + 8 * kk, en + 8 * kk);
+                    for (int k = 0; k < 128; ++k) en[k] = 0.f;
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < 16; ++kk)
+                        ptx::ldg256_na(reinterpret_cast<const float*>(ez4) + 8 * kk, en + 8 * kk);
+                }
 #pragma unroll
                 for (int c4 = 0; c4 < 4; ++c4) {
                     float v[32];
@@ -653,8 +697,10 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         }
 #undef VQKV_PHASE
 #undef VQKV_PHASE_DEP
+#ifdef VQKV_PHASE_CLOCKS
         if (clk_on)
             for (int k = 0; k < 13; ++k) atomicAdd(&counters[8 + k], ck[k]);
+#endif
         if (counters) {
             atomicAdd(&counters[0], n_rowstages);
             if (n_amb) atomicAdd(&counters[1], n_amb);

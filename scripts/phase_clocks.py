@@ -1,6 +1,8 @@
 """Per-phase epilogue clock breakdown of the tensor-core encoder (dev aid; VQKV_DBG=2)."""
 import os, sys, ctypes
 os.environ["VQKV_DBG"] = os.environ.get("VQKV_DBG", "2")
+# the phase counters exist only in the diagnostics build (python -c "from paper_2603_16435_b200 import build; build.build_diag()")
+os.environ.setdefault("VQKV_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "build", "diag", "libvqkv_b200.so"))
 import numpy as np, torch
 sys.path.insert(0, '.')
 from paper_2603_16435_b200 import codebook as P, device as Dv, _lib
