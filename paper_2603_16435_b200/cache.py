@@ -229,3 +229,45 @@ class DeviceCacheState:
             self.init_k[:, :ni] if ni else None, self.init_v[:, :ni] if ni else None,
             self.tail_k[:, :nt] if nt else None, self.tail_v[:, :nt] if nt else None,
             scale=scale, want_lse=want_lse)
+
+    def fidelity(self, original_keys: torch.Tensor, original_values: torch.Tensor, queries: torch.Tensor,
+                 scale: float = 0.0) -> Dict[str, torch.Tensor]:
+        """FidelityReport per stream (attention.cpp:90-134): attention over the cache against
+        attention over the original rows, and the compressed rows' reconstruction MSE.
+
+        original_keys [S, L, Dk] / original_values [S, L, Dv] (L = total_len), queries [S, Q, Dk].
+        Returns float64 tensors [S]: output_max_abs_err, output_mean_cosine,
+        key_intermediate_mse, value_intermediate_mse."""
+        L = self.total_len()
+        for t, nm, d in ((original_keys, "original_keys", self.kd.dim), (original_values, "original_values",
+                                                                          self.vd.dim)):
+            if t.dim() != 3 or t.shape[0] != self.n_streams or t.shape[1] != L:
+                raise InvalidInput("originals length does not match cache length")
+            if t.shape[2] != d:
+                raise InvalidInput("originals dimensions do not match the cache")
+        if queries.dim() != 3 or queries.shape[0] != self.n_streams or queries.shape[1] < 1 \
+                or queries.shape[2] != self.kd.dim:
+            raise InvalidInput("queries must be nonempty with the key dimension")
+        comp, _ = self.attend(queries.contiguous(), scale=scale, want_lse=False)
+        # the reference's attend_raw over the originals: the same kernel with every row raw
+        raw, _ = Dv.attend_decode(self.kstack, self.vstack, queries.contiguous(), None, None, 0, None, None,
+                                  original_keys.contiguous(), original_values.contiguous(), scale=scale,
+                                  want_lse=False)
+        c64, r64 = comp.double(), raw.double()
+        max_err = (comp - raw).abs().amax(dim=(1, 2)).double()
+        cn, rn = c64.norm(dim=2), r64.norm(dim=2)
+        denom = cn * rn
+        cos = torch.where(denom > 0, (c64 * r64).sum(dim=2) / torch.where(denom > 0, denom, torch.ones_like(denom)),
+                          ((cn == 0) & (rn == 0)).double())
+        out = dict(output_max_abs_err=max_err, output_mean_cosine=cos.mean(dim=1),
+                   key_intermediate_mse=torch.zeros(self.n_streams, dtype=torch.float64, device=self.device),
+                   value_intermediate_mse=torch.zeros(self.n_streams, dtype=torch.float64, device=self.device))
+        if self.n_comp > 0:
+            f, n = self.n_init, self.n_comp
+            rk = Dv.reconstruct_streams(self.kstack, self._payload(0), n, 0, n)
+            rv = Dv.reconstruct_streams(self.vstack, self._payload(1), n, 0, n)
+            dk = (original_keys[:, f:f + n] - rk).double()
+            dvv = (original_values[:, f:f + n] - rv).double()
+            out["key_intermediate_mse"] = (dk * dk).sum(dim=2).mean(dim=1)
+            out["value_intermediate_mse"] = (dvv * dvv).sum(dim=2).mean(dim=1)
+        return out

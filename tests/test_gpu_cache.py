@@ -174,3 +174,39 @@ def test_payload_append_bit_offsets(torch_mod):
         got = dst.cpu().numpy()
         for i in range(2):
             assert np.array_equal(got[i, : len(full)], np.frombuffer(bytes(full), np.uint8)), cut
+
+
+@pytest.mark.parametrize("D", [8, 128])
+def test_cache_fidelity_vs_oracle(torch_mod, D):
+    """fidelity (attention.cpp:90-134): reconstruction MSE exact, attention-based fields within tolerance."""
+    torch = torch_mod
+    from paper_2603_16435_b200.cache import DeviceCacheState
+
+    rng = O.Rng(7400 + D)
+    ks, vs = rng.stack(3, 32, D, O.KEY), rng.stack(2, 16, D, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    S, L, Q = 2, 40, 4
+    refs = [O.Cache(ks, vs, 3, 8, False) for _ in range(S)]
+    dc = DeviceCacheState(pk, pv, S, 3, 8)
+    keys = rng.matrix(S * L, D).reshape(S, L, D)
+    vals = rng.matrix(S * L, D).reshape(S, L, D)
+    for i, r in enumerate(refs):
+        r.prefill(keys[i], vals[i])
+    dc.prefill(torch.from_numpy(keys).cuda(), torch.from_numpy(vals).cuda())
+    q = rng.matrix(S * Q, D).reshape(S, Q, D)
+    rep = dc.fidelity(torch.from_numpy(keys).cuda(), torch.from_numpy(vals).cuda(), torch.from_numpy(q).cuda())
+    for i, r in enumerate(refs):
+        comp = np.stack([r.attend(q[i, j]) for j in range(Q)]).astype(np.float64)
+        raw = np.stack([O.attend_raw(keys[i], vals[i], q[i, j]) for j in range(Q)]).astype(np.float64)
+        ref_err = np.abs(comp - raw).max()
+        cos = np.mean([(c @ w) / (np.linalg.norm(c) * np.linalg.norm(w)) for c, w in zip(comp, raw)])
+        tol = ATT_TOL * max(1.0, np.abs(raw).max())
+        assert abs(rep["output_max_abs_err"][i].item() - ref_err) <= 2 * tol
+        assert abs(rep["output_mean_cosine"][i].item() - cos) <= 1e-3
+        rk, rv, ex = r.view_block(0, L)
+        mid = ~ex
+        kmse = np.mean(np.sum((keys[i][mid].astype(np.float64) - rk[mid]) ** 2, axis=1))
+        vmse = np.mean(np.sum((vals[i][mid].astype(np.float64) - rv[mid]) ** 2, axis=1))
+        # the reference evaluates these in fp32 (MatrixF arithmetic): fp32-level agreement
+        assert abs(rep["key_intermediate_mse"][i].item() - kmse) <= 1e-6 * max(1.0, kmse)
+        assert abs(rep["value_intermediate_mse"][i].item() - vmse) <= 1e-6 * max(1.0, vmse)
