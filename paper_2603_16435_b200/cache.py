@@ -271,3 +271,147 @@ class DeviceCacheState:
             out["key_intermediate_mse"] = (dk * dk).sum(dim=2).mean(dim=1)
             out["value_intermediate_mse"] = (dvv * dvv).sum(dim=2).mean(dim=1)
         return out
+
+    # ---- VQKS snapshots (kv_cache.cpp:206-312), one file per stream ------------------
+    def save_snapshot(self, stream: int, out) -> None:
+        """Write stream `stream` as the reference's VQKS snapshot (byte layout of
+        CacheState::save_snapshot).  `out` is a path or a binary file object."""
+        import struct
+
+        from .codebook import CodeMatrix, stack_content_hash
+        from .errors import IoError
+
+        if isinstance(out, str):
+            try:
+                with open(out, "wb") as f:
+                    return self.save_snapshot(stream, f)
+            except OSError as e:
+                raise IoError(f"cannot open {out} for writing") from e
+        if not 0 <= stream < self.n_streams:
+            raise InvalidInput(f"stream {stream} out of range")
+        i = stream
+        w = out.write
+        w(b"VQKS")
+        w(struct.pack("<IQQBBQII", 1, self.init_len, self.local_len, int(self.eager), int(self.prefilled),
+                      self.total_len(), self.kd.dim, self.vd.dim))
+        w(struct.pack("<QQQ", stack_content_hash(self.kstack), stack_content_hash(self.vstack), self.batched))
+        for t in (self.init_k, self.init_v):
+            w(struct.pack("<Q", self.n_init))
+            w(t[i, : self.n_init].contiguous().cpu().numpy().tobytes())
+        for which, sizes in ((0, self.kd.sizes), (1, self.vd.sizes)):
+            pay, _ = self.codes(which)
+            CodeMatrix.from_payload(sizes, pay[i].cpu().numpy(), self.n_comp).save(out)
+        w(self.knorm[i, : self.n_comp].contiguous().cpu().numpy().tobytes())
+        w(self.vnorm[i, : self.n_comp].contiguous().cpu().numpy().tobytes())
+        p = self.pending
+        for t, a, b in ((self.tail_k, 0, p), (self.tail_v, 0, p), (self.tail_k, p, self.n_tail),
+                        (self.tail_v, p, self.n_tail)):
+            w(struct.pack("<Q", b - a))
+            w(t[i, a:b].contiguous().cpu().numpy().tobytes())
+
+    @classmethod
+    def load_snapshots(cls, sources, key_stack, value_stack, device=None) -> "DeviceCacheState":
+        """CacheState::load_snapshot of one VQKS file per stream into one batched cache.
+        All snapshots must share policy and segment lengths (streams step in lockstep)."""
+        import io
+        import struct
+
+        import numpy as np
+
+        from .codebook import CodeMatrix, stack_content_hash
+        from .errors import FormatError, IoError
+
+        parsed = []
+        for src in sources:
+            if isinstance(src, str):
+                try:
+                    with open(src, "rb") as f:
+                        data = f.read()
+                except OSError as e:
+                    raise IoError(f"cannot open {src}") from e
+            else:
+                data = src.read()
+            inp = io.BytesIO(data)
+            off = 0
+
+            def rd(fmt, what):
+                nonlocal off
+                n = struct.calcsize(fmt)
+                b = inp.read(n)
+                if len(b) != n:
+                    raise FormatError(f"truncated file reading {what}", off)
+                off += n
+                return struct.unpack(fmt, b)[0]
+
+            def rd_f32(count, dim, what):
+                nonlocal off
+                nb = 4 * count * dim
+                b = inp.read(nb)
+                if len(b) != nb:
+                    raise FormatError(f"truncated file reading {what}", off)
+                off += nb
+                return np.frombuffer(b, np.float32).reshape(count, dim).copy()
+
+            if inp.read(4) != b"VQKS":
+                raise FormatError("bad magic (expected VQKS)", 0)
+            off = 4
+            version = rd("<I", "version")
+            if version != 1:
+                raise FormatError(f"unsupported snapshot version {version}", off - 4)
+            init_len, local_len = rd("<Q", "init_len"), rd("<Q", "local_len")
+            eager, prefilled = rd("<B", "eager flag") != 0, rd("<B", "prefilled flag") != 0
+            stored_len = rd("<Q", "total_len")
+            dk, dv = rd("<I", "key dim"), rd("<I", "value dim")
+            if dk != key_stack.dim() or dv != value_stack.dim():
+                raise InvalidInput("snapshot dimensions do not match the supplied stacks")
+            kh, vh = rd("<Q", "key stack hash"), rd("<Q", "value stack hash")
+            if kh != stack_content_hash(key_stack) or vh != stack_content_hash(value_stack):
+                raise InvalidInput("snapshot was built against different codebook stacks")
+            batched = rd("<Q", "compression count")
+            init_k = rd_f32(rd("<Q", "init keys"), dk, "init keys")
+            init_v = rd_f32(rd("<Q", "init values"), dv, "init values")
+            kc, off = CodeMatrix.load(inp, off)
+            vc, off = CodeMatrix.load(inp, off)
+            kn = rd_f32(kc.rows(), 1, "key residual norms")[:, 0]
+            vn = rd_f32(vc.rows(), 1, "value residual norms")[:, 0]
+            pend_k = rd_f32(rd("<Q", "pending keys"), dk, "pending keys")
+            pend_v = rd_f32(rd("<Q", "pending values"), dv, "pending values")
+            loc_k = rd_f32(rd("<Q", "local keys"), dk, "local keys")
+            loc_v = rd_f32(rd("<Q", "local values"), dv, "local values")
+            if len(init_k) + kc.rows() + len(pend_k) + len(loc_k) != stored_len:
+                raise FormatError("segment lengths do not add up to total_len", off)
+            parsed.append(dict(policy=(init_len, local_len, eager), prefilled=prefilled, batched=batched,
+                               init=(init_k, init_v), codes=(kc, vc), norms=(kn, vn), pending=(pend_k, pend_v),
+                               local=(loc_k, loc_v)))
+        if not parsed:
+            raise InvalidInput("no snapshots given")
+        first = parsed[0]
+        shape = lambda d: (d["policy"], d["prefilled"], d["batched"], len(d["init"][0]), d["codes"][0].rows(),
+                           len(d["pending"][0]), len(d["local"][0]))
+        if any(shape(d) != shape(first) for d in parsed):
+            raise InvalidInput("snapshots of one batched cache must share policy and segment lengths")
+        il, ll, eg = first["policy"]
+        cache = cls(key_stack, value_stack, len(parsed), il, ll, eg, device, capacity_rows=first["codes"][0].rows())
+        dev = cache.device
+        t = lambda arrs: torch.from_numpy(np.stack(arrs)).to(dev)
+        ni, nc = len(first["init"][0]), first["codes"][0].rows()
+        npd, nl = len(first["pending"][0]), len(first["local"][0])
+        if npd + nl > 2 * ll:
+            raise FormatError("pending + local rows exceed the window capacity", 0)
+        if ni:
+            cache.init_k[:, :ni] = t([d["init"][0] for d in parsed])
+            cache.init_v[:, :ni] = t([d["init"][1] for d in parsed])
+        if nc:
+            kb, vb = cache.kd.payload_bytes(nc), cache.vd.payload_bytes(nc)
+            cache.kpay[:, :kb] = t([d["codes"][0].payload() for d in parsed])
+            cache.vpay[:, :vb] = t([d["codes"][1].payload() for d in parsed])
+            cache.knorm[:, :nc] = t([d["norms"][0] for d in parsed])
+            cache.vnorm[:, :nc] = t([d["norms"][1] for d in parsed])
+        for j, (a, b) in enumerate(((0, npd), (npd, npd + nl))):
+            src = "pending" if j == 0 else "local"
+            if b > a:
+                cache.tail_k[:, a:b] = t([d[src][0] for d in parsed])
+                cache.tail_v[:, a:b] = t([d[src][1] for d in parsed])
+        cache.n_init, cache.n_comp, cache.n_tail = ni, nc, npd + nl
+        cache.prefilled, cache.batched = first["prefilled"], first["batched"]
+        return cache

@@ -210,3 +210,70 @@ def test_cache_fidelity_vs_oracle(torch_mod, D):
         # the reference evaluates these in fp32 (MatrixF arithmetic): fp32-level agreement
         assert abs(rep["key_intermediate_mse"][i].item() - kmse) <= 1e-6 * max(1.0, kmse)
         assert abs(rep["value_intermediate_mse"][i].item() - vmse) <= 1e-6 * max(1.0, vmse)
+
+
+def _vqks_from_oracle(r, ks, vs, init_len, local_len, eager, prefilled, kst_host, vst_host):
+    """An independent restatement of CacheState::save_snapshot (kv_cache.cpp:206-245) built
+    from the oracle cache's observable state -- the expected bytes for one stream."""
+    import struct
+
+    from paper_2603_16435_b200.codebook import stack_content_hash
+
+    c = r.counts()
+    L = c["total"]
+    k, v, ex = r.view_block(0, L)
+    ni, nc, npd = c["init"], c["compressed"], c["pending"]
+    kp, kn = r.codes(0)
+    vp, vn = r.codes(1)
+    b = b"VQKS" + struct.pack("<IQQBBQII", 1, init_len, local_len, int(eager), int(prefilled), L, ks.dim, vs.dim)
+    b += struct.pack("<QQQ", stack_content_hash(kst_host), stack_content_hash(vst_host), c["batched"])
+    b += struct.pack("<Q", ni) + k[:ni].tobytes() + struct.pack("<Q", ni) + v[:ni].tobytes()
+    for st, pay in ((ks, kp), (vs, vp)):
+        b += struct.pack("<I", st.n) + b"".join(struct.pack("<I", x) for x in st.sizes) + struct.pack("<Q", nc)
+        b += bytes(pay)
+    b += kn.tobytes() + vn.tobytes()
+    t0 = ni + nc
+    for rows in (k[t0:t0 + npd], v[t0:t0 + npd], k[t0 + npd:], v[t0 + npd:]):
+        b += struct.pack("<Q", len(rows)) + rows.tobytes()
+    return b
+
+
+def test_cache_vqks_snapshots(torch_mod, tmp_path):
+    """VQKS snapshots (kv_cache.cpp:206-312): bytes equal an independent restatement from the
+    oracle's state; loading them back gives an identical batched cache."""
+    import io
+
+    torch = torch_mod
+    from paper_2603_16435_b200.cache import DeviceCacheState
+    from paper_2603_16435_b200.errors import InvalidInput
+
+    rng = O.Rng(7500)
+    ks, vs = rng.stack(3, 16, 8, O.KEY), rng.stack(2, 8, 8, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    S, init_len, local_len = 2, 2, 4
+    refs = [O.Cache(ks, vs, init_len, local_len, False) for _ in range(S)]
+    dc = DeviceCacheState(pk, pv, S, init_len, local_len)
+    x = rng.matrix(S * 11, 8).reshape(S, 11, 8)
+    y = rng.matrix(S * 11, 8).reshape(S, 11, 8)
+    for i, r in enumerate(refs):
+        r.prefill(x[i], y[i])
+    dc.prefill(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+    for _ in range(6):  # leaves pending rows and one flush behind
+        k1, v1 = rng.matrix(S, 8), rng.matrix(S, 8)
+        for i, r in enumerate(refs):
+            r.append_token(k1[i], v1[i])
+        dc.append_token(torch.from_numpy(k1).cuda(), torch.from_numpy(v1).cuda())
+    paths = []
+    for i, r in enumerate(refs):
+        buf = io.BytesIO()
+        dc.save_snapshot(i, buf)
+        assert buf.getvalue() == _vqks_from_oracle(r, ks, vs, init_len, local_len, False, True, pk, pv)
+        p = str(tmp_path / f"s{i}.vqks")
+        dc.save_snapshot(i, p)
+        paths.append(p)
+    back = DeviceCacheState.load_snapshots(paths, pk, pv)
+    q = rng.matrix(S * 4, 8).reshape(S, 4, 8)
+    check_state(torch, back, refs, ks, vs, q)
+    other = product_stack(rng.stack(3, 16, 8, O.KEY))
+    with pytest.raises(InvalidInput):
+        DeviceCacheState.load_snapshots(paths, other, pv)
