@@ -213,15 +213,27 @@ __device__ void raw_rows(const MainArgs& a, uint32_t pair, float* smem) {
     }
     __syncthreads();
     // o[g][d] = sum_r p[r][g] v_r[d]; thread = (g, d)
+    // 8 independent accumulators keep 8 row loads in flight per thread
     for (uint32_t gd = threadIdx.x; gd < kG * kD; gd += blockDim.x) {
         const uint32_t g = gd / kD, d = gd % kD;
-        float acc = 0.f;
-        for (uint64_t r = 0; r < n_raw; ++r) {
-            const float* v = (r < a.n_init) ? a.init_v + (uint64_t(pair) * a.init_stride + r) * kD
-                                            : a.local_v + (uint64_t(pair) * a.local_stride + (r - a.n_init)) * kD;
-            acc = fmaf(ls[r * kG + g], __ldg(v + d), acc);
+        const float* iv = a.init_v + uint64_t(pair) * a.init_stride * kD + d;
+        const float* lv = a.local_v + uint64_t(pair) * a.local_stride * kD + d;
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        uint64_t r = 0;
+        for (; r + 8 <= n_raw; r += 8) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t rr = r + u;
+                const float x = (rr < a.n_init) ? __ldg(iv + rr * kD) : __ldg(lv + (rr - a.n_init) * kD);
+                acc[u] = fmaf(ls[rr * kG + g], x, acc[u]);
+            }
         }
-        a.part_o[(uint64_t(pair) * kG + g) * kD + d] = acc;
+        for (; r < n_raw; ++r) {
+            const float x = (r < a.n_init) ? __ldg(iv + r * kD) : __ldg(lv + (r - a.n_init) * kD);
+            acc[0] = fmaf(ls[r * kG + g], x, acc[0]);
+        }
+        a.part_o[(uint64_t(pair) * kG + g) * kD + d] =
+            ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     }
 }
 
@@ -248,6 +260,14 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
     const uint8_t* kc = a.kcodes + uint64_t(pair) * a.kstream_bytes;
     const uint8_t* vc = a.vcodes + uint64_t(pair) * a.vstream_bytes;
     const float4* lutp = a.lut + uint64_t(pair) * a.kentries;
+    // 32-bit key-code addressing: bit positions relative to the 8 B-aligned start of the
+    // pair's stream (stream bit counts < 2^32 are checked on the host)
+    const uint64_t* kc64 = reinterpret_cast<const uint64_t*>(reinterpret_cast<uintptr_t>(kc) & ~uintptr_t(7));
+    const uint32_t kbase_bits = uint32_t((reinterpret_cast<uintptr_t>(kc) & 7u) * 8u);
+    const uint32_t kwords = uint32_t((reinterpret_cast<uintptr_t>(a.kend) - reinterpret_cast<uintptr_t>(kc64)) >> 3 > 0xffffffffull
+                                         ? 0xffffffffu
+                                         : (reinterpret_cast<uintptr_t>(a.kend) - reinterpret_cast<uintptr_t>(kc64)) >> 3);
+    const uint32_t krow32 = uint32_t(a.krow_bits);
 
     float lg[kTokPerThread][kG];
 #pragma unroll
@@ -297,35 +317,45 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
             acc_off += (s < s1) ? a.kst[s].size : 0u;
         }
         // kKeyBatch tokens per batch: all their code-word loads are issued before any
-        // is used (branch-free: out-of-range tokens and the last bytes of the buffer
-        // read a dummy word; the rare buffer-tail tokens take read_bits64's careful path)
+        // is used (branch-free: out-of-range tokens and the last words of the buffer
+        // read a dummy word; the rare buffer-tail tokens take read_bits64's careful path).
+        // Bit positions are 32-bit, relative to the 8 B-aligned start of the pair's stream.
 #pragma unroll
         for (int kb = 0; kb < kTokPerThread; kb += kKeyBatch) {
-            uint64_t lo[kKeyBatch], hi[kKeyBatch];
+            uint2 lo[kKeyBatch], hi[kKeyBatch];
             uint32_t sh[kKeyBatch];
             bool fast[kKeyBatch];
 #pragma unroll
             for (int k = 0; k < kKeyBatch; ++k) {
-                const uint64_t t = threadIdx.x + uint64_t(kb + k) * kAttThreads;
-                const uint64_t pos = (t0 + t) * a.krow_bits + gbit;
-                const uint8_t* pb = kc + (pos >> 3);
-                const uintptr_t al = reinterpret_cast<uintptr_t>(pb) & ~uintptr_t(7);
-                sh[k] = uint32_t((reinterpret_cast<uintptr_t>(pb) - al) * 8 + (pos & 7));
-                fast[k] = (t < nt) && (al + 16 <= reinterpret_cast<uintptr_t>(a.kend));
-                const uint64_t* q = fast[k] ? reinterpret_cast<const uint64_t*>(al) : g_zero16;
+                const uint32_t t = threadIdx.x + uint32_t(kb + k) * kAttThreads;
+                const uint32_t pos = (uint32_t(t0) + t) * krow32 + gbit + kbase_bits;
+                const uint32_t wi = pos >> 6;
+                sh[k] = pos & 63u;
+                fast[k] = (t < nt) && (wi + 2u <= kwords);
+                const uint2* q = reinterpret_cast<const uint2*>(fast[k] ? kc64 + wi : g_zero16);
                 lo[k] = __ldg(q);
                 hi[k] = __ldg(q + 1);
             }
 #pragma unroll
             for (int k = 0; k < kKeyBatch; ++k) {
-                const uint64_t t = threadIdx.x + uint64_t(kb + k) * kAttThreads;
+                const uint32_t t = threadIdx.x + uint32_t(kb + k) * kAttThreads;
                 if (t < nt) {
-                    uint64_t w = sh[k] ? ((lo[k] >> sh[k]) | (hi[k] << (64 - sh[k]))) : lo[k];
-                    if (!fast[k]) w = read_bits64(kc, (t0 + t) * a.krow_bits + gbit, a.kend);
+                    // 64-bit window starting at bit sh of (lo, hi) as two 32-bit words
+                    const bool low = sh[k] < 32u;
+                    const uint32_t s5 = sh[k] & 31u;
+                    const uint32_t wa = low ? lo[k].x : lo[k].y, wb = low ? lo[k].y : hi[k].x;
+                    const uint32_t wc = low ? hi[k].x : hi[k].y;
+                    uint32_t w0 = __funnelshift_r(wa, wb, s5), w1 = __funnelshift_r(wb, wc, s5);
+                    if (!fast[k]) {
+                        const uint64_t w = read_bits64(kc, (t0 + t) * a.krow_bits + gbit, a.kend);
+                        w0 = uint32_t(w);
+                        w1 = uint32_t(w >> 32);
+                    }
 #pragma unroll
                     for (int q = 0; q < kGroupStages; ++q) {
                         if (lbits[q]) {
-                            const uint32_t z = uint32_t(w >> loff[q]) & ((1u << lbits[q]) - 1u);
+                            const uint32_t z = (loff[q] < 32u ? __funnelshift_r(w0, w1, loff[q]) : (w1 >> (loff[q] - 32u))) &
+                                               ((1u << lbits[q]) - 1u);
                             const float4 v = L[lofs[q] + z];
                             lg[kb + k][0] += v.x;
                             lg[kb + k][1] += v.y;
@@ -474,6 +504,8 @@ __global__ void lut_finish_kernel(const float* __restrict__ acc, const float* __
 bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a) {
     if (ks.dim != kD || vs.dim != kD || a.group != kG) return false;
     if (a.n_init + a.n_local > kSplitTokens) return false;
+    // 32-bit bit positions inside one pair's key-code stream (+ alignment slack)
+    if (uint64_t(a.n_comp) * ks.row_bits + 64 >= (1ull << 32)) return false;
     for (const auto& s : ks.stages)
         if (s.size > 1024 || s.bits > 10) return false;
     // 4 key stages per 64-bit read and LUT group (<= 64 KB)
