@@ -268,6 +268,13 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
                                          ? 0xffffffffu
                                          : (reinterpret_cast<uintptr_t>(a.kend) - reinterpret_cast<uintptr_t>(kc64)) >> 3);
     const uint32_t krow32 = uint32_t(a.krow_bits);
+    const uint64_t* vc64 = reinterpret_cast<const uint64_t*>(reinterpret_cast<uintptr_t>(vc) & ~uintptr_t(7));
+    const uint32_t vbase_bits = uint32_t((reinterpret_cast<uintptr_t>(vc) & 7u) * 8u);
+    const uint32_t vwords = uint32_t((reinterpret_cast<uintptr_t>(a.vend) - reinterpret_cast<uintptr_t>(vc64)) >> 3 > 0xffffffffull
+                                         ? 0xffffffffu
+                                         : (reinterpret_cast<uintptr_t>(a.vend) - reinterpret_cast<uintptr_t>(vc64)) >> 3);
+    const uint32_t vrow32 = uint32_t(a.vrow_bits);
+    const uint32_t nvwin = (a.vn + 5u) / 6u;
 
     float lg[kTokPerThread][kG];
 #pragma unroll
@@ -415,13 +422,43 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
         for (int g = 0; g < kG; ++g) P[g] = __float2uint_rn(lg[k][g] * kHistScale);
         // tokens whose weights all round to 0 in the 2^-18 fixed point add nothing
         if (t < nt && (P[0] | P[1] | P[2] | P[3]) != 0u) {
-            const uint64_t rb = (t0 + t) * a.vrow_bits;
-            for (uint32_t s0 = 0; s0 < a.vn; s0 += 6) {  // <= 6 fields per 64-bit window
-                const uint64_t w = read_bits64(vc, rb + vgb[s0 / 6u], a.vend);
+            const uint32_t rb = (uint32_t(t0) + uint32_t(t)) * vrow32 + vbase_bits;
+            // <= 6 fields per 64-bit window; windows of the common case (<= 3, i.e. up to
+            // 18 value stages) are loaded together before the histogram updates
+            uint32_t w0[3], w1[3];
+            bool ok3 = nvwin <= 3u;
+            if (ok3) {
+#pragma unroll
+                for (int wdw = 0; wdw < 3; ++wdw) {
+                    const uint32_t pos = rb + vgb[wdw < int(nvwin) ? wdw : 0];
+                    const uint32_t wi = pos >> 6;
+                    const bool f = wi + 2u <= vwords;
+                    ok3 = ok3 && (f || wdw >= int(nvwin));
+                    const uint2* q = reinterpret_cast<const uint2*>(f ? vc64 + wi : g_zero16);
+                    const uint2 lo = __ldg(q), hi = __ldg(q + 1);
+                    const uint32_t sh = pos & 63u, s5 = sh & 31u;
+                    const bool low = sh < 32u;
+                    const uint32_t wa = low ? lo.x : lo.y, wb = low ? lo.y : hi.x, wc = low ? hi.x : hi.y;
+                    w0[wdw] = __funnelshift_r(wa, wb, s5);
+                    w1[wdw] = __funnelshift_r(wb, wc, s5);
+                }
+            }
+            for (uint32_t s0 = 0, wdw = 0; s0 < a.vn; s0 += 6, ++wdw) {
+                uint32_t x0, x1;
+                if (ok3) {
+                    x0 = wdw == 0 ? w0[0] : (wdw == 1 ? w0[1] : w0[2]);
+                    x1 = wdw == 0 ? w1[0] : (wdw == 1 ? w1[1] : w1[2]);
+                } else {  // many value stages or the buffer tail: careful 64-bit reads
+                    const uint64_t w = read_bits64(vc, (t0 + t) * a.vrow_bits + vgb[wdw], a.vend);
+                    x0 = uint32_t(w);
+                    x1 = uint32_t(w >> 32);
+                }
                 const uint32_t s1 = min(a.vn, s0 + 6u);
-                for (uint32_t s = s0; s < s1; ++s) {
-                    const uint32_t d = vd[s];
-                    const uint32_t z = uint32_t(w >> ((d >> 5) & 63u)) & ((1u << (d & 31u)) - 1u);
+                for (uint32_t st = s0; st < s1; ++st) {
+                    const uint32_t d = vd[st];
+                    const uint32_t lo5 = (d >> 5) & 63u;
+                    const uint32_t z = (lo5 < 32u ? __funnelshift_r(x0, x1, lo5) : (x1 >> (lo5 - 32u))) &
+                                       ((1u << (d & 31u)) - 1u);
                     uint32_t* h = H + ((d >> 16) + z) * kG;
 #pragma unroll
                     for (int g = 0; g < kG; ++g)
@@ -506,6 +543,7 @@ bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const 
     if (a.n_init + a.n_local > kSplitTokens) return false;
     // 32-bit bit positions inside one pair's key-code stream (+ alignment slack)
     if (uint64_t(a.n_comp) * ks.row_bits + 64 >= (1ull << 32)) return false;
+    if (uint64_t(a.n_comp) * vs.row_bits + 64 >= (1ull << 32)) return false;
     for (const auto& s : ks.stages)
         if (s.size > 1024 || s.bits > 10) return false;
     // 4 key stages per 64-bit read and LUT group (<= 64 KB)
