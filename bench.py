@@ -104,7 +104,22 @@ def max_over_ranks(x, world):
 
 
 # --------------------------------------------------------------------------- inputs
-def gen_inputs(torch, n_streams, prefill, rank, pinned=True):
+def gpu_local_cpus(torch, device):
+    """Host CPUs on the GPU's NUMA node (sysfs local_cpulist of its PCI function), or None."""
+    try:
+        p = torch.cuda.get_device_properties(device)
+        bdf = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        txt = open(f"/sys/bus/pci/devices/{bdf}/local_cpulist").read().strip()
+        cpus = set()
+        for part in txt.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        return cpus & os.sched_getaffinity(0) or None
+    except Exception:
+        return None
+
+
+def gen_inputs(torch, n_streams, prefill, rank, pinned=True, device=0):
     """Synthetic K/V middle rows [n_streams, middle, D] (host, pinned)."""
     from paper_2603_16435_b200 import _lib
 
@@ -127,6 +142,21 @@ def gen_inputs(torch, n_streams, prefill, rank, pinned=True):
     with cf.ThreadPoolExecutor(max_workers=min(64, os.cpu_count() or 8)) as ex:
         list(ex.map(one, work))
     return K, V
+
+
+def gen_inputs_local(torch, n_streams, prefill, rank, device):
+    """gen_inputs with the pinned host buffers allocated and first touched from the CPUs
+    of the GPU's NUMA node (H2D from the remote socket runs at a fraction of the link);
+    the process affinity is restored afterwards (the CPU baselines use every core)."""
+    saved = os.sched_getaffinity(0)
+    local = gpu_local_cpus(torch, device)
+    try:
+        if local:
+            os.sched_setaffinity(0, local)
+        return gen_inputs(torch, n_streams, prefill, rank, device=device)
+    finally:
+        if local:
+            os.sched_setaffinity(0, saved)
 
 
 def make_stacks(device):
@@ -389,7 +419,7 @@ def run_ours(args, rank, world, local):
     middle = args.prefill - INIT_LEN - LOCAL_LEN
     ns = args.streams
     t_gen = time.perf_counter()
-    Kh, Vh = gen_inputs(torch, ns, args.prefill, rank)
+    Kh, Vh = gen_inputs_local(torch, ns, args.prefill, rank, local)
     t_gen = time.perf_counter() - t_gen
     Kd, Vd = Kh.to("cuda", non_blocking=True), Vh.to("cuda", non_blocking=True)
     kp = torch.empty((ns, kst.device.payload_bytes(middle)), dtype=torch.uint8, device="cuda")
