@@ -38,7 +38,10 @@ constexpr int kAttThreads = 512;
 constexpr int kTokPerThread = 16;
 constexpr int kSplitTokens = kAttThreads * kTokPerThread;  // 8192
 constexpr int kMaxVStages = 64;    // value stages supported by the LUT path
-constexpr int kKeyBatch = 4;      // key tokens whose code loads are in flight together
+constexpr int kKeyBatch = 4;
+constexpr uint32_t kQueueCap = 64;                       // per-warp value-token queue entries
+constexpr uint32_t kQueueOff = 131072 + 1024;             // smem offset of the queues (after the control area)
+constexpr uint32_t kMainSmem = kQueueOff + (kAttThreads / 32) * kQueueCap * (1 + 4) * 4;      // key tokens whose code loads are in flight together
 constexpr int kGroupStages = 4;    // LUT stages per smem buffer (4 x 16 KB)
 constexpr float kHistScale = 262144.0f;  // 2^18 fixed point for p in [0, 1]
 
@@ -414,59 +417,97 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
         if (threadIdx.x == first) vgb[threadIdx.x / 6u] = si.bit_off;
     }
     __syncthreads();
+    // Histogram updates of one token: its <= 6-field value-code windows, then one shared
+    // atomic per (stage, head) with a nonzero weight.
+    auto hist_token = [&](uint32_t t, const uint32_t (&P)[kG]) {
+        const uint32_t rb = (uint32_t(t0) + t) * vrow32 + vbase_bits;
+        // windows of the common case (<= 3, i.e. up to 18 value stages) load together
+        uint32_t w0[3], w1[3];
+        bool ok3 = nvwin <= 3u;
+        if (ok3) {
+#pragma unroll
+            for (int wdw = 0; wdw < 3; ++wdw) {
+                const uint32_t pos = rb + vgb[wdw < int(nvwin) ? wdw : 0];
+                const uint32_t wi = pos >> 6;
+                const bool f = wi + 2u <= vwords;
+                ok3 = ok3 && (f || wdw >= int(nvwin));
+                const uint2* q = reinterpret_cast<const uint2*>(f ? vc64 + wi : g_zero16);
+                const uint2 lo = __ldg(q), hi = __ldg(q + 1);
+                const uint32_t sh = pos & 63u, s5 = sh & 31u;
+                const bool low = sh < 32u;
+                const uint32_t wa = low ? lo.x : lo.y, wb = low ? lo.y : hi.x, wc = low ? hi.x : hi.y;
+                w0[wdw] = __funnelshift_r(wa, wb, s5);
+                w1[wdw] = __funnelshift_r(wb, wc, s5);
+            }
+        }
+        for (uint32_t s0 = 0, wdw = 0; s0 < a.vn; s0 += 6, ++wdw) {
+            uint32_t x0, x1;
+            if (ok3) {
+                x0 = wdw == 0 ? w0[0] : (wdw == 1 ? w0[1] : w0[2]);
+                x1 = wdw == 0 ? w1[0] : (wdw == 1 ? w1[1] : w1[2]);
+            } else {  // many value stages or the buffer tail: careful 64-bit reads
+                const uint64_t w = read_bits64(vc, (t0 + t) * a.vrow_bits + vgb[wdw], a.vend);
+                x0 = uint32_t(w);
+                x1 = uint32_t(w >> 32);
+            }
+            const uint32_t s1 = min(a.vn, s0 + 6u);
+            for (uint32_t st = s0; st < s1; ++st) {
+                const uint32_t d = vd[st];
+                const uint32_t lo5 = (d >> 5) & 63u;
+                const uint32_t z = (lo5 < 32u ? __funnelshift_r(x0, x1, lo5) : (x1 >> (lo5 - 32u))) &
+                                   ((1u << (d & 31u)) - 1u);
+                uint32_t* h = H + ((d >> 16) + z) * kG;
+#pragma unroll
+                for (int g = 0; g < kG; ++g)
+                    if (P[g]) atomicAdd(h + g, P[g]);
+            }
+        }
+    };
+    // Tokens whose weights all round to 0 in the 2^-18 fixed point add nothing; the others
+    // are compacted into a per-warp queue and processed 32 at a time, so the histogram
+    // loop runs with full warps instead of the few lanes that happen to contribute.
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t* qt = reinterpret_cast<uint32_t*>(smem_raw + kQueueOff) + (threadIdx.x >> 5) * (kQueueCap * (1 + kG));
+    uint32_t* qP = qt + kQueueCap;
+    uint32_t qlen = 0;
+    auto flush = [&](uint32_t n) {
+        if (lane < n) {
+            uint32_t P[kG];
+#pragma unroll
+            for (int g = 0; g < kG; ++g) P[g] = qP[lane * kG + g];
+            hist_token(qt[lane], P);
+        }
+    };
 #pragma unroll
     for (int k = 0; k < kTokPerThread; ++k) {
-        const uint64_t t = threadIdx.x + uint64_t(k) * kAttThreads;
+        const uint32_t t = threadIdx.x + uint32_t(k) * kAttThreads;
         uint32_t P[kG];
 #pragma unroll
         for (int g = 0; g < kG; ++g) P[g] = __float2uint_rn(lg[k][g] * kHistScale);
-        // tokens whose weights all round to 0 in the 2^-18 fixed point add nothing
-        if (t < nt && (P[0] | P[1] | P[2] | P[3]) != 0u) {
-            const uint32_t rb = (uint32_t(t0) + uint32_t(t)) * vrow32 + vbase_bits;
-            // <= 6 fields per 64-bit window; windows of the common case (<= 3, i.e. up to
-            // 18 value stages) are loaded together before the histogram updates
-            uint32_t w0[3], w1[3];
-            bool ok3 = nvwin <= 3u;
-            if (ok3) {
+        const bool act = t < nt && (P[0] | P[1] | P[2] | P[3]) != 0u;
+        const uint32_t mask = __ballot_sync(0xffffffffu, act);
+        if (act) {
+            const uint32_t pos = qlen + __popc(mask & ((1u << lane) - 1u));
+            qt[pos] = t;
 #pragma unroll
-                for (int wdw = 0; wdw < 3; ++wdw) {
-                    const uint32_t pos = rb + vgb[wdw < int(nvwin) ? wdw : 0];
-                    const uint32_t wi = pos >> 6;
-                    const bool f = wi + 2u <= vwords;
-                    ok3 = ok3 && (f || wdw >= int(nvwin));
-                    const uint2* q = reinterpret_cast<const uint2*>(f ? vc64 + wi : g_zero16);
-                    const uint2 lo = __ldg(q), hi = __ldg(q + 1);
-                    const uint32_t sh = pos & 63u, s5 = sh & 31u;
-                    const bool low = sh < 32u;
-                    const uint32_t wa = low ? lo.x : lo.y, wb = low ? lo.y : hi.x, wc = low ? hi.x : hi.y;
-                    w0[wdw] = __funnelshift_r(wa, wb, s5);
-                    w1[wdw] = __funnelshift_r(wb, wc, s5);
-                }
-            }
-            for (uint32_t s0 = 0, wdw = 0; s0 < a.vn; s0 += 6, ++wdw) {
-                uint32_t x0, x1;
-                if (ok3) {
-                    x0 = wdw == 0 ? w0[0] : (wdw == 1 ? w0[1] : w0[2]);
-                    x1 = wdw == 0 ? w1[0] : (wdw == 1 ? w1[1] : w1[2]);
-                } else {  // many value stages or the buffer tail: careful 64-bit reads
-                    const uint64_t w = read_bits64(vc, (t0 + t) * a.vrow_bits + vgb[wdw], a.vend);
-                    x0 = uint32_t(w);
-                    x1 = uint32_t(w >> 32);
-                }
-                const uint32_t s1 = min(a.vn, s0 + 6u);
-                for (uint32_t st = s0; st < s1; ++st) {
-                    const uint32_t d = vd[st];
-                    const uint32_t lo5 = (d >> 5) & 63u;
-                    const uint32_t z = (lo5 < 32u ? __funnelshift_r(x0, x1, lo5) : (x1 >> (lo5 - 32u))) &
-                                       ((1u << (d & 31u)) - 1u);
-                    uint32_t* h = H + ((d >> 16) + z) * kG;
+            for (int g = 0; g < kG; ++g) qP[pos * kG + g] = P[g];
+        }
+        qlen += __popc(mask);
+        if (qlen >= 32u) {
+            __syncwarp();
+            flush(32u);
+            __syncwarp();
+            if (lane + 32u < qlen) {  // keep the overflow for the next batch
+                qt[lane] = qt[lane + 32u];
 #pragma unroll
-                    for (int g = 0; g < kG; ++g)
-                        if (P[g]) atomicAdd(h + g, P[g]);
-                }
+                for (int g = 0; g < kG; ++g) qP[lane * kG + g] = qP[(lane + 32u) * kG + g];
             }
+            __syncwarp();
+            qlen -= 32u;
         }
     }
+    __syncwarp();
+    flush(qlen);
     __syncthreads();
     float* ph = a.part_h + (uint64_t(pair) * a.n_splits + split) * hsz;
     for (uint32_t i = threadIdx.x; i < hsz; i += blockDim.x) ph[i] = float(H[i]) * (1.0f / kHistScale);
@@ -604,7 +645,7 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
                     a.vcodes_dev + uint64_t(a.n_pairs - 1) * vstr + vpb, float(scale), n_splits,
                     ph, po, pm, pl, a.init_stride ? a.init_stride : a.n_init,
                     a.local_stride ? a.local_stride : a.n_local};
-        const size_t smem = 131072 + 64 + 64 * sizeof(float) + 4096;
+        const size_t smem = kMainSmem;
         static bool attr = false;
         if (!attr) {
             VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
