@@ -58,23 +58,23 @@ struct LutArgs {
 // LUT[pair][e] = scale * q_g . E[e] for all key entries e (stage-concatenated).
 // CTA: 128 entries x 8 pairs, 256 threads; thread = 4 entries x 4 queries of one pair.
 constexpr int kLutEntries = 128;
+constexpr int kLutStride = kD + 2;  // even row stride: 8 B-aligned float2 reads, 2 wavefronts per warp load
 __global__ void __launch_bounds__(256) lut_kernel(LutArgs a, uint32_t n_pairs) {
     extern __shared__ float lsm[];
-    float (*qs)[kG][kD] = reinterpret_cast<float (*)[kG][kD]>(lsm);                // [8][G][D]
-    float (*es)[kD + 1] = reinterpret_cast<float (*)[kD + 1]>(lsm + 8 * kG * kD);  // [128][D+1]
+    float4* qs = reinterpret_cast<float4*>(lsm);  // [8 pairs][D] x float4 over g: one LDS.128 per dim
+    float* es = lsm + 8 * kG * kD;                // [128 entries][kLutStride]
     const uint32_t e0 = blockIdx.x * kLutEntries, p0 = blockIdx.y * 8;
-    for (uint32_t i = threadIdx.x; i < 8 * kG * kD; i += blockDim.x) {
-        const uint32_t p = i / (kG * kD);
-        qs[p][(i / kD) % kG][i % kD] = (p0 + p < n_pairs) ? a.q[uint64_t(p0 + p) * kG * kD + (i % (kG * kD))] : 0.f;
+    for (uint32_t i = threadIdx.x; i < 8 * kD; i += blockDim.x) {
+        const uint32_t p = i / kD, c = i % kD;
+        const float* qp = a.q + uint64_t(p0 + p) * kG * kD + c;
+        qs[i] = (p0 + p < n_pairs) ? make_float4(qp[0], qp[kD], qp[2 * kD], qp[3 * kD]) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     for (uint32_t i = threadIdx.x; i < kLutEntries * kD / 4; i += blockDim.x) {
         const uint32_t r = (4 * i) / kD, c = (4 * i) % kD;
         const float4 v = (e0 + r < a.kentries) ? __ldg(reinterpret_cast<const float4*>(a.keff + uint64_t(e0 + r) * kD + c))
                                                : make_float4(0.f, 0.f, 0.f, 0.f);
-        es[r][c] = v.x;
-        es[r][c + 1] = v.y;
-        es[r][c + 2] = v.z;
-        es[r][c + 3] = v.w;
+        *reinterpret_cast<float2*>(es + r * kLutStride + c) = make_float2(v.x, v.y);
+        *reinterpret_cast<float2*>(es + r * kLutStride + c + 2) = make_float2(v.z, v.w);
     }
     __syncthreads();
     const uint32_t eg = threadIdx.x & 31, p = threadIdx.x >> 5;
@@ -83,17 +83,24 @@ __global__ void __launch_bounds__(256) lut_kernel(LutArgs a, uint32_t n_pairs) {
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int g = 0; g < kG; ++g) acc[i][g] = 0.f;
+    const float4* qp = qs + p * kD;
 #pragma unroll 4
-    for (int c = 0; c < kD; ++c) {
-        float qv[kG], ev[4];
+    for (int c = 0; c < kD; c += 2) {
+        const float4 q0 = qp[c], q1 = qp[c + 1];  // broadcast within the warp
+        float2 ev[4];
 #pragma unroll
-        for (int g = 0; g < kG; ++g) qv[g] = qs[p][g][c];
+        for (int i = 0; i < 4; ++i) ev[i] = *reinterpret_cast<const float2*>(es + (eg + 32 * i) * kLutStride + c);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) ev[i] = es[eg + 32 * i][c];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int g = 0; g < kG; ++g) acc[i][g] = fmaf(qv[g], ev[i], acc[i][g]);
+        for (int i = 0; i < 4; ++i) {
+            acc[i][0] = fmaf(q0.x, ev[i].x, acc[i][0]);
+            acc[i][1] = fmaf(q0.y, ev[i].x, acc[i][1]);
+            acc[i][2] = fmaf(q0.z, ev[i].x, acc[i][2]);
+            acc[i][3] = fmaf(q0.w, ev[i].x, acc[i][3]);
+            acc[i][0] = fmaf(q1.x, ev[i].y, acc[i][0]);
+            acc[i][1] = fmaf(q1.y, ev[i].y, acc[i][1]);
+            acc[i][2] = fmaf(q1.z, ev[i].y, acc[i][2]);
+            acc[i][3] = fmaf(q1.w, ev[i].y, acc[i][3]);
+        }
     }
     if (p0 + p < n_pairs)
 #pragma unroll
@@ -624,7 +631,7 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         ProfScope ps("attend_lut_build", s);
         LutArgs la{a.q_dev, ks.d_eff, ks.d_stages, ks.n, kent, float(scale), lut};
         dim3 grid(unsigned((kent + kLutEntries - 1) / kLutEntries), (a.n_pairs + 7) / 8);
-        const int lsmem = int(sizeof(float) * (8 * kG * kD + kLutEntries * (kD + 1)));
+        const int lsmem = int(sizeof(float) * (8 * kG * kD + kLutEntries * kLutStride));
         static bool lattr = false;
         if (!lattr) {
             VQKV_CUDA(cudaFuncSetAttribute(lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem));
