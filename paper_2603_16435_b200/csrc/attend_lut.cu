@@ -291,6 +291,8 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
     for (int k = 0; k < kTokPerThread; ++k)
 #pragma unroll
         for (int g = 0; g < kG; ++g) lg[k][g] = 0.f;
+    // the key logits accumulate as head pairs with packed FADD2 (2 instructions per lookup)
+    float2 (*lg2)[2] = reinterpret_cast<float2 (*)[2]>(lg);
 
     // ---- keys: LUT groups of kGroupStages stages, double-buffered bulk copies
     const uint32_t ngroups = (a.kn + kGroupStages - 1) / kGroupStages;
@@ -374,10 +376,8 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
                             const uint32_t z = (loff[q] < 32u ? __funnelshift_r(w0, w1, loff[q]) : (w1 >> (loff[q] - 32u))) &
                                                ((1u << lbits[q]) - 1u);
                             const float4 v = L[lofs[q] + z];
-                            lg[kb + k][0] += v.x;
-                            lg[kb + k][1] += v.y;
-                            lg[kb + k][2] += v.z;
-                            lg[kb + k][3] += v.w;
+                            lg2[kb + k][0] = ptx::add2(lg2[kb + k][0], make_float2(v.x, v.y));
+                            lg2[kb + k][1] = ptx::add2(lg2[kb + k][1], make_float2(v.z, v.w));
                         }
                     }
                 }
