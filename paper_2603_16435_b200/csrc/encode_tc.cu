@@ -122,10 +122,15 @@ __device__ __forceinline__ void store_a_chunk(uint8_t* a_tile, uint32_t i, int c
     for (int g = 0; g < 4; ++g) {
         const int kk = 32 * c4 + 8 * g;
         const int kb = kk >> 6, gi = (kk & 63) >> 3;
-        __half2 h0 = __floats2half2_rn(v[8 * g + 0] * sc, v[8 * g + 1] * sc);
-        __half2 h1 = __floats2half2_rn(v[8 * g + 2] * sc, v[8 * g + 3] * sc);
-        __half2 h2 = __floats2half2_rn(v[8 * g + 4] * sc, v[8 * g + 5] * sc);
-        __half2 h3 = __floats2half2_rn(v[8 * g + 6] * sc, v[8 * g + 7] * sc);
+        const float2 s2 = make_float2(sc, sc);
+        const float2 x0 = ptx::mul2(make_float2(v[8 * g + 0], v[8 * g + 1]), s2);
+        const float2 x1 = ptx::mul2(make_float2(v[8 * g + 2], v[8 * g + 3]), s2);
+        const float2 x2 = ptx::mul2(make_float2(v[8 * g + 4], v[8 * g + 5]), s2);
+        const float2 x3 = ptx::mul2(make_float2(v[8 * g + 6], v[8 * g + 7]), s2);
+        __half2 h0 = __floats2half2_rn(x0.x, x0.y);
+        __half2 h1 = __floats2half2_rn(x1.x, x1.y);
+        __half2 h2 = __floats2half2_rn(x2.x, x2.y);
+        __half2 h3 = __floats2half2_rn(x3.x, x3.y);
         uint4 w;
         w.x = *reinterpret_cast<uint32_t*>(&h0);
         w.y = *reinterpret_cast<uint32_t*>(&h1);
@@ -573,18 +578,28 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                             ptx::tc_wait_ld();
 #pragma unroll
                             for (int kk = 0; kk < 8; ++kk) {
-                                float pp[4];
-#pragma unroll
-                                for (int l = 0; l < 4; ++l)
-                                    pp[l] = __fmul_rn(ev[32 * c4 + 4 * kk + l], __shfl_sync(0xffffffffu, v[4 * kk + l], o));
-                                g0 = __fadd_rn(g0, pp[0]);
-                                g1 = __fadd_rn(g1, pp[1]);
-                                g2 = __fadd_rn(g2, pp[2]);
-                                g3 = __fadd_rn(g3, pp[3]);
+                                // packed FMUL2 / FADD2: each lane is the same IEEE op in the same order
+                                const float2 rv0 = make_float2(__shfl_sync(0xffffffffu, v[4 * kk], o),
+                                                               __shfl_sync(0xffffffffu, v[4 * kk + 1], o));
+                                const float2 rv1 = make_float2(__shfl_sync(0xffffffffu, v[4 * kk + 2], o),
+                                                               __shfl_sync(0xffffffffu, v[4 * kk + 3], o));
+                                const float2 p01 = ptx::mul2(make_float2(ev[32 * c4 + 4 * kk], ev[32 * c4 + 4 * kk + 1]), rv0);
+                                const float2 p23 = ptx::mul2(make_float2(ev[32 * c4 + 4 * kk + 2], ev[32 * c4 + 4 * kk + 3]), rv1);
+                                {
+                                    float2 g01 = ptx::add2(make_float2(g0, g1), p01), g23 = ptx::add2(make_float2(g2, g3), p23);
+                                    g0 = g01.x;
+                                    g1 = g01.y;
+                                    g2 = g23.x;
+                                    g3 = g23.y;
+                                }
                                 if (any_one) {
                                     float* rr = (kk & 1) ? r1 : r0;
-#pragma unroll
-                                    for (int l = 0; l < 4; ++l) rr[l] = __fadd_rn(rr[l], pp[l]);
+                                    const float2 a01 = ptx::add2(make_float2(rr[0], rr[1]), p01);
+                                    const float2 a23 = ptx::add2(make_float2(rr[2], rr[3]), p23);
+                                    rr[0] = a01.x;
+                                    rr[1] = a01.y;
+                                    rr[2] = a23.x;
+                                    rr[3] = a23.y;
                                 }
                             }
                         }
@@ -652,7 +667,12 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     ptx::tc_wait_ld();
                     if (c4 == 0) VQKV_PHASE_DEP(9, v[0])
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) v[k] = __fsub_rn(v[k], en[32 * c4 + k]);
+                    for (int k = 0; k < 32; k += 2) {  // FADD2 of -e: identical to v - e lane by lane
+                        const float2 d = ptx::add2(make_float2(v[k], v[k + 1]),
+                                                   make_float2(-en[32 * c4 + k], -en[32 * c4 + k + 1]));
+                        v[k] = d.x;
+                        v[k + 1] = d.y;
+                    }
                     if (c4 == 0) VQKV_PHASE_DEP(10, v[31])
                     ptx::tmem_st32(t_res + 32u * c4, v);
                     if (!last) {
