@@ -578,13 +578,14 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                             ptx::tc_wait_ld();
 #pragma unroll
                             for (int kk = 0; kk < 8; ++kk) {
-                                // packed FMUL2 / FADD2: each lane is the same IEEE op in the same order
-                                const float2 rv0 = make_float2(__shfl_sync(0xffffffffu, v[4 * kk], o),
-                                                               __shfl_sync(0xffffffffu, v[4 * kk + 1], o));
-                                const float2 rv1 = make_float2(__shfl_sync(0xffffffffu, v[4 * kk + 2], o),
-                                                               __shfl_sync(0xffffffffu, v[4 * kk + 3], o));
-                                const float2 p01 = ptx::mul2(make_float2(ev[32 * c4 + 4 * kk], ev[32 * c4 + 4 * kk + 1]), rv0);
-                                const float2 p23 = ptx::mul2(make_float2(ev[32 * c4 + 4 * kk + 2], ev[32 * c4 + 4 * kk + 3]), rv1);
+                                // scalar FMUL + packed FADD2: each lane is the same IEEE op in the same
+                                // order.  (ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even with
+                                // --fmad=false, so the products must not be f32x2; tests/test_sass.py.)
+                                float q[4];
+#pragma unroll
+                                for (int l = 0; l < 4; ++l)
+                                    q[l] = __fmul_rn(ev[32 * c4 + 4 * kk + l], __shfl_sync(0xffffffffu, v[4 * kk + l], o));
+                                const float2 p01 = make_float2(q[0], q[1]), p23 = make_float2(q[2], q[3]);
                                 {
                                     float2 g01 = ptx::add2(make_float2(g0, g1), p01), g23 = ptx::add2(make_float2(g2, g3), p23);
                                     g0 = g01.x;
@@ -649,7 +650,8 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 const float sc_n = ldexpf(1.0f, sigma_n);
                 if (!last) store_a_ext(a_tile, i, sigma_n);
                 const float4* ez4 = reinterpret_cast<const float4*>(eff + si.eff_off + uint64_t(z) * 128);
-                float R2n = 0.f, mxn = 0.f;
+                float2 R2p = make_float2(0.f, 0.f);
+                float mxn = 0.f;
                 float n0[4] = {0.f, 0.f, 0.f, 0.f}, n1[4] = {0.f, 0.f, 0.f, 0.f};
                 float en[128];  // e_z in one L2 round trip
                 if (dbg & 16u) {  // timing experiment only: no e_z gather (wrong residuals)
@@ -677,9 +679,9 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     ptx::tmem_st32(t_res + 32u * c4, v);
                     if (!last) {
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) {
-                            R2n = fmaf(v[k], v[k], R2n);
-                            mxn = fmaxf(mxn, fabsf(v[k]));
+                        for (int k = 0; k < 32; k += 2) {  // two partial sums: R2 only feeds the (slacked) window bound
+                            R2p = ptx::fma2(make_float2(v[k], v[k + 1]), make_float2(v[k], v[k + 1]), R2p);
+                            mxn = ptx::fmax3(mxn, fabsf(v[k]), fabsf(v[k + 1]));
                         }
                         store_a_chunk(a_tile, i, c4, v, sc_n);
                     } else {
@@ -688,7 +690,13 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         for (int kk = 0; kk < 8; ++kk) {
                             float* rr = (kk & 1) ? n1 : n0;
 #pragma unroll
-                            for (int l = 0; l < 4; ++l) rr[l] = __fadd_rn(rr[l], __fmul_rn(v[4 * kk + l], v[4 * kk + l]));
+                            for (int l = 0; l < 4; l += 2) {  // FMUL + FADD2 (not FMUL2: see the rescoring loop)
+                                const float2 x = make_float2(__fmul_rn(v[4 * kk + l], v[4 * kk + l]),
+                                                             __fmul_rn(v[4 * kk + l + 1], v[4 * kk + l + 1]));
+                                const float2 a = ptx::add2(make_float2(rr[l], rr[l + 1]), x);
+                                rr[l] = a.x;
+                                rr[l + 1] = a.y;
+                            }
                         }
                         if (residuals && valid && !exact_row) {
                             float4* o4 = reinterpret_cast<float4*>(residuals + grow * 128 + 32 * c4);
@@ -709,7 +717,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     for (int l = 0; l < 4; ++l) n0[l] = __fadd_rn(n0[l], n1[l]);
                     norms[grow] = __fsqrt_rn(__fadd_rn(__fadd_rn(n0[0], n0[2]), __fadd_rn(n0[1], n0[3])));
                 }
-                R2 = R2n;
+                R2 = __fadd_rn(R2p.x, R2p.y);
                 mx = mxn;
                 sigma = sigma_n;
                 VQKV_PHASE(4)
