@@ -168,9 +168,31 @@ typedef struct vqkv_attend_args {
     uint64_t local_stride;
     uint64_t kcodes_stride;
     uint64_t vcodes_stride;
+    /* key-code layout: VQKV_KEYCODES_ROWS (0) = the CodeMatrix payload above;
+     * VQKV_KEYCODES_GROUP_MAJOR (1) = the attention layout written by
+     * vqkv_keycodes_to_gm, kcodes_cap tokens per group segment (kcodes_stride =
+     * bytes between pairs, 0 = vqkv_keycodes_gm_bytes(key_stack, kcodes_cap)) */
+    uint32_t kcodes_layout;
+    uint64_t kcodes_cap;
 } vqkv_attend_args;
+#define VQKV_KEYCODES_ROWS 0
+#define VQKV_KEYCODES_GROUP_MAJOR 1
 int vqkv_attend_decode(vqkv_stack_t key_stack, vqkv_stack_t value_stack, const vqkv_attend_args* args,
                        void* stream);
+
+/* Group-major key codes (no reference counterpart: a device-resident copy of the key
+ * CodeMatrix rows laid out for the decode-attention kernel).  Per pair, per group g of
+ * 4 key stages: cap records of 5 bytes -- the group's fields, as they sit in the row
+ * (codebook.cpp:96-120), shifted to bit 0 -- stored as cap u32 words (bits 0-31) then
+ * cap bytes (bits 32-39).  Needs D = 128 and every key stage <= 1024 entries; cap must
+ * be a multiple of 16.  vqkv_keycodes_gm_bytes returns 0 when unsupported.
+ * vqkv_keycodes_to_gm writes rows [src_row, src_row + count) of each pair's payload
+ * (payload_stride bytes apart) to records [dst_row, dst_row + count) of each pair's
+ * group-major buffer (gm_stride bytes apart, 0 = vqkv_keycodes_gm_bytes). */
+uint64_t vqkv_keycodes_gm_bytes(vqkv_stack_t key_stack, uint64_t cap);
+int vqkv_keycodes_to_gm(vqkv_stack_t key_stack, const uint8_t* payload_dev, uint64_t payload_stride, uint32_t n_pairs,
+                        uint64_t src_row, uint64_t count, uint8_t* gm_dev, uint64_t cap, uint64_t gm_stride,
+                        uint64_t dst_row, void* stream);
 
 /* CodeMatrix::append of whole packed blocks (codebook.cpp:96-120), batched over
  * streams: for each stream i, bits [0, src_bits) of src + i*src_stride are

@@ -43,7 +43,12 @@ class AttendArgs(C.Structure):
         ("local_stride", C.c_uint64),
         ("kcodes_stride", C.c_uint64),
         ("vcodes_stride", C.c_uint64),
+        ("kcodes_layout", C.c_uint32),
+        ("kcodes_cap", C.c_uint64),
     ]
+
+
+KEYCODES_ROWS, KEYCODES_GROUP_MAJOR = 0, 1
 
 
 _SIGS = {
@@ -74,6 +79,11 @@ _SIGS = {
     "vqkv_encode_counters": (C.c_int, [P, u64p]),
     "vqkv_encode_phase_clocks": (C.c_int, [P, u64p]),
     "vqkv_payload_append": (C.c_int, [P, C.c_uint64, C.c_uint64, P, C.c_uint64, C.c_uint64, C.c_uint32, P]),
+    "vqkv_keycodes_gm_bytes": (C.c_uint64, [P, C.c_uint64]),
+    "vqkv_keycodes_to_gm": (
+        C.c_int,
+        [P, P, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, P, C.c_uint64, C.c_uint64, C.c_uint64, P],
+    ),
     "vqkv_profile_enable": (C.c_int, [C.c_int]),
     "vqkv_profile_collect": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), u64p]),
     "vqkv_generate_synthetic": (

@@ -24,6 +24,7 @@
 //                   value codebooks, add the raw part, normalise, emit lse.
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "tc_ptx.cuh"
 #include "vqkv_internal.cuh"
@@ -43,6 +44,10 @@ constexpr uint32_t kQueueCap = 64;                       // per-warp value-token
 constexpr uint32_t kQueueOff = 131072 + 1024;             // smem offset of the queues (after the control area)
 constexpr uint32_t kMainSmem = kQueueOff + (kAttThreads / 32) * kQueueCap * (1 + 4) * 4;      // key tokens whose code loads are in flight together
 constexpr int kGroupStages = 4;    // LUT stages per smem buffer (4 x 16 KB)
+constexpr uint32_t kGmCodeOff = 131072 + 1024;               // == kQueueOff: queues are used after the keys
+constexpr uint32_t kGmCodeBuf = 5 * kSplitTokens;              // one group's records of a split (40 KB)
+constexpr uint32_t kAlignSlack = 16384 - 1024;                 // 1 KB-aligned window start -> 16 KB alignment
+constexpr uint32_t kGmSmem = kGmCodeOff + 2 * kGmCodeBuf;
 constexpr float kHistScale = 262144.0f;  // 2^18 fixed point for p in [0, 1]
 
 struct LutArgs {
@@ -160,6 +165,7 @@ struct MainArgs {
     float* part_m;      // [pairs][splits+1][G]
     float* part_l;      // [pairs][splits+1][G]
     uint64_t init_stride, local_stride;  // rows between pairs
+    uint64_t gm_cap;                     // group-major key codes: token capacity per group segment
 };
 
 __device__ __forceinline__ float block_max(float v, float* red) {
@@ -247,6 +253,16 @@ __device__ void raw_rows(const MainArgs& a, uint32_t pair, float* smem) {
     }
 }
 
+__device__ __forceinline__ void lds128(uint32_t addr, float2& a, float2& b) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y) : "r"(addr));
+}
+
+// GM = 1: key codes in the group-major layout (attend_lut.cu, "group-major key codes"):
+// per LUT group one bulk copy of the split's 5-byte records lands next to the LUT group,
+// so every code byte crosses L2 -> SM once, and a lookup is SHF + LOP3 + LDS.128 + 2 FADD2
+// (slot address = 16 KB-aligned stage slot | code << 4).  GM = 0: reference CodeMatrix rows,
+// re-read per LUT group through L1/L2 (any geometry the LUT path supports).
+template <int GM>
 __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t pair = blockIdx.y, split = blockIdx.x;
@@ -262,9 +278,13 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
     }
     // smem: [0, 128K) two LUT group buffers (2 x 4 stages x 1024 x 16 B) / value histograms
     //       then mbarriers and reduction scratch
-    uint8_t* lut_buf = smem_raw;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 131072);
-    float* red = reinterpret_cast<float*>(smem_raw + 131072 + 64);
+    // the layout below starts at the first 16 KB-aligned shared address (the window
+    // starts after the 1 KB system reservation), so a LUT slot address is base | code << 4
+    uint8_t* const sm = smem_raw + ((16384u - (ptx::smem_u32(smem_raw) & 16383u)) & 16383u);
+    uint8_t* lut_buf = sm;
+    uint8_t* code_buf = sm + kGmCodeOff;  // GM: two record buffers (the value queues reuse them later)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 131072);
+    float* red = reinterpret_cast<float*>(sm + 131072 + 64);
     const uint64_t t0 = uint64_t(split) * kSplitTokens;
     const uint64_t nt = (a.n_comp - t0 < uint64_t(kSplitTokens)) ? (a.n_comp - t0) : uint64_t(kSplitTokens);
     const uint8_t* kc = a.kcodes + uint64_t(pair) * a.kstream_bytes;
@@ -309,18 +329,67 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
         uint32_t bytes = 0;
         for (uint32_t s = s0; s < s1; ++s) bytes += a.kst[s].size * 16u;
         const uint32_t bar = ptx::smem_u32(&bars[b]);
-        ptx::mbar_arrive_expect_tx(bar, bytes);
-        uint32_t off = 0;
-        for (uint32_t s = s0; s < s1; ++s) {
-            const uint32_t nb = a.kst[s].size * 16u;
-            ptx::bulk_g2s(ptx::smem_u32(lut_buf + b * 65536 + off), lutp + a.kst[s].eff_off / kD, nb, bar);
-            off += nb;
+        if constexpr (GM == 1) {
+            // stage q -> 16 KB slot q; a missing stage (partial last group) has code 0 and
+            // a zero entry 0; the split's records: lo32 words, then the high bytes
+            const uint32_t clo = uint32_t((nt * 4 + 15) & ~uint64_t(15)), chi = uint32_t((nt + 15) & ~uint64_t(15));
+            ptx::mbar_arrive_expect_tx(bar, bytes + (kGroupStages - (s1 - s0)) * 16u + clo + chi);
+            for (uint32_t s = s0; s < s0 + kGroupStages; ++s) {
+                uint8_t* dst = lut_buf + b * 65536 + (s - s0) * 16384;
+                if (s < s1)
+                    ptx::bulk_g2s(ptx::smem_u32(dst), lutp + a.kst[s].eff_off / kD, a.kst[s].size * 16u, bar);
+                else
+                    ptx::bulk_g2s(ptx::smem_u32(dst), g_zero16, 16u, bar);
+            }
+            const uint8_t* seg = kc + uint64_t(grp) * a.gm_cap * 5;
+            ptx::bulk_g2s(ptx::smem_u32(code_buf + b * kGmCodeBuf), seg + t0 * 4, clo, bar);
+            ptx::bulk_g2s(ptx::smem_u32(code_buf + b * kGmCodeBuf + 4 * kSplitTokens), seg + a.gm_cap * 4 + t0, chi, bar);
+        } else {
+            ptx::mbar_arrive_expect_tx(bar, bytes);
+            uint32_t off = 0;
+            for (uint32_t s = s0; s < s1; ++s) {
+                const uint32_t nb = a.kst[s].size * 16u;
+                ptx::bulk_g2s(ptx::smem_u32(lut_buf + b * 65536 + off), lutp + a.kst[s].eff_off / kD, nb, bar);
+                off += nb;
+            }
         }
     };
     if (threadIdx.x == 0) issue(0);
     for (uint32_t grp = 0; grp < ngroups; ++grp) {
         if (threadIdx.x == 0 && grp + 1 < ngroups) issue(grp + 1);
         ptx::mbar_wait(ptx::smem_u32(&bars[grp & 1]), (grp >> 1) & 1);
+        if constexpr (GM == 1) {
+            const uint32_t Lb = ptx::smem_u32(lut_buf) + (grp & 1) * 65536u;
+            const uint32_t* clo = reinterpret_cast<const uint32_t*>(code_buf + (grp & 1) * kGmCodeBuf);
+            const uint8_t* chi = code_buf + (grp & 1) * kGmCodeBuf + 4 * kSplitTokens;
+            // field q of the record x = rec << 4 sits at bit off_q: (x >> off_q) & (mask_q << 4)
+            uint32_t off[kGroupStages], msk[kGroupStages];
+#pragma unroll
+            for (int q = 0; q < kGroupStages; ++q) {
+                const uint32_t s = grp * kGroupStages + q;
+                off[q] = (s < a.kn) ? a.kst[s].bit_off - a.kst[grp * kGroupStages].bit_off : 0u;
+                msk[q] = (s < a.kn) ? ((1u << a.kst[s].bits) - 1u) << 4 : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < kTokPerThread; ++k) {
+                // tokens past nt read stale records (valid slots; their logits are masked below)
+                const uint32_t lt = threadIdx.x + uint32_t(k) * kAttThreads;
+                const uint32_t lo = clo[lt], hi = chi[lt];
+                const uint32_t xl = lo << 4, xh = __funnelshift_l(lo, hi, 4);
+                float2 v[4][2];
+                lds128(Lb | (xl & msk[0]), v[0][0], v[0][1]);
+                lds128((Lb + 16384u) | (__funnelshift_r(xl, xh, off[1]) & msk[1]), v[1][0], v[1][1]);
+                lds128((Lb + 32768u) | (__funnelshift_r(xl, xh, off[2]) & msk[2]), v[2][0], v[2][1]);
+                lds128((Lb + 49152u) | (__funnelshift_r(xl, xh, off[3]) & msk[3]), v[3][0], v[3][1]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    lg2[k][0] = ptx::add2(lg2[k][0], v[q][0]);
+                    lg2[k][1] = ptx::add2(lg2[k][1], v[q][1]);
+                }
+            }
+            __syncthreads();  // buffers (grp & 1) are refilled two groups later
+            continue;
+        }
         const uint32_t s0 = grp * kGroupStages;
         const uint32_t s1 = min(a.kn, s0 + kGroupStages);
         const float4* L = reinterpret_cast<const float4*>(lut_buf + (grp & 1) * 65536);
@@ -410,11 +479,11 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
     }
 
     // ---- values: int32 fixed-point histograms H[s][j][g] in smem (reuses the LUT area)
-    uint32_t* H = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* H = reinterpret_cast<uint32_t*>(sm);
     const uint32_t hsz = uint32_t(a.ventries) * kG;
     // value-stage descriptors, read once per CTA: entry offset << 16 | bit offset
     // within the stage's 6-stage window << 5 | bits; window start bits per group
-    uint32_t* vd = reinterpret_cast<uint32_t*>(smem_raw + 131072 + 64 + 256);
+    uint32_t* vd = reinterpret_cast<uint32_t*>(sm + 131072 + 64 + 256);
     uint32_t* vgb = vd + kMaxVStages;
     for (uint32_t i = threadIdx.x; i < hsz; i += blockDim.x) H[i] = 0u;
     if (threadIdx.x < a.vn) {
@@ -474,7 +543,7 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
     // are compacted into a per-warp queue and processed 32 at a time, so the histogram
     // loop runs with full warps instead of the few lanes that happen to contribute.
     const uint32_t lane = threadIdx.x & 31u;
-    uint32_t* qt = reinterpret_cast<uint32_t*>(smem_raw + kQueueOff) + (threadIdx.x >> 5) * (kQueueCap * (1 + kG));
+    uint32_t* qt = reinterpret_cast<uint32_t*>(sm + kQueueOff) + (threadIdx.x >> 5) * (kQueueCap * (1 + kG));
     uint32_t* qP = qt + kQueueCap;
     uint32_t qlen = 0;
     auto flush = [&](uint32_t n) {
@@ -616,6 +685,59 @@ bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const 
     return true;
 }
 
+// ---- group-major key codes ------------------------------------------------------------
+// Per pair, per LUT group g (stages 4g..4g+3): a segment of cap 5-byte records, stored as
+// cap little-endian u32 words (record bits 0-31) followed by cap bytes (bits 32-39).  A
+// record holds the group's fields in stage order at their CodeMatrix offsets relative to
+// the group's first field (codebook.cpp:96-120 row layout), missing stages as zeros.
+__global__ void gm_pack_kernel(const uint8_t* __restrict__ payload, uint64_t payload_stride, uint64_t row_bits,
+                               const uint8_t* payload_end, const uint32_t* __restrict__ gbit, const uint32_t* __restrict__ gwidth,
+                               uint32_t n_groups, uint64_t src_row, uint64_t count, uint8_t* __restrict__ gm, uint64_t cap,
+                               uint64_t gm_stride, uint64_t dst_row) {
+    const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    const uint32_t g = blockIdx.y, pair = blockIdx.z;
+    if (t >= count) return;
+    const uint8_t* src = payload + pair * payload_stride;
+    const uint64_t w = read_bits64(src, (src_row + t) * row_bits + gbit[g], payload_end);
+    const uint64_t rec = gwidth[g] >= 64 ? w : (w & ((1ull << gwidth[g]) - 1ull));
+    uint8_t* seg = gm + pair * gm_stride + uint64_t(g) * cap * 5;
+    reinterpret_cast<uint32_t*>(seg)[dst_row + t] = uint32_t(rec);
+    seg[cap * 4 + dst_row + t] = uint8_t(rec >> 32);
+}
+
+bool gm_supported(const vqkv_stack_s& ks) {
+    if (ks.dim != kD) return false;
+    for (const auto& st : ks.stages)
+        if (st.size > 1024 || st.bits > 10) return false;
+    return true;
+}
+
+uint64_t gm_pair_bytes(const vqkv_stack_s& ks, uint64_t cap) {
+    return uint64_t((ks.n + kGroupStages - 1) / kGroupStages) * cap * 5;
+}
+
+void launch_keycodes_to_gm(const vqkv_stack_s& ks, const uint8_t* payload, uint64_t payload_stride, uint32_t n_pairs,
+                           uint64_t src_row, uint64_t count, uint8_t* gm, uint64_t cap, uint64_t gm_stride,
+                           uint64_t dst_row, cudaStream_t s) {
+    const uint32_t ng = (ks.n + kGroupStages - 1) / kGroupStages;
+    std::vector<uint32_t> h(2 * ng);
+    for (uint32_t g = 0; g < ng; ++g) {
+        const uint32_t s0 = g * kGroupStages, s1 = std::min(ks.n, s0 + kGroupStages);
+        h[g] = ks.stages[s0].bit_off;
+        h[ng + g] = ks.stages[s1 - 1].bit_off + ks.stages[s1 - 1].bits - ks.stages[s0].bit_off;
+    }
+    uint32_t* d = nullptr;
+    VQKV_CUDA(cudaMallocAsync(&d, sizeof(uint32_t) * 2 * ng, s));
+    VQKV_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(uint32_t) * 2 * ng, cudaMemcpyHostToDevice, s));
+    const uint64_t pb = payload_bytes(ks.row_bits, src_row + count);
+    const uint8_t* end = payload + uint64_t(n_pairs - 1) * payload_stride + pb;
+    dim3 grid(unsigned((count + 255) / 256), ng, n_pairs);
+    gm_pack_kernel<<<grid, 256, 0, s>>>(payload, payload_stride, ks.row_bits, end, d, d + ng, ng, src_row, count, gm, cap,
+                                        gm_stride, dst_row);
+    launch_check("gm_pack_kernel");
+    VQKV_CUDA(cudaFreeAsync(d, s));
+}
+
 void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s) {
     const uint64_t kent = ks.total_rows, vent = vs.total_rows;
     const uint32_t n_splits = uint32_t((a.n_comp + kSplitTokens - 1) / kSplitTokens);
@@ -651,15 +773,20 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
                     a.kcodes_dev + uint64_t(a.n_pairs - 1) * kstr + kpb,
                     a.vcodes_dev + uint64_t(a.n_pairs - 1) * vstr + vpb, float(scale), n_splits,
                     ph, po, pm, pl, a.init_stride ? a.init_stride : a.n_init,
-                    a.local_stride ? a.local_stride : a.n_local};
-        const size_t smem = kMainSmem;
+                    a.local_stride ? a.local_stride : a.n_local, a.kcodes_cap};
         static bool attr = false;
         if (!attr) {
-            VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(kMainSmem + kAlignSlack)));
+            VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(kGmSmem + kAlignSlack)));
             attr = true;
         }
         dim3 grid(n_splits + 1, a.n_pairs);
-        attend_lut_kernel<<<grid, kAttThreads, smem, s>>>(ma);
+        if (a.kcodes_layout == VQKV_KEYCODES_GROUP_MAJOR)
+            attend_lut_kernel<1><<<grid, kAttThreads, kGmSmem + kAlignSlack, s>>>(ma);
+        else
+            attend_lut_kernel<0><<<grid, kAttThreads, kMainSmem + kAlignSlack, s>>>(ma);
         launch_check("attend_lut_kernel");
     }
     {

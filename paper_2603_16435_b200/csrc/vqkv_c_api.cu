@@ -467,8 +467,45 @@ int vqkv_attend_decode(vqkv_stack_t ks, vqkv_stack_t vs, const vqkv_attend_args*
         need(a->n_init == 0 || (a->init_k_dev && a->init_v_dev), VQKV_INVALID_INPUT, "null init rows");
         need(a->n_local == 0 || (a->local_k_dev && a->local_v_dev), VQKV_INVALID_INPUT, "null local rows");
         need(a->n_comp == 0 || (a->kcodes_dev && a->vcodes_dev), VQKV_INVALID_INPUT, "null code payloads");
+        need(a->kcodes_layout == VQKV_KEYCODES_ROWS || a->kcodes_layout == VQKV_KEYCODES_GROUP_MAJOR, VQKV_INVALID_INPUT,
+             "unknown key-code layout");
+        if (a->kcodes_layout == VQKV_KEYCODES_GROUP_MAJOR && a->n_comp > 0) {
+            need(vqkv_dev::gm_supported(*ks) && vqkv_dev::attend_path() != 1 && vqkv_dev::attend_lut_supported(*ks, *vs, *a),
+                 VQKV_INVALID_INPUT, "group-major key codes need the LUT attention path (D = 128, group 4, <= 1024 entries)");
+            const uint64_t need_b = vqkv_dev::gm_pair_bytes(*ks, a->kcodes_cap);
+            need(a->kcodes_cap % 16 == 0 && a->kcodes_cap >= a->n_comp, VQKV_INVALID_INPUT,
+                 "kcodes_cap must be a multiple of 16 and >= n_comp");
+            need(a->kcodes_stride == 0 || (a->kcodes_stride >= need_b && a->kcodes_stride % 16 == 0), VQKV_INVALID_INPUT,
+                 "group-major kcodes_stride must be >= the buffer size and a multiple of 16");
+            need(reinterpret_cast<uintptr_t>(a->kcodes_dev) % 16 == 0, VQKV_INVALID_INPUT,
+                 "group-major key codes must be 16-byte aligned");
+        }
         DeviceGuard g(ks->device);
         launch_attend(*ks, *vs, *a, as_stream(stream));
+    });
+}
+
+uint64_t vqkv_keycodes_gm_bytes(vqkv_stack_t ks, uint64_t cap) {
+    if (!ks || cap % 16 != 0 || !vqkv_dev::gm_supported(*ks)) return 0;
+    return vqkv_dev::gm_pair_bytes(*ks, cap);
+}
+
+int vqkv_keycodes_to_gm(vqkv_stack_t ks, const uint8_t* payload, uint64_t payload_stride, uint32_t n_pairs,
+                        uint64_t src_row, uint64_t count, uint8_t* gm, uint64_t cap, uint64_t gm_stride, uint64_t dst_row,
+                        void* stream) {
+    return guard([&] {
+        check_stack(ks);
+        need(vqkv_dev::gm_supported(*ks), VQKV_INVALID_INPUT, "stack has no group-major layout (D = 128, <= 1024 entries)");
+        need(cap % 16 == 0 && dst_row + count <= cap, VQKV_INVALID_INPUT, "records out of the group-major capacity");
+        const uint64_t gb = vqkv_dev::gm_pair_bytes(*ks, cap);
+        need(gm_stride == 0 || gm_stride >= gb, VQKV_INVALID_INPUT, "gm_stride below the buffer size");
+        const uint64_t pb = payload_bytes(ks->row_bits, src_row + count);
+        need(payload_stride == 0 || payload_stride >= pb, VQKV_INVALID_INPUT, "payload_stride below the payload size");
+        if (n_pairs == 0 || count == 0) return;
+        need(payload && gm, VQKV_INVALID_INPUT, "null device buffer");
+        DeviceGuard g(ks->device);
+        vqkv_dev::launch_keycodes_to_gm(*ks, payload, payload_stride ? payload_stride : pb, n_pairs, src_row, count, gm, cap,
+                                        gm_stride ? gm_stride : gb, dst_row, as_stream(stream));
     });
 }
 
@@ -566,6 +603,7 @@ int vqkv_attend_decode_host(vqkv_stack_t ks, vqkv_stack_t vs, const vqkv_attend_
         };
         need(h->init_stride == 0 && h->local_stride == 0 && h->kcodes_stride == 0 && h->vcodes_stride == 0,
              VQKV_INVALID_INPUT, "host attention buffers must be dense (strides 0)");
+        need(h->kcodes_layout == VQKV_KEYCODES_ROWS, VQKV_INVALID_INPUT, "host attention takes CodeMatrix key rows");
         vqkv_attend_args d = *h;
         d.q_dev = static_cast<const float*>(up(h->q_dev, sizeof(float) * P * G * Dk));
         d.init_k_dev = static_cast<const float*>(up(h->init_k_dev, sizeof(float) * P * h->n_init * Dk));

@@ -208,6 +208,13 @@ void launch_reconstruct(const vqkv_stack_s& st, const uint8_t* payload, uint32_t
                         uint64_t begin, uint64_t end, float* out, cudaStream_t s,
                         uint64_t stream_stride = 0);
 void launch_attend(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s);
+int attend_path();
+bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a);
+bool gm_supported(const vqkv_stack_s& ks);
+uint64_t gm_pair_bytes(const vqkv_stack_s& ks, uint64_t cap);
+void launch_keycodes_to_gm(const vqkv_stack_s& ks, const uint8_t* payload, uint64_t payload_stride, uint32_t n_pairs,
+                           uint64_t src_row, uint64_t count, uint8_t* gm, uint64_t cap, uint64_t gm_stride,
+                           uint64_t dst_row, cudaStream_t s);
 void launch_lse_combine(const float* o, const float* lse, uint32_t parts, uint64_t rows, uint32_t dv, float* out,
                         float* out_lse, cudaStream_t s);
 

@@ -137,6 +137,37 @@ def reconstruct_streams(stack, payload: torch.Tensor, rows: int, begin: int = 0,
     return out
 
 
+GM_ALIGN = 16  # group-major capacity granule (tokens)
+
+
+def keycodes_gm_bytes(kstack, cap: int) -> int:
+    """Bytes per pair of the group-major key-code layout for `cap` tokens (0: unsupported stack)."""
+    return int(_lib.load().vqkv_keycodes_gm_bytes(_dev(kstack).h, cap))
+
+
+def keycodes_to_gm(kstack, payload: torch.Tensor, count: int, gm: Optional[torch.Tensor] = None, cap: int = 0,
+                   src_row: int = 0, dst_row: int = 0) -> torch.Tensor:
+    """Write rows [src_row, src_row + count) of each pair's CodeMatrix payload into records
+    [dst_row, dst_row + count) of the group-major buffer gm [n_pairs, keycodes_gm_bytes(cap)] u8."""
+    kd = _dev(kstack)
+    if payload.dim() == 1:
+        payload = payload.unsqueeze(0)
+    stride = _pair_stride(payload, torch.uint8, "payload", 1)
+    n_pairs = payload.shape[0]
+    if gm is None:
+        cap = cap or -(-max(count + dst_row, 1) // GM_ALIGN) * GM_ALIGN
+        nb = keycodes_gm_bytes(kd, cap)
+        if nb == 0:
+            raise InvalidInput("stack has no group-major layout (D = 128, <= 1024 entries per stage)")
+        gm = torch.zeros((n_pairs, nb), dtype=torch.uint8, device=payload.device)
+    elif cap == 0:
+        raise InvalidInput("cap is required with an existing group-major buffer")
+    gstride = _pair_stride(gm, torch.uint8, "gm", 1)
+    _lib.call("vqkv_keycodes_to_gm", kd.h, payload.data_ptr(), stride, n_pairs, src_row, count, gm.data_ptr(), cap,
+              gstride, dst_row, _stream(payload))
+    return gm
+
+
 def attend_decode(
     kstack,
     vstack,
@@ -150,11 +181,14 @@ def attend_decode(
     local_v: Optional[torch.Tensor] = None,
     scale: float = 0.0,
     want_lse: bool = True,
+    kcodes_gm_cap: int = 0,
 ) -> Tuple[torch.Tensor, Optional[torch.Tensor]]:
     """Decode-step attention for q [n_pairs, group, Dk] over init | compressed | local.
 
     init_k [n_pairs, n_init, Dk], local_k [n_pairs, n_local, Dk] (likewise V),
-    kcodes/vcodes [n_pairs, payload_bytes(n_comp)] u8.  Returns (out [n_pairs, group, Dv], lse [n_pairs, group]).
+    kcodes/vcodes [n_pairs, payload_bytes(n_comp)] u8.  With kcodes_gm_cap > 0, kcodes is
+    the group-major layout (keycodes_to_gm) with that capacity.  Returns (out [n_pairs, group, Dv],
+    lse [n_pairs, group]).
     """
     kd, vd = _dev(kstack), _dev(vstack)
     _need(q, torch.float32, "q")
@@ -181,6 +215,7 @@ def attend_decode(
         local_k.data_ptr() if n_local else None, local_v.data_ptr() if n_local else None, n_local,
         float(scale), out.data_ptr(), lse.data_ptr() if lse is not None else None,
         strides.get("init_k", 0), strides.get("local_k", 0), strides.get("kcodes", 0), strides.get("vcodes", 0),
+        _lib.KEYCODES_GROUP_MAJOR if kcodes_gm_cap else _lib.KEYCODES_ROWS, kcodes_gm_cap,
     )
     import ctypes as C
 

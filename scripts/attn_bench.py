@@ -4,7 +4,8 @@ import numpy as np, torch
 sys.path.insert(0, '.')
 from paper_2603_16435_b200 import codebook as P, device as Dv
 B, HKV, G, D = 16, 8, 4, 128
-ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
+ctx = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 131072
+gm_mode = "--gm" in sys.argv
 n_init, n_local = 4, 1024
 n_comp = ctx - n_init - n_local
 pairs = B * HKV
@@ -19,7 +20,12 @@ vc = torch.randint(0, 256, (pairs, vb), dtype=torch.uint8, device='cuda')
 ik, iv = torch.randn(pairs, n_init, D, device='cuda'), torch.randn(pairs, n_init, D, device='cuda')
 lk, lv = torch.randn(pairs, n_local, D, device='cuda'), torch.randn(pairs, n_local, D, device='cuda')
 q = torch.randn(pairs, G, D, device='cuda')
-f = lambda: Dv.attend_decode(ks, vs, q, kc, vc, n_comp, ik, iv, lk, lv)
+if gm_mode:  # the cache's attention layout for the key codes (maintained at append time)
+    cap = -(-n_comp // 16) * 16
+    kg = Dv.keycodes_to_gm(ks, kc, n_comp, cap=cap)
+    f = lambda: Dv.attend_decode(ks, vs, q, kg, vc, n_comp, ik, iv, lk, lv, kcodes_gm_cap=cap)
+else:
+    f = lambda: Dv.attend_decode(ks, vs, q, kc, vc, n_comp, ik, iv, lk, lv)
 f(); torch.cuda.synchronize()
 from paper_2603_16435_b200 import _lib
 import ctypes

@@ -221,7 +221,7 @@ def test_lse_combine_matches_monolithic(torch_mod):
 
 
 @pytest.mark.parametrize("nk,sk,nv,sv,n_pairs,n_init,n_comp,n_local",
-                         [(6, 256, 4, 128, 3, 4, 9000, 40), (56, 1024, 16, 512, 2, 4, 3000, 17), (3, 64, 2, 64, 2, 0, 100, 0),
+                         [(6, 256, 4, 128, 3, 4, 9000, 40), (56, 1024, 16, 512, 2, 4, 3000, 17), (56, 1024, 16, 512, 1, 3, 8300, 5), (3, 64, 2, 64, 2, 0, 100, 0),
                           (4, 128, 4, 128, 1, 2, 0, 33)])
 def test_attention_lut_path_vs_oracle(torch_mod, nk, sk, nv, sv, n_pairs, n_init, n_comp, n_local):
     """LUT/histogram fast path (D=128, G=4) against the oracle's attend over the same segments."""
@@ -254,3 +254,87 @@ def test_attention_lut_path_vs_oracle(torch_mod, nk, sk, nv, sv, n_pairs, n_init
             assert abs(lse[pi, gg] - ref_lse) <= 1e-3 * max(1.0, abs(ref_lse))
     print(f"worst scaled attention error {worst:.2e} (tolerance {ATT_TOL:.2e})")
     assert worst <= ATT_TOL
+
+
+def gm_records_np(ks, codes, cap):
+    """The group-major layout (include/vqkv_c.h) built in numpy from unpacked codes."""
+    n_rows, n = codes.shape
+    ng = (n + 3) // 4
+    out = np.zeros(ng * cap * 5, np.uint8)
+    bits = [O.index_bit_width(int(ks.sizes[s])) for s in range(n)]
+    for g in range(ng):
+        rec = np.zeros(n_rows, np.uint64)
+        off = 0
+        for s in range(4 * g, min(n, 4 * g + 4)):
+            rec |= codes[:, s].astype(np.uint64) << np.uint64(off)
+            off += bits[s]
+        seg = out[g * cap * 5:(g + 1) * cap * 5]
+        seg[: 4 * cap].view(np.uint32)[:n_rows] = (rec & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+        seg[4 * cap: 4 * cap + n_rows] = (rec >> np.uint64(32)).astype(np.uint8)
+    return out
+
+
+@pytest.mark.parametrize("nk,sk,nv,sv,n_pairs,n_init,n_comp,n_local",
+                         [(56, 1024, 16, 512, 2, 4, 3000, 17), (56, 1024, 16, 512, 1, 3, 8300, 5),
+                          (6, 256, 4, 128, 3, 4, 9000, 40), (5, 1000, 3, 64, 2, 0, 700, 3), (1, 9, 1, 4, 1, 1, 40, 0)])
+def test_attention_group_major_keys(torch_mod, nk, sk, nv, sv, n_pairs, n_init, n_comp, n_local):
+    """Group-major key codes: the transcoder writes the documented records, attention over them
+    computes the same logits as over the CodeMatrix rows (same lookups, same order), and it
+    matches the oracle within the tolerance."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+
+    rng = O.Rng(nk * 7 + sk)
+    ks = rng.stack(nk, sk, 128, O.KEY)
+    vs = rng.stack(nv, sv, 128, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    G = 4
+    mk = lambda n: rng.matrix(max(n_pairs * n, 1), 128)[: n_pairs * n].reshape(n_pairs, n, 128)
+    init_k, init_v, loc_k, loc_v = mk(n_init), mk(n_init), mk(n_local), mk(n_local)
+    g = np.random.default_rng(nk + 1)
+    kcodes = [g.integers(0, sk, (n_comp, nk)).astype(np.uint32) for _ in range(n_pairs)]
+    kc = np.stack([ks.pack(c) for c in kcodes])
+    vc = np.stack([vs.pack(g.integers(0, sv, (n_comp, nv)).astype(np.uint32)) for _ in range(n_pairs)])
+    q = rng.matrix(n_pairs * G, 128).reshape(n_pairs, G, 128)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    cap = -(-n_comp // 16) * 16 + 32  # spare capacity
+    gm = Dv.keycodes_to_gm(pk, t(kc), n_comp, cap=cap, gm=torch.zeros((n_pairs, Dv.keycodes_gm_bytes(pk, cap)),
+                                                                     dtype=torch.uint8, device="cuda"))
+    gm_h = gm.cpu().numpy()
+    for pi in range(n_pairs):
+        assert np.array_equal(gm_h[pi], gm_records_np(ks, kcodes[pi], cap))
+    seg = lambda a, n: t(a) if n else None
+    args = (seg(init_k, n_init), seg(init_v, n_init), seg(loc_k, n_local), seg(loc_v, n_local))
+    o_rows, l_rows = Dv.attend_decode(pk, pv, t(q), t(kc), t(vc), n_comp, *args)
+    o_gm, l_gm = Dv.attend_decode(pk, pv, t(q), gm, t(vc), n_comp, *args, kcodes_gm_cap=cap)
+    # same logits bit for bit; the value contraction's fp32 L2 atomics make the last bits
+    # of o run-to-run dependent on either layout
+    assert torch.equal(l_rows, l_gm)
+    assert torch.allclose(o_rows, o_gm, rtol=1e-5, atol=1e-5)
+    out = o_gm.cpu().numpy()
+    for pi in range(n_pairs):
+        for gg in range(G):
+            ref, _ = O.attend_segments(ks, vs, init_k[pi], init_v[pi], kc[pi], vc[pi], n_comp, loc_k[pi], loc_v[pi],
+                                       q[pi, gg])
+            assert np.abs(out[pi, gg] - ref).max() <= ATT_TOL * max(1.0, np.abs(ref).max())
+
+
+def test_group_major_errors(torch_mod):
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+    from paper_2603_16435_b200.errors import InvalidInput
+
+    rng = O.Rng(3)
+    pk = product_stack(rng.stack(4, 2048, 128, O.KEY))  # > 1024 entries: no group-major layout
+    assert Dv.keycodes_gm_bytes(pk, 64) == 0
+    ks = rng.stack(4, 64, 128, O.KEY)
+    pk, pv = product_stack(ks), product_stack(rng.stack(2, 64, 128, O.VALUE))
+    assert Dv.keycodes_gm_bytes(pk, 24) == 0  # cap not a multiple of 16
+    kc = torch.zeros((1, ks.payload_bytes(100)), dtype=torch.uint8, device="cuda")
+    vc = torch.zeros((1, 100), dtype=torch.uint8, device="cuda")
+    gm = Dv.keycodes_to_gm(pk, kc, 100, cap=112)
+    q = torch.randn(1, 4, 128, device="cuda")
+    with pytest.raises(InvalidInput):
+        Dv.attend_decode(pk, pv, q, gm, vc, 100, kcodes_gm_cap=96)  # cap < n_comp
+    with pytest.raises(InvalidInput):
+        Dv.keycodes_to_gm(pk, kc, 100, gm=gm, cap=112, dst_row=20)  # past the capacity
