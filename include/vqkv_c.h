@@ -190,6 +190,9 @@ int vqkv_attend_decode(vqkv_stack_t key_stack, vqkv_stack_t value_stack, const v
  * (payload_stride bytes apart) to records [dst_row, dst_row + count) of each pair's
  * group-major buffer (gm_stride bytes apart, 0 = vqkv_keycodes_gm_bytes). */
 uint64_t vqkv_keycodes_gm_bytes(vqkv_stack_t key_stack, uint64_t cap);
+/* 1 when vqkv_attend_decode accepts args with kcodes_layout = VQKV_KEYCODES_GROUP_MAJOR
+ * (the LUT attention path covers them), else 0. */
+int vqkv_attend_gm_supported(vqkv_stack_t key_stack, vqkv_stack_t value_stack, const vqkv_attend_args* args);
 int vqkv_keycodes_to_gm(vqkv_stack_t key_stack, const uint8_t* payload_dev, uint64_t payload_stride, uint32_t n_pairs,
                         uint64_t src_row, uint64_t count, uint8_t* gm_dev, uint64_t cap, uint64_t gm_stride,
                         uint64_t dst_row, void* stream);

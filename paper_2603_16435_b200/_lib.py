@@ -80,6 +80,7 @@ _SIGS = {
     "vqkv_encode_phase_clocks": (C.c_int, [P, u64p]),
     "vqkv_payload_append": (C.c_int, [P, C.c_uint64, C.c_uint64, P, C.c_uint64, C.c_uint64, C.c_uint32, P]),
     "vqkv_keycodes_gm_bytes": (C.c_uint64, [P, C.c_uint64]),
+    "vqkv_attend_gm_supported": (C.c_int, [P, P, C.POINTER(AttendArgs)]),
     "vqkv_keycodes_to_gm": (
         C.c_int,
         [P, P, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, P, C.c_uint64, C.c_uint64, C.c_uint64, P],

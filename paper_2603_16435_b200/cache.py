@@ -13,6 +13,11 @@ buffers with `vqkv_payload_append`; pending + local rows share one contiguous ra
 of 2 * local_len rows, so a flush is one batched encode of the first `pending` rows
 (kv_cache.cpp:102-120) and attention reads every segment in place (strided views, no copies).
 
+Key codes are also kept in the group-major attention layout (include/vqkv_c.h,
+vqkv_keycodes_to_gm) when the key stack has one: each flush transcodes its new rows once, and
+decode attention stages that layout by bulk copy instead of re-reading CodeMatrix rows per LUT
+group.  The CodeMatrix payload stays the source of truth (codes, view_block, snapshots).
+
 Semantics follow the reference exactly: prefill split (kv_cache.cpp:61-100), eviction to
 pending and deferred (or eager) flush at local_len pending rows (:122-141), token order of
 view_block (:143-189), memory accounting (:191-204), error kinds and messages.
@@ -34,7 +39,8 @@ class DeviceCacheState:
     """Batched CacheState on one GPU: n_streams streams with identical token counts."""
 
     def __init__(self, key_stack, value_stack, n_streams: int, init_len: int = 4, local_len: int = 1024,
-                 eager: bool = False, device: Optional[torch.device] = None, capacity_rows: int = 0):
+                 eager: bool = False, device: Optional[torch.device] = None, capacity_rows: int = 0,
+                 attn_layout: str = "auto"):
         if local_len < 1:  # WindowPolicy::validate (kv_cache.cpp:41-45)
             raise InvalidInput("local_len must be >= 1")
         if n_streams < 1:
@@ -58,6 +64,14 @@ class DeviceCacheState:
         self.cap_rows = 0
         self.kpay = self.vpay = None
         self.knorm = self.vnorm = None
+        # attention layout of the key codes: "group_major" mirror, or "rows" (the payload itself)
+        if attn_layout not in ("auto", "rows", "group_major"):
+            raise InvalidInput("attn_layout must be 'auto', 'rows' or 'group_major'")
+        gm_ok = Dv.keycodes_gm_bytes(self.kd, Dv.GM_ALIGN) > 0
+        if attn_layout == "group_major" and not gm_ok:
+            raise InvalidInput("the key stack has no group-major layout (D = 128, <= 1024 entries per stage)")
+        self.attn_layout = "group_major" if (attn_layout != "rows" and gm_ok) else "rows"
+        self.kgm, self.gm_cap = None, 0
         self._grow(max(int(capacity_rows), 0))
 
     # ---- geometry ---------------------------------------------------------
@@ -94,6 +108,15 @@ class DeviceCacheState:
             knorm[:, : self.n_comp] = self.knorm[:, : self.n_comp]
             vnorm[:, : self.n_comp] = self.vnorm[:, : self.n_comp]
         self.kpay, self.vpay, self.knorm, self.vnorm, self.cap_rows = kpay, vpay, knorm, vnorm, cap
+        if self.attn_layout == "group_major":  # records depend on the capacity: rebuild from the payload
+            self.gm_cap = -(-cap // Dv.GM_ALIGN) * Dv.GM_ALIGN
+            self.kgm = torch.zeros((self.n_streams, Dv.keycodes_gm_bytes(self.kd, self.gm_cap)), dtype=torch.uint8,
+                                   device=self.device)
+            self._rebuild_gm()
+
+    def _rebuild_gm(self) -> None:
+        if self.kgm is not None and self.n_comp:
+            Dv.keycodes_to_gm(self.kstack, self.kpay, self.n_comp, gm=self.kgm, cap=self.gm_cap)
 
     def _encode_append(self, keys: torch.Tensor, values: torch.Tensor) -> None:
         """quantize_batch of [S, n, D] rows and CodeMatrix::append of the result."""
@@ -107,6 +130,8 @@ class DeviceCacheState:
         for pay, src, rb in ((self.kpay, kp, self.kd.row_bits), (self.vpay, vp, self.vd.row_bits)):
             _lib.call("vqkv_payload_append", pay.data_ptr(), pay.stride(0), self.n_comp * rb, src.data_ptr(),
                       src.stride(0), n * rb, self.n_streams, stream)
+        if self.kgm is not None:
+            Dv.keycodes_to_gm(self.kstack, kp, n, gm=self.kgm, cap=self.gm_cap, dst_row=self.n_comp)
         self.knorm[:, self.n_comp: self.n_comp + n] = kn
         self.vnorm[:, self.n_comp: self.n_comp + n] = vn
         self.n_comp += n
@@ -215,7 +240,10 @@ class DeviceCacheState:
         ratio = 1.0 - bits / float(self.n_comp * spt * 16) if self.n_comp else 0.0
         return dict(raw_bytes_equivalent=self.total_len() * spt * 2, compressed_payload_bits=bits,
                     codebook_overhead_bytes=self.kd.serialized_bytes() + self.vd.serialized_bytes(),
-                    effective_ratio=ratio)
+                    effective_ratio=ratio,
+                    # device-only: the group-major key-code mirror (5 B per token per 4 key stages)
+                    attention_layout_bytes=self.n_comp * 5 * (-(-self.kd.n // 4))
+                    if self.kgm is not None else 0)
 
     def attend(self, q: torch.Tensor, scale: float = 0.0, want_lse: bool = True):
         """Decode-step attention for q [S, G, Dk] over every segment, read in place
@@ -223,12 +251,14 @@ class DeviceCacheState:
         if self.total_len() == 0:
             raise InvalidState("cannot attend over an empty cache")
         ni, nt = self.n_init, self.n_tail
+        gm = (self.kgm is not None and self.n_comp > 0 and q.dim() == 3
+              and Dv.attend_gm_supported(self.kstack, self.vstack, self.n_streams, q.shape[1], ni, self.n_comp, nt))
         return Dv.attend_decode(
             self.kstack, self.vstack, q,
-            self.kpay if self.n_comp else None, self.vpay if self.n_comp else None, self.n_comp,
+            (self.kgm if gm else self.kpay) if self.n_comp else None, self.vpay if self.n_comp else None, self.n_comp,
             self.init_k[:, :ni] if ni else None, self.init_v[:, :ni] if ni else None,
             self.tail_k[:, :nt] if nt else None, self.tail_v[:, :nt] if nt else None,
-            scale=scale, want_lse=want_lse)
+            scale=scale, want_lse=want_lse, kcodes_gm_cap=self.gm_cap if gm else 0)
 
     def fidelity(self, original_keys: torch.Tensor, original_values: torch.Tensor, queries: torch.Tensor,
                  scale: float = 0.0) -> Dict[str, torch.Tensor]:
@@ -414,4 +444,5 @@ class DeviceCacheState:
                 cache.tail_v[:, a:b] = t([d[src][1] for d in parsed])
         cache.n_init, cache.n_comp, cache.n_tail = ni, nc, npd + nl
         cache.prefilled, cache.batched = first["prefilled"], first["batched"]
+        cache._rebuild_gm()
         return cache

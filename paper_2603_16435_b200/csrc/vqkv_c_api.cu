@@ -490,6 +490,13 @@ uint64_t vqkv_keycodes_gm_bytes(vqkv_stack_t ks, uint64_t cap) {
     return vqkv_dev::gm_pair_bytes(*ks, cap);
 }
 
+int vqkv_attend_gm_supported(vqkv_stack_t ks, vqkv_stack_t vs, const vqkv_attend_args* a) {
+    if (!ks || !vs || !a) return 0;
+    return (vqkv_dev::gm_supported(*ks) && vqkv_dev::attend_path() != 1 && vqkv_dev::attend_lut_supported(*ks, *vs, *a))
+               ? 1
+               : 0;
+}
+
 int vqkv_keycodes_to_gm(vqkv_stack_t ks, const uint8_t* payload, uint64_t payload_stride, uint32_t n_pairs,
                         uint64_t src_row, uint64_t count, uint8_t* gm, uint64_t cap, uint64_t gm_stride, uint64_t dst_row,
                         void* stream) {

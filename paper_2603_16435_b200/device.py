@@ -168,6 +168,16 @@ def keycodes_to_gm(kstack, payload: torch.Tensor, count: int, gm: Optional[torch
     return gm
 
 
+def attend_gm_supported(kstack, vstack, n_pairs: int, group: int, n_init: int, n_comp: int, n_local: int) -> bool:
+    """Whether attend_decode takes group-major key codes for this shape (the LUT path covers it)."""
+    import ctypes as C
+
+    a = _lib.AttendArgs()
+    a.n_pairs, a.group, a.n_init, a.n_comp, a.n_local = n_pairs, group, n_init, n_comp, n_local
+    a.kcodes_layout = _lib.KEYCODES_GROUP_MAJOR
+    return bool(_lib.load().vqkv_attend_gm_supported(_dev(kstack).h, _dev(vstack).h, C.byref(a)))
+
+
 def attend_decode(
     kstack,
     vstack,

@@ -277,3 +277,57 @@ def test_cache_vqks_snapshots(torch_mod, tmp_path):
     other = product_stack(rng.stack(3, 16, 8, O.KEY))
     with pytest.raises(InvalidInput):
         DeviceCacheState.load_snapshots(paths, other, pv)
+
+
+def test_cache_group_major_mirror(torch_mod, tmp_path):
+    """The group-major key-code mirror: kept in step through prefill, flushes and capacity
+    growth (records rebuilt from the payload) and snapshot loads; attention over it equals
+    attention over the CodeMatrix rows and the oracle."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+    from paper_2603_16435_b200.cache import DeviceCacheState
+
+    rng = O.Rng(7700)
+    ks, vs = rng.stack(5, 256, 128, O.KEY), rng.stack(3, 64, 128, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    S, init_len, local_len, L0 = 2, 4, 64, 2000
+    dc = DeviceCacheState(pk, pv, S, init_len, local_len)
+    rows = DeviceCacheState(pk, pv, S, init_len, local_len, attn_layout="rows")
+    assert dc.attn_layout == "group_major" and rows.kgm is None
+    ref = O.Cache(ks, vs, init_len, local_len, False)
+    x = rng.matrix(S * L0, 128).reshape(S, L0, 128)
+    y = rng.matrix(S * L0, 128).reshape(S, L0, 128)
+    for c in (dc, rows):
+        c.prefill(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+    ref.prefill(x[0], y[0])
+    q = rng.matrix(S * 4, 128).reshape(S, 4, 128)
+    qt = torch.from_numpy(q).cuda()
+
+    def check(c):
+        gm = Dv.keycodes_to_gm(pk, c.kpay, c.n_comp, cap=c.gm_cap)
+        assert torch.equal(gm, c.kgm[:, : gm.shape[1]])
+        o, l = c.attend(qt)
+        o2, l2 = rows.attend(qt)
+        assert torch.equal(l, l2) and torch.allclose(o, o2, rtol=1e-5, atol=1e-5)
+        for g in range(4):
+            r = ref.attend(q[0, g])
+            assert np.abs(o[0, g].cpu().numpy() - r).max() <= ATT_TOL * max(1.0, np.abs(r).max())
+
+    check(dc)
+    cap0 = dc.cap_rows
+    for _ in range(3 * local_len):  # flushes, then growth past the first capacity
+        k1, v1 = rng.matrix(S, 128), rng.matrix(S, 128)
+        ref.append_token(k1[0], v1[0])
+        for c in (dc, rows):
+            c.append_token(torch.from_numpy(k1).cuda(), torch.from_numpy(v1).cuda())
+    assert dc.cap_rows > cap0 and dc.counts()["batched"] >= 2
+    check(dc)
+    assert dc.memory_report()["attention_layout_bytes"] == dc.n_comp * 5 * 2
+    p = str(tmp_path / "s.vqks")
+    paths = []
+    for i in range(S):
+        paths.append(str(tmp_path / f"s{i}.vqks"))
+        dc.save_snapshot(i, paths[-1])
+    back = DeviceCacheState.load_snapshots(paths, pk, pv)
+    assert back.attn_layout == "group_major"
+    check(back)
