@@ -317,12 +317,17 @@ def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
         kc = torch.randint(0, 256, (n_pairs, kb_ + 16), dtype=torch.uint8, device="cuda", generator=gen)[:, :kb_]
         vc = torch.randint(0, 256, (n_pairs, vb_ + 16), dtype=torch.uint8, device="cuda", generator=gen)[:, :vb_]
         kc, vc = kc.contiguous(), vc.contiguous()
+        # the key codes as DeviceCacheState keeps them for attention: the group-major mirror
+        # (transcoded once per flushed row at append time, outside the decode step)
+        cap = -(-max(n_comp_, 1) // Dv.GM_ALIGN) * Dv.GM_ALIGN
+        kg = Dv.keycodes_to_gm(kst, kc, n_comp_, cap=cap)
+        del kc
         f = lambda n: (torch.randn(n_pairs, n, D, device="cuda", generator=gen) if n else None)
-        return kc, vc, f(n_init_), f(n_init_), f(n_local_), f(n_local_)
+        return (kg, cap), vc, f(n_init_), f(n_init_), f(n_local_), f(n_local_)
 
-    kc, vc, ik, iv, lk, lv = make(pairs, n_comp, n_init, n_local)
+    (kc, kcap), vc, ik, iv, lk, lv = make(pairs, n_comp, n_init, n_local)
     q = torch.randn(pairs, G, D, device="cuda", generator=gen)
-    run = lambda: Dv.attend_decode(kst, vst, q, kc, vc, n_comp, ik, iv, lk, lv)
+    run = lambda: Dv.attend_decode(kst, vst, q, kc, vc, n_comp, ik, iv, lk, lv, kcodes_gm_cap=kcap)
     for _ in range(max(1, args.warmup)):
         run()
     torch.cuda.synchronize()
@@ -342,7 +347,8 @@ def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
         "metric": "decode-attn cache tokens/s per layer-step (B*L/t)",
         "config": {"workload": "configs[2]: decode step, 128K-token VQ-compressed cache, batch 16, 8 KV heads "
                                f"sharded over {world} GPU(s), G=4", "context": ctx, "batch": B,
-                   "kv_heads_per_gpu": len(heads), "compressed_rows": n_comp, "raw_rows": n_init + n_local},
+                   "kv_heads_per_gpu": len(heads), "compressed_rows": n_comp, "raw_rows": n_init + n_local,
+                   "key_code_layout": "group-major (the cache's attention mirror, same 70 B per token)"},
         "value": B * ctx / (ms / 1e3), "unit": "tokens/s", "ms_per_layer_step": ms,
         "roofline": {"bound": "hbm", "achieved": bytes_rank / (ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                      "frac": bytes_rank / (ms / 1e3) / 1e9 / hbm,
@@ -357,9 +363,9 @@ def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
         nc = sh.comp[1] - sh.comp[0]
         ni = sh.init[1] - sh.init[0]
         nl = sh.local[1] - sh.local[0]
-        kc, vc, ik, iv, lk, lv = make(KV_HEADS, nc, ni, nl)
+        (kc, kcap), vc, ik, iv, lk, lv = make(KV_HEADS, nc, ni, nl)
         q1 = torch.randn(KV_HEADS, G, D, device="cuda", generator=torch.Generator(device="cuda").manual_seed(7))
-        part = lambda: Dv.attend_decode(kst, vst, q1, kc, vc, nc, ik, iv, lk, lv)
+        part = lambda: Dv.attend_decode(kst, vst, q1, kc, vc, nc, ik, iv, lk, lv, kcodes_gm_cap=kcap)
         o_l, l_l = part()
         sharding.gather_and_merge(o_l, l_l)
         torch.cuda.synchronize()
