@@ -189,34 +189,61 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
     return r;
 }
 
-// raw init/local rows of one pair: direct fp32 attention (no codebooks)
+// raw init/local rows of one pair: direct fp32 attention (no codebooks).  Latency matters
+// here (one CTA per pair runs beside the split CTAs): rows are read in batches with all
+// their loads in flight, and every value load feeds the 4 heads.
 __device__ void raw_rows(const MainArgs& a, uint32_t pair, float* smem) {
+    constexpr int kRowBatch = 8;
     float* red = smem;                 // 64
     float* qs = smem + 64;             // G*D
-    float* ls = qs + kG * kD;          // logits [n_raw][G] (n_raw <= 8192)
+    float* ls = qs + kG * kD;          // logits / weights [n_raw][G] (n_raw <= 8192)
+    float* po = ls + kSplitTokens * kG;  // [4 row groups][G][D] partial outputs
     for (uint32_t i = threadIdx.x; i < kG * kD; i += blockDim.x) qs[i] = a.q[uint64_t(pair) * kG * kD + i];
     __syncthreads();
-    const uint64_t n_raw = a.n_init + a.n_local;
+    const uint32_t n_raw = uint32_t(a.n_init + a.n_local);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (uint64_t r = warp; r < n_raw; r += nw) {
-        const float* k = (r < a.n_init) ? a.init_k + (uint64_t(pair) * a.init_stride + r) * kD
-                                        : a.local_k + (uint64_t(pair) * a.local_stride + (r - a.n_init)) * kD;
-        const float4 kv = reinterpret_cast<const float4*>(k)[lane];
-        for (int g = 0; g < kG; ++g) {
-            const float4 qv = reinterpret_cast<const float4*>(qs + g * kD)[lane];
-            float d = kv.x * qv.x + kv.y * qv.y + kv.z * qv.z + kv.w * qv.w;
+    auto krow = [&](uint32_t r) -> const float4* {
+        return reinterpret_cast<const float4*>(
+            (r < a.n_init) ? a.init_k + (uint64_t(pair) * a.init_stride + r) * kD
+                           : a.local_k + (uint64_t(pair) * a.local_stride + (r - a.n_init)) * kD);
+    };
+    float4 qv[kG];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-            if (lane == 0) ls[r * kG + g] = d * a.scale;
+    for (int g = 0; g < kG; ++g) qv[g] = reinterpret_cast<const float4*>(qs + g * kD)[lane];
+    const bool up = lane & 16u, b3 = lane & 8u;
+    for (uint32_t r0 = warp; r0 < n_raw; r0 += nw * kRowBatch) {
+        float4 kv[kRowBatch];
+#pragma unroll
+        for (int u = 0; u < kRowBatch; ++u) {
+            const uint32_t r = r0 + u * nw;
+            kv[u] = (r < n_raw) ? __ldg(krow(r) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kRowBatch; ++u) {
+            float d[kG];
+#pragma unroll
+            for (int g = 0; g < kG; ++g)
+                d[g] = kv[u].x * qv[g].x + kv[u].y * qv[g].y + kv[u].z * qv[g].z + kv[u].w * qv[g].w;
+            // 4-value butterfly: 6 shuffles leave head 2*bit4 + bit3 summed over the warp
+            float k0 = up ? d[2] : d[0], k1 = up ? d[3] : d[1];
+            k0 += __shfl_xor_sync(0xffffffffu, up ? d[0] : d[2], 16);
+            k1 += __shfl_xor_sync(0xffffffffu, up ? d[1] : d[3], 16);
+            float k = b3 ? k1 : k0;
+            k += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+            k += __shfl_xor_sync(0xffffffffu, k, 4);
+            k += __shfl_xor_sync(0xffffffffu, k, 2);
+            k += __shfl_xor_sync(0xffffffffu, k, 1);
+            const uint32_t r = r0 + u * nw;
+            if ((lane & 7u) == 0 && r < n_raw) ls[r * kG + (lane >> 3)] = k * a.scale;
         }
     }
     __syncthreads();
     for (int g = 0; g < kG; ++g) {
         float m = -INFINITY;
-        for (uint64_t r = threadIdx.x; r < n_raw; r += blockDim.x) m = fmaxf(m, ls[r * kG + g]);
+        for (uint32_t r = threadIdx.x; r < n_raw; r += blockDim.x) m = fmaxf(m, ls[r * kG + g]);
         m = block_max(m, red);
         float l = 0.f;
-        for (uint64_t r = threadIdx.x; r < n_raw; r += blockDim.x) {
+        for (uint32_t r = threadIdx.x; r < n_raw; r += blockDim.x) {
             const float p = __expf(ls[r * kG + g] - m);
             ls[r * kG + g] = p;
             l += p;
@@ -228,28 +255,42 @@ __device__ void raw_rows(const MainArgs& a, uint32_t pair, float* smem) {
         }
     }
     __syncthreads();
-    // o[g][d] = sum_r p[r][g] v_r[d]; thread = (g, d)
-    // 8 independent accumulators keep 8 row loads in flight per thread
-    for (uint32_t gd = threadIdx.x; gd < kG * kD; gd += blockDim.x) {
-        const uint32_t g = gd / kD, d = gd % kD;
+    // o[g][d] = sum_r p[r][g] v_r[d]: thread = (row group rg, d) over rows rg, rg + 4, ...;
+    // each value load feeds the 4 heads, kRowBatch loads in flight
+    {
+        const uint32_t d = threadIdx.x % kD, rg = threadIdx.x / kD, nrg = blockDim.x / kD;
         const float* iv = a.init_v + uint64_t(pair) * a.init_stride * kD + d;
         const float* lv = a.local_v + uint64_t(pair) * a.local_stride * kD + d;
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        uint64_t r = 0;
-        for (; r + 8 <= n_raw; r += 8) {
+        const float4* p4 = reinterpret_cast<const float4*>(ls);
+        float acc[kG] = {0.f, 0.f, 0.f, 0.f};
+        for (uint32_t r0 = rg; r0 < n_raw; r0 += nrg * kRowBatch) {
+            float x[kRowBatch];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint64_t rr = r + u;
-                const float x = (rr < a.n_init) ? __ldg(iv + rr * kD) : __ldg(lv + (rr - a.n_init) * kD);
-                acc[u] = fmaf(ls[rr * kG + g], x, acc[u]);
+            for (int u = 0; u < kRowBatch; ++u) {
+                const uint32_t r = r0 + u * nrg;
+                x[u] = (r >= n_raw) ? 0.f : (r < a.n_init) ? __ldg(iv + uint64_t(r) * kD) : __ldg(lv + uint64_t(r - a.n_init) * kD);
+            }
+#pragma unroll
+            for (int u = 0; u < kRowBatch; ++u) {
+                const uint32_t r = r0 + u * nrg;
+                if (r < n_raw) {
+                    const float4 p = p4[r];
+                    acc[0] = fmaf(p.x, x[u], acc[0]);
+                    acc[1] = fmaf(p.y, x[u], acc[1]);
+                    acc[2] = fmaf(p.z, x[u], acc[2]);
+                    acc[3] = fmaf(p.w, x[u], acc[3]);
+                }
             }
         }
-        for (; r < n_raw; ++r) {
-            const float x = (r < a.n_init) ? __ldg(iv + r * kD) : __ldg(lv + (r - a.n_init) * kD);
-            acc[0] = fmaf(ls[r * kG + g], x, acc[0]);
-        }
-        a.part_o[(uint64_t(pair) * kG + g) * kD + d] =
-            ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+#pragma unroll
+        for (int g = 0; g < kG; ++g) po[(rg * kG + g) * kD + d] = acc[g];
+    }
+    __syncthreads();
+    const uint32_t nrg = blockDim.x / kD;
+    for (uint32_t gd = threadIdx.x; gd < kG * kD; gd += blockDim.x) {
+        float o = 0.f;
+        for (uint32_t rg = 0; rg < nrg; ++rg) o += po[rg * kG * kD + gd];
+        a.part_o[uint64_t(pair) * kG * kD + gd] = o;
     }
 }
 
