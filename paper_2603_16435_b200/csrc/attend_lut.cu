@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(256) lut_kernel(LutArgs a, uint32_t n_pairs) {
     }
     __syncthreads();
     const uint32_t eg = threadIdx.x & 31, p = threadIdx.x >> 5;
-    float acc[4][kG];
+    __align__(8) float acc[4][kG];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -95,16 +95,15 @@ __global__ void __launch_bounds__(256) lut_kernel(LutArgs a, uint32_t n_pairs) {
         float2 ev[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) ev[i] = *reinterpret_cast<const float2*>(es + (eg + 32 * i) * kLutStride + c);
+        // packed FFMA2 over head pairs: per lane the same fmaf sequence as scalar code
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            acc[i][0] = fmaf(q0.x, ev[i].x, acc[i][0]);
-            acc[i][1] = fmaf(q0.y, ev[i].x, acc[i][1]);
-            acc[i][2] = fmaf(q0.z, ev[i].x, acc[i][2]);
-            acc[i][3] = fmaf(q0.w, ev[i].x, acc[i][3]);
-            acc[i][0] = fmaf(q1.x, ev[i].y, acc[i][0]);
-            acc[i][1] = fmaf(q1.y, ev[i].y, acc[i][1]);
-            acc[i][2] = fmaf(q1.z, ev[i].y, acc[i][2]);
-            acc[i][3] = fmaf(q1.w, ev[i].y, acc[i][3]);
+            float2* a2 = reinterpret_cast<float2*>(acc[i]);
+            const float2 ex = make_float2(ev[i].x, ev[i].x), ey = make_float2(ev[i].y, ev[i].y);
+            a2[0] = ptx::fma2(make_float2(q0.x, q0.y), ex, a2[0]);
+            a2[1] = ptx::fma2(make_float2(q0.z, q0.w), ex, a2[1]);
+            a2[0] = ptx::fma2(make_float2(q1.x, q1.y), ey, a2[0]);
+            a2[1] = ptx::fma2(make_float2(q1.z, q1.w), ey, a2[1]);
         }
     }
     if (p0 + p < n_pairs)
