@@ -654,29 +654,59 @@ __global__ void lut_weights_kernel(const float* __restrict__ part_m, const float
 
 // CTA = (pair, 256-entry chunk of the value codebooks): merge the split
 // histograms of the chunk, contract with the chunk's codebook rows and add the
-// partial output into acc[pair][g][d] (fp32 atomics in L2).
+// partial output into acc[pair][g][d] (fp32 atomics in L2).  Merge: every split's
+// load is in flight at once.  Contraction: thread = (d, quarter of the chunk), one
+// codebook load feeds the 4 heads.
 __global__ void __launch_bounds__(512) lut_contract_kernel(const float* __restrict__ part_h, const float* __restrict__ w,
                                                            uint32_t n_splits, const float* __restrict__ veff,
                                                            uint64_t ventries, float* __restrict__ acc) {
-    __shared__ float hs[256][kG];
+    constexpr int kChunk = 256, kMerge = 16;
+    __shared__ float4 hs[kChunk];
+    __shared__ float4 po[4][kD];
     const uint32_t pair = blockIdx.y;
-    const uint64_t e0 = uint64_t(blockIdx.x) * 256;
-    const uint32_t ne = uint32_t((ventries - e0 < 256) ? (ventries - e0) : 256);
+    const uint64_t e0 = uint64_t(blockIdx.x) * kChunk;
+    const uint32_t ne = uint32_t((ventries - e0 < kChunk) ? (ventries - e0) : kChunk);
     const uint32_t ns = n_splits + 1;
-    for (uint32_t i = threadIdx.x; i < 256 * kG; i += blockDim.x) {
+    float* hsf = reinterpret_cast<float*>(hs);
+    for (uint32_t i = threadIdx.x; i < kChunk * kG; i += blockDim.x) {
         const uint32_t e = i / kG, g = i % kG;
         float v = 0.f;
-        if (e < ne)
-            for (uint32_t s = 0; s < n_splits; ++s)
-                v = fmaf(w[(uint64_t(pair) * ns + s) * kG + g],
-                         __ldg(part_h + ((uint64_t(pair) * n_splits + s) * ventries + e0) * kG + i), v);
-        hs[e][g] = v;
+        if (e < ne) {
+            const float* src = part_h + (uint64_t(pair) * n_splits * ventries + e0) * kG + i;
+            const float* wp = w + uint64_t(pair) * ns * kG + g;
+            for (uint32_t s0 = 0; s0 < n_splits; s0 += kMerge) {
+                float x[kMerge];
+#pragma unroll
+                for (int k = 0; k < kMerge; ++k)
+                    x[k] = (s0 + k < n_splits) ? __ldg(src + uint64_t(s0 + k) * ventries * kG) : 0.f;
+#pragma unroll
+                for (int k = 0; k < kMerge; ++k)
+                    if (s0 + k < n_splits) v = fmaf(wp[(s0 + k) * kG], x[k], v);
+            }
+        }
+        hsf[i] = v;
     }
     __syncthreads();
-    const uint32_t g = threadIdx.x / kD, d = threadIdx.x % kD;
-    float o = 0.f;
-    for (uint32_t e = 0; e < ne; ++e) o = fmaf(hs[e][g], __ldg(veff + (e0 + e) * kD + d), o);
-    atomicAdd(acc + (uint64_t(pair) * kG + g) * kD + d, o);
+    const uint32_t d = threadIdx.x % kD, qt = threadIdx.x / kD;  // quarter qt: entries qt, qt + 4, ...
+    float o[kG] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (uint32_t e = qt; e < ne; e += 4) {
+        const float x = __ldg(veff + (e0 + e) * kD + d);
+        const float4 h = hs[e];
+        o[0] = fmaf(h.x, x, o[0]);
+        o[1] = fmaf(h.y, x, o[1]);
+        o[2] = fmaf(h.z, x, o[2]);
+        o[3] = fmaf(h.w, x, o[3]);
+    }
+    po[qt][d] = make_float4(o[0], o[1], o[2], o[3]);
+    __syncthreads();
+    if (threadIdx.x < kG * kD) {
+        const uint32_t g = threadIdx.x / kD, dd = threadIdx.x % kD;
+        const float* pf = reinterpret_cast<const float*>(po);
+        const float r = (pf[(0 * kD + dd) * kG + g] + pf[(1 * kD + dd) * kG + g]) +
+                        (pf[(2 * kD + dd) * kG + g] + pf[(3 * kD + dd) * kG + g]);
+        atomicAdd(acc + (uint64_t(pair) * kG + g) * kD + dd, r);
+    }
 }
 
 // out = (acc + w_raw * o_raw) / L, lse = M + log L
