@@ -116,6 +116,120 @@ __global__ void __launch_bounds__(256) lut_kernel(LutArgs a, uint32_t n_pairs) {
         }
 }
 
+// ---- LUT build on the tensor cores --------------------------------------------------------
+// The LUT is a GEMM: LUT[pair][e][g] = scale * E[e] . q[pair][g], i.e. [entries x 128] x
+// [128 x (pairs * G)].  fp16 split precision: E = E_hi + E_lo (stack operands, the encoder's
+// pre-swizzled chunks), q 2^sigma = Q_hi + Q_lo (per row power-of-two scale, exact), and
+// E_hi Q_lo + E_lo Q_hi + E_hi Q_hi accumulate in fp32 in TMEM; the dropped E_lo Q_lo and the
+// lo roundings are ~2^-22 relative to sum_k |E_k q_k|, the fp32 FFMA LUT's own error level.
+// q_prep_kernel: one warp per (pair, g) row -> Q_hi / Q_lo in 128-row SW128 K-major tiles
+// (the half_copy_kernel layout) and qscl[row] = scale * 2^-sigma.
+__global__ void q_prep_kernel(const float* __restrict__ q, uint32_t n_rows, uint32_t n_rows_pad, float scale,
+                              __half* __restrict__ qhi, __half* __restrict__ qlo, float* __restrict__ qscl) {
+    const uint32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (r >= n_rows_pad) return;
+    float4 v = (r < n_rows) ? reinterpret_cast<const float4*>(q + uint64_t(r) * kD)[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float m = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int sig = 0;
+    if (m > 0.f && isfinite(m)) {
+        int e;
+        frexpf(m, &e);  // m in [2^(e-1), 2^e): m 2^sig < 2^14
+        sig = min(100, max(-100, 14 - e));
+    }
+    const float sc = ldexpf(1.0f, sig);
+    const float x[4] = {v.x * sc, v.y * sc, v.z * sc, v.w * sc};
+    const uint32_t t = r >> 7, rr = r & 127;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t k = lane * 4 + i, kb = k >> 6, kk = k & 63;
+        const uint64_t off = uint64_t(t) * 16384 + kb * 8192 + rr * 64 + (((kk >> 3) ^ (rr & 7)) << 3) + (kk & 7);
+        const __half h = __float2half_rn(x[i]);
+        qhi[off] = h;
+        qlo[off] = __float2half_rn(x[i] - __half2float(h));
+    }
+    if (lane == 0) qscl[r] = (r < n_rows) ? ldexpf(scale, -sig) : 0.f;
+}
+
+// CTA = (128-entry chunk c of key stage s, 128-row tile of (pair, g) query rows), 128 threads:
+// one bulk-copy wave of the four 32 KB operands, 24 MMAs M128 N128 K16 issued by one thread,
+// then thread = entry row = TMEM lane stores its 32 pairs' float4 (coalesced across lanes).
+constexpr uint32_t kLutTcSmem = 4 * 32768 + 1024;
+__global__ void __launch_bounds__(128) lut_tc_kernel(const __half* __restrict__ eff16, const __half* __restrict__ eff16lo,
+                                                     const StageInfo* __restrict__ kst, const __half* __restrict__ qhi,
+                                                     const __half* __restrict__ qlo, const float* __restrict__ qscl,
+                                                     uint32_t n_pairs, uint64_t kentries, float4* __restrict__ lut) {
+    extern __shared__ uint8_t lsm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(lsm_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar_ld, bar_mma;
+    __shared__ uint32_t tmem_base;
+    const StageInfo si = kst[blockIdx.y];
+    const uint32_t c = blockIdx.x, tq = blockIdx.z;
+    if (c * 128 >= si.size) return;  // uniform per CTA
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(ptx::smem_u32(&bar_ld), 1);
+        ptx::mbar_init(ptx::smem_u32(&bar_mma), 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) {
+        ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 128);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t s_ehi = ptx::smem_u32(sm), s_elo = s_ehi + 32768, s_qhi = s_ehi + 65536, s_qlo = s_ehi + 98304;
+    if (threadIdx.x == 0) {
+        const uint32_t bar = ptx::smem_u32(&bar_ld);
+        ptx::mbar_arrive_expect_tx(bar, 4 * 32768);
+        const uint64_t eo = si.eff16_off + uint64_t(c) * 18432;
+        ptx::bulk_g2s(s_ehi, eff16 + eo, 32768, bar);
+        ptx::bulk_g2s(s_elo, eff16lo + eo, 32768, bar);
+        ptx::bulk_g2s(s_qhi, qhi + uint64_t(tq) * 16384, 32768, bar);
+        ptx::bulk_g2s(s_qlo, qlo + uint64_t(tq) * 16384, 32768, bar);
+        ptx::mbar_wait(bar, 0);
+        ptx::tc_fence_after();
+        constexpr uint32_t idesc = ptx::idesc_f16_f32(128, 128);
+        const uint32_t A[3] = {s_ehi, s_elo, s_ehi}, B[3] = {s_qlo, s_qhi, s_qhi};  // small terms first
+#pragma unroll
+        for (int part = 0; part < 3; ++part)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32;
+                ptx::mma_f16_ss(tmem, ptx::umma_desc_sw128(A[part] + koff), ptx::umma_desc_sw128(B[part] + koff), idesc,
+                                (part | k) ? 1u : 0u);
+            }
+        ptx::mma_commit(ptx::smem_u32(&bar_mma));
+    }
+    __syncwarp();
+    ptx::mbar_wait(ptx::smem_u32(&bar_mma), 0);
+    ptx::tc_fence_after();
+    const uint32_t j = c * 128 + warp * 32 + lane;  // entry within the stage
+    const uint64_t e = si.eff_off / kD + j;
+    const float* sclp = qscl + uint64_t(tq) * 128;
+#pragma unroll
+    for (int c4 = 0; c4 < 4; ++c4) {
+        float v[32];
+        ptx::tmem_ld32(tmem + ((warp * 32u) << 16) + 32u * c4, v);
+        ptx::tc_wait_ld();
+#pragma unroll
+        for (int pp = 0; pp < 8; ++pp) {
+            const uint32_t pair = tq * 32 + c4 * 8 + pp;
+            if (j < si.size && pair < n_pairs) {
+                const float4 sc = __ldg(reinterpret_cast<const float4*>(sclp) + c4 * 8 + pp);
+                lut[uint64_t(pair) * kentries + e] = make_float4(v[4 * pp] * sc.x, v[4 * pp + 1] * sc.y,
+                                                                 v[4 * pp + 2] * sc.z, v[4 * pp + 3] * sc.w);
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc(tmem, 128);
+}
+
 // Reads 64 bits starting at bit `pos` of a byte stream: two aligned 64-bit
 // loads when they stay inside [.., end), byte loads otherwise (buffer tails).
 __device__ __forceinline__ uint64_t read_bits64(const uint8_t* base, uint64_t pos, const uint8_t* end) {
@@ -725,6 +839,12 @@ __global__ void lut_finish_kernel(const float* __restrict__ acc, const float* __
 
 }  // namespace
 
+// tensor-core LUT build: D = 128 stacks carry the fp16 hi/lo operand chunks
+static bool lut_tc_ok(const vqkv_stack_s& ks) {
+    const char* e = getenv("VQKV_LUT_FFMA");
+    return !(e && e[0] == '1') && ks.dim == kD && ks.d_eff16 && ks.d_eff16lo;
+}
+
 bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a) {
     if (ks.dim != kD || vs.dim != kD || a.group != kG) return false;
     if (a.n_init + a.n_local > kSplitTokens) return false;
@@ -821,6 +941,30 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     VQKV_CUDA(cudaMallocAsync(&pl, sizeof(float) * a.n_pairs * (n_splits + 1) * kG, s));
     {
         ProfScope ps("attend_lut_build", s);
+        if (lut_tc_ok(ks)) {
+            // tensor-core LUT GEMM (VQKV_LUT_FFMA=1 selects the FFMA kernel below)
+            const uint32_t rows = a.n_pairs * kG, rows_pad = (rows + 127) / 128 * 128, qt = rows_pad / 128;
+            __half *qh = nullptr, *ql = nullptr;
+            float* qs = nullptr;
+            VQKV_CUDA(cudaMallocAsync(&qh, sizeof(__half) * rows_pad * kD, s));
+            VQKV_CUDA(cudaMallocAsync(&ql, sizeof(__half) * rows_pad * kD, s));
+            VQKV_CUDA(cudaMallocAsync(&qs, sizeof(float) * rows_pad, s));
+            q_prep_kernel<<<rows_pad / 8, 256, 0, s>>>(a.q_dev, rows, rows_pad, float(scale), qh, ql, qs);
+            launch_check("q_prep_kernel");
+            static bool tattr = false;
+            if (!tattr) {
+                VQKV_CUDA(cudaFuncSetAttribute(lut_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLutTcSmem)));
+                tattr = true;
+            }
+            uint32_t maxch = 0;
+            for (const auto& st : ks.stages) maxch = std::max(maxch, (st.size + 127) / 128);
+            lut_tc_kernel<<<dim3(maxch, ks.n, qt), 128, kLutTcSmem, s>>>(ks.d_eff16, ks.d_eff16lo, ks.d_stages, qh, ql, qs,
+                                                                        a.n_pairs, kent, lut);
+            launch_check("lut_tc_kernel");
+            VQKV_CUDA(cudaFreeAsync(qh, s));
+            VQKV_CUDA(cudaFreeAsync(ql, s));
+            VQKV_CUDA(cudaFreeAsync(qs, s));
+        } else {
         LutArgs la{a.q_dev, ks.d_eff, ks.d_stages, ks.n, kent, float(scale), lut};
         dim3 grid(unsigned((kent + kLutEntries - 1) / kLutEntries), (a.n_pairs + 7) / 8);
         const int lsmem = int(sizeof(float) * (8 * kG * kD + kLutEntries * kLutStride));
@@ -831,6 +975,7 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         }
         lut_kernel<<<grid, 256, lsmem, s>>>(la, a.n_pairs);
         launch_check("lut_kernel");
+        }
     }
     {
         ProfScope ps("attend", s);

@@ -40,7 +40,7 @@ __global__ void sqnorm_kernel(const float* __restrict__ eff, uint32_t D, uint64_
 // fp16 operand copy [pad_S][D] per stage and padded sqnorm (+inf on padding).
 __global__ void half_copy_kernel(const float* __restrict__ eff, const float* __restrict__ sqn,
                                  const StageInfo* __restrict__ stages, uint32_t stage, uint32_t D,
-                                 __half* __restrict__ eff16, float* __restrict__ sqn_pad) {
+                                 __half* __restrict__ eff16, __half* __restrict__ eff16lo, float* __restrict__ sqn_pad) {
     const StageInfo st = stages[stage];
     uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= uint64_t(st.pad_size) * D) return;
@@ -57,7 +57,11 @@ __global__ void half_copy_kernel(const float* __restrict__ eff, const float* __r
     const uint32_t c = j >> 7, rj = j & 127, kb = k >> 6, kk = k & 63;
     __half* chunk = eff16 + st.eff16_off + uint64_t(c) * 18432;
     const uint64_t off = kb * 8192 + rj * 64 + (((kk >> 3) ^ (rj & 7)) << 3) + (kk & 7);
-    chunk[off] = __float2half_rn(v);
+    const __half hi = __float2half_rn(v);
+    chunk[off] = hi;
+    // residual fp16(v - hi) in the same layout: hi + lo carries 22 bits of v (the decode-attention
+    // LUT GEMM's split-precision operand, attend_lut.cu lut_tc_kernel); v - hi is exact in fp32
+    eff16lo[st.eff16_off + uint64_t(c) * 18432 + off] = __float2half_rn(v - __half2float(hi));
     if (k < 16) {
         // ext block: element (rj, k) at (rj/8)*256 B + (k/8)*128 B + (rj%8)*16 B + (k%8)*2 B
         const uint64_t eoff = 16384 + (rj >> 3) * 128 + (k >> 3) * 64 + (rj & 7) * 8 + (k & 7);
@@ -102,11 +106,12 @@ void stack_build_device(vqkv_stack_s& st, const float* entries_host, const float
     }
     if (D == 128) {
         VQKV_CUDA(cudaMalloc(&st.d_eff16, sizeof(__half) * st.total_pad_rows * (D + 16)));
+        VQKV_CUDA(cudaMalloc(&st.d_eff16lo, sizeof(__half) * st.total_pad_rows * (D + 16)));
         VQKV_CUDA(cudaMalloc(&st.d_sqn_pad, sizeof(float) * st.total_pad_rows));
         for (uint32_t s = 0; s < st.n; ++s) {
             uint64_t n = uint64_t(st.stages[s].pad_size) * D;
             half_copy_kernel<<<unsigned((n + 255) / 256), 256>>>(st.d_eff, st.d_sqn, st.d_stages, s, D, st.d_eff16,
-                                                                 st.d_sqn_pad);
+                                                                 st.d_eff16lo, st.d_sqn_pad);
             launch_check("half_copy_kernel");
         }
     }

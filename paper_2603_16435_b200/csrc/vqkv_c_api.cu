@@ -193,6 +193,7 @@ int vqkv_stack_destroy(vqkv_stack_t s) {
         cudaFree(s->d_eff);
         cudaFree(s->d_sqn);
         cudaFree(s->d_eff16);
+        cudaFree(s->d_eff16lo);
         cudaFree(s->d_sqn_pad);
         cudaFree(s->d_error);
         cudaFree(s->d_counters);

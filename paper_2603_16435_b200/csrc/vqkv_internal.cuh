@@ -87,6 +87,7 @@ struct vqkv_stack_s {
     float* d_eff = nullptr;                   // [sum S_i][D] fp32 effective entries
     float* d_sqn = nullptr;                   // [sum S_i]
     __half* d_eff16 = nullptr;                // [sum pad_S_i][D] fp16 operand (D == 128 only)
+    __half* d_eff16lo = nullptr;              // fp16(eff - fp16(eff)), same layout (LUT GEMM operand)
     float* d_sqn_pad = nullptr;               // [sum pad_S_i] sqnorm, +inf on padding rows
     uint64_t total_rows = 0, total_pad_rows = 0;
     int* d_error = nullptr;                   // sticky device error flag

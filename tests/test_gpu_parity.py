@@ -338,3 +338,36 @@ def test_group_major_errors(torch_mod):
         Dv.attend_decode(pk, pv, q, gm, vc, 100, kcodes_gm_cap=96)  # cap < n_comp
     with pytest.raises(InvalidInput):
         Dv.keycodes_to_gm(pk, kc, 100, gm=gm, cap=112, dst_row=20)  # past the capacity
+
+
+@pytest.mark.parametrize("qscale", [1.0, 1e-3, 40.0])
+def test_attention_lut_tensor_core_vs_ffma(torch_mod, monkeypatch, qscale):
+    """The tensor-core LUT GEMM (fp16 hi/lo split, default for D = 128) against the fp32 FFMA
+    LUT kernel (VQKV_LUT_FFMA=1): same attention within fp32-level differences, and both
+    within the stated tolerance of the oracle."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+
+    nk, sk, nv, sv, n_pairs, n_comp = 56, 1024, 16, 512, 37, 3000  # 148 query rows: two row tiles
+    rng = O.Rng(91)
+    ks, vs = rng.stack(nk, sk, 128, O.KEY), rng.stack(nv, sv, 128, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    g = np.random.default_rng(9)
+    kc = np.stack([ks.pack(g.integers(0, sk, (n_comp, nk)).astype(np.uint32)) for _ in range(n_pairs)])
+    vc = np.stack([vs.pack(g.integers(0, sv, (n_comp, nv)).astype(np.uint32)) for _ in range(n_pairs)])
+    q = (rng.matrix(n_pairs * 4, 128) * np.float32(qscale)).reshape(n_pairs, 4, 128)
+    lk, lv = rng.matrix(n_pairs * 8, 128).reshape(n_pairs, 8, 128), rng.matrix(n_pairs * 8, 128).reshape(n_pairs, 8, 128)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    res = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("VQKV_LUT_FFMA", mode)
+        res[mode] = Dv.attend_decode(pk, pv, t(q), t(kc), t(vc), n_comp, None, None, t(lk), t(lv))
+    (o1, l1), (o2, l2) = res["1"], res["0"]
+    assert torch.allclose(l1, l2, rtol=1e-5, atol=1e-5)
+    assert torch.allclose(o1, o2, rtol=1e-4, atol=1e-4 * max(1.0, float(o1.abs().max())))
+    out = o2.cpu().numpy()
+    for pi in (0, n_pairs - 1):
+        for gg in range(4):
+            ref, _ = O.attend_segments(ks, vs, np.zeros((0, 128), np.float32), np.zeros((0, 128), np.float32), kc[pi],
+                                       vc[pi], n_comp, lk[pi], lv[pi], q[pi, gg])
+            assert np.abs(out[pi, gg] - ref).max() <= ATT_TOL * max(1.0, np.abs(ref).max())
