@@ -398,13 +398,20 @@ def run_reference(args, rank, world):
         pass  # the oracle has no warm-up effects; calibration happens inside each step
     cores = 1
     sample = ""
+    walls = []
     for _ in range(args.steps):
+        t_0 = time.perf_counter()
         r, cores, sample = cpu_encode_rate(seconds_target=max(2.0, args.cpu_seconds / 2))
+        walls.append(time.perf_counter() - t_0)
         rates.append(r)
     v = float(np.mean(rates))
+    full = 2 * args.streams * (args.prefill - INIT_LEN - LOCAL_LEN)  # K+V vectors of one full step
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": full / v * 1e3,
+        "ms_per_step_basis": "one full 32K-prefill step (%d K+V vectors) at the measured sample rate; each timed step "
+                             "ran a bounded sample in %.1f s wall" % (full, float(np.mean(walls))),
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generator, seeds 1000+sid)",
         "config": {"workload": "32K-token prefill encode, LLaMA3.1-8B KV shape (bounded CPU sample)",
                    "streams": args.streams, "rows_per_stream": args.prefill - INIT_LEN - LOCAL_LEN,
