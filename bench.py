@@ -355,6 +355,28 @@ def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
                      "algorithmic": "88 B of codes per compressed token-pair + 1 KB per raw row (fp32 K+V)",
                      "note": "on-chip bound: 56 LUT gathers + 16 histogram atomics per token-pair in shared memory"},
     }
+    # the kernel's own bound: shared-memory LUT gathers (main kernel, library profile hooks)
+    L = _lib.load()
+    L.vqkv_profile_enable(1)
+    for nm in (b"attend_lut_build", b"attend", b"attend_combine"):
+        L.vqkv_profile_collect(nm, None, None)
+    for _ in range(max(2, args.steps)):
+        run()
+    torch.cuda.synchronize()
+    part = {}
+    for nm in (b"attend_lut_build", b"attend", b"attend_combine"):
+        t_ms, n_l = ctypes.c_double(), ctypes.c_uint64()
+        L.vqkv_profile_collect(nm, ctypes.byref(t_ms), ctypes.byref(n_l))
+        part[nm.decode()] = t_ms.value / max(1, n_l.value)
+    L.vqkv_profile_enable(0)
+    smem_peak = 128 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12  # TB/s: 128 B/clk/SM at max clock
+    gathers = pairs * n_comp * kst.num_stages() * 16  # one 16 B LUT entry (4 heads) per (token, key stage)
+    out["kernel_ms"] = {"lut_gemm": part["attend_lut_build"], "main": part["attend"], "combine": part["attend_combine"]}
+    out["onchip"] = {"bound": "shared-memory LUT gathers (main kernel)", "algorithmic_bytes": gathers,
+                     "achieved": gathers / (part["attend"] / 1e3) / 1e12, "peak": smem_peak, "unit": "TB/s",
+                     "frac": gathers / (part["attend"] / 1e3) / 1e12 / smem_peak,
+                     "note": "16 B per (compressed token-pair, key stage) at 128 B/clk/SM x 148 SMs x max clock; "
+                             "random LDS.128 gathers also pay ~1.8x bank-conflict wavefronts (profiles/r1_attention_ncu.md)"}
     del kc, vc, ik, iv, lk, lv
     if world > 1:
         # configs[4]: 1M-token single sequence over the ranks, NCCL all-gather + LSE merge
