@@ -152,82 +152,114 @@ __global__ void q_prep_kernel(const float* __restrict__ q, uint32_t n_rows, uint
     if (lane == 0) qscl[r] = (r < n_rows) ? ldexpf(scale, -sig) : 0.f;
 }
 
-// CTA = (128-entry chunk c of key stage s, 128-row tile of (pair, g) query rows), 128 threads:
-// one bulk-copy wave of the four 32 KB operands, 24 MMAs M128 N128 K16 issued by one thread,
-// then thread = entry row = TMEM lane stores its 32 pairs' float4 (coalesced across lanes).
-constexpr uint32_t kLutTcSmem = 4 * 32768 + 1024;
-__global__ void __launch_bounds__(128) lut_tc_kernel(const __half* __restrict__ eff16, const __half* __restrict__ eff16lo,
+// CTA = 128-entry chunk c of key stage s, looping over the 128-row tiles of (pair, g) query
+// rows.  Warp 4 (one thread) loads the chunk's E_hi / E_lo once and double-buffers the Q tiles
+// by bulk copy, and issues 24 MMAs M128 N128 K16 per tile into one of two TMEM accumulators;
+// warps 0-3 (thread = entry row = TMEM lane) drain the other accumulator meanwhile: 32 pairs'
+// float4 per thread and tile, coalesced across lanes.
+constexpr uint32_t kLutTcSmem = 6 * 32768 + 1024;
+__global__ void __launch_bounds__(160) lut_tc_kernel(const __half* __restrict__ eff16, const __half* __restrict__ eff16lo,
                                                      const StageInfo* __restrict__ kst, const __half* __restrict__ qhi,
                                                      const __half* __restrict__ qlo, const float* __restrict__ qscl,
-                                                     uint32_t n_pairs, uint64_t kentries, float4* __restrict__ lut) {
+                                                     uint32_t n_pairs, uint32_t n_qtiles, uint64_t kentries,
+                                                     float4* __restrict__ lut) {
     extern __shared__ uint8_t lsm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(lsm_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar_ld, bar_mma;
+    __shared__ uint64_t bar_e, bar_q[2], bar_mma[2], bar_epi[2];
     __shared__ uint32_t tmem_base;
     const StageInfo si = kst[blockIdx.y];
-    const uint32_t c = blockIdx.x, tq = blockIdx.z;
+    const uint32_t c = blockIdx.x;
     if (c * 128 >= si.size) return;  // uniform per CTA
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        ptx::mbar_init(ptx::smem_u32(&bar_ld), 1);
-        ptx::mbar_init(ptx::smem_u32(&bar_mma), 1);
+        ptx::mbar_init(ptx::smem_u32(&bar_e), 1);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(ptx::smem_u32(&bar_q[b]), 1);
+            ptx::mbar_init(ptx::smem_u32(&bar_mma[b]), 1);
+            ptx::mbar_init(ptx::smem_u32(&bar_epi[b]), 128);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 0) {
-        ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 128);
+        ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 256);
         ptx::tmem_relinquish();
     }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = tmem_base;
-    const uint32_t s_ehi = ptx::smem_u32(sm), s_elo = s_ehi + 32768, s_qhi = s_ehi + 65536, s_qlo = s_ehi + 98304;
-    if (threadIdx.x == 0) {
-        const uint32_t bar = ptx::smem_u32(&bar_ld);
-        ptx::mbar_arrive_expect_tx(bar, 4 * 32768);
-        const uint64_t eo = si.eff16_off + uint64_t(c) * 18432;
-        ptx::bulk_g2s(s_ehi, eff16 + eo, 32768, bar);
-        ptx::bulk_g2s(s_elo, eff16lo + eo, 32768, bar);
-        ptx::bulk_g2s(s_qhi, qhi + uint64_t(tq) * 16384, 32768, bar);
-        ptx::bulk_g2s(s_qlo, qlo + uint64_t(tq) * 16384, 32768, bar);
-        ptx::mbar_wait(bar, 0);
-        ptx::tc_fence_after();
-        constexpr uint32_t idesc = ptx::idesc_f16_f32(128, 128);
-        const uint32_t A[3] = {s_ehi, s_elo, s_ehi}, B[3] = {s_qlo, s_qhi, s_qhi};  // small terms first
+    const uint32_t s_ehi = ptx::smem_u32(sm), s_elo = s_ehi + 32768;
+    auto s_qhi = [&](uint32_t b) { return s_ehi + 65536 + b * 65536; };
+    if (warp == 4) {
+        if (lane == 0) {
+            const uint64_t eo = si.eff16_off + uint64_t(c) * 18432;
+            ptx::mbar_arrive_expect_tx(ptx::smem_u32(&bar_e), 2 * 32768);
+            ptx::bulk_g2s(s_ehi, eff16 + eo, 32768, ptx::smem_u32(&bar_e));
+            ptx::bulk_g2s(s_elo, eff16lo + eo, 32768, ptx::smem_u32(&bar_e));
+            auto load_q = [&](uint32_t tq) {
+                const uint32_t b = tq & 1, bar = ptx::smem_u32(&bar_q[b]);
+                ptx::mbar_arrive_expect_tx(bar, 2 * 32768);
+                ptx::bulk_g2s(s_qhi(b), qhi + uint64_t(tq) * 16384, 32768, bar);
+                ptx::bulk_g2s(s_qhi(b) + 32768, qlo + uint64_t(tq) * 16384, 32768, bar);
+            };
+            load_q(0);
+            if (n_qtiles > 1) load_q(1);
+            ptx::mbar_wait(ptx::smem_u32(&bar_e), 0);
+            constexpr uint32_t idesc = ptx::idesc_f16_f32(128, 128);
+            for (uint32_t tq = 0; tq < n_qtiles; ++tq) {
+                const uint32_t b = tq & 1, use = tq >> 1;
+                ptx::mbar_wait(ptx::smem_u32(&bar_q[b]), use & 1);
+                if (tq >= 2) ptx::mbar_wait(ptx::smem_u32(&bar_epi[b]), (use - 1) & 1);  // accumulator b drained
+                ptx::tc_fence_after();
+                const uint32_t qh = s_qhi(b), ql = qh + 32768;
+                const uint32_t A[3] = {s_ehi, s_elo, s_ehi}, B[3] = {ql, qh, qh};  // small terms first
 #pragma unroll
-        for (int part = 0; part < 3; ++part)
+                for (int part = 0; part < 3; ++part)
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32;
-                ptx::mma_f16_ss(tmem, ptx::umma_desc_sw128(A[part] + koff), ptx::umma_desc_sw128(B[part] + koff), idesc,
-                                (part | k) ? 1u : 0u);
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32;
+                        ptx::mma_f16_ss(tmem + 128u * b, ptx::umma_desc_sw128(A[part] + koff),
+                                        ptx::umma_desc_sw128(B[part] + koff), idesc, (part | k) ? 1u : 0u);
+                    }
+                ptx::mma_commit(ptx::smem_u32(&bar_mma[b]));
+                if (tq + 2 < n_qtiles) {
+                    // Q buffer b is free once these MMAs complete
+                    ptx::mbar_wait(ptx::smem_u32(&bar_mma[b]), use & 1);
+                    load_q(tq + 2);
+                }
             }
-        ptx::mma_commit(ptx::smem_u32(&bar_mma));
-    }
-    __syncwarp();
-    ptx::mbar_wait(ptx::smem_u32(&bar_mma), 0);
-    ptx::tc_fence_after();
-    const uint32_t j = c * 128 + warp * 32 + lane;  // entry within the stage
-    const uint64_t e = si.eff_off / kD + j;
-    const float* sclp = qscl + uint64_t(tq) * 128;
+        }
+    } else {
+        const uint32_t j = c * 128 + warp * 32 + lane;  // entry within the stage
+        const uint64_t e = si.eff_off / kD + j;
+        for (uint32_t tq = 0; tq < n_qtiles; ++tq) {
+            const uint32_t b = tq & 1, use = tq >> 1;
+            ptx::mbar_wait(ptx::smem_u32(&bar_mma[b]), use & 1);
+            ptx::tc_fence_after();
+            const float* sclp = qscl + uint64_t(tq) * 128;
+            float v[4][32];
 #pragma unroll
-    for (int c4 = 0; c4 < 4; ++c4) {
-        float v[32];
-        ptx::tmem_ld32(tmem + ((warp * 32u) << 16) + 32u * c4, v);
-        ptx::tc_wait_ld();
+            for (int c4 = 0; c4 < 4; ++c4) ptx::tmem_ld32(tmem + ((warp * 32u) << 16) + 128u * b + 32u * c4, v[c4]);
+            ptx::tc_wait_ld();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(ptx::smem_u32(&bar_epi[b]));
 #pragma unroll
-        for (int pp = 0; pp < 8; ++pp) {
-            const uint32_t pair = tq * 32 + c4 * 8 + pp;
-            if (j < si.size && pair < n_pairs) {
-                const float4 sc = __ldg(reinterpret_cast<const float4*>(sclp) + c4 * 8 + pp);
-                lut[uint64_t(pair) * kentries + e] = make_float4(v[4 * pp] * sc.x, v[4 * pp + 1] * sc.y,
-                                                                 v[4 * pp + 2] * sc.z, v[4 * pp + 3] * sc.w);
-            }
+            for (int c4 = 0; c4 < 4; ++c4)
+#pragma unroll
+                for (int pp = 0; pp < 8; ++pp) {
+                    const uint32_t pair = tq * 32 + c4 * 8 + pp;
+                    if (j < si.size && pair < n_pairs) {
+                        const float4 sc = __ldg(reinterpret_cast<const float4*>(sclp) + c4 * 8 + pp);
+                        lut[uint64_t(pair) * kentries + e] = (
+                               make_float4(v[c4][4 * pp] * sc.x, v[c4][4 * pp + 1] * sc.y, v[c4][4 * pp + 2] * sc.z,
+                                           v[c4][4 * pp + 3] * sc.w));
+                    }
+                }
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 0) ptx::tmem_dealloc(tmem, 128);
+    if (warp == 0) ptx::tmem_dealloc(tmem, 256);
 }
 
 // Reads 64 bits starting at bit `pos` of a byte stream: two aligned 64-bit
@@ -958,8 +990,8 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
             }
             uint32_t maxch = 0;
             for (const auto& st : ks.stages) maxch = std::max(maxch, (st.size + 127) / 128);
-            lut_tc_kernel<<<dim3(maxch, ks.n, qt), 128, kLutTcSmem, s>>>(ks.d_eff16, ks.d_eff16lo, ks.d_stages, qh, ql, qs,
-                                                                        a.n_pairs, kent, lut);
+            lut_tc_kernel<<<dim3(maxch, ks.n), 160, kLutTcSmem, s>>>(ks.d_eff16, ks.d_eff16lo, ks.d_stages, qh, ql, qs,
+                                                                    a.n_pairs, qt, kent, lut);
             launch_check("lut_tc_kernel");
             VQKV_CUDA(cudaFreeAsync(qh, s));
             VQKV_CUDA(cudaFreeAsync(ql, s));
