@@ -21,7 +21,7 @@ for a, e, s, st in data:
     cur[1] = a; cur[3] += s; cur[5] += 1
     cur[4] = [x + y for x, y in zip(cur[4], st)]
 for a0, a1, e, s, st, n in segs:
-    if s > 0.01 * tot:
+    if s > float(sys.argv[2] if len(sys.argv) > 2 else 0.01) * tot:
         top = sorted(zip(st, [h[i][6:] for i in sc]), reverse=True)[:4]
         print(f"{a0 & 0xfffff:05x}-{a1 & 0xfffff:05x} n={n:4d} exec={e:8d} {100 * s / tot:5.1f}%  " +
               " ".join(f"{k}:{100 * v / max(s, 1):.0f}%" for v, k in top))
