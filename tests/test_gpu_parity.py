@@ -371,3 +371,60 @@ def test_attention_lut_tensor_core_vs_ffma(torch_mod, monkeypatch, qscale):
             ref, _ = O.attend_segments(ks, vs, np.zeros((0, 128), np.float32), np.zeros((0, 128), np.float32), kc[pi],
                                        vc[pi], n_comp, lk[pi], lv[pi], q[pi, gg])
             assert np.abs(out[pi, gg] - ref).max() <= ATT_TOL * max(1.0, np.abs(ref).max())
+
+
+def test_sequence_split_lut_path_matches_monolithic(torch_mod):
+    """configs[4] on one GPU: the 8-rank sequence split of bench.py (sharding.sequence_shards:
+    init rows on shard 0, local window on the last), each shard's (o, lse) from the group-major LUT
+    path, merged by the library's LSE combine == attention over the whole sequence; then the same
+    partials through sharding.gather_and_merge over a world-size-1 NCCL group."""
+    torch = torch_mod
+    import socket
+    import torch.distributed as dist
+    from paper_2603_16435_b200 import device as Dv, sharding
+
+    nk, sk, nv, sv, world = 56, 1024, 16, 512, 8
+    n_init, n_comp, n_local, heads = 4, 20000, 64, 2
+    rng = O.Rng(123)
+    ks, vs = rng.stack(nk, sk, 128, O.KEY), rng.stack(nv, sv, 128, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    g = np.random.default_rng(3)
+    kcodes = [g.integers(0, sk, (n_comp, nk)).astype(np.uint32) for _ in range(heads)]
+    vcodes = [g.integers(0, sv, (n_comp, nv)).astype(np.uint32) for _ in range(heads)]
+    ik, iv = rng.matrix(heads * n_init, 128).reshape(heads, n_init, 128), rng.matrix(heads * n_init, 128).reshape(heads, n_init, 128)
+    lk, lv = rng.matrix(heads * n_local, 128).reshape(heads, n_local, 128), rng.matrix(heads * n_local, 128).reshape(heads, n_local, 128)
+    q = rng.matrix(heads * 4, 128).reshape(heads, 4, 128)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+    def attend(c0, c1, init, local):
+        nc = c1 - c0
+        kc = t(np.stack([ks.pack(kcodes[h][c0:c1]) for h in range(heads)]))
+        vc = t(np.stack([vs.pack(vcodes[h][c0:c1]) for h in range(heads)]))
+        cap = -(-max(nc, 1) // Dv.GM_ALIGN) * Dv.GM_ALIGN
+        kg = Dv.keycodes_to_gm(pk, kc, nc, cap=cap)
+        seg = lambda a, on: t(a) if on else None
+        return Dv.attend_decode(pk, pv, t(q), kg, vc, nc, seg(ik, init), seg(iv, init), seg(lk, local), seg(lv, local),
+                                kcodes_gm_cap=cap)
+
+    full_o, full_l = attend(0, n_comp, True, True)
+    parts = [attend(sh.comp[0], sh.comp[1], sh.init[1] > 0, sh.local[1] > 0)
+             for sh in sharding.sequence_shards(n_init, n_comp, n_local, world)]
+    o_all = torch.stack([p[0].reshape(-1, 128) for p in parts]).contiguous()
+    l_all = torch.stack([p[1].reshape(-1) for p in parts]).contiguous()
+    mo, ml = Dv.lse_combine(o_all, l_all)
+    assert torch.allclose(mo, full_o.reshape(-1, 128), rtol=1e-4, atol=1e-4 * max(1.0, float(full_o.abs().max())))
+    assert torch.allclose(ml, full_l.reshape(-1), rtol=1e-5, atol=1e-5)
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        o1, l1 = sharding.gather_and_merge(parts[3][0], parts[3][1])
+        r1, rl1 = Dv.lse_combine(parts[3][0].reshape(1, -1, 128).contiguous(), parts[3][1].reshape(1, -1).contiguous())
+        assert torch.allclose(o1.reshape(-1, 128), r1, rtol=1e-6, atol=1e-6)
+        assert torch.allclose(l1.reshape(-1), rl1, rtol=1e-6, atol=1e-6)
+    finally:
+        dist.destroy_process_group()
