@@ -874,7 +874,11 @@ __global__ void lut_finish_kernel(const float* __restrict__ acc, const float* __
 // tensor-core LUT build: D = 128 stacks carry the fp16 hi/lo operand chunks
 static bool lut_tc_ok(const vqkv_stack_s& ks) {
     const char* e = getenv("VQKV_LUT_FFMA");
-    return !(e && e[0] == '1') && ks.dim == kD && ks.d_eff16 && ks.d_eff16lo;
+    if ((e && e[0] == '1') || ks.dim != kD || !ks.d_eff16 || !ks.d_eff16lo) return false;
+    // E_hi = fp16(e) must be finite with headroom (the FFMA kernel covers larger entries)
+    for (const auto& st : ks.stages)
+        if (!(st.max_abs < 32768.f)) return false;
+    return true;
 }
 
 bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a) {
