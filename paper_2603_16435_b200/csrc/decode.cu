@@ -38,30 +38,42 @@ reconstruct_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, uint
         float accg[4] = {0.f, 0.f, 0.f, 0.f};  // generic-D path: d = lane + 32*i (D <= 128 per pass)
         bool bad = false;
         for (uint32_t s0 = 0; s0 < n_stages; s0 += 32) {
-            uint32_t my = 0;
+            // lane l decodes stage s0 + l: its code and the element offset of the selected row
+            uint32_t my = 0, my_off = 0;
             const uint32_t sl = s0 + lane;
             if (sl < n_stages) {
                 const StageInfo si = stages[sl];
                 my = read_bits(pay, rbit + si.bit_off, si.bits);
                 if (my >= si.size) bad = true;
+                my_off = uint32_t(si.eff_off + uint64_t(my < si.size ? my : 0u) * D);
             }
             const uint32_t cnt = (n_stages - s0 < 32) ? (n_stages - s0) : 32;
-            for (uint32_t t = 0; t < cnt; ++t) {
-                const uint32_t z = __shfl_sync(0xffffffffu, my, t);
-                const StageInfo si = stages[s0 + t];
-                const uint32_t zz = (z < si.size) ? z : 0;
-                const float* e = eff + si.eff_off + uint64_t(zz) * D;
-                if constexpr (kD128) {
-                    const float4 v = __ldg(reinterpret_cast<const float4*>(e) + lane);
-                    acc.x = __fadd_rn(acc.x, v.x);
-                    acc.y = __fadd_rn(acc.y, v.y);
-                    acc.z = __fadd_rn(acc.z, v.z);
-                    acc.w = __fadd_rn(acc.w, v.w);
-                } else {
+            if constexpr (kD128) {
+                // 8 stage rows in flight per warp, added strictly in stage order
+                for (uint32_t t0 = 0; t0 < cnt; t0 += 8) {
+                    float4 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t off = __shfl_sync(0xffffffffu, my_off, (t0 + u) & 31u);
+                        v[u] = (t0 + u < cnt) ? __ldg(reinterpret_cast<const float4*>(eff + off) + lane)
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (t0 + u < cnt) {
+                            acc.x = __fadd_rn(acc.x, v[u].x);
+                            acc.y = __fadd_rn(acc.y, v[u].y);
+                            acc.z = __fadd_rn(acc.z, v[u].z);
+                            acc.w = __fadd_rn(acc.w, v[u].w);
+                        }
+                }
+            } else {
+                for (uint32_t t = 0; t < cnt; ++t) {
+                    const uint32_t off = __shfl_sync(0xffffffffu, my_off, t);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const uint32_t d = lane + 32u * i;
-                        if (d < D) accg[i] = __fadd_rn(accg[i], __ldg(e + d));
+                        if (d < D) accg[i] = __fadd_rn(accg[i], __ldg(eff + off + d));
                     }
                 }
             }
@@ -119,7 +131,8 @@ void launch_reconstruct(const vqkv_stack_s& st, const uint8_t* payload, uint32_t
     if (total == 0) return;
     const uint64_t sb = stream_stride ? stream_stride : payload_bytes(st.row_bits, rows);
     ProfScope ps("reconstruct", s);
-    if (st.dim <= 128) {
+    // warp-per-row kernel: 32-bit element offsets into the stage-concatenated codebook
+    if (st.dim <= 128 && st.total_rows * st.dim < (1ull << 32)) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st.device);
         uint64_t blocks = (total + kWarpsPerBlock - 1) / kWarpsPerBlock;
