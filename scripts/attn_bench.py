@@ -6,7 +6,8 @@ from paper_2603_16435_b200 import codebook as P, device as Dv
 B, HKV, G, D = 16, 8, 4, 128
 ctx = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 131072
 gm_mode = "--gm" in sys.argv
-n_init, n_local = 4, 1024
+import os
+n_init, n_local = (0, 0) if os.environ.get("NO_RAW") else (4, 1024)
 n_comp = ctx - n_init - n_local
 pairs = B * HKV
 def stack(seed, n, S):
@@ -17,8 +18,8 @@ ks, vs = stack(1, 56, 1024), stack(2, 16, 512)
 kb, vb = ks.device.payload_bytes(n_comp), vs.device.payload_bytes(n_comp)
 kc = torch.randint(0, 256, (pairs, kb), dtype=torch.uint8, device='cuda')
 vc = torch.randint(0, 256, (pairs, vb), dtype=torch.uint8, device='cuda')
-ik, iv = torch.randn(pairs, n_init, D, device='cuda'), torch.randn(pairs, n_init, D, device='cuda')
-lk, lv = torch.randn(pairs, n_local, D, device='cuda'), torch.randn(pairs, n_local, D, device='cuda')
+rnd = lambda n: torch.randn(pairs, n, D, device='cuda') if n else None
+ik, iv, lk, lv = rnd(n_init), rnd(n_init), rnd(n_local), rnd(n_local)
 q = torch.randn(pairs, G, D, device='cuda')
 if gm_mode:  # the cache's attention layout for the key codes (maintained at append time)
     cap = -(-n_comp // 16) * 16
