@@ -428,3 +428,27 @@ def test_sequence_split_lut_path_matches_monolithic(torch_mod):
         assert torch.allclose(l1.reshape(-1), rl1, rtol=1e-6, atol=1e-6)
     finally:
         dist.destroy_process_group()
+
+
+def test_attention_lut_large_entries_fall_back_to_ffma(torch_mod):
+    """Key entries beyond the fp16 range (|e| >= 2^15) take the FFMA LUT build instead of the
+    tensor-core GEMM; the result matches the oracle within the tolerance."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+
+    nk, sk, nv, sv, n_comp = 4, 256, 2, 64, 500
+    g = np.random.default_rng(17)
+    kent = [(g.standard_normal((sk, 128)) * (4e4 if s == 1 else 1.0)).astype(np.float32) for s in range(nk)]
+    vent = [g.standard_normal((sv, 128)).astype(np.float32) for _ in range(nv)]
+    ks, vs = O.Stack.from_entries(kent, kind=O.KEY), O.Stack.from_entries(vent, kind=O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    kc = ks.pack(g.integers(0, sk, (n_comp, nk)).astype(np.uint32))
+    vc = vs.pack(g.integers(0, sv, (n_comp, nv)).astype(np.uint32))
+    q = (g.standard_normal((1, 4, 128)) * 1e-5).astype(np.float32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    out, _ = Dv.attend_decode(pk, pv, t(q), t(kc[None]), t(vc[None]), n_comp)
+    out = out.cpu().numpy()
+    z = np.zeros((0, 128), np.float32)
+    for gg in range(4):
+        ref, _ = O.attend_segments(ks, vs, z, z, kc, vc, n_comp, z, z, q[0, gg])
+        assert np.abs(out[0, gg] - ref).max() <= ATT_TOL * max(1.0, np.abs(ref).max())
