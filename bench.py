@@ -518,7 +518,11 @@ def run_ours(args, rank, world, local):
             Dv.quantize_streams_host(kst, Kh, payload_host=kph, norms_host=knh, blocking=False)
             Dv.quantize_streams_host(vst, Vh, payload_host=vph, norms_host=vnh, blocking=False)
 
-        e2e_step()
+        n_e2e = max(1, min(args.steps, 3))
+        # warm-up as many back-to-back steps as are timed: the stream-ordered staging pool grows
+        # to its steady-state size (mapping memory) before the timed region
+        for _ in range(max(args.warmup, n_e2e)):
+            e2e_step()
         barrier(world)
         torch.cuda.synchronize()
         # the box's pinned H2D bandwidth (the e2e bound when copies exceed the encode time)
@@ -532,7 +536,6 @@ def run_ours(args, rank, world, local):
         del probe
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        n_e2e = max(1, min(args.steps, 3))
         for _ in range(n_e2e):
             e2e_step()
         e1.record()

@@ -248,9 +248,11 @@ int vqkv_encode_phase_clocks(vqkv_stack_t stack, uint64_t* out14);
 uint64_t vqkv_launch_count(void);
 /* Kernel timing hooks: when enabled, the library records a CUDA event pair on
  * the launching stream around each hot kernel (names: "encode_tc",
- * "encode_exact", "pack", "reconstruct", "attend", "attend_combine").
- * vqkv_profile_collect synchronizes on the recorded events, returns the summed
- * milliseconds and launch count for `name`, and forgets them. */
+ * "encode_exact", "pack", "reconstruct", "attend_lut_build", "attend", "attend_combine").
+ * vqkv_profile_collect synchronizes on the recorded events, returns the busy
+ * milliseconds of `name` (the length of the union of its launches' intervals:
+ * the sum for launches on one stream; chunked encodes overlap on two streams)
+ * and its launch count, and forgets them. */
 int vqkv_profile_enable(int on);
 int vqkv_profile_collect(const char* name, double* total_ms, uint64_t* launches);
 

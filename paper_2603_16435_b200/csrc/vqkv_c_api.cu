@@ -59,15 +59,79 @@ void need(bool ok, int code, const char* msg) {
 void check_stack(vqkv_stack_t s) { need(s != nullptr, VQKV_INVALID_INPUT, "null stack"); }
 
 // quantize_batch on device buffers (used by the device and host entry points)
+// Streams per encode launch when a call is split into chunks: 32-160 MiB of input per chunk,
+// picking the size whose tile count best fills whole rounds of the persistent grid (2 tiles
+// per SM).  Consecutive chunks alternate between two compute streams, so the SMs a launch
+// idles in its last round (uneven rescoring work per tile) are taken by the next chunk.
+uint32_t encode_chunk_streams(const vqkv_stack_s& st, uint32_t n_streams, uint64_t rows) {
+    const uint64_t per_stream_in = rows * st.dim * sizeof(float);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st.device);
+    const uint64_t slots = 2ull * uint64_t(sms), tiles_ps = (rows + 127) / 128;
+    const uint64_t lo = std::max<uint64_t>(1, (32ull << 20) / per_stream_in);
+    const uint64_t hi = std::max<uint64_t>(lo, (160ull << 20) / per_stream_in);
+    uint32_t chunk = uint32_t(std::min<uint64_t>(n_streams, lo));
+    double best_waste = 2.0;
+    for (uint64_t c = lo; c <= std::min<uint64_t>(hi, n_streams); ++c) {
+        const uint64_t t = c * tiles_ps, rounds = (t + slots - 1) / slots;
+        const double waste = double(rounds * slots - t) / double(rounds * slots);
+        if (waste < best_waste - 1e-3) {
+            best_waste = waste;
+            chunk = uint32_t(c);
+        }
+    }
+    return chunk;
+}
+
+// the stack's copy and second compute streams, created on first use
+void ensure_streams(vqkv_stack_s& st) {
+    std::lock_guard<std::mutex> lk(st.mu);
+    if (st.cp_in) return;
+    VQKV_CUDA(cudaStreamCreateWithFlags(&st.cp_in, cudaStreamNonBlocking));
+    VQKV_CUDA(cudaStreamCreateWithFlags(&st.cp_out, cudaStreamNonBlocking));
+    VQKV_CUDA(cudaStreamCreateWithFlags(&st.cs_alt, cudaStreamNonBlocking));
+}
+
+// cs_alt starts after everything already queued on s (fork) / s continues after cs_alt (join)
+void fork_alt(vqkv_stack_s& st, cudaStream_t s) {
+    cudaEvent_t e;
+    VQKV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    VQKV_CUDA(cudaEventRecord(e, s));
+    VQKV_CUDA(cudaStreamWaitEvent(st.cs_alt, e, 0));
+    cudaEventDestroy(e);
+}
+void join_alt(vqkv_stack_s& st, cudaStream_t s) {
+    cudaEvent_t e;
+    VQKV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    VQKV_CUDA(cudaEventRecord(e, st.cs_alt));
+    VQKV_CUDA(cudaStreamWaitEvent(s, e, 0));
+    cudaEventDestroy(e);
+}
+
 void quantize_device(vqkv_stack_s& st, const float* xs, uint32_t n_streams, uint64_t rows, uint64_t sb,
-                     uint8_t* payload, float* norms, float* residuals, cudaStream_t s) {
+                     uint8_t* payload, float* norms, float* residuals, cudaStream_t s, bool split = true) {
     const uint64_t total = uint64_t(n_streams) * rows;
     if (total == 0) return;
     const int path = g_encode_path.load();
     const bool tc = encode_tc_supported(st);
     if (path == 2 && !tc) fail(VQKV_UNSUPPORTED, "tensor-core encode path requires D == 128");
     if (tc && path != 1) {
-        launch_encode_tc(st, xs, n_streams, rows, sb, payload, norms, residuals, s);
+        const uint32_t chunk = split ? encode_chunk_streams(st, n_streams, rows) : n_streams;
+        if (chunk >= n_streams) {
+            launch_encode_tc(st, xs, n_streams, rows, sb, payload, norms, residuals, s);
+            return;
+        }
+        ensure_streams(st);
+        fork_alt(st, s);
+        const uint64_t pb = payload_bytes(st.row_bits, rows);
+        uint32_t i = 0;
+        for (uint32_t s0 = 0; s0 < n_streams; s0 += chunk, ++i) {
+            const uint32_t ns = std::min<uint32_t>(chunk, n_streams - s0);
+            launch_encode_tc(st, xs + uint64_t(s0) * rows * st.dim, ns, rows, sb, payload + uint64_t(s0) * pb,
+                             norms + uint64_t(s0) * rows, residuals ? residuals + uint64_t(s0) * rows * st.dim : nullptr,
+                             (i & 1) ? st.cs_alt : s);
+        }
+        join_alt(st, s);
         return;
     }
     uint16_t* codes = nullptr;
@@ -94,22 +158,38 @@ int vqkv_profile_collect(const char* name, double* total_ms, uint64_t* launches)
     return guard([&] {
         need(name != nullptr, VQKV_INVALID_INPUT, "null name");
         std::lock_guard<std::mutex> lk(g_prof_mu);
-        double ms = 0.0;
         uint64_t n = 0;
-        std::vector<ProfRec> keep;
-        for (auto& r : g_prof_recs) {
-            if (r.name == name) {
-                VQKV_CUDA(cudaEventSynchronize(r.b));
-                float t = 0.f;
-                VQKV_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
-                ms += t;
-                ++n;
-                cudaEventDestroy(r.a);
-                cudaEventDestroy(r.b);
+        std::vector<ProfRec> keep, mine;
+        for (auto& r : g_prof_recs) (r.name == name ? mine : keep).push_back(r);
+        // busy time = length of the union of the launches' [start, end] intervals (launches on
+        // two streams overlap; on one stream this is their sum), relative to the first start
+        std::vector<std::pair<double, double>> iv;
+        for (auto& r : mine) {
+            VQKV_CUDA(cudaEventSynchronize(r.b));
+            float t0 = 0.f, t1 = 0.f;
+            VQKV_CUDA(cudaEventElapsedTime(&t0, mine[0].a, r.a));
+            VQKV_CUDA(cudaEventElapsedTime(&t1, mine[0].a, r.b));
+            iv.emplace_back(t0, t1);
+            ++n;
+        }
+        for (auto& r : mine) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        std::sort(iv.begin(), iv.end());
+        double ms = 0.0, lo = 0.0, hi = 0.0;
+        bool open = false;
+        for (const auto& x : iv) {
+            if (open && x.first <= hi) {
+                hi = std::max(hi, x.second);
             } else {
-                keep.push_back(r);
+                if (open) ms += hi - lo;
+                lo = x.first;
+                hi = x.second;
+                open = true;
             }
         }
+        if (open) ms += hi - lo;
         g_prof_recs.swap(keep);
         if (total_ms) *total_ms = ms;
         if (launches) *launches = n;
@@ -199,6 +279,7 @@ int vqkv_stack_destroy(vqkv_stack_t s) {
         cudaFree(s->d_counters);
         if (s->cp_in) cudaStreamDestroy(s->cp_in);
         if (s->cp_out) cudaStreamDestroy(s->cp_out);
+        if (s->cs_alt) cudaStreamDestroy(s->cs_alt);
         delete s;
     });
 }
@@ -346,34 +427,17 @@ int vqkv_quantize_batch_host_async(vqkv_stack_t s, const float* xs, uint32_t n_s
         cudaStream_t cs = as_stream(stream);
         const uint64_t D = s->dim;
         const uint64_t pb = payload_bytes(s->row_bits, rows);
-        // chunk over streams: ~256 MiB of input per chunk, two buffer sets so
-        // the copy engines overlap the encoder (H2D i+1 | encode i | D2H i-1);
-        // staging comes from the stream-ordered pool and nothing blocks the host,
-        // so consecutive calls (e.g. K then V) keep the copy engines busy
-        uint64_t per_stream_in = rows * D * sizeof(float);
-        // chunk = streams per encode launch: 32-160 MiB of input (short pipeline fill), picking the size
-        // whose tile count best fills whole rounds of the persistent grid (2 tiles
-        // per SM), since every launch otherwise idles part of its last round
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
-        const uint64_t slots = 2ull * uint64_t(sms), tiles_ps = (rows + 127) / 128;
-        const uint64_t lo = std::max<uint64_t>(1, (32ull << 20) / per_stream_in);
-        const uint64_t hi = std::max<uint64_t>(lo, (160ull << 20) / per_stream_in);
-        uint32_t chunk = uint32_t(std::min<uint64_t>(n_streams, lo));
-        double best_waste = 2.0;
-        for (uint64_t c = lo; c <= std::min<uint64_t>(hi, n_streams); ++c) {
-            const uint64_t t = c * tiles_ps, rounds = (t + slots - 1) / slots;
-            const double waste = double(rounds * slots - t) / double(rounds * slots);
-            if (waste < best_waste - 1e-3) {
-                best_waste = waste;
-                chunk = uint32_t(c);
-            }
-        }
-        if (!s->cp_in) {
-            VQKV_CUDA(cudaStreamCreateWithFlags(&s->cp_in, cudaStreamNonBlocking));
-            VQKV_CUDA(cudaStreamCreateWithFlags(&s->cp_out, cudaStreamNonBlocking));
-        }
+        // chunk over streams (encode_chunk_streams), staging sets so the copy engines overlap
+        // the encoder (H2D i+1 | encode i | D2H i-1); staging comes from the stream-ordered pool
+        // and nothing blocks the host, so consecutive calls (e.g. K then V) keep the copy engines busy
+        const uint64_t per_stream_in = rows * D * sizeof(float);
+        const uint32_t chunk = encode_chunk_streams(*s, n_streams, rows);
+        ensure_streams(*s);
         cudaStream_t cp_in = s->cp_in, cp_out = s->cp_out;
+        // chunk encodes alternate between the caller's stream and cs_alt: a persistent encode
+        // launch idles SMs in its last round, and the next chunk's CTAs take them over
+        cudaStream_t cst[2] = {cs, s->cs_alt};
+        fork_alt(*s, cs);  // ordered after the caller's earlier work
         // staging sets: at least two (copy | encode overlap); up to ~4 GiB of HBM so a
         // call queued behind another one (values behind keys) prefetches its whole
         // input while the earlier encodes run
@@ -407,9 +471,10 @@ int vqkv_quantize_batch_host_async(vqkv_stack_t s, const float* xs, uint32_t n_s
             VQKV_CUDA(cudaMemcpyAsync(dx[b], xs + uint64_t(s0) * rows * D, per_stream_in * ns, cudaMemcpyHostToDevice,
                                       cp_in));
             VQKV_CUDA(cudaEventRecord(in_ready[b], cp_in));
-            VQKV_CUDA(cudaStreamWaitEvent(cs, in_ready[b], 0));
-            quantize_device(*s, dx[b], ns, rows, sb, dp[b], dn[b], nullptr, cs);
-            VQKV_CUDA(cudaEventRecord(done[b], cs));
+            cudaStream_t ce = cst[i & 1];
+            VQKV_CUDA(cudaStreamWaitEvent(ce, in_ready[b], 0));
+            quantize_device(*s, dx[b], ns, rows, sb, dp[b], dn[b], nullptr, ce, false);
+            VQKV_CUDA(cudaEventRecord(done[b], ce));
             VQKV_CUDA(cudaStreamWaitEvent(cp_out, done[b], 0));
             VQKV_CUDA(cudaMemcpyAsync(payload + uint64_t(s0) * pb, dp[b], pb * ns, cudaMemcpyDeviceToHost, cp_out));
             VQKV_CUDA(cudaMemcpyAsync(norms + uint64_t(s0) * rows, dn[b], sizeof(float) * rows * ns,
@@ -418,7 +483,7 @@ int vqkv_quantize_batch_host_async(vqkv_stack_t s, const float* xs, uint32_t n_s
         }
         // the caller's stream completes only after the last copy-out; staging is
         // returned to the pool in stream order behind it
-        VQKV_CUDA(cudaEventRecord(last, cp_out));
+        VQKV_CUDA(cudaEventRecord(last, cp_out));  // after every chunk's copy-out, hence every encode
         VQKV_CUDA(cudaStreamWaitEvent(cs, last, 0));
         for (uint32_t b = 0; b < nbuf; ++b) {
             VQKV_CUDA(cudaFreeAsync(dx[b], cs));

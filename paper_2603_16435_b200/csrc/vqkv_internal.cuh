@@ -93,6 +93,7 @@ struct vqkv_stack_s {
     int* d_error = nullptr;                   // sticky device error flag
     unsigned long long* d_counters = nullptr; // encode diagnostics [4]
     cudaStream_t cp_in = nullptr, cp_out = nullptr;  // host-buffer pipeline copy streams (lazy)
+    cudaStream_t cs_alt = nullptr;  // second compute stream: consecutive chunk encodes overlap their tails
     std::mutex mu;
 };
 

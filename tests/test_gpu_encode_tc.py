@@ -190,3 +190,24 @@ def test_full_size_round_trip_properties(torch_mod, kind, n, S):
         full_rows = o.unpack(pay[sidx].cpu().numpy(), rows)[:48]
         assert np.array_equal(full_rows, got)
         assert np.array_equal(rec[sidx, :48].cpu().numpy(), o.reconstruct_block(ref_pay, 48, 0, 48))
+
+
+@pytest.mark.parametrize("blocking", [True, False])
+def test_host_buffer_pipeline_matches_device_encode(torch_mod, blocking):
+    """vqkv_quantize_batch_host(_async): chunked H2D / encode / D2H over pinned host buffers,
+    chunk encodes alternating between two compute streams, gives the same payload and norms as
+    the device-resident encode of the same rows."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+
+    rng = O.Rng(5)
+    o = rng.stack(8, 256, 128, O.KEY)
+    p = product_stack(o)
+    streams, rows = 23, 31740  # 16 MB per stream: several chunks of 2-10 streams
+    gen = torch.Generator().manual_seed(3)
+    xh = torch.randn(streams, rows, 128, generator=gen).pin_memory()
+    pay_d, nrm_d = Dv.quantize_streams(p, xh.cuda())
+    pay_h, nrm_h = Dv.quantize_streams_host(p, xh, blocking=blocking)
+    torch.cuda.synchronize()
+    assert torch.equal(pay_h, pay_d.cpu())
+    assert torch.equal(nrm_h.view(torch.int32), nrm_d.cpu().view(torch.int32))
