@@ -240,6 +240,40 @@ void launch_encode_exact_rows(const vqkv_stack_s& st, const float* xs, const uin
     launch_check("encode_exact_kernel(rows)");
 }
 
+namespace {
+// CodeMatrix rows of a device list of global row indices (stream * rows + row), rows a whole number of
+// 16-bit words: one thread per listed row writes its own bytes.
+__global__ void pack_listed_rows_kernel(const uint16_t* __restrict__ codes, const uint32_t* __restrict__ list,
+                                        const uint32_t* __restrict__ n_list, const StageInfo* __restrict__ stages,
+                                        uint32_t n_stages, uint64_t rows, uint64_t stride, uint32_t row_bytes,
+                                        uint8_t* __restrict__ payload) {
+    const uint32_t n = *n_list;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint64_t g = list[k];
+        uint16_t* dst = reinterpret_cast<uint16_t*>(payload + (g / rows) * stride + (g % rows) * row_bytes);
+        uint32_t acc = 0, nb = 0;
+        for (uint32_t s = 0; s < n_stages; ++s) {
+            acc |= uint32_t(codes[g * n_stages + s]) << nb;
+            nb += stages[s].bits;
+            if (nb >= 16) {
+                *dst++ = uint16_t(acc);
+                acc >>= 16;
+                nb -= 16;
+            }
+        }
+    }
+}
+}  // namespace
+
+void launch_pack_listed_rows(const uint16_t* codes, const uint32_t* rows_dev, const uint32_t* n_rows_dev,
+                             uint64_t max_rows, uint64_t rows, uint32_t n_stages, const vqkv_stack_s& st,
+                             uint8_t* payload, cudaStream_t s) {
+    if (max_rows == 0) return;
+    pack_listed_rows_kernel<<<16, 256, 0, s>>>(codes, rows_dev, n_rows_dev, st.d_stages, n_stages, rows,
+                                               payload_bytes(st.row_bits, rows), uint32_t(st.row_bits / 8), payload);
+    launch_check("pack_listed_rows_kernel");
+}
+
 void launch_pack_codes(const uint16_t* codes, uint32_t n_streams, uint64_t rows, uint32_t n_stages,
                        const vqkv_stack_s& st, uint8_t* payload, cudaStream_t s) {
     const uint64_t sb = payload_bytes(st.row_bits, rows);

@@ -42,6 +42,9 @@ namespace vqkv_dev {
 void launch_encode_exact_rows(const vqkv_stack_s& st, const float* xs, const uint32_t* rows_dev,
                               const uint32_t* n_rows_dev, uint64_t max_rows, uint64_t search_block, uint16_t* codes,
                               float* norms, float* residuals, cudaStream_t s);
+void launch_pack_listed_rows(const uint16_t* codes, const uint32_t* rows_dev, const uint32_t* n_rows_dev,
+                             uint64_t max_rows, uint64_t rows, uint32_t n_stages, const vqkv_stack_s& st,
+                             uint8_t* payload, cudaStream_t s);
 
 namespace {
 
@@ -181,7 +184,8 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                  const float* __restrict__ sqn_pad, const float* __restrict__ eff, const float* __restrict__ xs,
                  uint32_t n_streams, uint64_t rows, uint64_t search_block, uint16_t* __restrict__ codes,
                  float* __restrict__ norms, float* __restrict__ residuals, uint32_t* __restrict__ exact_list,
-                 uint32_t* __restrict__ exact_count, unsigned long long* __restrict__ counters, uint32_t dbg) {
+                 uint32_t* __restrict__ exact_count, unsigned long long* __restrict__ counters, uint32_t dbg,
+                 uint8_t* __restrict__ payload, uint64_t pay_stride, uint32_t row_bytes) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* a_tiles = smem;                                  // 2 x 36 KB
@@ -403,6 +407,13 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
             }
             VQKV_PHASE(0)
 
+            // CodeMatrix row written directly (payload != nullptr: row_bits % 16 == 0): the row's
+            // LSB-first bit stream (codebook.cpp:96-120) is assembled stage by stage and stored 16 bits
+            // at a time; otherwise u16 codes go to the scratch for the pack kernel
+            uint32_t pk_acc = 0, pk_n = 0;
+            uint16_t* pk_dst = payload ? reinterpret_cast<uint16_t*>(payload + tl.stream * pay_stride +
+                                                                      (tl.row0 + i) * uint64_t(row_bytes))
+                                       : nullptr;
             for (uint32_t s = 0; s < n_stages; ++s) {
                 const StageInfo& si = (s < kSmemStages) ? ctl->st[s] : stages[s];
                 const bool any_one_s = (s < kSmemStages) ? (si.pad_ != 0.f)
@@ -641,7 +652,18 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         for (int l = 0; l < 4; ++l) ptx::prefetch_l1(ez + 32 * l);
                     }
                 }
-                if (valid && !exact_row) codes[grow * n_stages + s] = uint16_t(z);
+                if (pk_dst) {
+                    pk_acc |= z << pk_n;  // pk_n < 16 before, bits <= 12: no overflow
+                    pk_n += si.bits;
+                    if (pk_n >= 16) {
+                        if (valid && !exact_row) *pk_dst = uint16_t(pk_acc);
+                        ++pk_dst;
+                        pk_acc >>= 16;
+                        pk_n -= 16;
+                    }
+                } else if (valid && !exact_row) {
+                    codes[grow * n_stages + s] = uint16_t(z);
+                }
                 VQKV_PHASE(8)
 
                 // ---- residual update r -= e_z (exact fp32) fused with the next stage's A tile
@@ -775,6 +797,10 @@ void launch_encode_tc(const vqkv_stack_s& st, const float* xs, uint32_t n_stream
     VQKV_CUDA(cudaMallocAsync(&codes, sizeof(uint16_t) * total * st.n, s));
     VQKV_CUDA(cudaMallocAsync(&list, sizeof(uint32_t) * (total + 1), s));
     VQKV_CUDA(cudaMemsetAsync(list, 0, sizeof(uint32_t), s));
+    // direct CodeMatrix stores from the epilogue when rows are whole 16-bit words
+    bool direct = payload && st.row_bits > 0 && st.row_bits % 16 == 0 && (reinterpret_cast<uintptr_t>(payload) & 1) == 0;
+    for (const auto& si : st.stages) direct = direct && si.bits <= 16;
+    const uint64_t pb = payload_bytes(st.row_bits, rows);
     const uint64_t tiles = ((rows + 127) / 128) * n_streams;
     const uint64_t pairs = (tiles + 1) / 2;
     const unsigned grid = unsigned(std::min<uint64_t>(pairs, uint64_t(sms)));
@@ -782,12 +808,16 @@ void launch_encode_tc(const vqkv_stack_s& st, const float* xs, uint32_t n_stream
     ProfScope ps("encode_tc", s);
     encode_tc_kernel<<<grid, kThreads, kSmemBytes, s>>>(st.d_stages, st.n, st.d_eff16, st.d_sqn_pad, st.d_eff, xs,
                                                          n_streams, rows, search_block, codes, norms, residuals,
-                                                         list + 1, list, st.d_counters, dbg_flags());
+                                                         list + 1, list, st.d_counters, dbg_flags(),
+                                                         direct ? payload : nullptr, pb, uint32_t(st.row_bits / 8));
     launch_check("encode_tc_kernel");
     }
     // rows with non-finite input: exact reference semantics
     launch_encode_exact_rows(st, xs, list + 1, list, total, search_block, codes, norms, residuals, s);
-    launch_pack_codes(codes, n_streams, rows, st.n, st, payload, s);
+    if (direct)
+        launch_pack_listed_rows(codes, list + 1, list, total, rows, st.n, st, payload, s);  // the exact rows only
+    else
+        launch_pack_codes(codes, n_streams, rows, st.n, st, payload, s);
     VQKV_CUDA(cudaFreeAsync(list, s));
     VQKV_CUDA(cudaFreeAsync(codes, s));
 }
