@@ -6,6 +6,7 @@
 #include <vector>
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -64,6 +65,10 @@ void check_stack(vqkv_stack_t s) { need(s != nullptr, VQKV_INVALID_INPUT, "null 
 // per SM).  Consecutive chunks alternate between two compute streams, so the SMs a launch
 // idles in its last round (uneven rescoring work per tile) are taken by the next chunk.
 uint32_t encode_chunk_streams(const vqkv_stack_s& st, uint32_t n_streams, uint64_t rows) {
+    if (const char* e = getenv("VQKV_CHUNK_STREAMS")) {  // dev override (A/B timing)
+        const long v = strtol(e, nullptr, 10);
+        if (v > 0) return uint32_t(std::min<long>(v, long(n_streams)));
+    }
     const uint64_t per_stream_in = rows * st.dim * sizeof(float);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st.device);
