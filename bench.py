@@ -408,6 +408,31 @@ def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
             "tokens_per_gpu": sh.tokens, "ms_attention_per_layer_step": kern, "ms_nccl_lse_combine": comb,
             "tokens_per_s": total / ((kern + comb) / 1e3),
         }
+    else:
+        # configs[4] at N = 1: the same 1M-token sequence on this GPU alone (no split, no collective):
+        # the reference point for the N-GPU sequence split above
+        total = 1 << 20
+        nc = total - n_init - n_local
+        (kc, kcap), vc, ik, iv, lk, lv = make(KV_HEADS, nc, n_init, n_local)
+        q1 = torch.randn(KV_HEADS, G, D, device="cuda", generator=torch.Generator(device="cuda").manual_seed(7))
+        one = lambda: Dv.attend_decode(kst, vst, q1, kc, vc, nc, ik, iv, lk, lv, kcodes_gm_cap=kcap)
+        for _ in range(max(1, args.warmup)):
+            one()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(args.steps):
+            one()
+        a1.record()
+        torch.cuda.synchronize()
+        ms1 = a0.elapsed_time(a1) / args.steps
+        b1 = KV_HEADS * (kst.device.payload_bytes(nc) + vst.device.payload_bytes(nc)) + KV_HEADS * (n_init + n_local) * D * 8
+        out["sequence_1M_single_gpu"] = {
+            "config": "configs[4] at N=1: 1 sequence x 1,048,576 tokens, 8 KV heads, G=4, one GPU (no split)",
+            "ms_per_layer_step": ms1, "tokens_per_s": total / (ms1 / 1e3),
+            "hbm_gbs": b1 / (ms1 / 1e3) / 1e9, "hbm_frac": b1 / (ms1 / 1e3) / 1e9 / hbm,
+        }
+        del kc, vc, ik, iv, lk, lv
     return out
 
 
