@@ -89,11 +89,29 @@ uint32_t encode_chunk_streams(const vqkv_stack_s& st, uint32_t n_streams, uint64
 }
 
 // the stack's copy and second compute streams, created on first use
+// The copy streams are shared by every stack on a device, so host-buffer calls queued back to back
+// (values behind keys, then the next step's keys) copy in call order at the link's full bandwidth:
+// per-stack streams let the next call's prefetch halve the bandwidth of the inputs needed first.
+// (Each call stages all of its chunks, so an earlier call's copies never wait on its encodes.)
+struct DevCopyStreams {
+    cudaStream_t in = nullptr, out = nullptr;
+};
+std::mutex g_copy_mu;
+DevCopyStreams g_copy[64];
+
 void ensure_streams(vqkv_stack_s& st) {
     std::lock_guard<std::mutex> lk(st.mu);
     if (st.cp_in) return;
-    VQKV_CUDA(cudaStreamCreateWithFlags(&st.cp_in, cudaStreamNonBlocking));
-    VQKV_CUDA(cudaStreamCreateWithFlags(&st.cp_out, cudaStreamNonBlocking));
+    {
+        std::lock_guard<std::mutex> lk2(g_copy_mu);
+        DevCopyStreams& d = g_copy[st.device & 63];
+        if (!d.in) {
+            VQKV_CUDA(cudaStreamCreateWithFlags(&d.in, cudaStreamNonBlocking));
+            VQKV_CUDA(cudaStreamCreateWithFlags(&d.out, cudaStreamNonBlocking));
+        }
+        st.cp_in = d.in;
+        st.cp_out = d.out;
+    }
     VQKV_CUDA(cudaStreamCreateWithFlags(&st.cs_alt, cudaStreamNonBlocking));
 }
 
@@ -282,8 +300,6 @@ int vqkv_stack_destroy(vqkv_stack_t s) {
         cudaFree(s->d_sqn_pad);
         cudaFree(s->d_error);
         cudaFree(s->d_counters);
-        if (s->cp_in) cudaStreamDestroy(s->cp_in);
-        if (s->cp_out) cudaStreamDestroy(s->cp_out);
         if (s->cs_alt) cudaStreamDestroy(s->cs_alt);
         delete s;
     });
@@ -443,16 +459,15 @@ int vqkv_quantize_batch_host_async(vqkv_stack_t s, const float* xs, uint32_t n_s
         // launch idles SMs in its last round, and the next chunk's CTAs take them over
         cudaStream_t cst[2] = {cs, s->cs_alt};
         fork_alt(*s, cs);  // ordered after the caller's earlier work
-        // staging sets: at least two (copy | encode overlap); up to ~4 GiB of HBM so a
-        // call queued behind another one (values behind keys) prefetches its whole
-        // input while the earlier encodes run
         const uint32_t n_chunks = (n_streams + chunk - 1) / chunk;
         const uint64_t set_bytes = (per_stream_in + pb + sizeof(float) * rows) * chunk;
-        const uint32_t nbuf = std::min<uint32_t>(n_chunks, std::max<uint32_t>(2, uint32_t((4ull << 30) / set_bytes)));
+        // staging for every chunk (up to 16 GiB): the shared copy-in stream then never waits on this
+        // call's encodes, which would hold up the copies of the calls queued behind it
+        const uint32_t nbuf = std::min<uint32_t>(n_chunks, std::max<uint32_t>(2, uint32_t((16ull << 30) / set_bytes)));
         std::vector<float*> dx(nbuf), dn(nbuf);
         std::vector<uint8_t*> dp(nbuf);
         std::vector<cudaEvent_t> in_ready(nbuf), done(nbuf), out_done(nbuf);
-        cudaEvent_t alloc_ev, last;
+        cudaEvent_t last;
         for (uint32_t b = 0; b < nbuf; ++b) {
             // allocated in the copy-in stream's order: the copies of a call queued
             // behind another call's encodes start at once (not after those encodes)
@@ -463,16 +478,14 @@ int vqkv_quantize_batch_host_async(vqkv_stack_t s, const float* xs, uint32_t n_s
             VQKV_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
             VQKV_CUDA(cudaEventCreateWithFlags(&out_done[b], cudaEventDisableTiming));
         }
-        VQKV_CUDA(cudaEventCreateWithFlags(&alloc_ev, cudaEventDisableTiming));
         VQKV_CUDA(cudaEventCreateWithFlags(&last, cudaEventDisableTiming));
-        VQKV_CUDA(cudaEventRecord(alloc_ev, cp_in));  // staging allocated (copy-in stream order)
-        VQKV_CUDA(cudaStreamWaitEvent(cp_out, alloc_ev, 0));
-        for (uint32_t b = 0; b < nbuf; ++b) VQKV_CUDA(cudaEventRecord(out_done[b], cp_out));
         uint32_t i = 0;
         for (uint32_t s0 = 0; s0 < n_streams; s0 += chunk, ++i) {
             const uint32_t b = i % nbuf;
             const uint32_t ns = std::min<uint32_t>(chunk, n_streams - s0);
-            VQKV_CUDA(cudaStreamWaitEvent(cp_in, out_done[b], 0));  // buffer b free again
+            // a buffer's first use follows its allocation on cp_in; a reuse waits for its last copy-out
+            // (never for other calls' copies queued on the shared copy-out stream)
+            if (i >= nbuf) VQKV_CUDA(cudaStreamWaitEvent(cp_in, out_done[b], 0));
             VQKV_CUDA(cudaMemcpyAsync(dx[b], xs + uint64_t(s0) * rows * D, per_stream_in * ns, cudaMemcpyHostToDevice,
                                       cp_in));
             VQKV_CUDA(cudaEventRecord(in_ready[b], cp_in));
@@ -498,7 +511,6 @@ int vqkv_quantize_batch_host_async(vqkv_stack_t s, const float* xs, uint32_t n_s
             cudaEventDestroy(done[b]);
             cudaEventDestroy(out_done[b]);
         }
-        cudaEventDestroy(alloc_ev);
         cudaEventDestroy(last);
     });
 }
