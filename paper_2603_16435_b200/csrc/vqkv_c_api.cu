@@ -59,7 +59,6 @@ void need(bool ok, int code, const char* msg) {
 
 void check_stack(vqkv_stack_t s) { need(s != nullptr, VQKV_INVALID_INPUT, "null stack"); }
 
-// quantize_batch on device buffers (used by the device and host entry points)
 // Streams per encode launch when a call is split into chunks: 32-160 MiB of input per chunk,
 // picking the size whose tile count best fills whole rounds of the persistent grid (2 tiles
 // per SM).  Consecutive chunks alternate between two compute streams, so the SMs a launch
@@ -88,11 +87,11 @@ uint32_t encode_chunk_streams(const vqkv_stack_s& st, uint32_t n_streams, uint64
     return chunk;
 }
 
-// the stack's copy and second compute streams, created on first use
-// The copy streams are shared by every stack on a device, so host-buffer calls queued back to back
-// (values behind keys, then the next step's keys) copy in call order at the link's full bandwidth:
-// per-stack streams let the next call's prefetch halve the bandwidth of the inputs needed first.
-// (Each call stages all of its chunks, so an earlier call's copies never wait on its encodes.)
+// The stack's copy streams and second compute stream, created on first use.  The copy streams are
+// shared by every stack on a device (and live for the process), so host-buffer calls queued back to
+// back (values behind keys, then the next step's keys) copy in call order at the link's full
+// bandwidth: per-stack streams let the next call's prefetch halve the bandwidth of the inputs needed
+// first.  (Each call stages all of its chunks, so an earlier call's copies never wait on its encodes.)
 struct DevCopyStreams {
     cudaStream_t in = nullptr, out = nullptr;
 };
@@ -131,6 +130,8 @@ void join_alt(vqkv_stack_s& st, cudaStream_t s) {
     cudaEventDestroy(e);
 }
 
+// quantize_batch on device buffers (used by the device and host entry points); split = chunk the
+// streams over two compute streams (the host pipeline chunks itself and passes false)
 void quantize_device(vqkv_stack_s& st, const float* xs, uint32_t n_streams, uint64_t rows, uint64_t sb,
                      uint8_t* payload, float* norms, float* residuals, cudaStream_t s, bool split = true) {
     const uint64_t total = uint64_t(n_streams) * rows;
