@@ -211,3 +211,30 @@ def test_host_buffer_pipeline_matches_device_encode(torch_mod, blocking):
     torch.cuda.synchronize()
     assert torch.equal(pay_h, pay_d.cpu())
     assert torch.equal(nrm_h.view(torch.int32), nrm_d.cpu().view(torch.int32))
+
+
+def test_degenerate_sizes(torch_mod):
+    """Empty calls (quantize_batch with no rows, checks only when rows > 0 as codebook.cpp:225-237;
+    reconstruct_block of an empty range) and single-row / single-stream calls through every path."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+
+    rng = O.Rng(8)
+    o = rng.stack(3, 256, 128, O.KEY)
+    p = product_stack(o)
+    pay, nrm = Dv.quantize_streams(p, torch.empty((2, 0, 128), device="cuda"))
+    assert pay.shape == (2, 0) and nrm.shape == (2, 0)
+    pay, nrm = Dv.quantize_streams(p, torch.empty((0, 5, 128), device="cuda"))
+    assert pay.numel() == 0 and nrm.numel() == 0
+    x1 = rng.matrix(1, 128)
+    pay, nrm = Dv.quantize_streams(p, torch.from_numpy(x1).cuda())
+    ref_pay, ref_norm = o.quantize_batch(x1)
+    assert np.array_equal(pay[0].cpu().numpy(), ref_pay)
+    assert np.array_equal(nrm[0].cpu().numpy().view(np.uint32), ref_norm.view(np.uint32))
+    rec = Dv.reconstruct_streams(p, pay, 1, 1, 1)
+    assert rec.shape == (1, 0, 128)
+    rec = Dv.reconstruct_streams(p, pay, 1)
+    assert np.array_equal(rec[0].cpu().numpy(), o.reconstruct_block(ref_pay, 1, 0, 1))
+    # host-buffer path with one row
+    ph, nh = Dv.quantize_streams_host(p, torch.from_numpy(x1).reshape(1, 1, 128).contiguous())
+    assert np.array_equal(ph[0].numpy(), ref_pay)
