@@ -32,16 +32,22 @@ def _helper_lines():
 
 
 def _packed_ops(cubin):
-    out = subprocess.run([_tool("nvdisasm"), "-g", cubin], capture_output=True, text=True, check=True).stdout
-    cur, ops = None, []
+    # -gi: line info with inline call stacks; the innermost frame comes first
+    out = subprocess.run([_tool("nvdisasm"), "-gi", cubin], capture_output=True, text=True, check=True).stdout
+    cur, fresh, ops = None, True, []
     for ln in out.splitlines():
         m = re.search(r'## File "([^"]+)", line (\d+)', ln)
         if m:
-            cur = (os.path.basename(m.group(1)), int(m.group(2)))
+            if fresh:  # the first frame of a group is the innermost one
+                cur = (os.path.basename(m.group(1)), int(m.group(2)))
+                fresh = False
             continue
-        o = re.search(r"\b(FFMA2|FMUL2|FADD2)\b", ln)
+        if ln.strip().startswith("/*"):
+            fresh = True
+        o = re.search(r"\b(FFMA2|FMUL2|FADD2)\s+(R\d+),\s*(R\d+)[^,]*,\s*(R\d+)", ln)
         if o:
-            ops.append((o.group(1), cur))
+            # (op, innermost source line, whether both multiplicands are the same register pair)
+            ops.append((o.group(1), cur, o.group(3) == o.group(4)))
     return ops
 
 
@@ -53,5 +59,11 @@ def test_no_contracted_packed_fma_in_exact_kernels(unit):
         subprocess.run([_tool("cuobjdump"), "-xelf", f"{unit}.sm_100a.cubin", LIB], cwd=d, check=True,
                        capture_output=True)
         ops = _packed_ops(os.path.join(d, f"{unit}.sm_100a.cubin"))
-    bad = [(op, src) for op, src in ops if op == "FFMA2" and src != ("tc_ptx.cuh", lines["fma2"])]
+    ffma2 = [(src, sq) for op, src, sq in ops if op == "FFMA2"]
+    # Every FFMA2 must come from ptx::fma2.  The only intended one in these units is the window
+    # bound's sum of squares (encode_tc.cu, residual update: 4 x 16 unrolled), whose line records
+    # nvdisasm sometimes loses to a neighbouring hoisted instruction; those are accepted only as
+    # squares (both multiplicands one register pair), and the count caps them.
+    bad = [src for src, sq in ffma2 if src != ("tc_ptx.cuh", lines["fma2"]) and not sq]
     assert not bad, f"{len(bad)} FFMA2 not written as ptx::fma2 (contracted mul2+add2?): {bad[:4]}"
+    assert len(ffma2) <= (64 if unit == "encode_tc" else 0), f"{len(ffma2)} FFMA2 in {unit}"
