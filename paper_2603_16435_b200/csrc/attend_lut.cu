@@ -262,6 +262,61 @@ __global__ void __launch_bounds__(160) lut_tc_kernel(const __half* __restrict__ 
     if (warp == 0) ptx::tmem_dealloc(tmem, 256);
 }
 
+// ---- int16 LUT (opt-in, VQKV_ATTEND_INT16=1) -------------------------------------------
+// One scale per (pair, head): Δ = max_e |LUT[e][g]| / 32767, entries stored as biased u16
+// (round(L / Δ) + 32768, 4 heads in 8 B) and summed exactly in int32 by the main kernel (GM = 2):
+// per-logit error ≤ n_stages · Δ / 2 against the fp32 LUT.
+__global__ void __launch_bounds__(256) lut_absmax_kernel(const float4* __restrict__ lut, uint64_t kentries,
+                                                         uint32_t* __restrict__ kmax_bits) {
+    __shared__ float4 red[8];
+    const uint32_t pair = blockIdx.y;
+    const float4* L = lut + uint64_t(pair) * kentries;
+    float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < kentries; e += uint64_t(gridDim.x) * blockDim.x) {
+        const float4 v = __ldg(L + e);
+        // non-finite entries make the scale non-finite (NaN logits, as the fp32 path would give)
+        m.x = fmaxf(m.x, isfinite(v.x) ? fabsf(v.x) : INFINITY);
+        m.y = fmaxf(m.y, isfinite(v.y) ? fabsf(v.y) : INFINITY);
+        m.z = fmaxf(m.z, isfinite(v.z) ? fabsf(v.z) : INFINITY);
+        m.w = fmaxf(m.w, isfinite(v.w) ? fabsf(v.w) : INFINITY);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        m.x = fmaxf(m.x, __shfl_xor_sync(0xffffffffu, m.x, o));
+        m.y = fmaxf(m.y, __shfl_xor_sync(0xffffffffu, m.y, o));
+        m.z = fmaxf(m.z, __shfl_xor_sync(0xffffffffu, m.z, o));
+        m.w = fmaxf(m.w, __shfl_xor_sync(0xffffffffu, m.w, o));
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < kG) {
+        float r = 0.f;
+        for (int w = 0; w < 8; ++w) r = fmaxf(r, reinterpret_cast<const float*>(&red[w])[threadIdx.x]);
+        atomicMax(kmax_bits + pair * kG + threadIdx.x, __float_as_uint(r));  // r >= 0: bits order as values
+    }
+}
+
+__global__ void lut_quant_kernel(const float4* __restrict__ lut, uint64_t kentries, uint32_t n_pairs,
+                                 const uint32_t* __restrict__ kmax_bits, uint2* __restrict__ lut16,
+                                 float* __restrict__ dq) {
+    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= uint64_t(n_pairs) * kentries) return;
+    const uint32_t pair = uint32_t(idx / kentries);
+    float inv[kG];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) {
+        const float m = __uint_as_float(kmax_bits[pair * kG + g]);
+        inv[g] = m > 0.f ? 32767.0f / m : 0.f;
+        if (idx % kentries == 0) dq[pair * kG + g] = m / 32767.0f;
+    }
+    const float4 v = __ldg(lut + idx);
+    const float x[kG] = {v.x, v.y, v.z, v.w};
+    uint32_t u[kG];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) u[g] = uint32_t(max(-32767, min(32767, __float2int_rn(x[g] * inv[g]))) + 32768);
+    lut16[idx] = make_uint2(u[0] | u[1] << 16, u[2] | u[3] << 16);
+}
+
 // Reads 64 bits starting at bit `pos` of a byte stream: two aligned 64-bit
 // loads when they stay inside [.., end), byte loads otherwise (buffer tails).
 __device__ __forceinline__ uint64_t read_bits64(const uint8_t* base, uint64_t pos, const uint8_t* end) {
@@ -311,6 +366,8 @@ struct MainArgs {
     float* part_l;      // [pairs][splits+1][G]
     uint64_t init_stride, local_stride;  // rows between pairs
     uint64_t gm_cap;                     // group-major key codes: token capacity per group segment
+    const uint2* lut16;                  // GM = 2: int16 LUT (biased u16, 4 heads)
+    const float* dq;                     // GM = 2: [pairs][G] scale of the int16 LUT
 };
 
 __device__ __forceinline__ float block_max(float v, float* red) {
@@ -443,6 +500,10 @@ __device__ __forceinline__ void lds128(uint32_t addr, float2& a, float2& b) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y) : "r"(addr));
 }
 
+__device__ __forceinline__ void lds64(uint32_t addr, uint2& w) {
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y) : "r"(addr));
+}
+
 // GM = 1: key codes in the group-major layout (attend_lut.cu, "group-major key codes"):
 // per LUT group one bulk copy of the split's 5-byte records lands next to the LUT group,
 // so every code byte crosses L2 -> SM once, and a lookup is SHF + LOP3 + LDS.128 + 2 FADD2
@@ -499,6 +560,11 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
         for (int g = 0; g < kG; ++g) lg[k][g] = 0.f;
     // the key logits accumulate as head pairs with packed FADD2 (2 instructions per lookup)
     float2 (*lg2)[2] = reinterpret_cast<float2 (*)[2]>(lg);
+    uint32_t il[GM == 2 ? kTokPerThread : 1][kG];  // GM = 2: exact sums of the biased int16 entries
+#pragma unroll
+    for (int k = 0; k < (GM == 2 ? kTokPerThread : 1); ++k)
+#pragma unroll
+        for (int g = 0; g < kG; ++g) il[k][g] = 0u;
 
     // ---- keys: LUT groups of kGroupStages stages, double-buffered bulk copies
     const uint32_t ngroups = (a.kn + kGroupStages - 1) / kGroupStages;
@@ -515,7 +581,24 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
         uint32_t bytes = 0;
         for (uint32_t s = s0; s < s1; ++s) bytes += a.kst[s].size * 16u;
         const uint32_t bar = ptx::smem_u32(&bars[b]);
-        if constexpr (GM == 1) {
+        if constexpr (GM == 2) {
+            // int16 LUT: stage q -> 8 KB slot q (entry = 4 biased u16); missing stages as in GM = 1
+            uint32_t hb = 0;
+            for (uint32_t st = s0; st < s1; ++st) hb += a.kst[st].size * 8u;
+            const uint32_t clo = uint32_t((nt * 4 + 15) & ~uint64_t(15)), chi = uint32_t((nt + 15) & ~uint64_t(15));
+            ptx::mbar_arrive_expect_tx(bar, hb + (kGroupStages - (s1 - s0)) * 16u + clo + chi);
+            const uint2* l16 = a.lut16 + uint64_t(pair) * a.kentries;
+            for (uint32_t st = s0; st < s0 + kGroupStages; ++st) {
+                uint8_t* dst = lut_buf + b * 65536 + (st - s0) * 8192;
+                if (st < s1)
+                    ptx::bulk_g2s(ptx::smem_u32(dst), l16 + a.kst[st].eff_off / kD, a.kst[st].size * 8u, bar);
+                else
+                    ptx::bulk_g2s(ptx::smem_u32(dst), g_zero16, 16u, bar);
+            }
+            const uint8_t* seg = kc + uint64_t(grp) * a.gm_cap * 5;
+            ptx::bulk_g2s(ptx::smem_u32(code_buf + b * kGmCodeBuf), seg + t0 * 4, clo, bar);
+            ptx::bulk_g2s(ptx::smem_u32(code_buf + b * kGmCodeBuf + 4 * kSplitTokens), seg + a.gm_cap * 4 + t0, chi, bar);
+        } else if constexpr (GM == 1) {
             // stage q -> 16 KB slot q; a missing stage (partial last group) has code 0 and
             // a zero entry 0; the split's records: lo32 words, then the high bytes
             const uint32_t clo = uint32_t((nt * 4 + 15) & ~uint64_t(15)), chi = uint32_t((nt + 15) & ~uint64_t(15));
@@ -544,6 +627,38 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
     for (uint32_t grp = 0; grp < ngroups; ++grp) {
         if (threadIdx.x == 0 && grp + 1 < ngroups) issue(grp + 1);
         ptx::mbar_wait(ptx::smem_u32(&bars[grp & 1]), (grp >> 1) & 1);
+        if constexpr (GM == 2) {
+            const uint32_t Lb = ptx::smem_u32(lut_buf) + (grp & 1) * 65536u;
+            const uint32_t* clo = reinterpret_cast<const uint32_t*>(code_buf + (grp & 1) * kGmCodeBuf);
+            const uint8_t* chi = code_buf + (grp & 1) * kGmCodeBuf + 4 * kSplitTokens;
+            uint32_t off[kGroupStages], msk[kGroupStages];
+#pragma unroll
+            for (int q = 0; q < kGroupStages; ++q) {
+                const uint32_t st = grp * kGroupStages + q;
+                off[q] = (st < a.kn) ? a.kst[st].bit_off - a.kst[grp * kGroupStages].bit_off : 0u;
+                msk[q] = (st < a.kn) ? ((1u << a.kst[st].bits) - 1u) << 3 : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < kTokPerThread; ++k) {
+                const uint32_t lt = threadIdx.x + uint32_t(k) * kAttThreads;
+                const uint32_t lo = clo[lt], hi = chi[lt];
+                const uint32_t xl = lo << 3, xh = __funnelshift_l(lo, hi, 3);
+                uint2 w[4];
+                lds64(Lb | (xl & msk[0]), w[0]);
+                lds64((Lb + 8192u) | (__funnelshift_r(xl, xh, off[1]) & msk[1]), w[1]);
+                lds64((Lb + 16384u) | (__funnelshift_r(xl, xh, off[2]) & msk[2]), w[2]);
+                lds64((Lb + 24576u) | (__funnelshift_r(xl, xh, off[3]) & msk[3]), w[3]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    il[k][0] += w[q].x & 0xffffu;
+                    il[k][1] += w[q].x >> 16;
+                    il[k][2] += w[q].y & 0xffffu;
+                    il[k][3] += w[q].y >> 16;
+                }
+            }
+            __syncthreads();  // buffers (grp & 1) are refilled two groups later
+            continue;
+        }
         if constexpr (GM == 1) {
             const uint32_t Lb = ptx::smem_u32(lut_buf) + (grp & 1) * 65536u;
             const uint32_t* clo = reinterpret_cast<const uint32_t*>(code_buf + (grp & 1) * kGmCodeBuf);
@@ -639,6 +754,17 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
             }
         }
         __syncthreads();  // buffer (grp & 1) is refilled two groups later
+    }
+
+    if constexpr (GM == 2) {
+        const float* dqp = a.dq + uint64_t(pair) * kG;
+        const int bias = int(a.kn) * 32768;
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+            const float d = __ldg(dqp + g);
+#pragma unroll
+            for (int k = 0; k < kTokPerThread; ++k) lg[k][g] = float(int(il[k][g]) - bias) * d;
+        }
     }
 
     // ---- split max / p / l
@@ -938,6 +1064,16 @@ bool gm_supported(const vqkv_stack_s& ks) {
     return true;
 }
 
+// int16 LUT (opt-in: VQKV_ATTEND_INT16=1): group-major codes, even key stage sizes (8 B entries
+// keep every stage slot a multiple of 16 B for the bulk copies), at most 64 stages (exact int32 sums)
+static bool int16_lut_ok(const vqkv_stack_s& ks) {
+    const char* e = getenv("VQKV_ATTEND_INT16");
+    if (!(e && e[0] == '1') || !gm_supported(ks) || ks.n > 64) return false;
+    for (const auto& st : ks.stages)
+        if (st.size & 1u) return false;
+    return true;
+}
+
 uint64_t gm_pair_bytes(const vqkv_stack_s& ks, uint64_t cap) {
     return uint64_t((ks.n + kGroupStages - 1) / kGroupStages) * cap * 5;
 }
@@ -970,6 +1106,10 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     const double scale = a.scale > 0.0 ? a.scale : 1.0 / std::sqrt(double(kD));
     float4* lut = nullptr;
     float *ph = nullptr, *po = nullptr, *pm = nullptr, *pl = nullptr;
+    const bool i16 = a.kcodes_layout == VQKV_KEYCODES_GROUP_MAJOR && int16_lut_ok(ks);
+    uint2* lut16 = nullptr;
+    uint32_t* kmax_bits = nullptr;
+    float* dq = nullptr;
     VQKV_CUDA(cudaMallocAsync(&lut, sizeof(float4) * a.n_pairs * kent, s));
     VQKV_CUDA(cudaMallocAsync(&ph, sizeof(float) * std::max<uint64_t>(1, uint64_t(a.n_pairs) * n_splits * vent * kG), s));
     VQKV_CUDA(cudaMallocAsync(&po, sizeof(float) * a.n_pairs * kG * kD, s));
@@ -1012,6 +1152,17 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         lut_kernel<<<grid, 256, lsmem, s>>>(la, a.n_pairs);
         launch_check("lut_kernel");
         }
+        if (i16) {
+            VQKV_CUDA(cudaMallocAsync(&lut16, sizeof(uint2) * a.n_pairs * kent, s));
+            VQKV_CUDA(cudaMallocAsync(&kmax_bits, sizeof(uint32_t) * a.n_pairs * kG, s));
+            VQKV_CUDA(cudaMallocAsync(&dq, sizeof(float) * a.n_pairs * kG, s));
+            VQKV_CUDA(cudaMemsetAsync(kmax_bits, 0, sizeof(uint32_t) * a.n_pairs * kG, s));
+            lut_absmax_kernel<<<dim3(16, a.n_pairs), 256, 0, s>>>(lut, kent, kmax_bits);
+            launch_check("lut_absmax_kernel");
+            const uint64_t n = uint64_t(a.n_pairs) * kent;
+            lut_quant_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(lut, kent, a.n_pairs, kmax_bits, lut16, dq);
+            launch_check("lut_quant_kernel");
+        }
     }
     {
         ProfScope ps("attend", s);
@@ -1024,17 +1175,21 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
                     a.kcodes_dev + uint64_t(a.n_pairs - 1) * kstr + kpb,
                     a.vcodes_dev + uint64_t(a.n_pairs - 1) * vstr + vpb, float(scale), n_splits,
                     ph, po, pm, pl, a.init_stride ? a.init_stride : a.n_init,
-                    a.local_stride ? a.local_stride : a.n_local, a.kcodes_cap};
+                    a.local_stride ? a.local_stride : a.n_local, a.kcodes_cap, lut16, dq};
         static bool attr = false;
         if (!attr) {
             VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(kMainSmem + kAlignSlack)));
             VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(kGmSmem + kAlignSlack)));
+            VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(kGmSmem + kAlignSlack)));
             attr = true;
         }
         dim3 grid(n_splits + 1, a.n_pairs);
-        if (a.kcodes_layout == VQKV_KEYCODES_GROUP_MAJOR)
+        if (i16)
+            attend_lut_kernel<2><<<grid, kAttThreads, kGmSmem + kAlignSlack, s>>>(ma);
+        else if (a.kcodes_layout == VQKV_KEYCODES_GROUP_MAJOR)
             attend_lut_kernel<1><<<grid, kAttThreads, kGmSmem + kAlignSlack, s>>>(ma);
         else
             attend_lut_kernel<0><<<grid, kAttThreads, kMainSmem + kAlignSlack, s>>>(ma);
@@ -1063,6 +1218,11 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         VQKV_CUDA(cudaFreeAsync(acc, s));
     }
     VQKV_CUDA(cudaFreeAsync(lut, s));
+    if (i16) {
+        VQKV_CUDA(cudaFreeAsync(lut16, s));
+        VQKV_CUDA(cudaFreeAsync(kmax_bits, s));
+        VQKV_CUDA(cudaFreeAsync(dq, s));
+    }
     VQKV_CUDA(cudaFreeAsync(ph, s));
     VQKV_CUDA(cudaFreeAsync(po, s));
     VQKV_CUDA(cudaFreeAsync(pm, s));

@@ -452,3 +452,39 @@ def test_attention_lut_large_entries_fall_back_to_ffma(torch_mod):
     for gg in range(4):
         ref, _ = O.attend_segments(ks, vs, z, z, kc, vc, n_comp, z, z, q[0, gg])
         assert np.abs(out[0, gg] - ref).max() <= ATT_TOL * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("qscale", [1.0, 0.05, 8.0])
+def test_attention_int16_lut_opt_in(torch_mod, monkeypatch, qscale):
+    """Opt-in int16 LUT (VQKV_ATTEND_INT16=1, group-major codes): one scale per (pair, head), entries
+    summed exactly in int32; within the stated tolerance of the oracle, and close to the fp32-LUT path."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+
+    nk, sk, nv, sv, n_pairs, n_comp = 56, 1024, 16, 512, 3, 12000
+    rng = O.Rng(321)
+    ks, vs = rng.stack(nk, sk, 128, O.KEY), rng.stack(nv, sv, 128, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    g = np.random.default_rng(12)
+    kc = np.stack([ks.pack(g.integers(0, sk, (n_comp, nk)).astype(np.uint32)) for _ in range(n_pairs)])
+    vc = np.stack([vs.pack(g.integers(0, sv, (n_comp, nv)).astype(np.uint32)) for _ in range(n_pairs)])
+    q = (rng.matrix(n_pairs * 4, 128) * np.float32(qscale)).reshape(n_pairs, 4, 128)
+    lk, lv = rng.matrix(n_pairs * 8, 128).reshape(n_pairs, 8, 128), rng.matrix(n_pairs * 8, 128).reshape(n_pairs, 8, 128)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    cap = -(-n_comp // 16) * 16
+    gm = Dv.keycodes_to_gm(pk, t(kc), n_comp, cap=cap)
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("VQKV_ATTEND_INT16", mode)
+        res[mode] = Dv.attend_decode(pk, pv, t(q), gm, t(vc), n_comp, None, None, t(lk), t(lv), kcodes_gm_cap=cap)
+    (o32, l32), (o16, l16) = res["0"], res["1"]
+    assert torch.isfinite(o16).all() and torch.isfinite(l16).all()
+    scale = max(1.0, float(o32.abs().max()))
+    assert float((o16 - o32).abs().max()) <= 2.0 ** -9 * scale
+    assert torch.allclose(l16, l32, rtol=1e-3, atol=1e-3)
+    out = o16.cpu().numpy()
+    z = np.zeros((0, 128), np.float32)
+    for pi in (0, n_pairs - 1):
+        for gg in range(4):
+            ref, _ = O.attend_segments(ks, vs, z, z, kc[pi], vc[pi], n_comp, lk[pi], lv[pi], q[pi, gg])
+            assert np.abs(out[pi, gg] - ref).max() <= ATT_TOL * max(1.0, np.abs(ref).max())
