@@ -377,6 +377,32 @@ def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
                      "frac": gathers / (part["attend"] / 1e3) / 1e12 / smem_peak,
                      "note": "16 B per (compressed token-pair, key stage) at 128 B/clk/SM x 148 SMs x max clock; "
                              "random LDS.128 gathers also pay ~1.8x bank-conflict wavefronts (profiles/r1_attention_ncu.md)"}
+    # opt-in int16 LUT (VQKV_ATTEND_INT16=1) on the same inputs: time and deviation from the fp32 LUT
+    o32, _ = run()
+    os.environ["VQKV_ATTEND_INT16"] = "1"
+    try:
+        for _ in range(max(1, args.warmup)):
+            run()
+        torch.cuda.synchronize()
+        i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        i0.record()
+        for _ in range(args.steps):
+            run()
+        i1.record()
+        torch.cuda.synchronize()
+        ms16 = max_over_ranks(i0.elapsed_time(i1) / args.steps, world)
+        o16, _ = run()
+        torch.cuda.synchronize()
+        dev = float((o16 - o32).abs().amax(dim=-1).div(o32.abs().amax(dim=-1).clamp(min=1.0)).max())
+    finally:
+        os.environ.pop("VQKV_ATTEND_INT16", None)
+    out["int16_lut_opt_in"] = {
+        "ms_per_layer_step": ms16, "value": B * ctx / (ms16 / 1e3),
+        "hbm_frac": bytes_rank / (ms16 / 1e3) / 1e9 / hbm,
+        "max_dev_vs_fp32_lut": dev,
+        "note": "VQKV_ATTEND_INT16=1: int16 LUT, one scale per (pair, head), exact int32 sums; deviation = "
+                "max over rows of max|o16 - o32| / max(1, max|o32|) (tolerance vs the reference: 2^-7)",
+    }
     del kc, vc, ik, iv, lk, lv
     if world > 1:
         # configs[4]: 1M-token single sequence over the ranks, NCCL all-gather + LSE merge
