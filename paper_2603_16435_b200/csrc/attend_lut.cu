@@ -266,55 +266,65 @@ __global__ void __launch_bounds__(160) lut_tc_kernel(const __half* __restrict__ 
 // One scale per (pair, head): Δ = max_e |LUT[e][g]| / 32767, entries stored as biased u16
 // (round(L / Δ) + 32768, 4 heads in 8 B) and summed exactly in int32 by the main kernel (GM = 2):
 // per-logit error ≤ n_stages · Δ / 2 against the fp32 LUT.
-__global__ void __launch_bounds__(256) lut_absmax_kernel(const float4* __restrict__ lut, uint64_t kentries,
-                                                         uint32_t* __restrict__ kmax_bits) {
-    __shared__ float4 red[8];
-    const uint32_t pair = blockIdx.y;
+// CTA = pair: max_e |LUT[e][g]| over the pair's fp32 LUT, then the quantised copy (the second
+// read of the pair's 0.9 MB hits L2).
+__global__ void __launch_bounds__(1024) lut_int16_kernel(const float4* __restrict__ lut, uint64_t kentries,
+                                                         uint2* __restrict__ lut16, float* __restrict__ dq) {
+    __shared__ float red[32][kG];
+    __shared__ float smax[kG];
+    const uint32_t pair = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float4* L = lut + uint64_t(pair) * kentries;
-    float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < kentries; e += uint64_t(gridDim.x) * blockDim.x) {
-        const float4 v = __ldg(L + e);
-        // non-finite entries make the scale non-finite (NaN logits, as the fp32 path would give)
-        m.x = fmaxf(m.x, isfinite(v.x) ? fabsf(v.x) : INFINITY);
-        m.y = fmaxf(m.y, isfinite(v.y) ? fabsf(v.y) : INFINITY);
-        m.z = fmaxf(m.z, isfinite(v.z) ? fabsf(v.z) : INFINITY);
-        m.w = fmaxf(m.w, isfinite(v.w) ? fabsf(v.w) : INFINITY);
+    constexpr int kU = 8;  // loads in flight per thread
+    float m[kG] = {0.f, 0.f, 0.f, 0.f};
+    for (uint64_t e0 = threadIdx.x; e0 < kentries; e0 += uint64_t(kU) * blockDim.x) {
+        float4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t e = e0 + uint64_t(u) * blockDim.x;
+            v[u] = e < kentries ? __ldg(L + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const float x[kG] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int g = 0; g < kG; ++g) m[g] = fmaxf(m[g], isfinite(x[g]) ? fabsf(x[g]) : INFINITY);  // non-finite -> NaN logits
+        }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        m.x = fmaxf(m.x, __shfl_xor_sync(0xffffffffu, m.x, o));
-        m.y = fmaxf(m.y, __shfl_xor_sync(0xffffffffu, m.y, o));
-        m.z = fmaxf(m.z, __shfl_xor_sync(0xffffffffu, m.z, o));
-        m.w = fmaxf(m.w, __shfl_xor_sync(0xffffffffu, m.w, o));
+    for (int g = 0; g < kG; ++g) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m[g] = fmaxf(m[g], __shfl_xor_sync(0xffffffffu, m[g], o));
+        if (lane == 0) red[warp][g] = m[g];
     }
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
     __syncthreads();
     if (threadIdx.x < kG) {
         float r = 0.f;
-        for (int w = 0; w < 8; ++w) r = fmaxf(r, reinterpret_cast<const float*>(&red[w])[threadIdx.x]);
-        atomicMax(kmax_bits + pair * kG + threadIdx.x, __float_as_uint(r));  // r >= 0: bits order as values
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) r = fmaxf(r, red[w][threadIdx.x]);
+        smax[threadIdx.x] = r;
+        dq[pair * kG + threadIdx.x] = r / 32767.0f;
     }
-}
-
-__global__ void lut_quant_kernel(const float4* __restrict__ lut, uint64_t kentries, uint32_t n_pairs,
-                                 const uint32_t* __restrict__ kmax_bits, uint2* __restrict__ lut16,
-                                 float* __restrict__ dq) {
-    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= uint64_t(n_pairs) * kentries) return;
-    const uint32_t pair = uint32_t(idx / kentries);
+    __syncthreads();
     float inv[kG];
 #pragma unroll
-    for (int g = 0; g < kG; ++g) {
-        const float m = __uint_as_float(kmax_bits[pair * kG + g]);
-        inv[g] = m > 0.f ? 32767.0f / m : 0.f;
-        if (idx % kentries == 0) dq[pair * kG + g] = m / 32767.0f;
-    }
-    const float4 v = __ldg(lut + idx);
-    const float x[kG] = {v.x, v.y, v.z, v.w};
-    uint32_t u[kG];
+    for (int g = 0; g < kG; ++g) inv[g] = smax[g] > 0.f ? 32767.0f / smax[g] : 0.f;
+    uint2* Q = lut16 + uint64_t(pair) * kentries;
+    for (uint64_t e0 = threadIdx.x; e0 < kentries; e0 += uint64_t(kU) * blockDim.x) {
+        float4 v[kU];
 #pragma unroll
-    for (int g = 0; g < kG; ++g) u[g] = uint32_t(max(-32767, min(32767, __float2int_rn(x[g] * inv[g]))) + 32768);
-    lut16[idx] = make_uint2(u[0] | u[1] << 16, u[2] | u[3] << 16);
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t e = e0 + uint64_t(u) * blockDim.x;
+            v[u] = e < kentries ? __ldg(L + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t e = e0 + uint64_t(u) * blockDim.x;
+            const float x[kG] = {v[u].x, v[u].y, v[u].z, v[u].w};
+            uint32_t q[kG];
+#pragma unroll
+            for (int g = 0; g < kG; ++g) q[g] = uint32_t(max(-32767, min(32767, __float2int_rn(x[g] * inv[g]))) + 32768);
+            if (e < kentries) Q[e] = make_uint2(q[0] | q[1] << 16, q[2] | q[3] << 16);
+        }
+    }
 }
 
 // Reads 64 bits starting at bit `pos` of a byte stream: two aligned 64-bit
@@ -1108,7 +1118,6 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     float *ph = nullptr, *po = nullptr, *pm = nullptr, *pl = nullptr;
     const bool i16 = a.kcodes_layout == VQKV_KEYCODES_GROUP_MAJOR && int16_lut_ok(ks);
     uint2* lut16 = nullptr;
-    uint32_t* kmax_bits = nullptr;
     float* dq = nullptr;
     VQKV_CUDA(cudaMallocAsync(&lut, sizeof(float4) * a.n_pairs * kent, s));
     VQKV_CUDA(cudaMallocAsync(&ph, sizeof(float) * std::max<uint64_t>(1, uint64_t(a.n_pairs) * n_splits * vent * kG), s));
@@ -1154,14 +1163,9 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         }
         if (i16) {
             VQKV_CUDA(cudaMallocAsync(&lut16, sizeof(uint2) * a.n_pairs * kent, s));
-            VQKV_CUDA(cudaMallocAsync(&kmax_bits, sizeof(uint32_t) * a.n_pairs * kG, s));
             VQKV_CUDA(cudaMallocAsync(&dq, sizeof(float) * a.n_pairs * kG, s));
-            VQKV_CUDA(cudaMemsetAsync(kmax_bits, 0, sizeof(uint32_t) * a.n_pairs * kG, s));
-            lut_absmax_kernel<<<dim3(16, a.n_pairs), 256, 0, s>>>(lut, kent, kmax_bits);
-            launch_check("lut_absmax_kernel");
-            const uint64_t n = uint64_t(a.n_pairs) * kent;
-            lut_quant_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(lut, kent, a.n_pairs, kmax_bits, lut16, dq);
-            launch_check("lut_quant_kernel");
+            lut_int16_kernel<<<a.n_pairs, 1024, 0, s>>>(lut, kent, lut16, dq);
+            launch_check("lut_int16_kernel");
         }
     }
     {
@@ -1220,7 +1224,6 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     VQKV_CUDA(cudaFreeAsync(lut, s));
     if (i16) {
         VQKV_CUDA(cudaFreeAsync(lut16, s));
-        VQKV_CUDA(cudaFreeAsync(kmax_bits, s));
         VQKV_CUDA(cudaFreeAsync(dq, s));
     }
     VQKV_CUDA(cudaFreeAsync(ph, s));
