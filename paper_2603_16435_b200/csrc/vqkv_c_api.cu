@@ -302,6 +302,10 @@ int vqkv_stack_destroy(vqkv_stack_t s) {
         cudaFree(s->d_error);
         cudaFree(s->d_counters);
         if (s->cs_alt) cudaStreamDestroy(s->cs_alt);
+        for (auto& a : s->staging) {
+            if (a.done) cudaEventSynchronize(a.done), cudaEventDestroy(a.done);
+            if (a.base) cudaFree(a.base);
+        }
         delete s;
     });
 }
@@ -462,19 +466,38 @@ int vqkv_quantize_batch_host_async(vqkv_stack_t s, const float* xs, uint32_t n_s
         fork_alt(*s, cs);  // ordered after the caller's earlier work
         const uint32_t n_chunks = (n_streams + chunk - 1) / chunk;
         const uint64_t set_bytes = (per_stream_in + pb + sizeof(float) * rows) * chunk;
-        // staging for every chunk (up to 16 GiB): the shared copy-in stream then never waits on this
-        // call's encodes, which would hold up the copies of the calls queued behind it
+        // staging for every chunk (up to 16 GiB per arena): the shared copy-in stream then never waits
+        // on this call's encodes, which would hold up the copies of the calls queued behind it
         const uint32_t nbuf = std::min<uint32_t>(n_chunks, std::max<uint32_t>(2, uint32_t((16ull << 30) / set_bytes)));
         std::vector<float*> dx(nbuf), dn(nbuf);
         std::vector<uint8_t*> dp(nbuf);
         std::vector<cudaEvent_t> in_ready(nbuf), done(nbuf), out_done(nbuf);
         cudaEvent_t last;
+        // staging arena (see vqkv_stack_s::Staging): free once the call two before this one completed
+        auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+        const uint64_t bx = al(per_stream_in * chunk), bp = al(std::max<uint64_t>(pb * chunk, 1)),
+                       bn = al(sizeof(float) * rows * chunk);
+        vqkv_stack_s::Staging* arena;
+        {
+            std::lock_guard<std::mutex> lk(s->mu);
+            arena = &s->staging[s->staging_next];
+            s->staging_next ^= 1u;
+        }
+        if (arena->done) VQKV_CUDA(cudaEventSynchronize(arena->done));
+        else VQKV_CUDA(cudaEventCreateWithFlags(&arena->done, cudaEventDisableTiming));
+        const uint64_t need = uint64_t(nbuf) * (bx + bp + bn);
+        if (arena->bytes < need) {
+            if (arena->base) VQKV_CUDA(cudaFree(arena->base));
+            arena->base = nullptr;
+            arena->bytes = 0;
+            VQKV_CUDA(cudaMalloc(&arena->base, need));
+            arena->bytes = need;
+        }
         for (uint32_t b = 0; b < nbuf; ++b) {
-            // allocated in the copy-in stream's order: the copies of a call queued
-            // behind another call's encodes start at once (not after those encodes)
-            VQKV_CUDA(cudaMallocAsync(&dx[b], per_stream_in * chunk, cp_in));
-            VQKV_CUDA(cudaMallocAsync(&dp[b], std::max<uint64_t>(pb * chunk, 1), cp_in));
-            VQKV_CUDA(cudaMallocAsync(&dn[b], sizeof(float) * rows * chunk, cp_in));
+            uint8_t* p0 = arena->base + uint64_t(b) * (bx + bp + bn);
+            dx[b] = reinterpret_cast<float*>(p0);
+            dp[b] = p0 + bx;
+            dn[b] = reinterpret_cast<float*>(p0 + bx + bp);
             VQKV_CUDA(cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming));
             VQKV_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
             VQKV_CUDA(cudaEventCreateWithFlags(&out_done[b], cudaEventDisableTiming));
@@ -504,10 +527,8 @@ int vqkv_quantize_batch_host_async(vqkv_stack_t s, const float* xs, uint32_t n_s
         // returned to the pool in stream order behind it
         VQKV_CUDA(cudaEventRecord(last, cp_out));  // after every chunk's copy-out, hence every encode
         VQKV_CUDA(cudaStreamWaitEvent(cs, last, 0));
+        VQKV_CUDA(cudaEventRecord(arena->done, cs));  // after every copy-out: the arena is free again
         for (uint32_t b = 0; b < nbuf; ++b) {
-            VQKV_CUDA(cudaFreeAsync(dx[b], cs));
-            VQKV_CUDA(cudaFreeAsync(dp[b], cs));
-            VQKV_CUDA(cudaFreeAsync(dn[b], cs));
             cudaEventDestroy(in_ready[b]);  // released once complete
             cudaEventDestroy(done[b]);
             cudaEventDestroy(out_done[b]);

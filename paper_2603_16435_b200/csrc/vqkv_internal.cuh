@@ -94,6 +94,15 @@ struct vqkv_stack_s {
     unsigned long long* d_counters = nullptr; // encode diagnostics [4]
     cudaStream_t cp_in = nullptr, cp_out = nullptr;  // host-buffer pipeline copy streams (lazy)
     cudaStream_t cs_alt = nullptr;  // second compute stream: consecutive chunk encodes overlap their tails
+    // host-buffer calls stage through two persistent device arenas, used alternately: a call waits
+    // (host side) for the call two before it, so a host running ahead is held back instead of the
+    // stream-ordered pool growing (and mapping memory) inside the timed pipeline
+    struct Staging {
+        uint8_t* base = nullptr;
+        uint64_t bytes = 0;
+        cudaEvent_t done = nullptr;
+    } staging[2];
+    uint32_t staging_next = 0;
     std::mutex mu;
 };
 
