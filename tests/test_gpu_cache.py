@@ -279,10 +279,11 @@ def test_cache_vqks_snapshots(torch_mod, tmp_path):
         DeviceCacheState.load_snapshots(paths, other, pv)
 
 
-def test_cache_group_major_mirror(torch_mod, tmp_path):
+def test_cache_group_major_mirror(torch_mod, tmp_path, monkeypatch):
     """The group-major key-code mirror: kept in step through prefill, flushes and capacity
     growth (records rebuilt from the payload) and snapshot loads; attention over it equals
-    attention over the CodeMatrix rows and the oracle."""
+    attention over the CodeMatrix rows and the oracle (fp32 LUT)."""
+    monkeypatch.delenv("VQKV_ATTEND_INT16", raising=False)
     torch = torch_mod
     from paper_2603_16435_b200 import device as Dv
     from paper_2603_16435_b200.cache import DeviceCacheState

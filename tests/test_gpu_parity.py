@@ -277,11 +277,12 @@ def gm_records_np(ks, codes, cap):
 @pytest.mark.parametrize("nk,sk,nv,sv,n_pairs,n_init,n_comp,n_local",
                          [(56, 1024, 16, 512, 2, 4, 3000, 17), (56, 1024, 16, 512, 1, 3, 8300, 5),
                           (6, 256, 4, 128, 3, 4, 9000, 40), (5, 1000, 3, 64, 2, 0, 700, 3), (1, 9, 1, 4, 1, 1, 40, 0)])
-def test_attention_group_major_keys(torch_mod, nk, sk, nv, sv, n_pairs, n_init, n_comp, n_local):
+def test_attention_group_major_keys(torch_mod, monkeypatch, nk, sk, nv, sv, n_pairs, n_init, n_comp, n_local):
     """Group-major key codes: the transcoder writes the documented records, attention over them
     computes the same logits as over the CodeMatrix rows (same lookups, same order), and it
-    matches the oracle within the tolerance."""
+    matches the oracle within the tolerance.  (fp32 LUT: the opt-in int16 LUT is tested apart.)"""
     torch = torch_mod
+    monkeypatch.delenv("VQKV_ATTEND_INT16", raising=False)
     from paper_2603_16435_b200 import device as Dv
 
     rng = O.Rng(nk * 7 + sk)
