@@ -658,11 +658,13 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
                 lds64((Lb + 8192u) | (__funnelshift_r(xl, xh, off[1]) & msk[1]), w[1]);
                 lds64((Lb + 16384u) | (__funnelshift_r(xl, xh, off[2]) & msk[2]), w[2]);
                 lds64((Lb + 24576u) | (__funnelshift_r(xl, xh, off[3]) & msk[3]), w[3]);
+                // per 32-bit word: the whole word and its high half accumulate; the low-half sum is
+                // recovered exactly afterwards (full - (high << 16), mod 2^32: it stays below 2^22)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    il[k][0] += w[q].x & 0xffffu;
+                    il[k][0] += w[q].x;
                     il[k][1] += w[q].x >> 16;
-                    il[k][2] += w[q].y & 0xffffu;
+                    il[k][2] += w[q].y;
                     il[k][3] += w[q].y >> 16;
                 }
             }
@@ -769,6 +771,11 @@ __global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) 
     if constexpr (GM == 2) {
         const float* dqp = a.dq + uint64_t(pair) * kG;
         const int bias = int(a.kn) * 32768;
+#pragma unroll
+        for (int k = 0; k < kTokPerThread; ++k) {
+            il[k][0] -= il[k][1] << 16;
+            il[k][2] -= il[k][3] << 16;
+        }
 #pragma unroll
         for (int g = 0; g < kG; ++g) {
             const float d = __ldg(dqp + g);
