@@ -653,7 +653,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     }
                 }
                 if (pk_dst) {
-                    pk_acc |= z << pk_n;  // pk_n < 16 before, bits <= 12: no overflow
+                    pk_acc |= z << pk_n;  // pk_n < 16 before, bits <= 16: pk_n stays below 32
                     pk_n += si.bits;
                     if (pk_n >= 16) {
                         if (valid && !exact_row) *pk_dst = uint16_t(pk_acc);
