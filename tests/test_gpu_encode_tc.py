@@ -238,3 +238,15 @@ def test_degenerate_sizes(torch_mod):
     # host-buffer path with one row
     ph, nh = Dv.quantize_streams_host(p, torch.from_numpy(x1).reshape(1, 1, 128).contiguous())
     assert np.array_equal(ph[0].numpy(), ref_pay)
+
+
+def test_tc_encode_many_stages(torch_mod):
+    """More stages than the encoder caches in shared memory (kSmemStages = 128): the stage
+    descriptors past the cache are read from global memory; codes and norms stay bit-exact."""
+    rng = O.Rng(130)
+    o = rng.stack(130, 16, 128, O.KEY)
+    p = product_stack(o)
+    xs = rng.matrix(64, 128)
+    pay, nrm = run_tc(torch_mod, p, xs)
+    mism, ties = compare(o, p, xs, pay, nrm)
+    assert mism == 0
