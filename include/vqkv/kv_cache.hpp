@@ -7,7 +7,9 @@
 // are reconstructed on the GPU by view_block.  Single writer (kv_cache.hpp:41-44).
 #pragma once
 
+#include <cstring>
 #include <deque>
+#include <fstream>
 #include <string>
 #include <vector>
 
@@ -164,6 +166,12 @@ public:
     const std::vector<float>& key_residual_norms() const { return key_residual_norms_; }
     const std::vector<float>& value_residual_norms() const { return value_residual_norms_; }
 
+    /// VQKS snapshot (kv_cache.cpp:206-246): same byte layout as the reference.
+    void save_snapshot(const std::string& path) const;
+    /// kv_cache.cpp:248-312: rejects foreign stacks (content hash) and inconsistent lengths.
+    static CacheState load_snapshot(const std::string& path, const CodebookStack& key_stack,
+                                    const CodebookStack& value_stack);
+
     // raw segment access for the device attention path
     const MatrixF& init_keys() const { return init_keys_; }
     const MatrixF& init_values() const { return init_values_; }
@@ -219,5 +227,122 @@ private:
     std::deque<std::vector<float>> local_keys_, local_values_;
     size_t batched_compressions_ = 0;
 };
+
+namespace detail {
+template <class T>
+inline void put_scalar(std::ostream& out, T v) {
+    out.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+template <class T>
+inline T get_scalar(std::istream& in, size_t& offset, const char* what) {
+    T v{};
+    in.read(reinterpret_cast<char*>(&v), sizeof(T));
+    if (!in) throw FormatError(std::string("truncated file reading ") + what, offset);
+    offset += sizeof(T);
+    return v;
+}
+inline void get_bytes(std::istream& in, void* p, size_t n, size_t& offset, const char* what) {
+    in.read(static_cast<char*>(p), std::streamsize(n));
+    if (!in) throw FormatError(std::string("truncated file reading ") + what, offset);
+    offset += n;
+}
+}  // namespace detail
+
+inline void CacheState::save_snapshot(const std::string& path) const {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw IoError("cannot open " + path + " for writing");
+    using detail::put_scalar;
+    out.write("VQKS", 4);
+    put_scalar<uint32_t>(out, 1);
+    put_scalar<uint64_t>(out, policy_.init_len);
+    put_scalar<uint64_t>(out, policy_.local_len);
+    put_scalar<uint8_t>(out, policy_.eager ? 1 : 0);
+    put_scalar<uint8_t>(out, prefilled_ ? 1 : 0);
+    put_scalar<uint64_t>(out, total_len());
+    put_scalar<uint32_t>(out, uint32_t(key_dim()));
+    put_scalar<uint32_t>(out, uint32_t(value_dim()));
+    put_scalar<uint64_t>(out, stack_content_hash(*key_stack_));
+    put_scalar<uint64_t>(out, stack_content_hash(*value_stack_));
+    put_scalar<uint64_t>(out, batched_compressions_);
+    for (const MatrixF* m : {&init_keys_, &init_values_}) {
+        put_scalar<uint64_t>(out, uint64_t(m->rows()));
+        out.write(reinterpret_cast<const char*>(m->data()), std::streamsize(sizeof(float) * size_t(m->size())));
+    }
+    key_codes_.save(out);
+    value_codes_.save(out);
+    out.write(reinterpret_cast<const char*>(key_residual_norms_.data()),
+              std::streamsize(sizeof(float) * key_residual_norms_.size()));
+    out.write(reinterpret_cast<const char*>(value_residual_norms_.data()),
+              std::streamsize(sizeof(float) * value_residual_norms_.size()));
+    auto rows = [&](const auto& rs) {
+        put_scalar<uint64_t>(out, uint64_t(rs.size()));
+        for (const auto& r : rs) out.write(reinterpret_cast<const char*>(r.data()), std::streamsize(sizeof(float) * r.size()));
+    };
+    rows(pending_keys_);
+    rows(pending_values_);
+    rows(local_keys_);
+    rows(local_values_);
+    if (!out) throw IoError("write failed for " + path);
+}
+
+inline CacheState CacheState::load_snapshot(const std::string& path, const CodebookStack& key_stack,
+                                            const CodebookStack& value_stack) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError("cannot open " + path);
+    size_t off = 0;
+    char magic[4] = {};
+    in.read(magic, 4);
+    if (!in || std::memcmp(magic, "VQKS", 4) != 0) throw FormatError("bad magic, expected VQKS", 0);
+    off = 4;
+    using detail::get_scalar;
+    const auto version = get_scalar<uint32_t>(in, off, "version");
+    if (version != 1) throw FormatError("unsupported snapshot version " + std::to_string(version), off - 4);
+    WindowPolicy policy;
+    policy.init_len = get_scalar<uint64_t>(in, off, "init_len");
+    policy.local_len = get_scalar<uint64_t>(in, off, "local_len");
+    policy.eager = get_scalar<uint8_t>(in, off, "eager flag") != 0;
+    const bool prefilled = get_scalar<uint8_t>(in, off, "prefilled flag") != 0;
+    const auto stored_len = get_scalar<uint64_t>(in, off, "total_len");
+    const auto dk = get_scalar<uint32_t>(in, off, "key dim");
+    const auto dv = get_scalar<uint32_t>(in, off, "value dim");
+    if (int64_t(dk) != key_stack.dim() || int64_t(dv) != value_stack.dim())
+        throw InvalidInput("snapshot dimensions do not match the supplied stacks");
+    const auto kh = get_scalar<uint64_t>(in, off, "key stack hash");
+    const auto vh = get_scalar<uint64_t>(in, off, "value stack hash");
+    if (kh != stack_content_hash(key_stack) || vh != stack_content_hash(value_stack))
+        throw InvalidInput("snapshot was built against different codebook stacks");
+    CacheState st(key_stack, value_stack, policy);
+    st.prefilled_ = prefilled;
+    st.batched_compressions_ = get_scalar<uint64_t>(in, off, "compression count");
+    auto matrix = [&](MatrixF& m, int64_t cols, const char* what) {
+        const auto r = get_scalar<uint64_t>(in, off, what);
+        m.resize(int64_t(r), cols);
+        detail::get_bytes(in, m.data(), sizeof(float) * size_t(m.size()), off, what);
+    };
+    matrix(st.init_keys_, key_stack.dim(), "init keys");
+    matrix(st.init_values_, value_stack.dim(), "init values");
+    st.key_codes_ = CodeMatrix::load(in, off);
+    st.value_codes_ = CodeMatrix::load(in, off);
+    st.key_residual_norms_.resize(st.key_codes_.rows());
+    detail::get_bytes(in, st.key_residual_norms_.data(), sizeof(float) * st.key_residual_norms_.size(), off,
+                      "key residual norms");
+    st.value_residual_norms_.resize(st.value_codes_.rows());
+    detail::get_bytes(in, st.value_residual_norms_.data(), sizeof(float) * st.value_residual_norms_.size(), off,
+                      "value residual norms");
+    auto rows = [&](auto& rs, int64_t dim, const char* what) {
+        const auto n = get_scalar<uint64_t>(in, off, what);
+        for (uint64_t i = 0; i < n; ++i) {
+            std::vector<float> r(static_cast<size_t>(dim));
+            detail::get_bytes(in, r.data(), sizeof(float) * r.size(), off, what);
+            rs.push_back(std::move(r));
+        }
+    };
+    rows(st.pending_keys_, key_stack.dim(), "pending keys");
+    rows(st.pending_values_, value_stack.dim(), "pending values");
+    rows(st.local_keys_, key_stack.dim(), "local keys");
+    rows(st.local_values_, value_stack.dim(), "local values");
+    if (st.total_len() != stored_len) throw FormatError("segment lengths do not add up to total_len", off);
+    return st;
+}
 
 }  // namespace vqkv

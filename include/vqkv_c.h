@@ -5,7 +5,7 @@
  * boundary.  Every call returns an int status (VQKV_OK == 0) whose non-zero
  * values mirror the exception kinds of proj/core/include/vqkv/errors.hpp:12-49;
  * vqkv_last_error() returns the thread-local message.  The C++ mirror in
- * include/vqkv/*.hpp rethrows the matching vqkv:: exception.
+ * include/vqkv/ headers rethrows the matching vqkv:: exception.
  *
  * Each entry point replaces one reference interface (proj/core/...):
  *   vqkv_stack_create      <- load_stack + Codebook::refresh   (codebook.cpp:30-39, 277-316)
@@ -205,7 +205,7 @@ int vqkv_payload_append(uint8_t* dst_dev, uint64_t dst_stride, uint64_t dst_bits
                         uint64_t src_stride, uint64_t src_bits, uint32_t n_streams, void* stream);
 
 /* HOST-buffer variants (copy in, compute, copy out; synchronous), used by the
- * C++ mirror API (include/vqkv/*.hpp) whose signatures take host matrices. */
+ * C++ mirror API (include/vqkv/ headers) whose signatures take host matrices. */
 /* quantize_batch of `rows` host rows (one stream), optional final residuals */
 int vqkv_quantize_rows_host(vqkv_stack_t stack, const float* xs_host, uint64_t rows, uint64_t search_block,
                             uint8_t* payload_host, float* residual_norms_host, float* residuals_host);
@@ -216,6 +216,11 @@ int vqkv_reconstruct_block_host(vqkv_stack_t stack, const uint8_t* payload_host,
                                 uint64_t begin, uint64_t end, float* out_host);
 int vqkv_attend_decode_host(vqkv_stack_t key_stack, vqkv_stack_t value_stack,
                             const vqkv_attend_args* host_args);
+/* attend_raw (attention.cpp:71-88): softmax(scale q K^T) V over `rows` raw host rows
+ * keys [rows][dk], values [rows][dv], one query [dk] -> out [dv] (host), on `device`.
+ * scale <= 0 means 1/sqrt(dk).  No codebooks involved. */
+int vqkv_attend_raw_host(int device, const float* keys_host, const float* values_host, uint64_t rows, uint32_t dk,
+                         uint32_t dv, const float* query_host, double scale, float* out_host);
 
 /* Merge G partial attention results of a sequence split (one per shard):
  * o = sum_g exp(lse_g - LSE) o_g, LSE = log sum_g exp(lse_g).

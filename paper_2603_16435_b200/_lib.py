@@ -97,6 +97,7 @@ _SIGS = {
     "vqkv_nearest_host": (C.c_int, [P, C.c_uint32, P, C.c_uint64, u32p, fp]),
     "vqkv_reconstruct_block_host": (C.c_int, [P, P, C.c_uint64, C.c_uint64, C.c_uint64, P]),
     "vqkv_attend_decode_host": (C.c_int, [P, P, C.POINTER(AttendArgs)]),
+    "vqkv_attend_raw_host": (C.c_int, [C.c_int, P, P, C.c_uint64, C.c_uint32, C.c_uint32, P, C.c_double, P]),
 }
 
 EXPORTED = tuple(_SIGS)

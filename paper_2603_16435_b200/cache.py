@@ -216,6 +216,10 @@ class DeviceCacheState:
             values[:, b - begin: e - begin] = Dv.reconstruct_streams(self.vstack, self._payload(1), self.n_comp,
                                                                      b - ie, e - ie)
             exact[b - begin: e - begin] = False
+            # an out-of-range code (a foreign payload) only sets the stack's sticky device flag:
+            # surface it as the reference's InvalidCode (codebook.cpp:212-217)
+            for st in (self.kd, self.vd):
+                _lib.call("vqkv_stack_take_error", st.h)
         if end > ce:
             b = max(begin, ce)
             keys[:, b - begin:] = self.tail_k[:, b - ce: end - ce]
@@ -278,11 +282,25 @@ class DeviceCacheState:
         if queries.dim() != 3 or queries.shape[0] != self.n_streams or queries.shape[1] < 1 \
                 or queries.shape[2] != self.kd.dim:
             raise InvalidInput("queries must be nonempty with the key dimension")
-        comp, _ = self.attend(queries.contiguous(), scale=scale, want_lse=False)
-        # the reference's attend_raw over the originals: the same kernel with every row raw
-        raw, _ = Dv.attend_decode(self.kstack, self.vstack, queries.contiguous(), None, None, 0, None, None,
-                                  original_keys.contiguous(), original_values.contiguous(), scale=scale,
-                                  want_lse=False)
+        # the reference runs one query at a time (attention.cpp:104-106); the kernels take the
+        # queries as GQA groups, so they go in groups of 4 (the LUT kernel's G; the last group
+        # is padded with copies of its first query, whose outputs are dropped)
+        Q = queries.shape[1]
+        comp_parts, raw_parts = [], []
+        ok, ov = original_keys.contiguous(), original_values.contiguous()
+        for q0 in range(0, Q, 4):
+            qg = queries[:, q0:q0 + 4]
+            n = qg.shape[1]
+            if n < 4:
+                qg = torch.cat([qg, qg[:, :1].expand(-1, 4 - n, -1)], dim=1)
+            qg = qg.contiguous()
+            c, _ = self.attend(qg, scale=scale, want_lse=False)
+            # the reference's attend_raw over the originals: the same kernels with every row raw
+            r, _ = Dv.attend_decode(self.kstack, self.vstack, qg, None, None, 0, None, None, ok, ov, scale=scale,
+                                    want_lse=False)
+            comp_parts.append(c[:, :n])
+            raw_parts.append(r[:, :n])
+        comp, raw = torch.cat(comp_parts, dim=1), torch.cat(raw_parts, dim=1)
         c64, r64 = comp.double(), raw.double()
         max_err = (comp - raw).abs().amax(dim=(1, 2)).double()
         cn, rn = c64.norm(dim=2), r64.norm(dim=2)
@@ -349,7 +367,7 @@ class DeviceCacheState:
         import numpy as np
 
         from .codebook import CodeMatrix, stack_content_hash
-        from .errors import FormatError, IoError
+        from .errors import FormatError, InvalidCode, IoError
 
         parsed = []
         for src in sources:
@@ -402,6 +420,18 @@ class DeviceCacheState:
             init_v = rd_f32(rd("<Q", "init values"), dv, "init values")
             kc, off = CodeMatrix.load(inp, off)
             vc, off = CodeMatrix.load(inp, off)
+            # the codes must belong to the supplied stacks: same stage sizes and every index in
+            # range (the reference rejects bad indices with InvalidCode when it decodes them,
+            # codebook.cpp:212-217; the device decode would only raise a sticky flag)
+            for cm, st in ((kc, key_stack), (vc, value_stack)):
+                if list(cm.stage_sizes()) != [int(x) for x in st.stage_sizes()]:
+                    raise InvalidInput("snapshot code stage sizes do not match the supplied stacks")
+                if cm.rows():
+                    codes = cm.all_rows()
+                    bad = codes >= np.asarray(cm.stage_sizes(), dtype=codes.dtype)[None, :]
+                    if bad.any():
+                        r, st_i = map(int, np.argwhere(bad)[0])
+                        raise InvalidCode(f"index {int(codes[r, st_i])} out of range for stage {st_i}")
             kn = rd_f32(kc.rows(), 1, "key residual norms")[:, 0]
             vn = rd_f32(vc.rows(), 1, "value residual norms")[:, 0]
             pend_k = rd_f32(rd("<Q", "pending keys"), dk, "pending keys")

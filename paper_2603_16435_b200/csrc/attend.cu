@@ -93,9 +93,9 @@ attend_generic_kernel(StackView ksv, StackView vsv, SegArgs a, uint32_t Dk, uint
     float* ml = acc + G * Dv;                                    // m[G], l[G]
     for (uint32_t i = threadIdx.x; i < G * Dk; i += blockDim.x) q[i] = a.q[uint64_t(pair) * G * Dk + i];
     for (uint32_t i = lane; i < G * Dv; i += 32) acc[i] = 0.f;
-    if (lane < G) {
-        ml[lane] = -INFINITY;
-        ml[G + lane] = 0.f;
+    for (uint32_t g = lane; g < G; g += 32) {  // any group size
+        ml[g] = -INFINITY;
+        ml[G + g] = 0.f;
     }
     __syncthreads();
     const uint64_t L = a.n_init + a.n_comp + a.n_local;
@@ -259,6 +259,26 @@ void launch_attend(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_at
     VQKV_CUDA(cudaFreeAsync(pacc, s));
     VQKV_CUDA(cudaFreeAsync(pm, s));
     VQKV_CUDA(cudaFreeAsync(pl, s));
+}
+
+// attend_raw (attention.cpp:71-88): softmax(scale q K^T) V over raw rows only, one query --
+// the generic kernel with every row in the "local" segment (no codebooks are touched).
+void launch_attend_raw(int device, const float* keys, const float* values, uint64_t rows, uint32_t dk, uint32_t dv,
+                       const float* q, double scale, float* out, cudaStream_t s) {
+    vqkv_stack_s ks, vs;  // shape-only views: n_comp = 0, so no stage table is read
+    ks.device = vs.device = device;
+    ks.dim = dk;
+    vs.dim = dv;
+    vqkv_attend_args a{};
+    a.n_pairs = 1;
+    a.group = 1;
+    a.q_dev = q;
+    a.local_k_dev = keys;
+    a.local_v_dev = values;
+    a.n_local = rows;
+    a.scale = scale;
+    a.out_dev = out;
+    launch_attend(ks, vs, a, s);
 }
 
 void launch_lse_combine(const float* o, const float* lse, uint32_t parts, uint64_t rows, uint32_t dv, float* out,

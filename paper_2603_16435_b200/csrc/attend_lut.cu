@@ -1143,11 +1143,7 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
             VQKV_CUDA(cudaMallocAsync(&qs, sizeof(float) * rows_pad, s));
             q_prep_kernel<<<rows_pad / 8, 256, 0, s>>>(a.q_dev, rows, rows_pad, float(scale), qh, ql, qs);
             launch_check("q_prep_kernel");
-            static bool tattr = false;
-            if (!tattr) {
-                VQKV_CUDA(cudaFuncSetAttribute(lut_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLutTcSmem)));
-                tattr = true;
-            }
+            VQKV_CUDA(cudaFuncSetAttribute(lut_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLutTcSmem)));
             uint32_t maxch = 0;
             for (const auto& st : ks.stages) maxch = std::max(maxch, (st.size + 127) / 128);
             lut_tc_kernel<<<dim3(maxch, ks.n), 160, kLutTcSmem, s>>>(ks.d_eff16, ks.d_eff16lo, ks.d_stages, qh, ql, qs,
@@ -1160,11 +1156,7 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         LutArgs la{a.q_dev, ks.d_eff, ks.d_stages, ks.n, kent, float(scale), lut};
         dim3 grid(unsigned((kent + kLutEntries - 1) / kLutEntries), (a.n_pairs + 7) / 8);
         const int lsmem = int(sizeof(float) * (8 * kG * kD + kLutEntries * kLutStride));
-        static bool lattr = false;
-        if (!lattr) {
-            VQKV_CUDA(cudaFuncSetAttribute(lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem));
-            lattr = true;
-        }
+        VQKV_CUDA(cudaFuncSetAttribute(lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem));
         lut_kernel<<<grid, 256, lsmem, s>>>(la, a.n_pairs);
         launch_check("lut_kernel");
         }
@@ -1187,15 +1179,13 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
                     a.vcodes_dev + uint64_t(a.n_pairs - 1) * vstr + vpb, float(scale), n_splits,
                     ph, po, pm, pl, a.init_stride ? a.init_stride : a.n_init,
                     a.local_stride ? a.local_stride : a.n_local, a.kcodes_cap, lut16, dq};
-        static bool attr = false;
-        if (!attr) {
+        {  // per launch (per-device attribute)
             VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(kMainSmem + kAlignSlack)));
             VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(kGmSmem + kAlignSlack)));
             VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(kGmSmem + kAlignSlack)));
-            attr = true;
         }
         dim3 grid(n_splits + 1, a.n_pairs);
         if (i16)

@@ -19,13 +19,15 @@
 // residual as the reference.  Rows with non-finite input go to the exact
 // SIMT encoder (their tensor-core pass runs on zeros and is discarded).
 //
-// CTA layout (one CTA per SM, persistent over pairs of 128-row tiles that run
-// the stages in lockstep so every codebook chunk loaded to smem feeds two
-// MMAs):
-//   warp 0      bulk-copy producer (TMA engine): 32 KB pre-swizzled fp16
-//               codebook chunks (128 entries x K=128) into a 3-deep ring
-//   warp 1      MMA issuer: 8 x tcgen05.mma M128 N128 K16 per tile-chunk
-//   warp 2      TMEM allocator
+// CTA layout (one CTA per SM, persistent over pairs of 128-row tiles that
+// advance independently -- each tile has its own chunk ring, A tile and
+// accumulator, so one tile's stage end overlaps the other tile's MMAs):
+//   warps 0 / 2 (lane 0)  bulk-copy producer of tile 0 / 1 (TMA engine):
+//               36 KB pre-swizzled fp16 codebook chunks (128 entries x
+//               (K=128 + 16-wide ||e||^2 block)) into a 2-slot ring per tile
+//   warps 1 / 3 (lane 0)  MMA issuer of tile 0 / 1: per chunk 8 x
+//               tcgen05.mma M128 N128 K16 + one K16 MMA for the norm block
+//   warp 2      also allocates TMEM
 //   warps 4-7   epilogue of tile 0 (thread = row = TMEM lane)
 //   warps 8-11  epilogue of tile 1
 // TMEM (512 columns): [0,128) acc tile0, [128,256) acc tile1,
@@ -787,11 +789,8 @@ void launch_encode_tc(const vqkv_stack_s& st, const float* xs, uint32_t n_stream
     if (total >= (1ull << 32)) fail(VQKV_UNSUPPORTED, "more than 2^32 rows per call");
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st.device);
-    static bool attr_set = false;
-    if (!attr_set) {
-        VQKV_CUDA(cudaFuncSetAttribute(encode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
-        attr_set = true;
-    }
+    // per launch: the attribute is per device, and the call is cheap (no static flag to race on)
+    VQKV_CUDA(cudaFuncSetAttribute(encode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
     uint16_t* codes = nullptr;
     uint32_t* list = nullptr;  // [0] = count, [1..] = rows
     VQKV_CUDA(cudaMallocAsync(&codes, sizeof(uint16_t) * total * st.n, s));

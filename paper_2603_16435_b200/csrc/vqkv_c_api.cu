@@ -165,6 +165,33 @@ void quantize_device(vqkv_stack_s& st, const float* xs, uint32_t n_streams, uint
     VQKV_CUDA(cudaFreeAsync(codes, s));
 }
 
+// Carves the synchronous host entry points' device buffers out of the stack's grow-only scratch
+// (no cudaMalloc/cudaFree per call; nothing to leak when a call throws).  Caller holds host_mu.
+struct HostScratch {
+    vqkv_stack_s& st;
+    std::vector<uint64_t> sizes;
+    explicit HostScratch(vqkv_stack_s& s) : st(s) {}
+    // reserve `bytes` (+16 B of slack for whole-word reads), 256 B aligned; returns the offset
+    uint64_t add(uint64_t bytes) {
+        uint64_t off = 0;
+        for (uint64_t b : sizes) off += b;
+        sizes.push_back((bytes + 16 + 255) & ~uint64_t(255));
+        return off;
+    }
+    uint8_t* commit() {
+        uint64_t total = 0;
+        for (uint64_t b : sizes) total += b;
+        if (st.host_scratch_bytes < total) {
+            if (st.host_scratch) VQKV_CUDA(cudaFree(st.host_scratch));
+            st.host_scratch = nullptr;
+            st.host_scratch_bytes = 0;
+            VQKV_CUDA(cudaMalloc(&st.host_scratch, total));
+            st.host_scratch_bytes = total;
+        }
+        return st.host_scratch;
+    }
+};
+
 }  // namespace
 
 extern "C" {
@@ -301,6 +328,7 @@ int vqkv_stack_destroy(vqkv_stack_t s) {
         cudaFree(s->d_sqn_pad);
         cudaFree(s->d_error);
         cudaFree(s->d_counters);
+        if (s->host_scratch) cudaFree(s->host_scratch);
         if (s->cs_alt) cudaStreamDestroy(s->cs_alt);
         for (auto& a : s->staging) {
             if (a.done) cudaEventSynchronize(a.done), cudaEventDestroy(a.done);
@@ -464,6 +492,13 @@ int vqkv_quantize_batch_host_async(vqkv_stack_t s, const float* xs, uint32_t n_s
         // launch idles SMs in its last round, and the next chunk's CTAs take them over
         cudaStream_t cst[2] = {cs, s->cs_alt};
         fork_alt(*s, cs);  // ordered after the caller's earlier work
+        {  // the shared copy-in stream too: earlier work on `stream` may still be writing xs_host
+            cudaEvent_t e;
+            VQKV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            VQKV_CUDA(cudaEventRecord(e, cs));
+            VQKV_CUDA(cudaStreamWaitEvent(cp_in, e, 0));
+            cudaEventDestroy(e);
+        }
         const uint32_t n_chunks = (n_streams + chunk - 1) / chunk;
         const uint64_t set_bytes = (per_stream_in + pb + sizeof(float) * rows) * chunk;
         // staging for every chunk (up to 16 GiB per arena): the shared copy-in stream then never waits
@@ -628,22 +663,21 @@ int vqkv_quantize_rows_host(vqkv_stack_t s, const float* xs, uint64_t rows, uint
         need(sb >= 1, VQKV_INVALID_INPUT, "search_block must be >= 1");
         if (rows == 0) return;
         DeviceGuard g(s->device);
+        std::lock_guard<std::mutex> lk(s->host_mu);
         const uint64_t D = s->dim, pb = payload_bytes(s->row_bits, rows);
-        float *dx = nullptr, *dn = nullptr, *dr = nullptr;
-        uint8_t* dp = nullptr;
-        VQKV_CUDA(cudaMalloc(&dx, sizeof(float) * rows * D));
-        VQKV_CUDA(cudaMalloc(&dn, sizeof(float) * rows));
-        VQKV_CUDA(cudaMalloc(&dp, std::max<uint64_t>(pb, 16)));
-        if (residuals) VQKV_CUDA(cudaMalloc(&dr, sizeof(float) * rows * D));
+        HostScratch hs(*s);
+        const uint64_t ox = hs.add(sizeof(float) * rows * D), on = hs.add(sizeof(float) * rows), op = hs.add(pb),
+                       orr = residuals ? hs.add(sizeof(float) * rows * D) : 0;
+        uint8_t* base = hs.commit();
+        float* dx = reinterpret_cast<float*>(base + ox);
+        float* dn = reinterpret_cast<float*>(base + on);
+        uint8_t* dp = base + op;
+        float* dr = residuals ? reinterpret_cast<float*>(base + orr) : nullptr;
         VQKV_CUDA(cudaMemcpy(dx, xs, sizeof(float) * rows * D, cudaMemcpyHostToDevice));
         quantize_device(*s, dx, 1, rows, sb, dp, dn, dr, nullptr);
         if (pb && payload) VQKV_CUDA(cudaMemcpy(payload, dp, pb, cudaMemcpyDeviceToHost));
         if (norms) VQKV_CUDA(cudaMemcpy(norms, dn, sizeof(float) * rows, cudaMemcpyDeviceToHost));
         if (residuals) VQKV_CUDA(cudaMemcpy(residuals, dr, sizeof(float) * rows * D, cudaMemcpyDeviceToHost));
-        cudaFree(dx);
-        cudaFree(dn);
-        cudaFree(dp);
-        cudaFree(dr);
     });
 }
 
@@ -653,19 +687,17 @@ int vqkv_nearest_host(vqkv_stack_t s, uint32_t stage, const float* x, uint64_t s
         need(stage < s->n, VQKV_INVALID_INPUT, "stage out of range");
         need(sb >= 1, VQKV_INVALID_INPUT, "search_block must be >= 1");
         DeviceGuard g(s->device);
-        float* dx = nullptr;
-        uint32_t* di = nullptr;
-        float* dd = nullptr;
-        VQKV_CUDA(cudaMalloc(&dx, sizeof(float) * s->dim));
-        VQKV_CUDA(cudaMalloc(&di, sizeof(uint32_t)));
-        VQKV_CUDA(cudaMalloc(&dd, sizeof(float)));
+        std::lock_guard<std::mutex> lk(s->host_mu);
+        HostScratch hs(*s);
+        const uint64_t ox = hs.add(sizeof(float) * s->dim), oi = hs.add(sizeof(uint32_t)), od = hs.add(sizeof(float));
+        uint8_t* base = hs.commit();
+        float* dx = reinterpret_cast<float*>(base + ox);
+        uint32_t* di = reinterpret_cast<uint32_t*>(base + oi);
+        float* dd = reinterpret_cast<float*>(base + od);
         VQKV_CUDA(cudaMemcpy(dx, x, sizeof(float) * s->dim, cudaMemcpyHostToDevice));
         launch_nearest(*s, stage, dx, 1, sb, di, dd, nullptr);
         VQKV_CUDA(cudaMemcpy(index, di, sizeof(uint32_t), cudaMemcpyDeviceToHost));
         VQKV_CUDA(cudaMemcpy(distance, dd, sizeof(float), cudaMemcpyDeviceToHost));
-        cudaFree(dx);
-        cudaFree(di);
-        cudaFree(dd);
     });
 }
 
@@ -678,19 +710,19 @@ int vqkv_reconstruct_block_host(vqkv_stack_t s, const uint8_t* payload, uint64_t
                                          ") out of bounds for " + std::to_string(rows) + " rows");
         if (end == begin) return;
         DeviceGuard g(s->device);
+        std::lock_guard<std::mutex> lk(s->host_mu);
         const uint64_t pb = payload_bytes(s->row_bits, rows);
-        uint8_t* dp = nullptr;
-        float* dout = nullptr;
-        VQKV_CUDA(cudaMalloc(&dp, std::max<uint64_t>(pb, 16)));
-        VQKV_CUDA(cudaMalloc(&dout, sizeof(float) * (end - begin) * s->dim));
+        HostScratch hs(*s);
+        const uint64_t op = hs.add(pb), oo = hs.add(sizeof(float) * (end - begin) * s->dim);
+        uint8_t* base = hs.commit();
+        uint8_t* dp = base + op;
+        float* dout = reinterpret_cast<float*>(base + oo);
         if (pb) VQKV_CUDA(cudaMemcpy(dp, payload, pb, cudaMemcpyHostToDevice));
         launch_reconstruct(*s, dp, 1, rows, begin, end, dout, nullptr);
         VQKV_CUDA(cudaMemcpy(out, dout, sizeof(float) * (end - begin) * s->dim, cudaMemcpyDeviceToHost));
         int code = 0;
         VQKV_CUDA(cudaMemcpy(&code, s->d_error, sizeof(int), cudaMemcpyDeviceToHost));
         VQKV_CUDA(cudaMemset(s->d_error, 0, sizeof(int)));
-        cudaFree(dp);
-        cudaFree(dout);
         if (code) fail(VQKV_INVALID_CODE, "code index out of range for its stage");
     });
 }
@@ -702,37 +734,44 @@ int vqkv_attend_decode_host(vqkv_stack_t ks, vqkv_stack_t vs, const vqkv_attend_
         need(h != nullptr, VQKV_INVALID_INPUT, "null args");
         if (h->n_pairs == 0 || h->group == 0) return;
         need(h->n_init + h->n_comp + h->n_local >= 1, VQKV_INVALID_STATE, "cannot attend over an empty cache");
-        DeviceGuard g(ks->device);
-        const uint64_t P = h->n_pairs, G = h->group, Dk = ks->dim, Dv = vs->dim;
-        std::vector<void*> owned;
-        auto up = [&](const void* src, uint64_t bytes) -> void* {
-            if (!src || bytes == 0) return nullptr;
-            void* d = nullptr;
-            VQKV_CUDA(cudaMalloc(&d, bytes + 16));  // slack: the fast path reads whole 8-byte words
-            VQKV_CUDA(cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice));
-            owned.push_back(d);
-            return d;
-        };
+        need(ks->device == vs->device, VQKV_INVALID_INPUT, "key and value stacks live on different devices");
         need(h->init_stride == 0 && h->local_stride == 0 && h->kcodes_stride == 0 && h->vcodes_stride == 0,
              VQKV_INVALID_INPUT, "host attention buffers must be dense (strides 0)");
         need(h->kcodes_layout == VQKV_KEYCODES_ROWS, VQKV_INVALID_INPUT, "host attention takes CodeMatrix key rows");
+        DeviceGuard g(ks->device);
+        std::lock_guard<std::mutex> lk(ks->host_mu);
+        const uint64_t P = h->n_pairs, G = h->group, Dk = ks->dim, Dv = vs->dim;
+        struct Up {
+            const void* src;
+            uint64_t bytes, off;
+        };
+        HostScratch hs(*ks);
+        auto plan = [&](const void* src, uint64_t bytes) { return Up{src, bytes, (src && bytes) ? hs.add(bytes) : 0}; };
+        Up uq = plan(h->q_dev, sizeof(float) * P * G * Dk), uik = plan(h->init_k_dev, sizeof(float) * P * h->n_init * Dk),
+           uiv = plan(h->init_v_dev, sizeof(float) * P * h->n_init * Dv),
+           ulk = plan(h->local_k_dev, sizeof(float) * P * h->n_local * Dk),
+           ulv = plan(h->local_v_dev, sizeof(float) * P * h->n_local * Dv),
+           ukc = plan(h->kcodes_dev, P * payload_bytes(ks->row_bits, h->n_comp)),
+           uvc = plan(h->vcodes_dev, P * payload_bytes(vs->row_bits, h->n_comp));
+        const uint64_t oo = hs.add(sizeof(float) * P * G * Dv), ol = hs.add(sizeof(float) * P * G);
+        uint8_t* base = hs.commit();
+        auto up = [&](const Up& u) -> void* {
+            if (!u.src || !u.bytes) return nullptr;
+            VQKV_CUDA(cudaMemcpy(base + u.off, u.src, u.bytes, cudaMemcpyHostToDevice));
+            return base + u.off;
+        };
         vqkv_attend_args d = *h;
-        d.q_dev = static_cast<const float*>(up(h->q_dev, sizeof(float) * P * G * Dk));
-        d.init_k_dev = static_cast<const float*>(up(h->init_k_dev, sizeof(float) * P * h->n_init * Dk));
-        d.init_v_dev = static_cast<const float*>(up(h->init_v_dev, sizeof(float) * P * h->n_init * Dv));
-        d.local_k_dev = static_cast<const float*>(up(h->local_k_dev, sizeof(float) * P * h->n_local * Dk));
-        d.local_v_dev = static_cast<const float*>(up(h->local_v_dev, sizeof(float) * P * h->n_local * Dv));
-        d.kcodes_dev = static_cast<const uint8_t*>(up(h->kcodes_dev, P * payload_bytes(ks->row_bits, h->n_comp)));
-        d.vcodes_dev = static_cast<const uint8_t*>(up(h->vcodes_dev, P * payload_bytes(vs->row_bits, h->n_comp)));
-        float *dout = nullptr, *dlse = nullptr;
-        VQKV_CUDA(cudaMalloc(&dout, sizeof(float) * P * G * Dv));
-        owned.push_back(dout);
-        if (h->lse_dev) {
-            VQKV_CUDA(cudaMalloc(&dlse, sizeof(float) * P * G));
-            owned.push_back(dlse);
-        }
+        d.q_dev = static_cast<const float*>(up(uq));
+        d.init_k_dev = static_cast<const float*>(up(uik));
+        d.init_v_dev = static_cast<const float*>(up(uiv));
+        d.local_k_dev = static_cast<const float*>(up(ulk));
+        d.local_v_dev = static_cast<const float*>(up(ulv));
+        d.kcodes_dev = static_cast<const uint8_t*>(up(ukc));
+        d.vcodes_dev = static_cast<const uint8_t*>(up(uvc));
+        float* dout = reinterpret_cast<float*>(base + oo);
+        float* dlse = reinterpret_cast<float*>(base + ol);
         d.out_dev = dout;
-        d.lse_dev = dlse;
+        d.lse_dev = h->lse_dev ? dlse : nullptr;
         need(d.q_dev != nullptr, VQKV_INVALID_INPUT, "null query");
         need(d.n_init == 0 || (d.init_k_dev && d.init_v_dev), VQKV_INVALID_INPUT, "null init rows");
         need(d.n_local == 0 || (d.local_k_dev && d.local_v_dev), VQKV_INVALID_INPUT, "null local rows");
@@ -740,7 +779,31 @@ int vqkv_attend_decode_host(vqkv_stack_t ks, vqkv_stack_t vs, const vqkv_attend_
         launch_attend(*ks, *vs, d, nullptr);
         VQKV_CUDA(cudaMemcpy(h->out_dev, dout, sizeof(float) * P * G * Dv, cudaMemcpyDeviceToHost));
         if (h->lse_dev) VQKV_CUDA(cudaMemcpy(h->lse_dev, dlse, sizeof(float) * P * G, cudaMemcpyDeviceToHost));
-        for (void* p : owned) cudaFree(p);
+    });
+}
+
+int vqkv_attend_raw_host(int device, const float* keys, const float* values, uint64_t rows, uint32_t dk, uint32_t dv,
+                         const float* query, double scale, float* out) {
+    return guard([&] {
+        // attention.cpp:73-78
+        need(rows >= 1, VQKV_INVALID_INPUT, "keys and values must be nonempty and the same length");
+        need(dk >= 1 && dv >= 1, VQKV_INVALID_INPUT, "query dimension does not match key dimension");
+        need(keys && values && query && out, VQKV_INVALID_INPUT, "null host buffer");
+        DeviceGuard g(device);
+        struct Buf {  // RAII: freed on every path
+            void* p = nullptr;
+            ~Buf() {
+                if (p) cudaFree(p);
+            }
+        } b;
+        const uint64_t nk = rows * dk, nv = rows * dv;
+        VQKV_CUDA(cudaMalloc(&b.p, sizeof(float) * (nk + nv + dk + dv)));
+        float* d = static_cast<float*>(b.p);
+        VQKV_CUDA(cudaMemcpy(d, keys, sizeof(float) * nk, cudaMemcpyHostToDevice));
+        VQKV_CUDA(cudaMemcpy(d + nk, values, sizeof(float) * nv, cudaMemcpyHostToDevice));
+        VQKV_CUDA(cudaMemcpy(d + nk + nv, query, sizeof(float) * dk, cudaMemcpyHostToDevice));
+        launch_attend_raw(device, d, d + nk, rows, dk, dv, d + nk + nv, scale, d + nk + nv + dk, nullptr);
+        VQKV_CUDA(cudaMemcpy(out, d + nk + nv + dk, sizeof(float) * dv, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -103,6 +103,11 @@ struct vqkv_stack_s {
         cudaEvent_t done = nullptr;
     } staging[2];
     uint32_t staging_next = 0;
+    // device scratch of the synchronous *_host entry points (grow-only, freed with the stack;
+    // host_mu serialises those calls on this stack)
+    uint8_t* host_scratch = nullptr;
+    uint64_t host_scratch_bytes = 0;
+    std::mutex host_mu;
     std::mutex mu;
 };
 
@@ -226,6 +231,8 @@ uint64_t gm_pair_bytes(const vqkv_stack_s& ks, uint64_t cap);
 void launch_keycodes_to_gm(const vqkv_stack_s& ks, const uint8_t* payload, uint64_t payload_stride, uint32_t n_pairs,
                            uint64_t src_row, uint64_t count, uint8_t* gm, uint64_t cap, uint64_t gm_stride,
                            uint64_t dst_row, cudaStream_t s);
+void launch_attend_raw(int device, const float* keys, const float* values, uint64_t rows, uint32_t dk, uint32_t dv,
+                       const float* q, double scale, float* out, cudaStream_t s);
 void launch_lse_combine(const float* o, const float* lse, uint32_t parts, uint64_t rows, uint32_t dv, float* out,
                         float* out_lse, cudaStream_t s);
 

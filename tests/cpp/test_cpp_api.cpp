@@ -145,7 +145,7 @@ int main() {
         std::memcpy(q.data(), qm.data(), 64);
         AttentionConfig cfg;
         VectorF a = attend(state, q, cfg);
-        VectorF r = attend_raw(ks, vs, all.keys, all.values, q, cfg);
+        VectorF r = attend_raw(all.keys, all.values, q, cfg);
         float err = 0.f;
         for (int64_t i = 0; i < a.size(); ++i) err = std::max(err, std::fabs(a[i] - r[i]));
         report(err < 1e-4f, "attend over the compressed cache == attention over its logical view");
@@ -154,6 +154,57 @@ int main() {
         attend(state, q, cfg, &stats);
         report(stats.reconstructed_rows == state.compressed_rows() && stats.peak_reconstructed_scalars <= 4 * 32,
                "attend stats follow the reference's block accounting");
+    }
+    {  // D = 128 cache: attend over the LUT kernel, fidelity (attention.cpp:90-134), VQKS snapshot round trip
+        std::mt19937_64 rng(2024);
+        auto ks = random_stack(rng, 8, 256, 128);
+        auto vs = random_stack(rng, 4, 128, 128);
+        vs.cache_kind = CacheKind::value;
+        CacheState state(ks, vs, WindowPolicy{4, 32, false});
+        MatrixF keys = random_matrix(rng, 300, 128), values = random_matrix(rng, 300, 128);
+        state.prefill(keys, values);
+        MatrixF qs = random_matrix(rng, 3, 128);
+        AttentionConfig cfg;
+        FidelityReport fr = fidelity(state, keys, values, qs, cfg);
+        ViewBlock all = state.view_block(0, state.total_len());
+        VectorF q0 = detail::row_of(qs, 0);
+        VectorF a = attend(state, q0, cfg), r = attend_raw(all.keys, all.values, q0, cfg);
+        float err = 0.f, mx = 1.f;
+        for (int64_t i = 0; i < a.size(); ++i) err = std::max(err, std::fabs(a[i] - r[i])), mx = std::max(mx, std::fabs(r[i]));
+        report(err <= mx / 128.f, "attend (G=4 LUT kernel) == attend_raw over the logical view (2^-7 tolerance)");
+        report(fr.output_mean_cosine > 0.5 && fr.output_mean_cosine <= 1.0 + 1e-9 && fr.key_intermediate_mse > 0.0 &&
+                   fr.value_intermediate_mse > 0.0 && fr.output_max_abs_err >= 0.0,
+               "fidelity reports cosine, max error and intermediate MSE");
+        bool threw = false;
+        try {
+            fidelity(state, random_matrix(rng, 5, 128), values, qs, cfg);
+        } catch (const InvalidInput&) {
+            threw = true;
+        }
+        report(threw, "fidelity rejects originals of the wrong length (InvalidInput)");
+        const std::string path = "/tmp/vqkv_cpp_snapshot.vqks";
+        state.save_snapshot(path);
+        CacheState back = CacheState::load_snapshot(path, ks, vs);
+        ViewBlock all2 = back.view_block(0, back.total_len());
+        report(back.total_len() == state.total_len() && back.key_codes() == state.key_codes() &&
+                   back.value_codes() == state.value_codes() &&
+                   std::memcmp(all2.keys.data(), all.keys.data(), sizeof(float) * size_t(all.keys.size())) == 0,
+               "VQKS snapshot round-trips the cache bit for bit");
+        auto other = random_stack(rng, 8, 256, 128);
+        threw = false;
+        try {
+            CacheState::load_snapshot(path, other, vs);
+        } catch (const InvalidInput&) {
+            threw = true;
+        }
+        report(threw, "load_snapshot rejects a different key stack (content hash)");
+        threw = false;
+        try {
+            throw DivergedError("loss is NaN", 3);
+        } catch (const Error& e) {
+            threw = std::string(e.what()).find("(epoch 3)") != std::string::npos;
+        }
+        report(threw, "DivergedError carries the epoch (errors.hpp:44-49)");
     }
     {  // codebook_test.cpp:257-273 RSVQ round trip + hash
         std::mt19937_64 rng(13);

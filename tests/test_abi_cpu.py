@@ -56,3 +56,14 @@ def test_status_codes_without_gpu():
         _lib.call("vqkv_set_encode_path", 9)
     # lse_combine argument validation
     assert L.vqkv_lse_combine(None, None, 0, 1, 1, None, None, None) == 1
+
+
+def test_cpp_reference_signatures_compile():
+    """Every reference entry point binds to a pointer of the reference's signature
+    (tests/cpp/test_signatures.cpp; compile-only, no GPU)."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run(["g++", "-std=c++17", "-Wall", "-Werror", "-fsyntax-only", "-I" + os.path.join(root, "include"),
+                        os.path.join(root, "tests", "cpp", "test_signatures.cpp")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

@@ -176,16 +176,17 @@ def test_payload_append_bit_offsets(torch_mod):
             assert np.array_equal(got[i, : len(full)], np.frombuffer(bytes(full), np.uint8)), cut
 
 
-@pytest.mark.parametrize("D", [8, 128])
-def test_cache_fidelity_vs_oracle(torch_mod, D):
-    """fidelity (attention.cpp:90-134): reconstruction MSE exact, attention-based fields within tolerance."""
+@pytest.mark.parametrize("D,Q", [(8, 4), (128, 4), (8, 40), (128, 40)])
+def test_cache_fidelity_vs_oracle(torch_mod, D, Q):
+    """fidelity (attention.cpp:90-134): reconstruction MSE exact, attention-based fields within
+    tolerance; any number of queries (Q = 40: ten groups of the kernels' G = 4)."""
     torch = torch_mod
     from paper_2603_16435_b200.cache import DeviceCacheState
 
     rng = O.Rng(7400 + D)
     ks, vs = rng.stack(3, 32, D, O.KEY), rng.stack(2, 16, D, O.VALUE)
     pk, pv = product_stack(ks), product_stack(vs)
-    S, L, Q = 2, 40, 4
+    S, L = 2, 40
     refs = [O.Cache(ks, vs, 3, 8, False) for _ in range(S)]
     dc = DeviceCacheState(pk, pv, S, 3, 8)
     keys = rng.matrix(S * L, D).reshape(S, L, D)
@@ -277,6 +278,32 @@ def test_cache_vqks_snapshots(torch_mod, tmp_path):
     other = product_stack(rng.stack(3, 16, 8, O.KEY))
     with pytest.raises(InvalidInput):
         DeviceCacheState.load_snapshots(paths, other, pv)
+
+
+def test_cache_snapshot_rejects_out_of_range_codes(torch_mod):
+    """A VQKS file whose codes exceed their stage size (S = 12 -> 4-bit fields) is rejected with
+    InvalidCode at load, as the reference rejects it when decoding (codebook.cpp:212-217), and a
+    file written for other stage sizes with InvalidInput."""
+    import io
+    import struct
+
+    from paper_2603_16435_b200.cache import DeviceCacheState
+    from paper_2603_16435_b200.errors import InvalidCode
+
+    rng = O.Rng(7777)
+    ks, vs = rng.stack(2, 12, 8, O.KEY), rng.stack(2, 12, 8, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    r = O.Cache(ks, vs, 2, 4, False)
+    r.prefill(rng.matrix(20, 8), rng.matrix(20, 8))
+    good = _vqks_from_oracle(r, ks, vs, 2, 4, False, True, pk, pv)
+    DeviceCacheState.load_snapshots([io.BytesIO(good)], pk, pv)  # loads
+    # the key CodeMatrix payload starts after the header, the init rows and its own header
+    c = r.counts()
+    off = 4 + struct.calcsize("<IQQBBQII") + 24 + 2 * (8 + 4 * 8 * c["init"]) + 4 + 4 * 2 + 8
+    bad = bytearray(good)
+    bad[off] = 0xFF  # row 0: both 4-bit fields = 15 >= 12
+    with pytest.raises(InvalidCode):
+        DeviceCacheState.load_snapshots([io.BytesIO(bytes(bad))], pk, pv)
 
 
 def test_cache_group_major_mirror(torch_mod, tmp_path, monkeypatch):
