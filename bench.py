@@ -62,6 +62,10 @@ def parse():
     ap.add_argument("--no-attention", action="store_true")
     ap.add_argument("--attn-context", type=int, default=131072)
     ap.add_argument("--attn-batch", type=int, default=16)
+    ap.add_argument("--parity-streams", type=int, default=2,
+                    help="full streams of the timed encode output checked against the oracle (0 = skip)")
+    ap.add_argument("--parity-pairs", type=int, default=2,
+                    help="(sequence, KV head) pairs of the configs[2] attention checked against the oracle")
     return ap.parse_args()
 
 
@@ -159,6 +163,9 @@ def gen_inputs_local(torch, n_streams, prefill, rank, device):
             os.sched_setaffinity(0, saved)
 
 
+HOST_STACKS = {}  # kind -> (entries, projections): the same bytes the parity checker loads
+
+
 def make_stacks(device):
     from paper_2603_16435_b200 import _lib, codebook
 
@@ -168,8 +175,52 @@ def make_stacks(device):
         ent = np.empty((n, s, D), np.float32)
         prj = np.empty((n, D, D), np.float32)
         assert L.vqkv_random_stack(seed, n, s, D, ent.ctypes.data, prj.ctypes.data) == 0
+        HOST_STACKS[kind] = (ent, prj)
         out.append(codebook.CodebookStack.from_arrays(list(ent), list(prj), kind, device))
     return out
+
+
+def oracle_stacks():
+    """The checker's copies of the bench stacks (oracle restatement of codebook.cpp, refreshed on
+    the host from the same entries and projections the device stacks were built from)."""
+    from oracle import oracle as O
+
+    return tuple(O.Stack.from_entries(list(HOST_STACKS[k][0]), list(HOST_STACKS[k][1]), k) for k in (0, 1))
+
+
+def encode_parity(Kh, Vh, kp, vp, kn, vn, middle, streams):
+    """Checker (outside every timed region): the timed encode's output for `streams` full
+    streams against the oracle's quantize_batch on the same rows.  Codes bit-exact modulo
+    near-ties (tau of SURVEY.md 8c, counted), residual norms bit-exact on every exact row."""
+    from oracle import oracle as O
+
+    t0 = time.perf_counter()
+    ok, ov = oracle_stacks()
+    res = {}
+    for name, ost, X, P, N in (("K", ok, Kh, kp, kn), ("V", ov, Vh, vp, vn)):
+        tot = dict(rows_checked=0, mismatches=0, near_ties=0, norm_mismatches=0)
+        emax = ost.stage_max_norm()
+        for sid in streams:
+            codes, norms, ins = ost.quantize_rows_instrumented_mt(X[sid].numpy())
+            got = ost.unpack(P[sid].cpu().numpy(), middle)
+            c = O.classify_codes(got, codes, ins, emax)
+            same = (got == codes).all(axis=1)
+            gn = N[sid].cpu().numpy()
+            tot["norm_mismatches"] += int((gn[same].view(np.uint32) != norms[same].view(np.uint32)).sum())
+            for k in ("rows_checked", "mismatches", "near_ties"):
+                tot[k] += c[k]
+        res[name] = tot
+    return {
+        "streams": list(streams), "rows_per_stream": middle, "K": res["K"], "V": res["V"],
+        "rows_checked": res["K"]["rows_checked"] + res["V"]["rows_checked"],
+        "mismatches": res["K"]["mismatches"] + res["V"]["mismatches"],
+        "near_ties": res["K"]["near_ties"] + res["V"]["near_ties"],
+        "norm_mismatches": res["K"]["norm_mismatches"] + res["V"]["norm_mismatches"],
+        "tau": "2^-14 ||r|| max||e|| + 2^-22 max(|s1|,|s2|) at the first differing stage (SURVEY.md 8c)",
+        "bar": "codes bit-exact except counted near-ties; residual norms bit-exact (0 ULP)",
+        "checker": "oracle/vqkv_oracle.cpp (codebook.cpp:158-237 restated), host threads, outside the timed region",
+        "check_s": time.perf_counter() - t0,
+    }
 
 
 # --------------------------------------------------------------------------- clocks
@@ -316,15 +367,18 @@ def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
         kc = torch.randint(0, 256, (n_pairs, kb_ + 16), dtype=torch.uint8, device="cuda", generator=gen)[:, :kb_]
         vc = torch.randint(0, 256, (n_pairs, vb_ + 16), dtype=torch.uint8, device="cuda", generator=gen)[:, :vb_]
         kc, vc = kc.contiguous(), vc.contiguous()
-        # the key codes as DeviceCacheState keeps them for attention: the group-major mirror
-        # (transcoded once per flushed row at append time, outside the decode step)
+        # the key codes as DeviceCacheState keeps them: attention records (transcoded once per
+        # flushed row at append time, outside the decode step)
         cap = -(-max(n_comp_, 1) // Dv.GM_ALIGN) * Dv.GM_ALIGN
         kg = Dv.keycodes_to_gm(kst, kc, n_comp_, cap=cap)
+        kept["kc"] = kc[: args.parity_pairs].cpu().numpy()  # the checker's copy (CodeMatrix rows)
         del kc
         f = lambda n: (torch.randn(n_pairs, n, D, device="cuda", generator=gen) if n else None)
         return (kg, cap), vc, f(n_init_), f(n_init_), f(n_local_), f(n_local_)
 
+    kept = {}
     (kc, kcap), vc, ik, iv, lk, lv = make(pairs, n_comp, n_init, n_local)
+    kc_host = kept["kc"]
     q = torch.randn(pairs, G, D, device="cuda", generator=gen)
     run = lambda: Dv.attend_decode(kst, vst, q, kc, vc, n_comp, ik, iv, lk, lv, kcodes_gm_cap=kcap)
     for _ in range(max(1, args.warmup)):
@@ -347,12 +401,12 @@ def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
         "config": {"workload": "configs[2]: decode step, 128K-token VQ-compressed cache, batch 16, 8 KV heads "
                                f"sharded over {world} GPU(s), G=4", "context": ctx, "batch": B,
                    "kv_heads_per_gpu": len(heads), "compressed_rows": n_comp, "raw_rows": n_init + n_local,
-                   "key_code_layout": "group-major (the cache's attention mirror, same 70 B per token)"},
+                   "key_code_layout": "attention records (the cache's only key-code copy, 70 B per token)"},
         "value": B * ctx / (ms / 1e3), "unit": "tokens/s", "ms_per_layer_step": ms,
         "roofline": {"bound": "hbm", "achieved": bytes_rank / (ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                      "frac": bytes_rank / (ms / 1e3) / 1e9 / hbm,
                      "algorithmic": "88 B of codes per compressed token-pair + 1 KB per raw row (fp32 K+V)",
-                     "note": "on-chip bound: 56 LUT gathers + 16 histogram atomics per token-pair in shared memory"},
+                     "note": "on-chip bound: 56 conflict-free 16 B LUT reads per compressed token-pair from shared memory"},
     }
     # the kernel's own bound: shared-memory LUT gathers (main kernel, library profile hooks)
     L = _lib.load()
@@ -371,37 +425,45 @@ def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
     smem_peak = 128 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12  # TB/s: 128 B/clk/SM at max clock
     gathers = pairs * n_comp * kst.num_stages() * 16  # one 16 B LUT entry (4 heads) per (token, key stage)
     out["kernel_ms"] = {"lut_gemm": part["attend_lut_build"], "main": part["attend"], "combine": part["attend_combine"]}
-    out["onchip"] = {"bound": "shared-memory LUT gathers (main kernel)", "algorithmic_bytes": gathers,
+    out["onchip"] = {"bound": "shared-memory LUT reads (main kernel)", "algorithmic_bytes": gathers,
                      "achieved": gathers / (part["attend"] / 1e3) / 1e12, "peak": smem_peak, "unit": "TB/s",
                      "frac": gathers / (part["attend"] / 1e3) / 1e12 / smem_peak,
                      "note": "16 B per (compressed token-pair, key stage) at 128 B/clk/SM x 148 SMs x max clock; "
-                             "random LDS.128 gathers also pay ~1.8x bank-conflict wavefronts (profiles/r1_attention_ncu.md)"}
-    # opt-in int16 LUT (VQKV_ATTEND_INT16=1) on the same inputs: time and deviation from the fp32 LUT
+                             "rotated 8-stage rows make every LDS.128 conflict-free (1 wavefront per 8 lanes)"}
+    # checker (untimed): the first pairs' outputs against the oracle's attend (attention.cpp:26-69,
+    # double-precision online softmax over view_block order), every query head
     o32, _ = run()
-    os.environ["VQKV_ATTEND_INT16"] = "1"
-    try:
-        for _ in range(max(1, args.warmup)):
-            run()
-        torch.cuda.synchronize()
-        i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        i0.record()
-        for _ in range(args.steps):
-            run()
-        i1.record()
-        torch.cuda.synchronize()
-        ms16 = max_over_ranks(i0.elapsed_time(i1) / args.steps, world)
-        o16, _ = run()
-        torch.cuda.synchronize()
-        dev = float((o16 - o32).abs().amax(dim=-1).div(o32.abs().amax(dim=-1).clamp(min=1.0)).max())
-    finally:
-        os.environ.pop("VQKV_ATTEND_INT16", None)
-    out["int16_lut_opt_in"] = {
-        "ms_per_layer_step": ms16, "value": B * ctx / (ms16 / 1e3),
-        "hbm_frac": bytes_rank / (ms16 / 1e3) / 1e9 / hbm,
-        "max_dev_vs_fp32_lut": dev,
-        "note": "VQKV_ATTEND_INT16=1: int16 LUT, one scale per (pair, head), exact int32 sums; deviation = "
-                "max over rows of max|o16 - o32| / max(1, max|o32|) (tolerance vs the reference: 2^-7)",
-    }
+    if args.parity_pairs > 0:
+        try:
+            from concurrent.futures import ThreadPoolExecutor
+
+            from oracle import oracle as O
+
+            t_chk = time.perf_counter()
+            ok_, ov_ = oracle_stacks()
+            npp = min(args.parity_pairs, pairs)
+            host = lambda t: t[:npp].cpu().numpy() if t is not None else None
+            hq, hik, hiv, hlk, hlv = (host(t) for t in (q, ik, iv, lk, lv))
+            hvc = vc[:npp].cpu().numpy()
+            got = o32[:npp].cpu().numpy()
+
+            def one(pg):
+                pi, g = divmod(pg, G)
+                ref, _ = O.attend_segments(ok_, ov_, hik[pi], hiv[pi], kc_host[pi], hvc[pi], n_comp, hlk[pi], hlv[pi],
+                                           hq[pi, g])
+                return float(np.abs(got[pi, g] - ref).max() / max(1.0, float(np.abs(ref).max())))
+
+            with ThreadPoolExecutor(os.cpu_count() or 4) as ex:
+                devs = list(ex.map(one, range(npp * G)))
+            out["parity"] = {
+                "pairs_checked": npp, "queries_checked": npp * G, "tokens_per_query": ctx,
+                "max_dev": max(devs), "tol": 2.0 ** -7, "pass": bool(max(devs) <= 2.0 ** -7),
+                "metric": "max|o - o_ref| / max(1, max|o_ref|) per query (bf16-level bar 2^-7, SURVEY.md 8c)",
+                "checker": "oracle attend_segments (attention.cpp:26-69 over kv_cache.cpp:143-189 order), untimed",
+                "check_s": time.perf_counter() - t_chk,
+            }
+        except Exception as e:
+            out["parity"] = {"error": repr(e)}
     del kc, vc, ik, iv, lk, lv
     if world > 1:
         # configs[4]: 1M-token single sequence over the ranks, NCCL all-gather + LSE merge
@@ -555,6 +617,15 @@ def run_ours(args, rank, world, local):
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("encode_tc_kernel")
 
+    # ---- parity of the timed output (checker, untimed)
+    parity = None
+    if rank == 0 and args.parity_streams > 0:
+        try:
+            sids = sorted({0, ns - 1} if args.parity_streams == 2 else set(range(min(ns, args.parity_streams))))
+            parity = encode_parity(Kh, Vh, kp, vp, kn, vn, middle, sids)
+        except Exception as e:  # reported, never fatal for the headline line
+            parity = {"error": repr(e)}
+
     # ---- e2e through the public host-buffer API (H2D + encode + D2H each step)
     e2e = None
     if not args.no_e2e:
@@ -633,6 +704,16 @@ def run_ours(args, rank, world, local):
                          "l2_gather_tbps": gather / (d_ms / 1e3) / 1e12,
                          "note": "on-chip bound: one 512 B codebook-row gather from L2 per (vector, stage)"},
         }
+        if rank == 0 and args.parity_streams > 0:  # checker (untimed): 0 ULP on stream 0's rows
+            ok_, ov_ = oracle_stacks()
+            ref_k = ok_.reconstruct_block(kp[0].cpu().numpy(), middle, 0, rows_d)
+            ref_v = ov_.reconstruct_block(vp[0].cpu().numpy(), middle, 0, rows_d)
+            decode["parity"] = {
+                "rows_checked": 2 * rows_d,
+                "ulp_mismatches": int((dk[0].cpu().numpy().view(np.uint32) != ref_k.view(np.uint32)).sum()
+                                      + (dv[0].cpu().numpy().view(np.uint32) != ref_v.view(np.uint32)).sum()),
+                "bar": "0 ULP (ordered fp32 sums, codebook.cpp:208-223)",
+            }
         del dk, dv
     except Exception as e:  # reported, never fatal for the headline line
         decode = {"error": repr(e)}
@@ -683,6 +764,7 @@ def run_ours(args, rank, world, local):
                 "kernel_ms_per_step": enc_ms_per_step, "kernel_launches": int(enc_n.value),
             },
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": e2e,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),

@@ -180,15 +180,19 @@ typedef struct vqkv_attend_args {
 int vqkv_attend_decode(vqkv_stack_t key_stack, vqkv_stack_t value_stack, const vqkv_attend_args* args,
                        void* stream);
 
-/* Group-major key codes (no reference counterpart: a device-resident copy of the key
- * CodeMatrix rows laid out for the decode-attention kernel).  Per pair, per group g of
- * 4 key stages: cap records of 5 bytes -- the group's fields, as they sit in the row
- * (codebook.cpp:96-120), shifted to bit 0 -- stored as cap u32 words (bits 0-31) then
- * cap bytes (bits 32-39).  Needs D = 128 and every key stage <= 1024 entries; cap must
- * be a multiple of 16.  vqkv_keycodes_gm_bytes returns 0 when unsupported.
+/* Attention layout of key codes ("group-major records"; no reference counterpart: a
+ * device-resident form of the key CodeMatrix rows laid out for the decode-attention kernel,
+ * the same bytes per token at the paper geometry).  Per pair, per group g of 8 key stages:
+ * an 80-bit record per token t holding eight 10-bit fields, field k = the code of stage
+ * 8g + ((t & 7) ^ k) (0 past the last stage) -- the rotation makes the kernel's shared-memory
+ * LUT reads conflict-free -- stored as cap u64 words (record bits 0-63) then cap u16 words
+ * (bits 64-79).  Needs D = 128 and every key stage <= 1024 entries; cap must be a multiple of
+ * 16.  vqkv_keycodes_gm_bytes returns 0 when unsupported.
  * vqkv_keycodes_to_gm writes rows [src_row, src_row + count) of each pair's payload
  * (payload_stride bytes apart) to records [dst_row, dst_row + count) of each pair's
- * group-major buffer (gm_stride bytes apart, 0 = vqkv_keycodes_gm_bytes). */
+ * buffer (gm_stride bytes apart, 0 = vqkv_keycodes_gm_bytes).  vqkv_keycodes_from_gm is the
+ * inverse for records [0, count): it writes CodeMatrix payloads (codebook.cpp:96-120 bit layout,
+ * payload_stride bytes apart, 0 = dense) of `count` rows. */
 uint64_t vqkv_keycodes_gm_bytes(vqkv_stack_t key_stack, uint64_t cap);
 /* 1 when vqkv_attend_decode accepts args with kcodes_layout = VQKV_KEYCODES_GROUP_MAJOR
  * (the LUT attention path covers them), else 0. */
@@ -196,6 +200,9 @@ int vqkv_attend_gm_supported(vqkv_stack_t key_stack, vqkv_stack_t value_stack, c
 int vqkv_keycodes_to_gm(vqkv_stack_t key_stack, const uint8_t* payload_dev, uint64_t payload_stride, uint32_t n_pairs,
                         uint64_t src_row, uint64_t count, uint8_t* gm_dev, uint64_t cap, uint64_t gm_stride,
                         uint64_t dst_row, void* stream);
+int vqkv_keycodes_from_gm(vqkv_stack_t key_stack, const uint8_t* gm_dev, uint64_t cap, uint64_t gm_stride,
+                          uint32_t n_pairs, uint64_t count, uint8_t* payload_dev, uint64_t payload_stride,
+                          void* stream);
 
 /* CodeMatrix::append of whole packed blocks (codebook.cpp:96-120), batched over
  * streams: for each stream i, bits [0, src_bits) of src + i*src_stride are

@@ -323,6 +323,33 @@ class Stack:
         )
         return payload[: pb * n_streams], norms[: n_streams * rows_per_stream]
 
+    def quantize_rows_instrumented_mt(self, xs, threads=None, chunk=256, search_block=4096):
+        """quantize_batch of every row (codebook.cpp:225-237) with the per-stage instrumentation
+        the near-tie rule needs, spread over host threads (ctypes releases the GIL; rows are
+        independent, codebook.cpp:230-235).  Returns (codes [rows, n] u32, norms [rows],
+        dict(best, second, rnorm) [rows, n])."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        xs = f32(xs)
+        rows = xs.shape[0]
+        threads = threads or (os.cpu_count() or 1)
+        codes = np.empty((rows, self.n), np.uint32)
+        norms = np.empty(rows, np.float32)
+        best = np.empty((rows, self.n), np.float32)
+        second = np.empty((rows, self.n), np.float32)
+        rn = np.empty((rows, self.n), np.float32)
+
+        def one(r0):
+            r1 = min(rows, r0 + chunk)
+            pay, nrm, ins = self.quantize_batch(xs[r0:r1], search_block, instrument=True)
+            codes[r0:r1] = self.unpack(pay, r1 - r0)
+            norms[r0:r1] = nrm
+            best[r0:r1], second[r0:r1], rn[r0:r1] = ins["best"], ins["second"], ins["rnorm"]
+
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(one, range(0, rows, chunk)))
+        return codes, norms, dict(best=best, second=second, rnorm=rn)
+
     def reconstruct_block(self, payload, rows, begin, end):
         payload = np.ascontiguousarray(payload, np.uint8)
         if payload.size == 0:
@@ -476,3 +503,30 @@ def attend_segments(kst: Stack, vst: Stack, init_k, init_v, kpay, vpay, n_comp, 
         )
     )
     return out, lse.value
+
+
+def near_tie_tau(best, second, rnorm, emax):
+    """tau = 2^-14 ||r|| max||e|| + 2^-22 max(|s1|, |s2|)."""
+    return 2.0 ** -14 * rnorm * emax + 2.0 ** -22 * np.maximum(np.abs(best), np.abs(second))
+
+
+def classify_codes(got, ref, ins, emax):
+    """Per-row code parity against the oracle (north_star: bit-exact except reference near-ties).
+
+    A row whose codes differ is a counted near-tie when, at its FIRST differing stage, the
+    oracle's best/second-best score gap is <= tau (later stages of such a row follow a different
+    residual and are excluded); otherwise it is a mismatch.
+    Returns dict(rows_checked, mismatches, near_ties, mismatch_rows)."""
+    got = np.asarray(got)
+    ref = np.asarray(ref)
+    bad = np.nonzero((got != ref).any(axis=1))[0]
+    ties, mism = 0, []
+    for r in bad:
+        st = int(np.nonzero(got[r] != ref[r])[0][0])
+        gap = float(ins["second"][r, st]) - float(ins["best"][r, st])
+        tau = float(near_tie_tau(ins["best"][r, st], ins["second"][r, st], ins["rnorm"][r, st], emax[st]))
+        if gap <= tau:
+            ties += 1
+        else:
+            mism.append(int(r))
+    return dict(rows_checked=int(got.shape[0]), mismatches=len(mism), near_ties=ties, mismatch_rows=mism[:16])

@@ -85,6 +85,10 @@ _SIGS = {
         C.c_int,
         [P, P, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, P, C.c_uint64, C.c_uint64, C.c_uint64, P],
     ),
+    "vqkv_keycodes_from_gm": (
+        C.c_int,
+        [P, P, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, P, C.c_uint64, P],
+    ),
     "vqkv_profile_enable": (C.c_int, [C.c_int]),
     "vqkv_profile_collect": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), u64p]),
     "vqkv_generate_synthetic": (

@@ -13,10 +13,12 @@ buffers with `vqkv_payload_append`; pending + local rows share one contiguous ra
 of 2 * local_len rows, so a flush is one batched encode of the first `pending` rows
 (kv_cache.cpp:102-120) and attention reads every segment in place (strided views, no copies).
 
-Key codes are also kept in the group-major attention layout (include/vqkv_c.h,
-vqkv_keycodes_to_gm) when the key stack has one: each flush transcodes its new rows once, and
-decode attention stages that layout by bulk copy instead of re-reading CodeMatrix rows per LUT
-group.  The CodeMatrix payload stays the source of truth (codes, view_block, snapshots).
+When the key stack has an attention layout (D = 128, <= 1024 entries per stage) the key codes
+are kept ONLY as attention records (include/vqkv_c.h, vqkv_keycodes_to_gm: 10 B per token and
+group of 8 key stages, the CodeMatrix row's 70 B at the paper geometry): each flush transcodes its
+new rows once, decode attention reads them directly, and the CodeMatrix rows the reference API
+exposes (codes, view_block, fidelity, snapshots) are rebuilt on demand by vqkv_keycodes_from_gm.
+Value codes stay CodeMatrix rows (the attention kernel reads them as they are).
 
 Semantics follow the reference exactly: prefill split (kv_cache.cpp:61-100), eviction to
 pending and deferred (or eager) flush at local_len pending rows (:122-141), token order of
@@ -92,31 +94,41 @@ class DeviceCacheState:
 
     def _grow(self, rows: int) -> None:
         """Make room for `rows` compressed rows per stream (capacity doubles)."""
-        if rows <= self.cap_rows and self.kpay is not None:
+        if rows <= self.cap_rows and self.vpay is not None:
             return
         cap = max(rows, 2 * self.cap_rows, 1024)
-        kb, vb = self.kd.payload_bytes(cap), self.vd.payload_bytes(cap)
+        vb = self.vd.payload_bytes(cap)
         # zero-filled: payload_append ORs into the first partial byte
-        kpay = torch.zeros((self.n_streams, kb), dtype=torch.uint8, device=self.device)
         vpay = torch.zeros((self.n_streams, vb), dtype=torch.uint8, device=self.device)
         knorm = torch.zeros((self.n_streams, cap), dtype=torch.float32, device=self.device)
         vnorm = torch.zeros((self.n_streams, cap), dtype=torch.float32, device=self.device)
-        if self.kpay is not None and self.n_comp:
-            ob, ovb = self.kd.payload_bytes(self.n_comp), self.vd.payload_bytes(self.n_comp)
-            kpay[:, :ob] = self.kpay[:, :ob]
+        if self.vpay is not None and self.n_comp:
+            ovb = self.vd.payload_bytes(self.n_comp)
             vpay[:, :ovb] = self.vpay[:, :ovb]
             knorm[:, : self.n_comp] = self.knorm[:, : self.n_comp]
             vnorm[:, : self.n_comp] = self.vnorm[:, : self.n_comp]
-        self.kpay, self.vpay, self.knorm, self.vnorm, self.cap_rows = kpay, vpay, knorm, vnorm, cap
-        if self.attn_layout == "group_major":  # records depend on the capacity: rebuild from the payload
-            self.gm_cap = -(-cap // Dv.GM_ALIGN) * Dv.GM_ALIGN
-            self.kgm = torch.zeros((self.n_streams, Dv.keycodes_gm_bytes(self.kd, self.gm_cap)), dtype=torch.uint8,
-                                   device=self.device)
-            self._rebuild_gm()
-
-    def _rebuild_gm(self) -> None:
-        if self.kgm is not None and self.n_comp:
-            Dv.keycodes_to_gm(self.kstack, self.kpay, self.n_comp, gm=self.kgm, cap=self.gm_cap)
+        if self.attn_layout == "group_major":
+            # the key codes live ONLY as attention records: per key group a u64 plane and a u16
+            # plane of gm_cap tokens each; growing copies the first n_comp tokens of every plane
+            gm_cap = -(-cap // Dv.GM_ALIGN) * Dv.GM_ALIGN
+            ng = Dv.keycodes_gm_bytes(self.kd, Dv.GM_ALIGN) // (10 * Dv.GM_ALIGN)
+            kgm = torch.zeros((self.n_streams, Dv.keycodes_gm_bytes(self.kd, gm_cap)), dtype=torch.uint8,
+                              device=self.device)
+            if self.kgm is not None and self.n_comp:
+                n, oc = self.n_comp, self.gm_cap
+                old = self.kgm.view(self.n_streams, ng, oc * 10)
+                new = kgm.view(self.n_streams, ng, gm_cap * 10)
+                new[:, :, : n * 8] = old[:, :, : n * 8]
+                new[:, :, gm_cap * 8: gm_cap * 8 + n * 2] = old[:, :, oc * 8: oc * 8 + n * 2]
+            self.kgm, self.gm_cap = kgm, gm_cap
+        else:
+            kb = self.kd.payload_bytes(cap)
+            kpay = torch.zeros((self.n_streams, kb), dtype=torch.uint8, device=self.device)
+            if self.kpay is not None and self.n_comp:
+                ob = self.kd.payload_bytes(self.n_comp)
+                kpay[:, :ob] = self.kpay[:, :ob]
+            self.kpay = kpay
+        self.vpay, self.knorm, self.vnorm, self.cap_rows = vpay, knorm, vnorm, cap
 
     def _encode_append(self, keys: torch.Tensor, values: torch.Tensor) -> None:
         """quantize_batch of [S, n, D] rows and CodeMatrix::append of the result."""
@@ -127,11 +139,14 @@ class DeviceCacheState:
         kp, kn = Dv.quantize_streams(self.kstack, keys.contiguous())
         vp, vn = Dv.quantize_streams(self.vstack, values.contiguous())
         stream = Dv._stream(keys)
-        for pay, src, rb in ((self.kpay, kp, self.kd.row_bits), (self.vpay, vp, self.vd.row_bits)):
+        appends = [(self.vpay, vp, self.vd.row_bits)]
+        if self.kgm is not None:  # key rows -> attention records at token n_comp
+            Dv.keycodes_to_gm(self.kstack, kp, n, gm=self.kgm, cap=self.gm_cap, dst_row=self.n_comp)
+        else:
+            appends.append((self.kpay, kp, self.kd.row_bits))
+        for pay, src, rb in appends:
             _lib.call("vqkv_payload_append", pay.data_ptr(), pay.stride(0), self.n_comp * rb, src.data_ptr(),
                       src.stride(0), n * rb, self.n_streams, stream)
-        if self.kgm is not None:
-            Dv.keycodes_to_gm(self.kstack, kp, n, gm=self.kgm, cap=self.gm_cap, dst_row=self.n_comp)
         self.knorm[:, self.n_comp: self.n_comp + n] = kn
         self.vnorm[:, self.n_comp: self.n_comp + n] = vn
         self.n_comp += n
@@ -227,13 +242,17 @@ class DeviceCacheState:
         return keys, values, exact
 
     def _payload(self, which: int) -> torch.Tensor:
+        """CodeMatrix payload [S, payload_bytes(compressed)] of keys (0) / values (1); the key
+        payload is rebuilt from the attention records when the cache keeps only those."""
+        if which == 0 and self.kgm is not None:
+            return Dv.keycodes_from_gm(self.kstack, self.kgm, self.gm_cap, self.n_comp)
         st, pay = (self.kd, self.kpay) if which == 0 else (self.vd, self.vpay)
         return pay[:, : max(st.payload_bytes(self.n_comp), 1)]
 
     def codes(self, which: int) -> Tuple[torch.Tensor, torch.Tensor]:
         """(payload [S, payload_bytes(compressed)] u8, residual norms [S, compressed]) of keys (0) / values (1)."""
         st = self.kd if which == 0 else self.vd
-        pay = (self.kpay if which == 0 else self.vpay)[:, : st.payload_bytes(self.n_comp)]
+        pay = self._payload(which)[:, : st.payload_bytes(self.n_comp)]
         nrm = (self.knorm if which == 0 else self.vnorm)[:, : self.n_comp]
         return pay, nrm
 
@@ -245,9 +264,10 @@ class DeviceCacheState:
         return dict(raw_bytes_equivalent=self.total_len() * spt * 2, compressed_payload_bits=bits,
                     codebook_overhead_bytes=self.kd.serialized_bytes() + self.vd.serialized_bytes(),
                     effective_ratio=ratio,
-                    # device-only: the group-major key-code mirror (5 B per token per 4 key stages)
-                    attention_layout_bytes=self.n_comp * 5 * (-(-self.kd.n // 4))
-                    if self.kgm is not None else 0)
+                    # device bytes per stream holding the compressed codes: key attention records
+                    # (10 B per token and group of 8 key stages) or CodeMatrix rows, + value rows
+                    device_code_bytes=(self.n_comp * 10 * (-(-self.kd.n // 8)) if self.kgm is not None
+                                       else self.kd.payload_bytes(self.n_comp)) + self.vd.payload_bytes(self.n_comp))
 
     def attend(self, q: torch.Tensor, scale: float = 0.0, want_lse: bool = True):
         """Decode-step attention for q [S, G, Dk] over every segment, read in place
@@ -259,7 +279,8 @@ class DeviceCacheState:
               and Dv.attend_gm_supported(self.kstack, self.vstack, self.n_streams, q.shape[1], ni, self.n_comp, nt))
         return Dv.attend_decode(
             self.kstack, self.vstack, q,
-            (self.kgm if gm else self.kpay) if self.n_comp else None, self.vpay if self.n_comp else None, self.n_comp,
+            (self.kgm if gm else self._payload(0)) if self.n_comp else None, self.vpay if self.n_comp else None,
+            self.n_comp,
             self.init_k[:, :ni] if ni else None, self.init_v[:, :ni] if ni else None,
             self.tail_k[:, :nt] if nt else None, self.tail_v[:, :nt] if nt else None,
             scale=scale, want_lse=want_lse, kcodes_gm_cap=self.gm_cap if gm else 0)
@@ -462,8 +483,12 @@ class DeviceCacheState:
             cache.init_k[:, :ni] = t([d["init"][0] for d in parsed])
             cache.init_v[:, :ni] = t([d["init"][1] for d in parsed])
         if nc:
-            kb, vb = cache.kd.payload_bytes(nc), cache.vd.payload_bytes(nc)
-            cache.kpay[:, :kb] = t([d["codes"][0].payload() for d in parsed])
+            vb = cache.vd.payload_bytes(nc)
+            kp = t([d["codes"][0].payload() for d in parsed])
+            if cache.kgm is not None:
+                Dv.keycodes_to_gm(key_stack, kp, nc, gm=cache.kgm, cap=cache.gm_cap)
+            else:
+                cache.kpay[:, : kp.shape[1]] = kp
             cache.vpay[:, :vb] = t([d["codes"][1].payload() for d in parsed])
             cache.knorm[:, :nc] = t([d["norms"][0] for d in parsed])
             cache.vnorm[:, :nc] = t([d["norms"][1] for d in parsed])
@@ -474,5 +499,4 @@ class DeviceCacheState:
                 cache.tail_v[:, a:b] = t([d[src][1] for d in parsed])
         cache.n_init, cache.n_comp, cache.n_tail = ni, nc, npd + nl
         cache.prefilled, cache.batched = first["prefilled"], first["batched"]
-        cache._rebuild_gm()
         return cache

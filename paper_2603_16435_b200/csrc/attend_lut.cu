@@ -1,5 +1,5 @@
-// attend_lut.cu -- K3 fast path: decode-step attention over the compressed
-// cache in the dot-product domain (D = 128, G = 4 query heads per KV head).
+// attend_lut.cu -- K3: decode-step attention over the compressed cache in the
+// dot-product domain (D = 128, G = 4 query heads per KV head).
 //
 // Reference: attend (proj/core/src/attention.cpp:26-69) over
 // CacheState::view_block (kv_cache.cpp:143-189), whose compressed rows are
@@ -10,18 +10,49 @@
 // so keys cost one table lookup per (token, stage) and values one histogram
 // update per (token, stage); neither K nor V rows are ever materialised.
 //
-// Kernels (one launch each, all on the caller's stream):
-//   lut_kernel      LUT[pair][s][j] = float4 over g, fp32 (FFMA from the
-//                   fp32 effective entries; the table stays L2-hot per pair)
-//   attend_lut      CTA = (pair, split of <= 8192 compressed tokens):
-//                   keys: 4-stage LUT groups double-buffered into smem by bulk
-//                   copy (TMA engine), one LDS.128 + 4 FADD per (token, stage);
-//                   split max; p = exp(logit - max); values: int32 fixed-point
-//                   (2^-18) smem histograms via native shared atomics;
-//                   writes (H as fp32, m, l).  One extra CTA per pair handles
-//                   the raw init/local rows directly (o_acc, m, l).
-//   lut_combine     per pair: merge splits by LSE weights, contract H with the
-//                   value codebooks, add the raw part, normalise, emit lse.
+// Layouts (all per (sequence, KV head) pair):
+//   LUT      fp32, key stages in groups of 8: [group][j < R][slot 8][head 4] -- one
+//            128 B row per code value j holds the 8 stages' float4 entries.
+//   key codes ("attention records", vqkv_keycodes_to_gm): per group of 8 key stages
+//            and token t an 80-bit record of eight 10-bit fields, ROTATED: field k
+//            holds the code of stage slot (t & 7) ^ k.  Stored as two planes per group,
+//            cap x u64 (record bits 0-63) then cap x u16 (bits 64-79): 10 B per token
+//            and group, the CodeMatrix row's 70 B at the paper geometry.
+//   value codes: the reference CodeMatrix rows (codebook.cpp:74-151), unchanged.
+//
+// Why the rotation: the lanes of a warp hold consecutive tokens, so in one LDS.128
+// the 8 lanes of a quarter-warp read slots (lane & 7) ^ k -- 8 distinct 16 B bank
+// groups of the 128 B rows whatever the codes are.  Every key lookup is a
+// conflict-free wavefront (the round-1 layout lost 56 % of its wavefronts to bank
+// conflicts of random LDS.128 gathers).
+//
+// Kernels (one launch each, on the caller's stream):
+//   q_prep + lut_tc  the LUT GEMM on tcgen05 (split fp16, fp32 accumulate) -> fp32 LUT
+//   attend_atr       CTA = (pair, contiguous token range), 512 threads, chunks of 8192
+//                    tokens (16 per thread, logits in registers):
+//                      keys   - per LUT group: one 128 KB bulk copy (TMA engine) of the
+//                               group's rows into smem; per token 8 x (SHF, LOP3,
+//                               LDS.128, 2 FADD2) from the thread's 10 B record;
+//                      softmax- chunk max m_c, p = exp(l - m_c), l_c = sum p (fp32);
+//                      values - p in fixed point with quantum u_c = l_c 2^-28 (a
+//                               RELATIVE quantum: see the bound below); per token with a
+//                               nonzero weight the warp updates the 16 stages x 4 heads
+//                               of int32 smem histograms, lane = (stage slot, head), so
+//                               each ATOMS hits 32 distinct banks;
+//                      fold   - H into the CTA's fp32 accumulator (global, L2-resident)
+//                               rescaled to the running max (online softmax);
+//                    after the last chunk the CTA contracts its accumulator with the
+//                    value codebooks (o = sum H e) and writes (o, m, l).
+//                    One more CTA per pair attends the raw init/local rows directly.
+//   combine          per pair: LSE merge of its CTAs' partials, normalise, emit lse.
+//
+// Value-path error bound (rigorous).  In a chunk of n_c <= 8192 tokens the histogram
+// rounds each p_t to a multiple of u_c = l_c 2^-28 (round to nearest, |err| <= u_c/2;
+// tokens below u_c/2 round to 0 and are skipped).  The normaliser uses the exact fp32
+// l.  With chunk weights exp(m_c - M) and L = sum_c l_c exp(m_c - M):
+//     |o' - o|_inf <= sum_c n_c (u_c/2) exp(m_c - M) max_t|v_t|_inf / L
+//                  <= 8192 * 2^-29 * max_t|v_t|_inf = 2^-16 max_t|v_t|_inf,
+// independent of how flat or peaked the attention is (no absolute cut).
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -33,22 +64,23 @@ namespace vqkv_dev {
 
 namespace {
 
-constexpr int kG = 4;              // query heads per KV head on this path
-constexpr int kD = 128;            // head dim
-constexpr int kAttThreads = 512;
-constexpr int kTokPerThread = 16;
-constexpr int kSplitTokens = kAttThreads * kTokPerThread;  // 8192
-constexpr int kMaxVStages = 64;    // value stages supported by the LUT path
-constexpr int kKeyBatch = 4;
-constexpr uint32_t kQueueCap = 64;                       // per-warp value-token queue entries
-constexpr uint32_t kQueueOff = 131072 + 1024;             // smem offset of the queues (after the control area)
-constexpr uint32_t kMainSmem = kQueueOff + (kAttThreads / 32) * kQueueCap * (1 + 4) * 4;      // key tokens whose code loads are in flight together
-constexpr int kGroupStages = 4;    // LUT stages per smem buffer (4 x 16 KB)
-constexpr uint32_t kGmCodeOff = 131072 + 1024;               // == kQueueOff: queues are used after the keys
-constexpr uint32_t kGmCodeBuf = 5 * kSplitTokens;              // one group's records of a split (40 KB)
-constexpr uint32_t kAlignSlack = 16384 - 1024;                 // 1 KB-aligned window start -> 16 KB alignment
-constexpr uint32_t kGmSmem = kGmCodeOff + 2 * kGmCodeBuf;
-constexpr float kHistScale = 262144.0f;  // 2^18 fixed point for p in [0, 1]
+constexpr int kG = 4;                          // query heads per KV head on this path
+constexpr int kD = 128;                        // head dim
+constexpr int kThreads = 512;
+constexpr int kTok = 16;                       // tokens per thread per chunk
+constexpr int kChunk = kThreads * kTok;        // 8192 tokens per chunk
+constexpr int kGS = 8;                         // key stages per LUT group (one 128 B row)
+constexpr uint32_t kRowBytes = kGS * 16;       // 8 slots x float4
+constexpr uint32_t kLutBytes = 1024 * kRowBytes;  // 128 KB: one group, up to 1024 code values
+constexpr uint32_t kMaxVHalves = 8;            // value stages <= 64
+constexpr uint32_t kSmemCtl = 16384;           // barriers, reductions, value descriptors (raw CTAs: 10 KB)
+constexpr uint32_t kMainSmem = kLutBytes + kSmemCtl;
+constexpr float kQuantum = 268435456.0f;       // 2^28: p / u_c = p * 2^28 / l_c
+
+// LUT element offset (in float4) of (pair, stage s, code j)
+__host__ __device__ __forceinline__ uint64_t lut_off(uint64_t pair, uint32_t ng, uint32_t R, uint32_t s, uint32_t j) {
+    return ((pair * ng + (s >> 3)) * R + j) * kGS + (s & 7u);
+}
 
 struct LutArgs {
     const float* q;        // [pairs][G][D]
@@ -57,16 +89,17 @@ struct LutArgs {
     uint32_t kn;
     uint64_t kentries;     // total key entries (sum S)
     float scale;
-    float4* lut;           // [pairs][kentries]
+    float4* lut;           // grouped layout (lut_off)
+    uint32_t ng, R;
 };
 
-// LUT[pair][e] = scale * q_g . E[e] for all key entries e (stage-concatenated).
-// CTA: 128 entries x 8 pairs, 256 threads; thread = 4 entries x 4 queries of one pair.
+// FFMA fallback of the LUT build (entries too large for the fp16 split operands).
+// CTA: 128 entries (stage-concatenated) x 8 pairs, 256 threads; thread = 4 entries x 4 queries.
 constexpr int kLutEntries = 128;
-constexpr int kLutStride = kD + 2;  // even row stride: 8 B-aligned float2 reads, 2 wavefronts per warp load
+constexpr int kLutStride = kD + 2;  // even row stride: 8 B-aligned float2 reads
 __global__ void __launch_bounds__(256) lut_kernel(LutArgs a, uint32_t n_pairs) {
     extern __shared__ float lsm[];
-    float4* qs = reinterpret_cast<float4*>(lsm);  // [8 pairs][D] x float4 over g: one LDS.128 per dim
+    float4* qs = reinterpret_cast<float4*>(lsm);  // [8 pairs][D] x float4 over g
     float* es = lsm + 8 * kG * kD;                // [128 entries][kLutStride]
     const uint32_t e0 = blockIdx.x * kLutEntries, p0 = blockIdx.y * 8;
     for (uint32_t i = threadIdx.x; i < 8 * kD; i += blockDim.x) {
@@ -91,11 +124,10 @@ __global__ void __launch_bounds__(256) lut_kernel(LutArgs a, uint32_t n_pairs) {
     const float4* qp = qs + p * kD;
 #pragma unroll 4
     for (int c = 0; c < kD; c += 2) {
-        const float4 q0 = qp[c], q1 = qp[c + 1];  // broadcast within the warp
+        const float4 q0 = qp[c], q1 = qp[c + 1];
         float2 ev[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) ev[i] = *reinterpret_cast<const float2*>(es + (eg + 32 * i) * kLutStride + c);
-        // packed FFMA2 over head pairs: per lane the same fmaf sequence as scalar code
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             float2* a2 = reinterpret_cast<float2*>(acc[i]);
@@ -110,10 +142,21 @@ __global__ void __launch_bounds__(256) lut_kernel(LutArgs a, uint32_t n_pairs) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const uint32_t e = e0 + eg + 32 * i;
-            if (e < a.kentries)
-                a.lut[uint64_t(p0 + p) * a.kentries + e] = make_float4(acc[i][0] * a.scale, acc[i][1] * a.scale,
-                                                                        acc[i][2] * a.scale, acc[i][3] * a.scale);
+            if (e < a.kentries) {
+                uint32_t s = 0;  // stage of entry e (stages are few; scan)
+                while (s + 1 < a.kn && e >= uint32_t(a.kst[s + 1].eff_off / kD)) ++s;
+                const uint32_t j = e - uint32_t(a.kst[s].eff_off / kD);
+                a.lut[lut_off(p0 + p, a.ng, a.R, s, j)] = make_float4(acc[i][0] * a.scale, acc[i][1] * a.scale,
+                                                                      acc[i][2] * a.scale, acc[i][3] * a.scale);
+            }
         }
+}
+
+// slots of a partial last group (stages that do not exist) are read with code 0: zero row 0
+__global__ void lut_zero_missing_kernel(float4* lut, uint32_t ng, uint32_t R, uint32_t kn) {
+    const uint32_t pair = blockIdx.x, slot = threadIdx.x;
+    const uint32_t s = (ng - 1) * kGS + slot;
+    if (slot < kGS && s >= kn) lut[lut_off(pair, ng, R, s, 0)] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // ---- LUT build on the tensor cores --------------------------------------------------------
@@ -161,7 +204,7 @@ constexpr uint32_t kLutTcSmem = 6 * 32768 + 1024;
 __global__ void __launch_bounds__(160) lut_tc_kernel(const __half* __restrict__ eff16, const __half* __restrict__ eff16lo,
                                                      const StageInfo* __restrict__ kst, const __half* __restrict__ qhi,
                                                      const __half* __restrict__ qlo, const float* __restrict__ qscl,
-                                                     uint32_t n_pairs, uint32_t n_qtiles, uint64_t kentries,
+                                                     uint32_t n_pairs, uint32_t n_qtiles, uint32_t ng, uint32_t R,
                                                      float4* __restrict__ lut) {
     extern __shared__ uint8_t lsm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(lsm_raw) + 1023) & ~uintptr_t(1023));
@@ -231,7 +274,6 @@ __global__ void __launch_bounds__(160) lut_tc_kernel(const __half* __restrict__ 
         }
     } else {
         const uint32_t j = c * 128 + warp * 32 + lane;  // entry within the stage
-        const uint64_t e = si.eff_off / kD + j;
         for (uint32_t tq = 0; tq < n_qtiles; ++tq) {
             const uint32_t b = tq & 1, use = tq >> 1;
             ptx::mbar_wait(ptx::smem_u32(&bar_mma[b]), use & 1);
@@ -250,7 +292,7 @@ __global__ void __launch_bounds__(160) lut_tc_kernel(const __half* __restrict__ 
                     const uint32_t pair = tq * 32 + c4 * 8 + pp;
                     if (j < si.size && pair < n_pairs) {
                         const float4 sc = __ldg(reinterpret_cast<const float4*>(sclp) + c4 * 8 + pp);
-                        lut[uint64_t(pair) * kentries + e] = (
+                        lut[lut_off(pair, ng, R, blockIdx.y, j)] = (
                                make_float4(v[c4][4 * pp] * sc.x, v[c4][4 * pp + 1] * sc.y, v[c4][4 * pp + 2] * sc.z,
                                            v[c4][4 * pp + 3] * sc.w));
                     }
@@ -260,71 +302,6 @@ __global__ void __launch_bounds__(160) lut_tc_kernel(const __half* __restrict__ 
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 0) ptx::tmem_dealloc(tmem, 256);
-}
-
-// ---- int16 LUT (opt-in, VQKV_ATTEND_INT16=1) -------------------------------------------
-// One scale per (pair, head): Δ = max_e |LUT[e][g]| / 32767, entries stored as biased u16
-// (round(L / Δ) + 32768, 4 heads in 8 B) and summed exactly in int32 by the main kernel (GM = 2):
-// per-logit error ≤ n_stages · Δ / 2 against the fp32 LUT.
-// CTA = pair: max_e |LUT[e][g]| over the pair's fp32 LUT, then the quantised copy (the second
-// read of the pair's 0.9 MB hits L2).
-__global__ void __launch_bounds__(1024) lut_int16_kernel(const float4* __restrict__ lut, uint64_t kentries,
-                                                         uint2* __restrict__ lut16, float* __restrict__ dq) {
-    __shared__ float red[32][kG];
-    __shared__ float smax[kG];
-    const uint32_t pair = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const float4* L = lut + uint64_t(pair) * kentries;
-    constexpr int kU = 8;  // loads in flight per thread
-    float m[kG] = {0.f, 0.f, 0.f, 0.f};
-    for (uint64_t e0 = threadIdx.x; e0 < kentries; e0 += uint64_t(kU) * blockDim.x) {
-        float4 v[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const uint64_t e = e0 + uint64_t(u) * blockDim.x;
-            v[u] = e < kentries ? __ldg(L + e) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const float x[kG] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-            for (int g = 0; g < kG; ++g) m[g] = fmaxf(m[g], isfinite(x[g]) ? fabsf(x[g]) : INFINITY);  // non-finite -> NaN logits
-        }
-    }
-#pragma unroll
-    for (int g = 0; g < kG; ++g) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m[g] = fmaxf(m[g], __shfl_xor_sync(0xffffffffu, m[g], o));
-        if (lane == 0) red[warp][g] = m[g];
-    }
-    __syncthreads();
-    if (threadIdx.x < kG) {
-        float r = 0.f;
-        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) r = fmaxf(r, red[w][threadIdx.x]);
-        smax[threadIdx.x] = r;
-        dq[pair * kG + threadIdx.x] = r / 32767.0f;
-    }
-    __syncthreads();
-    float inv[kG];
-#pragma unroll
-    for (int g = 0; g < kG; ++g) inv[g] = smax[g] > 0.f ? 32767.0f / smax[g] : 0.f;
-    uint2* Q = lut16 + uint64_t(pair) * kentries;
-    for (uint64_t e0 = threadIdx.x; e0 < kentries; e0 += uint64_t(kU) * blockDim.x) {
-        float4 v[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const uint64_t e = e0 + uint64_t(u) * blockDim.x;
-            v[u] = e < kentries ? __ldg(L + e) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const uint64_t e = e0 + uint64_t(u) * blockDim.x;
-            const float x[kG] = {v[u].x, v[u].y, v[u].z, v[u].w};
-            uint32_t q[kG];
-#pragma unroll
-            for (int g = 0; g < kG; ++g) q[g] = uint32_t(max(-32767, min(32767, __float2int_rn(x[g] * inv[g]))) + 32768);
-            if (e < kentries) Q[e] = make_uint2(q[0] | q[1] << 16, q[2] | q[3] << 16);
-        }
-    }
 }
 
 // Reads 64 bits starting at bit `pos` of a byte stream: two aligned 64-bit
@@ -345,39 +322,36 @@ __device__ __forceinline__ uint64_t read_bits64(const uint8_t* base, uint64_t po
     return bsh ? ((v >> bsh) | (extra << (64 - bsh))) : v;
 }
 
-// always-valid 16 bytes: the target of clamped (ignored) loads in the batched key loop
-__device__ const uint64_t g_zero16[2] = {0ull, 0ull};
-
 struct MainArgs {
     const float* q;
     const float* init_k;
     const float* init_v;
     uint64_t n_init;
-    const uint8_t* kcodes;
-    const uint8_t* vcodes;
-    uint64_t n_comp;
     const float* local_k;
     const float* local_v;
     uint64_t n_local;
-    const StageInfo* kst;
-    uint32_t kn;
-    uint64_t krow_bits, kstream_bytes, kentries;
-    const StageInfo* vst;
-    uint32_t vn;
-    uint64_t vrow_bits, vstream_bytes, ventries;
-    const float4* lut;
-    const uint8_t* kend;
-    const uint8_t* vend;
-    float scale;
-    uint32_t n_splits;  // compressed splits per pair (+1 raw CTA)
-    float* part_h;      // [pairs][splits][ventries][G]
-    float* part_o;      // [pairs][G][D]  (raw CTA)
-    float* part_m;      // [pairs][splits+1][G]
-    float* part_l;      // [pairs][splits+1][G]
     uint64_t init_stride, local_stride;  // rows between pairs
-    uint64_t gm_cap;                     // group-major key codes: token capacity per group segment
-    const uint2* lut16;                  // GM = 2: int16 LUT (biased u16, 4 heads)
-    const float* dq;                     // GM = 2: [pairs][G] scale of the int16 LUT
+    float scale;
+    // keys: LUT + attention records
+    const float4* lut;
+    uint32_t ng, R;
+    const uint8_t* krec;     // records, krec_stride bytes between pairs, cap tokens per group segment
+    uint64_t krec_stride, cap;
+    // values: CodeMatrix rows
+    const uint8_t* vcodes;
+    uint64_t vstride, vrow_bits;
+    const uint8_t* vend;     // end of the last pair's value payload (reads stop here)
+    const StageInfo* vst;
+    uint32_t vn, vhalves, Rv;
+    const float* veff;
+    uint64_t n_comp;
+    uint32_t ctas_per_pair;  // main CTAs per pair
+    uint32_t n_main;         // main CTAs in the grid (raw CTAs follow)
+    uint64_t tok_per_cta;    // multiple of 512
+    float4* acc;             // per main CTA: fp32 histogram accumulator [vhalves][Rv][8 slots] x float4 (heads)
+    float* part_o;           // [n_main + pairs][G][D]: unnormalised sum p v
+    float* part_m;           // [n_main + pairs][G]
+    float* part_l;           // [n_main + pairs][G]
 };
 
 __device__ __forceinline__ float block_max(float v, float* red) {
@@ -401,15 +375,72 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
     return r;
 }
 
+
+// block-wide max / sum of 4 values per thread (one barrier pair for the 4 heads)
+__device__ __forceinline__ float4 block_max4(float4 v, float4* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x = fmaxf(v.x, __shfl_xor_sync(0xffffffffu, v.x, o));
+        v.y = fmaxf(v.y, __shfl_xor_sync(0xffffffffu, v.y, o));
+        v.z = fmaxf(v.z, __shfl_xor_sync(0xffffffffu, v.z, o));
+        v.w = fmaxf(v.w, __shfl_xor_sync(0xffffffffu, v.w, o));
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float4 r = red[0];
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+        const float4 x = red[w];
+        r = make_float4(fmaxf(r.x, x.x), fmaxf(r.y, x.y), fmaxf(r.z, x.z), fmaxf(r.w, x.w));
+    }
+    return r;
+}
+__device__ __forceinline__ float4 block_sum4(float4 v, float4* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+        v.z += __shfl_xor_sync(0xffffffffu, v.z, o);
+        v.w += __shfl_xor_sync(0xffffffffu, v.w, o);
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float4 r = red[0];
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+        const float4 x = red[w];
+        r = make_float4(r.x + x.x, r.y + x.y, r.z + x.z, r.w + x.w);
+    }
+    return r;
+}
+
+__device__ __forceinline__ void lds128(uint32_t addr, float2& a, float2& b) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y) : "r"(addr));
+}
+__device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ float4 ldcg4(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void stcg4(float4* p, float4 v) {
+    asm volatile("st.global.cg.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
 // raw init/local rows of one pair: direct fp32 attention (no codebooks).  Latency matters
-// here (one CTA per pair runs beside the split CTAs): rows are read in batches with all
+// here (one CTA per pair runs beside the main CTAs): rows are read in batches with all
 // their loads in flight, and every value load feeds the 4 heads.
-__device__ void raw_rows(const MainArgs& a, uint32_t pair, float* smem) {
+__device__ void raw_rows(const MainArgs& a, uint32_t pair, uint32_t slot, float* smem) {
     constexpr int kRowBatch = 8;
     float* red = smem;                 // 64
     float* qs = smem + 64;             // G*D
     float* ls = qs + kG * kD;          // logits / weights [n_raw][G] (n_raw <= 8192)
-    float* po = ls + kSplitTokens * kG;  // [4 row groups][G][D] partial outputs
+    float* po = ls + kChunk * kG;  // [4 row groups][G][D] partial outputs
     for (uint32_t i = threadIdx.x; i < kG * kD; i += blockDim.x) qs[i] = a.q[uint64_t(pair) * kG * kD + i];
     __syncthreads();
     const uint32_t n_raw = uint32_t(a.n_init + a.n_local);
@@ -462,8 +493,8 @@ __device__ void raw_rows(const MainArgs& a, uint32_t pair, float* smem) {
         }
         l = block_sum(l, red);
         if (threadIdx.x == 0) {
-            a.part_m[(uint64_t(pair) * (a.n_splits + 1) + a.n_splits) * kG + g] = m;
-            a.part_l[(uint64_t(pair) * (a.n_splits + 1) + a.n_splits) * kG + g] = l;
+            a.part_m[uint64_t(slot) * kG + g] = m;
+            a.part_l[uint64_t(slot) * kG + g] = l;
         }
     }
     __syncthreads();
@@ -502,514 +533,378 @@ __device__ void raw_rows(const MainArgs& a, uint32_t pair, float* smem) {
     for (uint32_t gd = threadIdx.x; gd < kG * kD; gd += blockDim.x) {
         float o = 0.f;
         for (uint32_t rg = 0; rg < nrg; ++rg) o += po[rg * kG * kD + gd];
-        a.part_o[uint64_t(pair) * kG * kD + gd] = o;
+        a.part_o[uint64_t(slot) * kG * kD + gd] = o;
     }
 }
 
-__device__ __forceinline__ void lds128(uint32_t addr, float2& a, float2& b) {
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y) : "r"(addr));
+// Field K (0..7) of an 80-bit attention record (w0 = bits 0-31, w1 = 32-63, w2 = 64-79),
+// shifted so its 10 bits sit at bits 7-16 (the code's row offset, 128 B per code); the bits
+// below are the previous field's and are masked off by the caller.  One SHF each.
+template <int K>
+__device__ __forceinline__ uint32_t field_at7(uint32_t w0, uint32_t w1, uint32_t w2) {
+    if constexpr (K == 0) return w0 << 7;
+    else if constexpr (K <= 3) return __funnelshift_r(w0, w1, 10 * K - 7);
+    else return __funnelshift_r(w1, w2, 10 * K - 39);
 }
 
-__device__ __forceinline__ void lds64(uint32_t addr, uint2& w) {
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y) : "r"(addr));
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// L2 prefetch of a chunk's records (both planes of one group segment), ahead of the LDGs
+__device__ __forceinline__ void ptx_prefetch_records(const uint8_t* seg, uint64_t cap, uint64_t c0, uint32_t n) {
+    const uint32_t lo = uint32_t(umin64((uint64_t(n) * 8u + 15u) & ~uint64_t(15), (cap - c0) * 8u));
+    const uint32_t hi = uint32_t(umin64((uint64_t(n) * 2u + 15u) & ~uint64_t(15), (cap - c0) * 2u));
+    if (lo) prefetch_l2_bulk(seg + c0 * 8u, lo);
+    if (hi) prefetch_l2_bulk(seg + cap * 8u + c0 * 2u, hi);
 }
 
-// GM = 1: key codes in the group-major layout (attend_lut.cu, "group-major key codes"):
-// per LUT group one bulk copy of the split's 5-byte records lands next to the LUT group,
-// so every code byte crosses L2 -> SM once, and a lookup is SHF + LOP3 + LDS.128 + 2 FADD2
-// (slot address = 16 KB-aligned stage slot | code << 4).  GM = 0: reference CodeMatrix rows,
-// re-read per LUT group through L1/L2 (any geometry the LUT path supports).
-template <int GM>
-__global__ void __launch_bounds__(kAttThreads, 1) attend_lut_kernel(MainArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const uint32_t pair = blockIdx.y, split = blockIdx.x;
+    const uint32_t cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     float* fsm = reinterpret_cast<float*>(smem_raw);
-    if (split == a.n_splits) {
+    if (cta >= a.n_main) {  // raw init/local rows of one pair
+        const uint32_t pair = cta - a.n_main;
         if (a.n_init + a.n_local > 0) {
-            raw_rows(a, pair, fsm);
-        } else if (threadIdx.x < kG) {
-            a.part_m[(uint64_t(pair) * (a.n_splits + 1) + a.n_splits) * kG + threadIdx.x] = -INFINITY;
-            a.part_l[(uint64_t(pair) * (a.n_splits + 1) + a.n_splits) * kG + threadIdx.x] = 0.f;
+            raw_rows(a, pair, cta, fsm);
+        } else if (tid < kG) {
+            a.part_m[uint64_t(cta) * kG + tid] = -INFINITY;
+            a.part_l[uint64_t(cta) * kG + tid] = 0.f;
         }
         return;
     }
-    // smem: [0, 128K) two LUT group buffers (2 x 4 stages x 1024 x 16 B) / value histograms
-    //       then mbarriers and reduction scratch
-    // the layout below starts at the first 16 KB-aligned shared address (the window
-    // starts after the 1 KB system reservation), so a LUT slot address is base | code << 4
-    uint8_t* const sm = smem_raw + ((16384u - (ptx::smem_u32(smem_raw) & 16383u)) & 16383u);
-    uint8_t* lut_buf = sm;
-    uint8_t* code_buf = sm + kGmCodeOff;  // GM: two record buffers (the value queues reuse them later)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 131072);
-    float* red = reinterpret_cast<float*>(sm + 131072 + 64);
-    const uint64_t t0 = uint64_t(split) * kSplitTokens;
-    const uint64_t nt = (a.n_comp - t0 < uint64_t(kSplitTokens)) ? (a.n_comp - t0) : uint64_t(kSplitTokens);
-    const uint8_t* kc = a.kcodes + uint64_t(pair) * a.kstream_bytes;
-    const uint8_t* vc = a.vcodes + uint64_t(pair) * a.vstream_bytes;
-    const float4* lutp = a.lut + uint64_t(pair) * a.kentries;
-    // 32-bit key-code addressing: bit positions relative to the 8 B-aligned start of the
-    // pair's stream (stream bit counts < 2^32 are checked on the host)
-    const uint64_t* kc64 = reinterpret_cast<const uint64_t*>(reinterpret_cast<uintptr_t>(kc) & ~uintptr_t(7));
-    const uint32_t kbase_bits = uint32_t((reinterpret_cast<uintptr_t>(kc) & 7u) * 8u);
-    const uint32_t kwords = uint32_t((reinterpret_cast<uintptr_t>(a.kend) - reinterpret_cast<uintptr_t>(kc64)) >> 3 > 0xffffffffull
-                                         ? 0xffffffffu
-                                         : (reinterpret_cast<uintptr_t>(a.kend) - reinterpret_cast<uintptr_t>(kc64)) >> 3);
-    const uint32_t krow32 = uint32_t(a.krow_bits);
-    const uint64_t* vc64 = reinterpret_cast<const uint64_t*>(reinterpret_cast<uintptr_t>(vc) & ~uintptr_t(7));
-    const uint32_t vbase_bits = uint32_t((reinterpret_cast<uintptr_t>(vc) & 7u) * 8u);
-    const uint32_t vwords = uint32_t((reinterpret_cast<uintptr_t>(a.vend) - reinterpret_cast<uintptr_t>(vc64)) >> 3 > 0xffffffffull
-                                         ? 0xffffffffu
-                                         : (reinterpret_cast<uintptr_t>(a.vend) - reinterpret_cast<uintptr_t>(vc64)) >> 3);
-    const uint32_t vrow32 = uint32_t(a.vrow_bits);
-    const uint32_t nvwin = (a.vn + 5u) / 6u;
-
-    float lg[kTokPerThread][kG];
-#pragma unroll
-    for (int k = 0; k < kTokPerThread; ++k)
-#pragma unroll
-        for (int g = 0; g < kG; ++g) lg[k][g] = 0.f;
-    // the key logits accumulate as head pairs with packed FADD2 (2 instructions per lookup)
-    float2 (*lg2)[2] = reinterpret_cast<float2 (*)[2]>(lg);
-    uint32_t il[GM == 2 ? kTokPerThread : 1][kG];  // GM = 2: exact sums of the biased int16 entries
-#pragma unroll
-    for (int k = 0; k < (GM == 2 ? kTokPerThread : 1); ++k)
-#pragma unroll
-        for (int g = 0; g < kG; ++g) il[k][g] = 0u;
-
-    // ---- keys: LUT groups of kGroupStages stages, double-buffered bulk copies
-    const uint32_t ngroups = (a.kn + kGroupStages - 1) / kGroupStages;
-    if (threadIdx.x == 0) {
-        ptx::mbar_init(ptx::smem_u32(&bars[0]), 1);
-        ptx::mbar_init(ptx::smem_u32(&bars[1]), 1);
+    const uint32_t pair = cta / a.ctas_per_pair, split = cta % a.ctas_per_pair;
+    const uint64_t t0 = uint64_t(split) * a.tok_per_cta;
+    const uint64_t t1 = min(a.n_comp, t0 + a.tok_per_cta);
+    uint8_t* const lutb = smem_raw;  // [0, 128 KB): one LUT group, then the chunk's value histograms
+    uint8_t* const ctl = smem_raw + kLutBytes;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ctl);
+    float4* red = reinterpret_cast<float4*>(ctl + 64);           // 16 x float4
+    uint32_t* vdesc = reinterpret_cast<uint32_t*>(ctl + 512);     // [halves][32 lanes]
+    uint32_t* vrow = vdesc + kMaxVHalves * 32;                    // [64]: first effective row of stage s
+    uint32_t* vsz = vrow + 64;                                    // [64]: stage sizes
+    const uint32_t HW = a.vhalves * a.Rv * 32u;                   // histogram words (x4 heads per quad)
+    if (tid == 0) {
+        ptx::mbar_init(ptx::smem_u32(bar), 1);
         ptx::fence_mbar_init();
     }
+    if (tid < a.vhalves * 32u) {  // lane (stage slot, head) of every half: the stage's field in the row
+        const uint32_t h = tid >> 5, s = h * 8u + ((tid & 31u) >> 2);
+        vdesc[tid] = (s < a.vn) ? (0x80000000u | (a.vst[s].bits << 16) | a.vst[s].bit_off) : 0u;
+    }
+    if (tid < a.vn) {
+        vrow[tid] = uint32_t(a.vst[tid].eff_off / kD);
+        vsz[tid] = a.vst[tid].size;
+    }
     __syncthreads();
-    auto issue = [&](uint32_t grp) {
-        const uint32_t b = grp & 1;
-        const uint32_t s0 = grp * kGroupStages;
-        const uint32_t s1 = min(a.kn, s0 + kGroupStages);
-        uint32_t bytes = 0;
-        for (uint32_t s = s0; s < s1; ++s) bytes += a.kst[s].size * 16u;
-        const uint32_t bar = ptx::smem_u32(&bars[b]);
-        if constexpr (GM == 2) {
-            // int16 LUT: stage q -> 8 KB slot q (entry = 4 biased u16); missing stages as in GM = 1
-            uint32_t hb = 0;
-            for (uint32_t st = s0; st < s1; ++st) hb += a.kst[st].size * 8u;
-            const uint32_t clo = uint32_t((nt * 4 + 15) & ~uint64_t(15)), chi = uint32_t((nt + 15) & ~uint64_t(15));
-            ptx::mbar_arrive_expect_tx(bar, hb + (kGroupStages - (s1 - s0)) * 16u + clo + chi);
-            const uint2* l16 = a.lut16 + uint64_t(pair) * a.kentries;
-            for (uint32_t st = s0; st < s0 + kGroupStages; ++st) {
-                uint8_t* dst = lut_buf + b * 65536 + (st - s0) * 8192;
-                if (st < s1)
-                    ptx::bulk_g2s(ptx::smem_u32(dst), l16 + a.kst[st].eff_off / kD, a.kst[st].size * 8u, bar);
-                else
-                    ptx::bulk_g2s(ptx::smem_u32(dst), g_zero16, 16u, bar);
-            }
-            const uint8_t* seg = kc + uint64_t(grp) * a.gm_cap * 5;
-            ptx::bulk_g2s(ptx::smem_u32(code_buf + b * kGmCodeBuf), seg + t0 * 4, clo, bar);
-            ptx::bulk_g2s(ptx::smem_u32(code_buf + b * kGmCodeBuf + 4 * kSplitTokens), seg + a.gm_cap * 4 + t0, chi, bar);
-        } else if constexpr (GM == 1) {
-            // stage q -> 16 KB slot q; a missing stage (partial last group) has code 0 and
-            // a zero entry 0; the split's records: lo32 words, then the high bytes
-            const uint32_t clo = uint32_t((nt * 4 + 15) & ~uint64_t(15)), chi = uint32_t((nt + 15) & ~uint64_t(15));
-            ptx::mbar_arrive_expect_tx(bar, bytes + (kGroupStages - (s1 - s0)) * 16u + clo + chi);
-            for (uint32_t s = s0; s < s0 + kGroupStages; ++s) {
-                uint8_t* dst = lut_buf + b * 65536 + (s - s0) * 16384;
-                if (s < s1)
-                    ptx::bulk_g2s(ptx::smem_u32(dst), lutp + a.kst[s].eff_off / kD, a.kst[s].size * 16u, bar);
-                else
-                    ptx::bulk_g2s(ptx::smem_u32(dst), g_zero16, 16u, bar);
-            }
-            const uint8_t* seg = kc + uint64_t(grp) * a.gm_cap * 5;
-            ptx::bulk_g2s(ptx::smem_u32(code_buf + b * kGmCodeBuf), seg + t0 * 4, clo, bar);
-            ptx::bulk_g2s(ptx::smem_u32(code_buf + b * kGmCodeBuf + 4 * kSplitTokens), seg + a.gm_cap * 4 + t0, chi, bar);
-        } else {
-            ptx::mbar_arrive_expect_tx(bar, bytes);
-            uint32_t off = 0;
-            for (uint32_t s = s0; s < s1; ++s) {
-                const uint32_t nb = a.kst[s].size * 16u;
-                ptx::bulk_g2s(ptx::smem_u32(lut_buf + b * 65536 + off), lutp + a.kst[s].eff_off / kD, nb, bar);
-                off += nb;
-            }
-        }
+
+    const uint32_t lut_s = ptx::smem_u32(lutb);
+    const float4* lutp = a.lut + uint64_t(pair) * a.ng * a.R * kGS;
+    const uint32_t grp_bytes = a.R * kRowBytes;
+    const uint32_t barp = ptx::smem_u32(bar);
+    auto issue = [&](uint32_t g) {  // one thread: the group's rows, one contiguous block
+        ptx::mbar_arrive_expect_tx(barp, grp_bytes);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(lutp + uint64_t(g) * a.R * kGS);
+        for (uint32_t off = 0; off < grp_bytes; off += 32768u)
+            ptx::bulk_g2s(lut_s + off, src + off, min(32768u, grp_bytes - off), barp);
     };
-    if (threadIdx.x == 0) issue(0);
-    for (uint32_t grp = 0; grp < ngroups; ++grp) {
-        if (threadIdx.x == 0 && grp + 1 < ngroups) issue(grp + 1);
-        ptx::mbar_wait(ptx::smem_u32(&bars[grp & 1]), (grp >> 1) & 1);
-        if constexpr (GM == 2) {
-            const uint32_t Lb = ptx::smem_u32(lut_buf) + (grp & 1) * 65536u;
-            const uint32_t* clo = reinterpret_cast<const uint32_t*>(code_buf + (grp & 1) * kGmCodeBuf);
-            const uint8_t* chi = code_buf + (grp & 1) * kGmCodeBuf + 4 * kSplitTokens;
-            uint32_t off[kGroupStages], msk[kGroupStages];
+    const uint8_t* krec = a.krec + uint64_t(pair) * a.krec_stride;
+    auto prefetch_records = [&](uint32_t g, uint64_t c0, uint32_t n) {  // into L2, ahead of the LDGs
+        const uint8_t* seg = krec + uint64_t(g) * a.cap * 10u;
+        ptx_prefetch_records(seg, a.cap, c0, n);
+    };
+    // value codes: 32-bit words relative to the 4 B-aligned start of the pair's payload
+    const uint8_t* vc = a.vcodes + uint64_t(pair) * a.vstride;
+    const uint32_t* vc32 = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(vc) & ~uintptr_t(3));
+    const uint32_t vbase_bits = uint32_t((reinterpret_cast<uintptr_t>(vc) & 3u) * 8u);
+    const uint64_t vwords64 = (reinterpret_cast<uintptr_t>(a.vend) - reinterpret_cast<uintptr_t>(vc32)) >> 2;
+    const uint32_t vwords = vwords64 > 0xffffffffull ? 0xffffffffu : uint32_t(vwords64);
+    const uint32_t vrow32 = uint32_t(a.vrow_bits);
+    const uint32_t l7 = (lane & 7u) << 4;  // this lane's slot rotation (token & 7 == lane & 7)
+
+    float4 M = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY), Lrun = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool first = true;
+    float4* accp = a.acc + uint64_t(cta) * (HW / 4u);
+    uint32_t phase = 0;
+    if (tid == 0 && t0 < t1) {
+        prefetch_records(0, t0, uint32_t(umin64(kChunk, t1 - t0)));
+        issue(0);
+    }
+    for (uint64_t c0 = t0; c0 < t1; c0 += kChunk) {
+        const uint32_t nt = uint32_t(umin64(kChunk, t1 - c0));
+        float2 lg[kTok][2];
 #pragma unroll
-            for (int q = 0; q < kGroupStages; ++q) {
-                const uint32_t st = grp * kGroupStages + q;
-                off[q] = (st < a.kn) ? a.kst[st].bit_off - a.kst[grp * kGroupStages].bit_off : 0u;
-                msk[q] = (st < a.kn) ? ((1u << a.kst[st].bits) - 1u) << 3 : 0u;
+        for (int k = 0; k < kTok; ++k) lg[k][0] = lg[k][1] = make_float2(0.f, 0.f);
+        // ---- keys: sum over the LUT groups of 8 conflict-free lookups per token
+        for (uint32_t g = 0; g < a.ng; ++g) {
+            if (tid == 0) {
+                if (g + 1 < a.ng) prefetch_records(g + 1, c0, nt);
+                else if (c0 + kChunk < t1) prefetch_records(0, c0 + kChunk, uint32_t(umin64(kChunk, t1 - c0 - kChunk)));
             }
+            const uint8_t* seg = krec + uint64_t(g) * a.cap * 10u;
+            const uint2* rlo = reinterpret_cast<const uint2*>(seg);
+            const uint16_t* rhi = reinterpret_cast<const uint16_t*>(seg + a.cap * 8u);
+            ptx::mbar_wait(barp, phase);
+            phase ^= 1u;
 #pragma unroll
-            for (int k = 0; k < kTokPerThread; ++k) {
-                const uint32_t lt = threadIdx.x + uint32_t(k) * kAttThreads;
-                const uint32_t lo = clo[lt], hi = chi[lt];
-                const uint32_t xl = lo << 3, xh = __funnelshift_l(lo, hi, 3);
+            for (int kb = 0; kb < kTok; kb += 4) {
                 uint2 w[4];
-                lds64(Lb | (xl & msk[0]), w[0]);
-                lds64((Lb + 8192u) | (__funnelshift_r(xl, xh, off[1]) & msk[1]), w[1]);
-                lds64((Lb + 16384u) | (__funnelshift_r(xl, xh, off[2]) & msk[2]), w[2]);
-                lds64((Lb + 24576u) | (__funnelshift_r(xl, xh, off[3]) & msk[3]), w[3]);
-                // per 32-bit word: the whole word and its high half accumulate; the low-half sum is
-                // recovered exactly afterwards (full - (high << 16), mod 2^32: it stays below 2^22)
+                uint32_t h[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    il[k][0] += w[q].x;
-                    il[k][1] += w[q].x >> 16;
-                    il[k][2] += w[q].y;
-                    il[k][3] += w[q].y >> 16;
+                for (int k = 0; k < 4; ++k) {
+                    // tokens past the range read the last valid record (their logits are masked)
+                    const uint64_t t = min(c0 + uint64_t(kb + k) * kThreads + tid, t1 - 1);
+                    w[k] = __ldg(rlo + t);
+                    h[k] = __ldg(rhi + t);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t w0 = w[k].x, w1 = w[k].y, w2 = h[k];
+                    float2* L = lg[kb + k];
+#define VQKV_LOOK(K)                                                                        \
+    {                                                                                       \
+        const uint32_t x = field_at7<K>(w0, w1, w2);                                        \
+        float2 u, v;                                                                        \
+        lds128(lut_s + ((x & 0x1FF80u) | (l7 ^ uint32_t((K) << 4))), u, v);                \
+        L[0] = ptx::add2(L[0], u);                                                          \
+        L[1] = ptx::add2(L[1], v);                                                          \
+    }
+                    VQKV_LOOK(0) VQKV_LOOK(1) VQKV_LOOK(2) VQKV_LOOK(3)
+                    VQKV_LOOK(4) VQKV_LOOK(5) VQKV_LOOK(6) VQKV_LOOK(7)
+#undef VQKV_LOOK
                 }
             }
-            __syncthreads();  // buffers (grp & 1) are refilled two groups later
-            continue;
+            __syncthreads();  // every lane is done with this group's rows
+            if (tid == 0 && g + 1 < a.ng) issue(g + 1);
         }
-        if constexpr (GM == 1) {
-            const uint32_t Lb = ptx::smem_u32(lut_buf) + (grp & 1) * 65536u;
-            const uint32_t* clo = reinterpret_cast<const uint32_t*>(code_buf + (grp & 1) * kGmCodeBuf);
-            const uint8_t* chi = code_buf + (grp & 1) * kGmCodeBuf + 4 * kSplitTokens;
-            // field q of the record x = rec << 4 sits at bit off_q: (x >> off_q) & (mask_q << 4)
-            uint32_t off[kGroupStages], msk[kGroupStages];
+
+        // ---- chunk softmax statistics (exact fp32 weights)
+        float4 mloc = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
 #pragma unroll
-            for (int q = 0; q < kGroupStages; ++q) {
-                const uint32_t s = grp * kGroupStages + q;
-                off[q] = (s < a.kn) ? a.kst[s].bit_off - a.kst[grp * kGroupStages].bit_off : 0u;
-                msk[q] = (s < a.kn) ? ((1u << a.kst[s].bits) - 1u) << 4 : 0u;
+        for (int k = 0; k < kTok; ++k)
+            if (uint32_t(k) * kThreads + tid < nt) {
+                mloc.x = fmaxf(mloc.x, lg[k][0].x);
+                mloc.y = fmaxf(mloc.y, lg[k][0].y);
+                mloc.z = fmaxf(mloc.z, lg[k][1].x);
+                mloc.w = fmaxf(mloc.w, lg[k][1].y);
             }
+        const float4 mc = block_max4(mloc, red);
+        float4 lloc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int k = 0; k < kTokPerThread; ++k) {
-                // tokens past nt read stale records (valid slots; their logits are masked below)
-                const uint32_t lt = threadIdx.x + uint32_t(k) * kAttThreads;
-                const uint32_t lo = clo[lt], hi = chi[lt];
-                const uint32_t xl = lo << 4, xh = __funnelshift_l(lo, hi, 4);
-                float2 v[4][2];
-                lds128(Lb | (xl & msk[0]), v[0][0], v[0][1]);
-                lds128((Lb + 16384u) | (__funnelshift_r(xl, xh, off[1]) & msk[1]), v[1][0], v[1][1]);
-                lds128((Lb + 32768u) | (__funnelshift_r(xl, xh, off[2]) & msk[2]), v[2][0], v[2][1]);
-                lds128((Lb + 49152u) | (__funnelshift_r(xl, xh, off[3]) & msk[3]), v[3][0], v[3][1]);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    lg2[k][0] = ptx::add2(lg2[k][0], v[q][0]);
-                    lg2[k][1] = ptx::add2(lg2[k][1], v[q][1]);
-                }
-            }
-            __syncthreads();  // buffers (grp & 1) are refilled two groups later
-            continue;
+        for (int k = 0; k < kTok; ++k) {
+            const bool ok = uint32_t(k) * kThreads + tid < nt;
+            const float p0 = ok ? __expf(lg[k][0].x - mc.x) : 0.f, p1 = ok ? __expf(lg[k][0].y - mc.y) : 0.f;
+            const float p2 = ok ? __expf(lg[k][1].x - mc.z) : 0.f, p3 = ok ? __expf(lg[k][1].y - mc.w) : 0.f;
+            lg[k][0] = make_float2(p0, p1);
+            lg[k][1] = make_float2(p2, p3);
+            lloc.x += p0;
+            lloc.y += p1;
+            lloc.z += p2;
+            lloc.w += p3;
         }
-        const uint32_t s0 = grp * kGroupStages;
-        const uint32_t s1 = min(a.kn, s0 + kGroupStages);
-        const float4* L = reinterpret_cast<const float4*>(lut_buf + (grp & 1) * 65536);
-        const uint32_t gbit = a.kst[s0].bit_off;
-        uint32_t loff[kGroupStages], lbits[kGroupStages], lofs[kGroupStages];
-        uint32_t acc_off = 0;
+        const float4 lc = block_sum4(lloc, red);
+        // fixed point relative to the chunk's normaliser: P = rint(p / u_c), u_c = l_c 2^-28
+        const float4 qs = make_float4(kQuantum / lc.x, kQuantum / lc.y, kQuantum / lc.z, kQuantum / lc.w);
+        uint32_t P[kTok][kG];
 #pragma unroll
-        for (int q = 0; q < kGroupStages; ++q) {
-            const uint32_t s = s0 + q;
-            lbits[q] = (s < s1) ? a.kst[s].bits : 0u;
-            loff[q] = (s < s1) ? a.kst[s].bit_off - gbit : 0u;
-            lofs[q] = acc_off;
-            acc_off += (s < s1) ? a.kst[s].size : 0u;
+        for (int k = 0; k < kTok; ++k) {
+            P[k][0] = __float2uint_rn(lg[k][0].x * qs.x);
+            P[k][1] = __float2uint_rn(lg[k][0].y * qs.y);
+            P[k][2] = __float2uint_rn(lg[k][1].x * qs.z);
+            P[k][3] = __float2uint_rn(lg[k][1].y * qs.w);
         }
-        // kKeyBatch tokens per batch: all their code-word loads are issued before any
-        // is used (branch-free: out-of-range tokens and the last words of the buffer
-        // read a dummy word; the rare buffer-tail tokens take read_bits64's careful path).
-        // Bit positions are 32-bit, relative to the 8 B-aligned start of the pair's stream.
+        // ---- values: int32 histograms [half][code][stage slot][head] over the LUT buffer
+        for (uint32_t i = tid; i < HW / 4u; i += kThreads) reinterpret_cast<uint4*>(lutb)[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+        const uint32_t myg = lane & 3u;
 #pragma unroll
-        for (int kb = 0; kb < kTokPerThread; kb += kKeyBatch) {
-            uint2 lo[kKeyBatch], hi[kKeyBatch];
-            uint32_t sh[kKeyBatch];
-            bool fast[kKeyBatch];
-#pragma unroll
-            for (int k = 0; k < kKeyBatch; ++k) {
-                const uint32_t t = threadIdx.x + uint32_t(kb + k) * kAttThreads;
-                const uint32_t pos = (uint32_t(t0) + t) * krow32 + gbit + kbase_bits;
-                const uint32_t wi = pos >> 6;
-                sh[k] = pos & 63u;
-                fast[k] = (t < nt) && (wi + 2u <= kwords);
-                const uint2* q = reinterpret_cast<const uint2*>(fast[k] ? kc64 + wi : g_zero16);
-                lo[k] = __ldg(q);
-                hi[k] = __ldg(q + 1);
-            }
-#pragma unroll
-            for (int k = 0; k < kKeyBatch; ++k) {
-                const uint32_t t = threadIdx.x + uint32_t(kb + k) * kAttThreads;
-                if (t < nt) {
-                    // 64-bit window starting at bit sh of (lo, hi) as two 32-bit words
-                    const bool low = sh[k] < 32u;
-                    const uint32_t s5 = sh[k] & 31u;
-                    const uint32_t wa = low ? lo[k].x : lo[k].y, wb = low ? lo[k].y : hi[k].x;
-                    const uint32_t wc = low ? hi[k].x : hi[k].y;
-                    uint32_t w0 = __funnelshift_r(wa, wb, s5), w1 = __funnelshift_r(wb, wc, s5);
-                    if (!fast[k]) {
-                        const uint64_t w = read_bits64(kc, (t0 + t) * a.krow_bits + gbit, a.kend);
-                        w0 = uint32_t(w);
-                        w1 = uint32_t(w >> 32);
-                    }
-#pragma unroll
-                    for (int q = 0; q < kGroupStages; ++q) {
-                        if (lbits[q]) {
-                            const uint32_t z = (loff[q] < 32u ? __funnelshift_r(w0, w1, loff[q]) : (w1 >> (loff[q] - 32u))) &
-                                               ((1u << lbits[q]) - 1u);
-                            const float4 v = L[lofs[q] + z];
-                            lg2[kb + k][0] = ptx::add2(lg2[kb + k][0], make_float2(v.x, v.y));
-                            lg2[kb + k][1] = ptx::add2(lg2[kb + k][1], make_float2(v.z, v.w));
+        for (int k = 0; k < kTok; ++k) {
+            const bool act = (uint32_t(k) * kThreads + tid < nt) && ((P[k][0] | P[k][1] | P[k][2] | P[k][3]) != 0u);
+            uint32_t m = __ballot_sync(0xffffffffu, act);
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1u;
+                const uint32_t q0 = __shfl_sync(0xffffffffu, P[k][0], src), q1 = __shfl_sync(0xffffffffu, P[k][1], src);
+                const uint32_t q2 = __shfl_sync(0xffffffffu, P[k][2], src), q3 = __shfl_sync(0xffffffffu, P[k][3], src);
+                const uint32_t myP = myg == 0u ? q0 : (myg == 1u ? q1 : (myg == 2u ? q2 : q3));
+                const uint64_t t = c0 + uint64_t(k) * kThreads + warp * 32u + uint32_t(src);
+                const uint32_t rowbit = vbase_bits + uint32_t(t) * vrow32;
+                for (uint32_t h = 0; h < a.vhalves; ++h) {
+                    const uint32_t d = vdesc[h * 32u + lane];
+                    if (d >> 31) {
+                        const uint32_t pos = rowbit + (d & 0xFFFFu), wi = pos >> 5;
+                        uint32_t z;
+                        if (wi + 1u < vwords) {
+                            z = __funnelshift_r(__ldg(vc32 + wi), __ldg(vc32 + wi + 1u), pos & 31u);
+                        } else {  // the last words of the buffer
+                            z = uint32_t(read_bits64(vc, t * a.vrow_bits + (d & 0xFFFFu), a.vend));
                         }
+                        z &= (1u << ((d >> 16) & 31u)) - 1u;
+                        if (myP) red_shared_add(lut_s + ((h * a.Rv + z) * 32u + lane) * 4u, myP);
                     }
                 }
             }
         }
-        __syncthreads();  // buffer (grp & 1) is refilled two groups later
+        __syncthreads();
+        // ---- fold the chunk into the CTA's accumulator, rescaled to the running max
+        const float4 Mn = make_float4(fmaxf(M.x, mc.x), fmaxf(M.y, mc.y), fmaxf(M.z, mc.z), fmaxf(M.w, mc.w));
+        const float4 al = first ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                : make_float4(__expf(M.x - Mn.x), __expf(M.y - Mn.y), __expf(M.z - Mn.z), __expf(M.w - Mn.w));
+        const float4 ec = make_float4(__expf(mc.x - Mn.x), __expf(mc.y - Mn.y), __expf(mc.z - Mn.z), __expf(mc.w - Mn.w));
+        const float4 be = make_float4(lc.x / kQuantum * ec.x, lc.y / kQuantum * ec.y, lc.z / kQuantum * ec.z,
+                                      lc.w / kQuantum * ec.w);
+        for (uint32_t i = tid; i < HW / 4u; i += kThreads) {
+            const uint4 hq = reinterpret_cast<const uint4*>(lutb)[i];
+            float4 v = make_float4(float(hq.x) * be.x, float(hq.y) * be.y, float(hq.z) * be.z, float(hq.w) * be.w);
+            if (!first) {
+                const float4 o = ldcg4(accp + i);
+                v = make_float4(fmaf(o.x, al.x, v.x), fmaf(o.y, al.y, v.y), fmaf(o.z, al.z, v.z), fmaf(o.w, al.w, v.w));
+            }
+            stcg4(accp + i, v);
+        }
+        Lrun = make_float4(fmaf(Lrun.x, al.x, lc.x * ec.x), fmaf(Lrun.y, al.y, lc.y * ec.y), fmaf(Lrun.z, al.z, lc.z * ec.z),
+                           fmaf(Lrun.w, al.w, lc.w * ec.w));
+        M = Mn;
+        first = false;
+        __syncthreads();  // histograms consumed: the buffer takes the next chunk's first LUT group
+        if (tid == 0 && c0 + kChunk < t1) issue(0);
     }
 
-    if constexpr (GM == 2) {
-        const float* dqp = a.dq + uint64_t(pair) * kG;
-        const int bias = int(a.kn) * 32768;
+    // ---- contraction: o[g][d] = sum_{h, j, slot} acc[h][j][slot][g] * e_{8h+slot}[j][d]
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!first) {
+        __threadfence_block();
+        const uint32_t d = tid & (kD - 1u), qtr = tid >> 7;  // 4 quarters of the (half, code) rows
+        for (uint32_t r = qtr; r < a.vhalves * a.Rv; r += 4u) {
+            const uint32_t h = r / a.Rv, j = r - h * a.Rv;
+            float4 hv[kGS];
+            float x[kGS];
 #pragma unroll
-        for (int k = 0; k < kTokPerThread; ++k) {
-            il[k][0] -= il[k][1] << 16;
-            il[k][2] -= il[k][3] << 16;
+            for (int sl = 0; sl < kGS; ++sl) {
+                const uint32_t s = h * 8u + uint32_t(sl);
+                const bool ok = s < a.vn && j < vsz[s < 64u ? s : 0u];
+                hv[sl] = ok ? ldcg4(accp + uint64_t(r) * kGS + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
+                x[sl] = ok ? __ldg(a.veff + (uint64_t(vrow[s]) + j) * kD + d) : 0.f;
+            }
+#pragma unroll
+            for (int sl = 0; sl < kGS; ++sl) {
+                o.x = fmaf(hv[sl].x, x[sl], o.x);
+                o.y = fmaf(hv[sl].y, x[sl], o.y);
+                o.z = fmaf(hv[sl].z, x[sl], o.z);
+                o.w = fmaf(hv[sl].w, x[sl], o.w);
+            }
         }
-#pragma unroll
-        for (int g = 0; g < kG; ++g) {
-            const float d = __ldg(dqp + g);
-#pragma unroll
-            for (int k = 0; k < kTokPerThread; ++k) lg[k][g] = float(int(il[k][g]) - bias) * d;
-        }
     }
-
-    // ---- split max / p / l
-    float mg[kG], lsum[kG];
-#pragma unroll
-    for (int g = 0; g < kG; ++g) {
-        float m = -INFINITY;
-#pragma unroll
-        for (int k = 0; k < kTokPerThread; ++k)
-            if (threadIdx.x + uint64_t(k) * kAttThreads < nt) m = fmaxf(m, lg[k][g]);
-        mg[g] = block_max(m, red);
-    }
-#pragma unroll
-    for (int g = 0; g < kG; ++g) {
-        float l = 0.f;
-#pragma unroll
-        for (int k = 0; k < kTokPerThread; ++k) {
-            const bool ok = threadIdx.x + uint64_t(k) * kAttThreads < nt;
-            const float p = ok ? __expf(lg[k][g] - mg[g]) : 0.f;
-            lg[k][g] = p;
-            l += p;
-        }
-        lsum[g] = block_sum(l, red);
-    }
-
-    // ---- values: int32 fixed-point histograms H[s][j][g] in smem (reuses the LUT area)
-    uint32_t* H = reinterpret_cast<uint32_t*>(sm);
-    const uint32_t hsz = uint32_t(a.ventries) * kG;
-    // value-stage descriptors, read once per CTA: entry offset << 16 | bit offset
-    // within the stage's 6-stage window << 5 | bits; window start bits per group
-    uint32_t* vd = reinterpret_cast<uint32_t*>(sm + 131072 + 64 + 256);
-    uint32_t* vgb = vd + kMaxVStages;
-    for (uint32_t i = threadIdx.x; i < hsz; i += blockDim.x) H[i] = 0u;
-    if (threadIdx.x < a.vn) {
-        const StageInfo si = a.vst[threadIdx.x];
-        const uint32_t first = (threadIdx.x / 6u) * 6u;
-        vd[threadIdx.x] = uint32_t(si.eff_off / kD) << 16 | (si.bit_off - a.vst[first].bit_off) << 5 | si.bits;
-        if (threadIdx.x == first) vgb[threadIdx.x / 6u] = si.bit_off;
-    }
+    float4* po = reinterpret_cast<float4*>(lutb);  // [4 quarters][D] x float4 (heads)
     __syncthreads();
-    // Histogram updates of one token: its <= 6-field value-code windows, then one shared
-    // atomic per (stage, head) with a nonzero weight.
-    auto hist_token = [&](uint32_t t, const uint32_t (&P)[kG]) {
-        const uint32_t rb = (uint32_t(t0) + t) * vrow32 + vbase_bits;
-        // windows of the common case (<= 3, i.e. up to 18 value stages) load together
-        uint32_t w0[3], w1[3];
-        bool ok3 = nvwin <= 3u;
-        if (ok3) {
-#pragma unroll
-            for (int wdw = 0; wdw < 3; ++wdw) {
-                const uint32_t pos = rb + vgb[wdw < int(nvwin) ? wdw : 0];
-                const uint32_t wi = pos >> 6;
-                const bool f = wi + 2u <= vwords;
-                ok3 = ok3 && (f || wdw >= int(nvwin));
-                const uint2* q = reinterpret_cast<const uint2*>(f ? vc64 + wi : g_zero16);
-                const uint2 lo = __ldg(q), hi = __ldg(q + 1);
-                const uint32_t sh = pos & 63u, s5 = sh & 31u;
-                const bool low = sh < 32u;
-                const uint32_t wa = low ? lo.x : lo.y, wb = low ? lo.y : hi.x, wc = low ? hi.x : hi.y;
-                w0[wdw] = __funnelshift_r(wa, wb, s5);
-                w1[wdw] = __funnelshift_r(wb, wc, s5);
-            }
-        }
-        for (uint32_t s0 = 0, wdw = 0; s0 < a.vn; s0 += 6, ++wdw) {
-            uint32_t x0, x1;
-            if (ok3) {
-                x0 = wdw == 0 ? w0[0] : (wdw == 1 ? w0[1] : w0[2]);
-                x1 = wdw == 0 ? w1[0] : (wdw == 1 ? w1[1] : w1[2]);
-            } else {  // many value stages or the buffer tail: careful 64-bit reads
-                const uint64_t w = read_bits64(vc, (t0 + t) * a.vrow_bits + vgb[wdw], a.vend);
-                x0 = uint32_t(w);
-                x1 = uint32_t(w >> 32);
-            }
-            const uint32_t s1 = min(a.vn, s0 + 6u);
-            for (uint32_t st = s0; st < s1; ++st) {
-                const uint32_t d = vd[st];
-                const uint32_t lo5 = (d >> 5) & 63u;
-                const uint32_t z = (lo5 < 32u ? __funnelshift_r(x0, x1, lo5) : (x1 >> (lo5 - 32u))) &
-                                   ((1u << (d & 31u)) - 1u);
-                uint32_t* h = H + ((d >> 16) + z) * kG;
-#pragma unroll
-                for (int g = 0; g < kG; ++g)
-                    if (P[g]) atomicAdd(h + g, P[g]);
-            }
-        }
-    };
-    // Tokens whose weights all round to 0 in the 2^-18 fixed point add nothing; the others
-    // are compacted into a per-warp queue and processed 32 at a time, so the histogram
-    // loop runs with full warps instead of the few lanes that happen to contribute.
-    const uint32_t lane = threadIdx.x & 31u;
-    uint32_t* qt = reinterpret_cast<uint32_t*>(sm + kQueueOff) + (threadIdx.x >> 5) * (kQueueCap * (1 + kG));
-    uint32_t* qP = qt + kQueueCap;
-    uint32_t qlen = 0;
-    auto flush = [&](uint32_t n) {
-        if (lane < n) {
-            uint32_t P[kG];
-#pragma unroll
-            for (int g = 0; g < kG; ++g) P[g] = qP[lane * kG + g];
-            hist_token(qt[lane], P);
-        }
-    };
-#pragma unroll
-    for (int k = 0; k < kTokPerThread; ++k) {
-        const uint32_t t = threadIdx.x + uint32_t(k) * kAttThreads;
-        uint32_t P[kG];
-#pragma unroll
-        for (int g = 0; g < kG; ++g) P[g] = __float2uint_rn(lg[k][g] * kHistScale);
-        const bool act = t < nt && (P[0] | P[1] | P[2] | P[3]) != 0u;
-        const uint32_t mask = __ballot_sync(0xffffffffu, act);
-        if (act) {
-            const uint32_t pos = qlen + __popc(mask & ((1u << lane) - 1u));
-            qt[pos] = t;
-#pragma unroll
-            for (int g = 0; g < kG; ++g) qP[pos * kG + g] = P[g];
-        }
-        qlen += __popc(mask);
-        if (qlen >= 32u) {
-            __syncwarp();
-            flush(32u);
-            __syncwarp();
-            if (lane + 32u < qlen) {  // keep the overflow for the next batch
-                qt[lane] = qt[lane + 32u];
-#pragma unroll
-                for (int g = 0; g < kG; ++g) qP[lane * kG + g] = qP[(lane + 32u) * kG + g];
-            }
-            __syncwarp();
-            qlen -= 32u;
-        }
-    }
-    __syncwarp();
-    flush(qlen);
+    po[tid] = o;
     __syncthreads();
-    float* ph = a.part_h + (uint64_t(pair) * a.n_splits + split) * hsz;
-    for (uint32_t i = threadIdx.x; i < hsz; i += blockDim.x) ph[i] = float(H[i]) * (1.0f / kHistScale);
-    if (threadIdx.x < kG) {
-        a.part_m[(uint64_t(pair) * (a.n_splits + 1) + split) * kG + threadIdx.x] = mg[threadIdx.x];
-        a.part_l[(uint64_t(pair) * (a.n_splits + 1) + split) * kG + threadIdx.x] = lsum[threadIdx.x];
-    }
-}
-
-// Split weights: w[pair][s][g] = exp(m_s - M), L = sum_s w l_s, M = max_s m_s.
-__global__ void lut_weights_kernel(const float* __restrict__ part_m, const float* __restrict__ part_l,
-                                   uint32_t n_splits, uint32_t n_pairs, float* __restrict__ w, float* __restrict__ ML) {
-    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;  // pair * G + g
-    if (idx >= n_pairs * kG) return;
-    const uint32_t pair = idx / kG, g = idx % kG, ns = n_splits + 1;
-    float M = -INFINITY;
-    for (uint32_t s = 0; s < ns; ++s) M = fmaxf(M, part_m[(uint64_t(pair) * ns + s) * kG + g]);
-    float L = 0.f;
-    for (uint32_t s = 0; s < ns; ++s) {
-        const float m = part_m[(uint64_t(pair) * ns + s) * kG + g];
-        const float ww = (m > -INFINITY) ? __expf(m - M) : 0.f;
-        w[(uint64_t(pair) * ns + s) * kG + g] = ww;
-        L += ww * part_l[(uint64_t(pair) * ns + s) * kG + g];
-    }
-    ML[idx * 2] = M;
-    ML[idx * 2 + 1] = L;
-}
-
-// CTA = (pair, 256-entry chunk of the value codebooks): merge the split
-// histograms of the chunk, contract with the chunk's codebook rows and add the
-// partial output into acc[pair][g][d] (fp32 atomics in L2).  Merge: every split's
-// load is in flight at once.  Contraction: thread = (d, quarter of the chunk), one
-// codebook load feeds the 4 heads.
-__global__ void __launch_bounds__(512) lut_contract_kernel(const float* __restrict__ part_h, const float* __restrict__ w,
-                                                           uint32_t n_splits, const float* __restrict__ veff,
-                                                           uint64_t ventries, float* __restrict__ acc) {
-    constexpr int kChunk = 256, kMerge = 16;
-    __shared__ float4 hs[kChunk];
-    __shared__ float4 po[4][kD];
-    const uint32_t pair = blockIdx.y;
-    const uint64_t e0 = uint64_t(blockIdx.x) * kChunk;
-    const uint32_t ne = uint32_t((ventries - e0 < kChunk) ? (ventries - e0) : kChunk);
-    const uint32_t ns = n_splits + 1;
-    float* hsf = reinterpret_cast<float*>(hs);
-    for (uint32_t i = threadIdx.x; i < kChunk * kG; i += blockDim.x) {
-        const uint32_t e = i / kG, g = i % kG;
-        float v = 0.f;
-        if (e < ne) {
-            const float* src = part_h + (uint64_t(pair) * n_splits * ventries + e0) * kG + i;
-            const float* wp = w + uint64_t(pair) * ns * kG + g;
-            for (uint32_t s0 = 0; s0 < n_splits; s0 += kMerge) {
-                float x[kMerge];
-#pragma unroll
-                for (int k = 0; k < kMerge; ++k)
-                    x[k] = (s0 + k < n_splits) ? __ldg(src + uint64_t(s0 + k) * ventries * kG) : 0.f;
-#pragma unroll
-                for (int k = 0; k < kMerge; ++k)
-                    if (s0 + k < n_splits) v = fmaf(wp[(s0 + k) * kG], x[k], v);
-            }
-        }
-        hsf[i] = v;
-    }
-    __syncthreads();
-    const uint32_t d = threadIdx.x % kD, qt = threadIdx.x / kD;  // quarter qt: entries qt, qt + 4, ...
-    float o[kG] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-    for (uint32_t e = qt; e < ne; e += 4) {
-        const float x = __ldg(veff + (e0 + e) * kD + d);
-        const float4 h = hs[e];
-        o[0] = fmaf(h.x, x, o[0]);
-        o[1] = fmaf(h.y, x, o[1]);
-        o[2] = fmaf(h.z, x, o[2]);
-        o[3] = fmaf(h.w, x, o[3]);
-    }
-    po[qt][d] = make_float4(o[0], o[1], o[2], o[3]);
-    __syncthreads();
-    if (threadIdx.x < kG * kD) {
-        const uint32_t g = threadIdx.x / kD, dd = threadIdx.x % kD;
+    {
+        const uint32_t g = tid >> 7, d = tid & (kD - 1u);
         const float* pf = reinterpret_cast<const float*>(po);
-        const float r = (pf[(0 * kD + dd) * kG + g] + pf[(1 * kD + dd) * kG + g]) +
-                        (pf[(2 * kD + dd) * kG + g] + pf[(3 * kD + dd) * kG + g]);
-        atomicAdd(acc + (uint64_t(pair) * kG + g) * kD + dd, r);
+        const float r = (pf[(0 * kD + d) * kG + g] + pf[(1 * kD + d) * kG + g]) +
+                        (pf[(2 * kD + d) * kG + g] + pf[(3 * kD + d) * kG + g]);
+        a.part_o[(uint64_t(cta) * kG + g) * kD + d] = r;
+    }
+    if (tid == 0) {
+        reinterpret_cast<float4*>(a.part_m)[cta] = M;
+        reinterpret_cast<float4*>(a.part_l)[cta] = Lrun;
     }
 }
 
-// out = (acc + w_raw * o_raw) / L, lse = M + log L
-__global__ void lut_finish_kernel(const float* __restrict__ acc, const float* __restrict__ part_o,
-                                  const float* __restrict__ w, const float* __restrict__ ML, uint32_t n_splits,
-                                  uint32_t n_pairs, float* __restrict__ out, float* __restrict__ lse) {
-    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // (pair, g, d)
-    if (idx >= uint64_t(n_pairs) * kG * kD) return;
-    const uint32_t pg = uint32_t(idx / kD), pair = pg / kG, g = pg % kG;
-    const float wr = w[(uint64_t(pair) * (n_splits + 1) + n_splits) * kG + g];
-    float v = acc[idx];
-    if (wr > 0.f) v = fmaf(wr, part_o[idx], v);
-    out[idx] = v / ML[pg * 2 + 1];
-    if (idx % kD == 0 && lse) lse[pg] = ML[pg * 2] + logf(ML[pg * 2 + 1]);
+// out[pair][g] = sum_c exp(m_c - M) o_c / sum_c exp(m_c - M) l_c over the pair's main CTAs and
+// its raw CTA; lse = M + log L (natural log of the sum of exp(scale * logits)).
+__global__ void atr_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_m,
+                                   const float* __restrict__ part_l, uint32_t cpp, uint32_t n_main,
+                                   float* __restrict__ out, float* __restrict__ lse) {
+    const uint32_t pair = blockIdx.x, d = threadIdx.x;
+    for (uint32_t g = 0; g < kG; ++g) {
+        auto slot = [&](uint32_t i) { return i < cpp ? pair * cpp + i : n_main + pair; };
+        float M = -INFINITY;
+        for (uint32_t i = 0; i <= cpp; ++i) M = fmaxf(M, part_m[uint64_t(slot(i)) * kG + g]);
+        float L = 0.f, o = 0.f;
+        for (uint32_t i = 0; i <= cpp; ++i) {
+            const uint32_t sl = slot(i);
+            const float m = part_m[uint64_t(sl) * kG + g];
+            if (m > -INFINITY) {
+                const float w = __expf(m - M);
+                L = fmaf(w, part_l[uint64_t(sl) * kG + g], L);
+                o = fmaf(w, part_o[(uint64_t(sl) * kG + g) * kD + d], o);
+            }
+        }
+        out[(uint64_t(pair) * kG + g) * kD + d] = o / L;
+        if (d == 0 && lse) lse[uint64_t(pair) * kG + g] = M + logf(L);
+    }
+}
+
+// ---- attention records -----------------------------------------------------------------
+// CodeMatrix rows -> records: thread = (token, group, pair); field k of token t's record is
+// the code of stage 8g + ((t & 7) ^ k) (0 for stages past the stack).
+__global__ void atr_pack_kernel(const uint8_t* __restrict__ payload, uint64_t payload_stride, uint64_t row_bits,
+                                const uint8_t* payload_end, const StageInfo* __restrict__ kst, uint32_t kn,
+                                uint64_t src_row, uint64_t count, uint8_t* __restrict__ rec, uint64_t cap,
+                                uint64_t rec_stride, uint64_t dst_row) {
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    const uint32_t g = blockIdx.y, pair = blockIdx.z;
+    if (i >= count) return;
+    const uint64_t t = dst_row + i;  // the record's token index fixes its rotation
+    const uint8_t* src = payload + pair * payload_stride;
+    const uint64_t rb = (src_row + i) * row_bits;
+    uint64_t lo = 0;
+    uint32_t hi = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+        const uint32_t s = g * 8u + ((uint32_t(t) & 7u) ^ k);
+        uint32_t z = 0;
+        if (s < kn) {
+            const StageInfo si = kst[s];
+            z = uint32_t(read_bits64(src, rb + si.bit_off, payload_end)) & ((1u << si.bits) - 1u);
+        }
+        const uint32_t b = 10u * k;
+        if (b + 10u <= 64u) {
+            lo |= uint64_t(z) << b;
+        } else if (b >= 64u) {
+            hi |= z << (b - 64u);
+        } else {  // field 6 straddles bit 64
+            lo |= uint64_t(z) << b;
+            hi |= z >> (64u - b);
+        }
+    }
+    uint8_t* seg = rec + pair * rec_stride + uint64_t(g) * cap * 10u;
+    reinterpret_cast<uint64_t*>(seg)[t] = lo;
+    reinterpret_cast<uint16_t*>(seg + cap * 8u)[t] = uint16_t(hi);
+}
+
+// records -> CodeMatrix rows [0, count) of a dense per-pair payload: thread = output byte; each
+// of its 8 bits is looked up as (token, stage, bit) and read from the token's record.
+__global__ void atr_unpack_kernel(const uint8_t* __restrict__ rec, uint64_t cap, uint64_t rec_stride,
+                                  const StageInfo* __restrict__ kst, uint32_t kn, uint64_t row_bits, uint64_t count,
+                                  uint8_t* __restrict__ payload, uint64_t payload_stride) {
+    extern __shared__ uint16_t bit_stage[];  // [row_bits]: stage of each row bit
+    for (uint32_t b = threadIdx.x; b < row_bits; b += blockDim.x) {
+        uint32_t s = 0;
+        while (s + 1 < kn && b >= kst[s + 1].bit_off) ++s;
+        bit_stage[b] = uint16_t(s);
+    }
+    __syncthreads();
+    const uint64_t nbytes = (count * row_bits + 7) / 8;
+    const uint64_t byte = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    const uint32_t pair = blockIdx.y;
+    if (byte >= nbytes) return;
+    const uint8_t* r = rec + pair * rec_stride;
+    uint32_t out = 0;
+    for (uint32_t i = 0; i < 8; ++i) {
+        const uint64_t bit = byte * 8 + i;
+        if (bit >= count * row_bits) break;
+        const uint64_t t = bit / row_bits;
+        const uint32_t rb = uint32_t(bit - t * row_bits), s = bit_stage[rb];
+        const uint32_t g = s >> 3, k = (uint32_t(t) & 7u) ^ (s & 7u), fb = rb - kst[s].bit_off;
+        const uint8_t* seg = r + uint64_t(g) * cap * 10u;
+        const uint64_t lo = reinterpret_cast<const uint64_t*>(seg)[t];
+        const uint32_t hi = reinterpret_cast<const uint16_t*>(seg + cap * 8u)[t];
+        const uint32_t pos = 10u * k + fb;  // bit of the 80-bit record
+        const uint32_t v = pos < 64u ? uint32_t(lo >> pos) & 1u : (hi >> (pos - 64u)) & 1u;
+        out |= v << i;
+    }
+    payload[pair * payload_stride + byte] = uint8_t(out);
 }
 
 }  // namespace
@@ -1024,54 +919,11 @@ static bool lut_tc_ok(const vqkv_stack_s& ks) {
     return true;
 }
 
-bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a) {
-    if (ks.dim != kD || vs.dim != kD || a.group != kG) return false;
-    if (a.n_init + a.n_local > kSplitTokens) return false;
-    // 32-bit bit positions inside one pair's key-code stream (+ alignment slack)
-    if (uint64_t(a.n_comp) * ks.row_bits + 64 >= (1ull << 32)) return false;
-    if (uint64_t(a.n_comp) * vs.row_bits + 64 >= (1ull << 32)) return false;
-    for (const auto& s : ks.stages)
-        if (s.size > 1024 || s.bits > 10) return false;
-    // 4 key stages per 64-bit read and LUT group (<= 64 KB)
-    for (uint32_t s0 = 0; s0 < ks.n; s0 += kGroupStages) {
-        uint32_t bits = 0, bytes = 0;
-        for (uint32_t s = s0; s < std::min(ks.n, s0 + kGroupStages); ++s) {
-            bits += ks.stages[s].bits;
-            bytes += ks.stages[s].size * 16u;
-        }
-        if (bits > 56 || bytes > 65536) return false;
-    }
-    uint32_t ventries = 0;
-    for (uint32_t s0 = 0; s0 < vs.n; s0 += 6) {
-        uint32_t bits = 0;
-        for (uint32_t s = s0; s < std::min(vs.n, s0 + 6u); ++s) bits += vs.stages[s].bits;
-        if (bits > 56) return false;
-    }
-    if (vs.n > uint32_t(kMaxVStages)) return false;
-    for (const auto& s : vs.stages) ventries += s.size;
-    if (ventries > 65535) return false;
-    if (uint64_t(ventries) * kG * 4 > 131072) return false;
-    return true;
-}
-
-// ---- group-major key codes ------------------------------------------------------------
-// Per pair, per LUT group g (stages 4g..4g+3): a segment of cap 5-byte records, stored as
-// cap little-endian u32 words (record bits 0-31) followed by cap bytes (bits 32-39).  A
-// record holds the group's fields in stage order at their CodeMatrix offsets relative to
-// the group's first field (codebook.cpp:96-120 row layout), missing stages as zeros.
-__global__ void gm_pack_kernel(const uint8_t* __restrict__ payload, uint64_t payload_stride, uint64_t row_bits,
-                               const uint8_t* payload_end, const uint32_t* __restrict__ gbit, const uint32_t* __restrict__ gwidth,
-                               uint32_t n_groups, uint64_t src_row, uint64_t count, uint8_t* __restrict__ gm, uint64_t cap,
-                               uint64_t gm_stride, uint64_t dst_row) {
-    const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    const uint32_t g = blockIdx.y, pair = blockIdx.z;
-    if (t >= count) return;
-    const uint8_t* src = payload + pair * payload_stride;
-    const uint64_t w = read_bits64(src, (src_row + t) * row_bits + gbit[g], payload_end);
-    const uint64_t rec = gwidth[g] >= 64 ? w : (w & ((1ull << gwidth[g]) - 1ull));
-    uint8_t* seg = gm + pair * gm_stride + uint64_t(g) * cap * 5;
-    reinterpret_cast<uint32_t*>(seg)[dst_row + t] = uint32_t(rec);
-    seg[cap * 4 + dst_row + t] = uint8_t(rec >> 32);
+static uint32_t key_groups(const vqkv_stack_s& ks) { return (ks.n + kGS - 1) / kGS; }
+static uint32_t max_size(const vqkv_stack_s& st) {
+    uint32_t m = 0;
+    for (const auto& s : st.stages) m = std::max(m, s.size);
+    return m;
 }
 
 bool gm_supported(const vqkv_stack_s& ks) {
@@ -1081,57 +933,86 @@ bool gm_supported(const vqkv_stack_s& ks) {
     return true;
 }
 
-// int16 LUT (opt-in: VQKV_ATTEND_INT16=1): group-major codes, even key stage sizes (8 B entries
-// keep every stage slot a multiple of 16 B for the bulk copies), at most 64 stages (exact int32 sums)
-static bool int16_lut_ok(const vqkv_stack_s& ks) {
-    const char* e = getenv("VQKV_ATTEND_INT16");
-    if (!(e && e[0] == '1') || !gm_supported(ks) || ks.n > 64) return false;
-    for (const auto& st : ks.stages)
-        if (st.size & 1u) return false;
+bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a) {
+    if (!gm_supported(ks) || vs.dim != kD || a.group != kG) return false;
+    if (a.n_init + a.n_local > kChunk) return false;  // the raw CTA keeps one weight per raw row in smem
+    if (vs.n > kMaxVHalves * 8 || vs.row_bits > 0xFFFF) return false;
+    for (const auto& s : vs.stages)
+        if (s.size > 1024 || s.bits > 10) return false;
+    const uint32_t halves = (vs.n + 7) / 8;
+    if (uint64_t(halves) * max_size(vs) * kRowBytes > kLutBytes) return false;  // histograms fit the LUT buffer
+    // 32-bit bit positions inside one pair's value stream (+ alignment slack)
+    if (uint64_t(a.n_comp) * vs.row_bits + 64 >= (1ull << 32)) return false;
     return true;
 }
 
-uint64_t gm_pair_bytes(const vqkv_stack_s& ks, uint64_t cap) {
-    return uint64_t((ks.n + kGroupStages - 1) / kGroupStages) * cap * 5;
-}
+uint64_t gm_pair_bytes(const vqkv_stack_s& ks, uint64_t cap) { return uint64_t(key_groups(ks)) * cap * 10u; }
 
 void launch_keycodes_to_gm(const vqkv_stack_s& ks, const uint8_t* payload, uint64_t payload_stride, uint32_t n_pairs,
                            uint64_t src_row, uint64_t count, uint8_t* gm, uint64_t cap, uint64_t gm_stride,
                            uint64_t dst_row, cudaStream_t s) {
-    const uint32_t ng = (ks.n + kGroupStages - 1) / kGroupStages;
-    std::vector<uint32_t> h(2 * ng);
-    for (uint32_t g = 0; g < ng; ++g) {
-        const uint32_t s0 = g * kGroupStages, s1 = std::min(ks.n, s0 + kGroupStages);
-        h[g] = ks.stages[s0].bit_off;
-        h[ng + g] = ks.stages[s1 - 1].bit_off + ks.stages[s1 - 1].bits - ks.stages[s0].bit_off;
-    }
-    uint32_t* d = nullptr;
-    VQKV_CUDA(cudaMallocAsync(&d, sizeof(uint32_t) * 2 * ng, s));
-    VQKV_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(uint32_t) * 2 * ng, cudaMemcpyHostToDevice, s));
     const uint64_t pb = payload_bytes(ks.row_bits, src_row + count);
     const uint8_t* end = payload + uint64_t(n_pairs - 1) * payload_stride + pb;
-    dim3 grid(unsigned((count + 255) / 256), ng, n_pairs);
-    gm_pack_kernel<<<grid, 256, 0, s>>>(payload, payload_stride, ks.row_bits, end, d, d + ng, ng, src_row, count, gm, cap,
-                                        gm_stride, dst_row);
-    launch_check("gm_pack_kernel");
-    VQKV_CUDA(cudaFreeAsync(d, s));
+    dim3 grid(unsigned((count + 255) / 256), key_groups(ks), n_pairs);
+    atr_pack_kernel<<<grid, 256, 0, s>>>(payload, payload_stride, ks.row_bits, end, ks.d_stages, ks.n, src_row, count, gm,
+                                         cap, gm_stride, dst_row);
+    launch_check("atr_pack_kernel");
+}
+
+void launch_keycodes_from_gm(const vqkv_stack_s& ks, const uint8_t* gm, uint64_t cap, uint64_t gm_stride,
+                             uint32_t n_pairs, uint64_t count, uint8_t* payload, uint64_t payload_stride,
+                             cudaStream_t s) {
+    const uint64_t nbytes = payload_bytes(ks.row_bits, count);
+    if (nbytes == 0) return;
+    dim3 grid(unsigned((nbytes + 255) / 256), n_pairs);
+    atr_unpack_kernel<<<grid, 256, sizeof(uint16_t) * ks.row_bits, s>>>(gm, cap, gm_stride, ks.d_stages, ks.n,
+                                                                          ks.row_bits, count, payload, payload_stride);
+    launch_check("atr_unpack_kernel");
 }
 
 void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s) {
-    const uint64_t kent = ks.total_rows, vent = vs.total_rows;
-    const uint32_t n_splits = uint32_t((a.n_comp + kSplitTokens - 1) / kSplitTokens);
+    const uint32_t ng = key_groups(ks), R = max_size(ks), vhalves = (vs.n + 7) / 8, Rv = max_size(vs);
     const double scale = a.scale > 0.0 ? a.scale : 1.0 / std::sqrt(double(kD));
+    const uint64_t n_comp = a.n_comp;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ks.device);
+    // main CTAs: contiguous token ranges of one pair, as many per pair as fill the SMs once
+    uint32_t cpp = 0;
+    uint64_t tpc = 0;
+    if (n_comp > 0) {
+        const uint64_t want = std::max<uint64_t>(1, uint64_t(sms) / a.n_pairs);
+        const uint64_t per = (n_comp + want - 1) / want;
+        tpc = (per + 511) / 512 * 512;
+        cpp = uint32_t((n_comp + tpc - 1) / tpc);
+    }
+    const uint32_t n_main = a.n_pairs * cpp, n_slots = n_main + a.n_pairs;
+    const uint64_t hquads = uint64_t(vhalves) * Rv * 8;
+    // key records: the caller's attention layout, or transcoded from CodeMatrix rows here
+    const uint8_t* krec = a.kcodes_dev;
+    uint64_t kstride = 0, cap = a.kcodes_cap;
+    uint8_t* ktmp = nullptr;
+    if (n_comp > 0) {
+        if (a.kcodes_layout == VQKV_KEYCODES_GROUP_MAJOR) {
+            kstride = a.kcodes_stride ? a.kcodes_stride : gm_pair_bytes(ks, cap);
+        } else {
+            cap = (n_comp + 15) / 16 * 16;
+            kstride = gm_pair_bytes(ks, cap);
+            VQKV_CUDA(cudaMallocAsync(&ktmp, kstride * a.n_pairs, s));
+            const uint64_t kpb = payload_bytes(ks.row_bits, n_comp);
+            launch_keycodes_to_gm(ks, a.kcodes_dev, a.kcodes_stride ? a.kcodes_stride : kpb, a.n_pairs, 0, n_comp, ktmp,
+                                  cap, kstride, 0, s);
+            krec = ktmp;
+        }
+    }
     float4* lut = nullptr;
-    float *ph = nullptr, *po = nullptr, *pm = nullptr, *pl = nullptr;
-    const bool i16 = a.kcodes_layout == VQKV_KEYCODES_GROUP_MAJOR && int16_lut_ok(ks);
-    uint2* lut16 = nullptr;
-    float* dq = nullptr;
-    VQKV_CUDA(cudaMallocAsync(&lut, sizeof(float4) * a.n_pairs * kent, s));
-    VQKV_CUDA(cudaMallocAsync(&ph, sizeof(float) * std::max<uint64_t>(1, uint64_t(a.n_pairs) * n_splits * vent * kG), s));
-    VQKV_CUDA(cudaMallocAsync(&po, sizeof(float) * a.n_pairs * kG * kD, s));
-    VQKV_CUDA(cudaMallocAsync(&pm, sizeof(float) * a.n_pairs * (n_splits + 1) * kG, s));
-    VQKV_CUDA(cudaMallocAsync(&pl, sizeof(float) * a.n_pairs * (n_splits + 1) * kG, s));
-    {
+    float4* acc = nullptr;
+    float *po = nullptr, *pm = nullptr, *pl = nullptr;
+    VQKV_CUDA(cudaMallocAsync(&po, sizeof(float) * n_slots * kG * kD, s));
+    VQKV_CUDA(cudaMallocAsync(&pm, sizeof(float) * n_slots * kG, s));
+    VQKV_CUDA(cudaMallocAsync(&pl, sizeof(float) * n_slots * kG, s));
+    if (n_comp > 0) {
+        VQKV_CUDA(cudaMallocAsync(&lut, sizeof(float4) * a.n_pairs * ng * R * kGS, s));
+        VQKV_CUDA(cudaMallocAsync(&acc, sizeof(float4) * std::max<uint64_t>(1, uint64_t(n_main) * hquads), s));
         ProfScope ps("attend_lut_build", s);
         if (lut_tc_ok(ks)) {
             // tensor-core LUT GEMM (VQKV_LUT_FFMA=1 selects the FFMA kernel below)
@@ -1147,83 +1028,75 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
             uint32_t maxch = 0;
             for (const auto& st : ks.stages) maxch = std::max(maxch, (st.size + 127) / 128);
             lut_tc_kernel<<<dim3(maxch, ks.n), 160, kLutTcSmem, s>>>(ks.d_eff16, ks.d_eff16lo, ks.d_stages, qh, ql, qs,
-                                                                    a.n_pairs, qt, kent, lut);
+                                                                    a.n_pairs, qt, ng, R, lut);
             launch_check("lut_tc_kernel");
             VQKV_CUDA(cudaFreeAsync(qh, s));
             VQKV_CUDA(cudaFreeAsync(ql, s));
             VQKV_CUDA(cudaFreeAsync(qs, s));
         } else {
-        LutArgs la{a.q_dev, ks.d_eff, ks.d_stages, ks.n, kent, float(scale), lut};
-        dim3 grid(unsigned((kent + kLutEntries - 1) / kLutEntries), (a.n_pairs + 7) / 8);
-        const int lsmem = int(sizeof(float) * (8 * kG * kD + kLutEntries * kLutStride));
-        VQKV_CUDA(cudaFuncSetAttribute(lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem));
-        lut_kernel<<<grid, 256, lsmem, s>>>(la, a.n_pairs);
-        launch_check("lut_kernel");
+            LutArgs la{a.q_dev, ks.d_eff, ks.d_stages, ks.n, ks.total_rows, float(scale), lut, ng, R};
+            dim3 grid(unsigned((ks.total_rows + kLutEntries - 1) / kLutEntries), (a.n_pairs + 7) / 8);
+            const int lsmem = int(sizeof(float) * (8 * kG * kD + kLutEntries * kLutStride));
+            VQKV_CUDA(cudaFuncSetAttribute(lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem));
+            lut_kernel<<<grid, 256, lsmem, s>>>(la, a.n_pairs);
+            launch_check("lut_kernel");
         }
-        if (i16) {
-            VQKV_CUDA(cudaMallocAsync(&lut16, sizeof(uint2) * a.n_pairs * kent, s));
-            VQKV_CUDA(cudaMallocAsync(&dq, sizeof(float) * a.n_pairs * kG, s));
-            lut_int16_kernel<<<a.n_pairs, 1024, 0, s>>>(lut, kent, lut16, dq);
-            launch_check("lut_int16_kernel");
+        if (ks.n % kGS) {
+            lut_zero_missing_kernel<<<a.n_pairs, 32, 0, s>>>(lut, ng, R, ks.n);
+            launch_check("lut_zero_missing_kernel");
         }
     }
     {
         ProfScope ps("attend", s);
-        const uint64_t kpb = payload_bytes(ks.row_bits, a.n_comp), vpb = payload_bytes(vs.row_bits, a.n_comp);
-        const uint64_t kstr = a.kcodes_stride ? a.kcodes_stride : kpb, vstr = a.vcodes_stride ? a.vcodes_stride : vpb;
-        MainArgs ma{a.q_dev, a.init_k_dev, a.init_v_dev, a.n_init, a.kcodes_dev, a.vcodes_dev, a.n_comp,
-                    a.local_k_dev, a.local_v_dev, a.n_local, ks.d_stages, ks.n, ks.row_bits, kstr, kent,
-                    vs.d_stages, vs.n, vs.row_bits, vstr, vent, lut,
-                    // end of the last pair's payload: reads stop here (earlier pairs may read into the next)
-                    a.kcodes_dev + uint64_t(a.n_pairs - 1) * kstr + kpb,
-                    a.vcodes_dev + uint64_t(a.n_pairs - 1) * vstr + vpb, float(scale), n_splits,
-                    ph, po, pm, pl, a.init_stride ? a.init_stride : a.n_init,
-                    a.local_stride ? a.local_stride : a.n_local, a.kcodes_cap, lut16, dq};
-        {  // per launch (per-device attribute)
-            VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(kMainSmem + kAlignSlack)));
-            VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(kGmSmem + kAlignSlack)));
-            VQKV_CUDA(cudaFuncSetAttribute(attend_lut_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(kGmSmem + kAlignSlack)));
-        }
-        dim3 grid(n_splits + 1, a.n_pairs);
-        if (i16)
-            attend_lut_kernel<2><<<grid, kAttThreads, kGmSmem + kAlignSlack, s>>>(ma);
-        else if (a.kcodes_layout == VQKV_KEYCODES_GROUP_MAJOR)
-            attend_lut_kernel<1><<<grid, kAttThreads, kGmSmem + kAlignSlack, s>>>(ma);
-        else
-            attend_lut_kernel<0><<<grid, kAttThreads, kMainSmem + kAlignSlack, s>>>(ma);
-        launch_check("attend_lut_kernel");
+        const uint64_t vpb = payload_bytes(vs.row_bits, n_comp);
+        const uint64_t vstr = a.vcodes_stride ? a.vcodes_stride : vpb;
+        MainArgs ma{};
+        ma.q = a.q_dev;
+        ma.init_k = a.init_k_dev;
+        ma.init_v = a.init_v_dev;
+        ma.n_init = a.n_init;
+        ma.local_k = a.local_k_dev;
+        ma.local_v = a.local_v_dev;
+        ma.n_local = a.n_local;
+        ma.init_stride = a.init_stride ? a.init_stride : a.n_init;
+        ma.local_stride = a.local_stride ? a.local_stride : a.n_local;
+        ma.scale = float(scale);
+        ma.lut = lut;
+        ma.ng = ng;
+        ma.R = R;
+        ma.krec = krec;
+        ma.krec_stride = kstride;
+        ma.cap = cap;
+        ma.vcodes = a.vcodes_dev;
+        ma.vstride = vstr;
+        ma.vrow_bits = vs.row_bits;
+        // end of the last pair's value payload: reads stop here (earlier pairs may read into the next)
+        ma.vend = n_comp ? a.vcodes_dev + uint64_t(a.n_pairs - 1) * vstr + vpb : nullptr;
+        ma.vst = vs.d_stages;
+        ma.vn = vs.n;
+        ma.vhalves = vhalves;
+        ma.Rv = Rv;
+        ma.veff = vs.d_eff;
+        ma.n_comp = n_comp;
+        ma.ctas_per_pair = std::max<uint32_t>(cpp, 1);
+        ma.n_main = n_main;
+        ma.tok_per_cta = tpc;
+        ma.acc = acc;
+        ma.part_o = po;
+        ma.part_m = pm;
+        ma.part_l = pl;
+        VQKV_CUDA(cudaFuncSetAttribute(attend_atr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMainSmem)));
+        attend_atr_kernel<<<n_slots, kThreads, kMainSmem, s>>>(ma);
+        launch_check("attend_atr_kernel");
     }
     {
         ProfScope ps("attend_combine", s);
-        float *w = nullptr, *ML = nullptr, *acc = nullptr;
-        VQKV_CUDA(cudaMallocAsync(&w, sizeof(float) * a.n_pairs * (n_splits + 1) * kG, s));
-        VQKV_CUDA(cudaMallocAsync(&ML, sizeof(float) * a.n_pairs * kG * 2, s));
-        VQKV_CUDA(cudaMallocAsync(&acc, sizeof(float) * a.n_pairs * kG * kD, s));
-        VQKV_CUDA(cudaMemsetAsync(acc, 0, sizeof(float) * a.n_pairs * kG * kD, s));
-        lut_weights_kernel<<<(a.n_pairs * kG + 127) / 128, 128, 0, s>>>(pm, pl, n_splits, a.n_pairs, w, ML);
-        launch_check("lut_weights_kernel");
-        if (n_splits > 0) {
-            dim3 g2(unsigned((vent + 255) / 256), a.n_pairs);
-            lut_contract_kernel<<<g2, 512, 0, s>>>(ph, w, n_splits, vs.d_eff, vent, acc);
-            launch_check("lut_contract_kernel");
-        }
-        const uint64_t n = uint64_t(a.n_pairs) * kG * kD;
-        lut_finish_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(acc, po, w, ML, n_splits, a.n_pairs, a.out_dev,
-                                                                   a.lse_dev);
-        launch_check("lut_finish_kernel");
-        VQKV_CUDA(cudaFreeAsync(w, s));
-        VQKV_CUDA(cudaFreeAsync(ML, s));
-        VQKV_CUDA(cudaFreeAsync(acc, s));
+        atr_combine_kernel<<<a.n_pairs, kD, 0, s>>>(po, pm, pl, cpp, n_main, a.out_dev, a.lse_dev);
+        launch_check("atr_combine_kernel");
     }
-    VQKV_CUDA(cudaFreeAsync(lut, s));
-    if (i16) {
-        VQKV_CUDA(cudaFreeAsync(lut16, s));
-        VQKV_CUDA(cudaFreeAsync(dq, s));
-    }
-    VQKV_CUDA(cudaFreeAsync(ph, s));
+    if (lut) VQKV_CUDA(cudaFreeAsync(lut, s));
+    if (acc) VQKV_CUDA(cudaFreeAsync(acc, s));
+    if (ktmp) VQKV_CUDA(cudaFreeAsync(ktmp, s));
     VQKV_CUDA(cudaFreeAsync(po, s));
     VQKV_CUDA(cudaFreeAsync(pm, s));
     VQKV_CUDA(cudaFreeAsync(pl, s));

@@ -656,6 +656,23 @@ int vqkv_keycodes_to_gm(vqkv_stack_t ks, const uint8_t* payload, uint64_t payloa
     });
 }
 
+int vqkv_keycodes_from_gm(vqkv_stack_t ks, const uint8_t* gm, uint64_t cap, uint64_t gm_stride, uint32_t n_pairs,
+                          uint64_t count, uint8_t* payload, uint64_t payload_stride, void* stream) {
+    return guard([&] {
+        check_stack(ks);
+        need(vqkv_dev::gm_supported(*ks), VQKV_INVALID_INPUT, "stack has no group-major layout (D = 128, <= 1024 entries)");
+        need(cap % 16 == 0 && count <= cap, VQKV_INVALID_INPUT, "records out of the group-major capacity");
+        const uint64_t gb = vqkv_dev::gm_pair_bytes(*ks, cap), pb = payload_bytes(ks->row_bits, count);
+        need(gm_stride == 0 || gm_stride >= gb, VQKV_INVALID_INPUT, "gm_stride below the buffer size");
+        need(payload_stride == 0 || payload_stride >= pb, VQKV_INVALID_INPUT, "payload_stride below the payload size");
+        if (n_pairs == 0 || count == 0) return;
+        need(payload && gm, VQKV_INVALID_INPUT, "null device buffer");
+        DeviceGuard g(ks->device);
+        vqkv_dev::launch_keycodes_from_gm(*ks, gm, cap, gm_stride ? gm_stride : gb, n_pairs, count, payload,
+                                          payload_stride ? payload_stride : pb, as_stream(stream));
+    });
+}
+
 int vqkv_quantize_rows_host(vqkv_stack_t s, const float* xs, uint64_t rows, uint64_t sb, uint8_t* payload, float* norms,
                             float* residuals) {
     return guard([&] {

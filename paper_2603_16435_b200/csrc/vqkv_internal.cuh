@@ -233,6 +233,9 @@ void launch_keycodes_to_gm(const vqkv_stack_s& ks, const uint8_t* payload, uint6
                            uint64_t dst_row, cudaStream_t s);
 void launch_attend_raw(int device, const float* keys, const float* values, uint64_t rows, uint32_t dk, uint32_t dv,
                        const float* q, double scale, float* out, cudaStream_t s);
+void launch_keycodes_from_gm(const vqkv_stack_s& ks, const uint8_t* gm, uint64_t cap, uint64_t gm_stride,
+                             uint32_t n_pairs, uint64_t count, uint8_t* payload, uint64_t payload_stride,
+                             cudaStream_t s);
 void launch_lse_combine(const float* o, const float* lse, uint32_t parts, uint64_t rows, uint32_t dv, float* out,
                         float* out_lse, cudaStream_t s);
 

@@ -168,6 +168,24 @@ def keycodes_to_gm(kstack, payload: torch.Tensor, count: int, gm: Optional[torch
     return gm
 
 
+def keycodes_from_gm(kstack, gm: torch.Tensor, cap: int, count: int,
+                     payload: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """CodeMatrix payloads [n_pairs, payload_bytes(count)] u8 of records [0, count) of the
+    attention layout gm [n_pairs, keycodes_gm_bytes(cap)] (inverse of keycodes_to_gm)."""
+    kd = _dev(kstack)
+    if gm.dim() == 1:
+        gm = gm.unsqueeze(0)
+    gstride = _pair_stride(gm, torch.uint8, "gm", 1)
+    n_pairs = gm.shape[0]
+    pb = kd.payload_bytes(count)
+    if payload is None:
+        payload = torch.empty((n_pairs, max(pb, 1)), dtype=torch.uint8, device=gm.device)
+    pstride = _pair_stride(payload, torch.uint8, "payload", 1)
+    _lib.call("vqkv_keycodes_from_gm", kd.h, gm.data_ptr(), cap, gstride, n_pairs, count, payload.data_ptr(), pstride,
+              _stream(gm))
+    return payload
+
+
 def attend_gm_supported(kstack, vstack, n_pairs: int, group: int, n_init: int, n_comp: int, n_local: int) -> bool:
     """Whether attend_decode takes group-major key codes for this shape (the LUT path covers it)."""
     import ctypes as C

@@ -306,11 +306,11 @@ def test_cache_snapshot_rejects_out_of_range_codes(torch_mod):
         DeviceCacheState.load_snapshots([io.BytesIO(bytes(bad))], pk, pv)
 
 
-def test_cache_group_major_mirror(torch_mod, tmp_path, monkeypatch):
-    """The group-major key-code mirror: kept in step through prefill, flushes and capacity
-    growth (records rebuilt from the payload) and snapshot loads; attention over it equals
-    attention over the CodeMatrix rows and the oracle (fp32 LUT)."""
-    monkeypatch.delenv("VQKV_ATTEND_INT16", raising=False)
+def test_cache_attention_records_only(torch_mod, tmp_path):
+    """The key codes live only as attention records (no CodeMatrix copy on the device): kept in
+    step through prefill, flushes and capacity growth (planes copied) and snapshot loads; the
+    CodeMatrix rows rebuilt from them equal the rows-layout cache's payload byte for byte, and
+    attention over them equals attention over the rows-layout cache bit for bit and the oracle."""
     torch = torch_mod
     from paper_2603_16435_b200 import device as Dv
     from paper_2603_16435_b200.cache import DeviceCacheState
@@ -321,7 +321,7 @@ def test_cache_group_major_mirror(torch_mod, tmp_path, monkeypatch):
     S, init_len, local_len, L0 = 2, 4, 64, 2000
     dc = DeviceCacheState(pk, pv, S, init_len, local_len)
     rows = DeviceCacheState(pk, pv, S, init_len, local_len, attn_layout="rows")
-    assert dc.attn_layout == "group_major" and rows.kgm is None
+    assert dc.attn_layout == "group_major" and dc.kpay is None and rows.kgm is None
     ref = O.Cache(ks, vs, init_len, local_len, False)
     x = rng.matrix(S * L0, 128).reshape(S, L0, 128)
     y = rng.matrix(S * L0, 128).reshape(S, L0, 128)
@@ -332,14 +332,15 @@ def test_cache_group_major_mirror(torch_mod, tmp_path, monkeypatch):
     qt = torch.from_numpy(q).cuda()
 
     def check(c):
-        gm = Dv.keycodes_to_gm(pk, c.kpay, c.n_comp, cap=c.gm_cap)
-        assert torch.equal(gm, c.kgm[:, : gm.shape[1]])
+        assert torch.equal(c.codes(0)[0], rows.codes(0)[0])
         o, l = c.attend(qt)
         o2, l2 = rows.attend(qt)
-        assert torch.equal(l, l2) and torch.allclose(o, o2, rtol=1e-5, atol=1e-5)
+        assert torch.equal(l, l2) and torch.equal(o, o2)
         for g in range(4):
             r = ref.attend(q[0, g])
             assert np.abs(o[0, g].cpu().numpy() - r).max() <= ATT_TOL * max(1.0, np.abs(r).max())
+        rp, _ = ref.codes(0)
+        assert np.array_equal(c.codes(0)[0][0].cpu().numpy(), rp)
 
     check(dc)
     cap0 = dc.cap_rows
@@ -350,12 +351,16 @@ def test_cache_group_major_mirror(torch_mod, tmp_path, monkeypatch):
             c.append_token(torch.from_numpy(k1).cuda(), torch.from_numpy(v1).cuda())
     assert dc.cap_rows > cap0 and dc.counts()["batched"] >= 2
     check(dc)
-    assert dc.memory_report()["attention_layout_bytes"] == dc.n_comp * 5 * 2
-    p = str(tmp_path / "s.vqks")
+    # 5 key stages = 1 group of 8: 10 B per token, + 3 x 6-bit value fields
+    assert dc.memory_report()["device_code_bytes"] == dc.n_comp * 10 + pv_bytes(dc)
     paths = []
     for i in range(S):
         paths.append(str(tmp_path / f"s{i}.vqks"))
         dc.save_snapshot(i, paths[-1])
     back = DeviceCacheState.load_snapshots(paths, pk, pv)
-    assert back.attn_layout == "group_major"
+    assert back.attn_layout == "group_major" and back.kpay is None
     check(back)
+
+
+def pv_bytes(c):
+    return c.vd.payload_bytes(c.n_comp)
