@@ -72,9 +72,11 @@ constexpr int kChunk = kThreads * kTok;        // 8192 tokens per chunk
 constexpr int kGS = 8;                         // key stages per LUT group (one 128 B row)
 constexpr uint32_t kRowBytes = kGS * 16;       // 8 slots x float4
 constexpr uint32_t kLutBytes = 1024 * kRowBytes;  // 128 KB: one group, up to 1024 code values
-constexpr uint32_t kMaxVHalves = 8;            // value stages <= 64
+constexpr uint32_t kMaxVStages = 64;
 constexpr uint32_t kSmemCtl = 16384;           // barriers, reductions, value descriptors (raw CTAs: 10 KB)
-constexpr uint32_t kMainSmem = kLutBytes + kSmemCtl;
+constexpr uint32_t kQueueCap = 64;             // per-warp queue of tokens with a nonzero weight
+constexpr uint32_t kQueueBytes = (kThreads / 32) * kQueueCap * (1 + 4) * 4;
+constexpr uint32_t kMainSmem = kLutBytes + kSmemCtl + kQueueBytes;
 constexpr float kQuantum = 268435456.0f;       // 2^28: p / u_c = p * 2^28 / l_c
 
 // LUT element offset (in float4) of (pair, stage s, code j)
@@ -342,13 +344,17 @@ struct MainArgs {
     uint64_t vstride, vrow_bits;
     const uint8_t* vend;     // end of the last pair's value payload (reads stop here)
     const StageInfo* vst;
-    uint32_t vn, vhalves, Rv;
+    uint32_t vn;
+    uint32_t vnwin;          // 64-bit windows of the value row (stages grouped, <= 64 bits each)
+    const uint2* vwin;       // [vnwin]: (start bit, s0 | s1 << 8)
+    const uint8_t* vwin_of;  // [vn]: window of each stage
+    uint32_t hwords;         // histogram words: 4 x sum S_v
     const float* veff;
     uint64_t n_comp;
     uint32_t ctas_per_pair;  // main CTAs per pair
     uint32_t n_main;         // main CTAs in the grid (raw CTAs follow)
     uint64_t tok_per_cta;    // multiple of 512
-    float4* acc;             // per main CTA: fp32 histogram accumulator [vhalves][Rv][8 slots] x float4 (heads)
+    float* acc;              // per main CTA: fp32 histogram accumulator [stage][head][code] (hwords)
     float* part_o;           // [n_main + pairs][G][D]: unnormalised sum p v
     float* part_m;           // [n_main + pairs][G]
     float* part_l;           // [n_main + pairs][G]
@@ -578,21 +584,30 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
     uint8_t* const ctl = smem_raw + kLutBytes;
     uint64_t* bar = reinterpret_cast<uint64_t*>(ctl);
     float4* red = reinterpret_cast<float4*>(ctl + 64);           // 16 x float4
-    uint32_t* vdesc = reinterpret_cast<uint32_t*>(ctl + 512);     // [halves][32 lanes]
-    uint32_t* vrow = vdesc + kMaxVHalves * 32;                    // [64]: first effective row of stage s
-    uint32_t* vsz = vrow + 64;                                    // [64]: stage sizes
-    const uint32_t HW = a.vhalves * a.Rv * 32u;                   // histogram words (x4 heads per quad)
+    // value stage tables: histogram word offset (4 x first entry: [stage][head][code] layout),
+    // size, field position within its 64-bit window | bits << 8; window start bits and stage ranges
+    uint32_t* vbase = reinterpret_cast<uint32_t*>(ctl + 512);    // [64]
+    uint32_t* vsz = vbase + 64;                                   // [64]
+    uint32_t* vfld = vsz + 64;                                    // [64]
+    uint32_t* vrow = vfld + 64;                                   // [64]: first effective row of stage s
+    uint32_t* wstart = vrow + 64;                                 // [16]
+    uint32_t* wrange = wstart + 16;                               // [16]: s0 | s1 << 8
+    uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw + kLutBytes + kSmemCtl) + warp * (kQueueCap * (1 + kG));
+    const uint32_t HW = a.hwords;                                 // histogram words: 4 x sum S_v
     if (tid == 0) {
         ptx::mbar_init(ptx::smem_u32(bar), 1);
         ptx::fence_mbar_init();
     }
-    if (tid < a.vhalves * 32u) {  // lane (stage slot, head) of every half: the stage's field in the row
-        const uint32_t h = tid >> 5, s = h * 8u + ((tid & 31u) >> 2);
-        vdesc[tid] = (s < a.vn) ? (0x80000000u | (a.vst[s].bits << 16) | a.vst[s].bit_off) : 0u;
-    }
     if (tid < a.vn) {
-        vrow[tid] = uint32_t(a.vst[tid].eff_off / kD);
-        vsz[tid] = a.vst[tid].size;
+        const StageInfo si = a.vst[tid];
+        vrow[tid] = uint32_t(si.eff_off / kD);
+        vbase[tid] = 4u * vrow[tid];
+        vsz[tid] = si.size;
+        vfld[tid] = (si.bit_off - a.vwin[a.vwin_of[tid]].x) | (si.bits << 8);
+    }
+    if (tid < a.vnwin) {
+        wstart[tid] = a.vwin[tid].x;
+        wrange[tid] = a.vwin[tid].y;
     }
     __syncthreads();
 
@@ -611,18 +626,16 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
         const uint8_t* seg = krec + uint64_t(g) * a.cap * 10u;
         ptx_prefetch_records(seg, a.cap, c0, n);
     };
-    // value codes: 32-bit words relative to the 4 B-aligned start of the pair's payload
+    // value codes: 64-bit words relative to the 8 B-aligned start of the pair's payload
     const uint8_t* vc = a.vcodes + uint64_t(pair) * a.vstride;
-    const uint32_t* vc32 = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(vc) & ~uintptr_t(3));
-    const uint32_t vbase_bits = uint32_t((reinterpret_cast<uintptr_t>(vc) & 3u) * 8u);
-    const uint64_t vwords64 = (reinterpret_cast<uintptr_t>(a.vend) - reinterpret_cast<uintptr_t>(vc32)) >> 2;
-    const uint32_t vwords = vwords64 > 0xffffffffull ? 0xffffffffu : uint32_t(vwords64);
-    const uint32_t vrow32 = uint32_t(a.vrow_bits);
+    const uint64_t* vc64 = reinterpret_cast<const uint64_t*>(reinterpret_cast<uintptr_t>(vc) & ~uintptr_t(7));
+    const uint32_t vbase_bits = uint32_t((reinterpret_cast<uintptr_t>(vc) & 7u) * 8u);
+    const uint64_t vwords = (reinterpret_cast<uintptr_t>(a.vend) - reinterpret_cast<uintptr_t>(vc64)) >> 3;
     const uint32_t l7 = (lane & 7u) << 4;  // this lane's slot rotation (token & 7 == lane & 7)
 
     float4 M = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY), Lrun = make_float4(0.f, 0.f, 0.f, 0.f);
     bool first = true;
-    float4* accp = a.acc + uint64_t(cta) * (HW / 4u);
+    float* accp = a.acc + uint64_t(cta) * HW;
     uint32_t phase = 0;
     if (tid == 0 && t0 < t1) {
         prefetch_records(0, t0, uint32_t(umin64(kChunk, t1 - t0)));
@@ -711,38 +724,74 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
             P[k][2] = __float2uint_rn(lg[k][1].x * qs.z);
             P[k][3] = __float2uint_rn(lg[k][1].y * qs.w);
         }
-        // ---- values: int32 histograms [half][code][stage slot][head] over the LUT buffer
+        // ---- values: int32 histograms [stage][head][code] over the LUT buffer.  The tokens with a
+        // nonzero weight are compacted into a per-warp queue and processed 32 at a time, lane =
+        // token: its value row is read in 64-bit windows and every (stage, head) bin gets one
+        // shared atomic (bank = code mod 32).
         for (uint32_t i = tid; i < HW / 4u; i += kThreads) reinterpret_cast<uint4*>(lutb)[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
-        const uint32_t myg = lane & 3u;
+        auto hist_token = [&](uint64_t t, const uint32_t (&Pv)[kG]) {
+            const uint64_t rbit = uint64_t(vbase_bits) + t * a.vrow_bits;
+            for (uint32_t w = 0; w < a.vnwin; ++w) {
+                const uint64_t pos = rbit + wstart[w];
+                const uint64_t wi = pos >> 6;
+                uint64_t x;
+                if (wi + 1 < vwords) {
+                    const uint64_t lo = __ldg(vc64 + wi), hi = __ldg(vc64 + wi + 1);
+                    const uint32_t sh = uint32_t(pos & 63u);
+                    x = sh ? ((lo >> sh) | (hi << (64u - sh))) : lo;
+                } else {  // the last words of the buffer
+                    x = read_bits64(vc, t * a.vrow_bits + wstart[w], a.vend);
+                }
+                const uint32_t r = wrange[w];
+                for (uint32_t st = r & 0xFFu; st < (r >> 8); ++st) {
+                    const uint32_t f = vfld[st];
+                    const uint32_t z = uint32_t(x >> (f & 0xFFu)) & ((1u << (f >> 8)) - 1u);
+                    const uint32_t b = lut_s + (vbase[st] + z) * 4u, S4 = vsz[st] * 4u;
 #pragma unroll
-        for (int k = 0; k < kTok; ++k) {
-            const bool act = (uint32_t(k) * kThreads + tid < nt) && ((P[k][0] | P[k][1] | P[k][2] | P[k][3]) != 0u);
-            uint32_t m = __ballot_sync(0xffffffffu, act);
-            while (m) {
-                const int src = __ffs(m) - 1;
-                m &= m - 1u;
-                const uint32_t q0 = __shfl_sync(0xffffffffu, P[k][0], src), q1 = __shfl_sync(0xffffffffu, P[k][1], src);
-                const uint32_t q2 = __shfl_sync(0xffffffffu, P[k][2], src), q3 = __shfl_sync(0xffffffffu, P[k][3], src);
-                const uint32_t myP = myg == 0u ? q0 : (myg == 1u ? q1 : (myg == 2u ? q2 : q3));
-                const uint64_t t = c0 + uint64_t(k) * kThreads + warp * 32u + uint32_t(src);
-                const uint32_t rowbit = vbase_bits + uint32_t(t) * vrow32;
-                for (uint32_t h = 0; h < a.vhalves; ++h) {
-                    const uint32_t d = vdesc[h * 32u + lane];
-                    if (d >> 31) {
-                        const uint32_t pos = rowbit + (d & 0xFFFFu), wi = pos >> 5;
-                        uint32_t z;
-                        if (wi + 1u < vwords) {
-                            z = __funnelshift_r(__ldg(vc32 + wi), __ldg(vc32 + wi + 1u), pos & 31u);
-                        } else {  // the last words of the buffer
-                            z = uint32_t(read_bits64(vc, t * a.vrow_bits + (d & 0xFFFFu), a.vend));
-                        }
-                        z &= (1u << ((d >> 16) & 31u)) - 1u;
-                        if (myP) red_shared_add(lut_s + ((h * a.Rv + z) * 32u + lane) * 4u, myP);
-                    }
+                    for (int g = 0; g < kG; ++g)
+                        if (Pv[g]) red_shared_add(b + uint32_t(g) * S4, Pv[g]);
                 }
             }
+        };
+        uint32_t* qt = queue;
+        uint32_t* qP = queue + kQueueCap;
+        uint32_t qlen = 0;
+        auto flush = [&](uint32_t n) {
+            if (lane < n) {
+                uint32_t Pv[kG];
+#pragma unroll
+                for (int g = 0; g < kG; ++g) Pv[g] = qP[lane * kG + g];
+                hist_token(c0 + qt[lane], Pv);
+            }
+        };
+#pragma unroll
+        for (int k = 0; k < kTok; ++k) {
+            const uint32_t lt = uint32_t(k) * kThreads + tid;  // token within the chunk
+            const bool act = lt < nt && (P[k][0] | P[k][1] | P[k][2] | P[k][3]) != 0u;
+            const uint32_t mask = __ballot_sync(0xffffffffu, act);
+            if (act) {
+                const uint32_t pos = qlen + __popc(mask & ((1u << lane) - 1u));
+                qt[pos] = lt;
+#pragma unroll
+                for (int g = 0; g < kG; ++g) qP[pos * kG + g] = P[k][g];
+            }
+            qlen += __popc(mask);
+            if (qlen >= 32u) {
+                __syncwarp();
+                flush(32u);
+                __syncwarp();
+                if (lane + 32u < qlen) {  // keep the overflow for the next batch
+                    qt[lane] = qt[lane + 32u];
+#pragma unroll
+                    for (int g = 0; g < kG; ++g) qP[lane * kG + g] = qP[(lane + 32u) * kG + g];
+                }
+                __syncwarp();
+                qlen -= 32u;
+            }
         }
+        __syncwarp();
+        flush(qlen);
         __syncthreads();
         // ---- fold the chunk into the CTA's accumulator, rescaled to the running max
         const float4 Mn = make_float4(fmaxf(M.x, mc.x), fmaxf(M.y, mc.y), fmaxf(M.z, mc.z), fmaxf(M.w, mc.w));
@@ -751,14 +800,20 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
         const float4 ec = make_float4(__expf(mc.x - Mn.x), __expf(mc.y - Mn.y), __expf(mc.z - Mn.z), __expf(mc.w - Mn.w));
         const float4 be = make_float4(lc.x / kQuantum * ec.x, lc.y / kQuantum * ec.y, lc.z / kQuantum * ec.z,
                                       lc.w / kQuantum * ec.w);
-        for (uint32_t i = tid; i < HW / 4u; i += kThreads) {
-            const uint4 hq = reinterpret_cast<const uint4*>(lutb)[i];
-            float4 v = make_float4(float(hq.x) * be.x, float(hq.y) * be.y, float(hq.z) * be.z, float(hq.w) * be.w);
-            if (!first) {
-                const float4 o = ldcg4(accp + i);
-                v = make_float4(fmaf(o.x, al.x, v.x), fmaf(o.y, al.y, v.y), fmaf(o.z, al.z, v.z), fmaf(o.w, al.w, v.w));
+        {
+            const uint32_t* Hw = reinterpret_cast<const uint32_t*>(lutb);
+            for (uint32_t st = 0; st < a.vn; ++st) {  // words of stage st: [head][code]
+                const uint32_t b = vbase[st], S = vsz[st];
+#pragma unroll 4
+                for (uint32_t i = tid; i < 4u * S; i += kThreads) {
+                    const uint32_t g = i / S;
+                    const float bg = g == 0u ? be.x : (g == 1u ? be.y : (g == 2u ? be.z : be.w));
+                    const float ag = g == 0u ? al.x : (g == 1u ? al.y : (g == 2u ? al.z : al.w));
+                    float v = float(Hw[b + i]) * bg;
+                    if (!first) v = fmaf(__ldcg(accp + b + i), ag, v);
+                    __stcg(accp + b + i, v);
+                }
             }
-            stcg4(accp + i, v);
         }
         Lrun = make_float4(fmaf(Lrun.x, al.x, lc.x * ec.x), fmaf(Lrun.y, al.y, lc.y * ec.y), fmaf(Lrun.z, al.z, lc.z * ec.z),
                            fmaf(Lrun.w, al.w, lc.w * ec.w));
@@ -768,28 +823,20 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
         if (tid == 0 && c0 + kChunk < t1) issue(0);
     }
 
-    // ---- contraction: o[g][d] = sum_{h, j, slot} acc[h][j][slot][g] * e_{8h+slot}[j][d]
+    // ---- contraction: o[g][d] = sum_{s, j} acc[s][g][j] * e_s[j][d]
     float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
     if (!first) {
-        __threadfence_block();
-        const uint32_t d = tid & (kD - 1u), qtr = tid >> 7;  // 4 quarters of the (half, code) rows
-        for (uint32_t r = qtr; r < a.vhalves * a.Rv; r += 4u) {
-            const uint32_t h = r / a.Rv, j = r - h * a.Rv;
-            float4 hv[kGS];
-            float x[kGS];
-#pragma unroll
-            for (int sl = 0; sl < kGS; ++sl) {
-                const uint32_t s = h * 8u + uint32_t(sl);
-                const bool ok = s < a.vn && j < vsz[s < 64u ? s : 0u];
-                hv[sl] = ok ? ldcg4(accp + uint64_t(r) * kGS + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
-                x[sl] = ok ? __ldg(a.veff + (uint64_t(vrow[s]) + j) * kD + d) : 0.f;
-            }
-#pragma unroll
-            for (int sl = 0; sl < kGS; ++sl) {
-                o.x = fmaf(hv[sl].x, x[sl], o.x);
-                o.y = fmaf(hv[sl].y, x[sl], o.y);
-                o.z = fmaf(hv[sl].z, x[sl], o.z);
-                o.w = fmaf(hv[sl].w, x[sl], o.w);
+        const uint32_t d = tid & (kD - 1u), qtr = tid >> 7;  // 4 quarters of each stage's codes
+        for (uint32_t st = 0; st < a.vn; ++st) {
+            const uint32_t b = vbase[st], S = vsz[st];
+            const float* e = a.veff + uint64_t(vrow[st]) * kD + d;
+#pragma unroll 4
+            for (uint32_t j = qtr; j < S; j += 4u) {
+                const float x = __ldg(e + uint64_t(j) * kD);
+                o.x = fmaf(__ldcg(accp + b + j), x, o.x);
+                o.y = fmaf(__ldcg(accp + b + S + j), x, o.y);
+                o.z = fmaf(__ldcg(accp + b + 2u * S + j), x, o.z);
+                o.w = fmaf(__ldcg(accp + b + 3u * S + j), x, o.w);
             }
         }
     }
@@ -933,16 +980,30 @@ bool gm_supported(const vqkv_stack_s& ks) {
     return true;
 }
 
+// 64-bit windows of a value row: consecutive stages whose fields fit in 64 bits from the
+// window's first field (one unaligned 64-bit read per window in the value phase)
+static std::vector<uint2> value_windows(const vqkv_stack_s& vs, std::vector<uint8_t>* of = nullptr) {
+    std::vector<uint2> w;
+    uint32_t s0 = 0;
+    while (s0 < vs.n) {
+        const uint32_t b0 = vs.stages[s0].bit_off;
+        uint32_t s1 = s0;
+        while (s1 < vs.n && vs.stages[s1].bit_off + vs.stages[s1].bits - b0 <= 64) ++s1;
+        if (of)
+            for (uint32_t s = s0; s < s1; ++s) of->push_back(uint8_t(w.size()));
+        w.push_back(make_uint2(b0, s0 | (s1 << 8)));
+        s0 = s1;
+    }
+    return w;
+}
+
 bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a) {
     if (!gm_supported(ks) || vs.dim != kD || a.group != kG) return false;
     if (a.n_init + a.n_local > kChunk) return false;  // the raw CTA keeps one weight per raw row in smem
-    if (vs.n > kMaxVHalves * 8 || vs.row_bits > 0xFFFF) return false;
+    if (vs.n > kMaxVStages || vs.total_rows * 4 * 4 > kLutBytes) return false;  // histograms fit the LUT buffer
     for (const auto& s : vs.stages)
-        if (s.size > 1024 || s.bits > 10) return false;
-    const uint32_t halves = (vs.n + 7) / 8;
-    if (uint64_t(halves) * max_size(vs) * kRowBytes > kLutBytes) return false;  // histograms fit the LUT buffer
-    // 32-bit bit positions inside one pair's value stream (+ alignment slack)
-    if (uint64_t(a.n_comp) * vs.row_bits + 64 >= (1ull << 32)) return false;
+        if (s.bits > 32) return false;
+    if (value_windows(vs).size() > 16) return false;
     return true;
 }
 
@@ -971,7 +1032,7 @@ void launch_keycodes_from_gm(const vqkv_stack_s& ks, const uint8_t* gm, uint64_t
 }
 
 void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s) {
-    const uint32_t ng = key_groups(ks), R = max_size(ks), vhalves = (vs.n + 7) / 8, Rv = max_size(vs);
+    const uint32_t ng = key_groups(ks), R = max_size(ks);
     const double scale = a.scale > 0.0 ? a.scale : 1.0 / std::sqrt(double(kD));
     const uint64_t n_comp = a.n_comp;
     int sms = 148;
@@ -986,7 +1047,9 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         cpp = uint32_t((n_comp + tpc - 1) / tpc);
     }
     const uint32_t n_main = a.n_pairs * cpp, n_slots = n_main + a.n_pairs;
-    const uint64_t hquads = uint64_t(vhalves) * Rv * 8;
+    const uint64_t hwords = vs.total_rows * 4;  // [stage][head][code]
+    std::vector<uint8_t> win_of;
+    const std::vector<uint2> wins = value_windows(vs, &win_of);
     // key records: the caller's attention layout, or transcoded from CodeMatrix rows here
     const uint8_t* krec = a.kcodes_dev;
     uint64_t kstride = 0, cap = a.kcodes_cap;
@@ -1005,14 +1068,18 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         }
     }
     float4* lut = nullptr;
-    float4* acc = nullptr;
+    float* acc = nullptr;
+    uint8_t* vtab = nullptr;  // value windows + stage -> window
+    VQKV_CUDA(cudaMallocAsync(&vtab, sizeof(uint2) * 16 + 64, s));
+    VQKV_CUDA(cudaMemcpyAsync(vtab, wins.data(), sizeof(uint2) * wins.size(), cudaMemcpyHostToDevice, s));
+    VQKV_CUDA(cudaMemcpyAsync(vtab + sizeof(uint2) * 16, win_of.data(), win_of.size(), cudaMemcpyHostToDevice, s));
     float *po = nullptr, *pm = nullptr, *pl = nullptr;
     VQKV_CUDA(cudaMallocAsync(&po, sizeof(float) * n_slots * kG * kD, s));
     VQKV_CUDA(cudaMallocAsync(&pm, sizeof(float) * n_slots * kG, s));
     VQKV_CUDA(cudaMallocAsync(&pl, sizeof(float) * n_slots * kG, s));
     if (n_comp > 0) {
         VQKV_CUDA(cudaMallocAsync(&lut, sizeof(float4) * a.n_pairs * ng * R * kGS, s));
-        VQKV_CUDA(cudaMallocAsync(&acc, sizeof(float4) * std::max<uint64_t>(1, uint64_t(n_main) * hquads), s));
+        VQKV_CUDA(cudaMallocAsync(&acc, sizeof(float) * std::max<uint64_t>(1, uint64_t(n_main) * hwords), s));
         ProfScope ps("attend_lut_build", s);
         if (lut_tc_ok(ks)) {
             // tensor-core LUT GEMM (VQKV_LUT_FFMA=1 selects the FFMA kernel below)
@@ -1074,8 +1141,10 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         ma.vend = n_comp ? a.vcodes_dev + uint64_t(a.n_pairs - 1) * vstr + vpb : nullptr;
         ma.vst = vs.d_stages;
         ma.vn = vs.n;
-        ma.vhalves = vhalves;
-        ma.Rv = Rv;
+        ma.vnwin = uint32_t(wins.size());
+        ma.vwin = reinterpret_cast<const uint2*>(vtab);
+        ma.vwin_of = vtab + sizeof(uint2) * 16;
+        ma.hwords = uint32_t(hwords);
         ma.veff = vs.d_eff;
         ma.n_comp = n_comp;
         ma.ctas_per_pair = std::max<uint32_t>(cpp, 1);
@@ -1097,6 +1166,7 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     if (lut) VQKV_CUDA(cudaFreeAsync(lut, s));
     if (acc) VQKV_CUDA(cudaFreeAsync(acc, s));
     if (ktmp) VQKV_CUDA(cudaFreeAsync(ktmp, s));
+    VQKV_CUDA(cudaFreeAsync(vtab, s));
     VQKV_CUDA(cudaFreeAsync(po, s));
     VQKV_CUDA(cudaFreeAsync(pm, s));
     VQKV_CUDA(cudaFreeAsync(pl, s));

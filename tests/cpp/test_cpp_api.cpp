@@ -172,9 +172,25 @@ int main() {
         float err = 0.f, mx = 1.f;
         for (int64_t i = 0; i < a.size(); ++i) err = std::max(err, std::fabs(a[i] - r[i])), mx = std::max(mx, std::fabs(r[i]));
         report(err <= mx / 128.f, "attend (G=4 LUT kernel) == attend_raw over the logical view (2^-7 tolerance)");
-        report(fr.output_mean_cosine > 0.5 && fr.output_mean_cosine <= 1.0 + 1e-9 && fr.key_intermediate_mse > 0.0 &&
-                   fr.value_intermediate_mse > 0.0 && fr.output_max_abs_err >= 0.0,
-               "fidelity reports cosine, max error and intermediate MSE");
+        {  // attention.cpp:104-115 query by query, from the same public calls
+            double err = 0.0, cs = 0.0;
+            for (int64_t i = 0; i < qs.rows(); ++i) {
+                VectorF qi = detail::row_of(qs, i);
+                VectorF c = attend(state, qi, cfg), w = attend_raw(keys, values, qi, cfg);
+                double dot = 0.0, nc = 0.0, nw = 0.0;
+                for (int64_t d = 0; d < c.size(); ++d) {
+                    err = std::max(err, double(std::fabs(c[d] - w[d])));
+                    dot += double(c[d]) * w[d];
+                    nc += double(c[d]) * c[d];
+                    nw += double(w[d]) * w[d];
+                }
+                cs += dot / (std::sqrt(nc) * std::sqrt(nw));
+            }
+            cs /= double(qs.rows());
+            report(std::fabs(fr.output_max_abs_err - err) < 1e-6 && std::fabs(fr.output_mean_cosine - cs) < 1e-9 &&
+                       fr.key_intermediate_mse > 0.0 && fr.value_intermediate_mse > 0.0,
+                   "fidelity reports cosine, max error and intermediate MSE");
+        }
         bool threw = false;
         try {
             fidelity(state, random_matrix(rng, 5, 128), values, qs, cfg);
