@@ -634,17 +634,40 @@ def run_ours(args, rank, world, local):
         knh = torch.empty((ns, middle), dtype=torch.float32, pin_memory=True)
         vnh = torch.empty((ns, middle), dtype=torch.float32, pin_memory=True)
 
+        # K and V are independent calls on their own caller streams, and consecutive steps alternate
+        # between two such stream pairs (double buffering, as a serving loop would): each call's
+        # copy-in is ordered after its own stream's earlier work (stream semantics), so the next
+        # step's copies overlap this step's encodes
+        e2e_streams = [(torch.cuda.Stream(), torch.cuda.Stream()) for _ in range(2)]
+        e2e_i = [0]
+
+        def e2e_fork():
+            main = torch.cuda.current_stream()
+            for pair in e2e_streams:
+                for st in pair:
+                    st.wait_stream(main)
+
+        def e2e_join():
+            main = torch.cuda.current_stream()
+            for pair in e2e_streams:
+                for st in pair:
+                    main.wait_stream(st)
+
         def e2e_step():
-            # queued back to back (the value copies overlap the key encodes); the
-            # stream synchronization below puts every result on the host
-            Dv.quantize_streams_host(kst, Kh, payload_host=kph, norms_host=knh, blocking=False)
-            Dv.quantize_streams_host(vst, Vh, payload_host=vph, norms_host=vnh, blocking=False)
+            sK, sV = e2e_streams[e2e_i[0] & 1]
+            e2e_i[0] += 1
+            with torch.cuda.stream(sK):
+                Dv.quantize_streams_host(kst, Kh, payload_host=kph, norms_host=knh, blocking=False)
+            with torch.cuda.stream(sV):
+                Dv.quantize_streams_host(vst, Vh, payload_host=vph, norms_host=vnh, blocking=False)
 
         n_e2e = max(1, min(args.steps, 3))
         # warm-up as many back-to-back steps as are timed: the stream-ordered staging pool grows
         # to its steady-state size (mapping memory) before the timed region
+        e2e_fork()
         for _ in range(max(args.warmup, n_e2e)):
             e2e_step()
+        e2e_join()
         barrier(world)
         torch.cuda.synchronize()
         # the box's pinned H2D bandwidth (the e2e bound when copies exceed the encode time)
@@ -658,8 +681,10 @@ def run_ours(args, rank, world, local):
         del probe
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        e2e_fork()
         for _ in range(n_e2e):
             e2e_step()
+        e2e_join()
         e1.record()
         torch.cuda.synchronize()
         e_ms = max_over_ranks(e0.elapsed_time(e1) / n_e2e, world)
@@ -667,7 +692,7 @@ def run_ours(args, rank, world, local):
             "value": world * vectors_per_rank / (e_ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": int(Kh.numel() * 4 + Vh.numel() * 4),
             "d2h_bytes_per_step": int(kph.numel() + vph.numel() + knh.numel() * 4 + vnh.numel() * 4),
-            "ms_per_step": e_ms, "api": "vqkv_quantize_batch_host_async x2 (pinned host buffers), then sync",
+            "ms_per_step": e_ms, "api": "vqkv_quantize_batch_host_async: K and V on their own caller streams, steps alternating between two stream pairs (pinned host buffers), then sync",
             "h2d_gbps_probe": h2d_gbps,
         }
 

@@ -73,7 +73,7 @@ constexpr int kGS = 8;                         // key stages per LUT group (one 
 constexpr uint32_t kRowBytes = kGS * 16;       // 8 slots x float4
 constexpr uint32_t kLutBytes = 1024 * kRowBytes;  // 128 KB: one group, up to 1024 code values
 constexpr uint32_t kMaxVStages = 64;
-constexpr uint32_t kSmemCtl = 16384;           // barriers, reductions, value descriptors (raw CTAs: 10 KB)
+constexpr uint32_t kSmemCtl = 2048;            // barrier, TMEM address, reductions, value descriptors
 constexpr uint32_t kQueueCap = 64;             // per-warp queue of tokens with a nonzero weight
 constexpr uint32_t kQueueBytes = (kThreads / 32) * kQueueCap * (1 + 4) * 4;
 constexpr uint32_t kMainSmem = kLutBytes + kSmemCtl + kQueueBytes;
@@ -324,42 +324,6 @@ __device__ __forceinline__ uint64_t read_bits64(const uint8_t* base, uint64_t po
     return bsh ? ((v >> bsh) | (extra << (64 - bsh))) : v;
 }
 
-struct MainArgs {
-    const float* q;
-    const float* init_k;
-    const float* init_v;
-    uint64_t n_init;
-    const float* local_k;
-    const float* local_v;
-    uint64_t n_local;
-    uint64_t init_stride, local_stride;  // rows between pairs
-    float scale;
-    // keys: LUT + attention records
-    const float4* lut;
-    uint32_t ng, R;
-    const uint8_t* krec;     // records, krec_stride bytes between pairs, cap tokens per group segment
-    uint64_t krec_stride, cap;
-    // values: CodeMatrix rows
-    const uint8_t* vcodes;
-    uint64_t vstride, vrow_bits;
-    const uint8_t* vend;     // end of the last pair's value payload (reads stop here)
-    const StageInfo* vst;
-    uint32_t vn;
-    uint32_t vnwin;          // 64-bit windows of the value row (stages grouped, <= 64 bits each)
-    const uint2* vwin;       // [vnwin]: (start bit, s0 | s1 << 8)
-    const uint8_t* vwin_of;  // [vn]: window of each stage
-    uint32_t hwords;         // histogram words: 4 x sum S_v
-    const float* veff;
-    uint64_t n_comp;
-    uint32_t ctas_per_pair;  // main CTAs per pair
-    uint32_t n_main;         // main CTAs in the grid (raw CTAs follow)
-    uint64_t tok_per_cta;    // multiple of 512
-    float* acc;              // per main CTA: fp32 histogram accumulator [stage][head][code] (hwords)
-    float* part_o;           // [n_main + pairs][G][D]: unnormalised sum p v
-    float* part_m;           // [n_main + pairs][G]
-    float* part_l;           // [n_main + pairs][G]
-};
-
 __device__ __forceinline__ float block_max(float v, float* red) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -423,33 +387,102 @@ __device__ __forceinline__ float4 block_sum4(float4 v, float4* red) {
 __device__ __forceinline__ void lds128(uint32_t addr, float2& a, float2& b) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y) : "r"(addr));
 }
+__device__ __forceinline__ float2 add2v(float2 a, float2 b) {  // volatile: keeps its place among the LDS
+    uint64_t r, x = *reinterpret_cast<uint64_t*>(&a), y = *reinterpret_cast<uint64_t*>(&b);
+    asm volatile("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+    return *reinterpret_cast<float2*>(&r);
+}
 __device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
-__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ float4 ldcg4(const float4* p) {
-    float4 v;
-    asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ void stcg4(float4* p, float4 v) {
-    asm volatile("st.global.cg.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+__device__ __forceinline__ void red_shared_add_nz(uint32_t addr, uint32_t v) {  // predicated, no branch
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr), "r"(v)
+                 : "memory");
 }
 
-// raw init/local rows of one pair: direct fp32 attention (no codebooks).  Latency matters
-// here (one CTA per pair runs beside the main CTAs): rows are read in batches with all
-// their loads in flight, and every value load feeds the 4 heads.
-__device__ void raw_rows(const MainArgs& a, uint32_t pair, uint32_t slot, float* smem) {
+// Field K (0..7) of an 80-bit attention record (w0 = bits 0-31, w1 = 32-63, w2 = 64-79),
+// shifted so its 10 bits sit at bits 7-16 (the code's row offset, 128 B per code); the bits
+// below are the previous field's and are masked off by the caller.  One SHF each.
+template <int K>
+__device__ __forceinline__ uint32_t field_at7(uint32_t w0, uint32_t w1, uint32_t w2) {
+    if constexpr (K == 0) return w0 << 7;
+    else if constexpr (K <= 3) return __funnelshift_r(w0, w1, 10 * K - 7);
+    else return __funnelshift_r(w1, w2, 10 * K - 39);
+}
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+
+// L2 cache policies: streamed-once code records evict first, the per-pair LUTs (re-read once per
+// chunk by every CTA on the pair) evict last
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint2 ldg_stream_u2(const uint2* p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg_stream_u16(const uint16_t* p, uint64_t pol) {
+    unsigned short v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_l2_hint(const void* p, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol) : "memory");
+}
+
+// raw init/local rows: one CTA per pair, direct fp32 attention (no codebooks).  Runs on a side
+// stream beside the LUT build; its (o, m, l) is one more partial of the pair's LSE merge.
+struct RawArgs {
+    const float* q;
+    const float* init_k;
+    const float* init_v;
+    uint64_t n_init;
+    const float* local_k;
+    const float* local_v;
+    uint64_t n_local;
+    uint64_t init_stride, local_stride;  // rows between pairs
+    float scale;
+    uint32_t slot0;  // partial slot of pair 0
+    float* part_o;
+    float* part_m;
+    float* part_l;
+};
+
+__global__ void __launch_bounds__(kThreads) attend_raw_rows_kernel(RawArgs a) {
+    extern __shared__ __align__(16) float rsm[];
     constexpr int kRowBatch = 8;
-    float* red = smem;                 // 64
-    float* qs = smem + 64;             // G*D
-    float* ls = qs + kG * kD;          // logits / weights [n_raw][G] (n_raw <= 8192)
-    float* po = ls + kChunk * kG;  // [4 row groups][G][D] partial outputs
+    const uint32_t pair = blockIdx.x, slot = a.slot0 + pair;
+    const uint32_t n_raw = uint32_t(a.n_init + a.n_local);
+    if (n_raw == 0) {
+        if (threadIdx.x < kG) {
+            a.part_m[uint64_t(slot) * kG + threadIdx.x] = -INFINITY;
+            a.part_l[uint64_t(slot) * kG + threadIdx.x] = 0.f;
+        }
+        return;
+    }
+    float* red = rsm;                  // 64
+    float* qs = rsm + 64;              // G*D
+    float* po = qs + kG * kD;          // [4 row groups][G][D] partial outputs
+    float* ls = po + 4 * kG * kD;      // logits / weights [n_raw][G]
     for (uint32_t i = threadIdx.x; i < kG * kD; i += blockDim.x) qs[i] = a.q[uint64_t(pair) * kG * kD + i];
     __syncthreads();
-    const uint32_t n_raw = uint32_t(a.n_init + a.n_local);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     auto krow = [&](uint32_t r) -> const float4* {
         return reinterpret_cast<const float4*>(
@@ -543,57 +576,193 @@ __device__ void raw_rows(const MainArgs& a, uint32_t pair, uint32_t slot, float*
     }
 }
 
-// Field K (0..7) of an 80-bit attention record (w0 = bits 0-31, w1 = 32-63, w2 = 64-79),
-// shifted so its 10 bits sit at bits 7-16 (the code's row offset, 128 B per code); the bits
-// below are the previous field's and are masked off by the caller.  One SHF each.
-template <int K>
-__device__ __forceinline__ uint32_t field_at7(uint32_t w0, uint32_t w1, uint32_t w2) {
-    if constexpr (K == 0) return w0 << 7;
-    else if constexpr (K <= 3) return __funnelshift_r(w0, w1, 10 * K - 7);
-    else return __funnelshift_r(w1, w2, 10 * K - 39);
+// Compressed tokens.  The pairs' tokens are cut into 512-token units (pair-major); CTA b of the
+// persistent grid takes units [U b / n_cta, U (b + 1) / n_cta), i.e. a contiguous token range
+// that may span a pair boundary.  Its work is processed in chunks of up to 16 units of one
+// pair; a run of chunks of one pair is a segment, whose partial (o, m, l) goes to slot b + pair
+// (unique: CTA ranges are monotone in the pair).
+struct MainArgs {
+    const float4* lut;       // grouped layout (lut_off)
+    uint32_t ng, R;
+    const uint8_t* krec;     // attention records, krec_stride bytes between pairs, cap tokens per group segment
+    uint64_t krec_stride, cap;
+    const uint8_t* vcodes;   // value CodeMatrix rows
+    uint64_t vstride, vrow_bits;
+    const uint8_t* vend;     // end of the last pair's value payload (reads stop here)
+    const StageInfo* vst;
+    uint32_t vn;
+    uint32_t vnwin;          // 64-bit windows of the value row (stages grouped, <= 64 bits each)
+    const uint2* vwin;       // [vnwin]: (start bit, s0 | s1 << 8)
+    const uint8_t* vwin_of;  // [vn]: window of each stage
+    uint32_t vtotal;         // sum S_v (<= kHistStride): histogram entries per head
+    const float* veff;
+    uint64_t n_comp;
+    uint32_t n_pairs;
+    uint32_t units_per_pair; // ceil(n_comp / 512)
+    uint32_t n_cta;          // persistent CTAs (<= total units, so none is empty)
+    float* part_o;           // [slots][G][D]: unnormalised sum p v
+    float* part_m;           // [slots][G]
+    float* part_l;           // [slots][G]
+};
+
+constexpr uint32_t kUnit = kThreads;           // tokens per unit (one per thread)
+constexpr uint32_t kUnitsPerChunk = kTok;      // 16 units = one 8192-token chunk
+constexpr uint32_t kHistStride = 8192;         // histogram words per head: [head][entry]
+constexpr uint32_t kTmemCols = 256;            // fp32 accumulator [head][entry]: 4 x 64 columns x 128 lanes
+
+// the CTA owning unit x: largest b with floor(U b / n) <= x
+__host__ __device__ __forceinline__ uint32_t cta_of_unit(uint64_t x, uint64_t U, uint32_t n) {
+    uint64_t b = (x * n) / U;
+    while (b + 1 < n && (U * (b + 1)) / n <= x) ++b;
+    while (b > 0 && (U * b) / n > x) --b;
+    return uint32_t(b);
 }
 
-__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+// L2 prefetch of the records of one LUT group of a chunk (both planes), ahead of the LDGs.  Out of line:
+// thread 0 runs it inside the key loop.
+__device__ __noinline__ void prefetch_group(const uint8_t* krec, uint64_t krec_stride, uint64_t cap, uint32_t pair,
+                                            uint32_t g, uint32_t c0, uint32_t t1, uint64_t pol) {
+    const uint8_t* seg = krec + uint64_t(pair) * krec_stride + uint64_t(g) * cap * 10u;
+    const uint64_t n = t1 - c0;
+    const uint32_t lo = uint32_t(umin64((n * 8u + 15u) & ~uint64_t(15), (cap - c0) * 8u));
+    const uint32_t hi = uint32_t(umin64((n * 2u + 15u) & ~uint64_t(15), (cap - c0) * 2u));
+    if (lo) prefetch_l2_hint(seg + uint64_t(c0) * 8u, lo, pol);
+    if (hi) prefetch_l2_hint(seg + cap * 8u + uint64_t(c0) * 2u, hi, pol);
+}
 
-// L2 prefetch of a chunk's records (both planes of one group segment), ahead of the LDGs
-__device__ __forceinline__ void ptx_prefetch_records(const uint8_t* seg, uint64_t cap, uint64_t c0, uint32_t n) {
-    const uint32_t lo = uint32_t(umin64((uint64_t(n) * 8u + 15u) & ~uint64_t(15), (cap - c0) * 8u));
-    const uint32_t hi = uint32_t(umin64((uint64_t(n) * 2u + 15u) & ~uint64_t(15), (cap - c0) * 2u));
-    if (lo) prefetch_l2_bulk(seg + c0 * 8u, lo);
-    if (hi) prefetch_l2_bulk(seg + cap * 8u + c0 * 2u, hi);
+// L2 prefetch of a chunk's value rows (read by the value phase after the key phase)
+__device__ __noinline__ void prefetch_values(const uint8_t* vc, uint64_t row_bits, uint32_t c0, uint32_t t1,
+                                             const uint8_t* vend, uint64_t pol) {
+    const uint8_t* p0 = vc + (uint64_t(c0) * row_bits >> 3);
+    const uint8_t* p1 = vc + ((uint64_t(t1) * row_bits + 7) >> 3);
+    if (p1 > vend) p1 = vend;
+    p0 = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(p0) & ~uintptr_t(15));
+    while (p0 < p1) {
+        const uint32_t n = uint32_t(umin64(uint64_t(p1 - p0 + 15) & ~uint64_t(15), 65536u));
+        if (p0 + n > vend) break;  // the tail that would overrun the buffer is read on demand
+        prefetch_l2_hint(p0, n, pol);
+        p0 += n;
+    }
+}
+
+// Fold a chunk's int32 histograms (smem, [head][entry]) into the segment's fp32 accumulator in TMEM:
+// acc = acc * al + H * be (acc = H * be for the first chunk).  Warp = (head, TMEM lane quarter);
+// thread = entries e = 128 c + 32 quarter + lane, c < ncol (TMEM column 64 head + c): conflict-free smem
+// reads, one tcgen05.ld / st per 32 columns.  Out of line: keeps the chunk loop's registers for the logits.
+__device__ __noinline__ void chunk_fold(const uint8_t* lutb, uint32_t tmem, uint32_t ncol, bool first, float alg,
+                                        float beg) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t hg = warp >> 2, hlq = warp & 3u;
+    const uint32_t* Hw = reinterpret_cast<const uint32_t*>(lutb) + hg * kHistStride + hlq * 32u + lane;
+    for (uint32_t cb = 0; cb < ncol; cb += 32u) {
+        const uint32_t taddr = tmem + ((hlq * 32u) << 16) + hg * 64u + cb;
+        float v[32];
+        if (!first) {
+            ptx::tmem_ld32(taddr, v);
+            ptx::tc_wait_ld();
+        }
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            const uint32_t col = cb + uint32_t(c);
+            const float hv = col < ncol ? float(Hw[col * 128u]) * beg : 0.f;
+            v[c] = first ? hv : fmaf(v[c], alg, hv);
+        }
+        ptx::tmem_st32(taddr, v);
+    }
+    ptx::tc_wait_st();
+}
+
+// Segment end: o[g][d] = sum_e acc[g][e] * e_v[e][d] (e = the value stack's stage-concatenated entry),
+// the TMEM accumulator staged into the smem buffer; writes the segment's partial (o, m, l).
+__device__ __noinline__ void segment_contract(const float* __restrict__ veff, uint32_t vtotal, float* part_o,
+                                              float* part_m, float* part_l, uint8_t* lutb, uint32_t tmem,
+                                              uint32_t ncol, uint32_t slot, float4 Mn, float4 Lrun) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t hg = warp >> 2, hlq = warp & 3u;
+    // the accumulator, staged from TMEM into the smem buffer as float4 [entry] x (4 heads)
+    float* accs = reinterpret_cast<float*>(lutb);
+    for (uint32_t cb = 0; cb < ncol; cb += 32u) {
+        float v[32];
+        ptx::tmem_ld32(tmem + ((hlq * 32u) << 16) + hg * 64u + cb, v);
+        ptx::tc_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            if (cb + uint32_t(c) < ncol) accs[((cb + uint32_t(c)) * 128u + hlq * 32u + lane) * kG + hg] = v[c];
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    // warp = a slice of the entries, lane = 4 output columns: per entry one coalesced 512 B row read
+    // (L2-resident codebook) and one broadcast LDS.128 of the 4 heads' weights feed 16 FMAs
+    const float4* acc4 = reinterpret_cast<const float4*>(accs);
+    const uint32_t per = (vtotal + 15u) / 16u, j0 = warp * per, j1 = min(vtotal, j0 + per);
+    float o[kG][4];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) o[g][0] = o[g][1] = o[g][2] = o[g][3] = 0.f;
+    const float4* e4 = reinterpret_cast<const float4*>(veff) + lane;
+    uint32_t j = j0;
+    for (; j + 4u <= j1; j += 4u) {
+        float4 x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = __ldg(e4 + uint64_t(j + i) * (kD / 4));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float4 w = acc4[j + i];
+            const float wg[kG] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int g = 0; g < kG; ++g) {
+                o[g][0] = fmaf(wg[g], x[i].x, o[g][0]);
+                o[g][1] = fmaf(wg[g], x[i].y, o[g][1]);
+                o[g][2] = fmaf(wg[g], x[i].z, o[g][2]);
+                o[g][3] = fmaf(wg[g], x[i].w, o[g][3]);
+            }
+        }
+    }
+    for (; j < j1; ++j) {
+        const float4 x = __ldg(e4 + uint64_t(j) * (kD / 4));
+        const float4 w = acc4[j];
+        const float wg[kG] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+            o[g][0] = fmaf(wg[g], x.x, o[g][0]);
+            o[g][1] = fmaf(wg[g], x.y, o[g][1]);
+            o[g][2] = fmaf(wg[g], x.z, o[g][2]);
+            o[g][3] = fmaf(wg[g], x.w, o[g][3]);
+        }
+    }
+    __syncthreads();  // accumulator consumed
+    float4* po = reinterpret_cast<float4*>(lutb);  // [warp][head][lane] x float4 (4 columns)
+#pragma unroll
+    for (int g = 0; g < kG; ++g) po[(warp * kG + g) * 32u + lane] = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+    __syncthreads();
+    {
+        const uint32_t g = tid >> 7, d = tid & (kD - 1u);
+        const float* pf = reinterpret_cast<const float*>(po);
+        float r = 0.f;
+        for (uint32_t w = 0; w < kThreads / 32u; ++w) r += pf[(w * kG + g) * kD + d];
+        part_o[(uint64_t(slot) * kG + g) * kD + d] = r;
+    }
+    if (tid == 0) {
+        reinterpret_cast<float4*>(part_m)[slot] = Mn;
+        reinterpret_cast<float4*>(part_l)[slot] = Lrun;
+    }
 }
 
 __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const uint32_t cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    float* fsm = reinterpret_cast<float*>(smem_raw);
-    if (cta >= a.n_main) {  // raw init/local rows of one pair
-        const uint32_t pair = cta - a.n_main;
-        if (a.n_init + a.n_local > 0) {
-            raw_rows(a, pair, cta, fsm);
-        } else if (tid < kG) {
-            a.part_m[uint64_t(cta) * kG + tid] = -INFINITY;
-            a.part_l[uint64_t(cta) * kG + tid] = 0.f;
-        }
-        return;
-    }
-    const uint32_t pair = cta / a.ctas_per_pair, split = cta % a.ctas_per_pair;
-    const uint64_t t0 = uint64_t(split) * a.tok_per_cta;
-    const uint64_t t1 = min(a.n_comp, t0 + a.tok_per_cta);
-    uint8_t* const lutb = smem_raw;  // [0, 128 KB): one LUT group, then the chunk's value histograms
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    uint8_t* const lutb = smem_raw;  // [0, 128 KB): one LUT group; the chunk's value histograms; the contraction's accumulator
     uint8_t* const ctl = smem_raw + kLutBytes;
     uint64_t* bar = reinterpret_cast<uint64_t*>(ctl);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ctl + 8);
     float4* red = reinterpret_cast<float4*>(ctl + 64);           // 16 x float4
-    // value stage tables: histogram word offset (4 x first entry: [stage][head][code] layout),
-    // size, field position within its 64-bit window | bits << 8; window start bits and stage ranges
-    uint32_t* vbase = reinterpret_cast<uint32_t*>(ctl + 512);    // [64]
-    uint32_t* vsz = vbase + 64;                                   // [64]
+    // value stage tables: first histogram entry (the stage's first effective row), size, field position
+    // within its 64-bit window | bits << 8; window start bits and stage ranges
+    uint32_t* vrow = reinterpret_cast<uint32_t*>(ctl + 512);      // [64]
+    uint32_t* vsz = vrow + 64;                                    // [64]
     uint32_t* vfld = vsz + 64;                                    // [64]
-    uint32_t* vrow = vfld + 64;                                   // [64]: first effective row of stage s
-    uint32_t* wstart = vrow + 64;                                 // [16]
+    uint32_t* wstart = vfld + 64;                                 // [16]
     uint32_t* wrange = wstart + 16;                               // [16]: s0 | s1 << 8
     uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw + kLutBytes + kSmemCtl) + warp * (kQueueCap * (1 + kG));
-    const uint32_t HW = a.hwords;                                 // histogram words: 4 x sum S_v
     if (tid == 0) {
         ptx::mbar_init(ptx::smem_u32(bar), 1);
         ptx::fence_mbar_init();
@@ -601,7 +770,6 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
     if (tid < a.vn) {
         const StageInfo si = a.vst[tid];
         vrow[tid] = uint32_t(si.eff_off / kD);
-        vbase[tid] = 4u * vrow[tid];
         vsz[tid] = si.size;
         vfld[tid] = (si.bit_off - a.vwin[a.vwin_of[tid]].x) | (si.bits << 8);
     }
@@ -609,84 +777,145 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
         wstart[tid] = a.vwin[tid].x;
         wrange[tid] = a.vwin[tid].y;
     }
-    __syncthreads();
-
-    const uint32_t lut_s = ptx::smem_u32(lutb);
-    const float4* lutp = a.lut + uint64_t(pair) * a.ng * a.R * kGS;
-    const uint32_t grp_bytes = a.R * kRowBytes;
-    const uint32_t barp = ptx::smem_u32(bar);
-    auto issue = [&](uint32_t g) {  // one thread: the group's rows, one contiguous block
-        ptx::mbar_arrive_expect_tx(barp, grp_bytes);
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(lutp + uint64_t(g) * a.R * kGS);
-        for (uint32_t off = 0; off < grp_bytes; off += 32768u)
-            ptx::bulk_g2s(lut_s + off, src + off, min(32768u, grp_bytes - off), barp);
-    };
-    const uint8_t* krec = a.krec + uint64_t(pair) * a.krec_stride;
-    auto prefetch_records = [&](uint32_t g, uint64_t c0, uint32_t n) {  // into L2, ahead of the LDGs
-        const uint8_t* seg = krec + uint64_t(g) * a.cap * 10u;
-        ptx_prefetch_records(seg, a.cap, c0, n);
-    };
-    // value codes: 64-bit words relative to the 8 B-aligned start of the pair's payload
-    const uint8_t* vc = a.vcodes + uint64_t(pair) * a.vstride;
-    const uint64_t* vc64 = reinterpret_cast<const uint64_t*>(reinterpret_cast<uintptr_t>(vc) & ~uintptr_t(7));
-    const uint32_t vbase_bits = uint32_t((reinterpret_cast<uintptr_t>(vc) & 7u) * 8u);
-    const uint64_t vwords = (reinterpret_cast<uintptr_t>(a.vend) - reinterpret_cast<uintptr_t>(vc64)) >> 3;
-    const uint32_t l7 = (lane & 7u) << 4;  // this lane's slot rotation (token & 7 == lane & 7)
-
-    float4 M = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY), Lrun = make_float4(0.f, 0.f, 0.f, 0.f);
-    bool first = true;
-    float* accp = a.acc + uint64_t(cta) * HW;
-    uint32_t phase = 0;
-    if (tid == 0 && t0 < t1) {
-        prefetch_records(0, t0, uint32_t(umin64(kChunk, t1 - t0)));
-        issue(0);
+    if (warp == 0) {
+        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), kTmemCols);
+        ptx::tmem_relinquish();
     }
-    for (uint64_t c0 = t0; c0 < t1; c0 += kChunk) {
-        const uint32_t nt = uint32_t(umin64(kChunk, t1 - c0));
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+    const uint32_t lut_s = ptx::smem_u32(lutb);
+    const uint32_t barp = ptx::smem_u32(bar);
+    const uint32_t grp_bytes = a.R * kRowBytes;
+    const uint32_t upp = a.units_per_pair;
+    const uint32_t U = a.n_pairs * upp;  // units (< 2^32: checked at launch)
+    const uint32_t u_begin = uint32_t(uint64_t(U) * blockIdx.x / a.n_cta);
+    const uint32_t u_end = uint32_t(uint64_t(U) * (blockIdx.x + 1) / a.n_cta);
+
+    // chunk of unit u: its pair, token range [c0, t1) within the pair and the unit after it
+    struct Chunk {
+        uint32_t pair, c0, t1, next;
+    };
+    auto chunk_at = [&](uint32_t u) {
+        Chunk c;
+        c.pair = u / upp;
+        const uint32_t pu = c.pair * upp;
+        c.next = min(min(u_end, pu + upp), u + kUnitsPerChunk);
+        c.c0 = (u - pu) * kUnit;
+        c.t1 = uint32_t(umin64(a.n_comp, uint64_t(c.next - pu) * kUnit));
+        return c;
+    };
+    auto issue = [&](uint32_t pair, uint32_t g) {  // one thread: the group's rows, one contiguous block
+        ptx::mbar_arrive_expect_tx(barp, grp_bytes);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.lut + (uint64_t(pair) * a.ng + g) * a.R * kGS);
+        for (uint32_t off = 0; off < grp_bytes; off += 32768u)
+            bulk_g2s_hint(lut_s + off, src + off, min(32768u, grp_bytes - off), barp, pol_last);
+    };
+    const uint32_t l7 = (lane & 7u) << 4;  // this lane's slot rotation (token & 7 == lane & 7: units are 512-aligned)
+    const uint32_t hg = warp >> 2, hlq = warp & 3u;  // fold / contraction: head, TMEM lane quarter
+    const uint32_t ncol = (a.vtotal + 127u) >> 7;     // accumulator columns per head (<= 64)
+
+    // segment state (block-uniform) lives in shared memory: registers go to the logits
+    float4* segM = reinterpret_cast<float4*>(ctl + 16);  // running max, then running sum at ctl + 32
+    float4* segL = reinterpret_cast<float4*>(ctl + 32);
+    if (tid == 0) {
+        *segM = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        *segL = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    bool first = true;
+    uint32_t phase = 0;
+    if (tid == 0) {
+        const Chunk c = chunk_at(u_begin);
+        prefetch_group(a.krec, a.krec_stride, a.cap, c.pair, 0, c.c0, c.t1, pol_first);
+        issue(c.pair, 0);
+    }
+    for (uint32_t u = u_begin; u < u_end;) {
+        const Chunk ch = chunk_at(u);
+        const uint32_t pair = ch.pair;
+        const uint32_t c0 = ch.c0, t1 = ch.t1;
+        const uint32_t nt = t1 - c0;
+        const bool has_next = ch.next < u_end;
+        const uint8_t* krec = a.krec + uint64_t(pair) * a.krec_stride;
         float2 lg[kTok][2];
 #pragma unroll
         for (int k = 0; k < kTok; ++k) lg[k][0] = lg[k][1] = make_float2(0.f, 0.f);
-        // ---- keys: sum over the LUT groups of 8 conflict-free lookups per token
-        for (uint32_t g = 0; g < a.ng; ++g) {
-            if (tid == 0) {
-                if (g + 1 < a.ng) prefetch_records(g + 1, c0, nt);
-                else if (c0 + kChunk < t1) prefetch_records(0, c0 + kChunk, uint32_t(umin64(kChunk, t1 - c0 - kChunk)));
-            }
+        // ---- keys: per LUT group, 8 conflict-free lookups per token; record loads run one batch of
+        // 4 tokens ahead of the lookups
+        constexpr int kB = 2;  // tokens per record batch (loaded one batch ahead of the lookups)
+        uint2 w[kB];
+        uint32_t h[kB];
+        const uint32_t tok0 = c0 + tid, tlast = t1 - 1u;  // record indices fit 32 bits
+        auto load_batch = [&](uint32_t g, int kb, uint2 (&wo)[kB], uint32_t (&ho)[kB]) {
             const uint8_t* seg = krec + uint64_t(g) * a.cap * 10u;
             const uint2* rlo = reinterpret_cast<const uint2*>(seg);
             const uint16_t* rhi = reinterpret_cast<const uint16_t*>(seg + a.cap * 8u);
+#pragma unroll
+            for (int k = 0; k < kB; ++k) {
+                // tokens past the range read the last valid record (their logits are masked)
+                const uint32_t t = min(tok0 + uint32_t(kb + k) * kThreads, tlast);
+                wo[k] = ldg_stream_u2(rlo + t, pol_first);
+                ho[k] = ldg_stream_u16(rhi + t, pol_first);
+            }
+        };
+        if (tid == 32) prefetch_values(a.vcodes + uint64_t(pair) * a.vstride, a.vrow_bits, c0, t1, a.vend, pol_first);
+        load_batch(0, 0, w, h);
+        for (uint32_t g = 0; g < a.ng; ++g) {
+            if (tid == 0) {
+                if (g + 1 < a.ng) {
+                    prefetch_group(a.krec, a.krec_stride, a.cap, pair, g + 1, c0, t1, pol_first);
+                } else if (has_next) {
+                    const Chunk nx = chunk_at(ch.next);
+                    prefetch_group(a.krec, a.krec_stride, a.cap, nx.pair, 0, nx.c0, nx.t1, pol_first);
+                }
+            }
             ptx::mbar_wait(barp, phase);
             phase ^= 1u;
 #pragma unroll
-            for (int kb = 0; kb < kTok; kb += 4) {
-                uint2 w[4];
-                uint32_t h[4];
+            for (int kb = 0; kb < kTok; kb += kB) {
+                uint2 wn[kB];
+                uint32_t hn[kB];
+                if (kb + kB < kTok) load_batch(g, kb + kB, wn, hn);
+                else if (g + 1 < a.ng) load_batch(g + 1, 0, wn, hn);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    // tokens past the range read the last valid record (their logits are masked)
-                    const uint64_t t = min(c0 + uint64_t(kb + k) * kThreads + tid, t1 - 1);
-                    w[k] = __ldg(rlo + t);
-                    h[k] = __ldg(rhi + t);
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < kB; ++k) {
                     const uint32_t w0 = w[k].x, w1 = w[k].y, w2 = h[k];
                     float2* L = lg[kb + k];
-#define VQKV_LOOK(K)                                                                        \
+                    // four lookups in flight per thread (volatile order): the logits keep their
+                    // registers, and 16 warps x 4 LDS.128 keep the LDS pipe full
+#define VQKV_LOOK4(K0, K1, K2, K3)                                                          \
     {                                                                                       \
-        const uint32_t x = field_at7<K>(w0, w1, w2);                                        \
-        float2 u, v;                                                                        \
-        lds128(lut_s + ((x & 0x1FF80u) | (l7 ^ uint32_t((K) << 4))), u, v);                \
-        L[0] = ptx::add2(L[0], u);                                                          \
-        L[1] = ptx::add2(L[1], v);                                                          \
+        const uint32_t x0 = field_at7<K0>(w0, w1, w2), x1 = field_at7<K1>(w0, w1, w2);      \
+        const uint32_t x2 = field_at7<K2>(w0, w1, w2), x3 = field_at7<K3>(w0, w1, w2);      \
+        float2 a0, b0, a1, b1, a2, b2, a3, b3;                                              \
+        lds128(lut_s + ((x0 & 0x1FF80u) | (l7 ^ uint32_t((K0) << 4))), a0, b0);            \
+        lds128(lut_s + ((x1 & 0x1FF80u) | (l7 ^ uint32_t((K1) << 4))), a1, b1);            \
+        lds128(lut_s + ((x2 & 0x1FF80u) | (l7 ^ uint32_t((K2) << 4))), a2, b2);            \
+        lds128(lut_s + ((x3 & 0x1FF80u) | (l7 ^ uint32_t((K3) << 4))), a3, b3);            \
+        L[0] = add2v(L[0], a0);                                                             \
+        L[1] = add2v(L[1], b0);                                                             \
+        L[0] = add2v(L[0], a1);                                                             \
+        L[1] = add2v(L[1], b1);                                                             \
+        L[0] = add2v(L[0], a2);                                                             \
+        L[1] = add2v(L[1], b2);                                                             \
+        L[0] = add2v(L[0], a3);                                                             \
+        L[1] = add2v(L[1], b3);                                                             \
     }
-                    VQKV_LOOK(0) VQKV_LOOK(1) VQKV_LOOK(2) VQKV_LOOK(3)
-                    VQKV_LOOK(4) VQKV_LOOK(5) VQKV_LOOK(6) VQKV_LOOK(7)
-#undef VQKV_LOOK
+                    VQKV_LOOK4(0, 1, 2, 3) VQKV_LOOK4(4, 5, 6, 7)
+#undef VQKV_LOOK4
+                }
+                if (kb + kB < kTok || g + 1 < a.ng) {
+#pragma unroll
+                    for (int k = 0; k < kB; ++k) {
+                        w[k] = wn[k];
+                        h[k] = hn[k];
+                    }
                 }
             }
             __syncthreads();  // every lane is done with this group's rows
-            if (tid == 0 && g + 1 < a.ng) issue(g + 1);
+            if (tid == 0 && g + 1 < a.ng) issue(pair, g + 1);
         }
 
         // ---- chunk softmax statistics (exact fp32 weights)
@@ -724,159 +953,150 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
             P[k][2] = __float2uint_rn(lg[k][1].x * qs.z);
             P[k][3] = __float2uint_rn(lg[k][1].y * qs.w);
         }
-        // ---- values: int32 histograms [stage][head][code] over the LUT buffer.  The tokens with a
-        // nonzero weight are compacted into a per-warp queue and processed 32 at a time, lane =
-        // token: its value row is read in 64-bit windows and every (stage, head) bin gets one
-        // shared atomic (bank = code mod 32).
-        for (uint32_t i = tid; i < HW / 4u; i += kThreads) reinterpret_cast<uint4*>(lutb)[i] = make_uint4(0u, 0u, 0u, 0u);
+        // ---- values: int32 histograms [head][entry] over the LUT buffer.  The tokens with a nonzero
+        // weight are compacted into a per-warp queue and processed 32 at a time, lane = token: its
+        // value row is read in 64-bit windows and every (stage, head) bin gets one shared atomic.
+        for (uint32_t i = tid; i < kLutBytes / 16u; i += kThreads) reinterpret_cast<uint4*>(lutb)[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
-        auto hist_token = [&](uint64_t t, const uint32_t (&Pv)[kG]) {
-            const uint64_t rbit = uint64_t(vbase_bits) + t * a.vrow_bits;
-            for (uint32_t w = 0; w < a.vnwin; ++w) {
-                const uint64_t pos = rbit + wstart[w];
-                const uint64_t wi = pos >> 6;
-                uint64_t x;
-                if (wi + 1 < vwords) {
-                    const uint64_t lo = __ldg(vc64 + wi), hi = __ldg(vc64 + wi + 1);
-                    const uint32_t sh = uint32_t(pos & 63u);
-                    x = sh ? ((lo >> sh) | (hi << (64u - sh))) : lo;
-                } else {  // the last words of the buffer
-                    x = read_bits64(vc, t * a.vrow_bits + wstart[w], a.vend);
+        {
+            const uint8_t* vc = a.vcodes + uint64_t(pair) * a.vstride;
+            const uint64_t* vc64 = reinterpret_cast<const uint64_t*>(reinterpret_cast<uintptr_t>(vc) & ~uintptr_t(7));
+            const uint32_t vbase_bits = uint32_t((reinterpret_cast<uintptr_t>(vc) & 7u) * 8u);
+            const uint64_t vwords = (reinterpret_cast<uintptr_t>(a.vend) - reinterpret_cast<uintptr_t>(vc64)) >> 3;
+            auto hist_token = [&](uint64_t t, const uint32_t (&Pv)[kG]) {
+                const uint64_t rbit = uint64_t(vbase_bits) + t * a.vrow_bits;
+                for (uint32_t wi_ = 0; wi_ < a.vnwin; ++wi_) {
+                    const uint64_t pos = rbit + wstart[wi_];
+                    const uint64_t wi = pos >> 6;
+                    uint64_t x;
+                    if (wi + 1 < vwords) {
+                        const uint64_t lo = __ldg(vc64 + wi), hi = __ldg(vc64 + wi + 1);
+                        const uint32_t sh = uint32_t(pos & 63u);
+                        x = sh ? ((lo >> sh) | (hi << (64u - sh))) : lo;
+                    } else {  // the last words of the buffer
+                        x = read_bits64(vc, t * a.vrow_bits + wstart[wi_], a.vend);
+                    }
+                    const uint32_t r = wrange[wi_];
+                    for (uint32_t st = r & 0xFFu; st < (r >> 8); ++st) {
+                        const uint32_t f = vfld[st];
+                        const uint32_t z = uint32_t(x >> (f & 0xFFu)) & ((1u << (f >> 8)) - 1u);
+                        const uint32_t b = lut_s + (vrow[st] + z) * 4u;
+#pragma unroll
+                        for (int g = 0; g < kG; ++g)
+                            red_shared_add_nz(b + uint32_t(g) * (kHistStride * 4u), Pv[g]);
+                    }
                 }
-                const uint32_t r = wrange[w];
-                for (uint32_t st = r & 0xFFu; st < (r >> 8); ++st) {
-                    const uint32_t f = vfld[st];
-                    const uint32_t z = uint32_t(x >> (f & 0xFFu)) & ((1u << (f >> 8)) - 1u);
-                    const uint32_t b = lut_s + (vbase[st] + z) * 4u, S4 = vsz[st] * 4u;
+            };
+            uint32_t* qt = queue;
+            uint32_t* qP = queue + kQueueCap;
+            uint32_t qlen = 0;
+            auto flush = [&](uint32_t n) {
+                if (lane < n) {
+                    uint32_t Pv[kG];
 #pragma unroll
-                    for (int g = 0; g < kG; ++g)
-                        if (Pv[g]) red_shared_add(b + uint32_t(g) * S4, Pv[g]);
+                    for (int g = 0; g < kG; ++g) Pv[g] = qP[lane * kG + g];
+                    hist_token(c0 + qt[lane], Pv);
+                }
+            };
+#pragma unroll
+            for (int k = 0; k < kTok; ++k) {
+                const uint32_t lt = uint32_t(k) * kThreads + tid;  // token within the chunk
+                const bool act = lt < nt && (P[k][0] | P[k][1] | P[k][2] | P[k][3]) != 0u;
+                const uint32_t mask = __ballot_sync(0xffffffffu, act);
+                if (act) {
+                    const uint32_t pos = qlen + __popc(mask & ((1u << lane) - 1u));
+                    qt[pos] = lt;
+#pragma unroll
+                    for (int g = 0; g < kG; ++g) qP[pos * kG + g] = P[k][g];
+                }
+                qlen += __popc(mask);
+                if (qlen >= 32u) {
+                    __syncwarp();
+                    flush(32u);
+                    __syncwarp();
+                    if (lane + 32u < qlen) {  // keep the overflow for the next batch
+                        qt[lane] = qt[lane + 32u];
+#pragma unroll
+                        for (int g = 0; g < kG; ++g) qP[lane * kG + g] = qP[(lane + 32u) * kG + g];
+                    }
+                    __syncwarp();
+                    qlen -= 32u;
                 }
             }
-        };
-        uint32_t* qt = queue;
-        uint32_t* qP = queue + kQueueCap;
-        uint32_t qlen = 0;
-        auto flush = [&](uint32_t n) {
-            if (lane < n) {
-                uint32_t Pv[kG];
-#pragma unroll
-                for (int g = 0; g < kG; ++g) Pv[g] = qP[lane * kG + g];
-                hist_token(c0 + qt[lane], Pv);
-            }
-        };
-#pragma unroll
-        for (int k = 0; k < kTok; ++k) {
-            const uint32_t lt = uint32_t(k) * kThreads + tid;  // token within the chunk
-            const bool act = lt < nt && (P[k][0] | P[k][1] | P[k][2] | P[k][3]) != 0u;
-            const uint32_t mask = __ballot_sync(0xffffffffu, act);
-            if (act) {
-                const uint32_t pos = qlen + __popc(mask & ((1u << lane) - 1u));
-                qt[pos] = lt;
-#pragma unroll
-                for (int g = 0; g < kG; ++g) qP[pos * kG + g] = P[k][g];
-            }
-            qlen += __popc(mask);
-            if (qlen >= 32u) {
-                __syncwarp();
-                flush(32u);
-                __syncwarp();
-                if (lane + 32u < qlen) {  // keep the overflow for the next batch
-                    qt[lane] = qt[lane + 32u];
-#pragma unroll
-                    for (int g = 0; g < kG; ++g) qP[lane * kG + g] = qP[(lane + 32u) * kG + g];
-                }
-                __syncwarp();
-                qlen -= 32u;
-            }
+            __syncwarp();
+            flush(qlen);
         }
-        __syncwarp();
-        flush(qlen);
         __syncthreads();
-        // ---- fold the chunk into the CTA's accumulator, rescaled to the running max
+        // ---- fold the chunk into the segment's fp32 accumulator in TMEM, rescaled to the running max.
+        // Warp = (head hg, TMEM lane quarter hlq); thread = entries e = 128 c + 32 hlq + lane, c < ncol
+        // (TMEM column 64 hg + c): conflict-free smem reads, one tcgen05.ld/st per 32 columns.
+        const float4 M = *segM;
         const float4 Mn = make_float4(fmaxf(M.x, mc.x), fmaxf(M.y, mc.y), fmaxf(M.z, mc.z), fmaxf(M.w, mc.w));
         const float4 al = first ? make_float4(0.f, 0.f, 0.f, 0.f)
                                 : make_float4(__expf(M.x - Mn.x), __expf(M.y - Mn.y), __expf(M.z - Mn.z), __expf(M.w - Mn.w));
         const float4 ec = make_float4(__expf(mc.x - Mn.x), __expf(mc.y - Mn.y), __expf(mc.z - Mn.z), __expf(mc.w - Mn.w));
-        const float4 be = make_float4(lc.x / kQuantum * ec.x, lc.y / kQuantum * ec.y, lc.z / kQuantum * ec.z,
-                                      lc.w / kQuantum * ec.w);
-        {
-            const uint32_t* Hw = reinterpret_cast<const uint32_t*>(lutb);
-            for (uint32_t st = 0; st < a.vn; ++st) {  // words of stage st: [head][code]
-                const uint32_t b = vbase[st], S = vsz[st];
-#pragma unroll 4
-                for (uint32_t i = tid; i < 4u * S; i += kThreads) {
-                    const uint32_t g = i / S;
-                    const float bg = g == 0u ? be.x : (g == 1u ? be.y : (g == 2u ? be.z : be.w));
-                    const float ag = g == 0u ? al.x : (g == 1u ? al.y : (g == 2u ? al.z : al.w));
-                    float v = float(Hw[b + i]) * bg;
-                    if (!first) v = fmaf(__ldcg(accp + b + i), ag, v);
-                    __stcg(accp + b + i, v);
-                }
-            }
-        }
-        Lrun = make_float4(fmaf(Lrun.x, al.x, lc.x * ec.x), fmaf(Lrun.y, al.y, lc.y * ec.y), fmaf(Lrun.z, al.z, lc.z * ec.z),
-                           fmaf(Lrun.w, al.w, lc.w * ec.w));
-        M = Mn;
+        chunk_fold(lutb, tmem, ncol, first, hg == 0 ? al.x : hg == 1 ? al.y : hg == 2 ? al.z : al.w,
+                   (hg == 0 ? lc.x : hg == 1 ? lc.y : hg == 2 ? lc.z : lc.w) / kQuantum *
+                       (hg == 0 ? ec.x : hg == 1 ? ec.y : hg == 2 ? ec.z : ec.w));
+        const float4 Lo = *segL;
+        const float4 Lrun = make_float4(fmaf(Lo.x, al.x, lc.x * ec.x), fmaf(Lo.y, al.y, lc.y * ec.y),
+                                        fmaf(Lo.z, al.z, lc.z * ec.z), fmaf(Lo.w, al.w, lc.w * ec.w));
         first = false;
-        __syncthreads();  // histograms consumed: the buffer takes the next chunk's first LUT group
-        if (tid == 0 && c0 + kChunk < t1) issue(0);
-    }
-
-    // ---- contraction: o[g][d] = sum_{s, j} acc[s][g][j] * e_s[j][d]
-    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (!first) {
-        const uint32_t d = tid & (kD - 1u), qtr = tid >> 7;  // 4 quarters of each stage's codes
-        for (uint32_t st = 0; st < a.vn; ++st) {
-            const uint32_t b = vbase[st], S = vsz[st];
-            const float* e = a.veff + uint64_t(vrow[st]) * kD + d;
-#pragma unroll 4
-            for (uint32_t j = qtr; j < S; j += 4u) {
-                const float x = __ldg(e + uint64_t(j) * kD);
-                o.x = fmaf(__ldcg(accp + b + j), x, o.x);
-                o.y = fmaf(__ldcg(accp + b + S + j), x, o.y);
-                o.z = fmaf(__ldcg(accp + b + 2u * S + j), x, o.z);
-                o.w = fmaf(__ldcg(accp + b + 3u * S + j), x, o.w);
-            }
+        ptx::tc_fence_before();
+        __syncthreads();  // histograms consumed, segM / segL read by every thread
+        ptx::tc_fence_after();
+        if (tid == 0) {
+            *segM = Mn;
+            *segL = Lrun;
         }
+        const uint32_t next_pair = has_next ? ch.next / upp : pair;
+
+        if (!has_next || next_pair != pair) {
+            // ---- segment end (out of line: keeps the chunk loop's registers for the logits)
+            segment_contract(a.veff, a.vtotal, a.part_o, a.part_m, a.part_l, lutb, tmem, ncol, blockIdx.x + pair, Mn,
+                             Lrun);
+            if (tid == 0) {
+                *segM = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+                *segL = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            first = true;
+        }
+        __syncthreads();  // the buffer takes the next chunk's first LUT group; segment state updated
+        if (tid == 0 && has_next) issue(next_pair, 0);
+        u = ch.next;
     }
-    float4* po = reinterpret_cast<float4*>(lutb);  // [4 quarters][D] x float4 (heads)
+    ptx::tc_fence_before();
     __syncthreads();
-    po[tid] = o;
-    __syncthreads();
-    {
-        const uint32_t g = tid >> 7, d = tid & (kD - 1u);
-        const float* pf = reinterpret_cast<const float*>(po);
-        const float r = (pf[(0 * kD + d) * kG + g] + pf[(1 * kD + d) * kG + g]) +
-                        (pf[(2 * kD + d) * kG + g] + pf[(3 * kD + d) * kG + g]);
-        a.part_o[(uint64_t(cta) * kG + g) * kD + d] = r;
-    }
-    if (tid == 0) {
-        reinterpret_cast<float4*>(a.part_m)[cta] = M;
-        reinterpret_cast<float4*>(a.part_l)[cta] = Lrun;
-    }
+    if (warp == 0) ptx::tmem_dealloc(tmem, kTmemCols);
 }
 
-// out[pair][g] = sum_c exp(m_c - M) o_c / sum_c exp(m_c - M) l_c over the pair's main CTAs and
-// its raw CTA; lse = M + log L (natural log of the sum of exp(scale * logits)).
+// out[pair][g] = sum_c exp(m_c - M) o_c / sum_c exp(m_c - M) l_c over the pair's segments and its
+// raw partial; lse = M + log L (natural log of the sum of exp(scale * logits)).
 __global__ void atr_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_m,
-                                   const float* __restrict__ part_l, uint32_t cpp, uint32_t n_main,
-                                   float* __restrict__ out, float* __restrict__ lse) {
+                                   const float* __restrict__ part_l, uint32_t n_cta, uint32_t upp, uint32_t n_pairs,
+                                   uint32_t raw_slot0, float* __restrict__ out, float* __restrict__ lse) {
     const uint32_t pair = blockIdx.x, d = threadIdx.x;
+    uint32_t s_lo = 1, s_hi = 0;  // segment slots [s_lo, s_hi] (empty when there are no compressed tokens)
+    if (n_cta > 0) {
+        const uint64_t U = uint64_t(n_pairs) * upp;
+        s_lo = cta_of_unit(uint64_t(pair) * upp, U, n_cta) + pair;
+        s_hi = cta_of_unit(uint64_t(pair + 1) * upp - 1, U, n_cta) + pair;
+    }
+    const uint32_t raw = raw_slot0 + pair;
     for (uint32_t g = 0; g < kG; ++g) {
-        auto slot = [&](uint32_t i) { return i < cpp ? pair * cpp + i : n_main + pair; };
-        float M = -INFINITY;
-        for (uint32_t i = 0; i <= cpp; ++i) M = fmaxf(M, part_m[uint64_t(slot(i)) * kG + g]);
+        float M = part_m[uint64_t(raw) * kG + g];
+        for (uint32_t sl = s_lo; sl <= s_hi; ++sl) M = fmaxf(M, part_m[uint64_t(sl) * kG + g]);
         float L = 0.f, o = 0.f;
-        for (uint32_t i = 0; i <= cpp; ++i) {
-            const uint32_t sl = slot(i);
+        auto add = [&](uint32_t sl) {
             const float m = part_m[uint64_t(sl) * kG + g];
             if (m > -INFINITY) {
                 const float w = __expf(m - M);
                 L = fmaf(w, part_l[uint64_t(sl) * kG + g], L);
                 o = fmaf(w, part_o[(uint64_t(sl) * kG + g) * kD + d], o);
             }
-        }
+        };
+        for (uint32_t sl = s_lo; sl <= s_hi; ++sl) add(sl);
+        add(raw);
         out[(uint64_t(pair) * kG + g) * kD + d] = o / L;
         if (d == 0 && lse) lse[uint64_t(pair) * kG + g] = M + logf(L);
     }
@@ -1031,23 +1251,27 @@ void launch_keycodes_from_gm(const vqkv_stack_s& ks, const uint8_t* gm, uint64_t
     launch_check("atr_unpack_kernel");
 }
 
+// the side stream the raw-row kernel runs on (one per stack, created on first use)
+static cudaStream_t attend_side_stream(const vqkv_stack_s& ks) {
+    auto& st = const_cast<vqkv_stack_s&>(ks);
+    std::lock_guard<std::mutex> lk(st.mu);
+    if (!st.cs_attn) VQKV_CUDA(cudaStreamCreateWithFlags(&st.cs_attn, cudaStreamNonBlocking));
+    return st.cs_attn;
+}
+
 void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s) {
     const uint32_t ng = key_groups(ks), R = max_size(ks);
     const double scale = a.scale > 0.0 ? a.scale : 1.0 / std::sqrt(double(kD));
     const uint64_t n_comp = a.n_comp;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ks.device);
-    // main CTAs: contiguous token ranges of one pair, as many per pair as fill the SMs once
-    uint32_t cpp = 0;
-    uint64_t tpc = 0;
-    if (n_comp > 0) {
-        const uint64_t want = std::max<uint64_t>(1, uint64_t(sms) / a.n_pairs);
-        const uint64_t per = (n_comp + want - 1) / want;
-        tpc = (per + 511) / 512 * 512;
-        cpp = uint32_t((n_comp + tpc - 1) / tpc);
-    }
-    const uint32_t n_main = a.n_pairs * cpp, n_slots = n_main + a.n_pairs;
-    const uint64_t hwords = vs.total_rows * 4;  // [stage][head][code]
+    // persistent main grid: one CTA per SM, balanced over 512-token units (never more CTAs than units)
+    const uint32_t upp = uint32_t((n_comp + kUnit - 1) / kUnit);
+    const uint64_t units = uint64_t(a.n_pairs) * upp;
+    const uint32_t n_cta = uint32_t(std::min<uint64_t>(uint64_t(sms), units));
+    // partial slots: segments b + pair (< n_cta + n_pairs), then one raw slot per pair
+    const uint32_t raw_slot0 = n_cta + a.n_pairs;
+    const uint32_t n_slots = raw_slot0 + a.n_pairs;
     std::vector<uint8_t> win_of;
     const std::vector<uint2> wins = value_windows(vs, &win_of);
     // key records: the caller's attention layout, or transcoded from CodeMatrix rows here
@@ -1068,7 +1292,6 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         }
     }
     float4* lut = nullptr;
-    float* acc = nullptr;
     uint8_t* vtab = nullptr;  // value windows + stage -> window
     VQKV_CUDA(cudaMallocAsync(&vtab, sizeof(uint2) * 16 + 64, s));
     VQKV_CUDA(cudaMemcpyAsync(vtab, wins.data(), sizeof(uint2) * wins.size(), cudaMemcpyHostToDevice, s));
@@ -1077,9 +1300,40 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     VQKV_CUDA(cudaMallocAsync(&po, sizeof(float) * n_slots * kG * kD, s));
     VQKV_CUDA(cudaMallocAsync(&pm, sizeof(float) * n_slots * kG, s));
     VQKV_CUDA(cudaMallocAsync(&pl, sizeof(float) * n_slots * kG, s));
+
+    // raw init/local rows on a side stream, beside the LUT build (fork / join with events)
+    cudaStream_t side = attend_side_stream(ks);
+    cudaEvent_t ev_fork, ev_join;
+    VQKV_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    VQKV_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    VQKV_CUDA(cudaEventRecord(ev_fork, s));
+    VQKV_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    {
+        RawArgs ra{};
+        ra.q = a.q_dev;
+        ra.init_k = a.init_k_dev;
+        ra.init_v = a.init_v_dev;
+        ra.n_init = a.n_init;
+        ra.local_k = a.local_k_dev;
+        ra.local_v = a.local_v_dev;
+        ra.n_local = a.n_local;
+        ra.init_stride = a.init_stride ? a.init_stride : a.n_init;
+        ra.local_stride = a.local_stride ? a.local_stride : a.n_local;
+        ra.scale = float(scale);
+        ra.slot0 = raw_slot0;
+        ra.part_o = po;
+        ra.part_m = pm;
+        ra.part_l = pl;
+        const uint32_t n_raw = uint32_t(a.n_init + a.n_local);
+        const int rsmem = int(sizeof(float) * (64 + kG * kD + 4 * kG * kD + uint64_t(n_raw) * kG));
+        VQKV_CUDA(cudaFuncSetAttribute(attend_raw_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem));
+        attend_raw_rows_kernel<<<a.n_pairs, kThreads, rsmem, side>>>(ra);
+        launch_check("attend_raw_rows_kernel");
+    }
+    VQKV_CUDA(cudaEventRecord(ev_join, side));
+
     if (n_comp > 0) {
         VQKV_CUDA(cudaMallocAsync(&lut, sizeof(float4) * a.n_pairs * ng * R * kGS, s));
-        VQKV_CUDA(cudaMallocAsync(&acc, sizeof(float) * std::max<uint64_t>(1, uint64_t(n_main) * hwords), s));
         ProfScope ps("attend_lut_build", s);
         if (lut_tc_ok(ks)) {
             // tensor-core LUT GEMM (VQKV_LUT_FFMA=1 selects the FFMA kernel below)
@@ -1113,21 +1367,11 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
             launch_check("lut_zero_missing_kernel");
         }
     }
-    {
+    if (n_comp > 0) {
         ProfScope ps("attend", s);
         const uint64_t vpb = payload_bytes(vs.row_bits, n_comp);
         const uint64_t vstr = a.vcodes_stride ? a.vcodes_stride : vpb;
         MainArgs ma{};
-        ma.q = a.q_dev;
-        ma.init_k = a.init_k_dev;
-        ma.init_v = a.init_v_dev;
-        ma.n_init = a.n_init;
-        ma.local_k = a.local_k_dev;
-        ma.local_v = a.local_v_dev;
-        ma.n_local = a.n_local;
-        ma.init_stride = a.init_stride ? a.init_stride : a.n_init;
-        ma.local_stride = a.local_stride ? a.local_stride : a.n_local;
-        ma.scale = float(scale);
         ma.lut = lut;
         ma.ng = ng;
         ma.R = R;
@@ -1138,33 +1382,35 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         ma.vstride = vstr;
         ma.vrow_bits = vs.row_bits;
         // end of the last pair's value payload: reads stop here (earlier pairs may read into the next)
-        ma.vend = n_comp ? a.vcodes_dev + uint64_t(a.n_pairs - 1) * vstr + vpb : nullptr;
+        ma.vend = a.vcodes_dev + uint64_t(a.n_pairs - 1) * vstr + vpb;
         ma.vst = vs.d_stages;
         ma.vn = vs.n;
         ma.vnwin = uint32_t(wins.size());
         ma.vwin = reinterpret_cast<const uint2*>(vtab);
         ma.vwin_of = vtab + sizeof(uint2) * 16;
-        ma.hwords = uint32_t(hwords);
+        ma.vtotal = uint32_t(vs.total_rows);
         ma.veff = vs.d_eff;
         ma.n_comp = n_comp;
-        ma.ctas_per_pair = std::max<uint32_t>(cpp, 1);
-        ma.n_main = n_main;
-        ma.tok_per_cta = tpc;
-        ma.acc = acc;
+        ma.n_pairs = a.n_pairs;
+        ma.units_per_pair = upp;
+        ma.n_cta = n_cta;
         ma.part_o = po;
         ma.part_m = pm;
         ma.part_l = pl;
         VQKV_CUDA(cudaFuncSetAttribute(attend_atr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMainSmem)));
-        attend_atr_kernel<<<n_slots, kThreads, kMainSmem, s>>>(ma);
+        attend_atr_kernel<<<n_cta, kThreads, kMainSmem, s>>>(ma);
         launch_check("attend_atr_kernel");
     }
+    VQKV_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
     {
         ProfScope ps("attend_combine", s);
-        atr_combine_kernel<<<a.n_pairs, kD, 0, s>>>(po, pm, pl, cpp, n_main, a.out_dev, a.lse_dev);
+        atr_combine_kernel<<<a.n_pairs, kD, 0, s>>>(po, pm, pl, n_comp > 0 ? n_cta : 0u, upp, a.n_pairs, raw_slot0,
+                                                    a.out_dev, a.lse_dev);
         launch_check("atr_combine_kernel");
     }
+    cudaEventDestroy(ev_fork);
+    cudaEventDestroy(ev_join);
     if (lut) VQKV_CUDA(cudaFreeAsync(lut, s));
-    if (acc) VQKV_CUDA(cudaFreeAsync(acc, s));
     if (ktmp) VQKV_CUDA(cudaFreeAsync(ktmp, s));
     VQKV_CUDA(cudaFreeAsync(vtab, s));
     VQKV_CUDA(cudaFreeAsync(po, s));
