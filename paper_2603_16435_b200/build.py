@@ -105,6 +105,24 @@ def build_diag() -> str:
     return DIAG_LIB
 
 
+def build_variant(name: str, defines=()) -> str:
+    """Development A/B build with extra -D flags into build/var/<name>.so (load it with VQKV_LIB).
+    Not the product library."""
+    obj_dir = os.path.join(ROOT, "build", "var", name)
+    os.makedirs(obj_dir, exist_ok=True)
+    lib = os.path.join(ROOT, "build", "var", name + ".so")
+    srcs = _sources()
+    extra = tuple("-D" + d for d in defines)
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+        objs = list(ex.map(lambda s: _compile(s, False, obj_dir, extra), srcs))
+    if _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-cudart", "static", "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    return lib
+
+
 CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_cpp_api.cpp")
 CPP_TEST_BIN = os.path.join(ROOT, "build", "test_cpp_api")
 

@@ -67,16 +67,28 @@ namespace {
 constexpr int kG = 4;                          // query heads per KV head on this path
 constexpr int kD = 128;                        // head dim
 constexpr int kThreads = 512;
-constexpr int kTok = 16;                       // tokens per thread per chunk
+#ifndef VQKV_ATTN_EXP
+#define VQKV_ATTN_EXP 0  // development experiments (variant builds only)
+#endif
+#ifndef VQKV_ATTN_KB
+#define VQKV_ATTN_KB 2  // key records loaded per batch, one batch ahead of the lookups
+#endif
+#ifndef VQKV_ATTN_TOK
+#define VQKV_ATTN_TOK 16
+#endif
+constexpr int kTok = VQKV_ATTN_TOK;            // tokens per thread per chunk
 constexpr int kChunk = kThreads * kTok;        // 8192 tokens per chunk
 constexpr int kGS = 8;                         // key stages per LUT group (one 128 B row)
 constexpr uint32_t kRowBytes = kGS * 16;       // 8 slots x float4
 constexpr uint32_t kLutBytes = 1024 * kRowBytes;  // 128 KB: one group, up to 1024 code values
 constexpr uint32_t kMaxVStages = 64;
 constexpr uint32_t kSmemCtl = 2048;            // barrier, TMEM address, reductions, value descriptors
-constexpr uint32_t kQueueCap = 64;             // per-warp queue of tokens with a nonzero weight
-constexpr uint32_t kQueueBytes = (kThreads / 32) * kQueueCap * (1 + 4) * 4;
-constexpr uint32_t kMainSmem = kLutBytes + kSmemCtl + kQueueBytes;
+constexpr uint32_t kQueueCap = 32 + 32 * 4;    // per-warp queue of (token, head) entries with a nonzero weight
+constexpr uint32_t kQueueBytes = (kThreads / 32) * kQueueCap * 8;
+constexpr uint32_t kSlabTok = 4 * kThreads;      // value rows staged per slab (4 tokens per thread)
+constexpr uint32_t kSlabBytes = 38400;           // per slab buffer: rows of up to 149 bits + alignment slack
+constexpr uint32_t kMaxSlabRowBits = ((kSlabBytes - 48) * 8) / kSlabTok;
+constexpr uint32_t kMainSmem = kLutBytes + kSmemCtl + kQueueBytes + 2 * kSlabBytes;
 constexpr float kQuantum = 268435456.0f;       // 2^28: p / u_c = p * 2^28 / l_c
 
 // LUT element offset (in float4) of (pair, stage s, code j)
@@ -412,7 +424,6 @@ __device__ __forceinline__ uint32_t field_at7(uint32_t w0, uint32_t w1, uint32_t
 
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
-
 // L2 cache policies: streamed-once code records evict first, the per-pair LUTs (re-read once per
 // chunk by every CTA on the pair) evict last
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -595,6 +606,7 @@ struct MainArgs {
     const uint2* vwin;       // [vnwin]: (start bit, s0 | s1 << 8)
     const uint8_t* vwin_of;  // [vn]: window of each stage
     uint32_t vtotal;         // sum S_v (<= kHistStride): histogram entries per head
+    uint32_t vslab;          // value rows staged in shared memory per slab (row_bits <= kMaxSlabRowBits)
     const float* veff;
     uint64_t n_comp;
     uint32_t n_pairs;
@@ -605,10 +617,28 @@ struct MainArgs {
     float* part_l;           // [slots][G]
 };
 
+// VQKV_ATTN_PHASES (diagnostics builds only): thread 0 of every CTA accumulates clock64 per phase
+// into vqkv_attn_phase_clk[cta][8]: keys (incl. LUT waits), LUT waits, softmax, values, fold, contraction, chunks
+#ifdef VQKV_ATTN_PHASES
+__device__ unsigned long long vqkv_attn_phase_clk[256][16];
+#define PHASE_T(v) long long v = clock64()
+#define PHASE_ADD(i, t0) do { ph_acc[i] += clock64() - (t0); } while (0)
+#define PHASE_CNT(i) do { ph_acc[i] += 1; } while (0)
+#define PHASE_DECL unsigned long long ph_acc[16] = {0};
+#define PHASE_FLUSH do { if (threadIdx.x == 0) for (int i_ = 0; i_ < 16; ++i_) vqkv_attn_phase_clk[blockIdx.x][i_] += ph_acc[i_]; } while (0)
+#else
+#define PHASE_CNT(i) (void)0
+#define PHASE_DECL
+#define PHASE_FLUSH (void)0
+#define PHASE_T(v) (void)0
+#define PHASE_ADD(i, t0) (void)0
+#endif
+
 constexpr uint32_t kUnit = kThreads;           // tokens per unit (one per thread)
 constexpr uint32_t kUnitsPerChunk = kTok;      // 16 units = one 8192-token chunk
 constexpr uint32_t kHistStride = 8192;         // histogram words per head: [head][entry]
-constexpr uint32_t kTmemCols = 256;            // fp32 accumulator [head][entry]: 4 x 64 columns x 128 lanes
+constexpr uint32_t kTmemCols = 512;            // [0, 256): fp32 accumulator [head][entry] (4 x 64 columns x 128 lanes);
+                                               // [256, 512): the chunk's fixed-point weights (16 tokens x 4 heads per thread)
 
 // the CTA owning unit x: largest b with floor(U b / n) <= x
 __host__ __device__ __forceinline__ uint32_t cta_of_unit(uint64_t x, uint64_t U, uint32_t n) {
@@ -616,6 +646,117 @@ __host__ __device__ __forceinline__ uint32_t cta_of_unit(uint64_t x, uint64_t U,
     while (b + 1 < n && (U * (b + 1)) / n <= x) ++b;
     while (b > 0 && (U * b) / n > x) --b;
     return uint32_t(b);
+}
+
+// The value tables of the chunk loop (smem control block) and the pair's value rows.
+struct ValueHist {
+    const uint8_t* vc;     // the pair's value payload
+    const uint8_t* vend;   // end of the last pair's payload (reads stop here)
+    uint64_t row_bits;
+    uint32_t nwin;
+    const uint8_t* ctl;    // smem control block: vrow / vsz / vfld / wstart / wrange tables
+    uint32_t hist;         // smem address of the histograms [head][entry]
+};
+
+// One (token, head) entry of the value phase: the token's value row is read in 64-bit windows (the
+// loads of the first 4 windows issued up front) and each stage's bin of that head gets one shared
+// atomic.  Out of line: keeps the chunk loop's registers for the logits.
+__device__ __noinline__ void hist_entry(const ValueHist& vh, uint32_t t, uint32_t g, uint32_t Pv) {
+    const uint32_t* vrow = reinterpret_cast<const uint32_t*>(vh.ctl + 512);
+    const uint32_t* vfld = vrow + 128;
+    const uint32_t* wstart = vfld + 64;
+    const uint32_t* wrange = wstart + 16;
+    const uint64_t* vc64 = reinterpret_cast<const uint64_t*>(reinterpret_cast<uintptr_t>(vh.vc) & ~uintptr_t(7));
+    const uint32_t vbase_bits = uint32_t((reinterpret_cast<uintptr_t>(vh.vc) & 7u) * 8u);
+    const uint64_t vwords = (reinterpret_cast<uintptr_t>(vh.vend) - reinterpret_cast<uintptr_t>(vc64)) >> 3;
+    const uint32_t hb = vh.hist + g * (kHistStride * 4u);
+    const uint64_t rbit = uint64_t(vbase_bits) + uint64_t(t) * vh.row_bits;
+    constexpr int kW = 4;  // windows loaded up front (16 x 9-bit value rows need 3)
+    uint64_t lo[kW], hi[kW];
+#pragma unroll
+    for (int w = 0; w < kW; ++w) {
+        lo[w] = hi[w] = 0;
+        if (uint32_t(w) < vh.nwin) {
+            const uint64_t wi = (rbit + wstart[w]) >> 6;
+            if (wi + 1 < vwords) {
+                lo[w] = __ldg(vc64 + wi);
+                hi[w] = __ldg(vc64 + wi + 1);
+            }
+        }
+    }
+    for (uint32_t w = 0; w < vh.nwin; ++w) {
+        const uint64_t pos = rbit + wstart[w];
+        uint64_t x;
+        if ((pos >> 6) + 1 < vwords) {
+            uint64_t l, h;
+            if (w < uint32_t(kW)) {
+                l = lo[0], h = hi[0];
+#pragma unroll
+                for (int k = 1; k < kW; ++k)
+                    if (w == uint32_t(k)) l = lo[k], h = hi[k];
+            } else {
+                l = __ldg(vc64 + (pos >> 6));
+                h = __ldg(vc64 + (pos >> 6) + 1);
+            }
+            const uint32_t sh = uint32_t(pos & 63u);
+            x = sh ? ((l >> sh) | (h << (64u - sh))) : l;
+        } else {  // the last words of the buffer
+            x = read_bits64(vh.vc, uint64_t(t) * vh.row_bits + wstart[w], vh.vend);
+        }
+        const uint32_t r = wrange[w];
+        for (uint32_t st = r & 0xFFu; st < (r >> 8); ++st) {
+            const uint32_t f = vfld[st];
+            const uint32_t z = uint32_t(x >> (f & 0xFFu)) & ((1u << (f >> 8)) - 1u);
+            red_shared_add(hb + (vrow[st] + z) * 4u, Pv);
+        }
+    }
+}
+
+// hist_entry with the token's value row staged in shared memory: rbit = the row's first bit relative to
+// the (16 B-aligned) slab buffer at smem address vbuf.
+__device__ __noinline__ void hist_entry_smem(uint32_t vbuf, uint32_t rbit, uint32_t nwin, const uint8_t* ctl,
+                                             uint32_t hb, uint32_t Pv) {
+    const uint32_t* vrow = reinterpret_cast<const uint32_t*>(ctl + 512);
+    const uint32_t* vfld = vrow + 128;
+    const uint32_t* wstart = vfld + 64;
+    const uint32_t* wrange = wstart + 16;
+    for (uint32_t w = 0; w < nwin; ++w) {
+        const uint32_t pos = rbit + wstart[w];
+        uint64_t l, h;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(l) : "r"(vbuf + ((pos >> 6) << 3)));
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(h) : "r"(vbuf + ((pos >> 6) << 3) + 8u));
+        const uint32_t sh = pos & 63u;
+        const uint64_t x = sh ? ((l >> sh) | (h << (64u - sh))) : l;
+        const uint32_t r = wrange[w];
+        for (uint32_t st = r & 0xFFu; st < (r >> 8); ++st) {
+            const uint32_t f = vfld[st];
+            const uint32_t z = uint32_t(x >> (f & 0xFFu)) & ((1u << (f >> 8)) - 1u);
+            red_shared_add(hb + (vrow[st] + z) * 4u, Pv);
+        }
+    }
+}
+
+// A slab of a chunk's value rows, [st0, st1) of the pair, as bulk-copied into a slab buffer: the copy
+// covers the 16 B-aligned bytes around the rows (never past the payload's last 16 B-aligned byte);
+// head = bits between the buffer start and row st0; staged = bits of the buffer holding row data.
+struct Slab {
+    const uint8_t* src;
+    uint32_t bytes, head, staged;
+};
+__device__ __forceinline__ Slab slab_of(const uint8_t* vc, const uint8_t* vend, uint64_t row_bits, uint32_t st0,
+                                        uint32_t st1) {
+    Slab sl;
+    const uint8_t* b0 = vc + (uint64_t(st0) * row_bits >> 3);  // st0 * row_bits is a multiple of 8 (st0 % 512 == 0)
+    const uint8_t* b1 = vc + ((uint64_t(st1) * row_bits + 7) >> 3);
+    const uintptr_t s0 = reinterpret_cast<uintptr_t>(b0) & ~uintptr_t(15);
+    uintptr_t s1 = (reinterpret_cast<uintptr_t>(b1) + 15) & ~uintptr_t(15);
+    const uintptr_t e16 = reinterpret_cast<uintptr_t>(vend) & ~uintptr_t(15);
+    if (s1 > e16) s1 = e16 > s0 ? e16 : s0;
+    sl.src = reinterpret_cast<const uint8_t*>(s0);
+    sl.bytes = uint32_t(s1 - s0);
+    sl.head = uint32_t(reinterpret_cast<uintptr_t>(b0) - s0) * 8u;
+    sl.staged = sl.bytes * 8u;
+    return sl;
 }
 
 // L2 prefetch of the records of one LUT group of a chunk (both planes), ahead of the LDGs.  Out of line:
@@ -762,9 +903,13 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
     uint32_t* vfld = vsz + 64;                                    // [64]
     uint32_t* wstart = vfld + 64;                                 // [16]
     uint32_t* wrange = wstart + 16;                               // [16]: s0 | s1 << 8
-    uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw + kLutBytes + kSmemCtl) + warp * (kQueueCap * (1 + kG));
+    uint2* queue = reinterpret_cast<uint2*>(smem_raw + kLutBytes + kSmemCtl) + warp * kQueueCap;
+    uint64_t* vbar = reinterpret_cast<uint64_t*>(ctl + 48);      // [2]: slab buffers full
+    const uint32_t vbuf0 = ptx::smem_u32(smem_raw + kLutBytes + kSmemCtl + kQueueBytes);
     if (tid == 0) {
         ptx::mbar_init(ptx::smem_u32(bar), 1);
+        ptx::mbar_init(ptx::smem_u32(&vbar[0]), 1);
+        ptx::mbar_init(ptx::smem_u32(&vbar[1]), 1);
         ptx::fence_mbar_init();
     }
     if (tid < a.vn) {
@@ -786,6 +931,8 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    PHASE_DECL
+    PHASE_T(t_kernel);
     const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
     const uint32_t lut_s = ptx::smem_u32(lutb);
     const uint32_t barp = ptx::smem_u32(bar);
@@ -814,6 +961,17 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
         for (uint32_t off = 0; off < grp_bytes; off += 32768u)
             bulk_g2s_hint(lut_s + off, src + off, min(32768u, grp_bytes - off), barp, pol_last);
     };
+    // slab sl of a chunk's value rows into slab buffer sl & 1 (thread 0)
+    auto issue_slab = [&](uint32_t pair, uint32_t c0, uint32_t t1, uint32_t sl) {
+        const uint32_t st0 = c0 + sl * kSlabTok;
+        if (st0 >= t1) return;
+        const Slab x = slab_of(a.vcodes + uint64_t(pair) * a.vstride, a.vend, a.vrow_bits, st0, min(t1, st0 + kSlabTok));
+        const uint32_t vb = ptx::smem_u32(&vbar[sl & 1u]);
+        ptx::mbar_arrive_expect_tx(vb, x.bytes);
+        for (uint32_t off = 0; off < x.bytes; off += 32768u)
+            bulk_g2s_hint(vbuf0 + (sl & 1u) * kSlabBytes + off, x.src + off, min(32768u, x.bytes - off), vb, pol_first);
+    };
+    uint32_t vph = 0;  // slab buffer parities
     const uint32_t l7 = (lane & 7u) << 4;  // this lane's slot rotation (token & 7 == lane & 7: units are 512-aligned)
     const uint32_t hg = warp >> 2, hlq = warp & 3u;  // fold / contraction: head, TMEM lane quarter
     const uint32_t ncol = (a.vtotal + 127u) >> 7;     // accumulator columns per head (<= 64)
@@ -839,12 +997,13 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
         const uint32_t nt = t1 - c0;
         const bool has_next = ch.next < u_end;
         const uint8_t* krec = a.krec + uint64_t(pair) * a.krec_stride;
+        PHASE_T(t_keys);
         float2 lg[kTok][2];
 #pragma unroll
         for (int k = 0; k < kTok; ++k) lg[k][0] = lg[k][1] = make_float2(0.f, 0.f);
         // ---- keys: per LUT group, 8 conflict-free lookups per token; record loads run one batch of
         // 4 tokens ahead of the lookups
-        constexpr int kB = 2;  // tokens per record batch (loaded one batch ahead of the lookups)
+        constexpr int kB = VQKV_ATTN_KB;  // tokens per record batch (loaded one batch ahead of the lookups)
         uint2 w[kB];
         uint32_t h[kB];
         const uint32_t tok0 = c0 + tid, tlast = t1 - 1u;  // record indices fit 32 bits
@@ -860,7 +1019,6 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
                 ho[k] = ldg_stream_u16(rhi + t, pol_first);
             }
         };
-        if (tid == 32) prefetch_values(a.vcodes + uint64_t(pair) * a.vstride, a.vrow_bits, c0, t1, a.vend, pol_first);
         load_batch(0, 0, w, h);
         for (uint32_t g = 0; g < a.ng; ++g) {
             if (tid == 0) {
@@ -871,7 +1029,19 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
                     prefetch_group(a.krec, a.krec_stride, a.cap, nx.pair, 0, nx.c0, nx.t1, pol_first);
                 }
             }
+            if (g + 1 == a.ng) {  // the value rows: the first two slabs into shared memory (or L2) ahead of the value phase
+                if (a.vslab) {
+                    if (tid == 0) {
+                        issue_slab(pair, c0, t1, 0);
+                        issue_slab(pair, c0, t1, 1);
+                    }
+                } else if (tid == 32) {
+                    prefetch_values(a.vcodes + uint64_t(pair) * a.vstride, a.vrow_bits, c0, t1, a.vend, pol_last);
+                }
+            }
+            PHASE_T(tw);
             ptx::mbar_wait(barp, phase);
+            PHASE_ADD(1, tw);
             phase ^= 1u;
 #pragma unroll
             for (int kb = 0; kb < kTok; kb += kB) {
@@ -918,6 +1088,8 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
             if (tid == 0 && g + 1 < a.ng) issue(pair, g + 1);
         }
 
+        PHASE_ADD(0, t_keys);
+        PHASE_T(t_soft);
         // ---- chunk softmax statistics (exact fp32 weights)
         float4 mloc = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
 #pragma unroll
@@ -943,90 +1115,163 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
             lloc.w += p3;
         }
         const float4 lc = block_sum4(lloc, red);
-        // fixed point relative to the chunk's normaliser: P = rint(p / u_c), u_c = l_c 2^-28
+        // fixed point relative to the chunk's normaliser: P = rint(p / u_c), u_c = l_c 2^-28.  The weights go
+        // to this thread's TMEM columns (256 + 64 (warp / 4) + 4 k + g): the value phase reads them back 4
+        // tokens at a time, so the logit registers are free for its row loads
         const float4 qs = make_float4(kQuantum / lc.x, kQuantum / lc.y, kQuantum / lc.z, kQuantum / lc.w);
-        uint32_t P[kTok][kG];
+        const uint32_t tP = tmem + ((hlq * 32u) << 16) + 256u + hg * 64u;
 #pragma unroll
-        for (int k = 0; k < kTok; ++k) {
-            P[k][0] = __float2uint_rn(lg[k][0].x * qs.x);
-            P[k][1] = __float2uint_rn(lg[k][0].y * qs.y);
-            P[k][2] = __float2uint_rn(lg[k][1].x * qs.z);
-            P[k][3] = __float2uint_rn(lg[k][1].y * qs.w);
+        for (int k0 = 0; k0 < kTok; k0 += 8) {
+            float pw[32];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                pw[4 * k + 0] = __uint_as_float(__float2uint_rn(lg[k0 + k][0].x * qs.x));
+                pw[4 * k + 1] = __uint_as_float(__float2uint_rn(lg[k0 + k][0].y * qs.y));
+                pw[4 * k + 2] = __uint_as_float(__float2uint_rn(lg[k0 + k][1].x * qs.z));
+                pw[4 * k + 3] = __uint_as_float(__float2uint_rn(lg[k0 + k][1].y * qs.w));
+            }
+            ptx::tmem_st32(tP + uint32_t(k0) * 4u, pw);
         }
-        // ---- values: int32 histograms [head][entry] over the LUT buffer.  The tokens with a nonzero
-        // weight are compacted into a per-warp queue and processed 32 at a time, lane = token: its
-        // value row is read in 64-bit windows and every (stage, head) bin gets one shared atomic.
+        ptx::tc_wait_st();
+        PHASE_ADD(2, t_soft);
+        PHASE_T(t_val);
+        // ---- values: int32 histograms [head][entry] over the LUT buffer.  The (token, head) pairs with a
+        // nonzero weight are compacted into a per-warp queue and processed 32 at a time, lane = entry:
+        // the token's value row is read in 64-bit windows (all loads first) and each stage's bin of
+        // that head gets one shared atomic.
         for (uint32_t i = tid; i < kLutBytes / 16u; i += kThreads) reinterpret_cast<uint4*>(lutb)[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
+        PHASE_ADD(8, t_val);
         {
-            const uint8_t* vc = a.vcodes + uint64_t(pair) * a.vstride;
-            const uint64_t* vc64 = reinterpret_cast<const uint64_t*>(reinterpret_cast<uintptr_t>(vc) & ~uintptr_t(7));
-            const uint32_t vbase_bits = uint32_t((reinterpret_cast<uintptr_t>(vc) & 7u) * 8u);
-            const uint64_t vwords = (reinterpret_cast<uintptr_t>(a.vend) - reinterpret_cast<uintptr_t>(vc64)) >> 3;
-            auto hist_token = [&](uint64_t t, const uint32_t (&Pv)[kG]) {
-                const uint64_t rbit = uint64_t(vbase_bits) + t * a.vrow_bits;
-                for (uint32_t wi_ = 0; wi_ < a.vnwin; ++wi_) {
-                    const uint64_t pos = rbit + wstart[wi_];
-                    const uint64_t wi = pos >> 6;
-                    uint64_t x;
-                    if (wi + 1 < vwords) {
-                        const uint64_t lo = __ldg(vc64 + wi), hi = __ldg(vc64 + wi + 1);
-                        const uint32_t sh = uint32_t(pos & 63u);
-                        x = sh ? ((lo >> sh) | (hi << (64u - sh))) : lo;
-                    } else {  // the last words of the buffer
-                        x = read_bits64(vc, t * a.vrow_bits + wstart[wi_], a.vend);
+            ValueHist vh;
+            vh.vc = a.vcodes + uint64_t(pair) * a.vstride;
+            vh.vend = a.vend;
+            vh.row_bits = a.vrow_bits;
+            vh.nwin = a.vnwin;
+            vh.ctl = ctl;
+            vh.hist = lut_s;
+            const uint8_t* vcp = a.vcodes + uint64_t(pair) * a.vstride;
+            // lane = (entry, stage) processing: this lane's stage and its field / histogram row
+            const uint32_t lanes_e = a.vn <= 16u ? 16u : (a.vn <= 32u ? 32u : 0u);
+            const uint32_t s_st = lanes_e ? lane % lanes_e : 0u;
+            const bool s_on = lanes_e != 0u && s_st < a.vn;
+            const StageInfo s_si = a.vst[s_on ? s_st : 0u];
+            const uint32_t s_bit = s_si.bit_off, s_bits = s_si.bits, s_row = vrow[s_on ? s_st : 0u];
+            const uint32_t s_mask = s_bits >= 32u ? 0xFFFFFFFFu : ((1u << s_bits) - 1u);
+            for (uint32_t sl = 0; sl < uint32_t(kTok) / 4u; ++sl) {
+                const uint32_t st0 = c0 + sl * kSlabTok;
+                if (st0 >= t1) break;
+                const Slab x = slab_of(vcp, a.vend, a.vrow_bits, st0, min(t1, st0 + kSlabTok));
+                const uint32_t vbuf = vbuf0 + (sl & 1u) * kSlabBytes;
+                // every row of the slab in the staged bytes (all but the payload buffer's last rows)
+                const bool all_staged = a.vslab && x.head + (min(t1, st0 + kSlabTok) - st0) * uint32_t(a.vrow_bits) <= x.staged;
+                PHASE_T(t_sw);
+                if (a.vslab) {
+                    ptx::mbar_wait(ptx::smem_u32(&vbar[sl & 1u]), (vph >> (sl & 1u)) & 1u);
+                    vph ^= 1u << (sl & 1u);
+                }
+                PHASE_ADD(9, t_sw);
+                PHASE_T(t_cp);
+                // a batch of queued entries, lane = (entry, stage): lanes_e lanes per entry (16 when the
+                // value stack has <= 16 stages), each extracting its stage's code from the staged row and
+                // doing that bin's one atomic -- short dependency chains instead of a 16-stage loop per lane
+                auto process_batch = [&](uint32_t b0, uint32_t n) {
+#if VQKV_ATTN_EXP == 2
+                    return;
+#endif
+                    if (!all_staged || lanes_e == 0u) {  // generic path: lane = entry
+                        if (lane < n) {
+                            const uint2 e = queue[b0 + lane];
+                            const uint32_t lt = e.x & 0xFFFFu, g = e.x >> 16;
+                            const uint32_t rbit = x.head + (c0 + lt - st0) * uint32_t(a.vrow_bits);
+                            if (a.vslab && rbit + uint32_t(a.vrow_bits) <= x.staged)
+                                hist_entry_smem(vbuf, rbit, a.vnwin, ctl, lut_s + g * (kHistStride * 4u), e.y);
+                            else
+                                hist_entry(vh, c0 + lt, g, e.y);
+                        }
+                        return;
                     }
-                    const uint32_t r = wrange[wi_];
-                    for (uint32_t st = r & 0xFFu; st < (r >> 8); ++st) {
-                        const uint32_t f = vfld[st];
-                        const uint32_t z = uint32_t(x >> (f & 0xFFu)) & ((1u << (f >> 8)) - 1u);
-                        const uint32_t b = lut_s + (vrow[st] + z) * 4u;
+                    if (lanes_e == 16u) {
+                        // two entries per step (lanes 0-15 / 16-31), four steps in flight, no branches
+                        const uint32_t sub = lane >> 4;
+                        for (uint32_t i0 = 0; i0 < n; i0 += 8u) {
+                            uint32_t addr[4], pv[4];
+                            uint64_t lw[4], hw[4];
+                            uint32_t sh[4];
 #pragma unroll
-                        for (int g = 0; g < kG; ++g)
-                            red_shared_add_nz(b + uint32_t(g) * (kHistStride * 4u), Pv[g]);
+                            for (int u = 0; u < 4; ++u) {
+                                const uint32_t i = i0 + 2u * uint32_t(u) + sub;
+                                const uint2 e = queue[b0 + min(i, n - 1u)];
+                                const uint32_t lt = e.x & 0xFFFFu, g = e.x >> 16;
+                                const uint32_t pos = x.head + (c0 + lt - st0) * uint32_t(a.vrow_bits) + s_bit;
+                                const uint32_t wa = vbuf + ((pos >> 6) << 3);
+                                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(lw[u]) : "r"(wa));
+                                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(hw[u]) : "r"(wa + 8u));
+                                sh[u] = pos & 63u;
+                                addr[u] = lut_s + (g * kHistStride + s_row) * 4u;
+                                pv[u] = (i < n && s_on) ? e.y : 0u;  // padding steps add nothing
+                            }
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const uint32_t z = uint32_t(sh[u] ? ((lw[u] >> sh[u]) | (hw[u] << (64u - sh[u]))) : lw[u]) & s_mask;
+                                red_shared_add(addr[u] + z * 4u, pv[u]);
+                            }
+                        }
+                        return;
+                    }
+                    const uint32_t per = 32u / lanes_e, sub = lane / lanes_e;
+#pragma unroll 4
+                    for (uint32_t i = sub; i < n; i += per) {
+                        const uint2 e = queue[b0 + i];
+                        const uint32_t lt = e.x & 0xFFFFu, g = e.x >> 16;
+                        const uint32_t pos = x.head + (c0 + lt - st0) * uint32_t(a.vrow_bits) + s_bit;
+                        if (!s_on) continue;
+                        const uint32_t wa = vbuf + ((pos >> 6) << 3);
+                        uint64_t l, h;
+                        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(l) : "r"(wa));
+                        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(h) : "r"(wa + 8u));
+                        const uint32_t shf = pos & 63u;
+                        const uint32_t z = uint32_t(shf ? ((l >> shf) | (h << (64u - shf))) : l) & s_mask;
+                        red_shared_add(lut_s + (g * kHistStride + s_row + z) * 4u, e.y);
+                    }
+                };
+                uint32_t qlen = 0;
+                uint32_t P4[16];
+                ptx::tmem_ld16(tP + sl * 16u, P4);
+                ptx::tc_wait_ld();
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t lt = (sl * 4u + uint32_t(k)) * kThreads + tid;  // token within the chunk
+#pragma unroll
+                    for (int g = 0; g < kG; ++g) {
+                        const bool act = lt < nt && P4[4 * k + g] != 0u;
+                        const uint32_t mask = __ballot_sync(0xffffffffu, act);
+                        if (act)
+                            queue[qlen + __popc(mask & ((1u << lane) - 1u))] = make_uint2(lt | (uint32_t(g) << 16), P4[4 * k + g]);
+                        qlen += __popc(mask);
+                    }
+                    if (qlen >= 32u) {
+                        __syncwarp();
+                        const uint32_t full = qlen & ~31u;
+                        for (uint32_t b = 0; b < full; b += 32u) process_batch(b, 32u);
+                        __syncwarp();
+                        if (lane < qlen - full) queue[lane] = queue[full + lane];  // keep the remainder
+                        __syncwarp();
+                        qlen -= full;
                     }
                 }
-            };
-            uint32_t* qt = queue;
-            uint32_t* qP = queue + kQueueCap;
-            uint32_t qlen = 0;
-            auto flush = [&](uint32_t n) {
-                if (lane < n) {
-                    uint32_t Pv[kG];
-#pragma unroll
-                    for (int g = 0; g < kG; ++g) Pv[g] = qP[lane * kG + g];
-                    hist_token(c0 + qt[lane], Pv);
-                }
-            };
-#pragma unroll
-            for (int k = 0; k < kTok; ++k) {
-                const uint32_t lt = uint32_t(k) * kThreads + tid;  // token within the chunk
-                const bool act = lt < nt && (P[k][0] | P[k][1] | P[k][2] | P[k][3]) != 0u;
-                const uint32_t mask = __ballot_sync(0xffffffffu, act);
-                if (act) {
-                    const uint32_t pos = qlen + __popc(mask & ((1u << lane) - 1u));
-                    qt[pos] = lt;
-#pragma unroll
-                    for (int g = 0; g < kG; ++g) qP[pos * kG + g] = P[k][g];
-                }
-                qlen += __popc(mask);
-                if (qlen >= 32u) {
-                    __syncwarp();
-                    flush(32u);
-                    __syncwarp();
-                    if (lane + 32u < qlen) {  // keep the overflow for the next batch
-                        qt[lane] = qt[lane + 32u];
-#pragma unroll
-                        for (int g = 0; g < kG; ++g) qP[lane * kG + g] = qP[(lane + 32u) * kG + g];
-                    }
-                    __syncwarp();
-                    qlen -= 32u;
-                }
+                __syncwarp();
+                process_batch(0, qlen);  // the slab's remainder (its buffer is recycled next)
+                PHASE_ADD(10, t_cp);
+                PHASE_T(t_sb);
+                __syncthreads();
+                PHASE_ADD(11, t_sb);
+                if (a.vslab && tid == 0 && sl + 2u < uint32_t(kTok) / 4u) issue_slab(pair, c0, t1, sl + 2u);
             }
-            __syncwarp();
-            flush(qlen);
         }
         __syncthreads();
+        PHASE_ADD(3, t_val);
+        PHASE_T(t_fold);
         // ---- fold the chunk into the segment's fp32 accumulator in TMEM, rescaled to the running max.
         // Warp = (head hg, TMEM lane quarter hlq); thread = entries e = 128 c + 32 hlq + lane, c < ncol
         // (TMEM column 64 hg + c): conflict-free smem reads, one tcgen05.ld/st per 32 columns.
@@ -1050,6 +1295,8 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
             *segL = Lrun;
         }
         const uint32_t next_pair = has_next ? ch.next / upp : pair;
+        PHASE_ADD(4, t_fold);
+        PHASE_T(t_con);
 
         if (!has_next || next_pair != pair) {
             // ---- segment end (out of line: keeps the chunk loop's registers for the logits)
@@ -1062,12 +1309,16 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
             first = true;
         }
         __syncthreads();  // the buffer takes the next chunk's first LUT group; segment state updated
+        PHASE_ADD(5, t_con);
+        PHASE_CNT(6);
         if (tid == 0 && has_next) issue(next_pair, 0);
         u = ch.next;
     }
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 0) ptx::tmem_dealloc(tmem, kTmemCols);
+    PHASE_ADD(7, t_kernel);
+    PHASE_FLUSH;
 }
 
 // out[pair][g] = sum_c exp(m_c - M) o_c / sum_c exp(m_c - M) l_c over the pair's segments and its
@@ -1389,6 +1640,7 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         ma.vwin = reinterpret_cast<const uint2*>(vtab);
         ma.vwin_of = vtab + sizeof(uint2) * 16;
         ma.vtotal = uint32_t(vs.total_rows);
+        ma.vslab = vs.row_bits <= kMaxSlabRowBits ? 1u : 0u;
         ma.veff = vs.d_eff;
         ma.n_comp = n_comp;
         ma.n_pairs = a.n_pairs;
@@ -1419,3 +1671,13 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
 }
 
 }  // namespace vqkv_dev
+
+#ifdef VQKV_ATTN_PHASES
+// diagnostics builds only (not part of include/vqkv_c.h): read-and-clear the per-CTA phase clocks
+extern "C" int vqkv_attn_phase_read(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out, vqkv_dev::vqkv_attn_phase_clk, sizeof(unsigned long long) * 256 * 16) != cudaSuccess) return 1;
+    static unsigned long long zero[256 * 16];
+    return cudaMemcpyToSymbol(vqkv_dev::vqkv_attn_phase_clk, zero, sizeof(zero)) != cudaSuccess;
+}
+#endif
