@@ -476,7 +476,19 @@ def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
         q1 = torch.randn(KV_HEADS, G, D, device="cuda", generator=torch.Generator(device="cuda").manual_seed(7))
         part = lambda: Dv.attend_decode(kst, vst, q1, kc, vc, nc, ik, iv, lk, lv, kcodes_gm_cap=kcap)
         o_l, l_l = part()
-        sharding.gather_and_merge(o_l, l_l)
+        # the exchange step through the library's C-ABI entry (vqkv_lse_allgather_combine) on the
+        # process group's own NCCL communicator; torch's all-gather + merge if the pointer is unavailable
+        combine_api = "vqkv_lse_allgather_combine"
+        try:
+            import torch.distributed as dist
+
+            comm = dist.distributed_c10d._get_default_group()._get_backend(torch.device("cuda", local))._comm_ptr()
+            combine = lambda: sharding.nccl_gather_and_merge(comm, o_l.reshape(-1, D), l_l.reshape(-1))
+            combine()
+        except Exception:
+            combine_api = "torch.distributed.all_gather_into_tensor + vqkv_lse_combine"
+            combine = lambda: sharding.gather_and_merge(o_l, l_l)
+            combine()
         torch.cuda.synchronize()
         barrier(world)
         a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
@@ -485,7 +497,7 @@ def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
             o_l, l_l = part()
         a1.record()
         for _ in range(args.steps):
-            sharding.gather_and_merge(o_l, l_l)
+            combine()
         a2.record()
         torch.cuda.synchronize()
         kern = max_over_ranks(a0.elapsed_time(a1) / args.steps, world)
@@ -493,6 +505,7 @@ def bench_attention(torch, Dv, _lib, kst, vst, args, rank, world, local):
         out["sequence_split_1M"] = {
             "config": f"configs[4]: 1 sequence x 1,048,576 tokens over {world} GPUs, 8 KV heads, G=4",
             "tokens_per_gpu": sh.tokens, "ms_attention_per_layer_step": kern, "ms_nccl_lse_combine": comb,
+            "combine_api": combine_api,
             "tokens_per_s": total / ((kern + comb) / 1e3),
         }
     else:

@@ -235,6 +235,21 @@ int vqkv_attend_raw_host(int device, const float* keys_host, const float* values
 int vqkv_lse_combine(const float* parts_o_dev, const float* parts_lse_dev, uint32_t n_parts, uint64_t rows,
                      uint32_t dv, float* out_dev, float* out_lse_dev, void* stream);
 
+/* Sequence-split decode attention (configs[4]), the one exchange step: every rank of the NCCL
+ * communicator `nccl_comm` (an ncclComm_t) holds the partial result of its contiguous token shard for
+ * the same rows (query heads), part_o_dev fp32 [rows][dv] and part_lse_dev fp32 [rows] (the lse output
+ * of vqkv_attend_decode).  One ncclAllGather of both (grouped), then the vqkv_lse_combine merge on every
+ * rank: out_dev [rows][dv], out_lse_dev [rows] (may be null).  gather_o_dev [world][rows][dv] and
+ * gather_lse_dev [world][rows] are caller scratch, or null for stream-ordered allocations.  All work is
+ * stream-ordered on `stream`; NCCL (libnccl.so.2) is loaded on first use. */
+int vqkv_lse_allgather_combine(void* nccl_comm, const float* part_o_dev, const float* part_lse_dev, uint64_t rows,
+                               uint32_t dv, float* gather_o_dev, float* gather_lse_dev, float* out_dev,
+                               float* out_lse_dev, void* stream);
+/* ncclCommInitAll(comms, ndev, devs): one communicator per listed device in this process (the
+ * single-process 8-GPU layout); vqkv_nccl_comm_destroy releases one. */
+int vqkv_nccl_comm_init_all(int ndev, const int* devs, void** comms);
+int vqkv_nccl_comm_destroy(void* comm);
+
 /* ---------------------------------------------------------------------------
  * Diagnostics / test hooks.
  * ------------------------------------------------------------------------- */

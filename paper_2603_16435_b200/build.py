@@ -77,7 +77,7 @@ def build(verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     if _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static", "-lpthread"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static", "-lpthread", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
@@ -98,7 +98,7 @@ def build_diag() -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(lambda s: _compile(s, False, obj_dir, ("-DVQKV_PHASE_CLOCKS",)), srcs))
     if _stale(DIAG_LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", DIAG_LIB, *objs, "-cudart", "static", "-lpthread"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", DIAG_LIB, *objs, "-cudart", "static", "-lpthread", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
@@ -116,7 +116,7 @@ def build_variant(name: str, defines=()) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(lambda s: _compile(s, False, obj_dir, extra), srcs))
     if _stale(lib, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-cudart", "static", "-lpthread"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-cudart", "static", "-lpthread", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

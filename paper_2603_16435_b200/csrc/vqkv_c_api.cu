@@ -835,4 +835,29 @@ int vqkv_lse_combine(const float* o, const float* lse, uint32_t parts, uint64_t 
     });
 }
 
+int vqkv_lse_allgather_combine(void* comm, const float* o, const float* lse, uint64_t rows, uint32_t dv, float* go,
+                               float* gl, float* out, float* out_lse, void* stream) {
+    return guard([&] {
+        need(comm != nullptr, VQKV_INVALID_INPUT, "null NCCL communicator");
+        if (rows == 0) return;
+        need(o && lse && out, VQKV_INVALID_INPUT, "null device buffer");
+        need(dv >= 1, VQKV_INVALID_INPUT, "dv must be >= 1");
+        lse_allgather_combine(comm, o, lse, rows, dv, go, gl, out, out_lse, as_stream(stream));
+    });
+}
+
+int vqkv_nccl_comm_init_all(int ndev, const int* devs, void** comms) {
+    return guard([&] {
+        need(ndev >= 1 && devs && comms, VQKV_INVALID_INPUT, "ndev >= 1 devices and a comms array required");
+        nccl_comm_init_all(ndev, devs, comms);
+    });
+}
+
+int vqkv_nccl_comm_destroy(void* comm) {
+    return guard([&] {
+        need(comm != nullptr, VQKV_INVALID_INPUT, "null NCCL communicator");
+        nccl_comm_destroy(comm);
+    });
+}
+
 }  // extern "C"

@@ -239,5 +239,9 @@ void launch_keycodes_from_gm(const vqkv_stack_s& ks, const uint8_t* gm, uint64_t
                              cudaStream_t s);
 void launch_lse_combine(const float* o, const float* lse, uint32_t parts, uint64_t rows, uint32_t dv, float* out,
                         float* out_lse, cudaStream_t s);
+void nccl_comm_init_all(int ndev, const int* devs, void** comms);
+void nccl_comm_destroy(void* comm);
+void lse_allgather_combine(void* comm, const float* part_o, const float* part_lse, uint64_t rows, uint32_t dv,
+                           float* gather_o, float* gather_lse, float* out, float* out_lse, cudaStream_t s);
 
 }  // namespace vqkv_dev

@@ -100,3 +100,54 @@ def gather_and_merge(o_local: torch.Tensor, lse_local: torch.Tensor, group=None)
     else:
         o, lse = lse_merge(o_all.reshape(world, rows, dv), l_all.reshape(world, rows))
     return o.reshape(o_local.shape), lse.reshape(lse_local.shape)
+
+
+class NcclComms:
+    """ncclCommInitAll over local devices through the library (vqkv_nccl_comm_init_all): the
+    single-process layout a C++ host uses for the 8-GPU sequence split."""
+
+    def __init__(self, devices):
+        import ctypes as C
+
+        from . import _lib
+
+        self.devices = list(devices)
+        n = len(self.devices)
+        self._h = (C.c_void_p * n)()
+        _lib.call("vqkv_nccl_comm_init_all", n, (C.c_int * n)(*self.devices), self._h)
+
+    def comm(self, i: int) -> int:
+        return int(self._h[i])
+
+    def close(self):
+        from . import _lib
+
+        for i in range(len(self.devices)):
+            if self._h[i]:
+                _lib.call("vqkv_nccl_comm_destroy", self._h[i])
+                self._h[i] = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_gather_and_merge(comm: int, o_local: torch.Tensor, lse_local: torch.Tensor):
+    """The library's exchange step (vqkv_lse_allgather_combine): ncclAllGather of this rank's partial
+    (o [rows, dv], lse [rows]) on the communicator's device, then the LSE merge -> (o, lse)."""
+    from . import _lib
+
+    if not (o_local.is_cuda and lse_local.is_cuda):
+        raise ValueError("nccl_gather_and_merge needs CUDA tensors")
+    o_local = o_local.contiguous()
+    lse_local = lse_local.contiguous()
+    rows = lse_local.numel()
+    dv = o_local.shape[-1]
+    out = torch.empty_like(o_local)
+    out_lse = torch.empty_like(lse_local)
+    s = torch.cuda.current_stream(o_local.device).cuda_stream
+    _lib.call("vqkv_lse_allgather_combine", comm, o_local.data_ptr(), lse_local.data_ptr(), rows, dv, None, None,
+              out.data_ptr(), out_lse.data_ptr(), s)
+    return out, out_lse

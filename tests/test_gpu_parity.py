@@ -440,6 +440,18 @@ def test_sequence_split_lut_path_matches_monolithic(torch_mod):
     finally:
         dist.destroy_process_group()
 
+    # the C-ABI exchange step a C++ host calls (vqkv_lse_allgather_combine over an ncclCommInitAll
+    # communicator): world size 1 here, so the merge of the gathered partial is the partial itself
+    comms = sharding.NcclComms([0])
+    try:
+        o2, l2 = sharding.nccl_gather_and_merge(comms.comm(0), parts[5][0].reshape(-1, 128), parts[5][1].reshape(-1))
+        torch.cuda.synchronize()
+        r2, rl2 = Dv.lse_combine(parts[5][0].reshape(1, -1, 128).contiguous(), parts[5][1].reshape(1, -1).contiguous())
+        assert torch.allclose(o2, r2, rtol=1e-6, atol=1e-6)
+        assert torch.allclose(l2, rl2, rtol=1e-6, atol=1e-6)
+    finally:
+        comms.close()
+
 
 def test_attention_lut_large_entries_fall_back_to_ffma(torch_mod):
     """Key entries beyond the fp16 range (|e| >= 2^15) take the FFMA LUT build instead of the
