@@ -250,6 +250,19 @@ int vqkv_lse_allgather_combine(void* nccl_comm, const float* part_o_dev, const f
 int vqkv_nccl_comm_init_all(int ndev, const int* devs, void** comms);
 int vqkv_nccl_comm_destroy(void* comm);
 
+/* One mini-batch of the codebook trainer (trainer.cpp:22-86, accumulate_loss): rows x D fp32 on the device,
+ * quantized with the reference's search order; the per-stage residual chain, loss terms and
+ * straight-through gradients are computed on the GPU in the reference's fp32 operation order.
+ * grad_proj_dev: fp32 [N][D][D] (null: loss only), the gradient of the projections summed over the batch
+ * rows in order (trainer.cpp:62-67; the caller divides the step by rows, trainer.cpp:229-233).
+ * sums_host: double [3 + N] = { sum ||r_N||^2, sum_i ||r_{i+1}||^2, sum_i commitment_i, then per stage i
+ * sum ||r_{i+1}||^2 (holdout_stage_mse) }.  Synchronizes `stream`. */
+int vqkv_train_batch(vqkv_stack_t stack, const float* batch_dev, uint64_t rows, float beta, float gamma,
+                     int square_commitment, float* grad_proj_dev, double* sums_host, void* stream);
+/* vqkv_train_batch with host buffers: batch_host [rows][D], grad_proj_host [N][D][D] (may be null). */
+int vqkv_train_batch_host(vqkv_stack_t stack, const float* batch_host, uint64_t rows, float beta, float gamma,
+                          int square_commitment, float* grad_proj_host, double* sums_host);
+
 /* ---------------------------------------------------------------------------
  * Diagnostics / test hooks.
  * ------------------------------------------------------------------------- */

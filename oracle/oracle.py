@@ -108,6 +108,8 @@ def lib():
                 C.c_int,
                 [fp, fp, C.c_int64, C.c_int64, C.c_int64, fp, C.c_int64, C.c_double, fp],
             ),
+            "orc_train_batch": (C.c_int, [P, fp, C.c_uint64, C.c_float, C.c_float, C.c_int, fp, dp]),
+            "orc_train": (P, [fp, C.c_uint64, C.c_int64, C.c_uint32, u32p, C.c_void_p, C.c_int, dp, dp]),
             "orc_attend_segments": (
                 C.c_int,
                 [P, P, fp, fp, C.c_uint64, u8p, u8p, C.c_uint64, fp, fp, C.c_uint64, fp,
@@ -530,3 +532,42 @@ def classify_codes(got, ref, ins, emax):
         else:
             mism.append(int(r))
     return dict(rows_checked=int(got.shape[0]), mismatches=len(mism), near_ties=ties, mismatch_rows=mism[:16])
+
+
+class TrainConfig(C.Structure):
+    """orc_train_config (trainer.hpp TrainConfig, train_entries = false)."""
+
+    _fields_ = [("learning_rate", C.c_float), ("batch_size", C.c_uint64), ("epochs", C.c_uint64), ("beta", C.c_float),
+                ("gamma", C.c_float), ("seed", C.c_uint64), ("init_scale", C.c_float),
+                ("square_commitment", C.c_int), ("holdout_fraction", C.c_float)]
+
+
+def train_config(learning_rate=0.001, batch_size=65536, epochs=20, beta=0.25, gamma=1.0, seed=0, init_scale=1.0,
+                 square_commitment=False, holdout_fraction=0.01):
+    return TrainConfig(learning_rate, batch_size, epochs, beta, gamma, seed, init_scale, int(square_commitment),
+                       holdout_fraction)
+
+
+def train_batch(stack, batch, beta=0.25, gamma=1.0, square_commitment=False, grads=True):
+    """accumulate_loss over one batch (trainer.cpp:36-86): (sums [3 + N], grad [N, D, D] or None)."""
+    b = f32(batch)
+    n, d = stack.n, stack.dim
+    sums = np.zeros(3 + n, np.float64)
+    g = np.zeros((n, d, d), np.float32) if grads else None
+    _check(lib().orc_train_batch(stack.h, _f(b), b.shape[0], beta, gamma, int(square_commitment),
+                                 _f(g) if grads else None, sums.ctypes.data_as(C.POINTER(C.c_double))))
+    return sums, g
+
+
+def train(data, stage_sizes, cfg, kind=KEY):
+    """train() (trainer.cpp:166-248): (Stack, per_epoch_loss, per_stage_mse)."""
+    x = f32(data)
+    sizes = np.asarray(stage_sizes, np.uint32)
+    el = np.zeros(int(cfg.epochs), np.float64)
+    sm = np.zeros(len(sizes), np.float64)
+    h = lib().orc_train(_f(x), x.shape[0], x.shape[1], len(sizes), sizes.ctypes.data_as(C.POINTER(C.c_uint32)),
+                        C.byref(cfg), kind, el.ctypes.data_as(C.POINTER(C.c_double)),
+                        sm.ctypes.data_as(C.POINTER(C.c_double)))
+    if not h:
+        raise OracleError(1, lib().orc_last_error().decode())
+    return Stack(h), el, sm

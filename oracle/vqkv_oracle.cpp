@@ -29,6 +29,8 @@
 #include <deque>
 #include <fstream>
 #include <limits>
+#include <memory>
+#include <numeric>
 #include <random>
 #include <sstream>
 #include <stdexcept>
@@ -989,4 +991,144 @@ int orc_attend_segments(const orc_stack* kst, const orc_stack* vst, const float*
     });
 }
 
+}  // extern "C"
+
+// ---- trainer (trainer.cpp:22-248), restated for the checker --------------------------------
+namespace orc {
+// one row of accumulate_loss (trainer.cpp:43-79): residual chain, loss sums, gradient outer products
+void train_row(const orc_stack& st, const float* x, float beta, float gamma, bool sq_commit, double* sums,
+               std::vector<float>* grad) {
+    const size_t N = st.stages.size();
+    const int64_t D = st.dim();
+    std::vector<uint32_t> codes(N);
+    std::vector<float> tmp(static_cast<size_t>(D));
+    quantize(st, x, 4096, codes.data(), tmp.data());  // forward_pass (trainer.cpp:22-34)
+    std::vector<std::vector<float>> r(N + 1, std::vector<float>(static_cast<size_t>(D)));
+    std::memcpy(r[0].data(), x, sizeof(float) * size_t(D));
+    for (size_t i = 0; i < N; ++i) {
+        const float* e = &st.stages[i].effective[size_t(codes[i]) * size_t(D)];
+        for (int64_t k = 0; k < D; ++k) r[i + 1][size_t(k)] = r[i][size_t(k)] - e[k];
+    }
+    std::vector<float> sq(N);
+    for (size_t i = 0; i < N; ++i) sq[i] = squared_norm(r[i + 1].data(), D);
+    sums[0] += double(sq[N - 1]);
+    for (size_t i = 0; i < N; ++i) {
+        const double s = double(sq[i]);
+        sums[1] += s;
+        sums[2] += sq_commit ? s : std::sqrt(s);
+        sums[3 + i] += s;
+    }
+    if (!grad) return;
+    const std::vector<float>& fin = r[N];
+    std::vector<float> suffix(static_cast<size_t>(D), 0.f);
+    std::vector<std::vector<float>> gev(N, std::vector<float>(static_cast<size_t>(D)));
+    for (size_t i = N; i-- > 0;) {
+        const float b2 = 2.0f * beta;
+        const float norm = std::sqrt(sq[i]);
+        for (int64_t k = 0; k < D; ++k) {
+            gev[i][size_t(k)] = (-2.0f * fin[size_t(k)] - b2 * r[i + 1][size_t(k)]) - gamma * suffix[size_t(k)];
+            const float step = sq_commit ? 2.0f * r[i + 1][size_t(k)] : (norm > 0.0f ? r[i + 1][size_t(k)] / norm : 0.0f);
+            suffix[size_t(k)] = suffix[size_t(k)] + step;
+        }
+    }
+    for (size_t i = 0; i < N; ++i) {
+        const float* ent = &st.stages[i].entries[size_t(codes[i]) * size_t(D)];
+        float* g = grad[i].data();
+        for (int64_t a = 0; a < D; ++a)
+            for (int64_t b = 0; b < D; ++b) g[size_t(a * D + b)] = g[size_t(a * D + b)] + gev[i][size_t(a)] * ent[b];
+    }
+}
+}  // namespace orc
+
+extern "C" {
+int orc_train_batch(const orc_stack* s, const float* batch, uint64_t rows, float beta, float gamma,
+                    int square_commitment, float* grad, double* sums) {
+    return guard([&] {
+        const size_t N = s->stages.size();
+        const int64_t D = s->dim();
+        for (size_t i = 0; i < 3 + N; ++i) sums[i] = 0.0;
+        std::vector<std::vector<float>> g;
+        if (grad) g.assign(N, std::vector<float>(size_t(D * D), 0.f));
+        for (uint64_t r = 0; r < rows; ++r)
+            orc::train_row(*s, batch + r * uint64_t(D), beta, gamma, square_commitment != 0, sums, grad ? g.data() : nullptr);
+        if (grad)
+            for (size_t i = 0; i < N; ++i) std::memcpy(grad + i * size_t(D * D), g[i].data(), sizeof(float) * size_t(D * D));
+    });
+}
+
+orc_stack* orc_train(const float* data, uint64_t count, int64_t dim, uint32_t n_stages, const uint32_t* sizes,
+                     const orc_train_config* c, int kind, double* epoch_loss, double* stage_mse) {
+    orc_stack* out = nullptr;
+    int st = guard([&] {
+        if (count < 1 || dim < 1) orc::invalid_input("dataset must have count >= 1 and D >= 1");
+        size_t batch = size_t(c->batch_size);
+        if (count < 10 * batch) batch = std::min<size_t>(batch, 1024);
+        std::mt19937_64 rng(c->seed);
+        std::vector<size_t> order(count);
+        std::iota(order.begin(), order.end(), size_t{0});
+        std::shuffle(order.begin(), order.end(), rng);
+        size_t n_hold = 0;
+        if (count >= 2) {
+            n_hold = std::max<size_t>(1, size_t(std::llround(double(count) * c->holdout_fraction)));
+            n_hold = std::min<size_t>(n_hold, count - 1);
+        }
+        std::vector<size_t> hold(order.end() - ptrdiff_t(n_hold), order.end());
+        std::vector<size_t> train_rows(order.begin(), order.end() - ptrdiff_t(n_hold));
+        if (hold.empty()) hold = train_rows;
+        // init_stack (trainer.cpp:125-148): its own generator on the same seed
+        auto s = std::make_unique<orc_stack>();
+        s->kind = kind;
+        {
+            std::mt19937_64 irng(c->seed);
+            std::normal_distribution<float> gauss(0.0f, 1.0f);
+            for (uint32_t i = 0; i < n_stages; ++i) {
+                orc::Codebook cb;
+                cb.S = sizes[i];
+                cb.D = dim;
+                cb.entries.resize(size_t(cb.S * dim));
+                for (auto& v : cb.entries) v = c->init_scale * gauss(irng);
+                cb.projection.assign(size_t(dim * dim), 0.f);
+                for (int64_t k = 0; k < dim; ++k) cb.projection[size_t(k * dim + k)] = 1.f;
+                cb.refresh();
+                s->stages.push_back(std::move(cb));
+            }
+        }
+        const size_t N = n_stages;
+        std::vector<float> buf, grad(N * size_t(dim * dim));
+        std::vector<double> sums(3 + N);
+        for (uint64_t e = 0; e < c->epochs; ++e) {
+            std::shuffle(train_rows.begin(), train_rows.end(), rng);
+            double eloss = 0.0;
+            size_t seen = 0;
+            for (size_t b0 = 0; b0 < train_rows.size(); b0 += batch) {
+                const size_t len = std::min(batch, train_rows.size() - b0);
+                buf.resize(len * size_t(dim));
+                for (size_t i = 0; i < len; ++i)
+                    std::memcpy(&buf[i * size_t(dim)], data + train_rows[b0 + i] * uint64_t(dim), sizeof(float) * size_t(dim));
+                int r = orc_train_batch(s.get(), buf.data(), len, c->beta, c->gamma, c->square_commitment, grad.data(),
+                                        sums.data());
+                if (r != ORC_OK) orc::invalid_input(g_err);
+                const double recon = sums[0] / double(len), pull = sums[1] / double(len), com = sums[2] / double(len);
+                const double total = recon + c->beta * pull + c->gamma * com;
+                if (!std::isfinite(total)) orc::invalid_input("training loss became non-finite");
+                const float step = c->learning_rate / float(len);
+                for (size_t i = 0; i < N; ++i) {
+                    auto& p = s->stages[i].projection;
+                    for (size_t k = 0; k < p.size(); ++k) p[k] = p[k] - step * grad[i * size_t(dim * dim) + k];
+                    s->stages[i].refresh();
+                }
+                eloss += total * double(len);
+                seen += len;
+            }
+            if (epoch_loss) epoch_loss[e] = eloss / double(seen);
+        }
+        if (stage_mse) {
+            std::vector<double> acc(3 + N, 0.0);
+            for (size_t rr : hold) orc::train_row(*s, data + rr * uint64_t(dim), 0.f, 0.f, false, acc.data(), nullptr);
+            for (size_t i = 0; i < N; ++i) stage_mse[i] = acc[3 + i] / double(hold.size());
+        }
+        out = s.release();
+    });
+    return st == ORC_OK ? out : nullptr;
+}
 }  // extern "C"

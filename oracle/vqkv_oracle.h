@@ -138,6 +138,27 @@ int orc_attend_segments(const orc_stack* kst, const orc_stack* vst, const float*
                         const float* local_v, uint64_t n_local, const float* q, double scale,
                         uint64_t block_rows, float* out, double* lse);
 
+/* ---- trainer (proj/core/src/trainer.cpp:22-248) ---------------------------- */
+/* accumulate_loss over one batch (trainer.cpp:36-86): sums[0..2] = sum over rows of ||r_N||^2,
+   sum_i ||r_{i+1}||^2, sum_i commitment_i (before the division by the batch size), sums[3 + i] = sum of
+   ||r_{i+1}||^2 per stage; grad (N x D x D, or NULL) = the projections' gradient summed over rows. */
+int orc_train_batch(const orc_stack*, const float* batch, uint64_t rows, float beta, float gamma,
+                    int square_commitment, float* grad, double* sums);
+typedef struct {
+    float learning_rate;
+    uint64_t batch_size;
+    uint64_t epochs;
+    float beta, gamma;
+    uint64_t seed;
+    float init_scale;
+    int square_commitment;
+    float holdout_fraction;
+} orc_train_config;
+/* train() (trainer.cpp:166-248, train_entries = false): returns the trained stack; epoch_loss [epochs],
+   stage_mse [N] (may be NULL). */
+orc_stack* orc_train(const float* data, uint64_t count, int64_t dim, uint32_t n_stages, const uint32_t* sizes,
+                     const orc_train_config* cfg, int kind, double* epoch_loss, double* stage_mse);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,8 @@ _SIGS = {
     "vqkv_lse_allgather_combine": (C.c_int, [P, P, P, C.c_uint64, C.c_uint32, P, P, P, P, P]),
     "vqkv_nccl_comm_init_all": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(P)]),
     "vqkv_nccl_comm_destroy": (C.c_int, [P]),
+    "vqkv_train_batch": (C.c_int, [P, P, C.c_uint64, C.c_float, C.c_float, C.c_int, P, C.POINTER(C.c_double), P]),
+    "vqkv_train_batch_host": (C.c_int, [P, P, C.c_uint64, C.c_float, C.c_float, C.c_int, P, C.POINTER(C.c_double)]),
     "vqkv_encode_counters": (C.c_int, [P, u64p]),
     "vqkv_encode_phase_clocks": (C.c_int, [P, u64p]),
     "vqkv_payload_append": (C.c_int, [P, C.c_uint64, C.c_uint64, P, C.c_uint64, C.c_uint64, C.c_uint32, P]),

@@ -141,6 +141,24 @@ def build_cpp_tests() -> str:
     return CPP_TEST_BIN
 
 
+CLI_SRC = os.path.join(ROOT, "tools", "vqkv_cli.cpp")
+CLI_BIN = os.path.join(ROOT, "build", "vqkv")
+
+
+def build_cli() -> str:
+    """The `vqkv` command-line front end (tools/vqkv_cli.cpp) over the drop-in C++ API."""
+    lib = build()
+    deps = [CLI_SRC, lib] + _headers()
+    if _stale(CLI_BIN, deps):
+        os.makedirs(os.path.dirname(CLI_BIN), exist_ok=True)
+        cmd = ["g++", "-O2", "-std=c++17", "-I" + os.path.join(ROOT, "include"), CLI_SRC, "-o", CLI_BIN,
+               "-L" + OUT_DIR, "-lvqkv_b200", "-Wl,-rpath," + OUT_DIR, "-Wl,-rpath,$ORIGIN/../paper_2603_16435_b200/lib"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"CLI build failed:\n{r.stdout}\n{r.stderr}")
+    return CLI_BIN
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))
     print(build_cpp_tests())

@@ -135,7 +135,7 @@ void stack_build_device(vqkv_stack_s& st, const float* entries_host, const float
         st.stages[s].max_norm = std::nextafter(std::sqrt(m), INFINITY);
     }
     VQKV_CUDA(cudaMemcpy(st.d_stages, st.stages.data(), sizeof(StageInfo) * st.n, cudaMemcpyHostToDevice));
-    cudaFree(d_entries);
+    st.d_raw = d_entries;  // kept: the trainer's straight-through gradients use the raw entries (trainer.cpp:62-67)
     cudaFree(d_proj);
 }
 

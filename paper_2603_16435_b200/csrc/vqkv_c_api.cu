@@ -322,6 +322,7 @@ int vqkv_stack_destroy(vqkv_stack_t s) {
         cudaDeviceSynchronize();
         cudaFree(s->d_stages);
         cudaFree(s->d_eff);
+        cudaFree(s->d_raw);
         cudaFree(s->d_sqn);
         cudaFree(s->d_eff16);
         cudaFree(s->d_eff16lo);
@@ -843,6 +844,39 @@ int vqkv_lse_allgather_combine(void* comm, const float* o, const float* lse, uin
         need(o && lse && out, VQKV_INVALID_INPUT, "null device buffer");
         need(dv >= 1, VQKV_INVALID_INPUT, "dv must be >= 1");
         lse_allgather_combine(comm, o, lse, rows, dv, go, gl, out, out_lse, as_stream(stream));
+    });
+}
+
+int vqkv_train_batch(vqkv_stack_t s, const float* batch, uint64_t rows, float beta, float gamma, int square_commitment,
+                     float* grad_proj, double* sums, void* stream) {
+    return guard([&] {
+        check_stack(s);
+        need(rows >= 1, VQKV_INVALID_INPUT, "loss needs a nonempty batch");
+        need(batch && sums, VQKV_INVALID_INPUT, "null buffer");
+        need(beta >= 0.f && gamma >= 0.f, VQKV_INVALID_INPUT, "beta and gamma must be nonnegative");
+        DeviceGuard g(s->device);
+        train_batch(*s, batch, rows, beta, gamma, square_commitment != 0, grad_proj, sums, as_stream(stream));
+    });
+}
+
+int vqkv_train_batch_host(vqkv_stack_t s, const float* batch, uint64_t rows, float beta, float gamma,
+                          int square_commitment, float* grad_proj, double* sums) {
+    return guard([&] {
+        check_stack(s);
+        need(rows >= 1, VQKV_INVALID_INPUT, "loss needs a nonempty batch");
+        need(batch && sums, VQKV_INVALID_INPUT, "null buffer");
+        need(beta >= 0.f && gamma >= 0.f, VQKV_INVALID_INPUT, "beta and gamma must be nonnegative");
+        DeviceGuard g(s->device);
+        std::lock_guard<std::mutex> lk(s->host_mu);
+        const uint64_t D = s->dim, gb = grad_proj ? sizeof(float) * uint64_t(s->n) * D * D : 0;
+        HostScratch hs(*s);
+        const uint64_t ob = hs.add(sizeof(float) * rows * D), og = hs.add(std::max<uint64_t>(gb, 1));
+        uint8_t* base = hs.commit();
+        float* db = reinterpret_cast<float*>(base + ob);
+        float* dg = reinterpret_cast<float*>(base + og);
+        VQKV_CUDA(cudaMemcpy(db, batch, sizeof(float) * rows * D, cudaMemcpyHostToDevice));
+        train_batch(*s, db, rows, beta, gamma, square_commitment != 0, grad_proj ? dg : nullptr, sums, nullptr);
+        if (grad_proj) VQKV_CUDA(cudaMemcpy(grad_proj, dg, gb, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -85,6 +85,7 @@ struct vqkv_stack_s {
     std::vector<vqkv_dev::StageInfo> stages;  // host copy
     vqkv_dev::StageInfo* d_stages = nullptr;  // device copy
     float* d_eff = nullptr;                   // [sum S_i][D] fp32 effective entries
+    float* d_raw = nullptr;                   // [sum S_i][D] fp32 raw entries (trainer gradients)
     float* d_sqn = nullptr;                   // [sum S_i]
     __half* d_eff16 = nullptr;                // [sum pad_S_i][D] fp16 operand (D == 128 only)
     __half* d_eff16lo = nullptr;              // fp16(eff - fp16(eff)), same layout (LUT GEMM operand)
@@ -239,6 +240,8 @@ void launch_keycodes_from_gm(const vqkv_stack_s& ks, const uint8_t* gm, uint64_t
                              cudaStream_t s);
 void launch_lse_combine(const float* o, const float* lse, uint32_t parts, uint64_t rows, uint32_t dv, float* out,
                         float* out_lse, cudaStream_t s);
+void train_batch(const vqkv_stack_s& st, const float* batch, uint64_t rows, float beta, float gamma,
+                 bool square_commitment, float* grad_proj, double* sums_host, cudaStream_t s);
 void nccl_comm_init_all(int ndev, const int* devs, void** comms);
 void nccl_comm_destroy(void* comm);
 void lse_allgather_combine(void* comm, const float* part_o, const float* part_lse, uint64_t rows, uint32_t dv,
