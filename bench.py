@@ -41,6 +41,9 @@ LAYERS, KV_HEADS, D = 32, 8, 128
 PREFILL, INIT_LEN, LOCAL_LEN = 32768, 4, 1024
 K_SHAPE, V_SHAPE = (56, 1024), (16, 512)
 METRIC = "KV vectors/sec VQ-encoded and decode-attn tokens/sec at LLaMA3.1-8B shape"
+# L2 -> SM bandwidth measured on this pool's B200s (scripts/micro/l2_gather.cu: bulk copies of 36 KB chunks,
+# 2 CTAs per SM, L2-resident source; profiles/r2_decode.md)
+L2_PEAK_TBPS = 20.8
 UNIT = "KV vectors/s"
 
 
@@ -740,7 +743,10 @@ def run_ours(args, rank, world, local):
                          "unit": "GB/s", "frac": (code_bytes + out_bytes) / (d_ms / 1e3) / 1e9 / hbm,
                          "algorithmic": "row_bits/8 in + 4*D out per vector",
                          "l2_gather_tbps": gather / (d_ms / 1e3) / 1e12,
-                         "note": "on-chip bound: one 512 B codebook-row gather from L2 per (vector, stage)"},
+                         "l2_peak_tbps_measured": L2_PEAK_TBPS,
+                         "l2_frac": gather / (d_ms / 1e3) / 1e12 / L2_PEAK_TBPS,
+                         "note": "on-chip bound: one 512 B codebook-row gather from L2 per (vector, stage); "
+                                 "l2_frac against the measured L2->SM peak (profiles/r2_decode.md)"},
         }
         if rank == 0 and args.parity_streams > 0:  # checker (untimed): 0 ULP on stream 0's rows
             ok_, ov_ = oracle_stacks()
