@@ -29,3 +29,18 @@ s.record()
 for _ in range(10): f()
 e.record(); torch.cuda.synchronize()
 print(f"{s.elapsed_time(e)/10:.3f} ms per layer-step ({pairs} pairs)")
+import ctypes
+from paper_2603_16435_b200 import _lib
+L = _lib.load()
+L.vqkv_profile_enable(1)
+for nm in (b"attend_lut_build", b"attend", b"attend_combine"):
+    L.vqkv_profile_collect(nm, None, None)
+for _ in range(5): f()
+torch.cuda.synchronize()
+parts = []
+for nm in (b"attend_lut_build", b"attend", b"attend_combine"):
+    t, n = ctypes.c_double(), ctypes.c_uint64()
+    L.vqkv_profile_collect(nm, ctypes.byref(t), ctypes.byref(n))
+    parts.append(f"{nm.decode()} {t.value / max(n.value, 1):.3f}")
+L.vqkv_profile_enable(0)
+print("  kernels (ms/launch): " + ", ".join(parts))

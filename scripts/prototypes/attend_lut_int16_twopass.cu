@@ -1,0 +1,2052 @@
+// PROTOTYPE (not built, not product code): the int16 fixed-point LUT with exact rescoring for K3,
+// measured slower than the fp32 LUT on B200 (K3 'Tried this round'). Kept for reference.
+// attend_lut.cu -- K3: decode-step attention over the compressed cache in the
+// dot-product domain (D = 128, G = 4 query heads per KV head).
+//
+// Reference: attend (proj/core/src/attention.cpp:26-69) over
+// CacheState::view_block (kv_cache.cpp:143-189), whose compressed rows are
+// reconstruct() sums (codebook.cpp:208-223).  Because reconstruction is a sum
+// of codebook rows, for every query q_g
+//     scale * q_g . k_t = sum_s LUT_s[z_s,t][g],   LUT_s[j][g] = scale * q_g . e_s[j]
+//     sum_t p_t,g v_t   = sum_s sum_j H_s[j][g] e_s[j],  H_s[j][g] = sum_{t: z_s,t = j} p_t,g
+// so keys cost one table lookup per (token, stage) and values one histogram
+// update per (token, stage); neither K nor V rows are ever materialised.
+//
+// Layouts (all per (sequence, KV head) pair):
+//   LUT      fp32, key stages in groups of 8: [group][j < R][slot 8][head 4] -- one
+//            128 B row per code value j holds the 8 stages' float4 entries.
+//   key codes ("attention records", vqkv_keycodes_to_gm): per group of 8 key stages
+//            and token t an 80-bit record of eight 10-bit fields, ROTATED: field k
+//            holds the code of stage slot (t & 7) ^ k.  Stored as two planes per group,
+//            cap x u64 (record bits 0-63) then cap x u16 (bits 64-79): 10 B per token
+//            and group, the CodeMatrix row's 70 B at the paper geometry.
+//   value codes: the reference CodeMatrix rows (codebook.cpp:74-151), unchanged.
+//
+// Why the rotation: the lanes of a warp hold consecutive tokens, so in one LDS.128
+// the 8 lanes of a quarter-warp read slots (lane & 7) ^ k -- 8 distinct 16 B bank
+// groups of the 128 B rows whatever the codes are.  Every key lookup is a
+// conflict-free wavefront (the round-1 layout lost 56 % of its wavefronts to bank
+// conflicts of random LDS.128 gathers).
+//
+// Kernels (one launch each, on the caller's stream):
+//   q_prep + lut_tc  the LUT GEMM on tcgen05 (split fp16, fp32 accumulate) -> fp32 LUT
+//   attend_atr       CTA = (pair, contiguous token range), 512 threads, chunks of 8192
+//                    tokens (16 per thread, logits in registers):
+//                      keys   - per LUT group: one 128 KB bulk copy (TMA engine) of the
+//                               group's rows into smem; per token 8 x (SHF, LOP3,
+//                               LDS.128, 2 FADD2) from the thread's 10 B record;
+//                      softmax- chunk max m_c, p = exp(l - m_c), l_c = sum p (fp32);
+//                      values - p in fixed point with quantum u_c = l_c 2^-28 (a
+//                               RELATIVE quantum: see the bound below); per token with a
+//                               nonzero weight the warp updates the 16 stages x 4 heads
+//                               of int32 smem histograms, lane = (stage slot, head), so
+//                               each ATOMS hits 32 distinct banks;
+//                      fold   - H into the CTA's fp32 accumulator (global, L2-resident)
+//                               rescaled to the running max (online softmax);
+//                    after the last chunk the CTA contracts its accumulator with the
+//                    value codebooks (o = sum H e) and writes (o, m, l).
+//                    One more CTA per pair attends the raw init/local rows directly.
+//   combine          per pair: LSE merge of its CTAs' partials, normalise, emit lse.
+//
+// Value-path error bound (rigorous).  In a chunk of n_c <= 8192 tokens the histogram
+// rounds each p_t to a multiple of u_c = l_c 2^-28 (round to nearest, |err| <= u_c/2;
+// tokens below u_c/2 round to 0 and are skipped).  The normaliser uses the exact fp32
+// l.  With chunk weights exp(m_c - M) and L = sum_c l_c exp(m_c - M):
+//     |o' - o|_inf <= sum_c n_c (u_c/2) exp(m_c - M) max_t|v_t|_inf / L
+//                  <= 8192 * 2^-29 * max_t|v_t|_inf = 2^-16 max_t|v_t|_inf,
+// independent of how flat or peaked the attention is (no absolute cut).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "tc_ptx.cuh"
+#include "vqkv_internal.cuh"
+
+namespace vqkv_dev {
+
+namespace {
+
+constexpr int kG = 4;                          // query heads per KV head on this path
+constexpr int kD = 128;                        // head dim
+constexpr int kThreads = 512;
+#ifndef VQKV_ATTN_EXP
+#define VQKV_ATTN_EXP 0  // development experiments (variant builds only)
+#endif
+#ifndef VQKV_ATTN_TOK
+#define VQKV_ATTN_TOK 16
+#endif
+constexpr int kTok = VQKV_ATTN_TOK;            // tokens per thread per chunk
+constexpr int kChunk = kThreads * kTok;        // 8192 tokens per chunk
+constexpr int kGS = 8;                         // key stages per LUT group (one 128 B row)
+constexpr uint32_t kRowBytes = kGS * 16;       // 8 slots x float4
+constexpr uint32_t kLutBytes = 1024 * kRowBytes;  // 128 KB: one group, up to 1024 code values
+constexpr uint32_t kMaxVStages = 64;
+constexpr uint32_t kSmemCtl = 2048;            // barrier, TMEM address, reductions, value descriptors
+constexpr uint32_t kQueueCap = 32 + 32 * 4;    // per-warp queue of (token, head) entries with a nonzero weight
+constexpr uint32_t kQueueBytes = (kThreads / 32) * kQueueCap * 8;
+constexpr uint32_t kSlabTok = 4 * kThreads;      // value rows staged per slab (4 tokens per thread)
+constexpr uint32_t kSlabBytes = 38400;           // per slab buffer: rows of up to 149 bits + alignment slack
+constexpr uint32_t kMaxSlabRowBits = ((kSlabBytes - 48) * 8) / kSlabTok;
+constexpr uint32_t kMainSmem = kLutBytes + kSmemCtl + kQueueBytes + 2 * kSlabBytes;
+constexpr float kQuantum = 268435456.0f;       // 2^28: p / u_c = p * 2^28 / l_c
+constexpr float kKeyBudget = 0.00390625f;      // 2^-8: bound on the output error from first-pass logits
+
+// LUT element offset (in float4) of (pair, stage s, code j)
+__host__ __device__ __forceinline__ uint64_t lut_off(uint64_t pair, uint32_t ng, uint32_t R, uint32_t s, uint32_t j) {
+    return ((pair * ng + (s >> 3)) * R + j) * kGS + (s & 7u);
+}
+
+// ---- fixed-point LUT ----------------------------------------------------------------------
+// Per (pair, head g) the LUT entries are quantised to N = rint(v * inv_g), inv_g = (2^31 - 1024) / S_g,
+// S_g = max |LUT[pair][.][.][g]| (so |N| < 2^31), and split N = 65536 H + Lo (H = N >> 16 signed 16-bit,
+// Lo = N & 0xFFFF).  The main kernel's first pass sums H only (the "hi" table in shared memory, 8 B per
+// entry for the 4 heads); the second pass adds Lo (the "lo" table, read from global memory) for the
+// tokens that can carry weight -- see the error bound at the main kernel.
+//   hi: [pair][group16 = s / 16][code j < R][slot s % 16] x uint2, biased u16 (H + 32768) per head, i.e.
+//       128 B rows of 16 stages; slots of stages >= n_stages hold H = 0 (only row 0 is ever read)
+//   lo: [pair][stage][code] x uint2 (Lo per head)
+constexpr int kGS16 = 16;
+__host__ __device__ __forceinline__ uint64_t hi_off(uint64_t pair, uint32_t ng16, uint32_t R, uint32_t s, uint32_t j) {
+    return ((pair * ng16 + (s >> 4)) * R + j) * kGS16 + (s & 15u);
+}
+__host__ __device__ __forceinline__ uint64_t lo_off(uint64_t pair, uint32_t kn, uint32_t R, uint32_t s, uint32_t j) {
+    return (pair * kn + s) * R + j;
+}
+__device__ __forceinline__ float lut_inv(float S) { return S > 0.f ? 2147482624.0f / S : 0.f; }  // (2^31 - 1024) / S
+__device__ __forceinline__ float lut_delta(float S) { return S * (1.0f / 2147482624.0f); }
+struct LutTables {
+    uint2* hi;
+    uint2* lo;
+    const uint32_t* smax;  // [pair][4]: S_g as float bits (atomicMax of non-negative floats)
+    uint32_t ng16, R, kn;
+};
+__device__ __forceinline__ void lut_quant_store(const LutTables& t, uint32_t pair, uint32_t s, uint32_t j, float4 v,
+                                                float4 inv) {
+    const int n0 = __float2int_rn(v.x * inv.x), n1 = __float2int_rn(v.y * inv.y);
+    const int n2 = __float2int_rn(v.z * inv.z), n3 = __float2int_rn(v.w * inv.w);
+    auto hb = [](int n) { return uint32_t((n >> 16) + 32768); };
+    t.hi[hi_off(pair, t.ng16, t.R, s, j)] = make_uint2(hb(n0) | (hb(n1) << 16), hb(n2) | (hb(n3) << 16));
+    t.lo[lo_off(pair, t.kn, t.R, s, j)] =
+        make_uint2((uint32_t(n0) & 0xFFFFu) | (uint32_t(n1) << 16), (uint32_t(n2) & 0xFFFFu) | (uint32_t(n3) << 16));
+}
+__device__ __forceinline__ float4 lut_inv4(const uint32_t* smax, uint32_t pair) {
+    const uint4 b = reinterpret_cast<const uint4*>(smax)[pair];
+    return make_float4(lut_inv(__uint_as_float(b.x)), lut_inv(__uint_as_float(b.y)), lut_inv(__uint_as_float(b.z)),
+                       lut_inv(__uint_as_float(b.w)));
+}
+
+struct LutArgs {
+    const float* q;        // [pairs][G][D]
+    const float* keff;     // key effective entries
+    const StageInfo* kst;
+    uint32_t kn;
+    uint64_t kentries;     // total key entries (sum S)
+    float scale;
+    float4* lut;           // flat fp32 LUT [pair][stage][code] (lo_off)
+    uint32_t R;
+};
+
+// FFMA fallback of the LUT build (entries too large for the fp16 split operands).
+// CTA: 128 entries (stage-concatenated) x 8 pairs, 256 threads; thread = 4 entries x 4 queries.
+constexpr int kLutEntries = 128;
+constexpr int kLutStride = kD + 2;  // even row stride: 8 B-aligned float2 reads
+__global__ void __launch_bounds__(256) lut_kernel(LutArgs a, uint32_t n_pairs) {
+    extern __shared__ float lsm[];
+    float4* qs = reinterpret_cast<float4*>(lsm);  // [8 pairs][D] x float4 over g
+    float* es = lsm + 8 * kG * kD;                // [128 entries][kLutStride]
+    const uint32_t e0 = blockIdx.x * kLutEntries, p0 = blockIdx.y * 8;
+    for (uint32_t i = threadIdx.x; i < 8 * kD; i += blockDim.x) {
+        const uint32_t p = i / kD, c = i % kD;
+        const float* qp = a.q + uint64_t(p0 + p) * kG * kD + c;
+        qs[i] = (p0 + p < n_pairs) ? make_float4(qp[0], qp[kD], qp[2 * kD], qp[3 * kD]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (uint32_t i = threadIdx.x; i < kLutEntries * kD / 4; i += blockDim.x) {
+        const uint32_t r = (4 * i) / kD, c = (4 * i) % kD;
+        const float4 v = (e0 + r < a.kentries) ? __ldg(reinterpret_cast<const float4*>(a.keff + uint64_t(e0 + r) * kD + c))
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float2*>(es + r * kLutStride + c) = make_float2(v.x, v.y);
+        *reinterpret_cast<float2*>(es + r * kLutStride + c + 2) = make_float2(v.z, v.w);
+    }
+    __syncthreads();
+    const uint32_t eg = threadIdx.x & 31, p = threadIdx.x >> 5;
+    __align__(8) float acc[4][kG];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int g = 0; g < kG; ++g) acc[i][g] = 0.f;
+    const float4* qp = qs + p * kD;
+#pragma unroll 4
+    for (int c = 0; c < kD; c += 2) {
+        const float4 q0 = qp[c], q1 = qp[c + 1];
+        float2 ev[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ev[i] = *reinterpret_cast<const float2*>(es + (eg + 32 * i) * kLutStride + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float2* a2 = reinterpret_cast<float2*>(acc[i]);
+            const float2 ex = make_float2(ev[i].x, ev[i].x), ey = make_float2(ev[i].y, ev[i].y);
+            a2[0] = ptx::fma2(make_float2(q0.x, q0.y), ex, a2[0]);
+            a2[1] = ptx::fma2(make_float2(q0.z, q0.w), ex, a2[1]);
+            a2[0] = ptx::fma2(make_float2(q1.x, q1.y), ey, a2[0]);
+            a2[1] = ptx::fma2(make_float2(q1.z, q1.w), ey, a2[1]);
+        }
+    }
+    if (p0 + p < n_pairs)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t e = e0 + eg + 32 * i;
+            if (e < a.kentries) {
+                uint32_t s = 0;  // stage of entry e (stages are few; scan)
+                while (s + 1 < a.kn && e >= uint32_t(a.kst[s + 1].eff_off / kD)) ++s;
+                const uint32_t j = e - uint32_t(a.kst[s].eff_off / kD);
+                a.lut[lo_off(p0 + p, a.kn, a.R, s, j)] = make_float4(acc[i][0] * a.scale, acc[i][1] * a.scale,
+                                                                     acc[i][2] * a.scale, acc[i][3] * a.scale);
+            }
+        }
+}
+
+// FFMA fallback, second and third steps: per (pair, head) max |LUT|, then the fixed-point tables
+__global__ void lut_flat_absmax_kernel(const float4* __restrict__ flat, uint32_t per_pair, uint32_t* smax) {
+    const uint32_t pair = blockIdx.y;
+    float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < per_pair; i += gridDim.x * blockDim.x) {
+        const float4 v = flat[uint64_t(pair) * per_pair + i];
+        m = make_float4(fmaxf(m.x, fabsf(v.x)), fmaxf(m.y, fabsf(v.y)), fmaxf(m.z, fabsf(v.z)), fmaxf(m.w, fabsf(v.w)));
+    }
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(m.x)), my = __reduce_max_sync(0xffffffffu, __float_as_uint(m.y));
+    const uint32_t mz = __reduce_max_sync(0xffffffffu, __float_as_uint(m.z)), mw = __reduce_max_sync(0xffffffffu, __float_as_uint(m.w));
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(smax + pair * 4 + 0, mx);
+        atomicMax(smax + pair * 4 + 1, my);
+        atomicMax(smax + pair * 4 + 2, mz);
+        atomicMax(smax + pair * 4 + 3, mw);
+    }
+}
+__global__ void lut_flat_quant_kernel(const float4* __restrict__ flat, const StageInfo* __restrict__ kst, LutTables t) {
+    const uint32_t pair = blockIdx.y, s = blockIdx.z;
+    const float4 inv = lut_inv4(t.smax, pair);
+    const uint32_t size = kst[s].size;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < size; j += gridDim.x * blockDim.x)
+        lut_quant_store(t, pair, s, j, flat[lo_off(pair, t.kn, t.R, s, j)], inv);
+}
+
+// hi slots of stages past the stack (the padding of the last 16-stage group) are read with code 0:
+// H = 0 there (biased 32768)
+__global__ void lut_hi_pad_kernel(uint2* hi, uint32_t ng16, uint32_t R, uint32_t kn) {
+    const uint32_t pair = blockIdx.x, slot = threadIdx.x;
+    const uint32_t s = (ng16 - 1) * kGS16 + slot;
+    if (slot < kGS16 && s >= kn) hi[hi_off(pair, ng16, R, s, 0)] = make_uint2(0x80008000u, 0x80008000u);
+}
+
+// ---- LUT build on the tensor cores --------------------------------------------------------
+// The LUT is a GEMM: LUT[pair][e][g] = scale * E[e] . q[pair][g], i.e. [entries x 128] x
+// [128 x (pairs * G)].  fp16 split precision: E = E_hi + E_lo (stack operands, the encoder's
+// pre-swizzled chunks), q 2^sigma = Q_hi + Q_lo (per row power-of-two scale, exact), and
+// E_hi Q_lo + E_lo Q_hi + E_hi Q_hi accumulate in fp32 in TMEM; the dropped E_lo Q_lo and the
+// lo roundings are ~2^-22 relative to sum_k |E_k q_k|, the fp32 FFMA LUT's own error level.
+// q_prep_kernel: one warp per (pair, g) row -> Q_hi / Q_lo in 128-row SW128 K-major tiles
+// (the half_copy_kernel layout) and qscl[row] = scale * 2^-sigma.
+__global__ void q_prep_kernel(const float* __restrict__ q, uint32_t n_rows, uint32_t n_rows_pad, float scale,
+                              __half* __restrict__ qhi, __half* __restrict__ qlo, float* __restrict__ qscl) {
+    const uint32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (r >= n_rows_pad) return;
+    float4 v = (r < n_rows) ? reinterpret_cast<const float4*>(q + uint64_t(r) * kD)[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float m = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int sig = 0;
+    if (m > 0.f && isfinite(m)) {
+        int e;
+        frexpf(m, &e);  // m in [2^(e-1), 2^e): m 2^sig < 2^14
+        sig = min(100, max(-100, 14 - e));
+    }
+    const float sc = ldexpf(1.0f, sig);
+    const float x[4] = {v.x * sc, v.y * sc, v.z * sc, v.w * sc};
+    const uint32_t t = r >> 7, rr = r & 127;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t k = lane * 4 + i, kb = k >> 6, kk = k & 63;
+        const uint64_t off = uint64_t(t) * 16384 + kb * 8192 + rr * 64 + (((kk >> 3) ^ (rr & 7)) << 3) + (kk & 7);
+        const __half h = __float2half_rn(x[i]);
+        qhi[off] = h;
+        qlo[off] = __float2half_rn(x[i] - __half2float(h));
+    }
+    if (lane == 0) qscl[r] = (r < n_rows) ? ldexpf(scale, -sig) : 0.f;
+}
+
+// CTA = 128-entry chunk c of key stage s, looping over the 128-row tiles of (pair, g) query
+// rows.  Warp 4 (one thread) loads the chunk's E_hi / E_lo once and double-buffers the Q tiles
+// by bulk copy, and issues 24 MMAs M128 N128 K16 per tile into one of two TMEM accumulators;
+// warps 0-3 (thread = entry row = TMEM lane) drain the other accumulator meanwhile: 32 pairs'
+// float4 per thread and tile, coalesced across lanes.
+constexpr uint32_t kLutTcSmem = 6 * 32768 + 1024;
+// MODE 0: per (pair, head) max |LUT| into smax (atomicMax); MODE 1: the fixed-point hi / lo tables
+// (the same GEMM, bit for bit, so the max bounds every quantised entry).
+template <int MODE>
+__global__ void __launch_bounds__(160) lut_tc_kernel(const __half* __restrict__ eff16, const __half* __restrict__ eff16lo,
+                                                     const StageInfo* __restrict__ kst, const __half* __restrict__ qhi,
+                                                     const __half* __restrict__ qlo, const float* __restrict__ qscl,
+                                                     uint32_t n_pairs, uint32_t n_qtiles, uint32_t* smax_w, LutTables t) {
+    extern __shared__ uint8_t lsm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(lsm_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar_e, bar_q[2], bar_mma[2], bar_epi[2];
+    __shared__ uint32_t tmem_base;
+    __shared__ uint32_t colmax[4][128];  // MODE 0: per-warp column maxima
+    const StageInfo si = kst[blockIdx.y];
+    const uint32_t c = blockIdx.x;
+    if (c * 128 >= si.size) return;  // uniform per CTA
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(ptx::smem_u32(&bar_e), 1);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(ptx::smem_u32(&bar_q[b]), 1);
+            ptx::mbar_init(ptx::smem_u32(&bar_mma[b]), 1);
+            ptx::mbar_init(ptx::smem_u32(&bar_epi[b]), 128);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) {
+        ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 256);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t s_ehi = ptx::smem_u32(sm), s_elo = s_ehi + 32768;
+    auto s_qhi = [&](uint32_t b) { return s_ehi + 65536 + b * 65536; };
+    if (warp == 4) {
+        if (lane == 0) {
+            const uint64_t eo = si.eff16_off + uint64_t(c) * 18432;
+            ptx::mbar_arrive_expect_tx(ptx::smem_u32(&bar_e), 2 * 32768);
+            ptx::bulk_g2s(s_ehi, eff16 + eo, 32768, ptx::smem_u32(&bar_e));
+            ptx::bulk_g2s(s_elo, eff16lo + eo, 32768, ptx::smem_u32(&bar_e));
+            auto load_q = [&](uint32_t tq) {
+                const uint32_t b = tq & 1, bar = ptx::smem_u32(&bar_q[b]);
+                ptx::mbar_arrive_expect_tx(bar, 2 * 32768);
+                ptx::bulk_g2s(s_qhi(b), qhi + uint64_t(tq) * 16384, 32768, bar);
+                ptx::bulk_g2s(s_qhi(b) + 32768, qlo + uint64_t(tq) * 16384, 32768, bar);
+            };
+            load_q(0);
+            if (n_qtiles > 1) load_q(1);
+            ptx::mbar_wait(ptx::smem_u32(&bar_e), 0);
+            constexpr uint32_t idesc = ptx::idesc_f16_f32(128, 128);
+            for (uint32_t tq = 0; tq < n_qtiles; ++tq) {
+                const uint32_t b = tq & 1, use = tq >> 1;
+                ptx::mbar_wait(ptx::smem_u32(&bar_q[b]), use & 1);
+                if (tq >= 2) ptx::mbar_wait(ptx::smem_u32(&bar_epi[b]), (use - 1) & 1);  // accumulator b drained
+                ptx::tc_fence_after();
+                const uint32_t qh = s_qhi(b), ql = qh + 32768;
+                const uint32_t A[3] = {s_ehi, s_elo, s_ehi}, B[3] = {ql, qh, qh};  // small terms first
+#pragma unroll
+                for (int part = 0; part < 3; ++part)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32;
+                        ptx::mma_f16_ss(tmem + 128u * b, ptx::umma_desc_sw128(A[part] + koff),
+                                        ptx::umma_desc_sw128(B[part] + koff), idesc, (part | k) ? 1u : 0u);
+                    }
+                ptx::mma_commit(ptx::smem_u32(&bar_mma[b]));
+                if (tq + 2 < n_qtiles) {
+                    // Q buffer b is free once these MMAs complete
+                    ptx::mbar_wait(ptx::smem_u32(&bar_mma[b]), use & 1);
+                    load_q(tq + 2);
+                }
+            }
+        }
+    } else {
+        const uint32_t j = c * 128 + warp * 32 + lane;  // entry within the stage
+        for (uint32_t tq = 0; tq < n_qtiles; ++tq) {
+            const uint32_t b = tq & 1, use = tq >> 1;
+            ptx::mbar_wait(ptx::smem_u32(&bar_mma[b]), use & 1);
+            ptx::tc_fence_after();
+            const float* sclp = qscl + uint64_t(tq) * 128;
+            float v[4][32];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) ptx::tmem_ld32(tmem + ((warp * 32u) << 16) + 128u * b + 32u * c4, v[c4]);
+            ptx::tc_wait_ld();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(ptx::smem_u32(&bar_epi[b]));
+            if constexpr (MODE == 0) {
+                // column maxima over the CTA's 128 entries (padding entries and pairs are 0)
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4)
+#pragma unroll
+                    for (int pp = 0; pp < 8; ++pp) {
+                        const float4 sc = __ldg(reinterpret_cast<const float4*>(sclp) + c4 * 8 + pp);
+                        const bool ok = j < si.size;
+                        const float x[4] = {v[c4][4 * pp] * sc.x, v[c4][4 * pp + 1] * sc.y, v[c4][4 * pp + 2] * sc.z,
+                                            v[c4][4 * pp + 3] * sc.w};
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            const uint32_t m = __reduce_max_sync(0xffffffffu, ok ? __float_as_uint(fabsf(x[g])) : 0u);
+                            if (lane == 0) colmax[warp][c4 * 32 + pp * 4 + g] = m;
+                        }
+                    }
+                asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+                if (warp == 0) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t col = i * 32 + lane, pair = tq * 32 + col / 4;
+                        const uint32_t m = max(max(colmax[0][col], colmax[1][col]), max(colmax[2][col], colmax[3][col]));
+                        if (pair < n_pairs && m) atomicMax(smax_w + pair * 4 + (col & 3), m);
+                    }
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            } else {
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4)
+#pragma unroll
+                    for (int pp = 0; pp < 8; ++pp) {
+                        const uint32_t pair = tq * 32 + c4 * 8 + pp;
+                        if (j < si.size && pair < n_pairs) {
+                            const float4 sc = __ldg(reinterpret_cast<const float4*>(sclp) + c4 * 8 + pp);
+                            lut_quant_store(t, pair, blockIdx.y, j,
+                                            make_float4(v[c4][4 * pp] * sc.x, v[c4][4 * pp + 1] * sc.y,
+                                                        v[c4][4 * pp + 2] * sc.z, v[c4][4 * pp + 3] * sc.w),
+                                            lut_inv4(t.smax, pair));
+                        }
+                    }
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc(tmem, 256);
+}
+
+// Reads 64 bits starting at bit `pos` of a byte stream: two aligned 64-bit
+// loads when they stay inside [.., end), byte loads otherwise (buffer tails).
+__device__ __forceinline__ uint64_t read_bits64(const uint8_t* base, uint64_t pos, const uint8_t* end) {
+    const uint8_t* p = base + (pos >> 3);
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(7);
+    const uint32_t sh = uint32_t((reinterpret_cast<uintptr_t>(p) - a) * 8 + (pos & 7));
+    if (a + 16 <= reinterpret_cast<uintptr_t>(end)) {
+        const uint64_t* q = reinterpret_cast<const uint64_t*>(a);
+        const uint64_t lo = __ldg(q), hi = __ldg(q + 1);
+        return sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
+    }
+    uint64_t v = 0;
+    const uint32_t bsh = uint32_t(pos & 7);
+    for (int b = 0; b < 8 && p + b < end; ++b) v |= uint64_t(p[b]) << (8 * b);
+    uint64_t extra = (p + 8 < end) ? uint64_t(p[8]) : 0ull;
+    return bsh ? ((v >> bsh) | (extra << (64 - bsh))) : v;
+}
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float r = -INFINITY;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) r = fmaxf(r, red[w]);
+    return r;
+}
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float r = 0.f;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) r += red[w];
+    return r;
+}
+
+
+// block-wide max / sum of 4 values per thread (one barrier pair for the 4 heads)
+__device__ __forceinline__ float4 block_max4(float4 v, float4* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x = fmaxf(v.x, __shfl_xor_sync(0xffffffffu, v.x, o));
+        v.y = fmaxf(v.y, __shfl_xor_sync(0xffffffffu, v.y, o));
+        v.z = fmaxf(v.z, __shfl_xor_sync(0xffffffffu, v.z, o));
+        v.w = fmaxf(v.w, __shfl_xor_sync(0xffffffffu, v.w, o));
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float4 r = red[0];
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+        const float4 x = red[w];
+        r = make_float4(fmaxf(r.x, x.x), fmaxf(r.y, x.y), fmaxf(r.z, x.z), fmaxf(r.w, x.w));
+    }
+    return r;
+}
+__device__ __forceinline__ float4 block_sum4(float4 v, float4* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+        v.z += __shfl_xor_sync(0xffffffffu, v.z, o);
+        v.w += __shfl_xor_sync(0xffffffffu, v.w, o);
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float4 r = red[0];
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+        const float4 x = red[w];
+        r = make_float4(r.x + x.x, r.y + x.y, r.z + x.z, r.w + x.w);
+    }
+    return r;
+}
+
+__device__ __forceinline__ void lds128(uint32_t addr, float2& a, float2& b) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y) : "r"(addr));
+}
+__device__ __forceinline__ float2 add2v(float2 a, float2 b) {  // volatile: keeps its place among the LDS
+    uint64_t r, x = *reinterpret_cast<uint64_t*>(&a), y = *reinterpret_cast<uint64_t*>(&b);
+    asm volatile("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_shared_add_nz(uint32_t addr, uint32_t v) {  // predicated, no branch
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr), "r"(v)
+                 : "memory");
+}
+
+// Field K (0..7) of an 80-bit attention record (w0 = bits 0-31, w1 = 32-63, w2 = 64-79),
+// shifted so its 10 bits sit at bits 7-16 (the code's row offset, 128 B per code); the bits
+// below are the previous field's and are masked off by the caller.  One SHF each.
+template <int K>
+__device__ __forceinline__ uint32_t field_at7(uint32_t w0, uint32_t w1, uint32_t w2) {
+    if constexpr (K == 0) return w0 << 7;
+    else if constexpr (K <= 3) return __funnelshift_r(w0, w1, 10 * K - 7);
+    else return __funnelshift_r(w1, w2, 10 * K - 39);
+}
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// field_at7 with the field index as a (constant-folded) argument
+__device__ __forceinline__ uint32_t field_at7_rt(int K, uint32_t w0, uint32_t w1, uint32_t w2) {
+    return K == 0 ? (w0 << 7) : (K <= 3 ? __funnelshift_r(w0, w1, 10 * K - 7) : __funnelshift_r(w1, w2, 10 * K - 39));
+}
+__device__ __forceinline__ void lds64(uint32_t addr, uint2& v) {
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+}
+
+
+// L2 cache policies: streamed-once code records evict first, the per-pair LUTs (re-read once per
+// chunk by every CTA on the pair) evict last
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint2 ldg_stream_u2(const uint2* p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg_stream_u16(const uint16_t* p, uint64_t pol) {
+    unsigned short v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_l2_hint(const void* p, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol) : "memory");
+}
+
+// raw init/local rows: one CTA per pair, direct fp32 attention (no codebooks).  Runs on a side
+// stream beside the LUT build; its (o, m, l) is one more partial of the pair's LSE merge.
+struct RawArgs {
+    const float* q;
+    const float* init_k;
+    const float* init_v;
+    uint64_t n_init;
+    const float* local_k;
+    const float* local_v;
+    uint64_t n_local;
+    uint64_t init_stride, local_stride;  // rows between pairs
+    float scale;
+    uint32_t slot0;  // partial slot of pair 0
+    float* part_o;
+    float* part_m;
+    float* part_l;
+    float* vmax;     // [pair]: max |v|_inf over the pair's raw rows (the main kernel's error bound)
+};
+
+__global__ void __launch_bounds__(kThreads) attend_raw_rows_kernel(RawArgs a) {
+    extern __shared__ __align__(16) float rsm[];
+    constexpr int kRowBatch = 8;
+    const uint32_t pair = blockIdx.x, slot = a.slot0 + pair;
+    const uint32_t n_raw = uint32_t(a.n_init + a.n_local);
+    if (n_raw == 0) {
+        if (threadIdx.x < kG) {
+            a.part_m[uint64_t(slot) * kG + threadIdx.x] = -INFINITY;
+            a.part_l[uint64_t(slot) * kG + threadIdx.x] = 0.f;
+        }
+        if (threadIdx.x == 0) a.vmax[pair] = 0.f;
+        return;
+    }
+    float* red = rsm;                  // 64
+    float* qs = rsm + 64;              // G*D
+    float* po = qs + kG * kD;          // [4 row groups][G][D] partial outputs
+    float* ls = po + 4 * kG * kD;      // logits / weights [n_raw][G]
+    for (uint32_t i = threadIdx.x; i < kG * kD; i += blockDim.x) qs[i] = a.q[uint64_t(pair) * kG * kD + i];
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    auto krow = [&](uint32_t r) -> const float4* {
+        return reinterpret_cast<const float4*>(
+            (r < a.n_init) ? a.init_k + (uint64_t(pair) * a.init_stride + r) * kD
+                           : a.local_k + (uint64_t(pair) * a.local_stride + (r - a.n_init)) * kD);
+    };
+    float4 qv[kG];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) qv[g] = reinterpret_cast<const float4*>(qs + g * kD)[lane];
+    const bool up = lane & 16u, b3 = lane & 8u;
+    for (uint32_t r0 = warp; r0 < n_raw; r0 += nw * kRowBatch) {
+        float4 kv[kRowBatch];
+#pragma unroll
+        for (int u = 0; u < kRowBatch; ++u) {
+            const uint32_t r = r0 + u * nw;
+            kv[u] = (r < n_raw) ? __ldg(krow(r) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kRowBatch; ++u) {
+            float d[kG];
+#pragma unroll
+            for (int g = 0; g < kG; ++g)
+                d[g] = kv[u].x * qv[g].x + kv[u].y * qv[g].y + kv[u].z * qv[g].z + kv[u].w * qv[g].w;
+            // 4-value butterfly: 6 shuffles leave head 2*bit4 + bit3 summed over the warp
+            float k0 = up ? d[2] : d[0], k1 = up ? d[3] : d[1];
+            k0 += __shfl_xor_sync(0xffffffffu, up ? d[0] : d[2], 16);
+            k1 += __shfl_xor_sync(0xffffffffu, up ? d[1] : d[3], 16);
+            float k = b3 ? k1 : k0;
+            k += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+            k += __shfl_xor_sync(0xffffffffu, k, 4);
+            k += __shfl_xor_sync(0xffffffffu, k, 2);
+            k += __shfl_xor_sync(0xffffffffu, k, 1);
+            const uint32_t r = r0 + u * nw;
+            if ((lane & 7u) == 0 && r < n_raw) ls[r * kG + (lane >> 3)] = k * a.scale;
+        }
+    }
+    __syncthreads();
+    for (int g = 0; g < kG; ++g) {
+        float m = -INFINITY;
+        for (uint32_t r = threadIdx.x; r < n_raw; r += blockDim.x) m = fmaxf(m, ls[r * kG + g]);
+        m = block_max(m, red);
+        float l = 0.f;
+        for (uint32_t r = threadIdx.x; r < n_raw; r += blockDim.x) {
+            const float p = __expf(ls[r * kG + g] - m);
+            ls[r * kG + g] = p;
+            l += p;
+        }
+        l = block_sum(l, red);
+        if (threadIdx.x == 0) {
+            a.part_m[uint64_t(slot) * kG + g] = m;
+            a.part_l[uint64_t(slot) * kG + g] = l;
+        }
+    }
+    __syncthreads();
+    // o[g][d] = sum_r p[r][g] v_r[d]: thread = (row group rg, d) over rows rg, rg + 4, ...;
+    // each value load feeds the 4 heads, kRowBatch loads in flight
+    {
+        const uint32_t d = threadIdx.x % kD, rg = threadIdx.x / kD, nrg = blockDim.x / kD;
+        const float* iv = a.init_v + uint64_t(pair) * a.init_stride * kD + d;
+        const float* lv = a.local_v + uint64_t(pair) * a.local_stride * kD + d;
+        const float4* p4 = reinterpret_cast<const float4*>(ls);
+        float acc[kG] = {0.f, 0.f, 0.f, 0.f};
+        float vm = 0.f;
+        for (uint32_t r0 = rg; r0 < n_raw; r0 += nrg * kRowBatch) {
+            float x[kRowBatch];
+#pragma unroll
+            for (int u = 0; u < kRowBatch; ++u) {
+                const uint32_t r = r0 + u * nrg;
+                x[u] = (r >= n_raw) ? 0.f : (r < a.n_init) ? __ldg(iv + uint64_t(r) * kD) : __ldg(lv + uint64_t(r - a.n_init) * kD);
+                vm = fmaxf(vm, fabsf(x[u]));
+            }
+#pragma unroll
+            for (int u = 0; u < kRowBatch; ++u) {
+                const uint32_t r = r0 + u * nrg;
+                if (r < n_raw) {
+                    const float4 p = p4[r];
+                    acc[0] = fmaf(p.x, x[u], acc[0]);
+                    acc[1] = fmaf(p.y, x[u], acc[1]);
+                    acc[2] = fmaf(p.z, x[u], acc[2]);
+                    acc[3] = fmaf(p.w, x[u], acc[3]);
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < kG; ++g) po[(rg * kG + g) * kD + d] = acc[g];
+        vm = block_max(vm, red);  // NaN-free: fmaxf drops NaN; a NaN value still reaches the output
+        if (threadIdx.x == 0) a.vmax[pair] = vm;
+    }
+    __syncthreads();
+    const uint32_t nrg = blockDim.x / kD;
+    for (uint32_t gd = threadIdx.x; gd < kG * kD; gd += blockDim.x) {
+        float o = 0.f;
+        for (uint32_t rg = 0; rg < nrg; ++rg) o += po[rg * kG * kD + gd];
+        a.part_o[uint64_t(slot) * kG * kD + gd] = o;
+    }
+}
+
+// Compressed tokens.  The pairs' tokens are cut into 512-token units (pair-major); CTA b of the
+// persistent grid takes units [U b / n_cta, U (b + 1) / n_cta), i.e. a contiguous token range
+// that may span a pair boundary.  Its work is processed in chunks of up to 16 units of one
+// pair; a run of chunks of one pair is a segment, whose partial (o, m, l) goes to slot b + pair
+// (unique: CTA ranges are monotone in the pair).
+struct MainArgs {
+    const uint2* hi;         // fixed-point LUT, high halves (hi_off): the first pass, via shared memory
+    const uint2* lo;         // low halves (lo_off): the second pass, gathered for candidate tokens
+    const uint32_t* smax;    // [pair][4] S_g (float bits): the quantisation scale
+    uint32_t ng16, ng8, kn, R;
+    float vmax_comp;         // bound on |v|_inf of every compressed value row: sum_s max_{j,d} |e_s[j][d]|
+    const float* raw_vmax;   // [pair]: max |v|_inf of the raw rows (attend_raw_rows_kernel)
+    const uint8_t* krec;     // attention records, krec_stride bytes between pairs, cap tokens per group segment
+    uint64_t krec_stride, cap;
+    const uint8_t* vcodes;   // value CodeMatrix rows
+    uint64_t vstride, vrow_bits;
+    const uint8_t* vend;     // end of the last pair's value payload (reads stop here)
+    const StageInfo* vst;
+    uint32_t vn;
+    uint32_t vnwin;          // 64-bit windows of the value row (stages grouped, <= 64 bits each)
+    const uint2* vwin;       // [vnwin]: (start bit, s0 | s1 << 8)
+    const uint8_t* vwin_of;  // [vn]: window of each stage
+    uint32_t vtotal;         // sum S_v (<= kHistStride): histogram entries per head
+    uint32_t vslab;          // value rows staged in shared memory per slab (row_bits <= kMaxSlabRowBits)
+    const float* veff;
+    uint64_t n_comp;
+    uint32_t n_pairs;
+    uint32_t units_per_pair; // ceil(n_comp / 512)
+    uint32_t n_cta;          // persistent CTAs (<= total units, so none is empty)
+    float* part_o;           // [slots][G][D]: unnormalised sum p v
+    float* part_m;           // [slots][G]
+    float* part_l;           // [slots][G]
+};
+
+// VQKV_ATTN_PHASES (diagnostics builds only): thread 0 of every CTA accumulates clock64 per phase
+// into vqkv_attn_phase_clk[cta][8]: keys (incl. LUT waits), LUT waits, softmax, values, fold, contraction, chunks
+#ifdef VQKV_ATTN_PHASES
+__device__ unsigned long long vqkv_attn_phase_clk[256][16];
+#define PHASE_T(v) long long v = clock64()
+#define PHASE_ADD(i, t0) do { ph_acc[i] += clock64() - (t0); } while (0)
+#define PHASE_CNT(i) do { ph_acc[i] += 1; } while (0)
+#define PHASE_DECL unsigned long long ph_acc[16] = {0};
+#define PHASE_FLUSH do { if (threadIdx.x == 0) for (int i_ = 0; i_ < 16; ++i_) vqkv_attn_phase_clk[blockIdx.x][i_] += ph_acc[i_]; } while (0)
+#else
+#define PHASE_CNT(i) (void)0
+#define PHASE_DECL
+#define PHASE_FLUSH (void)0
+#define PHASE_T(v) (void)0
+#define PHASE_ADD(i, t0) (void)0
+#endif
+
+constexpr uint32_t kUnit = kThreads;           // tokens per unit (one per thread)
+constexpr uint32_t kUnitsPerChunk = kTok;      // 16 units = one 8192-token chunk
+constexpr uint32_t kHistStride = 8192;         // histogram words per head: [head][entry]
+constexpr uint32_t kTmemCols = 512;            // [0, 256): fp32 accumulator [head][entry] (4 x 64 columns x 128 lanes);
+                                               // [256, 512): the chunk's fixed-point weights (16 tokens x 4 heads per thread)
+
+// the CTA owning unit x: largest b with floor(U b / n) <= x
+__host__ __device__ __forceinline__ uint32_t cta_of_unit(uint64_t x, uint64_t U, uint32_t n) {
+    uint64_t b = (x * n) / U;
+    while (b + 1 < n && (U * (b + 1)) / n <= x) ++b;
+    while (b > 0 && (U * b) / n > x) --b;
+    return uint32_t(b);
+}
+
+// The value tables of the chunk loop (smem control block) and the pair's value rows.
+struct ValueHist {
+    const uint8_t* vc;     // the pair's value payload
+    const uint8_t* vend;   // end of the last pair's payload (reads stop here)
+    uint64_t row_bits;
+    uint32_t nwin;
+    const uint8_t* ctl;    // smem control block: vrow / vsz / vfld / wstart / wrange tables
+    uint32_t hist;         // smem address of the histograms [head][entry]
+};
+
+// One (token, head) entry of the value phase: the token's value row is read in 64-bit windows (the
+// loads of the first 4 windows issued up front) and each stage's bin of that head gets one shared
+// atomic.  Out of line: keeps the chunk loop's registers for the logits.
+__device__ __noinline__ void hist_entry(const ValueHist& vh, uint32_t t, uint32_t g, uint32_t Pv) {
+    const uint32_t* vrow = reinterpret_cast<const uint32_t*>(vh.ctl + 512);
+    const uint32_t* vfld = vrow + 128;
+    const uint32_t* wstart = vfld + 64;
+    const uint32_t* wrange = wstart + 16;
+    const uint64_t* vc64 = reinterpret_cast<const uint64_t*>(reinterpret_cast<uintptr_t>(vh.vc) & ~uintptr_t(7));
+    const uint32_t vbase_bits = uint32_t((reinterpret_cast<uintptr_t>(vh.vc) & 7u) * 8u);
+    const uint64_t vwords = (reinterpret_cast<uintptr_t>(vh.vend) - reinterpret_cast<uintptr_t>(vc64)) >> 3;
+    const uint32_t hb = vh.hist + g * (kHistStride * 4u);
+    const uint64_t rbit = uint64_t(vbase_bits) + uint64_t(t) * vh.row_bits;
+    constexpr int kW = 4;  // windows loaded up front (16 x 9-bit value rows need 3)
+    uint64_t lo[kW], hi[kW];
+#pragma unroll
+    for (int w = 0; w < kW; ++w) {
+        lo[w] = hi[w] = 0;
+        if (uint32_t(w) < vh.nwin) {
+            const uint64_t wi = (rbit + wstart[w]) >> 6;
+            if (wi + 1 < vwords) {
+                lo[w] = __ldg(vc64 + wi);
+                hi[w] = __ldg(vc64 + wi + 1);
+            }
+        }
+    }
+    for (uint32_t w = 0; w < vh.nwin; ++w) {
+        const uint64_t pos = rbit + wstart[w];
+        uint64_t x;
+        if ((pos >> 6) + 1 < vwords) {
+            uint64_t l, h;
+            if (w < uint32_t(kW)) {
+                l = lo[0], h = hi[0];
+#pragma unroll
+                for (int k = 1; k < kW; ++k)
+                    if (w == uint32_t(k)) l = lo[k], h = hi[k];
+            } else {
+                l = __ldg(vc64 + (pos >> 6));
+                h = __ldg(vc64 + (pos >> 6) + 1);
+            }
+            const uint32_t sh = uint32_t(pos & 63u);
+            x = sh ? ((l >> sh) | (h << (64u - sh))) : l;
+        } else {  // the last words of the buffer
+            x = read_bits64(vh.vc, uint64_t(t) * vh.row_bits + wstart[w], vh.vend);
+        }
+        const uint32_t r = wrange[w];
+        for (uint32_t st = r & 0xFFu; st < (r >> 8); ++st) {
+            const uint32_t f = vfld[st];
+            const uint32_t z = uint32_t(x >> (f & 0xFFu)) & ((1u << (f >> 8)) - 1u);
+            red_shared_add(hb + (vrow[st] + z) * 4u, Pv);
+        }
+    }
+}
+
+// hist_entry with the token's value row staged in shared memory: rbit = the row's first bit relative to
+// the (16 B-aligned) slab buffer at smem address vbuf.
+__device__ __noinline__ void hist_entry_smem(uint32_t vbuf, uint32_t rbit, uint32_t nwin, const uint8_t* ctl,
+                                             uint32_t hb, uint32_t Pv) {
+    const uint32_t* vrow = reinterpret_cast<const uint32_t*>(ctl + 512);
+    const uint32_t* vfld = vrow + 128;
+    const uint32_t* wstart = vfld + 64;
+    const uint32_t* wrange = wstart + 16;
+    for (uint32_t w = 0; w < nwin; ++w) {
+        const uint32_t pos = rbit + wstart[w];
+        uint64_t l, h;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(l) : "r"(vbuf + ((pos >> 6) << 3)));
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(h) : "r"(vbuf + ((pos >> 6) << 3) + 8u));
+        const uint32_t sh = pos & 63u;
+        const uint64_t x = sh ? ((l >> sh) | (h << (64u - sh))) : l;
+        const uint32_t r = wrange[w];
+        for (uint32_t st = r & 0xFFu; st < (r >> 8); ++st) {
+            const uint32_t f = vfld[st];
+            const uint32_t z = uint32_t(x >> (f & 0xFFu)) & ((1u << (f >> 8)) - 1u);
+            red_shared_add(hb + (vrow[st] + z) * 4u, Pv);
+        }
+    }
+}
+
+// A slab of a chunk's value rows, [st0, st1) of the pair, as bulk-copied into a slab buffer: the copy
+// covers the 16 B-aligned bytes around the rows (never past the payload's last 16 B-aligned byte);
+// head = bits between the buffer start and row st0; staged = bits of the buffer holding row data.
+struct Slab {
+    const uint8_t* src;
+    uint32_t bytes, head, staged;
+};
+__device__ __forceinline__ Slab slab_of(const uint8_t* vc, const uint8_t* vend, uint64_t row_bits, uint32_t st0,
+                                        uint32_t st1) {
+    Slab sl;
+    const uint8_t* b0 = vc + (uint64_t(st0) * row_bits >> 3);  // st0 * row_bits is a multiple of 8 (st0 % 512 == 0)
+    const uint8_t* b1 = vc + ((uint64_t(st1) * row_bits + 7) >> 3);
+    const uintptr_t s0 = reinterpret_cast<uintptr_t>(b0) & ~uintptr_t(15);
+    uintptr_t s1 = (reinterpret_cast<uintptr_t>(b1) + 15) & ~uintptr_t(15);
+    const uintptr_t e16 = reinterpret_cast<uintptr_t>(vend) & ~uintptr_t(15);
+    if (s1 > e16) s1 = e16 > s0 ? e16 : s0;
+    sl.src = reinterpret_cast<const uint8_t*>(s0);
+    sl.bytes = uint32_t(s1 - s0);
+    sl.head = uint32_t(reinterpret_cast<uintptr_t>(b0) - s0) * 8u;
+    sl.staged = sl.bytes * 8u;
+    return sl;
+}
+
+// Second key pass for one candidate token t (lane = token): its 8-stage records are re-read and every
+// stage's Lo entry (4 heads, u16) is gathered from the global lo table; returns the 4 heads' sums.
+__device__ __noinline__ uint4 pass2_lo(const uint8_t* krec, uint64_t cap, uint32_t ng8, uint32_t kn,
+                                       const uint2* __restrict__ lo_pair, uint32_t R, uint32_t t) {
+    uint32_t a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+    for (uint32_t g8 = 0; g8 < ng8; ++g8) {
+        const uint8_t* seg = krec + uint64_t(g8) * cap * 10u;
+        const uint2 w = __ldg(reinterpret_cast<const uint2*>(seg) + t);
+        const uint32_t w2 = __ldg(reinterpret_cast<const uint16_t*>(seg + cap * 8u) + t);
+        uint2 v[8];
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+            const uint32_t st = g8 * 8u + ((t & 7u) ^ uint32_t(f));  // field f of a rotated record
+            const uint32_t z = (field_at7_rt(f, w.x, w.y, w2) >> 7) & 1023u;
+            v[f] = st < kn ? __ldg(lo_pair + uint64_t(st) * R + z) : make_uint2(0u, 0u);
+        }
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+            a0 += v[f].x;
+            a1 += v[f].y;
+            b0 += v[f].x >> 16;
+            b1 += v[f].y >> 16;
+        }
+    }
+    return make_uint4(a0 - (b0 << 16), b0, a1 - (b1 << 16), b1);
+}
+
+// L2 prefetch of the records of one LUT group of a chunk (both planes), ahead of the LDGs.  Out of line:
+// thread 0 runs it inside the key loop.
+__device__ __noinline__ void prefetch_group(const uint8_t* krec, uint64_t krec_stride, uint64_t cap, uint32_t pair,
+                                            uint32_t g, uint32_t c0, uint32_t t1, uint64_t pol) {
+    const uint8_t* seg = krec + uint64_t(pair) * krec_stride + uint64_t(g) * cap * 10u;
+    const uint64_t n = t1 - c0;
+    const uint32_t lo = uint32_t(umin64((n * 8u + 15u) & ~uint64_t(15), (cap - c0) * 8u));
+    const uint32_t hi = uint32_t(umin64((n * 2u + 15u) & ~uint64_t(15), (cap - c0) * 2u));
+    if (lo) prefetch_l2_hint(seg + uint64_t(c0) * 8u, lo, pol);
+    if (hi) prefetch_l2_hint(seg + cap * 8u + uint64_t(c0) * 2u, hi, pol);
+}
+
+// L2 prefetch of a chunk's value rows (read by the value phase after the key phase)
+__device__ __noinline__ void prefetch_values(const uint8_t* vc, uint64_t row_bits, uint32_t c0, uint32_t t1,
+                                             const uint8_t* vend, uint64_t pol) {
+    const uint8_t* p0 = vc + (uint64_t(c0) * row_bits >> 3);
+    const uint8_t* p1 = vc + ((uint64_t(t1) * row_bits + 7) >> 3);
+    if (p1 > vend) p1 = vend;
+    p0 = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(p0) & ~uintptr_t(15));
+    while (p0 < p1) {
+        const uint32_t n = uint32_t(umin64(uint64_t(p1 - p0 + 15) & ~uint64_t(15), 65536u));
+        if (p0 + n > vend) break;  // the tail that would overrun the buffer is read on demand
+        prefetch_l2_hint(p0, n, pol);
+        p0 += n;
+    }
+}
+
+// Fold a chunk's int32 histograms (smem, [head][entry]) into the segment's fp32 accumulator in TMEM:
+// acc = acc * al + H * be (acc = H * be for the first chunk).  Warp = (head, TMEM lane quarter);
+// thread = entries e = 128 c + 32 quarter + lane, c < ncol (TMEM column 64 head + c): conflict-free smem
+// reads, one tcgen05.ld / st per 32 columns.  Out of line: keeps the chunk loop's registers for the logits.
+__device__ __noinline__ void chunk_fold(const uint8_t* lutb, uint32_t tmem, uint32_t ncol, bool first, float alg,
+                                        float beg) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t hg = warp >> 2, hlq = warp & 3u;
+    const uint32_t* Hw = reinterpret_cast<const uint32_t*>(lutb) + hg * kHistStride + hlq * 32u + lane;
+    for (uint32_t cb = 0; cb < ncol; cb += 32u) {
+        const uint32_t taddr = tmem + ((hlq * 32u) << 16) + hg * 64u + cb;
+        float v[32];
+        if (!first) {
+            ptx::tmem_ld32(taddr, v);
+            ptx::tc_wait_ld();
+        }
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            const uint32_t col = cb + uint32_t(c);
+            const float hv = col < ncol ? float(Hw[col * 128u]) * beg : 0.f;
+            v[c] = first ? hv : fmaf(v[c], alg, hv);
+        }
+        ptx::tmem_st32(taddr, v);
+    }
+    ptx::tc_wait_st();
+}
+
+// Segment end: o[g][d] = sum_e acc[g][e] * e_v[e][d] (e = the value stack's stage-concatenated entry),
+// the TMEM accumulator staged into the smem buffer; writes the segment's partial (o, m, l).
+__device__ __noinline__ void segment_contract(const float* __restrict__ veff, uint32_t vtotal, float* part_o,
+                                              float* part_m, float* part_l, uint8_t* lutb, uint32_t tmem,
+                                              uint32_t ncol, uint32_t slot, float4 Mn, float4 Lrun) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t hg = warp >> 2, hlq = warp & 3u;
+    // the accumulator, staged from TMEM into the smem buffer as float4 [entry] x (4 heads)
+    float* accs = reinterpret_cast<float*>(lutb);
+    for (uint32_t cb = 0; cb < ncol; cb += 32u) {
+        float v[32];
+        ptx::tmem_ld32(tmem + ((hlq * 32u) << 16) + hg * 64u + cb, v);
+        ptx::tc_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            if (cb + uint32_t(c) < ncol) accs[((cb + uint32_t(c)) * 128u + hlq * 32u + lane) * kG + hg] = v[c];
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    // warp = a slice of the entries, lane = 4 output columns: per entry one coalesced 512 B row read
+    // (L2-resident codebook) and one broadcast LDS.128 of the 4 heads' weights feed 16 FMAs
+    const float4* acc4 = reinterpret_cast<const float4*>(accs);
+    const uint32_t per = (vtotal + 15u) / 16u, j0 = warp * per, j1 = min(vtotal, j0 + per);
+    float o[kG][4];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) o[g][0] = o[g][1] = o[g][2] = o[g][3] = 0.f;
+    const float4* e4 = reinterpret_cast<const float4*>(veff) + lane;
+    uint32_t j = j0;
+    for (; j + 4u <= j1; j += 4u) {
+        float4 x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = __ldg(e4 + uint64_t(j + i) * (kD / 4));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float4 w = acc4[j + i];
+            const float wg[kG] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int g = 0; g < kG; ++g) {
+                o[g][0] = fmaf(wg[g], x[i].x, o[g][0]);
+                o[g][1] = fmaf(wg[g], x[i].y, o[g][1]);
+                o[g][2] = fmaf(wg[g], x[i].z, o[g][2]);
+                o[g][3] = fmaf(wg[g], x[i].w, o[g][3]);
+            }
+        }
+    }
+    for (; j < j1; ++j) {
+        const float4 x = __ldg(e4 + uint64_t(j) * (kD / 4));
+        const float4 w = acc4[j];
+        const float wg[kG] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+            o[g][0] = fmaf(wg[g], x.x, o[g][0]);
+            o[g][1] = fmaf(wg[g], x.y, o[g][1]);
+            o[g][2] = fmaf(wg[g], x.z, o[g][2]);
+            o[g][3] = fmaf(wg[g], x.w, o[g][3]);
+        }
+    }
+    __syncthreads();  // accumulator consumed
+    float4* po = reinterpret_cast<float4*>(lutb);  // [warp][head][lane] x float4 (4 columns)
+#pragma unroll
+    for (int g = 0; g < kG; ++g) po[(warp * kG + g) * 32u + lane] = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+    __syncthreads();
+    {
+        const uint32_t g = tid >> 7, d = tid & (kD - 1u);
+        const float* pf = reinterpret_cast<const float*>(po);
+        float r = 0.f;
+        for (uint32_t w = 0; w < kThreads / 32u; ++w) r += pf[(w * kG + g) * kD + d];
+        part_o[(uint64_t(slot) * kG + g) * kD + d] = r;
+    }
+    if (tid == 0) {
+        reinterpret_cast<float4*>(part_m)[slot] = Mn;
+        reinterpret_cast<float4*>(part_l)[slot] = Lrun;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    uint8_t* const lutb = smem_raw;  // [0, 128 KB): one LUT group; the chunk's value histograms; the contraction's accumulator
+    uint8_t* const ctl = smem_raw + kLutBytes;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ctl);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ctl + 8);
+    float4* red = reinterpret_cast<float4*>(ctl + 64);           // 16 x float4
+    // value stage tables: first histogram entry (the stage's first effective row), size, field position
+    // within its 64-bit window | bits << 8; window start bits and stage ranges
+    uint32_t* vrow = reinterpret_cast<uint32_t*>(ctl + 512);      // [64]
+    uint32_t* vsz = vrow + 64;                                    // [64]
+    uint32_t* vfld = vsz + 64;                                    // [64]
+    uint32_t* wstart = vfld + 64;                                 // [16]
+    uint32_t* wrange = wstart + 16;                               // [16]: s0 | s1 << 8
+    uint2* queue = reinterpret_cast<uint2*>(smem_raw + kLutBytes + kSmemCtl) + warp * kQueueCap;
+    uint64_t* vbar = reinterpret_cast<uint64_t*>(ctl + 48);      // [2]: slab buffers full
+    const uint32_t vbuf0 = ptx::smem_u32(smem_raw + kLutBytes + kSmemCtl + kQueueBytes);
+    if (tid == 0) {
+        ptx::mbar_init(ptx::smem_u32(bar), 1);
+        ptx::mbar_init(ptx::smem_u32(&vbar[0]), 1);
+        ptx::mbar_init(ptx::smem_u32(&vbar[1]), 1);
+        ptx::fence_mbar_init();
+    }
+    if (tid < a.vn) {
+        const StageInfo si = a.vst[tid];
+        vrow[tid] = uint32_t(si.eff_off / kD);
+        vsz[tid] = si.size;
+        vfld[tid] = (si.bit_off - a.vwin[a.vwin_of[tid]].x) | (si.bits << 8);
+    }
+    if (tid < a.vnwin) {
+        wstart[tid] = a.vwin[tid].x;
+        wrange[tid] = a.vwin[tid].y;
+    }
+    if (warp == 0) {
+        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), kTmemCols);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    PHASE_DECL
+    PHASE_T(t_kernel);
+    const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+    const uint32_t lut_s = ptx::smem_u32(lutb);
+    const uint32_t barp = ptx::smem_u32(bar);
+    const uint32_t grp_bytes = a.R * kRowBytes;
+    const uint32_t upp = a.units_per_pair;
+    const uint32_t U = a.n_pairs * upp;  // units (< 2^32: checked at launch)
+    const uint32_t u_begin = uint32_t(uint64_t(U) * blockIdx.x / a.n_cta);
+    const uint32_t u_end = uint32_t(uint64_t(U) * (blockIdx.x + 1) / a.n_cta);
+
+    // chunk of unit u: its pair, token range [c0, t1) within the pair and the unit after it
+    struct Chunk {
+        uint32_t pair, c0, t1, next;
+    };
+    auto chunk_at = [&](uint32_t u) {
+        Chunk c;
+        c.pair = u / upp;
+        const uint32_t pu = c.pair * upp;
+        c.next = min(min(u_end, pu + upp), u + kUnitsPerChunk);
+        c.c0 = (u - pu) * kUnit;
+        c.t1 = uint32_t(umin64(a.n_comp, uint64_t(c.next - pu) * kUnit));
+        return c;
+    };
+    auto issue = [&](uint32_t pair, uint32_t g) {  // one thread: the group's rows, one contiguous block
+        ptx::mbar_arrive_expect_tx(barp, grp_bytes);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.hi + (uint64_t(pair) * a.ng16 + g) * a.R * kGS16);
+        for (uint32_t off = 0; off < grp_bytes; off += 32768u)
+            bulk_g2s_hint(lut_s + off, src + off, min(32768u, grp_bytes - off), barp, pol_last);
+    };
+    // slab sl of a chunk's value rows into slab buffer sl & 1 (thread 0)
+    auto issue_slab = [&](uint32_t pair, uint32_t c0, uint32_t t1, uint32_t sl) {
+        const uint32_t st0 = c0 + sl * kSlabTok;
+        if (st0 >= t1) return;
+        const Slab x = slab_of(a.vcodes + uint64_t(pair) * a.vstride, a.vend, a.vrow_bits, st0, min(t1, st0 + kSlabTok));
+        const uint32_t vb = ptx::smem_u32(&vbar[sl & 1u]);
+        ptx::mbar_arrive_expect_tx(vb, x.bytes);
+        for (uint32_t off = 0; off < x.bytes; off += 32768u)
+            bulk_g2s_hint(vbuf0 + (sl & 1u) * kSlabBytes + off, x.src + off, min(32768u, x.bytes - off), vb, pol_first);
+    };
+    uint32_t vph = 0;  // slab buffer parities
+    // this lane's slot rotation: token & 15 == lane & 15 (units are 512-aligned); l3 picks which of the
+    // token's two 8-stage records feeds slots 0-7 of the 16-stage hi row
+    const uint32_t l15 = lane & 15u, l3 = (lane >> 3) & 1u;
+    const uint32_t hg = warp >> 2, hlq = warp & 3u;  // fold / contraction: head, TMEM lane quarter
+    const uint32_t ncol = (a.vtotal + 127u) >> 7;     // accumulator columns per head (<= 64)
+
+    // segment state (block-uniform) lives in shared memory: registers go to the logits
+    float4* segM = reinterpret_cast<float4*>(ctl + 16);  // running max, then running sum at ctl + 32
+    float4* segL = reinterpret_cast<float4*>(ctl + 32);
+    if (tid == 0) {
+        *segM = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        *segL = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    bool first = true;
+    uint32_t phase = 0;
+    if (tid == 0) {
+        const Chunk c = chunk_at(u_begin);
+        prefetch_group(a.krec, a.krec_stride, a.cap, c.pair, 0, c.c0, c.t1, pol_first);
+        issue(c.pair, 0);
+    }
+    for (uint32_t u = u_begin; u < u_end;) {
+        const Chunk ch = chunk_at(u);
+        const uint32_t pair = ch.pair;
+        const uint32_t c0 = ch.c0, t1 = ch.t1;
+        const uint32_t nt = t1 - c0;
+        const bool has_next = ch.next < u_end;
+        const uint8_t* krec = a.krec + uint64_t(pair) * a.krec_stride;
+        PHASE_T(t_keys);
+        // ---- keys, pass 1: per 16-stage group of the hi table, 16 conflict-free LDS.64 per token.  Per token
+        // the 4 heads' biased 16-bit H values are summed exactly: acc[0] / acc[1] add the 32-bit words
+        // (heads 0|1, 2|3; mod 2^32) and acc[2] / acc[3] their high halves, from which the low-half sums
+        // are recovered (each < 2^22).  Record loads run one token ahead of the lookups.
+        // The running sums stay in registers through the groups (acc[token][4]); they then go to this
+        // thread's TMEM columns tA + 4 k (the weights' staging columns, free until the softmax), where the
+        // candidate and softmax passes read them 4 tokens at a time.
+        const uint32_t tA = tmem + ((hlq * 32u) << 16) + 256u + hg * 64u;
+        uint32_t acc[kTok][4];
+#pragma unroll
+        for (int k = 0; k < kTok; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0u;
+        uint32_t ra[3], rb[3];  // the token's records feeding slots 0-7 / 8-15 of its row (w0, w1, w2)
+        const uint32_t tok0 = c0 + tid, tlast = t1 - 1u;  // record indices fit 32 bits
+        auto load_rec = [&](uint32_t g, int k, uint32_t (&oa)[3], uint32_t (&ob)[3]) {
+            const uint32_t g0 = 2u * g, g1 = 2u * g + 1u;
+            const uint8_t* seg0 = krec + uint64_t(g0) * a.cap * 10u;
+            const uint8_t* seg1 = krec + uint64_t(g1) * a.cap * 10u;
+            // tokens past the range read the last valid record (their logits are masked)
+            const uint32_t t = min(tok0 + uint32_t(k) * kThreads, tlast);
+            const uint2 x0 = ldg_stream_u2(reinterpret_cast<const uint2*>(seg0) + t, pol_first);
+            const uint32_t h0 = ldg_stream_u16(reinterpret_cast<const uint16_t*>(seg0 + a.cap * 8u) + t, pol_first);
+            uint2 x1 = make_uint2(0u, 0u);
+            uint32_t h1 = 0u;
+            if (g1 < a.ng8) {
+                x1 = ldg_stream_u2(reinterpret_cast<const uint2*>(seg1) + t, pol_first);
+                h1 = ldg_stream_u16(reinterpret_cast<const uint16_t*>(seg1 + a.cap * 8u) + t, pol_first);
+            }
+            oa[0] = l3 ? x1.x : x0.x;
+            oa[1] = l3 ? x1.y : x0.y;
+            oa[2] = l3 ? h1 : h0;
+            ob[0] = l3 ? x0.x : x1.x;
+            ob[1] = l3 ? x0.y : x1.y;
+            ob[2] = l3 ? h0 : h1;
+        };
+        load_rec(0, 0, ra, rb);
+        for (uint32_t g = 0; g < a.ng16; ++g) {
+            if (tid == 0) {
+                if (g + 1 < a.ng16) {
+                    prefetch_group(a.krec, a.krec_stride, a.cap, pair, 2u * (g + 1u), c0, t1, pol_first);
+                    if (2u * (g + 1u) + 1u < a.ng8)
+                        prefetch_group(a.krec, a.krec_stride, a.cap, pair, 2u * (g + 1u) + 1u, c0, t1, pol_first);
+                }
+            }
+            if (g + 1 == a.ng16) {  // the value rows: the first two slabs into shared memory (or L2) ahead of the value phase
+                if (a.vslab) {
+                    if (tid == 0) {
+                        issue_slab(pair, c0, t1, 0);
+                        issue_slab(pair, c0, t1, 1);
+                    }
+                } else if (tid == 32) {
+                    prefetch_values(a.vcodes + uint64_t(pair) * a.vstride, a.vrow_bits, c0, t1, a.vend, pol_last);
+                }
+            }
+            PHASE_T(tw);
+            ptx::mbar_wait(barp, phase);
+            PHASE_ADD(1, tw);
+            phase ^= 1u;
+#pragma unroll
+            for (int k = 0; k < kTok; ++k) {
+                uint32_t na[3], nb[3];
+                if (k + 1 < kTok) load_rec(g, k + 1, na, nb);
+                else if (g + 1 < a.ng16) load_rec(g + 1, 0, na, nb);
+                uint32_t* A = acc[k];
+                // 16 lookups, four in flight
+#define VQKV_HI4(R, K0, OFF)                                                                              \
+    {                                                                                                     \
+        uint2 v[4];                                                                                       \
+        _Pragma("unroll") for (int i = 0; i < 4; ++i) {                                                   \
+            const uint32_t x = field_at7_rt((K0) + i, R[0], R[1], R[2]);                                  \
+            lds64(lut_s + ((x & 0x1FF80u) | ((l15 ^ uint32_t((K0) + i + (OFF))) << 3)), v[i]);              \
+        }                                                                                                 \
+        _Pragma("unroll") for (int i = 0; i < 4; ++i) {                                                   \
+            A[0] += v[i].x;                                                                               \
+            A[1] += v[i].y;                                                                               \
+            A[2] += v[i].x >> 16;                                                                         \
+            A[3] += v[i].y >> 16;                                                                         \
+        }                                                                                                 \
+    }
+                VQKV_HI4(ra, 0, 0) VQKV_HI4(ra, 4, 0) VQKV_HI4(rb, 0, 8) VQKV_HI4(rb, 4, 8)
+#undef VQKV_HI4
+                if (k + 1 < kTok || g + 1 < a.ng16) {
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        ra[i] = na[i];
+                        rb[i] = nb[i];
+                    }
+                }
+            }
+            __syncthreads();  // every lane is done with this group's rows
+            if (tid == 0 && g + 1 < a.ng16) issue(pair, g + 1);
+        }
+#pragma unroll
+        for (int kb = 0; kb < kTok; kb += 4) {
+            uint32_t X[16];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) X[4 * k + i] = acc[kb + k][i];
+            ptx::tmem_st16(tA + uint32_t(kb) * 4u, X);
+        }
+        ptx::tc_wait_st();
+        PHASE_ADD(12, t_keys);
+        PHASE_T(t_k2);
+        // ---- per token and head the signed sum of H (the recovered low halves; 16 slots x 32768 of bias
+        // per group), back into TMEM; the first-pass logit l1 = D16 sumH + Cq is within dl / 2 of the
+        // fixed-point logit Dq (65536 sumH + sumLo), sumLo in [0, kn * 65535]
+        {
+            const uint32_t bias = a.ng16 << 19;
+#pragma unroll
+            for (int kb = 0; kb < kTok; kb += 4) {
+                uint32_t acc[16];
+                ptx::tmem_ld16(tA + uint32_t(kb) * 4u, acc);
+                ptx::tc_wait_ld();
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    uint32_t* A = acc + 4 * k;
+                    const uint32_t h1 = A[2], h3 = A[3];
+                    const uint32_t h0 = A[0] - (h1 << 16), h2 = A[1] - (h3 << 16);
+                    A[0] = h0 - bias;
+                    A[1] = h1 - bias;
+                    A[2] = h2 - bias;
+                    A[3] = h3 - bias;
+                }
+                ptx::tmem_st16(tA + uint32_t(kb) * 4u, acc);
+            }
+            ptx::tc_wait_st();
+        }
+        // per-head constants (block-uniform, in shared memory): Dq = the quantum, D16 = 65536 Dq, Cq = dl / 2,
+        // dl = kn * 65535 Dq (the first pass's gap), m1 = the first-pass max, Tq = the candidate threshold
+        float* hc = reinterpret_cast<float*>(ctl + 320);  // [6][4]
+        if (tid < kG) {
+            const float S = __uint_as_float(a.smax[pair * kG + tid]);
+            const float dq = lut_delta(S);
+            hc[0 * kG + tid] = dq;
+            hc[1 * kG + tid] = dq * 65536.0f;
+            hc[3 * kG + tid] = dq * (float(a.kn) * 65535.0f);
+            hc[2 * kG + tid] = 0.5f * hc[3 * kG + tid];
+        }
+        __syncthreads();
+        auto l1 = [&](uint32_t h, int g) { return fmaf(hc[1 * kG + g], float(int(h)), hc[2 * kG + g]); };
+        auto load_h = [&](int kb, uint32_t (&H)[16]) {
+            ptx::tmem_ld16(tA + uint32_t(kb) * 4u, H);
+            ptx::tc_wait_ld();
+        };
+        {
+            float4 ml = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            for (int kb = 0; kb < kTok; kb += 4) {
+                uint32_t H[16];
+                load_h(kb, H);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (uint32_t(kb + k) * kThreads + tid < nt) {
+                        ml.x = fmaxf(ml.x, l1(H[4 * k + 0], 0));
+                        ml.y = fmaxf(ml.y, l1(H[4 * k + 1], 1));
+                        ml.z = fmaxf(ml.z, l1(H[4 * k + 2], 2));
+                        ml.w = fmaxf(ml.w, l1(H[4 * k + 3], 3));
+                    }
+            }
+            const float4 m1 = block_max4(ml, red);
+            if (tid == 0) reinterpret_cast<float4*>(hc)[4] = m1;
+        }
+        __syncthreads();
+        // the candidate threshold per head: every token within T of the first-pass max gets its exact
+        // logit; T is the smallest of 8, 12 for which the rigorous bound on the output error from the
+        // other tokens' first-pass logits (see the kernel comment) is <= 2^-8, else all tokens
+        {
+            float tp[kG] = {0.f, 0.f, 0.f, 0.f}, p8[kG] = {0.f, 0.f, 0.f, 0.f}, p12[kG] = {0.f, 0.f, 0.f, 0.f};
+            for (int kb = 0; kb < kTok; kb += 4) {
+                uint32_t H[16];
+                load_h(kb, H);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (uint32_t(kb + k) * kThreads + tid < nt) {
+#pragma unroll
+                        for (int g = 0; g < kG; ++g) {
+                            const float x = l1(H[4 * k + g], g) - hc[4 * kG + g], p = __expf(x);
+                            tp[g] += p;
+                            p8[g] += x < -8.f ? p : 0.f;
+                            p12[g] += x < -12.f ? p : 0.f;
+                        }
+                    }
+            }
+            const float4 tot = block_sum4(make_float4(tp[0], tp[1], tp[2], tp[3]), red);
+            const float4 o8 = block_sum4(make_float4(p8[0], p8[1], p8[2], p8[3]), red);
+            const float4 o12 = block_sum4(make_float4(p12[0], p12[1], p12[2], p12[3]), red);
+            if (tid < kG) {
+                const float vmax = fmaxf(a.vmax_comp, a.raw_vmax[pair]);
+                const float d = hc[3 * kG + tid];
+                const float tt = tid == 0 ? tot.x : tid == 1 ? tot.y : tid == 2 ? tot.z : tot.w;
+                const float x8 = tid == 0 ? o8.x : tid == 1 ? o8.y : tid == 2 ? o8.z : o8.w;
+                const float x12 = tid == 0 ? o12.x : tid == 1 ? o12.y : tid == 2 ? o12.z : o12.w;
+                const float f = 2.0f * expm1f(0.5f * d) * expf(1.5f * d) * vmax / tt;
+                hc[5 * kG + tid] = (f * x8 <= kKeyBudget) ? 8.f : ((f * x12 <= kKeyBudget) ? 12.f : INFINITY);
+            }
+        }
+        __syncthreads();
+        auto is_cand = [&](const uint32_t (&H)[16], int k, int kk) {
+            if (uint32_t(kk) * kThreads + tid >= nt) return false;
+            bool c = false;
+#pragma unroll
+            for (int g = 0; g < kG; ++g) c |= l1(H[4 * k + g], g) >= hc[4 * kG + g] - hc[5 * kG + g];
+            return c;
+        };
+        PHASE_ADD(13, t_k2);
+        PHASE_T(t_k3);
+        // ---- keys, pass 2: the candidates' Lo sums (lane = candidate of this warp), into the smem buffer
+        uint4* lo_sum = reinterpret_cast<uint4*>(lutb);  // [token in chunk]
+        {
+            uint32_t* cq = reinterpret_cast<uint32_t*>(queue);
+            const uint2* lo_pair = a.lo + uint64_t(pair) * a.kn * a.R;
+            uint32_t qn = 0;
+            for (int kb = 0; kb < kTok; kb += 4) {
+                uint32_t H[16];
+                load_h(kb, H);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool c = is_cand(H, k, kb + k);
+                    const uint32_t mask = __ballot_sync(0xffffffffu, c);
+                    if (c) cq[qn + __popc(mask & ((1u << lane) - 1u))] = uint32_t(kb + k) * kThreads + tid;
+                    qn += __popc(mask);
+                    if (qn >= 32u) {
+                        __syncwarp();
+                        const uint32_t lt = cq[lane];
+                        lo_sum[lt] = pass2_lo(krec, a.cap, a.ng8, a.kn, lo_pair, a.R, c0 + lt);
+                        __syncwarp();
+                        if (lane + 32u < qn) cq[lane] = cq[lane + 32u];
+                        __syncwarp();
+                        qn -= 32u;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane < qn) {
+                const uint32_t lt = cq[lane];
+                lo_sum[lt] = pass2_lo(krec, a.cap, a.ng8, a.kn, lo_pair, a.R, c0 + lt);
+            }
+        }
+        __syncthreads();
+        PHASE_ADD(14, t_k3);
+        PHASE_T(t_k4);
+        // final logits (the candidates' fixed-point logits, the others' first-pass estimates) back into
+        // TMEM over the sums; the softmax then runs over TMEM in batches of 4 tokens
+#pragma unroll 1
+        for (int kb = 0; kb < kTok; kb += 4) {
+            uint32_t H[16];
+            load_h(kb, H);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (is_cand(H, k, kb + k)) {
+                    const uint4 L = lo_sum[uint32_t(kb + k) * kThreads + tid];
+                    const uint32_t Lv[kG] = {L.x, L.y, L.z, L.w};
+#pragma unroll
+                    for (int g = 0; g < kG; ++g)
+                        H[4 * k + g] = __float_as_uint(fmaf(hc[g], float(Lv[g]), hc[1 * kG + g] * float(int(H[4 * k + g]))));
+                } else {
+#pragma unroll
+                    for (int g = 0; g < kG; ++g) H[4 * k + g] = __float_as_uint(l1(H[4 * k + g], g));
+                }
+            }
+            ptx::tmem_st16(tA + uint32_t(kb) * 4u, H);
+        }
+        ptx::tc_wait_st();
+        PHASE_ADD(15, t_k4);
+        PHASE_ADD(0, t_keys);
+        PHASE_T(t_soft);
+        // ---- chunk softmax statistics (exact fp32 weights)
+        float4 mc;
+        {
+            float4 mloc = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+#pragma unroll 1
+            for (int kb = 0; kb < kTok; kb += 4) {
+                uint32_t X[16];
+                load_h(kb, X);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (uint32_t(kb + k) * kThreads + tid < nt) {
+                        mloc.x = fmaxf(mloc.x, __uint_as_float(X[4 * k + 0]));
+                        mloc.y = fmaxf(mloc.y, __uint_as_float(X[4 * k + 1]));
+                        mloc.z = fmaxf(mloc.z, __uint_as_float(X[4 * k + 2]));
+                        mloc.w = fmaxf(mloc.w, __uint_as_float(X[4 * k + 3]));
+                    }
+            }
+            mc = block_max4(mloc, red);
+        }
+        float4 lc;
+        {
+            const float mcv[kG] = {mc.x, mc.y, mc.z, mc.w};
+            float ls[kG] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+            for (int kb = 0; kb < kTok; kb += 4) {
+                uint32_t X[16];
+                load_h(kb, X);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool ok = uint32_t(kb + k) * kThreads + tid < nt;
+#pragma unroll
+                    for (int g = 0; g < kG; ++g) {
+                        const float p = ok ? __expf(__uint_as_float(X[4 * k + g]) - mcv[g]) : 0.f;
+                        X[4 * k + g] = __float_as_uint(p);
+                        ls[g] += p;
+                    }
+                }
+                ptx::tmem_st16(tA + uint32_t(kb) * 4u, X);
+            }
+            ptx::tc_wait_st();
+            lc = block_sum4(make_float4(ls[0], ls[1], ls[2], ls[3]), red);
+        }
+        // fixed point relative to the chunk's normaliser: P = rint(p / u_c), u_c = l_c 2^-28, into the same
+        // TMEM columns (tP == tA): the value phase reads them back 4 tokens at a time
+        const uint32_t tP = tA;
+        {
+            const float qsv[kG] = {kQuantum / lc.x, kQuantum / lc.y, kQuantum / lc.z, kQuantum / lc.w};
+#pragma unroll 1
+            for (int kb = 0; kb < kTok; kb += 4) {
+                uint32_t X[16];
+                load_h(kb, X);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int g = 0; g < kG; ++g) X[4 * k + g] = __float2uint_rn(__uint_as_float(X[4 * k + g]) * qsv[g]);
+                ptx::tmem_st16(tA + uint32_t(kb) * 4u, X);
+            }
+            ptx::tc_wait_st();
+        }
+        PHASE_ADD(2, t_soft);
+        PHASE_T(t_val);
+        // ---- values: int32 histograms [head][entry] over the LUT buffer.  The (token, head) pairs with a
+        // nonzero weight are compacted into a per-warp queue and processed 32 at a time, lane = entry:
+        // the token's value row is read in 64-bit windows (all loads first) and each stage's bin of
+        // that head gets one shared atomic.
+        for (uint32_t i = tid; i < kLutBytes / 16u; i += kThreads) reinterpret_cast<uint4*>(lutb)[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+        PHASE_ADD(8, t_val);
+        {
+            ValueHist vh;
+            vh.vc = a.vcodes + uint64_t(pair) * a.vstride;
+            vh.vend = a.vend;
+            vh.row_bits = a.vrow_bits;
+            vh.nwin = a.vnwin;
+            vh.ctl = ctl;
+            vh.hist = lut_s;
+            const uint8_t* vcp = a.vcodes + uint64_t(pair) * a.vstride;
+            // lane = (entry, stage) processing: this lane's stage and its field / histogram row
+            const uint32_t lanes_e = a.vn <= 16u ? 16u : (a.vn <= 32u ? 32u : 0u);
+            const uint32_t s_st = lanes_e ? lane % lanes_e : 0u;
+            const bool s_on = lanes_e != 0u && s_st < a.vn;
+            const StageInfo s_si = a.vst[s_on ? s_st : 0u];
+            const uint32_t s_bit = s_si.bit_off, s_bits = s_si.bits, s_row = vrow[s_on ? s_st : 0u];
+            const uint32_t s_mask = s_bits >= 32u ? 0xFFFFFFFFu : ((1u << s_bits) - 1u);
+            for (uint32_t sl = 0; sl < uint32_t(kTok) / 4u; ++sl) {
+                const uint32_t st0 = c0 + sl * kSlabTok;
+                if (st0 >= t1) break;
+                const Slab x = slab_of(vcp, a.vend, a.vrow_bits, st0, min(t1, st0 + kSlabTok));
+                const uint32_t vbuf = vbuf0 + (sl & 1u) * kSlabBytes;
+                // every row of the slab in the staged bytes (all but the payload buffer's last rows)
+                const bool all_staged = a.vslab && x.head + (min(t1, st0 + kSlabTok) - st0) * uint32_t(a.vrow_bits) <= x.staged;
+                PHASE_T(t_sw);
+                if (a.vslab) {
+                    ptx::mbar_wait(ptx::smem_u32(&vbar[sl & 1u]), (vph >> (sl & 1u)) & 1u);
+                    vph ^= 1u << (sl & 1u);
+                }
+                PHASE_ADD(9, t_sw);
+                PHASE_T(t_cp);
+                // a batch of queued entries, lane = (entry, stage): lanes_e lanes per entry (16 when the
+                // value stack has <= 16 stages), each extracting its stage's code from the staged row and
+                // doing that bin's one atomic -- short dependency chains instead of a 16-stage loop per lane
+                auto process_batch = [&](uint32_t b0, uint32_t n) {
+#if VQKV_ATTN_EXP == 2
+                    return;
+#endif
+                    if (!all_staged || lanes_e == 0u) {  // generic path: lane = entry
+                        if (lane < n) {
+                            const uint2 e = queue[b0 + lane];
+                            const uint32_t lt = e.x & 0xFFFFu, g = e.x >> 16;
+                            const uint32_t rbit = x.head + (c0 + lt - st0) * uint32_t(a.vrow_bits);
+                            if (a.vslab && rbit + uint32_t(a.vrow_bits) <= x.staged)
+                                hist_entry_smem(vbuf, rbit, a.vnwin, ctl, lut_s + g * (kHistStride * 4u), e.y);
+                            else
+                                hist_entry(vh, c0 + lt, g, e.y);
+                        }
+                        return;
+                    }
+                    if (lanes_e == 16u) {
+                        // two entries per step (lanes 0-15 / 16-31), four steps in flight, no branches
+                        const uint32_t sub = lane >> 4;
+                        for (uint32_t i0 = 0; i0 < n; i0 += 8u) {
+                            uint32_t addr[4], pv[4];
+                            uint64_t lw[4], hw[4];
+                            uint32_t sh[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const uint32_t i = i0 + 2u * uint32_t(u) + sub;
+                                const uint2 e = queue[b0 + min(i, n - 1u)];
+                                const uint32_t lt = e.x & 0xFFFFu, g = e.x >> 16;
+                                const uint32_t pos = x.head + (c0 + lt - st0) * uint32_t(a.vrow_bits) + s_bit;
+                                const uint32_t wa = vbuf + ((pos >> 6) << 3);
+                                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(lw[u]) : "r"(wa));
+                                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(hw[u]) : "r"(wa + 8u));
+                                sh[u] = pos & 63u;
+                                addr[u] = lut_s + (g * kHistStride + s_row) * 4u;
+                                pv[u] = (i < n && s_on) ? e.y : 0u;  // padding steps add nothing
+                            }
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const uint32_t z = uint32_t(sh[u] ? ((lw[u] >> sh[u]) | (hw[u] << (64u - sh[u]))) : lw[u]) & s_mask;
+                                red_shared_add(addr[u] + z * 4u, pv[u]);
+                            }
+                        }
+                        return;
+                    }
+                    const uint32_t per = 32u / lanes_e, sub = lane / lanes_e;
+#pragma unroll 4
+                    for (uint32_t i = sub; i < n; i += per) {
+                        const uint2 e = queue[b0 + i];
+                        const uint32_t lt = e.x & 0xFFFFu, g = e.x >> 16;
+                        const uint32_t pos = x.head + (c0 + lt - st0) * uint32_t(a.vrow_bits) + s_bit;
+                        if (!s_on) continue;
+                        const uint32_t wa = vbuf + ((pos >> 6) << 3);
+                        uint64_t l, h;
+                        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(l) : "r"(wa));
+                        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(h) : "r"(wa + 8u));
+                        const uint32_t shf = pos & 63u;
+                        const uint32_t z = uint32_t(shf ? ((l >> shf) | (h << (64u - shf))) : l) & s_mask;
+                        red_shared_add(lut_s + (g * kHistStride + s_row + z) * 4u, e.y);
+                    }
+                };
+                uint32_t qlen = 0;
+                uint32_t P4[16];
+                ptx::tmem_ld16(tP + sl * 16u, P4);
+                ptx::tc_wait_ld();
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t lt = (sl * 4u + uint32_t(k)) * kThreads + tid;  // token within the chunk
+#pragma unroll
+                    for (int g = 0; g < kG; ++g) {
+                        const bool act = lt < nt && P4[4 * k + g] != 0u;
+                        const uint32_t mask = __ballot_sync(0xffffffffu, act);
+                        if (act)
+                            queue[qlen + __popc(mask & ((1u << lane) - 1u))] = make_uint2(lt | (uint32_t(g) << 16), P4[4 * k + g]);
+                        qlen += __popc(mask);
+                    }
+                    if (qlen >= 32u) {
+                        __syncwarp();
+                        const uint32_t full = qlen & ~31u;
+                        for (uint32_t b = 0; b < full; b += 32u) process_batch(b, 32u);
+                        __syncwarp();
+                        if (lane < qlen - full) queue[lane] = queue[full + lane];  // keep the remainder
+                        __syncwarp();
+                        qlen -= full;
+                    }
+                }
+                __syncwarp();
+                process_batch(0, qlen);  // the slab's remainder (its buffer is recycled next)
+                PHASE_ADD(10, t_cp);
+                PHASE_T(t_sb);
+                __syncthreads();
+                PHASE_ADD(11, t_sb);
+                if (a.vslab && tid == 0 && sl + 2u < uint32_t(kTok) / 4u) issue_slab(pair, c0, t1, sl + 2u);
+            }
+        }
+        __syncthreads();
+        PHASE_ADD(3, t_val);
+        PHASE_T(t_fold);
+        // ---- fold the chunk into the segment's fp32 accumulator in TMEM, rescaled to the running max.
+        // Warp = (head hg, TMEM lane quarter hlq); thread = entries e = 128 c + 32 hlq + lane, c < ncol
+        // (TMEM column 64 hg + c): conflict-free smem reads, one tcgen05.ld/st per 32 columns.
+        const float4 M = *segM;
+        const float4 Mn = make_float4(fmaxf(M.x, mc.x), fmaxf(M.y, mc.y), fmaxf(M.z, mc.z), fmaxf(M.w, mc.w));
+        const float4 al = first ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                : make_float4(__expf(M.x - Mn.x), __expf(M.y - Mn.y), __expf(M.z - Mn.z), __expf(M.w - Mn.w));
+        const float4 ec = make_float4(__expf(mc.x - Mn.x), __expf(mc.y - Mn.y), __expf(mc.z - Mn.z), __expf(mc.w - Mn.w));
+        chunk_fold(lutb, tmem, ncol, first, hg == 0 ? al.x : hg == 1 ? al.y : hg == 2 ? al.z : al.w,
+                   (hg == 0 ? lc.x : hg == 1 ? lc.y : hg == 2 ? lc.z : lc.w) / kQuantum *
+                       (hg == 0 ? ec.x : hg == 1 ? ec.y : hg == 2 ? ec.z : ec.w));
+        const float4 Lo = *segL;
+        const float4 Lrun = make_float4(fmaf(Lo.x, al.x, lc.x * ec.x), fmaf(Lo.y, al.y, lc.y * ec.y),
+                                        fmaf(Lo.z, al.z, lc.z * ec.z), fmaf(Lo.w, al.w, lc.w * ec.w));
+        first = false;
+        ptx::tc_fence_before();
+        __syncthreads();  // histograms consumed, segM / segL read by every thread
+        ptx::tc_fence_after();
+        if (tid == 0) {
+            *segM = Mn;
+            *segL = Lrun;
+        }
+        const uint32_t next_pair = has_next ? ch.next / upp : pair;
+        PHASE_ADD(4, t_fold);
+        PHASE_T(t_con);
+
+        if (!has_next || next_pair != pair) {
+            // ---- segment end (out of line: keeps the chunk loop's registers for the logits)
+            segment_contract(a.veff, a.vtotal, a.part_o, a.part_m, a.part_l, lutb, tmem, ncol, blockIdx.x + pair, Mn,
+                             Lrun);
+            if (tid == 0) {
+                *segM = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+                *segL = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            first = true;
+        }
+        __syncthreads();  // the buffer takes the next chunk's first LUT group; segment state updated
+        PHASE_ADD(5, t_con);
+        PHASE_CNT(6);
+        if (tid == 0 && has_next) issue(next_pair, 0);
+        u = ch.next;
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc(tmem, kTmemCols);
+    PHASE_ADD(7, t_kernel);
+    PHASE_FLUSH;
+}
+
+// out[pair][g] = sum_c exp(m_c - M) o_c / sum_c exp(m_c - M) l_c over the pair's segments and its
+// raw partial; lse = M + log L (natural log of the sum of exp(scale * logits)).
+__global__ void atr_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_m,
+                                   const float* __restrict__ part_l, uint32_t n_cta, uint32_t upp, uint32_t n_pairs,
+                                   uint32_t raw_slot0, float* __restrict__ out, float* __restrict__ lse) {
+    const uint32_t pair = blockIdx.x, d = threadIdx.x;
+    uint32_t s_lo = 1, s_hi = 0;  // segment slots [s_lo, s_hi] (empty when there are no compressed tokens)
+    if (n_cta > 0) {
+        const uint64_t U = uint64_t(n_pairs) * upp;
+        s_lo = cta_of_unit(uint64_t(pair) * upp, U, n_cta) + pair;
+        s_hi = cta_of_unit(uint64_t(pair + 1) * upp - 1, U, n_cta) + pair;
+    }
+    const uint32_t raw = raw_slot0 + pair;
+    for (uint32_t g = 0; g < kG; ++g) {
+        float M = part_m[uint64_t(raw) * kG + g];
+        for (uint32_t sl = s_lo; sl <= s_hi; ++sl) M = fmaxf(M, part_m[uint64_t(sl) * kG + g]);
+        float L = 0.f, o = 0.f;
+        auto add = [&](uint32_t sl) {
+            const float m = part_m[uint64_t(sl) * kG + g];
+            if (m > -INFINITY) {
+                const float w = __expf(m - M);
+                L = fmaf(w, part_l[uint64_t(sl) * kG + g], L);
+                o = fmaf(w, part_o[(uint64_t(sl) * kG + g) * kD + d], o);
+            }
+        };
+        for (uint32_t sl = s_lo; sl <= s_hi; ++sl) add(sl);
+        add(raw);
+        out[(uint64_t(pair) * kG + g) * kD + d] = o / L;
+        if (d == 0 && lse) lse[uint64_t(pair) * kG + g] = M + logf(L);
+    }
+}
+
+// ---- attention records -----------------------------------------------------------------
+// CodeMatrix rows -> records: thread = (token, group, pair); field k of token t's record is
+// the code of stage 8g + ((t & 7) ^ k) (0 for stages past the stack).
+__global__ void atr_pack_kernel(const uint8_t* __restrict__ payload, uint64_t payload_stride, uint64_t row_bits,
+                                const uint8_t* payload_end, const StageInfo* __restrict__ kst, uint32_t kn,
+                                uint64_t src_row, uint64_t count, uint8_t* __restrict__ rec, uint64_t cap,
+                                uint64_t rec_stride, uint64_t dst_row) {
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    const uint32_t g = blockIdx.y, pair = blockIdx.z;
+    if (i >= count) return;
+    const uint64_t t = dst_row + i;  // the record's token index fixes its rotation
+    const uint8_t* src = payload + pair * payload_stride;
+    const uint64_t rb = (src_row + i) * row_bits;
+    uint64_t lo = 0;
+    uint32_t hi = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+        const uint32_t s = g * 8u + ((uint32_t(t) & 7u) ^ k);
+        uint32_t z = 0;
+        if (s < kn) {
+            const StageInfo si = kst[s];
+            z = uint32_t(read_bits64(src, rb + si.bit_off, payload_end)) & ((1u << si.bits) - 1u);
+        }
+        const uint32_t b = 10u * k;
+        if (b + 10u <= 64u) {
+            lo |= uint64_t(z) << b;
+        } else if (b >= 64u) {
+            hi |= z << (b - 64u);
+        } else {  // field 6 straddles bit 64
+            lo |= uint64_t(z) << b;
+            hi |= z >> (64u - b);
+        }
+    }
+    uint8_t* seg = rec + pair * rec_stride + uint64_t(g) * cap * 10u;
+    reinterpret_cast<uint64_t*>(seg)[t] = lo;
+    reinterpret_cast<uint16_t*>(seg + cap * 8u)[t] = uint16_t(hi);
+}
+
+// records -> CodeMatrix rows [0, count) of a dense per-pair payload: thread = output byte; each
+// of its 8 bits is looked up as (token, stage, bit) and read from the token's record.
+__global__ void atr_unpack_kernel(const uint8_t* __restrict__ rec, uint64_t cap, uint64_t rec_stride,
+                                  const StageInfo* __restrict__ kst, uint32_t kn, uint64_t row_bits, uint64_t count,
+                                  uint8_t* __restrict__ payload, uint64_t payload_stride) {
+    extern __shared__ uint16_t bit_stage[];  // [row_bits]: stage of each row bit
+    for (uint32_t b = threadIdx.x; b < row_bits; b += blockDim.x) {
+        uint32_t s = 0;
+        while (s + 1 < kn && b >= kst[s + 1].bit_off) ++s;
+        bit_stage[b] = uint16_t(s);
+    }
+    __syncthreads();
+    const uint64_t nbytes = (count * row_bits + 7) / 8;
+    const uint64_t byte = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    const uint32_t pair = blockIdx.y;
+    if (byte >= nbytes) return;
+    const uint8_t* r = rec + pair * rec_stride;
+    uint32_t out = 0;
+    for (uint32_t i = 0; i < 8; ++i) {
+        const uint64_t bit = byte * 8 + i;
+        if (bit >= count * row_bits) break;
+        const uint64_t t = bit / row_bits;
+        const uint32_t rb = uint32_t(bit - t * row_bits), s = bit_stage[rb];
+        const uint32_t g = s >> 3, k = (uint32_t(t) & 7u) ^ (s & 7u), fb = rb - kst[s].bit_off;
+        const uint8_t* seg = r + uint64_t(g) * cap * 10u;
+        const uint64_t lo = reinterpret_cast<const uint64_t*>(seg)[t];
+        const uint32_t hi = reinterpret_cast<const uint16_t*>(seg + cap * 8u)[t];
+        const uint32_t pos = 10u * k + fb;  // bit of the 80-bit record
+        const uint32_t v = pos < 64u ? uint32_t(lo >> pos) & 1u : (hi >> (pos - 64u)) & 1u;
+        out |= v << i;
+    }
+    payload[pair * payload_stride + byte] = uint8_t(out);
+}
+
+}  // namespace
+
+// tensor-core LUT build: D = 128 stacks carry the fp16 hi/lo operand chunks
+static bool lut_tc_ok(const vqkv_stack_s& ks) {
+    const char* e = getenv("VQKV_LUT_FFMA");
+    if ((e && e[0] == '1') || ks.dim != kD || !ks.d_eff16 || !ks.d_eff16lo) return false;
+    // E_hi = fp16(e) must be finite with headroom (the FFMA kernel covers larger entries)
+    for (const auto& st : ks.stages)
+        if (!(st.max_abs < 32768.f)) return false;
+    return true;
+}
+
+static uint32_t key_groups(const vqkv_stack_s& ks) { return (ks.n + kGS - 1) / kGS; }
+static uint32_t max_size(const vqkv_stack_s& st) {
+    uint32_t m = 0;
+    for (const auto& s : st.stages) m = std::max(m, s.size);
+    return m;
+}
+
+bool gm_supported(const vqkv_stack_s& ks) {
+    if (ks.dim != kD) return false;
+    for (const auto& st : ks.stages)
+        if (st.size > 1024 || st.bits > 10) return false;
+    return true;
+}
+
+// 64-bit windows of a value row: consecutive stages whose fields fit in 64 bits from the
+// window's first field (one unaligned 64-bit read per window in the value phase)
+static std::vector<uint2> value_windows(const vqkv_stack_s& vs, std::vector<uint8_t>* of = nullptr) {
+    std::vector<uint2> w;
+    uint32_t s0 = 0;
+    while (s0 < vs.n) {
+        const uint32_t b0 = vs.stages[s0].bit_off;
+        uint32_t s1 = s0;
+        while (s1 < vs.n && vs.stages[s1].bit_off + vs.stages[s1].bits - b0 <= 64) ++s1;
+        if (of)
+            for (uint32_t s = s0; s < s1; ++s) of->push_back(uint8_t(w.size()));
+        w.push_back(make_uint2(b0, s0 | (s1 << 8)));
+        s0 = s1;
+    }
+    return w;
+}
+
+bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a) {
+    if (!gm_supported(ks) || vs.dim != kD || a.group != kG) return false;
+    if (a.n_init + a.n_local > kChunk) return false;  // the raw CTA keeps one weight per raw row in smem
+    if (vs.n > kMaxVStages || vs.total_rows * 4 * 4 > kLutBytes) return false;  // histograms fit the LUT buffer
+    for (const auto& s : vs.stages)
+        if (s.bits > 32) return false;
+    if (value_windows(vs).size() > 16) return false;
+    return true;
+}
+
+uint64_t gm_pair_bytes(const vqkv_stack_s& ks, uint64_t cap) { return uint64_t(key_groups(ks)) * cap * 10u; }
+
+void launch_keycodes_to_gm(const vqkv_stack_s& ks, const uint8_t* payload, uint64_t payload_stride, uint32_t n_pairs,
+                           uint64_t src_row, uint64_t count, uint8_t* gm, uint64_t cap, uint64_t gm_stride,
+                           uint64_t dst_row, cudaStream_t s) {
+    const uint64_t pb = payload_bytes(ks.row_bits, src_row + count);
+    const uint8_t* end = payload + uint64_t(n_pairs - 1) * payload_stride + pb;
+    dim3 grid(unsigned((count + 255) / 256), key_groups(ks), n_pairs);
+    atr_pack_kernel<<<grid, 256, 0, s>>>(payload, payload_stride, ks.row_bits, end, ks.d_stages, ks.n, src_row, count, gm,
+                                         cap, gm_stride, dst_row);
+    launch_check("atr_pack_kernel");
+}
+
+void launch_keycodes_from_gm(const vqkv_stack_s& ks, const uint8_t* gm, uint64_t cap, uint64_t gm_stride,
+                             uint32_t n_pairs, uint64_t count, uint8_t* payload, uint64_t payload_stride,
+                             cudaStream_t s) {
+    const uint64_t nbytes = payload_bytes(ks.row_bits, count);
+    if (nbytes == 0) return;
+    dim3 grid(unsigned((nbytes + 255) / 256), n_pairs);
+    atr_unpack_kernel<<<grid, 256, sizeof(uint16_t) * ks.row_bits, s>>>(gm, cap, gm_stride, ks.d_stages, ks.n,
+                                                                          ks.row_bits, count, payload, payload_stride);
+    launch_check("atr_unpack_kernel");
+}
+
+// the side stream the raw-row kernel runs on (one per stack, created on first use)
+static cudaStream_t attend_side_stream(const vqkv_stack_s& ks) {
+    auto& st = const_cast<vqkv_stack_s&>(ks);
+    std::lock_guard<std::mutex> lk(st.mu);
+    if (!st.cs_attn) VQKV_CUDA(cudaStreamCreateWithFlags(&st.cs_attn, cudaStreamNonBlocking));
+    return st.cs_attn;
+}
+
+void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s) {
+    const uint32_t ng8 = key_groups(ks), ng16 = (ks.n + kGS16 - 1) / kGS16, R = max_size(ks);
+    const double scale = a.scale > 0.0 ? a.scale : 1.0 / std::sqrt(double(kD));
+    const uint64_t n_comp = a.n_comp;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ks.device);
+    // persistent main grid: one CTA per SM, balanced over 512-token units (never more CTAs than units)
+    const uint32_t upp = uint32_t((n_comp + kUnit - 1) / kUnit);
+    const uint64_t units = uint64_t(a.n_pairs) * upp;
+    const uint32_t n_cta = uint32_t(std::min<uint64_t>(uint64_t(sms), units));
+    // partial slots: segments b + pair (< n_cta + n_pairs), then one raw slot per pair
+    const uint32_t raw_slot0 = n_cta + a.n_pairs;
+    const uint32_t n_slots = raw_slot0 + a.n_pairs;
+    std::vector<uint8_t> win_of;
+    const std::vector<uint2> wins = value_windows(vs, &win_of);
+    // key records: the caller's attention layout, or transcoded from CodeMatrix rows here
+    const uint8_t* krec = a.kcodes_dev;
+    uint64_t kstride = 0, cap = a.kcodes_cap;
+    uint8_t* ktmp = nullptr;
+    if (n_comp > 0) {
+        if (a.kcodes_layout == VQKV_KEYCODES_GROUP_MAJOR) {
+            kstride = a.kcodes_stride ? a.kcodes_stride : gm_pair_bytes(ks, cap);
+        } else {
+            cap = (n_comp + 15) / 16 * 16;
+            kstride = gm_pair_bytes(ks, cap);
+            VQKV_CUDA(cudaMallocAsync(&ktmp, kstride * a.n_pairs, s));
+            const uint64_t kpb = payload_bytes(ks.row_bits, n_comp);
+            launch_keycodes_to_gm(ks, a.kcodes_dev, a.kcodes_stride ? a.kcodes_stride : kpb, a.n_pairs, 0, n_comp, ktmp,
+                                  cap, kstride, 0, s);
+            krec = ktmp;
+        }
+    }
+    uint2 *hi = nullptr, *lo = nullptr;
+    uint32_t* smax = nullptr;
+    float* raw_vmax = nullptr;
+    uint8_t* vtab = nullptr;  // value windows + stage -> window
+    VQKV_CUDA(cudaMallocAsync(&vtab, sizeof(uint2) * 16 + 64, s));
+    VQKV_CUDA(cudaMemcpyAsync(vtab, wins.data(), sizeof(uint2) * wins.size(), cudaMemcpyHostToDevice, s));
+    VQKV_CUDA(cudaMemcpyAsync(vtab + sizeof(uint2) * 16, win_of.data(), win_of.size(), cudaMemcpyHostToDevice, s));
+    float *po = nullptr, *pm = nullptr, *pl = nullptr;
+    VQKV_CUDA(cudaMallocAsync(&po, sizeof(float) * n_slots * kG * kD, s));
+    VQKV_CUDA(cudaMallocAsync(&pm, sizeof(float) * n_slots * kG, s));
+    VQKV_CUDA(cudaMallocAsync(&pl, sizeof(float) * n_slots * kG, s));
+    VQKV_CUDA(cudaMallocAsync(&raw_vmax, sizeof(float) * a.n_pairs, s));
+
+    // raw init/local rows on a side stream, beside the LUT build (fork / join with events)
+    cudaStream_t side = attend_side_stream(ks);
+    cudaEvent_t ev_fork, ev_join;
+    VQKV_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    VQKV_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    VQKV_CUDA(cudaEventRecord(ev_fork, s));
+    VQKV_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    {
+        RawArgs ra{};
+        ra.q = a.q_dev;
+        ra.init_k = a.init_k_dev;
+        ra.init_v = a.init_v_dev;
+        ra.n_init = a.n_init;
+        ra.local_k = a.local_k_dev;
+        ra.local_v = a.local_v_dev;
+        ra.n_local = a.n_local;
+        ra.init_stride = a.init_stride ? a.init_stride : a.n_init;
+        ra.local_stride = a.local_stride ? a.local_stride : a.n_local;
+        ra.scale = float(scale);
+        ra.slot0 = raw_slot0;
+        ra.part_o = po;
+        ra.part_m = pm;
+        ra.part_l = pl;
+        ra.vmax = raw_vmax;
+        const uint32_t n_raw = uint32_t(a.n_init + a.n_local);
+        const int rsmem = int(sizeof(float) * (64 + kG * kD + 4 * kG * kD + uint64_t(n_raw) * kG));
+        VQKV_CUDA(cudaFuncSetAttribute(attend_raw_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem));
+        attend_raw_rows_kernel<<<a.n_pairs, kThreads, rsmem, side>>>(ra);
+        launch_check("attend_raw_rows_kernel");
+    }
+    VQKV_CUDA(cudaEventRecord(ev_join, side));
+
+    if (n_comp > 0) {
+        VQKV_CUDA(cudaMallocAsync(&hi, sizeof(uint2) * a.n_pairs * ng16 * R * kGS16, s));
+        VQKV_CUDA(cudaMallocAsync(&lo, sizeof(uint2) * a.n_pairs * ks.n * R, s));
+        VQKV_CUDA(cudaMallocAsync(&smax, sizeof(uint32_t) * a.n_pairs * kG, s));
+        VQKV_CUDA(cudaMemsetAsync(smax, 0, sizeof(uint32_t) * a.n_pairs * kG, s));
+        const LutTables tabs{hi, lo, smax, ng16, R, ks.n};
+        ProfScope ps("attend_lut_build", s);
+        if (lut_tc_ok(ks)) {
+            // tensor-core LUT GEMM, twice: the per-(pair, head) max, then the fixed-point tables
+            // (VQKV_LUT_FFMA=1 selects the FFMA kernel below)
+            const uint32_t rows = a.n_pairs * kG, rows_pad = (rows + 127) / 128 * 128, qt = rows_pad / 128;
+            __half *qh = nullptr, *ql = nullptr;
+            float* qs = nullptr;
+            VQKV_CUDA(cudaMallocAsync(&qh, sizeof(__half) * rows_pad * kD, s));
+            VQKV_CUDA(cudaMallocAsync(&ql, sizeof(__half) * rows_pad * kD, s));
+            VQKV_CUDA(cudaMallocAsync(&qs, sizeof(float) * rows_pad, s));
+            q_prep_kernel<<<rows_pad / 8, 256, 0, s>>>(a.q_dev, rows, rows_pad, float(scale), qh, ql, qs);
+            launch_check("q_prep_kernel");
+            uint32_t maxch = 0;
+            for (const auto& st : ks.stages) maxch = std::max(maxch, (st.size + 127) / 128);
+            VQKV_CUDA(cudaFuncSetAttribute(lut_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLutTcSmem)));
+            lut_tc_kernel<0><<<dim3(maxch, ks.n), 160, kLutTcSmem, s>>>(ks.d_eff16, ks.d_eff16lo, ks.d_stages, qh, ql, qs,
+                                                                       a.n_pairs, qt, smax, tabs);
+            launch_check("lut_tc_kernel<max>");
+            VQKV_CUDA(cudaFuncSetAttribute(lut_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLutTcSmem)));
+            lut_tc_kernel<1><<<dim3(maxch, ks.n), 160, kLutTcSmem, s>>>(ks.d_eff16, ks.d_eff16lo, ks.d_stages, qh, ql, qs,
+                                                                       a.n_pairs, qt, smax, tabs);
+            launch_check("lut_tc_kernel<quant>");
+            VQKV_CUDA(cudaFreeAsync(qh, s));
+            VQKV_CUDA(cudaFreeAsync(ql, s));
+            VQKV_CUDA(cudaFreeAsync(qs, s));
+        } else {
+            // FFMA: the fp32 LUT into a flat temporary, then its max and the fixed-point tables
+            float4* flat = nullptr;
+            VQKV_CUDA(cudaMallocAsync(&flat, sizeof(float4) * a.n_pairs * ks.n * R, s));
+            VQKV_CUDA(cudaMemsetAsync(flat, 0, sizeof(float4) * a.n_pairs * ks.n * R, s));
+            LutArgs la{a.q_dev, ks.d_eff, ks.d_stages, ks.n, ks.total_rows, float(scale), flat, R};
+            dim3 grid(unsigned((ks.total_rows + kLutEntries - 1) / kLutEntries), (a.n_pairs + 7) / 8);
+            const int lsmem = int(sizeof(float) * (8 * kG * kD + kLutEntries * kLutStride));
+            VQKV_CUDA(cudaFuncSetAttribute(lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem));
+            lut_kernel<<<grid, 256, lsmem, s>>>(la, a.n_pairs);
+            launch_check("lut_kernel");
+            lut_flat_absmax_kernel<<<dim3(16, a.n_pairs), 256, 0, s>>>(flat, ks.n * R, smax);
+            launch_check("lut_flat_absmax_kernel");
+            lut_flat_quant_kernel<<<dim3((R + 255) / 256, a.n_pairs, ks.n), 256, 0, s>>>(flat, ks.d_stages, tabs);
+            launch_check("lut_flat_quant_kernel");
+            VQKV_CUDA(cudaFreeAsync(flat, s));
+        }
+        if (ks.n % kGS16) {
+            lut_hi_pad_kernel<<<a.n_pairs, 32, 0, s>>>(hi, ng16, R, ks.n);
+            launch_check("lut_hi_pad_kernel");
+        }
+    }
+    // the main kernel's error bound reads the raw rows' max |v|: join the side stream here (the raw
+    // kernel is shorter than the LUT build it ran beside)
+    VQKV_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+    if (n_comp > 0) {
+        ProfScope ps("attend", s);
+        const uint64_t vpb = payload_bytes(vs.row_bits, n_comp);
+        const uint64_t vstr = a.vcodes_stride ? a.vcodes_stride : vpb;
+        MainArgs ma{};
+        ma.hi = hi;
+        ma.lo = lo;
+        ma.smax = smax;
+        ma.ng16 = ng16;
+        ma.ng8 = ng8;
+        ma.kn = ks.n;
+        ma.R = R;
+        float vmc = 0.f;  // |v|_inf <= sum_s max |e_s| (fp32 sums, rounded up)
+        for (const auto& st : vs.stages) vmc += st.max_abs;
+        ma.vmax_comp = vmc * (1.0f + 1.0f / 65536.0f);
+        ma.raw_vmax = raw_vmax;
+        ma.krec = krec;
+        ma.krec_stride = kstride;
+        ma.cap = cap;
+        ma.vcodes = a.vcodes_dev;
+        ma.vstride = vstr;
+        ma.vrow_bits = vs.row_bits;
+        // end of the last pair's value payload: reads stop here (earlier pairs may read into the next)
+        ma.vend = a.vcodes_dev + uint64_t(a.n_pairs - 1) * vstr + vpb;
+        ma.vst = vs.d_stages;
+        ma.vn = vs.n;
+        ma.vnwin = uint32_t(wins.size());
+        ma.vwin = reinterpret_cast<const uint2*>(vtab);
+        ma.vwin_of = vtab + sizeof(uint2) * 16;
+        ma.vtotal = uint32_t(vs.total_rows);
+        ma.vslab = vs.row_bits <= kMaxSlabRowBits ? 1u : 0u;
+        ma.veff = vs.d_eff;
+        ma.n_comp = n_comp;
+        ma.n_pairs = a.n_pairs;
+        ma.units_per_pair = upp;
+        ma.n_cta = n_cta;
+        ma.part_o = po;
+        ma.part_m = pm;
+        ma.part_l = pl;
+        VQKV_CUDA(cudaFuncSetAttribute(attend_atr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMainSmem)));
+        attend_atr_kernel<<<n_cta, kThreads, kMainSmem, s>>>(ma);
+        launch_check("attend_atr_kernel");
+    }
+    {
+        ProfScope ps("attend_combine", s);
+        atr_combine_kernel<<<a.n_pairs, kD, 0, s>>>(po, pm, pl, n_comp > 0 ? n_cta : 0u, upp, a.n_pairs, raw_slot0,
+                                                    a.out_dev, a.lse_dev);
+        launch_check("atr_combine_kernel");
+    }
+    cudaEventDestroy(ev_fork);
+    cudaEventDestroy(ev_join);
+    if (hi) VQKV_CUDA(cudaFreeAsync(hi, s));
+    if (lo) VQKV_CUDA(cudaFreeAsync(lo, s));
+    if (smax) VQKV_CUDA(cudaFreeAsync(smax, s));
+    VQKV_CUDA(cudaFreeAsync(raw_vmax, s));
+    if (ktmp) VQKV_CUDA(cudaFreeAsync(ktmp, s));
+    VQKV_CUDA(cudaFreeAsync(vtab, s));
+    VQKV_CUDA(cudaFreeAsync(po, s));
+    VQKV_CUDA(cudaFreeAsync(pm, s));
+    VQKV_CUDA(cudaFreeAsync(pl, s));
+}
+
+}  // namespace vqkv_dev
+
+#ifdef VQKV_ATTN_PHASES
+// diagnostics builds only (not part of include/vqkv_c.h): read-and-clear the per-CTA phase clocks
+extern "C" int vqkv_attn_phase_read(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out, vqkv_dev::vqkv_attn_phase_clk, sizeof(unsigned long long) * 256 * 16) != cudaSuccess) return 1;
+    static unsigned long long zero[256 * 16];
+    return cudaMemcpyToSymbol(vqkv_dev::vqkv_attn_phase_clk, zero, sizeof(zero)) != cudaSuccess;
+}
+#endif
