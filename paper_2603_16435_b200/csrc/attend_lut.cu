@@ -288,11 +288,14 @@ __global__ void __launch_bounds__(160) lut_tc_kernel(const __half* __restrict__ 
         }
     } else {
         const uint32_t j = c * 128 + warp * 32 + lane;  // entry within the stage
+        __shared__ __align__(16) float sc_s[2][128];     // the q-tile's row scales (one load per thread)
         for (uint32_t tq = 0; tq < n_qtiles; ++tq) {
             const uint32_t b = tq & 1, use = tq >> 1;
+            sc_s[b][threadIdx.x] = qscl[uint64_t(tq) * 128 + threadIdx.x];
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps: scales in, tile tq - 2's reads done
             ptx::mbar_wait(ptx::smem_u32(&bar_mma[b]), use & 1);
             ptx::tc_fence_after();
-            const float* sclp = qscl + uint64_t(tq) * 128;
+            const float* sclp = sc_s[b];
             float v[4][32];
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) ptx::tmem_ld32(tmem + ((warp * 32u) << 16) + 128u * b + 32u * c4, v[c4]);
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(160) lut_tc_kernel(const __half* __restrict__ 
                 for (int pp = 0; pp < 8; ++pp) {
                     const uint32_t pair = tq * 32 + c4 * 8 + pp;
                     if (j < si.size && pair < n_pairs) {
-                        const float4 sc = __ldg(reinterpret_cast<const float4*>(sclp) + c4 * 8 + pp);
+                        const float4 sc = reinterpret_cast<const float4*>(sclp)[c4 * 8 + pp];
                         lut[lut_off(pair, ng, R, blockIdx.y, j)] = (
                                make_float4(v[c4][4 * pp] * sc.x, v[c4][4 * pp + 1] * sc.y, v[c4][4 * pp + 2] * sc.z,
                                            v[c4][4 * pp + 3] * sc.w));
