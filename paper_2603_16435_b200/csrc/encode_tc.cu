@@ -484,6 +484,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                             ptx::tc_wait_ld();
                             ptx::tc_fence_before();
                             ptx::mbar_arrive(bar_empty);
+                            VQKV_PHASE_DEP(12, v3[31])
                             mA[4 * c] = max32(v0);
                             mA[4 * c + 1] = max32(v1);
                             mA[4 * c + 2] = max32(v2);

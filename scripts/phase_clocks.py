@@ -24,8 +24,8 @@ d = [out[k] - base[k] for k in range(14)]
 warps = 8 * 148
 ms = s.elapsed_time(e)
 print(f"n={n} S={S} streams={streams}: {ms:.2f} ms  (~{ms*1.9e6:.3g} clk per warp at 1.9 GHz)")
-names = ["prologue", "acc wait", "chunk max", "candidates", "upd: st-wait+arrive", "rs setup", "rs load+dot", "rs min", "code store", "upd: issue+ld0", "upd: e_z wait", "upd: rest", "-"]
-tot = sum(d[:12])
-for k in range(12):
+names = ["prologue", "acc wait", "chunk max", "candidates", "upd: st-wait+arrive", "rs setup", "rs load+dot", "rs min", "code store", "upd: issue+ld0", "upd: e_z wait", "upd: rest", "acc ld"]
+tot = sum(d[:13])
+for k in range(13):
     print(f"  {names[k]:13s} {d[k]/warps:12.4g} clk/warp  {100*d[k]/tot:5.1f}%")
 print("  rescored pairs", d[13])
