@@ -51,10 +51,12 @@ void launch_pack_listed_rows(const uint16_t* codes, const uint32_t* rows_dev, co
 namespace {
 
 constexpr int kThreads = 384;
-constexpr int kNB = 2;                    // codebook chunk ring depth per tile
+constexpr int kNB = 2;                    // codebook chunk ring depth per tile (single-CTA kernel)
+constexpr int kNBPair = 3;                // ring depth per tile of the CTA-pair kernel (half chunks)
 constexpr uint32_t kChunkBytes = 36864;   // 128 entries x (128 + 16) fp16
 constexpr uint32_t kATileBytes = 36864;   // 128 rows x (128 + 16) fp16
 constexpr uint32_t kExtOff = 32768;       // the 16-wide K block (||e||^2 / row scale)
+constexpr uint32_t kHalfBytes = 18432;    // CTA-pair kernel: this CTA's 64 entries of a chunk
 constexpr int kMaxChunks = 8;            // chunks per super-block (1024 entries)
 constexpr int kMaxSuper = 4;             // super-blocks per stage: S <= 4096
 constexpr uint32_t kSmemStages = 128;     // stage descriptors cached in smem
@@ -63,13 +65,14 @@ constexpr uint32_t kSmemStages = 128;     // stage descriptors cached in smem
 // re-read A from shared memory per instruction, and at N=64 that pushes the
 // operand traffic to 192 B/clk, above the ~128 B/clk smem path.)
 constexpr uint32_t kIdesc = ptx::idesc_f16_f32(128, 128);
+constexpr uint32_t kIdescPair = ptx::idesc_f16_f32(256, 128);
 // register split: 128 x kCtlRegs + 256 x kEpiRegs <= 64K (launch allocation 168)
 constexpr uint32_t kCtlRegs = 56, kEpiRegs = 224;
 constexpr uint32_t kSleepNs = 1000000;  // control-thread barrier suspend hint
 
 struct __align__(8) SmemCtl {
-    uint64_t b_full[2][kNB];   // per tile: its own codebook-chunk ring
-    uint64_t b_empty[2][kNB];
+    uint64_t b_full[2][kNBPair];   // per tile: its own codebook-chunk ring
+    uint64_t b_empty[2][kNBPair];
     uint64_t acc_full[2];
     uint64_t acc_empty[2];
     uint64_t a_ready[2];
@@ -80,6 +83,8 @@ struct __align__(8) SmemCtl {
     StageInfo st[kSmemStages];
 };
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + 2 * kATileBytes + 2 * kNB * kChunkBytes + sizeof(SmemCtl);
+constexpr size_t kSmemBytesPair = 1024 + 2 * kATileBytes + 2 * kNBPair * kHalfBytes + sizeof(SmemCtl);
+static_assert(kNBPair * kHalfBytes <= kNB * kChunkBytes, "pair ring must fit the single-CTA layout");
 
 // tree maximum of 32 values with 3-input FMNMX
 __device__ __forceinline__ float max32(const float (&v)[32]) {
@@ -149,10 +154,11 @@ __device__ __forceinline__ void store_a_chunk(uint8_t* a_tile, uint32_t i, int c
 struct JobIter {
     const StageInfo* st;
     uint32_t n_stages;
-    uint64_t n_pairs, p;
+    uint32_t n_pairs, p, stride;  // work items (< 2^25: rows per call < 2^32)
     uint32_t s = 0, c = 0, nch = 0;
     bool done;
-    __device__ JobIter(const StageInfo* stg, uint32_t ns, uint64_t np) : st(stg), n_stages(ns), n_pairs(np), p(blockIdx.x) {
+    __device__ JobIter(const StageInfo* stg, uint32_t ns, uint32_t np, uint32_t first, uint32_t step)
+        : st(stg), n_stages(ns), n_pairs(np), p(first), stride(step) {
         done = p >= n_pairs;
         nch = done ? 0 : st[0].pad_size / 128;
     }
@@ -161,7 +167,7 @@ struct JobIter {
         c = 0;
         if (++s == n_stages) {
             s = 0;
-            p += gridDim.x;
+            p += stride;
             done = p >= n_pairs;
         }
         if (!done) nch = st[s].pad_size / 128;
@@ -181,6 +187,12 @@ __device__ __forceinline__ Tile tile_of(uint64_t t, uint64_t tiles_per_stream, u
     return r;
 }
 
+// kPair = false: one CTA per SM, M=128 tiles.  kPair = true: clusters of two CTAs (one SM pair);
+// each tile slot is a 256-row pair tile (128 rows per CTA) computed by cta_group::2 MMAs that the
+// leader CTA issues: A rows come from each CTA's own shared memory, each CTA stages only its 64
+// entries of every codebook chunk (half the chunk stream and half the B operand reads per SM), and
+// each CTA's epilogue reads its own rows' accumulators from its own TMEM.
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
 encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const __half* __restrict__ eff16,
                  const float* __restrict__ sqn_pad, const float* __restrict__ eff, const float* __restrict__ xs,
@@ -188,27 +200,38 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                  float* __restrict__ norms, float* __restrict__ residuals, uint32_t* __restrict__ exact_list,
                  uint32_t* __restrict__ exact_count, unsigned long long* __restrict__ counters, uint32_t dbg,
                  uint8_t* __restrict__ payload, uint64_t pay_stride, uint32_t row_bytes) {
+    constexpr int NB = kPair ? kNBPair : kNB;
+    constexpr uint32_t kSlot = kPair ? kHalfBytes : kChunkBytes;  // ring slot bytes
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* a_tiles = smem;                                  // 2 x 36 KB
-    uint8_t* b_ring = smem + 2 * kATileBytes;                 // 2 tiles x kNB x 36 KB
-    SmemCtl* ctl = reinterpret_cast<SmemCtl*>(b_ring + 2 * kNB * kChunkBytes);
+    uint8_t* b_ring = smem + 2 * kATileBytes;                 // 2 tiles x NB x slot
+    SmemCtl* ctl = reinterpret_cast<SmemCtl*>(b_ring + 2 * NB * kSlot);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // (these are re-derived from special registers and parameters where used: the epilogue keeps
+    // its registers for the score tiles)
+    // cluster rank (clusters are consecutive CTA pairs along x): 0 = leader, issues the MMAs
+#define VQKV_RANK (kPair ? (blockIdx.x & 1u) : 0u)
     const uint64_t tiles_per_stream = (rows + 127) / 128;
     const uint64_t n_tiles = tiles_per_stream * n_streams;
-    const uint64_t n_pairs = (n_tiles + 1) / 2;
+    // work items: pairs of tiles (one per tile slot), or quads (a pair tile per slot) per cluster
+#define VQKV_N_ITEMS uint32_t(kPair ? (((rows + 127) / 128) * n_streams + 3) / 4 : (((rows + 127) / 128) * n_streams + 1) / 2)
+#define VQKV_ITEM0 (kPair ? blockIdx.x >> 1 : blockIdx.x)
+#define VQKV_ITEM_STEP (kPair ? gridDim.x >> 1 : gridDim.x)
 
     if (threadIdx.x == 0) {
         for (int t = 0; t < 2; ++t)
-            for (int i = 0; i < kNB; ++i) {
-                ptx::mbar_init(ptx::smem_u32(&ctl->b_full[t][i]), 1);
+            for (int i = 0; i < NB; ++i) {
+                // the leader's full barrier also collects the peer's "my half landed" arrival
+                ptx::mbar_init(ptx::smem_u32(&ctl->b_full[t][i]), (kPair && VQKV_RANK == 0) ? 2 : 1);
                 ptx::mbar_init(ptx::smem_u32(&ctl->b_empty[t][i]), 1);
             }
         for (int t = 0; t < 2; ++t) {
             ptx::mbar_init(ptx::smem_u32(&ctl->acc_full[t]), 1);
-            ptx::mbar_init(ptx::smem_u32(&ctl->acc_empty[t]), 128);
-            ptx::mbar_init(ptx::smem_u32(&ctl->a_ready[t]), 128);
+            // pair kernel: one arrival per epilogue warp of both CTAs
+            ptx::mbar_init(ptx::smem_u32(&ctl->acc_empty[t]), kPair ? 8 : 128);
+            ptx::mbar_init(ptx::smem_u32(&ctl->a_ready[t]), kPair ? 8 : 128);
         }
         ptx::fence_mbar_init();
     }
@@ -218,11 +241,19 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         ctl->st[i] = si;
     }
     if (warp == 2) {
-        ptx::tmem_alloc(ptx::smem_u32(&ctl->tmem_base), 512);
-        ptx::tmem_relinquish();
+        if constexpr (kPair) {
+            ptx::tmem_alloc2(ptx::smem_u32(&ctl->tmem_base), 512);
+            ptx::tmem_relinquish2();
+        } else {
+            ptx::tmem_alloc(ptx::smem_u32(&ctl->tmem_base), 512);
+            ptx::tmem_relinquish();
+        }
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair)
+        ptx::cluster_sync();  // both CTAs' barriers and TMEM exist before any cross-CTA traffic
+    else
+        __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = ctl->tmem_base;
     const StageInfo* stg = (n_stages <= kSmemStages) ? ctl->st : stages;  // producer / MMA stage walk
@@ -240,22 +271,47 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
         const uint32_t t = warp >> 1;
         if (lane == 0 && (warp & 1) == 0) {
             // ------------------------------------------------------------ producer
-            JobIter it(stg, n_stages, n_pairs);
+            JobIter it(stg, n_stages, VQKV_N_ITEMS, VQKV_ITEM0, VQKV_ITEM_STEP);
             uint32_t slot = 0, ph = 0, n_loaded = 0;
             while (!it.done) {
                 ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->b_empty[t][slot]), ph ^ 1, kSleepNs);
                 const uint32_t bar = ptx::smem_u32(&ctl->b_full[t][slot]);
-                if ((dbg & 4u) || ((dbg & 8u) && n_loaded >= uint32_t(kNB))) {
+                if ((dbg & 4u) || ((dbg & 8u) && n_loaded >= uint32_t(NB))) {
                     // timing experiments only (wrong codes): bit 2 no codebook traffic at all,
                     // bit 3 keep re-using the first ring fill (realistic ambiguity, no chunk stream)
                     ptx::mbar_arrive(bar);
                 } else {
-                    ptx::mbar_arrive_expect_tx(bar, kChunkBytes);
-                    const __half* src = eff16 + stg[it.s].eff16_off + uint64_t(it.c) * (kChunkBytes / 2);
-                    ptx::bulk_g2s(ptx::smem_u32(b_ring + (t * kNB + slot) * kChunkBytes), src, kChunkBytes, bar);
+                    ptx::mbar_arrive_expect_tx(bar, kSlot);
+                    const uint8_t* src = reinterpret_cast<const uint8_t*>(eff16 + stg[it.s].eff16_off) +
+                                         uint64_t(it.c) * kChunkBytes;
+                    const uint32_t dst = ptx::smem_u32(b_ring + (t * NB + slot) * kSlot);
+                    if constexpr (kPair) {
+                        // this CTA's entries [64 rank, 64 rank + 64) of the chunk: both 64-wide K blocks
+                        // (SW128 rows of 128 B) and the ext block's 8 core-matrix row groups
+                        ptx::bulk_g2s(dst, src + VQKV_RANK * 8192u, 8192u, bar);
+                        ptx::bulk_g2s(dst + 8192u, src + 16384u + VQKV_RANK * 8192u, 8192u, bar);
+                        ptx::bulk_g2s(dst + 16384u, src + kExtOff + VQKV_RANK * 2048u, 2048u, bar);
+                    } else {
+                        ptx::bulk_g2s(dst, src, kChunkBytes, bar);
+                    }
                     ++n_loaded;
                 }
-                if (++slot == kNB) {
+                if (++slot == NB) {
+                    slot = 0;
+                    ph ^= 1;
+                }
+                it.next();
+            }
+        } else if (lane == 0 && kPair && VQKV_RANK != 0) {
+            // ------------------------------------------------------------ peer: half-chunk forwarder
+            // the leader's MMAs read this CTA's half of each chunk: tell its full barrier when it landed
+            JobIter it(stg, n_stages, VQKV_N_ITEMS, VQKV_ITEM0, VQKV_ITEM_STEP);
+            uint32_t slot = 0, ph = 0;
+            while (!it.done) {
+                const uint32_t bar = ptx::smem_u32(&ctl->b_full[t][slot]);
+                ptx::mbar_wait_sleep(bar, ph, kSleepNs);
+                ptx::mbar_arrive_cluster(ptx::mapa(bar, 0u));
+                if (++slot == NB) {
                     slot = 0;
                     ph ^= 1;
                 }
@@ -263,34 +319,53 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
             }
         } else if (lane == 0) {
             // ------------------------------------------------------------ MMA issuer
-            JobIter it(stg, n_stages, n_pairs);
+            JobIter it(stg, n_stages, VQKV_N_ITEMS, VQKV_ITEM0, VQKV_ITEM_STEP);
             uint32_t slot = 0, ph = 0, a_ph = 0, e_ph = 1;
             const uint32_t a_base = ptx::smem_u32(a_tiles) + t * kATileBytes;
             const uint32_t b_base = ptx::smem_u32(b_ring);
+            // K-block stride of the B operand in shared memory: 64 or 128 entry rows of 128 B
+            constexpr uint32_t kBkb = kPair ? 8192u : 16384u;
+            constexpr uint32_t kBext = kPair ? 16384u : kExtOff;
             while (!it.done) {
+                // (pair kernel: the peer's arrivals use default .cta semantics, as in CUTLASS's 2-SM
+                // pipelines; the data they hand over is ordered by tcgen05 / proxy fences)
                 ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->b_full[t][slot]), ph, kSleepNs);
                 if (it.c == 0) {
                     ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->a_ready[t]), a_ph, kSleepNs);
                     a_ph ^= 1;
                 }
-                const uint32_t bb = b_base + (t * kNB + slot) * kChunkBytes;
                 ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->acc_empty[t]), e_ph, kSleepNs);
+                const uint32_t bb = b_base + (t * NB + slot) * kSlot;
                 e_ph ^= 1;
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + 128u * t;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32;
-                    ptx::mma_f16_ss(d, ptx::umma_desc_sw128(a_base + koff), ptx::umma_desc_sw128(bb + koff), kIdesc,
-                                    k > 0 ? 1u : 0u);
+                    const uint32_t koff = (k & 3) * 32;
+                    const uint64_t ad = ptx::umma_desc_sw128(a_base + (k >> 2) * 16384 + koff);
+                    const uint64_t bd = ptx::umma_desc_sw128(bb + (k >> 2) * kBkb + koff);
+                    if constexpr (kPair)
+                        ptx::mma2_f16_ss(d, ad, bd, kIdescPair, k > 0 ? 1u : 0u);
+                    else
+                        ptx::mma_f16_ss(d, ad, bd, kIdesc, k > 0 ? 1u : 0u);
                 }
                 // + (-2^(sigma-1)) * (||e||^2 hi + lo): the score's norm term
-                if (!(dbg & 1u))
-                    ptx::mma_f16_ss(d, ptx::umma_desc_noswz(a_base + kExtOff, 128, 256),
-                                    ptx::umma_desc_noswz(bb + kExtOff, 128, 256), kIdesc, 1u);
-                ptx::mma_commit(ptx::smem_u32(&ctl->acc_full[t]));
-                ptx::mma_commit(ptx::smem_u32(&ctl->b_empty[t][slot]));
-                if (++slot == kNB) {
+                if (!(dbg & 1u)) {
+                    const uint64_t ad = ptx::umma_desc_noswz(a_base + kExtOff, 128, 256);
+                    const uint64_t bd = ptx::umma_desc_noswz(bb + kBext, 128, 256);
+                    if constexpr (kPair)
+                        ptx::mma2_f16_ss(d, ad, bd, kIdescPair, 1u);
+                    else
+                        ptx::mma_f16_ss(d, ad, bd, kIdesc, 1u);
+                }
+                if constexpr (kPair) {
+                    ptx::mma2_commit_mc(ptx::smem_u32(&ctl->acc_full[t]), uint16_t(3));
+                    ptx::mma2_commit_mc(ptx::smem_u32(&ctl->b_empty[t][slot]), uint16_t(3));
+                } else {
+                    ptx::mma_commit(ptx::smem_u32(&ctl->acc_full[t]));
+                    ptx::mma_commit(ptx::smem_u32(&ctl->b_empty[t][slot]));
+                }
+                if (++slot == NB) {
                     slot = 0;
                     ph ^= 1;
                 }
@@ -336,8 +411,20 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
 #define VQKV_PHASE_DEP(k, dep) {}
 #endif
 
-        for (uint64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
-            const Tile tl = tile_of(2 * p + t, tiles_per_stream, rows, n_tiles);
+        // release of the accumulator / the next A tile to the MMA issuer: every thread (single CTA),
+        // or one lane per warp after the warp's own tcgen05 / shared-memory work (CTA pair: the
+        // peer CTA's warps arrive on the leader's barriers)
+        auto release = [&](uint32_t bar, bool smem_written) {
+            if constexpr (kPair) {
+                if (smem_written) __syncwarp();  // the other lanes' proxy fences precede lane 0's arrive
+                // the leader's barrier (mapa of its own address is itself)
+                ptx::mbar_arrive_cluster_if(ptx::mapa(bar, 0u), lane == 0);
+            } else {
+                ptx::mbar_arrive(bar);
+            }
+        };
+        for (uint32_t p = VQKV_ITEM0; p < VQKV_N_ITEMS; p += VQKV_ITEM_STEP) {
+            const Tile tl = tile_of(kPair ? 4ull * p + 2 * t + VQKV_RANK : 2ull * p + t, tiles_per_stream, rows, n_tiles);
             const bool valid = i < tl.nvalid;
             const uint64_t grow = tl.stream * rows + tl.row0 + i;  // global row index
             bool exact_row = false;
@@ -405,7 +492,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 store_a_ext(a_tile, i, sigma);
                 ptx::fence_async_smem();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(bar_aready);
+                release(bar_aready, true);
             }
             VQKV_PHASE(0)
 
@@ -429,9 +516,9 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                         f_ph ^= 1;
                         ptx::tc_fence_after();
                         ptx::tc_fence_before();
-                        ptx::mbar_arrive(bar_empty);
+                        release(bar_empty, false);
                     }
-                    if (s + 1 < n_stages) ptx::mbar_arrive(bar_aready);
+                    if (s + 1 < n_stages) release(bar_aready, true);
                     continue;
                 }
                 // ---- error window ("exactness of the tensor-core encoder")
@@ -483,7 +570,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                             ptx::tmem_ld32(t_acc + 96u, v3);
                             ptx::tc_wait_ld();
                             ptx::tc_fence_before();
-                            ptx::mbar_arrive(bar_empty);
+                            release(bar_empty, false);
                             VQKV_PHASE_DEP(12, v3[31])
                             mA[4 * c] = max32(v0);
                             mA[4 * c + 1] = max32(v1);
@@ -736,7 +823,7 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                 if (!last) {
                     ptx::fence_async_smem();
                     ptx::tc_fence_before();
-                    ptx::mbar_arrive(bar_aready);
+                    release(bar_aready, true);
                 } else if (valid && !exact_row) {
 #pragma unroll
                     for (int l = 0; l < 4; ++l) n0[l] = __fadd_rn(n0[l], n1[l]);
@@ -762,11 +849,26 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
     }
     __syncwarp();
     ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == 2) ptx::tmem_dealloc(tmem, 512);
+#undef VQKV_RANK
+#undef VQKV_N_ITEMS
+#undef VQKV_ITEM0
+#undef VQKV_ITEM_STEP
+    if constexpr (kPair) {
+        ptx::cluster_sync();  // the leader's last MMAs wrote the peer's TMEM
+        if (warp == 2) ptx::tmem_dealloc2(tmem, 512);
+    } else {
+        __syncthreads();
+        if (warp == 2) ptx::tmem_dealloc(tmem, 512);
+    }
 }
 
 }  // namespace
+
+// CTA-pair (cta_group::2) encoder: VQKV_ENC_PAIR=0 selects the single-CTA kernel
+bool encode_pair_mode() {
+    const char* e = getenv("VQKV_ENC_PAIR");
+    return !(e && e[0] == '0');
+}
 
 uint32_t dbg_flags() {
     const char* e = getenv("VQKV_DBG");
@@ -790,8 +892,6 @@ void launch_encode_tc(const vqkv_stack_s& st, const float* xs, uint32_t n_stream
     if (total >= (1ull << 32)) fail(VQKV_UNSUPPORTED, "more than 2^32 rows per call");
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st.device);
-    // per launch: the attribute is per device, and the call is cheap (no static flag to race on)
-    VQKV_CUDA(cudaFuncSetAttribute(encode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
     uint16_t* codes = nullptr;
     uint32_t* list = nullptr;  // [0] = count, [1..] = rows
     VQKV_CUDA(cudaMallocAsync(&codes, sizeof(uint16_t) * total * st.n, s));
@@ -802,14 +902,43 @@ void launch_encode_tc(const vqkv_stack_s& st, const float* xs, uint32_t n_stream
     for (const auto& si : st.stages) direct = direct && si.bits <= 16;
     const uint64_t pb = payload_bytes(st.row_bits, rows);
     const uint64_t tiles = ((rows + 127) / 128) * n_streams;
-    const uint64_t pairs = (tiles + 1) / 2;
-    const unsigned grid = unsigned(std::min<uint64_t>(pairs, uint64_t(sms)));
+    uint8_t* pay = direct ? payload : nullptr;
+    const uint32_t rb = uint32_t(st.row_bits / 8);
     {
     ProfScope ps("encode_tc", s);
-    encode_tc_kernel<<<grid, kThreads, kSmemBytes, s>>>(st.d_stages, st.n, st.d_eff16, st.d_sqn_pad, st.d_eff, xs,
-                                                         n_streams, rows, search_block, codes, norms, residuals,
-                                                         list + 1, list, st.d_counters, dbg_flags(),
-                                                         direct ? payload : nullptr, pb, uint32_t(st.row_bits / 8));
+    if (encode_pair_mode()) {
+        // clusters of two CTAs on an SM pair, 4 tiles in flight per cluster
+        const uint64_t quads = (tiles + 3) / 4;
+        const unsigned clusters = unsigned(std::min<uint64_t>(quads, uint64_t(sms / 2)));
+        VQKV_CUDA(cudaFuncSetAttribute(encode_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kSmemBytesPair)));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * clusters);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = kSmemBytesPair;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        VQKV_CUDA(cudaLaunchKernelEx(&cfg, encode_tc_kernel<true>, (const StageInfo*)st.d_stages, st.n,
+                                     (const __half*)st.d_eff16, (const float*)st.d_sqn_pad, (const float*)st.d_eff, xs,
+                                     n_streams, rows, search_block, codes, norms, residuals, list + 1, list,
+                                     st.d_counters, dbg_flags(), pay, pb, rb));
+    } else {
+        const uint64_t pairs = (tiles + 1) / 2;
+        const unsigned grid = unsigned(std::min<uint64_t>(pairs, uint64_t(sms)));
+        // per launch: the attribute is per device, and the call is cheap (no static flag to race on)
+        VQKV_CUDA(cudaFuncSetAttribute(encode_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kSmemBytes)));
+        encode_tc_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(st.d_stages, st.n, st.d_eff16, st.d_sqn_pad, st.d_eff,
+                                                                   xs, n_streams, rows, search_block, codes, norms,
+                                                                   residuals, list + 1, list, st.d_counters, dbg_flags(),
+                                                                   pay, pb, rb);
+    }
     launch_check("encode_tc_kernel");
     }
     // rows with non-finite input: exact reference semantics
