@@ -52,7 +52,10 @@ namespace {
 
 constexpr int kThreads = 384;
 constexpr int kNB = 2;                    // codebook chunk ring depth per tile (single-CTA kernel)
-constexpr int kNBPair = 3;                // ring depth per tile of the CTA-pair kernel (half chunks)
+#ifndef VQKV_NBPAIR
+#define VQKV_NBPAIR 3
+#endif
+constexpr int kNBPair = VQKV_NBPAIR;               // ring depth per tile of the CTA-pair kernel (half chunks)
 constexpr uint32_t kChunkBytes = 36864;   // 128 entries x (128 + 16) fp16
 constexpr uint32_t kATileBytes = 36864;   // 128 rows x (128 + 16) fp16
 constexpr uint32_t kExtOff = 32768;       // the 16-wide K block (||e||^2 / row scale)
@@ -255,7 +258,10 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
     else
         __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem = ctl->tmem_base;
+    // a 512-column allocation owns all of TMEM, so its address is lane 0, column 0 (a constant keeps
+    // it out of the epilogue's registers)
+    const uint32_t tmem = 0u;
+    if (threadIdx.x == 0 && ctl->tmem_base != 0u) __trap();
     const StageInfo* stg = (n_stages <= kSmemStages) ? ctl->st : stages;  // producer / MMA stage walk
     // control warpgroup (producer / MMA threads) hands registers to the epilogue
     if (warp < 4)
