@@ -1032,6 +1032,16 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
                     prefetch_group(a.krec, a.krec_stride, a.cap, nx.pair, 0, nx.c0, nx.t1, pol_first);
                 }
             }
+            if (tid == 64) {
+                // the next LUT group (or the next chunk's first) into L2 while this group is read
+                const uint32_t npair = (g + 1 < a.ng) ? pair : (has_next ? ch.next / upp : pair);
+                const uint32_t ng1 = (g + 1 < a.ng) ? g + 1 : 0u;
+                if (g + 1 < a.ng || has_next) {
+                    const uint8_t* src = reinterpret_cast<const uint8_t*>(a.lut + (uint64_t(npair) * a.ng + ng1) * a.R * kGS);
+                    for (uint32_t off = 0; off < grp_bytes; off += 32768u)
+                        prefetch_l2_hint(src + off, min(32768u, grp_bytes - off), pol_last);
+                }
+            }
             if (g + 1 == a.ng) {  // the value rows: the first two slabs into shared memory (or L2) ahead of the value phase
                 if (a.vslab) {
                     if (tid == 0) {
