@@ -5,6 +5,7 @@
 //   2 LDS.128 conflict-free rotated gather (8 lanes of a quarter-warp hit 8 distinct 16 B groups)
 //   3 LDS.64 conflict-free rotated gather (16 lanes of a half-warp hit 16 distinct 8 B groups)
 //   4 LDS.32 random
+//   5 ATOMS.ADD u64, random bins (two heads' fixed-point weights packed in one 64-bit word)
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o smem_rates smem_rates.cu
 #include <cstdint>
 #include <cstdio>
@@ -28,7 +29,8 @@ __global__ void k(int iters, uint32_t* out, long long* clk) {
     else if (mode == 1) ad[u] = base + 4u * (c * 32u + lane);
     else if (mode == 2) ad[u] = base + ((c * 2u) << 7) + ((((lane & 7u) ^ u)) << 4);
     else if (mode == 3) ad[u] = base + ((c * 2u) << 7) + ((((lane & 15u) ^ u)) << 3);
-    else ad[u] = base + 4u * ((x >> 3) & 32767u);
+    else if (mode == 4) ad[u] = base + 4u * ((x >> 3) & 32767u);
+    else ad[u] = base + 8u * ((u & 3u) * 512u + c);
   }
   long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
@@ -38,6 +40,8 @@ __global__ void k(int iters, uint32_t* out, long long* clk) {
       const uint32_t a = ad[u] ^ flip;
       if (mode <= 1) {
         asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(x) : "memory");
+      } else if (mode == 5) {
+        asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(a), "l"((unsigned long long)x) : "memory");
       } else if (mode == 2) {
         uint32_t a0, a1, a2, a3;
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "r"(a));
@@ -63,9 +67,9 @@ int main() {
   cudaMalloc(&out, 4096 * 4); cudaMalloc(&clk, 4096 * 8);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const char* names[] = {"ATOMS u32 random bins", "ATOMS u32 conflict-free", "LDS.128 rotated", "LDS.64 rotated",
-                         "LDS.32 random"};
-  void (*fn[5])(int, uint32_t*, long long*) = {k<0>, k<1>, k<2>, k<3>, k<4>};
-  for (int mode = 0; mode < 5; ++mode) {
+                         "LDS.32 random", "ATOMS u64 random bins"};
+  void (*fn[6])(int, uint32_t*, long long*) = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>};
+  for (int mode : {5, 0, 1, 2, 3, 4}) {
     cudaFuncSetAttribute(fn[mode], cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
     for (int thr : {256, 512, 1024}) {
       const int iters = 4000;

@@ -66,4 +66,5 @@ def test_no_contracted_packed_fma_in_exact_kernels(unit):
     # squares (both multiplicands one register pair), and the count caps them.
     bad = [src for src, sq in ffma2 if src != ("tc_ptx.cuh", lines["fma2"]) and not sq]
     assert not bad, f"{len(bad)} FFMA2 not written as ptx::fma2 (contracted mul2+add2?): {bad[:4]}"
-    assert len(ffma2) <= (64 if unit == "encode_tc" else 0), f"{len(ffma2)} FFMA2 in {unit}"
+    # encode_tc holds two kernels (CTA-pair and single-CTA), 64 window-bound squares each
+    assert len(ffma2) <= (128 if unit == "encode_tc" else 0), f"{len(ffma2)} FFMA2 in {unit}"
