@@ -250,3 +250,35 @@ def test_tc_encode_many_stages(torch_mod):
     pay, nrm = run_tc(torch_mod, p, xs)
     mism, ties = compare(o, p, xs, pay, nrm)
     assert mism == 0
+
+
+@pytest.mark.parametrize(
+    "seed,n,S,rows,streams",
+    [(301, 4, 1024, 1000, 3), (302, 3, 384, 130, 5), (303, 2, 4096, 257, 2), (304, 6, 200, 64, 1),
+     (305, 16, 512, 2000, 9)],
+)
+def test_cta_pair_kernel_matches_single_cta_kernel(torch_mod, monkeypatch, seed, n, S, rows, streams):
+    """The CTA-pair encoder (cta_group::2, default) and the single-CTA kernel (VQKV_ENC_PAIR=0) give
+    identical payloads, norms and final residuals, including tile counts that leave a pair tile or
+    a whole quad partly empty, and rows on the exact path (non-finite input)."""
+    rng = O.Rng(seed)
+    o = rng.stack(n, S, 128)
+    p = product_stack(o)
+    xs = rng.matrix(rows * streams, 128)
+    xs[3, 7] = np.nan
+    xs[rows * streams - 1, 0] = np.inf
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("VQKV_ENC_PAIR", mode)
+        outs[mode] = run_tc(torch_mod, p, xs, n_streams=streams, residuals=True)
+    for a, b in zip(outs["1"], outs["0"]):
+        assert a.shape == b.shape
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+    # and the pair kernel against the oracle on the first stream (finite rows bit-exact; the
+    # non-finite row's norm is NaN on both sides, with a different NaN payload)
+    ref_pay, ref_norm = o.quantize_batch(xs[:rows])
+    got_codes, ref_codes = o.unpack(outs["1"][0][0], rows), o.unpack(ref_pay, rows)
+    fin = np.isfinite(xs[:rows]).all(1)
+    assert np.array_equal(got_codes[fin], ref_codes[fin])
+    assert np.array_equal(outs["1"][1][0][fin].view(np.uint32), ref_norm[fin].view(np.uint32))
+    assert np.array_equal(np.isnan(outs["1"][1][0][~fin]), np.isnan(ref_norm[~fin]))
