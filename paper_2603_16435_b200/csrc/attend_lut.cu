@@ -55,6 +55,7 @@
 // independent of how flat or peaked the attention is (no absolute cut).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "tc_ptx.cuh"
@@ -314,6 +315,149 @@ __global__ void __launch_bounds__(160) lut_tc_kernel(const __half* __restrict__ 
                                            v[c4][4 * pp + 3] * sc.w));
                     }
                 }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc(tmem, 256);
+}
+
+// Persistent, query-tile stationary LUT GEMM (the default; lut_tc_kernel above is the per-chunk
+// version).  CTA = (query tile tq, replica r of cpq): it keeps its 128 (pair, g) query rows (Q_hi /
+// Q_lo, 64 KB) in shared memory and streams the key chunks (s, c) = items r, r + cpq, ... through a
+// two-slot ring (E_hi / E_lo, 64 KB per slot) by bulk copy; 24 MMAs per item into one of two TMEM
+// accumulators while warps 0-3 drain the other.  One wave over the SMs instead of one CTA per
+// (stage, chunk), and the query tile is read once per CTA instead of once per chunk.
+constexpr uint32_t kLutTc2Smem = 6 * 32768 + 1024;
+constexpr uint32_t kLutTc2MaxStages = 128;
+// (register budget for 3 x 192 threads: leaves room for a raw-row CTA of the side stream on the SM)
+__global__ void __launch_bounds__(192, 3) lut_tc2_kernel(const __half* __restrict__ eff16, const __half* __restrict__ eff16lo,
+                                                          const StageInfo* __restrict__ kst, uint32_t n_stages,
+                                                          const __half* __restrict__ qhi, const __half* __restrict__ qlo,
+                                                          const float* __restrict__ qscl, uint32_t n_pairs, uint32_t cpq,
+                                                          uint32_t ng, uint32_t R, float4* __restrict__ lut) {
+    extern __shared__ uint8_t lsm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(lsm_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar_q, e_full[2], e_empty[2], acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_base;
+    __shared__ uint32_t pre[kLutTc2MaxStages + 1];  // chunk prefix over the stages
+    __shared__ __align__(16) float sc_s[128];        // the query tile's row scales
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tq = blockIdx.x / cpq, rep = blockIdx.x % cpq;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(ptx::smem_u32(&bar_q), 1);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(ptx::smem_u32(&e_full[b]), 1);
+            ptx::mbar_init(ptx::smem_u32(&e_empty[b]), 1);
+            ptx::mbar_init(ptx::smem_u32(&acc_full[b]), 1);
+            ptx::mbar_init(ptx::smem_u32(&acc_empty[b]), 128);
+        }
+        ptx::fence_mbar_init();
+        uint32_t acc = 0;
+        for (uint32_t st = 0; st < n_stages; ++st) {
+            pre[st] = acc;
+            acc += (kst[st].size + 127u) / 128u;
+        }
+        pre[n_stages] = acc;
+    }
+    if (threadIdx.x < 128) sc_s[threadIdx.x] = qscl[uint64_t(tq) * 128 + threadIdx.x];
+    if (warp == 0) {
+        ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 256);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t n_items = pre[n_stages];
+    const uint32_t s_q = ptx::smem_u32(sm);  // Q_hi, Q_lo at + 32 KB
+    auto s_e = [&](uint32_t b) { return s_q + 65536u + b * 65536u; };  // E_hi, E_lo at + 32 KB
+    // item -> (stage, chunk): the stage whose chunk range holds it
+    auto item_sc = [&](uint32_t it, uint32_t& st, uint32_t& c) {
+        uint32_t lo = 0, hi = n_stages - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (pre[mid] <= it) lo = mid; else hi = mid - 1;
+        }
+        st = lo;
+        c = it - pre[lo];
+    };
+    if (warp == 4) {
+        if (lane == 0) {  // producer: the query tile once, then the key chunks
+            ptx::mbar_arrive_expect_tx(ptx::smem_u32(&bar_q), 65536);
+            ptx::bulk_g2s(s_q, qhi + uint64_t(tq) * 16384, 32768, ptx::smem_u32(&bar_q));
+            ptx::bulk_g2s(s_q + 32768, qlo + uint64_t(tq) * 16384, 32768, ptx::smem_u32(&bar_q));
+            uint32_t k = 0;
+            for (uint32_t it = rep; it < n_items; it += cpq, ++k) {
+                const uint32_t b = k & 1u, u = k >> 1;
+                ptx::mbar_wait(ptx::smem_u32(&e_empty[b]), (u & 1u) ^ 1u);
+                uint32_t st, c;
+                item_sc(it, st, c);
+                const uint64_t eo = kst[st].eff16_off + uint64_t(c) * 18432;
+                ptx::mbar_arrive_expect_tx(ptx::smem_u32(&e_full[b]), 65536);
+                ptx::bulk_g2s(s_e(b), eff16 + eo, 32768, ptx::smem_u32(&e_full[b]));
+                ptx::bulk_g2s(s_e(b) + 32768, eff16lo + eo, 32768, ptx::smem_u32(&e_full[b]));
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {  // MMA issuer
+            constexpr uint32_t idesc = ptx::idesc_f16_f32(128, 128);
+            ptx::mbar_wait(ptx::smem_u32(&bar_q), 0);
+            uint32_t k = 0;
+            for (uint32_t it = rep; it < n_items; it += cpq, ++k) {
+                const uint32_t b = k & 1u, u = k >> 1;
+                ptx::mbar_wait(ptx::smem_u32(&e_full[b]), u & 1u);
+                ptx::mbar_wait(ptx::smem_u32(&acc_empty[b]), (u & 1u) ^ 1u);
+                ptx::tc_fence_after();
+                const uint32_t eh = s_e(b), el = eh + 32768, qh = s_q, ql = s_q + 32768;
+                const uint32_t A[3] = {eh, el, eh}, B[3] = {ql, qh, qh};  // small terms first
+#pragma unroll
+                for (int part = 0; part < 3; ++part)
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint32_t koff = (kk >> 2) * 16384 + (kk & 3) * 32;
+                        ptx::mma_f16_ss(tmem + 128u * b, ptx::umma_desc_sw128(A[part] + koff),
+                                        ptx::umma_desc_sw128(B[part] + koff), idesc, (part | kk) ? 1u : 0u);
+                    }
+                ptx::mma_commit(ptx::smem_u32(&acc_full[b]));
+                ptx::mma_commit(ptx::smem_u32(&e_empty[b]));
+            }
+        }
+    } else {
+        // epilogue: thread = entry row of the chunk = TMEM lane; 32 pairs' float4 per item
+        uint32_t k = 0;
+        for (uint32_t it = rep; it < n_items; it += cpq, ++k) {
+            const uint32_t b = k & 1u, u = k >> 1;
+            uint32_t st, c;
+            item_sc(it, st, c);
+            const uint32_t size = kst[st].size, j = c * 128u + warp * 32u + lane;
+            ptx::mbar_wait(ptx::smem_u32(&acc_full[b]), u & 1u);
+            ptx::tc_fence_after();
+            // two halves of 64 columns (16 pairs each): fewer live registers
+#pragma unroll 1
+            for (int hh = 0; hh < 2; ++hh) {
+                float v[2][32];
+#pragma unroll
+                for (int c4 = 0; c4 < 2; ++c4)
+                    ptx::tmem_ld32(tmem + ((warp * 32u) << 16) + 128u * b + 64u * hh + 32u * c4, v[c4]);
+                ptx::tc_wait_ld();
+                if (hh == 1) {
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(ptx::smem_u32(&acc_empty[b]));
+                }
+#pragma unroll
+                for (int c4 = 0; c4 < 2; ++c4)
+#pragma unroll
+                    for (int pp = 0; pp < 8; ++pp) {
+                        const uint32_t pair = tq * 32 + (2 * hh + c4) * 8 + pp;
+                        if (j < size && pair < n_pairs) {
+                            const float4 sc = reinterpret_cast<const float4*>(sc_s)[(2 * hh + c4) * 8 + pp];
+                            lut[lut_off(pair, ng, R, st, j)] =
+                                make_float4(v[c4][4 * pp] * sc.x, v[c4][4 * pp + 1] * sc.y, v[c4][4 * pp + 2] * sc.z,
+                                            v[c4][4 * pp + 3] * sc.w);
+                        }
+                    }
+            }
         }
     }
     ptx::tc_fence_before();
@@ -1591,6 +1735,9 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         const uint32_t n_raw = uint32_t(a.n_init + a.n_local);
         const int rsmem = int(sizeof(float) * (64 + kG * kD + 4 * kG * kD + uint64_t(n_raw) * kG));
         VQKV_CUDA(cudaFuncSetAttribute(attend_raw_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem));
+        // the largest shared-memory carveout: an SM running raw-row CTAs can take a LUT-build CTA beside
+        // them (the carveout of an SM only changes when it is idle)
+        VQKV_CUDA(cudaFuncSetAttribute(attend_raw_rows_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attend_raw_rows_kernel<<<a.n_pairs, kThreads, rsmem, side>>>(ra);
         launch_check("attend_raw_rows_kernel");
     }
@@ -1609,12 +1756,22 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
             VQKV_CUDA(cudaMallocAsync(&qs, sizeof(float) * rows_pad, s));
             q_prep_kernel<<<rows_pad / 8, 256, 0, s>>>(a.q_dev, rows, rows_pad, float(scale), qh, ql, qs);
             launch_check("q_prep_kernel");
-            VQKV_CUDA(cudaFuncSetAttribute(lut_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLutTcSmem)));
-            uint32_t maxch = 0;
-            for (const auto& st : ks.stages) maxch = std::max(maxch, (st.size + 127) / 128);
-            lut_tc_kernel<<<dim3(maxch, ks.n), 160, kLutTcSmem, s>>>(ks.d_eff16, ks.d_eff16lo, ks.d_stages, qh, ql, qs,
-                                                                    a.n_pairs, qt, ng, R, lut);
-            launch_check("lut_tc_kernel");
+            const char* lv = getenv("VQKV_LUT_TC1");  // dev A/B: the per-chunk kernel
+            if (ks.n <= kLutTc2MaxStages && !(lv && lv[0] == '1')) {
+                const uint32_t cpq = std::max<uint32_t>(1u, uint32_t(sms) / qt);
+                VQKV_CUDA(cudaFuncSetAttribute(lut_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               int(kLutTc2Smem)));
+                lut_tc2_kernel<<<qt * cpq, 192, kLutTc2Smem, s>>>(ks.d_eff16, ks.d_eff16lo, ks.d_stages, ks.n, qh, ql,
+                                                                  qs, a.n_pairs, cpq, ng, R, lut);
+                launch_check("lut_tc2_kernel");
+            } else {
+                VQKV_CUDA(cudaFuncSetAttribute(lut_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLutTcSmem)));
+                uint32_t maxch = 0;
+                for (const auto& st : ks.stages) maxch = std::max(maxch, (st.size + 127) / 128);
+                lut_tc_kernel<<<dim3(maxch, ks.n), 160, kLutTcSmem, s>>>(ks.d_eff16, ks.d_eff16lo, ks.d_stages, qh, ql,
+                                                                        qs, a.n_pairs, qt, ng, R, lut);
+                launch_check("lut_tc_kernel");
+            }
             VQKV_CUDA(cudaFreeAsync(qh, s));
             VQKV_CUDA(cudaFreeAsync(ql, s));
             VQKV_CUDA(cudaFreeAsync(qs, s));
