@@ -281,9 +281,11 @@ int vqkv_encode_counters(vqkv_stack_t stack, uint64_t* counters3);
  * [6] rescoring loads + dot products, [7] rescoring min-reduction, [8] code
  * store, then inside the update: [9] e_z loads issued + first residual TMEM
  * load, [10] wait for the e_z gather, [11] rest of the update, ([4] is the
- * final store-wait + arrive); [13] the number of rescored (row, candidate)
- * pairs.  Synchronizes. */
-int vqkv_encode_phase_clocks(vqkv_stack_t stack, uint64_t* out14);
+ * final store-wait + arrive), [12] accumulator loads; [13] the number of
+ * rescored (row, candidate) pairs; MMA-issuer thread totals: [14] waits for
+ * a free accumulator, [15] MMA + commit issue, [16] waits for the chunk,
+ * [17] waits for the A tile.  Synchronizes. */
+int vqkv_encode_phase_clocks(vqkv_stack_t stack, uint64_t* out18);
 /* number of kernel launches issued by the library since load (all threads) */
 uint64_t vqkv_launch_count(void);
 /* Kernel timing hooks: when enabled, the library records a CUDA event pair on

@@ -332,15 +332,25 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
             // K-block stride of the B operand in shared memory: 64 or 128 entry rows of 128 B
             constexpr uint32_t kBkb = kPair ? 8192u : 16384u;
             constexpr uint32_t kBext = kPair ? 16384u : kExtOff;
+#ifdef VQKV_PHASE_CLOCKS
+            unsigned long long mk[4] = {0, 0, 0, 0};
+            long long m0 = clock64(), m1;
+#define VQKV_MCLK(k) { m1 = clock64(); mk[k] += (unsigned long long)(m1 - m0); m0 = m1; }
+#else
+#define VQKV_MCLK(k) {}
+#endif
             while (!it.done) {
                 // (pair kernel: the peer's arrivals use default .cta semantics, as in CUTLASS's 2-SM
                 // pipelines; the data they hand over is ordered by tcgen05 / proxy fences)
                 ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->b_full[t][slot]), ph, kSleepNs);
+                VQKV_MCLK(2)
                 if (it.c == 0) {
                     ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->a_ready[t]), a_ph, kSleepNs);
                     a_ph ^= 1;
                 }
+                VQKV_MCLK(3)
                 ptx::mbar_wait_sleep(ptx::smem_u32(&ctl->acc_empty[t]), e_ph, kSleepNs);
+                VQKV_MCLK(0)
                 const uint32_t bb = b_base + (t * NB + slot) * kSlot;
                 e_ph ^= 1;
                 ptx::tc_fence_after();
@@ -371,12 +381,18 @@ encode_tc_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, const 
                     ptx::mma_commit(ptx::smem_u32(&ctl->acc_full[t]));
                     ptx::mma_commit(ptx::smem_u32(&ctl->b_empty[t][slot]));
                 }
+                VQKV_MCLK(1)
                 if (++slot == NB) {
                     slot = 0;
                     ph ^= 1;
                 }
                 it.next();
             }
+#ifdef VQKV_PHASE_CLOCKS
+            if ((dbg & 2u) && counters)
+                for (int k = 0; k < 4; ++k) atomicAdd(&counters[21 + k], mk[k]);
+#endif
+#undef VQKV_MCLK
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ epilogue

@@ -416,6 +416,7 @@ int vqkv_encode_phase_clocks(vqkv_stack_t s, uint64_t* c) {
         VQKV_CUDA(cudaMemcpy(h, s->d_counters, sizeof(h), cudaMemcpyDeviceToHost));
         for (int i = 0; i < 13; ++i) c[i] = h[8 + i];
         c[13] = h[3];
+        for (int i = 0; i < 4; ++i) c[14 + i] = h[21 + i];
     });
 }
 

@@ -14,13 +14,13 @@ st = P.CodebookStack.from_arrays([g.standard_normal((S, 128), dtype=np.float32) 
 x = torch.randn(streams, 31740, 128, device='cuda')
 Dv.quantize_streams(st, x); torch.cuda.synchronize()
 L = _lib.load()
-base = (ctypes.c_uint64 * 14)()
+base = (ctypes.c_uint64 * 18)()
 L.vqkv_encode_phase_clocks(Dv._dev(st).h, base)
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record(); Dv.quantize_streams(st, x); e.record(); torch.cuda.synchronize()
-out = (ctypes.c_uint64 * 14)()
+out = (ctypes.c_uint64 * 18)()
 L.vqkv_encode_phase_clocks(Dv._dev(st).h, out)
-d = [out[k] - base[k] for k in range(14)]
+d = [out[k] - base[k] for k in range(18)]
 warps = 8 * 148
 ms = s.elapsed_time(e)
 print(f"n={n} S={S} streams={streams}: {ms:.2f} ms  (~{ms*1.9e6:.3g} clk per warp at 1.9 GHz)")
@@ -29,3 +29,6 @@ tot = sum(d[:13])
 for k in range(13):
     print(f"  {names[k]:13s} {d[k]/warps:12.4g} clk/warp  {100*d[k]/tot:5.1f}%")
 print("  rescored pairs", d[13])
+mma_threads = 2 * 148 if os.environ.get("VQKV_ENC_PAIR", "1") == "0" else 2 * 74  # leader MMA-issuer threads
+print("  MMA issuer (clk per thread, leader threads only): acc-free wait %.4g, issue %.4g, chunk wait %.4g, A-tile wait %.4g"
+      % tuple(d[14 + k] / mma_threads for k in range(4)))
