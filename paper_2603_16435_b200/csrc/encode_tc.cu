@@ -928,6 +928,7 @@ void launch_encode_tc(const vqkv_stack_s& st, const float* xs, uint32_t n_stream
     const uint32_t rb = uint32_t(st.row_bits / 8);
     {
     ProfScope ps("encode_tc", s);
+    bool launched = false;
     if (encode_pair_mode()) {
         // clusters of two CTAs on an SM pair, 4 tiles in flight per cluster
         const uint64_t quads = (tiles + 3) / 4;
@@ -946,11 +947,20 @@ void launch_encode_tc(const vqkv_stack_s& st, const float* xs, uint32_t n_stream
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        VQKV_CUDA(cudaLaunchKernelEx(&cfg, encode_tc_kernel<true>, (const StageInfo*)st.d_stages, st.n,
-                                     (const __half*)st.d_eff16, (const float*)st.d_sqn_pad, (const float*)st.d_eff, xs,
-                                     n_streams, rows, search_block, codes, norms, residuals, list + 1, list,
-                                     st.d_counters, dbg_flags(), pay, pb, rb));
-    } else {
+        const cudaError_t le = cudaLaunchKernelEx(&cfg, encode_tc_kernel<true>, (const StageInfo*)st.d_stages, st.n,
+                                                  (const __half*)st.d_eff16, (const float*)st.d_sqn_pad,
+                                                  (const float*)st.d_eff, xs, n_streams, rows, search_block, codes,
+                                                  norms, residuals, list + 1, list, st.d_counters, dbg_flags(), pay, pb,
+                                                  rb);
+        if (le == cudaSuccess) {
+            launched = true;
+        } else {
+            // a context that cannot place SM-pair clusters (e.g. a partitioned GPU): the single-CTA
+            // tensor-core kernel computes the same codes
+            (void)cudaGetLastError();
+        }
+    }
+    if (!launched) {
         const uint64_t pairs = (tiles + 1) / 2;
         const unsigned grid = unsigned(std::min<uint64_t>(pairs, uint64_t(sms)));
         // per launch: the attribute is per device, and the call is cheap (no static flag to race on)
