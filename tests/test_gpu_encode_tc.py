@@ -255,7 +255,7 @@ def test_tc_encode_many_stages(torch_mod):
 @pytest.mark.parametrize(
     "seed,n,S,rows,streams",
     [(301, 4, 1024, 1000, 3), (302, 3, 384, 130, 5), (303, 2, 4096, 257, 2), (304, 6, 200, 64, 1),
-     (305, 16, 512, 2000, 9)],
+     (305, 16, 512, 2000, 9), (306, 2, 256, 8, 7), (307, 3, 128, 512, 4)],
 )
 def test_cta_pair_kernel_matches_single_cta_kernel(torch_mod, monkeypatch, seed, n, S, rows, streams):
     """The CTA-pair encoder (cta_group::2, default) and the single-CTA kernel (VQKV_ENC_PAIR=0) give
