@@ -988,12 +988,16 @@ __device__ __noinline__ void segment_contract(const float* __restrict__ veff, ui
     for (int g = 0; g < kG; ++g) o[g][0] = o[g][1] = o[g][2] = o[g][3] = 0.f;
     const float4* e4 = reinterpret_cast<const float4*>(veff) + lane;
     uint32_t j = j0;
-    for (; j + 4u <= j1; j += 4u) {
-        float4 x[4];
+#ifndef VQKV_CONTRACT_MLP
+#define VQKV_CONTRACT_MLP 16
+#endif
+    constexpr uint32_t kM = VQKV_CONTRACT_MLP;  // codebook rows in flight per warp
+    for (; j + kM <= j1; j += kM) {
+        float4 x[kM];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) x[i] = __ldg(e4 + uint64_t(j + i) * (kD / 4));
+        for (int i = 0; i < int(kM); ++i) x[i] = __ldg(e4 + uint64_t(j + i) * (kD / 4));
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < int(kM); ++i) {
             const float4 w = acc4[j + i];
             const float wg[kG] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -1351,12 +1355,16 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
                     if (lanes_e == 16u) {
                         // two entries per step (lanes 0-15 / 16-31), four steps in flight, no branches
                         const uint32_t sub = lane >> 4;
-                        for (uint32_t i0 = 0; i0 < n; i0 += 8u) {
-                            uint32_t addr[4], pv[4];
-                            uint64_t lw[4], hw[4];
-                            uint32_t sh[4];
+#ifndef VQKV_VAL_STEPS
+#define VQKV_VAL_STEPS 4
+#endif
+                        constexpr int kU = VQKV_VAL_STEPS;  // steps (entry pairs) in flight
+                        for (uint32_t i0 = 0; i0 < n; i0 += 2u * kU) {
+                            uint32_t addr[kU], pv[kU];
+                            uint64_t lw[kU], hw[kU];
+                            uint32_t sh[kU];
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) {
+                            for (int u = 0; u < kU; ++u) {
                                 const uint32_t i = i0 + 2u * uint32_t(u) + sub;
                                 const uint2 e = queue[b0 + min(i, n - 1u)];
                                 const uint32_t lt = e.x & 0xFFFFu, g = e.x >> 16;
@@ -1369,7 +1377,7 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
                                 pv[u] = (i < n && s_on) ? e.y : 0u;  // padding steps add nothing
                             }
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) {
+                            for (int u = 0; u < kU; ++u) {
                                 const uint32_t z = uint32_t(sh[u] ? ((lw[u] >> sh[u]) | (hw[u] << (64u - sh[u]))) : lw[u]) & s_mask;
                                 red_shared_add(addr[u] + z * 4u, pv[u]);
                             }
