@@ -695,41 +695,64 @@ __global__ void __launch_bounds__(kThreads) attend_raw_rows_kernel(RawArgs a) {
         }
     }
     __syncthreads();
-    // o[g][d] = sum_r p[r][g] v_r[d]: thread = (row group rg, d) over rows rg, rg + 4, ...;
-    // each value load feeds the 4 heads, kRowBatch loads in flight
+    // o[g][d] = sum_r p[r][g] v_r[d]: warp = row stream (rows warp, warp + 16, ...), lane = 4 columns:
+    // one coalesced 512 B row per warp-load, kRowBatch rows in flight per warp, each value feeding the
+    // 4 heads; the 16 streams' partials are summed in a fixed order (4 rounds into 4 smem slices)
     {
-        const uint32_t d = threadIdx.x % kD, rg = threadIdx.x / kD, nrg = blockDim.x / kD;
-        const float* iv = a.init_v + uint64_t(pair) * a.init_stride * kD + d;
-        const float* lv = a.local_v + uint64_t(pair) * a.local_stride * kD + d;
+        const float4* iv = reinterpret_cast<const float4*>(a.init_v + uint64_t(pair) * a.init_stride * kD) + lane;
+        const float4* lv = reinterpret_cast<const float4*>(a.local_v + uint64_t(pair) * a.local_stride * kD) + lane;
         const float4* p4 = reinterpret_cast<const float4*>(ls);
-        float acc[kG] = {0.f, 0.f, 0.f, 0.f};
-        for (uint32_t r0 = rg; r0 < n_raw; r0 += nrg * kRowBatch) {
-            float x[kRowBatch];
+        float4 acc[kG];
+#pragma unroll
+        for (int g = 0; g < kG; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (uint32_t r0 = warp; r0 < n_raw; r0 += nw * kRowBatch) {
+            float4 x[kRowBatch];
 #pragma unroll
             for (int u = 0; u < kRowBatch; ++u) {
-                const uint32_t r = r0 + u * nrg;
-                x[u] = (r >= n_raw) ? 0.f : (r < a.n_init) ? __ldg(iv + uint64_t(r) * kD) : __ldg(lv + uint64_t(r - a.n_init) * kD);
+                const uint32_t r = r0 + u * nw;
+                x[u] = (r >= n_raw) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                    : (r < a.n_init) ? __ldg(iv + uint64_t(r) * (kD / 4))
+                                                     : __ldg(lv + uint64_t(r - a.n_init) * (kD / 4));
             }
 #pragma unroll
             for (int u = 0; u < kRowBatch; ++u) {
-                const uint32_t r = r0 + u * nrg;
+                const uint32_t r = r0 + u * nw;
                 if (r < n_raw) {
                     const float4 p = p4[r];
-                    acc[0] = fmaf(p.x, x[u], acc[0]);
-                    acc[1] = fmaf(p.y, x[u], acc[1]);
-                    acc[2] = fmaf(p.z, x[u], acc[2]);
-                    acc[3] = fmaf(p.w, x[u], acc[3]);
+                    const float pw[kG] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+                    for (int g = 0; g < kG; ++g) {
+                        acc[g].x = fmaf(pw[g], x[u].x, acc[g].x);
+                        acc[g].y = fmaf(pw[g], x[u].y, acc[g].y);
+                        acc[g].z = fmaf(pw[g], x[u].z, acc[g].z);
+                        acc[g].w = fmaf(pw[g], x[u].w, acc[g].w);
+                    }
                 }
             }
         }
+        // streams 4k .. 4k + 3 in round k add into slice (warp & 3)
+        float4* po4 = reinterpret_cast<float4*>(po);
+        for (uint32_t k = 0; k < nw / 4u; ++k) {
+            if (warp / 4u == k) {
 #pragma unroll
-        for (int g = 0; g < kG; ++g) po[(rg * kG + g) * kD + d] = acc[g];
+                for (int g = 0; g < kG; ++g) {
+                    float4& o = po4[((warp & 3u) * kG + g) * (kD / 4) + lane];
+                    if (k == 0) {
+                        o = acc[g];
+                    } else {
+                        o.x += acc[g].x;
+                        o.y += acc[g].y;
+                        o.z += acc[g].z;
+                        o.w += acc[g].w;
+                    }
+                }
+            }
+            __syncthreads();
+        }
     }
-    __syncthreads();
-    const uint32_t nrg = blockDim.x / kD;
     for (uint32_t gd = threadIdx.x; gd < kG * kD; gd += blockDim.x) {
         float o = 0.f;
-        for (uint32_t rg = 0; rg < nrg; ++rg) o += po[rg * kG * kD + gd];
+        for (uint32_t rg = 0; rg < 4u; ++rg) o += po[rg * kG * kD + gd];
         a.part_o[uint64_t(slot) * kG * kD + gd] = o;
     }
 }
@@ -750,8 +773,8 @@ struct MainArgs {
     const StageInfo* vst;
     uint32_t vn;
     uint32_t vnwin;          // 64-bit windows of the value row (stages grouped, <= 64 bits each)
-    const uint2* vwin;       // [vnwin]: (start bit, s0 | s1 << 8)
-    const uint8_t* vwin_of;  // [vn]: window of each stage
+    uint2 vwin[16];          // [vnwin]: (start bit, s0 | s1 << 8) -- kernel parameters, no per-call copy
+    uint8_t vwin_of[kMaxVStages];  // [vn]: window of each stage
     uint32_t vtotal;         // sum S_v (<= kHistStride): histogram entries per head
     uint32_t vslab;          // value rows staged in shared memory per slab (row_bits <= kMaxSlabRowBits)
     const float* veff;
@@ -1708,10 +1731,6 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         }
     }
     float4* lut = nullptr;
-    uint8_t* vtab = nullptr;  // value windows + stage -> window
-    VQKV_CUDA(cudaMallocAsync(&vtab, sizeof(uint2) * 16 + 64, s));
-    VQKV_CUDA(cudaMemcpyAsync(vtab, wins.data(), sizeof(uint2) * wins.size(), cudaMemcpyHostToDevice, s));
-    VQKV_CUDA(cudaMemcpyAsync(vtab + sizeof(uint2) * 16, win_of.data(), win_of.size(), cudaMemcpyHostToDevice, s));
     float *po = nullptr, *pm = nullptr, *pl = nullptr;
     VQKV_CUDA(cudaMallocAsync(&po, sizeof(float) * n_slots * kG * kD, s));
     VQKV_CUDA(cudaMallocAsync(&pm, sizeof(float) * n_slots * kG, s));
@@ -1815,8 +1834,8 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         ma.vst = vs.d_stages;
         ma.vn = vs.n;
         ma.vnwin = uint32_t(wins.size());
-        ma.vwin = reinterpret_cast<const uint2*>(vtab);
-        ma.vwin_of = vtab + sizeof(uint2) * 16;
+        for (size_t w = 0; w < wins.size() && w < 16; ++w) ma.vwin[w] = wins[w];
+        for (size_t st = 0; st < win_of.size() && st < kMaxVStages; ++st) ma.vwin_of[st] = win_of[st];
         ma.vtotal = uint32_t(vs.total_rows);
         ma.vslab = vs.row_bits <= kMaxSlabRowBits ? 1u : 0u;
         ma.veff = vs.d_eff;
@@ -1842,7 +1861,6 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     cudaEventDestroy(ev_join);
     if (lut) VQKV_CUDA(cudaFreeAsync(lut, s));
     if (ktmp) VQKV_CUDA(cudaFreeAsync(ktmp, s));
-    VQKV_CUDA(cudaFreeAsync(vtab, s));
     VQKV_CUDA(cudaFreeAsync(po, s));
     VQKV_CUDA(cudaFreeAsync(pm, s));
     VQKV_CUDA(cudaFreeAsync(pl, s));
