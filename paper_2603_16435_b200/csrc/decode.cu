@@ -49,17 +49,21 @@ reconstruct_kernel(const StageInfo* __restrict__ stages, uint32_t n_stages, uint
             }
             const uint32_t cnt = (n_stages - s0 < 32) ? (n_stages - s0) : 32;
             if constexpr (kD128) {
-                // 8 stage rows in flight per warp, added strictly in stage order
-                for (uint32_t t0 = 0; t0 < cnt; t0 += 8) {
-                    float4 v[8];
+                // kFly stage rows in flight per warp, added strictly in stage order
+#ifndef VQKV_DEC_FLY
+#define VQKV_DEC_FLY 8
+#endif
+                constexpr int kFly = VQKV_DEC_FLY;
+                for (uint32_t t0 = 0; t0 < cnt; t0 += kFly) {
+                    float4 v[kFly];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
+                    for (int u = 0; u < kFly; ++u) {
                         const uint32_t off = __shfl_sync(0xffffffffu, my_off, (t0 + u) & 31u);
                         v[u] = (t0 + u < cnt) ? __ldg(reinterpret_cast<const float4*>(eff + off) + lane)
                                               : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
+                    for (int u = 0; u < kFly; ++u)
                         if (t0 + u < cnt) {
                             acc.x = __fadd_rn(acc.x, v[u].x);
                             acc.y = __fadd_rn(acc.y, v[u].y);
