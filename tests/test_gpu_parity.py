@@ -47,7 +47,11 @@ def test_stack_refresh_bit_exact(torch_mod, seed, n, S, D):
 
 
 @pytest.mark.parametrize("seed,n,S,D,rows", [(11, 3, 16, 8, 50), (12, 5, 300, 7, 33), (13, 2, 1024, 128, 300),
-                                              (14, 1, 1, 4, 5), (15, 8, 256, 128, 130)])
+                                              (14, 1, 1, 4, 5), (15, 8, 256, 128, 130),
+                                              # D = 128 with <= 32 stages (next-row code prefetch kernel),
+                                              # exactly 32, and 40 (general kernel)
+                                              (16, 16, 512, 128, 700), (17, 32, 100, 128, 90),
+                                              (18, 40, 64, 128, 77)])
 def test_reconstruct_block_bit_exact(torch_mod, seed, n, S, D, rows):
     """codebook.cpp:239-250 on random codes; every partition concatenates identically."""
     from paper_2603_16435_b200 import codebook as P
@@ -85,6 +89,12 @@ def test_reconstruct_errors(torch_mod):
     with pytest.raises(E.InvalidInput):
         P.reconstruct_block(p, good, 1, 0)
     assert P.reconstruct_block(p, good, 1, 1).shape == (0, 4)
+    # D = 128, few stages: the invalid code in the third row is reported, its neighbours decode
+    o2 = O.Rng(22).stack(3, 5, 128)
+    p2 = product_stack(o2)
+    bad = P.CodeMatrix.from_payload([5, 5, 5], np.array([0x00, 0x00, 0x00, 0x00, 0xFF, 0x01], np.uint8), 5)
+    with pytest.raises(E.InvalidCode):
+        P.reconstruct_block(p2, bad, 0, 5)
 
 
 def _encode_cases():
