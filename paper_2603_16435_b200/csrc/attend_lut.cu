@@ -554,11 +554,6 @@ __device__ __forceinline__ float2 add2v(float2 a, float2 b) {  // volatile: keep
 __device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
-__device__ __forceinline__ void red_shared_add_nz(uint32_t addr, uint32_t v) {  // predicated, no branch
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr), "r"(v)
-                 : "memory");
-}
-
 // Field K (0..7) of an 80-bit attention record (w0 = bits 0-31, w1 = 32-63, w2 = 64-79),
 // shifted so its 10 bits sit at bits 7-16 (the code's row offset, 128 B per code); the bits
 // below are the previous field's and are masked off by the caller.  One SHF each.
