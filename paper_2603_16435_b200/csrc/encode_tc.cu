@@ -71,6 +71,10 @@ constexpr uint32_t kIdesc = ptx::idesc_f16_f32(128, 128);
 constexpr uint32_t kIdescPair = ptx::idesc_f16_f32(256, 128);
 // register split: 128 x kCtlRegs + 256 x kEpiRegs <= 64K (launch allocation 168)
 constexpr uint32_t kCtlRegs = 56, kEpiRegs = 224;
+// setmaxnreg.inc blocks until the registers exist: what the control warpgroup releases plus the
+// register file's slack over the launch allocation (168 x 384) must cover the epilogue's increase
+static_assert((168u - kCtlRegs) * 128u + (65536u - 168u * kThreads) >= (kEpiRegs - 168u) * 256u,
+              "register hand-over would block");
 constexpr uint32_t kSleepNs = 1000000;  // control-thread barrier suspend hint
 
 struct __align__(8) SmemCtl {
