@@ -214,11 +214,50 @@ int attend_path() {
 bool attend_lut_supported(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a);
 void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s);
 
+// Group sizes other than the LUT kernel's 4 query heads per KV head: the heads run through the LUT
+// path in groups of 4 (the last group padded by repeating its last head), each from a compact
+// [pair][4][Dk] copy of its queries, the outputs copied back into [pair][group][Dv].  Each group
+// re-reads the codes, which still beats the generic per-token kernel by a wide margin.
+bool attend_lut_grouped(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s) {
+    constexpr uint32_t kLutG = 4;
+    if (a.group == kLutG || a.group == 0 || a.n_pairs == 0) return false;
+    vqkv_attend_args a4 = a;
+    a4.group = kLutG;
+    if (!attend_lut_supported(ks, vs, a4)) return false;
+    const uint32_t G = a.group, Dk = ks.dim, Dv = vs.dim, P = a.n_pairs;
+    float *q4 = nullptr, *o4 = nullptr, *l4 = nullptr;
+    VQKV_CUDA(cudaMallocAsync(&q4, sizeof(float) * P * kLutG * Dk, s));
+    VQKV_CUDA(cudaMallocAsync(&o4, sizeof(float) * P * kLutG * Dv, s));
+    VQKV_CUDA(cudaMallocAsync(&l4, sizeof(float) * P * kLutG, s));
+    for (uint32_t h0 = 0; h0 < G; h0 += kLutG) {
+        const uint32_t nh = std::min(kLutG, G - h0);
+        for (uint32_t j = 0; j < kLutG; ++j) {  // head h0 + j (the last one repeated as padding)
+            const uint32_t h = h0 + std::min(j, nh - 1);
+            VQKV_CUDA(cudaMemcpy2DAsync(q4 + j * Dk, sizeof(float) * kLutG * Dk, a.q_dev + size_t(h) * Dk,
+                                        sizeof(float) * G * Dk, sizeof(float) * Dk, P, cudaMemcpyDeviceToDevice, s));
+        }
+        a4.q_dev = q4;
+        a4.out_dev = o4;
+        a4.lse_dev = a.lse_dev ? l4 : nullptr;
+        launch_attend_lut(ks, vs, a4, s);
+        VQKV_CUDA(cudaMemcpy2DAsync(a.out_dev + size_t(h0) * Dv, sizeof(float) * G * Dv, o4, sizeof(float) * kLutG * Dv,
+                                    sizeof(float) * nh * Dv, P, cudaMemcpyDeviceToDevice, s));
+        if (a.lse_dev)
+            VQKV_CUDA(cudaMemcpy2DAsync(a.lse_dev + h0, sizeof(float) * G, l4, sizeof(float) * kLutG, sizeof(float) * nh, P,
+                                        cudaMemcpyDeviceToDevice, s));
+    }
+    VQKV_CUDA(cudaFreeAsync(q4, s));
+    VQKV_CUDA(cudaFreeAsync(o4, s));
+    VQKV_CUDA(cudaFreeAsync(l4, s));
+    return true;
+}
+
 void launch_attend(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s) {
     if (attend_path() != 1 && attend_lut_supported(ks, vs, a)) {
         launch_attend_lut(ks, vs, a, s);
         return;
     }
+    if (attend_path() != 1 && attend_lut_grouped(ks, vs, a, s)) return;
     const uint32_t Dk = ks.dim, Dv = vs.dim, G = a.group;
     const uint64_t L = a.n_init + a.n_comp + a.n_local;
     int sms = 148;

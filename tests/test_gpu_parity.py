@@ -270,6 +270,42 @@ def test_attention_lut_path_vs_oracle(torch_mod, nk, sk, nv, sv, n_pairs, n_init
     assert worst <= ATT_TOL
 
 
+@pytest.mark.parametrize("G", [1, 2, 3, 6, 8, 13])
+def test_attention_other_group_sizes_use_lut_path(torch_mod, monkeypatch, G):
+    """Group sizes other than 4 run through the LUT path in groups of 4 heads (the last one padded):
+    same results as the oracle and as the generic kernel (VQKV_ATTEND_PATH=1)."""
+    torch = torch_mod
+    from paper_2603_16435_b200 import device as Dv
+
+    nk, sk, nv, sv, n_pairs, n_init, n_comp, n_local = 56, 1024, 16, 512, 3, 4, 2500, 9
+    rng = O.Rng(900 + G)
+    ks = rng.stack(nk, sk, 128, O.KEY)
+    vs = rng.stack(nv, sv, 128, O.VALUE)
+    pk, pv = product_stack(ks), product_stack(vs)
+    mk = lambda n: rng.matrix(n_pairs * n, 128).reshape(n_pairs, n, 128)
+    init_k, init_v, loc_k, loc_v = mk(n_init), mk(n_init), mk(n_local), mk(n_local)
+    g = np.random.default_rng(G)
+    kc = np.stack([ks.pack(g.integers(0, sk, (n_comp, nk)).astype(np.uint32)) for _ in range(n_pairs)])
+    vc = np.stack([vs.pack(g.integers(0, sv, (n_comp, nv)).astype(np.uint32)) for _ in range(n_pairs)])
+    q = rng.matrix(n_pairs * G, 128).reshape(n_pairs, G, 128)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    run = lambda: [x.cpu().numpy() for x in Dv.attend_decode(pk, pv, t(q), t(kc), t(vc), n_comp, t(init_k), t(init_v),
+                                                             t(loc_k), t(loc_v))]
+    out, lse = run()
+    monkeypatch.setenv("VQKV_ATTEND_PATH", "1")
+    out_g, lse_g = run()
+    monkeypatch.delenv("VQKV_ATTEND_PATH")
+    assert out.shape == (n_pairs, G, 128) and lse.shape == (n_pairs, G)
+    assert np.abs(out - out_g).max() <= ATT_TOL * max(1.0, np.abs(out_g).max())
+    assert np.abs(lse - lse_g).max() <= 1e-3 * max(1.0, np.abs(lse_g).max())
+    for pi in range(n_pairs):
+        for gg in (0, G - 1):
+            ref, ref_lse = O.attend_segments(ks, vs, init_k[pi], init_v[pi], kc[pi], vc[pi], n_comp, loc_k[pi], loc_v[pi],
+                                             q[pi, gg])
+            assert np.abs(out[pi, gg] - ref).max() <= ATT_TOL * max(1.0, np.abs(ref).max())
+            assert abs(lse[pi, gg] - ref_lse) <= 1e-3 * max(1.0, abs(ref_lse))
+
+
 def gm_records_np(ks, codes, cap, t0=0):
     """The attention record layout (include/vqkv_c.h) built in numpy from unpacked codes: per
     group of 8 key stages, token t's 80-bit record holds in field k the code of stage
