@@ -1180,10 +1180,14 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
             const uint8_t* seg = krec + uint64_t(g) * a.cap * 10u;
             const uint2* rlo = reinterpret_cast<const uint2*>(seg);
             const uint16_t* rhi = reinterpret_cast<const uint16_t*>(seg + a.cap * 8u);
+            // re-derived per batch (an opaque copy of tok0): hoisted, the 16 clamped indices would be
+            // spilled and reloaded in the key loop
+            uint32_t t0v;
+            asm volatile("mov.u32 %0, %1;" : "=r"(t0v) : "r"(tok0));
 #pragma unroll
             for (int k = 0; k < kB; ++k) {
                 // tokens past the range read the last valid record (their logits are masked)
-                const uint32_t t = min(tok0 + uint32_t(kb + k) * kThreads, tlast);
+                const uint32_t t = min(t0v + uint32_t(kb + k) * kThreads, tlast);
                 wo[k] = ldg_stream_u2(rlo + t, pol_first);
                 ho[k] = ldg_stream_u16(rhi + t, pol_first);
             }
