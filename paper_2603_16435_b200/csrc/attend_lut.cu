@@ -752,9 +752,9 @@ __global__ void __launch_bounds__(kThreads) attend_raw_rows_kernel(RawArgs a) {
     }
 }
 
-// Compressed tokens.  The pairs' tokens are cut into 512-token units (pair-major); CTA b of the
-// persistent grid takes units [U b / n_cta, U (b + 1) / n_cta), i.e. a contiguous token range
-// that may span a pair boundary.  Its work is processed in chunks of up to 16 units of one
+// Compressed tokens.  The pairs' tokens are cut into 512-token units and those into chunks of 16
+// units per pair (pair-major; a pair's last chunk partial); CTA b of the persistent grid takes chunks
+// [C b / n_cta, C (b + 1) / n_cta), i.e. a contiguous token range that may span a pair boundary.  Its work is processed in chunks of up to 16 units of one
 // pair; a run of chunks of one pair is a segment, whose partial (o, m, l) goes to slot b + pair
 // (unique: CTA ranges are monotone in the pair).
 struct MainArgs {
@@ -776,7 +776,7 @@ struct MainArgs {
     uint64_t n_comp;
     uint32_t n_pairs;
     uint32_t units_per_pair; // ceil(n_comp / 512)
-    uint32_t n_cta;          // persistent CTAs (<= total units, so none is empty)
+    uint32_t n_cta;          // persistent CTAs (<= total chunks, so none is empty)
     float* part_o;           // [slots][G][D]: unnormalised sum p v
     float* part_m;           // [slots][G]
     float* part_l;           // [slots][G]
@@ -1108,8 +1108,17 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
     const uint32_t grp_bytes = a.R * kRowBytes;
     const uint32_t upp = a.units_per_pair;
     const uint32_t U = a.n_pairs * upp;  // units (< 2^32: checked at launch)
-    const uint32_t u_begin = uint32_t(uint64_t(U) * blockIdx.x / a.n_cta);
-    const uint32_t u_end = uint32_t(uint64_t(U) * (blockIdx.x + 1) / a.n_cta);
+    // CTA ranges are whole chunks (the pair-major chunk list: ceil(upp / 16) chunks per pair, the last
+    // one partial): a range cut inside a chunk would cost its CTA an extra chunk (all the LUT groups
+    // and per-chunk fixed work again for a few tokens)
+    const uint32_t cpp = (upp + kUnitsPerChunk - 1) / kUnitsPerChunk;
+    const uint32_t C = a.n_pairs * cpp;
+    auto unit_of_chunk = [&](uint32_t k) {
+        const uint32_t p = k / cpp;
+        return min(p * upp + (k - p * cpp) * kUnitsPerChunk, U);
+    };
+    const uint32_t u_begin = unit_of_chunk(uint32_t(uint64_t(C) * blockIdx.x / a.n_cta));
+    const uint32_t u_end = unit_of_chunk(uint32_t(uint64_t(C) * (blockIdx.x + 1) / a.n_cta));
 
     // chunk of unit u: its pair, token range [c0, t1) within the pair and the unit after it
     struct Chunk {
@@ -1515,10 +1524,10 @@ __global__ void atr_combine_kernel(const float* __restrict__ part_o, const float
                                    uint32_t raw_slot0, float* __restrict__ out, float* __restrict__ lse) {
     const uint32_t pair = blockIdx.x, d = threadIdx.x;
     uint32_t s_lo = 1, s_hi = 0;  // segment slots [s_lo, s_hi] (empty when there are no compressed tokens)
-    if (n_cta > 0) {
-        const uint64_t U = uint64_t(n_pairs) * upp;
-        s_lo = cta_of_unit(uint64_t(pair) * upp, U, n_cta) + pair;
-        s_hi = cta_of_unit(uint64_t(pair + 1) * upp - 1, U, n_cta) + pair;
+    if (n_cta > 0) {  // the CTAs holding the pair's first and last chunks (ranges are whole chunks)
+        const uint64_t cpp = (upp + kUnitsPerChunk - 1) / kUnitsPerChunk, C = uint64_t(n_pairs) * cpp;
+        s_lo = cta_of_unit(uint64_t(pair) * cpp, C, n_cta) + pair;
+        s_hi = cta_of_unit(uint64_t(pair + 1) * cpp - 1, C, n_cta) + pair;
     }
     const uint32_t raw = raw_slot0 + pair;
     for (uint32_t g = 0; g < kG; ++g) {
@@ -1706,7 +1715,8 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     // persistent main grid: one CTA per SM, balanced over 512-token units (never more CTAs than units)
     const uint32_t upp = uint32_t((n_comp + kUnit - 1) / kUnit);
     const uint64_t units = uint64_t(a.n_pairs) * upp;
-    const uint32_t n_cta = uint32_t(std::min<uint64_t>(uint64_t(sms), units));
+    const uint64_t chunks_total = uint64_t(a.n_pairs) * ((upp + kUnitsPerChunk - 1) / kUnitsPerChunk);
+    const uint32_t n_cta = uint32_t(std::min<uint64_t>(uint64_t(sms), chunks_total));  // every CTA has a chunk
     // partial slots: segments b + pair (< n_cta + n_pairs), then one raw slot per pair
     const uint32_t raw_slot0 = n_cta + a.n_pairs;
     const uint32_t n_slots = raw_slot0 + a.n_pairs;
