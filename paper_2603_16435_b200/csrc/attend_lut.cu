@@ -620,7 +620,10 @@ struct RawArgs {
 
 __global__ void __launch_bounds__(kThreads) attend_raw_rows_kernel(RawArgs a) {
     extern __shared__ __align__(16) float rsm[];
-    constexpr int kRowBatch = 8;
+#ifndef VQKV_RAW_BATCH
+#define VQKV_RAW_BATCH 16
+#endif
+    constexpr int kRowBatch = VQKV_RAW_BATCH;
     const uint32_t pair = blockIdx.x, slot = a.slot0 + pair;
     const uint32_t n_raw = uint32_t(a.n_init + a.n_local);
     if (n_raw == 0) {
