@@ -465,6 +465,146 @@ __global__ void __launch_bounds__(192, 3) lut_tc2_kernel(const __half* __restric
     if (warp == 0) ptx::tmem_dealloc(tmem, 256);
 }
 
+// LUT GEMM over stage pairs (the default): like lut_tc2_kernel (persistent, query-tile stationary), but
+// an item is (stage pair sp, chunk c): stages 2 sp and 2 sp + 1 accumulate into the two halves of a
+// 256-column TMEM buffer (double-buffered per item), so each (pair, code) gets its two adjacent LUT slots
+// as one 32-byte store -- a full L2 sector, half the store instructions of one 16 B store per stage.
+__global__ void __launch_bounds__(192, 3) lut_tc4_kernel(const __half* __restrict__ eff16, const __half* __restrict__ eff16lo,
+                                                          const StageInfo* __restrict__ kst, uint32_t n_stages,
+                                                          const __half* __restrict__ qhi, const __half* __restrict__ qlo,
+                                                          const float* __restrict__ qscl, uint32_t n_pairs, uint32_t cpq,
+                                                          uint32_t maxch, uint32_t ng, uint32_t R, float4* __restrict__ lut) {
+    extern __shared__ uint8_t lsm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(lsm_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar_q, e_full[2], e_empty[2], acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(16) float sc_s[128];  // the query tile's row scales
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tq = blockIdx.x / cpq, rep = blockIdx.x % cpq;
+    const uint32_t nsp = (n_stages + 1) / 2, n_items = nsp * maxch;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(ptx::smem_u32(&bar_q), 1);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(ptx::smem_u32(&e_full[b]), 1);
+            ptx::mbar_init(ptx::smem_u32(&e_empty[b]), 1);
+            ptx::mbar_init(ptx::smem_u32(&acc_full[b]), 1);
+            ptx::mbar_init(ptx::smem_u32(&acc_empty[b]), 128);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (threadIdx.x < 128) sc_s[threadIdx.x] = qscl[uint64_t(tq) * 128 + threadIdx.x];
+    if (warp == 0) {
+        ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 512);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t s_q = ptx::smem_u32(sm);  // Q_hi, Q_lo at + 32 KB
+    auto s_e = [&](uint32_t b) { return s_q + 65536u + b * 65536u; };  // E_hi, E_lo at + 32 KB
+    auto has = [&](uint32_t st, uint32_t c) { return st < n_stages && c * 128u < kst[st].size; };
+    if (warp == 4) {
+        if (lane == 0) {  // producer: the query tile once, then per item the (up to) two stages' chunks
+            ptx::mbar_arrive_expect_tx(ptx::smem_u32(&bar_q), 65536);
+            ptx::bulk_g2s(s_q, qhi + uint64_t(tq) * 16384, 32768, ptx::smem_u32(&bar_q));
+            ptx::bulk_g2s(s_q + 32768, qlo + uint64_t(tq) * 16384, 32768, ptx::smem_u32(&bar_q));
+            uint32_t k = 0;  // ring steps
+            for (uint32_t it = rep; it < n_items; it += cpq) {
+                const uint32_t sp = it / maxch, c = it % maxch;
+                for (uint32_t h = 0; h < 2; ++h) {
+                    const uint32_t st = 2 * sp + h;
+                    if (!has(st, c)) continue;
+                    const uint32_t b = k & 1u, u = k >> 1;
+                    ptx::mbar_wait(ptx::smem_u32(&e_empty[b]), (u & 1u) ^ 1u);
+                    const uint64_t eo = kst[st].eff16_off + uint64_t(c) * 18432;
+                    ptx::mbar_arrive_expect_tx(ptx::smem_u32(&e_full[b]), 65536);
+                    ptx::bulk_g2s(s_e(b), eff16 + eo, 32768, ptx::smem_u32(&e_full[b]));
+                    ptx::bulk_g2s(s_e(b) + 32768, eff16lo + eo, 32768, ptx::smem_u32(&e_full[b]));
+                    ++k;
+                }
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {  // MMA issuer
+            constexpr uint32_t idesc = ptx::idesc_f16_f32(128, 128);
+            ptx::mbar_wait(ptx::smem_u32(&bar_q), 0);
+            uint32_t k = 0, ki = 0;
+            for (uint32_t it = rep; it < n_items; it += cpq, ++ki) {
+                const uint32_t sp = it / maxch, c = it % maxch;
+                const uint32_t ab = ki & 1u, au = ki >> 1;
+                ptx::mbar_wait(ptx::smem_u32(&acc_empty[ab]), (au & 1u) ^ 1u);
+                ptx::tc_fence_after();
+                for (uint32_t h = 0; h < 2; ++h) {
+                    const uint32_t st = 2 * sp + h;
+                    if (!has(st, c)) continue;
+                    const uint32_t b = k & 1u, u = k >> 1;
+                    ptx::mbar_wait(ptx::smem_u32(&e_full[b]), u & 1u);
+                    ptx::tc_fence_after();
+                    const uint32_t eh = s_e(b), el = eh + 32768, qh = s_q, ql = s_q + 32768;
+                    const uint32_t A[3] = {eh, el, eh}, B[3] = {ql, qh, qh};  // small terms first
+#pragma unroll
+                    for (int part = 0; part < 3; ++part)
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const uint32_t koff = (kk >> 2) * 16384 + (kk & 3) * 32;
+                            ptx::mma_f16_ss(tmem + 256u * ab + 128u * h, ptx::umma_desc_sw128(A[part] + koff),
+                                            ptx::umma_desc_sw128(B[part] + koff), idesc, (part | kk) ? 1u : 0u);
+                        }
+                    ptx::mma_commit(ptx::smem_u32(&e_empty[b]));
+                    ++k;
+                }
+                ptx::mma_commit(ptx::smem_u32(&acc_full[ab]));
+            }
+        }
+    } else {
+        // epilogue: thread = entry row j (TMEM lane); per pair the two stages' 4 heads = one 32 B store
+        uint32_t ki = 0;
+        for (uint32_t it = rep; it < n_items; it += cpq, ++ki) {
+            const uint32_t sp = it / maxch, c = it % maxch;
+            const uint32_t ab = ki & 1u, au = ki >> 1;
+            const uint32_t j = c * 128u + warp * 32u + lane;
+            const bool v0 = has(2 * sp, c) && j < kst[2 * sp].size;
+            const bool v1 = has(2 * sp + 1, c) && j < kst[2 * sp + 1].size;
+            ptx::mbar_wait(ptx::smem_u32(&acc_full[ab]), au & 1u);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem + ((warp * 32u) << 16) + 256u * ab;
+#pragma unroll 1
+            for (uint32_t q8 = 0; q8 < 4; ++q8) {  // 8 pairs (32 columns) per step
+                float x0[32], x1[32];
+                ptx::tmem_ld32(tbase + 32u * q8, x0);
+                ptx::tmem_ld32(tbase + 128u + 32u * q8, x1);
+                ptx::tc_wait_ld();
+                if (q8 == 3) {
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(ptx::smem_u32(&acc_empty[ab]));
+                }
+                if (!(v0 || v1)) continue;
+#pragma unroll
+                for (int pp = 0; pp < 8; ++pp) {
+                    const uint32_t pair = tq * 32 + q8 * 8 + pp;
+                    if (pair < n_pairs) {
+                        const float4 sc = reinterpret_cast<const float4*>(sc_s)[q8 * 8 + pp];
+                        float o[8];
+                        o[0] = v0 ? x0[4 * pp] * sc.x : 0.f;
+                        o[1] = v0 ? x0[4 * pp + 1] * sc.y : 0.f;
+                        o[2] = v0 ? x0[4 * pp + 2] * sc.z : 0.f;
+                        o[3] = v0 ? x0[4 * pp + 3] * sc.w : 0.f;
+                        o[4] = v1 ? x1[4 * pp] * sc.x : 0.f;
+                        o[5] = v1 ? x1[4 * pp + 1] * sc.y : 0.f;
+                        o[6] = v1 ? x1[4 * pp + 2] * sc.z : 0.f;
+                        o[7] = v1 ? x1[4 * pp + 3] * sc.w : 0.f;
+                        ptx::stg256(lut + lut_off(pair, ng, R, 2 * sp, j), o);
+                    }
+                }
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc(tmem, 512);
+}
+
 // Reads 64 bits starting at bit `pos` of a byte stream: two aligned 64-bit
 // loads when they stay inside [.., end), byte loads otherwise (buffer tails).
 __device__ __forceinline__ uint64_t read_bits64(const uint8_t* base, uint64_t pos, const uint8_t* end) {
@@ -1795,8 +1935,17 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
             VQKV_CUDA(cudaMallocAsync(&qs, sizeof(float) * rows_pad, s));
             q_prep_kernel<<<rows_pad / 8, 256, 0, s>>>(a.q_dev, rows, rows_pad, float(scale), qh, ql, qs);
             launch_check("q_prep_kernel");
-            const char* lv = getenv("VQKV_LUT_TC1");  // dev A/B: the per-chunk kernel
-            if (ks.n <= kLutTc2MaxStages && !(lv && lv[0] == '1')) {
+            const char* lv = getenv("VQKV_LUT_TC1");  // dev A/B: 1 = per-chunk kernel, 2 = per-stage items
+            uint32_t maxch4 = 0;
+            for (const auto& st : ks.stages) maxch4 = std::max(maxch4, (st.size + 127) / 128);
+            if (!(lv && (lv[0] == '1' || lv[0] == '2'))) {
+                const uint32_t cpq = std::max<uint32_t>(1u, uint32_t(sms) / qt);
+                VQKV_CUDA(cudaFuncSetAttribute(lut_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               int(kLutTc2Smem)));
+                lut_tc4_kernel<<<qt * cpq, 192, kLutTc2Smem, s>>>(ks.d_eff16, ks.d_eff16lo, ks.d_stages, ks.n, qh, ql,
+                                                                  qs, a.n_pairs, cpq, maxch4, ng, R, lut);
+                launch_check("lut_tc4_kernel");
+            } else if (ks.n <= kLutTc2MaxStages && !(lv && lv[0] == '1')) {
                 const uint32_t cpq = std::max<uint32_t>(1u, uint32_t(sms) / qt);
                 VQKV_CUDA(cudaFuncSetAttribute(lut_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                int(kLutTc2Smem)));

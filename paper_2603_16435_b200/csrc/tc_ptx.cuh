@@ -85,6 +85,13 @@ __device__ __forceinline__ void ldg256_na(const float* p, float* r) {
                  : "l"(p));
 }
 
+// 32-byte store (one full L2 sector)
+__device__ __forceinline__ void stg256(void* p, const float (&r)[8]) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]),
+                 "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
+                 : "memory");
+}
+
 __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
