@@ -1841,12 +1841,20 @@ void launch_keycodes_from_gm(const vqkv_stack_s& ks, const uint8_t* gm, uint64_t
     launch_check("atr_unpack_kernel");
 }
 
-// the side stream the raw-row kernel runs on (one per stack, created on first use)
-static cudaStream_t attend_side_stream(const vqkv_stack_s& ks) {
+// the streams of a decode-attention call beside the caller's (one pair per stack, created on first
+// use): the main kernel at the highest priority, the raw-row kernel at the lowest, so that the main
+// kernel's CTAs take every SM first and the raw-row CTAs run in its tail as its CTAs retire
+static void attend_streams(const vqkv_stack_s& ks, cudaStream_t& lo, cudaStream_t& hi) {
     auto& st = const_cast<vqkv_stack_s&>(ks);
     std::lock_guard<std::mutex> lk(st.mu);
-    if (!st.cs_attn) VQKV_CUDA(cudaStreamCreateWithFlags(&st.cs_attn, cudaStreamNonBlocking));
-    return st.cs_attn;
+    if (!st.cs_attn) {
+        int least = 0, greatest = 0;
+        VQKV_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        VQKV_CUDA(cudaStreamCreateWithPriority(&st.cs_attn, cudaStreamNonBlocking, least));
+        VQKV_CUDA(cudaStreamCreateWithPriority(&st.cs_attn_hi, cudaStreamNonBlocking, greatest));
+    }
+    lo = st.cs_attn;
+    hi = st.cs_attn_hi;
 }
 
 void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqkv_attend_args& a, cudaStream_t s) {
@@ -1887,40 +1895,6 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     VQKV_CUDA(cudaMallocAsync(&po, sizeof(float) * n_slots * kG * kD, s));
     VQKV_CUDA(cudaMallocAsync(&pm, sizeof(float) * n_slots * kG, s));
     VQKV_CUDA(cudaMallocAsync(&pl, sizeof(float) * n_slots * kG, s));
-
-    // raw init/local rows on a side stream, beside the LUT build (fork / join with events)
-    cudaStream_t side = attend_side_stream(ks);
-    cudaEvent_t ev_fork, ev_join;
-    VQKV_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    VQKV_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-    VQKV_CUDA(cudaEventRecord(ev_fork, s));
-    VQKV_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
-    {
-        RawArgs ra{};
-        ra.q = a.q_dev;
-        ra.init_k = a.init_k_dev;
-        ra.init_v = a.init_v_dev;
-        ra.n_init = a.n_init;
-        ra.local_k = a.local_k_dev;
-        ra.local_v = a.local_v_dev;
-        ra.n_local = a.n_local;
-        ra.init_stride = a.init_stride ? a.init_stride : a.n_init;
-        ra.local_stride = a.local_stride ? a.local_stride : a.n_local;
-        ra.scale = float(scale);
-        ra.slot0 = raw_slot0;
-        ra.part_o = po;
-        ra.part_m = pm;
-        ra.part_l = pl;
-        const uint32_t n_raw = uint32_t(a.n_init + a.n_local);
-        const int rsmem = int(sizeof(float) * (64 + kG * kD + 4 * kG * kD + uint64_t(n_raw) * kG));
-        VQKV_CUDA(cudaFuncSetAttribute(attend_raw_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem));
-        // the largest shared-memory carveout: an SM running raw-row CTAs can take a LUT-build CTA beside
-        // them (the carveout of an SM only changes when it is idle)
-        VQKV_CUDA(cudaFuncSetAttribute(attend_raw_rows_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        attend_raw_rows_kernel<<<a.n_pairs, kThreads, rsmem, side>>>(ra);
-        launch_check("attend_raw_rows_kernel");
-    }
-    VQKV_CUDA(cudaEventRecord(ev_join, side));
 
     if (n_comp > 0) {
         VQKV_CUDA(cudaMallocAsync(&lut, sizeof(float4) * a.n_pairs * ng * R * kGS, s));
@@ -1976,8 +1950,46 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
             launch_check("lut_zero_missing_kernel");
         }
     }
+    cudaStream_t side, hi;
+    attend_streams(ks, side, hi);
+    cudaEvent_t ev_fork, ev_join, ev_main;
+    VQKV_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    VQKV_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    VQKV_CUDA(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
+    VQKV_CUDA(cudaEventRecord(ev_fork, s));
+    VQKV_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    VQKV_CUDA(cudaStreamWaitEvent(hi, ev_fork, 0));
+    // raw init/local rows on the low-priority stream once the LUT is built: they run in the main
+    // kernel's tail (fork / join with events)
+    {
+        RawArgs ra{};
+        ra.q = a.q_dev;
+        ra.init_k = a.init_k_dev;
+        ra.init_v = a.init_v_dev;
+        ra.n_init = a.n_init;
+        ra.local_k = a.local_k_dev;
+        ra.local_v = a.local_v_dev;
+        ra.n_local = a.n_local;
+        ra.init_stride = a.init_stride ? a.init_stride : a.n_init;
+        ra.local_stride = a.local_stride ? a.local_stride : a.n_local;
+        ra.scale = float(scale);
+        ra.slot0 = raw_slot0;
+        ra.part_o = po;
+        ra.part_m = pm;
+        ra.part_l = pl;
+        const uint32_t n_raw = uint32_t(a.n_init + a.n_local);
+        const int rsmem = int(sizeof(float) * (64 + kG * kD + 4 * kG * kD + uint64_t(n_raw) * kG));
+        VQKV_CUDA(cudaFuncSetAttribute(attend_raw_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem));
+        // the largest shared-memory carveout: an SM running raw-row CTAs can take a LUT-build CTA beside
+        // them (the carveout of an SM only changes when it is idle)
+        VQKV_CUDA(cudaFuncSetAttribute(attend_raw_rows_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        attend_raw_rows_kernel<<<a.n_pairs, kThreads, rsmem, side>>>(ra);
+        launch_check("attend_raw_rows_kernel");
+    }
+    VQKV_CUDA(cudaEventRecord(ev_join, side));
+
     if (n_comp > 0) {
-        ProfScope ps("attend", s);
+        ProfScope ps("attend", hi);
         const uint64_t vpb = payload_bytes(vs.row_bits, n_comp);
         const uint64_t vstr = a.vcodes_stride ? a.vcodes_stride : vpb;
         MainArgs ma{};
@@ -2008,9 +2020,11 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         ma.part_m = pm;
         ma.part_l = pl;
         VQKV_CUDA(cudaFuncSetAttribute(attend_atr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMainSmem)));
-        attend_atr_kernel<<<n_cta, kThreads, kMainSmem, s>>>(ma);
+        attend_atr_kernel<<<n_cta, kThreads, kMainSmem, hi>>>(ma);
         launch_check("attend_atr_kernel");
     }
+    VQKV_CUDA(cudaEventRecord(ev_main, hi));
+    VQKV_CUDA(cudaStreamWaitEvent(s, ev_main, 0));
     VQKV_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
     {
         ProfScope ps("attend_combine", s);
@@ -2020,6 +2034,7 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     }
     cudaEventDestroy(ev_fork);
     cudaEventDestroy(ev_join);
+    cudaEventDestroy(ev_main);
     if (lut) VQKV_CUDA(cudaFreeAsync(lut, s));
     if (ktmp) VQKV_CUDA(cudaFreeAsync(ktmp, s));
     VQKV_CUDA(cudaFreeAsync(po, s));

@@ -332,6 +332,7 @@ int vqkv_stack_destroy(vqkv_stack_t s) {
         if (s->host_scratch) cudaFree(s->host_scratch);
         if (s->cs_alt) cudaStreamDestroy(s->cs_alt);
         if (s->cs_attn) cudaStreamDestroy(s->cs_attn);
+        if (s->cs_attn_hi) cudaStreamDestroy(s->cs_attn_hi);
         for (auto& a : s->staging) {
             if (a.done) cudaEventSynchronize(a.done), cudaEventDestroy(a.done);
             if (a.base) cudaFree(a.base);

@@ -95,7 +95,8 @@ struct vqkv_stack_s {
     unsigned long long* d_counters = nullptr; // encode diagnostics [4]
     cudaStream_t cp_in = nullptr, cp_out = nullptr;  // host-buffer pipeline copy streams (lazy)
     cudaStream_t cs_alt = nullptr;  // second compute stream: consecutive chunk encodes overlap their tails
-    cudaStream_t cs_attn = nullptr; // decode attention: the raw-row kernel runs here beside the LUT build
+    cudaStream_t cs_attn = nullptr;    // decode attention: the raw-row kernel (lowest stream priority)
+    cudaStream_t cs_attn_hi = nullptr; // decode attention: the main kernel (highest stream priority)
     // host-buffer calls stage through two persistent device arenas, used alternately: a call waits
     // (host side) for the call two before it, so a host running ahead is held back instead of the
     // stream-ordered pool growing (and mapping memory) inside the timed pipeline
