@@ -1850,8 +1850,13 @@ static void attend_streams(const vqkv_stack_s& ks, cudaStream_t& lo, cudaStream_
     if (!st.cs_attn) {
         int least = 0, greatest = 0;
         VQKV_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        VQKV_CUDA(cudaStreamCreateWithPriority(&st.cs_attn, cudaStreamNonBlocking, least));
-        VQKV_CUDA(cudaStreamCreateWithPriority(&st.cs_attn_hi, cudaStreamNonBlocking, greatest));
+        cudaStream_t l = nullptr, h = nullptr;
+        VQKV_CUDA(cudaStreamCreateWithPriority(&l, cudaStreamNonBlocking, least));
+        const cudaError_t e = cudaStreamCreateWithPriority(&h, cudaStreamNonBlocking, greatest);
+        if (e != cudaSuccess) cudaStreamDestroy(l);
+        VQKV_CUDA(e);
+        st.cs_attn = l;  // both or neither
+        st.cs_attn_hi = h;
     }
     lo = st.cs_attn;
     hi = st.cs_attn_hi;
