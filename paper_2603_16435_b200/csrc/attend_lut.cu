@@ -74,6 +74,9 @@ constexpr int kThreads = 512;
 #ifndef VQKV_ATTN_KB
 #define VQKV_ATTN_KB 2  // key records loaded per batch, one batch ahead of the lookups
 #endif
+#ifndef VQKV_ATTN_HANDOFF
+#define VQKV_ATTN_HANDOFF 1  // pairs split between two CTAs are contracted once (accumulator hand-off)
+#endif
 #ifndef VQKV_ATTN_TOK
 #define VQKV_ATTN_TOK 16
 #endif
@@ -736,6 +739,14 @@ __device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uin
         "l"(src), "r"(bytes), "r"(bar), "l"(pol)
         : "memory");
 }
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void prefetch_l2_hint(const void* p, uint32_t bytes, uint64_t pol) {
     asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol) : "memory");
 }
@@ -923,6 +934,9 @@ struct MainArgs {
     float* part_o;           // [slots][G][D]: unnormalised sum p v
     float* part_m;           // [slots][G]
     float* part_l;           // [slots][G]
+    float4* park;            // [n_cta][ncol * 128]: accumulators handed across CTA boundaries (slot = boundary)
+    float4* pmeta;           // [n_cta][2]: their running max and sum
+    uint32_t* bsync;         // [2 n_cta], zeroed per call: arrivals per boundary, then ready flags
 };
 
 // VQKV_ATTN_PHASES (diagnostics builds only): thread 0 of every CTA accumulates clock64 per phase
@@ -1123,9 +1137,23 @@ __device__ __noinline__ void chunk_fold(const uint8_t* lutb, uint32_t tmem, uint
 
 // Segment end: o[g][d] = sum_e acc[g][e] * e_v[e][d] (e = the value stack's stage-concatenated entry),
 // the TMEM accumulator staged into the smem buffer; writes the segment's partial (o, m, l).
+// Pairs split between CTAs are contracted once.  At each CTA boundary the pair continues across, both
+// CTAs' segments arrive (one atomic per boundary): the first parks its accumulator (float4 [entry], with
+// its running max and sum) and moves on; the second merges it before going on.  A segment meets at most
+// two boundaries (its CTA's right one first, then the left one); it parks, or ends with the merged
+// accumulator contracted.  A second arriver only waits for the first one's park stores, so no CTA
+// waits on a CTA that has not arrived.
+struct Handoff {
+    float4* park;      // [n_cta][n_ent]
+    float4* pmeta;     // [n_cta][2]
+    uint32_t* bsync;   // [2 n_cta]: arrivals, ready flags
+    uint32_t n_cta;
+    uint32_t kright, kleft;  // boundary indices, ~0u when the segment does not meet that boundary
+    uint32_t* bcast;   // shared-memory word
+};
 __device__ __noinline__ void segment_contract(const float* __restrict__ veff, uint32_t vtotal, float* part_o,
                                               float* part_m, float* part_l, uint8_t* lutb, uint32_t tmem,
-                                              uint32_t ncol, uint32_t slot, float4 Mn, float4 Lrun) {
+                                              uint32_t ncol, uint32_t slot, float4 Mn, float4 Lrun, Handoff h) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t hg = warp >> 2, hlq = warp & 3u;
     // the accumulator, staged from TMEM into the smem buffer as float4 [entry] x (4 heads)
@@ -1140,6 +1168,78 @@ __device__ __noinline__ void segment_contract(const float* __restrict__ veff, ui
     }
     ptx::tc_fence_before();
     __syncthreads();
+    const uint32_t n_ent = ncol * 128u;
+    float4* a4 = reinterpret_cast<float4*>(accs);
+    auto empty_partial = [&]() {
+        if (tid == 0) {
+            reinterpret_cast<float4*>(part_m)[slot] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            reinterpret_cast<float4*>(part_l)[slot] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    // arrive at boundary k: true for the first arriver; the second waits for the first one's park
+    auto arrive = [&](uint32_t k) {
+        if (tid == 0) {
+            const uint32_t first = atomicAdd(h.bsync + k, 1u) == 0u;
+            if (!first)
+                while (ld_acquire_gpu(h.bsync + h.n_cta + k) == 0u) __nanosleep(256);
+            *h.bcast = first;
+        }
+        __syncthreads();
+        const bool first = *h.bcast != 0u;
+        __syncthreads();
+        return first;
+    };
+    auto park = [&](uint32_t k) {  // the accumulator (or an empty one: max -inf, data not written)
+        if (Mn.x > -INFINITY)
+            for (uint32_t e = tid; e < n_ent; e += kThreads) __stcg(h.park + uint64_t(k) * n_ent + e, a4[e]);
+        if (tid == 0) {
+            __stcg(h.pmeta + 2u * k, Mn);
+            __stcg(h.pmeta + 2u * k + 1u, Lrun);
+        }
+        __threadfence();  // every thread's park stores before the ready flag
+        __syncthreads();
+        if (tid == 0) st_release_gpu(h.bsync + h.n_cta + k, 1u);
+    };
+    auto merge = [&](uint32_t k) {  // acc = acc e^(Mn - M) + parked e^(Mp - M), M = max(Mn, Mp)
+        const float4 Mp = __ldcg(h.pmeta + 2u * k), Lp = __ldcg(h.pmeta + 2u * k + 1u);
+        if (!(Mp.x > -INFINITY)) return;  // an empty park
+        const float4 M = make_float4(fmaxf(Mn.x, Mp.x), fmaxf(Mn.y, Mp.y), fmaxf(Mn.z, Mp.z), fmaxf(Mn.w, Mp.w));
+        const float4 al = make_float4(__expf(Mn.x - M.x), __expf(Mn.y - M.y), __expf(Mn.z - M.z), __expf(Mn.w - M.w));
+        const float4 be = make_float4(__expf(Mp.x - M.x), __expf(Mp.y - M.y), __expf(Mp.z - M.z), __expf(Mp.w - M.w));
+        const float4* src = h.park + uint64_t(k) * n_ent;
+        for (uint32_t e = tid; e < n_ent; e += kThreads) {
+            const float4 x = a4[e], y = __ldcg(src + e);
+            a4[e] = make_float4(fmaf(y.x, be.x, x.x * al.x), fmaf(y.y, be.y, x.y * al.y), fmaf(y.z, be.z, x.z * al.z),
+                                fmaf(y.w, be.w, x.w * al.w));
+        }
+        Lrun = make_float4(fmaf(Lp.x, be.x, Lrun.x * al.x), fmaf(Lp.y, be.y, Lrun.y * al.y),
+                           fmaf(Lp.z, be.z, Lrun.z * al.z), fmaf(Lp.w, be.w, Lrun.w * al.w));
+        Mn = M;
+        __syncthreads();
+    };
+    if (h.kright != ~0u) {
+        if (arrive(h.kright)) {
+            park(h.kright);
+            Mn = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);  // given away: e^(-inf - M) = 0 below
+            Lrun = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            merge(h.kright);
+        }
+    }
+    if (h.kleft != ~0u) {
+        if (arrive(h.kleft)) {
+            park(h.kleft);
+            empty_partial();
+            __syncthreads();
+            return;
+        }
+        merge(h.kleft);
+    }
+    if (!(Mn.x > -INFINITY)) {  // everything handed over
+        empty_partial();
+        __syncthreads();
+        return;
+    }
     // warp = a slice of the entries, lane = 4 output columns: per entry one coalesced 512 B row read
     // (L2-resident codebook) and one broadcast LDS.128 of the 4 heads' weights feed 16 FMAs
     const float4* acc4 = reinterpret_cast<const float4*>(accs);
@@ -1262,6 +1362,9 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
     };
     const uint32_t u_begin = unit_of_chunk(uint32_t(uint64_t(C) * blockIdx.x / a.n_cta));
     const uint32_t u_end = unit_of_chunk(uint32_t(uint64_t(C) * (blockIdx.x + 1) / a.n_cta));
+    // CTA b's chunks are [cta_chunk0(b), cta_chunk0(b + 1))
+    auto cta_chunk0 = [&](uint32_t b) { return uint32_t(uint64_t(C) * b / a.n_cta); };
+    auto chunk_pair = [&](uint32_t k) { return k / cpp; };
 
     // chunk of unit u: its pair, token range [c0, t1) within the pair and the unit after it
     struct Chunk {
@@ -1638,9 +1741,16 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
         PHASE_T(t_con);
 
         if (!has_next || next_pair != pair) {
-            // ---- segment end (out of line: keeps the chunk loop's registers for the logits)
+            // ---- segment end (out of line: keeps the chunk loop's registers for the logits); a pair that
+            // continues into the next CTA or from the previous one is handed over (segment_contract)
+            const uint32_t b = blockIdx.x;
+            Handoff ho{a.park, a.pmeta, a.bsync, a.n_cta, ~0u, ~0u, reinterpret_cast<uint32_t*>(ctl + 320)};
+            if (VQKV_ATTN_HANDOFF && a.park) {
+                if (!has_next && b + 1u < a.n_cta && chunk_pair(cta_chunk0(b + 1u)) == pair) ho.kright = b;
+                if (b > 0u && chunk_pair(cta_chunk0(b)) == pair && chunk_pair(cta_chunk0(b) - 1u) == pair) ho.kleft = b - 1u;
+            }
             segment_contract(a.veff, a.vtotal, a.part_o, a.part_m, a.part_l, lutb, tmem, ncol, blockIdx.x + pair, Mn,
-                             Lrun);
+                             Lrun, ho);
             if (tid == 0) {
                 *segM = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
                 *segL = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1900,6 +2010,16 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     VQKV_CUDA(cudaMallocAsync(&po, sizeof(float) * n_slots * kG * kD, s));
     VQKV_CUDA(cudaMallocAsync(&pm, sizeof(float) * n_slots * kG, s));
     VQKV_CUDA(cudaMallocAsync(&pl, sizeof(float) * n_slots * kG, s));
+    // boundary hand-off scratch: one parked accumulator per CTA boundary, arrival counters and ready flags
+    const uint64_t park_ent = uint64_t((vs.total_rows + 127) / 128) * 128u;
+    float4 *park = nullptr, *pmeta = nullptr;
+    uint32_t* bsync = nullptr;
+    if (n_comp > 0) {
+        VQKV_CUDA(cudaMallocAsync(&park, sizeof(float4) * park_ent * n_cta, s));
+        VQKV_CUDA(cudaMallocAsync(&pmeta, sizeof(float4) * 2 * n_cta, s));
+        VQKV_CUDA(cudaMallocAsync(&bsync, sizeof(uint32_t) * 2 * n_cta, s));
+        VQKV_CUDA(cudaMemsetAsync(bsync, 0, sizeof(uint32_t) * 2 * n_cta, s));
+    }
 
     if (n_comp > 0) {
         VQKV_CUDA(cudaMallocAsync(&lut, sizeof(float4) * a.n_pairs * ng * R * kGS, s));
@@ -2024,6 +2144,9 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
         ma.part_o = po;
         ma.part_m = pm;
         ma.part_l = pl;
+        ma.park = park;
+        ma.pmeta = pmeta;
+        ma.bsync = bsync;
         VQKV_CUDA(cudaFuncSetAttribute(attend_atr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMainSmem)));
         attend_atr_kernel<<<n_cta, kThreads, kMainSmem, hi>>>(ma);
         launch_check("attend_atr_kernel");
@@ -2045,6 +2168,9 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     VQKV_CUDA(cudaFreeAsync(po, s));
     VQKV_CUDA(cudaFreeAsync(pm, s));
     VQKV_CUDA(cudaFreeAsync(pl, s));
+    if (park) VQKV_CUDA(cudaFreeAsync(park, s));
+    if (pmeta) VQKV_CUDA(cudaFreeAsync(pmeta, s));
+    if (bsync) VQKV_CUDA(cudaFreeAsync(bsync, s));
 }
 
 }  // namespace vqkv_dev

@@ -236,7 +236,10 @@ def test_lse_combine_matches_monolithic(torch_mod):
                           # > 18 value stages: value-code windows read one at a time; 8192-token split edge
                           (8, 512, 24, 64, 2, 4, 8192, 8), (9, 1024, 40, 32, 1, 1, 8193, 2),
                           # more pairs than SMs: CTA token ranges span several pairs (several segments per CTA)
-                          (4, 128, 4, 128, 200, 2, 600, 3), (56, 1024, 16, 512, 300, 1, 10, 2)])
+                          (4, 128, 4, 128, 200, 2, 600, 3), (56, 1024, 16, 512, 300, 1, 10, 2),
+                          # pairs spanning 3-5 CTAs (one chunk each): accumulators handed over across CTA
+                          # boundaries, including chains through single-segment middle CTAs
+                          (4, 128, 4, 128, 1, 2, 40000, 3), (8, 256, 4, 128, 3, 1, 20000, 2)])
 def test_attention_lut_path_vs_oracle(torch_mod, nk, sk, nv, sv, n_pairs, n_init, n_comp, n_local):
     """LUT/histogram fast path (D=128, G=4) against the oracle's attend over the same segments."""
     torch = torch_mod
