@@ -68,9 +68,6 @@ namespace {
 constexpr int kG = 4;                          // query heads per KV head on this path
 constexpr int kD = 128;                        // head dim
 constexpr int kThreads = 512;
-#ifndef VQKV_ATTN_EXP
-#define VQKV_ATTN_EXP 0  // development experiments (variant builds only)
-#endif
 #ifndef VQKV_ATTN_KB
 #define VQKV_ATTN_KB 2  // key records loaded per batch, one batch ahead of the lookups
 #endif
@@ -1614,9 +1611,6 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
                 // value stack has <= 16 stages), each extracting its stage's code from the staged row and
                 // doing that bin's one atomic -- short dependency chains instead of a 16-stage loop per lane
                 auto process_batch = [&](uint32_t b0, uint32_t n) {
-#if VQKV_ATTN_EXP == 2
-                    return;
-#endif
                     if (!all_staged || lanes_e == 0u) {  // generic path: lane = entry
                         if (lane < n) {
                             const uint2 e = queue[b0 + lane];
