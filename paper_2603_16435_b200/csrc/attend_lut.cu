@@ -1769,7 +1769,7 @@ __global__ void __launch_bounds__(kThreads, 1) attend_atr_kernel(MainArgs a) {
 __global__ void atr_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_m,
                                    const float* __restrict__ part_l, uint32_t n_cta, uint32_t upp, uint32_t n_pairs,
                                    uint32_t raw_slot0, float* __restrict__ out, float* __restrict__ lse) {
-    const uint32_t pair = blockIdx.x, d = threadIdx.x;
+    const uint32_t pair = blockIdx.x, d = threadIdx.x, g = blockIdx.y;  // one CTA per (pair, head)
     uint32_t s_lo = 1, s_hi = 0;  // segment slots [s_lo, s_hi] (empty when there are no compressed tokens)
     if (n_cta > 0) {  // the CTAs holding the pair's first and last chunks (ranges are whole chunks)
         const uint64_t cpp = (upp + kUnitsPerChunk - 1) / kUnitsPerChunk, C = uint64_t(n_pairs) * cpp;
@@ -1777,7 +1777,7 @@ __global__ void atr_combine_kernel(const float* __restrict__ part_o, const float
         s_hi = cta_of_unit(uint64_t(pair + 1) * cpp - 1, C, n_cta) + pair;
     }
     const uint32_t raw = raw_slot0 + pair;
-    for (uint32_t g = 0; g < kG; ++g) {
+    {
         float M = part_m[uint64_t(raw) * kG + g];
         for (uint32_t sl = s_lo; sl <= s_hi; ++sl) M = fmaxf(M, part_m[uint64_t(sl) * kG + g]);
         float L = 0.f, o = 0.f;
@@ -2150,7 +2150,7 @@ void launch_attend_lut(const vqkv_stack_s& ks, const vqkv_stack_s& vs, const vqk
     VQKV_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
     {
         ProfScope ps("attend_combine", s);
-        atr_combine_kernel<<<a.n_pairs, kD, 0, s>>>(po, pm, pl, n_comp > 0 ? n_cta : 0u, upp, a.n_pairs, raw_slot0,
+        atr_combine_kernel<<<dim3(a.n_pairs, kG), kD, 0, s>>>(po, pm, pl, n_comp > 0 ? n_cta : 0u, upp, a.n_pairs, raw_slot0,
                                                     a.out_dev, a.lse_dev);
         launch_check("atr_combine_kernel");
     }
